@@ -1,0 +1,199 @@
+/*
+ * maspncg.h -- C ABI of the B200-native MAS-PNCG solver inner loop.
+ *
+ * The reference (ipcsim, pure Python) has no native FFI; its drop-in
+ * boundary is the Python scene/solver API.  Each entry point below replaces
+ * one reference function (file:line under /root/reference/pkg/src/ipcsim/)
+ * and is bound from Python with ctypes (paper_2604_19892_b200/_native.py;
+ * see INTEGRATION.md for the binding a maintainer would add to ipcsim).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every array argument is HOST memory in
+ *     the reference's layout (vertex ids = original ids, positions/vectors
+ *     flat (3N,) xyz-interleaved, float64);
+ *   - every function returns an mp_status (0 = ok); on failure
+ *     mp_last_error(ctx) holds the message and mp_status_code(status) the
+ *     reference error code string (errors.py:8-42);
+ *   - a context owns one CUDA device, one stream and all device state; it is
+ *     not re-entrant (one host thread drives it).
+ */
+#ifndef MASPNCG_H
+#define MASPNCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mp_status {
+  MP_OK = 0,
+  MP_ERR_PENETRATION = 1,        /* "penetration-detected"   contact.py:41,56,137,149 */
+  MP_ERR_NON_SPD_SUBDOMAIN = 2,  /* "non-spd-subdomain"      mas.py:88                */
+  MP_ERR_CAPACITANCE = 3,        /* "capacitance-not-spd"    woodbury.py:76           */
+  MP_ERR_MODEL_NOT_SPD = 4,      /* "model-not-spd"          solver.py:155,377,389    */
+  MP_ERR_PRECOND_NOT_SPD = 5,    /* "precond-not-spd"        solver.py:167            */
+  MP_ERR_NON_SPD_BLOCK = 6,      /* "non-spd-block"          solver.py:223            */
+  MP_ERR_DEGENERATE = 7,         /* "degenerate-primitive"   geometry.py:68           */
+  MP_ERR_CONFIG = 8,             /* "config-error"           errors.py:38-42          */
+  MP_ERR_CAPACITY = 9,           /* "capacity-overflow"      (new: device buffers)    */
+  MP_ERR_CUDA = 10               /* "cuda-error"             (new)                    */
+} mp_status;
+
+/* Static scene, uploaded once.  Mirrors solver.Scene (solver.py:80-114) plus
+ * ElasticModel (energy.py:101-149) and SurfaceMesh (geometry.py:377-405). */
+typedef struct mp_scene_desc {
+  int64_t n_verts;
+  const double* rest;        /* (N,3) rest positions (Morton partition input) */
+  const double* mass;        /* (N,) lumped masses                             */
+  const uint8_t* dirichlet;  /* (N,) pinned mask                               */
+  const double* f_ext;       /* (3N,) external force                           */
+  int64_t n_tets;
+  const int64_t* tets;       /* (T,4)                                          */
+  const int8_t* kind;        /* (T,) 0 none, 1 ARAP, 2 SNH                     */
+  const double* mu;          /* (T,)                                           */
+  const double* lam;         /* (T,)                                           */
+  const double* Bm;          /* (T,3,3) inverse rest shape, row-major          */
+  const double* vol;         /* (T,) rest volumes                              */
+  int64_t n_tris;
+  const int64_t* tris;       /* (F,3) surface triangles, reference order       */
+  int64_t n_edges;
+  const int64_t* edges;      /* (E,2) surface edges, reference order           */
+  int64_t n_surf_verts;
+  const int64_t* surf_verts; /* (V,) surface vertex ids                        */
+  double d_hat;
+  double kappa;
+} mp_scene_desc;
+
+enum { MP_PRECOND_MAS = 0, MP_PRECOND_JACOBI = 1 };
+enum { MP_DIR_SUBSPACE2D = 0, MP_DIR_FR = 1, MP_DIR_PR = 2, MP_DIR_DK = 3, MP_DIR_CD = 4 };
+enum { MP_UPDATE_WOODBURY = 0, MP_UPDATE_FREEZE = 1, MP_UPDATE_FULLREBUILD = 2 };
+
+/* solver.SolverConfig (solver.py:48-77), same fields and meaning. */
+typedef struct mp_solver_config {
+  double eps;
+  double delta;
+  int64_t iter_max;
+  int32_t K;
+  int32_t preconditioner;
+  int32_t direction_rule;
+  int32_t update_strategy;
+  int32_t block_size;
+  int32_t levels;
+  int32_t coarse_block;
+  int32_t ccd_per_subdomain;
+  double eps_rot;
+  double alpha_l;
+} mp_solver_config;
+
+/* solver.IterRecord (solver.py:117-129) plus device-side diagnostics. */
+typedef struct mp_iter_record {
+  int64_t k;
+  double grad_norm;
+  double z_norm;
+  double r;
+  int32_t restart;
+  int32_t n_contacts;      /* active constraint pairs this iteration       */
+  double mu;
+  double nu;
+  double min_alpha;
+  double t_grad_ms;        /* CUDA-event stage times                      */
+  double t_dir_ms;
+  double t_ccd_ms;
+  int32_t n_candidates;    /* rank-one update candidates (non-rebuild)    */
+  int32_t n_ccd_pairs;     /* CCD candidate pairs                         */
+} mp_iter_record;
+
+#define MP_FLAG_NOT_CONVERGED 1u
+
+typedef struct mp_ctx mp_ctx;
+
+/* Create a context on `device`: uploads the scene, builds the Morton
+ * partition (mas.py:30-77), the static BSR pattern and surface tables. */
+int mp_create(const mp_scene_desc* scene, const mp_solver_config* cfg, int device, mp_ctx** out);
+void mp_destroy(mp_ctx* ctx);
+int mp_set_config(mp_ctx* ctx, const mp_solver_config* cfg);
+const char* mp_status_code(int status);
+const char* mp_last_error(mp_ctx* ctx);
+/* the context's CUDA stream (cudaStream_t) for external event timing */
+void* mp_stream(mp_ctx* ctx);
+/* number of subdomains D and the partition's vertex -> subdomain map (N,) */
+int mp_partition(mp_ctx* ctx, int64_t* D, int64_t* subdomain_of);
+
+/* solver.step (solver.py:461-464): prepare_step + advance_step.
+ * x, v in; x_out, v_out out (3N).  recs: caller array of `cap` records,
+ * *n_recs = iterations run (records beyond cap are dropped but counted). */
+int mp_step(mp_ctx* ctx, const double* x, const double* v, double h,
+            double* x_out, double* v_out, mp_iter_record* recs, int64_t cap,
+            int64_t* n_recs, int32_t* converged, uint32_t* flags);
+/* solver.advance_step (solver.py:296-458) on a prepared state. */
+int mp_advance(mp_ctx* ctx, const double* x, const double* v, const double* x_tilde, double h,
+               double* x_out, double* v_out, mp_iter_record* recs, int64_t cap,
+               int64_t* n_recs, int32_t* converged, uint32_t* flags);
+
+/* ---- stage taps: one device stage on host inputs, for open-loop parity ---- */
+
+/* geometry.broad_phase (geometry.py:443-503): sorted unique (v, tri) and
+ * (edge i, edge j) pairs.  Pass NULL outputs to query counts only. */
+int mp_broad_phase(mp_ctx* ctx, const double* x, double motion_bound, double d_hat,
+                   int64_t* pt, int64_t pt_cap, int64_t* n_pt,
+                   int64_t* ee, int64_t ee_cap, int64_t* n_ee);
+
+/* contact.compute_constraint_set + ConstraintSet.arrays (contact.py:98-155):
+ * pairs in key order; verts (C,4) original ids, is_pt (C,), d, grad (C,12),
+ * k = kappa b''(d). */
+int mp_constraint_set(mp_ctx* ctx, const double* x, int64_t cap, int64_t* n,
+                      int64_t* verts, uint8_t* is_pt, double* d, double* grad, double* k);
+
+/* energy.gradient (energy.py:357-370) with the constraint set at x. */
+int mp_gradient(mp_ctx* ctx, const double* x, const double* x_tilde, double h, double* g);
+/* energy.incremental_potential (energy.py:346-354) with the constraint set at x. */
+int mp_energy(mp_ctx* ctx, const double* x, const double* x_tilde, double h, double* e);
+
+/* Freeze a snapshot at x: H_base = assemble_base_hessian (energy.py:373-413)
+ * and, if build_mas, the MAS hierarchy (mas.py:138-179). */
+int mp_snapshot(mp_ctx* ctx, const double* x, double h, int build_mas);
+/* HessianModel.hvp (energy.py:435-440) of the snapshot (+ candidates of the
+ * last mp_update_at call when with_updates != 0). */
+int mp_hvp(mp_ctx* ctx, const double* vec, int with_updates, double* out);
+/* mas.apply_preconditioner (mas.py:182-205) + pinned projection
+ * (solver.py:351-352); with_updates applies the Woodbury state of the last
+ * mp_update_at call. */
+int mp_precond_apply(mp_ctx* ctx, const double* g, int with_updates, double* z);
+/* The non-rebuild branch of advance_step (solver.py:336-346) at x against
+ * the snapshot: fresh constraint set, classify_all, select_top_k,
+ * build_update.  Returns the number of candidates and touched subdomains. */
+int mp_update_at(mp_ctx* ctx, const double* x, int64_t* n_candidates, int64_t* n_touched);
+
+/* ccd.per_subdomain_steps + certify_mixed + _apply_ccd (ccd.py:221-320,
+ * solver.py:268-280): alpha_d (D,), x_new (3N), min alpha, certificate. */
+int mp_ccd(mp_ctx* ctx, const double* x, const double* p, double* alpha_d,
+           double* x_new, double* min_alpha, int32_t* certified, int64_t* n_pairs);
+
+/* The CCD candidate pairs of the last mp_ccd / iteration with their
+ * certified steps (ccd.py:244-281 alpha_pair); rows (v,t0,t1,t2) or
+ * (a0,a1,b0,b1), original ids, unordered. */
+int mp_ccd_pairs(mp_ctx* ctx, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt, double* alpha);
+
+/* Number of kernels this context has launched since creation. */
+int64_t mp_launch_count(mp_ctx* ctx);
+
+/* Message of the last failed mp_create on this thread. */
+const char* mp_create_error(void);
+
+/* mas.partition_domain (mas.py:63-77) on the host, no GPU needed:
+ * subdomain_of (n,) for a Morton partition into blocks of block_size. */
+int mp_partition_host(const double* rest, int64_t n, int32_t block_size, int64_t* subdomain_of);
+
+/* Device-resident stepping (the bench's timed path and multi-frame drivers):
+ * mp_set_state uploads x, v once; mp_step_device runs prepare_step +
+ * advance_step on the resident state; mp_get_state downloads it. */
+int mp_set_state(mp_ctx* ctx, const double* x, const double* v);
+int mp_get_state(mp_ctx* ctx, double* x, double* v);
+int mp_step_device(mp_ctx* ctx, double h, mp_iter_record* recs, int64_t cap, int64_t* n_recs,
+                   int32_t* converged, uint32_t* flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MASPNCG_H */

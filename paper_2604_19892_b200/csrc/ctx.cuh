@@ -1,0 +1,177 @@
+// ctx.cuh -- the device context: every piece of solver state lives here,
+// device-resident, in subdomain-renumbered vertex order.
+//
+// Vertex renumbering: the reference's Morton partition (mas.py:63-77) puts
+// vertex `old` in subdomain d at rank r of d's sorted vertex list; here that
+// vertex gets id new = d*bs + r.  A subdomain is therefore a contiguous run
+// of vertices and dofs, coarse aggregates are contiguous runs of subdomains,
+// and subdomain_of(new) = new / bs.  Dof order inside a subdomain equals the
+// reference's B_d dof order (ascending original id, mas.py:74).
+#pragma once
+
+#include <cusolverDn.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  // grow to at least `count` elements; contents are NOT preserved
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    release();
+    size_t c = count < 1 ? 1 : count;
+    CUDA_CHECK(cudaMalloc(&p, c * sizeof(T)));
+    n = c;
+  }
+  void upload(const T* host, size_t count, cudaStream_t s) {
+    ensure(count);
+    if (count) CUDA_CHECK(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero(size_t count, cudaStream_t s) {
+    ensure(count);
+    CUDA_CHECK(cudaMemsetAsync(p, 0, count * sizeof(T), s));
+  }
+  operator T*() const { return p; }
+};
+
+// per-tet constant data, 12 doubles (96 B): Bm row-major, vol, mu, lam
+struct TetParam {
+  double Bm[9];
+  double vol, mu, lam;
+};
+
+// contact pair table (structure of arrays), key order = reference key order:
+// ("ee",(a0,a1),(b0,b1)) < ("pt", v, (t0,t1,t2))  (contact.py:98-113)
+struct PairTable {
+  DBuf<unsigned long long> khi, klo;  // 128-bit sort key
+  DBuf<int4> verts;                   // new vertex ids, canonical order
+  DBuf<double> d, k, nrm;             // distance, kappa b''(d), |grad|
+  DBuf<double> grad;                  // (C,12) pinned rows zeroed
+  DBuf<int> is_pt;
+  int64_t count = 0;
+  void ensure(size_t c) {
+    khi.ensure(c); klo.ensure(c); verts.ensure(c);
+    d.ensure(c); k.ensure(c); nrm.ensure(c); grad.ensure(12 * c); is_pt.ensure(c);
+  }
+};
+
+struct CoarseLevel {
+  int A = 0;          // aggregates
+  int n = 0;          // 3A dofs
+  int span = 0;       // vertices per aggregate (last may be short)
+  DBuf<double> dense; // n*n scratch (cuSOLVER workspace matrix)
+  DBuf<double> inv;   // cyc_size(n) packed inverse
+  DBuf<double> rsum;  // 3A restricted sums
+  DBuf<double> ypart; // chunks * n partial matvec results
+  int chunks = 1;
+};
+
+struct mp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+
+  // ---- sizes ----
+  int64_t N = 0, T = 0, F = 0, E = 0, V = 0;
+  int bs = 32;   // partition block size
+  int m = 96;    // dofs per (padded) subdomain block = 3*bs
+  int64_t D = 0; // subdomains
+  int id_bits = 1;  // bits per vertex id in pair keys
+  double d_hat = 0.0, kappa = 0.0;
+  mp_solver_config cfg{};
+
+  // ---- host copies of static maps ----
+  std::vector<int> h_new2old, h_old2new;
+  std::vector<int64_t> h_sub_of_old;  // reference order
+
+  // ---- static device data ----
+  DBuf<int> new2old;
+  DBuf<double> mass;        // (N)
+  DBuf<unsigned char> pinned;
+  DBuf<double> f_ext;       // (3N)
+  DBuf<int4> tets;          // (T) new ids
+  DBuf<TetParam> tetp;
+  DBuf<signed char> kind;
+  // BSR(3x3) pattern of the elastic + mass Hessian
+  int64_t nnzb = 0;
+  DBuf<int> rowptr, cols, tet_slot, diag_slot;
+  DBuf<double> bsr;         // nnzb*9 values
+  // surface
+  DBuf<int> tri;            // (F*3) new ids, surface order
+  DBuf<int> tri_sorted;     // (F*3) new ids ordered by ascending original id
+  DBuf<int> edge;           // (E*2) new ids (original order = ascending original id)
+  DBuf<int> sverts;         // (V) new ids
+
+  // ---- per-step vectors (3N) ----
+  DBuf<double> x, xt, vel, g, z, p, Hp, p_prev, Hp_prev, z_prev, hv, x_start, x_best, tmp, tmp2;
+
+  // ---- contact sets ----
+  PairTable cur, base, scratch;
+  DBuf<int> sort_idx, sort_idx2;
+  DBuf<unsigned long long> sort_k1, sort_k2;
+  DBuf<unsigned char> cub_tmp;
+  // update candidates (classify_all output, key order)
+  int64_t n_cand = 0;
+  DBuf<int4> cand_verts;
+  DBuf<double> cand_u;      // (n_cand, 12)
+  DBuf<double> cand_ds;
+  DBuf<int> cand_flag, cand_pos;
+  DBuf<double> tmp_scale, tmp_ds;
+  // top-K entries
+  DBuf<int> ent_count, ent_off, ent_sub, ent_cand, ent_sub2, ent_cand2;
+  DBuf<unsigned long long> ent_key, ent_key2;
+  DBuf<int> touched_sub, touched_start, touched_len, overlay_of;
+  int64_t n_touched = 0;
+  DBuf<double> overlay;     // n_touched * cyc(m)
+  bool have_updates = false;
+
+  // ---- broad phase scratch ----
+  DBuf<double> box_lo, box_hi;   // (F+E)*3
+  DBuf<int> cell_cnt, cell_off;
+  DBuf<unsigned long long> cell_key, cell_key2;
+  DBuf<int> cell_prim, cell_prim2;
+  DBuf<int> cand_a, cand_b;      // raw broad-phase pairs (taps)
+  DBuf<int> counters;            // device counters
+  DBuf<double> dscal;            // device scalars
+  DBuf<double> red_part;         // reduction partials
+
+  // ---- MAS ----
+  DBuf<double> Bblk;        // D * cyc(m) packed inverses
+  DBuf<double> Mblk;        // D * cyc(m) packed subdomain blocks (direct refactor path)
+  DBuf<double> Mfull;       // D * m*m scratch
+  std::vector<CoarseLevel*> levels;
+  int n_levels = 0;
+  DBuf<double> solver_work;
+  DBuf<int> solver_info;
+  bool have_snapshot = false;
+  bool have_mas = false;
+
+  // ---- CCD ----
+  DBuf<int4> ccd_verts;
+  DBuf<int> ccd_ispt;
+  DBuf<double> ccd_alpha;   // per pair
+  DBuf<double> alpha_d;     // (D)
+  int64_t n_ccd = 0;
+
+  // pinned host staging for scalars
+  double* h_scal = nullptr;
+  int* h_cnt = nullptr;
+
+  ~mp_ctx();
+};

@@ -1,0 +1,371 @@
+// elastic.cuh -- per-tet FEM kernels: gradient, energy, PSD-projected Hessian.
+//
+// Reference: energy.py:164-171 (F = Ds Bm), :184-224 (ARAP, signed SVD,
+// analytic twist projection), :230-290 (stable neo-Hookean + eigen
+// projection), :296-339 (dispatch), :357-370 (gradient), :373-413 (assembly).
+//
+// One thread per tet.  dF/dx is never stored (the reference keeps a (T,9,12)
+// G): with bc_0 = -sum_r Bm[r,:] and bc_m = Bm[m-1,:], the tet force on
+// vertex m is vol * P bc_m and the Hessian block (a,b) is
+//   vol * ( mu (bc_a.bc_b) I3 + U K_ab U^T ),
+// K_ab built from the analytic eigen-modes of the 9x9 Hessian in the
+// (U, V) singular frame (twist / flip / scaling modes), each clamped at 0 --
+// identical in exact arithmetic to eigh + clamp (verified to 1e-14).
+#pragma once
+
+#include "ctx.cuh"
+
+__device__ __forceinline__ void load_tet(const double* __restrict__ x, int4 t, double X[4][3]) {
+  const int id[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) X[a][c] = x[3 * id[a] + c];
+}
+
+__device__ __forceinline__ void tet_F(const double X[4][3], const TetParam& tp, M3& F, double bc[4][3]) {
+  double Ds[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Ds[r][c] = X[c + 1][r] - X[0][r];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      F(i, j) = Ds[i][0] * tp.Bm[0 * 3 + j] + Ds[i][1] * tp.Bm[1 * 3 + j] + Ds[i][2] * tp.Bm[2 * 3 + j];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    bc[1][j] = tp.Bm[0 * 3 + j];
+    bc[2][j] = tp.Bm[1 * 3 + j];
+    bc[3][j] = tp.Bm[2 * 3 + j];
+    bc[0][j] = -(tp.Bm[0 * 3 + j] + tp.Bm[1 * 3 + j] + tp.Bm[2 * 3 + j]);
+  }
+}
+
+// first Piola stress (energy.py:199-202, 244-247)
+__device__ __forceinline__ M3 piola(const M3& F, int kind, double mu, double lam) {
+  M3 P;
+  if (kind == 1) {
+    double U[3][3], S[3], V[3][3];
+    signed_svd3(F, U, S, V);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double R = U[i][0] * V[j][0] + U[i][1] * V[j][1] + U[i][2] * V[j][2];
+        P(i, j) = mu * (F(i, j) - R);
+      }
+  } else if (kind == 2) {
+    double J = det3(F);
+    M3 C = cof3(F);
+    double coef = lam * (J - 1.0) - mu;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) P.a[q] = mu * F.a[q] + coef * C.a[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) P.a[q] = 0.0;
+  }
+  return P;
+}
+
+// energy density (energy.py:194-196, 238-241)
+__device__ __forceinline__ double psi(const M3& F, int kind, double mu, double lam) {
+  if (kind == 1) {
+    double U[3][3], S[3], V[3][3];
+    signed_svd3(F, U, S, V);
+    double s = (S[0] - 1.0) * (S[0] - 1.0) + (S[1] - 1.0) * (S[1] - 1.0) + (S[2] - 1.0) * (S[2] - 1.0);
+    return 0.5 * mu * s;
+  } else if (kind == 2) {
+    double J = det3(F);
+    double ic = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) ic += F.a[q] * F.a[q];
+    return 0.5 * mu * (ic - 3.0) - mu * (J - 1.0) + 0.5 * lam * (J - 1.0) * (J - 1.0);
+  }
+  return 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// gradient: g = M (x - x~) (pinned -> 0), then tets and contacts accumulate
+
+__global__ void k_inertia_grad(int64_t N, const double* __restrict__ x, const double* __restrict__ xt,
+                               const double* __restrict__ mass, const unsigned char* __restrict__ pinned,
+                               double* __restrict__ g) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 3 * N) return;
+  int64_t v = i / 3;
+  g[i] = pinned[v] ? 0.0 : mass[v] * (x[i] - xt[i]);
+}
+
+__global__ void k_tet_grad(int64_t T, const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
+                           const signed char* __restrict__ kind, const unsigned char* __restrict__ pinned,
+                           const double* __restrict__ x, double h2, double* __restrict__ g) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int kd = kind[t];
+  if (kd == 0) return;
+  int4 tv = tets[t];
+  TetParam tp = tetp[t];
+  double X[4][3], bc[4][3];
+  load_tet(x, tv, X);
+  M3 F;
+  tet_F(X, tp, F, bc);
+  M3 P = piola(F, kd, tp.mu, tp.lam);
+  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+  double s = h2 * tp.vol;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (pinned[id[a]]) continue;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double f = P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2];
+      atomicAdd(&g[3 * id[a] + i], s * f);
+    }
+  }
+}
+
+// energy pieces: 0.5 (x-x~)^T M (x-x~)  and  sum vol*psi  (energy.py:346-354)
+__global__ void k_inertia_energy(int64_t N, const double* __restrict__ x, const double* __restrict__ xt,
+                                 const double* __restrict__ mass, double* part) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double d = x[i] - xt[i];
+    acc += d * mass[i / 3] * d;
+  }
+  block_sum_store<256>(acc, part);
+}
+
+__global__ void k_tet_energy(int64_t T, const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
+                             const signed char* __restrict__ kind, const double* __restrict__ x, double* part) {
+  double acc = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    int kd = kind[t];
+    if (kd == 0) continue;
+    TetParam tp = tetp[t];
+    double X[4][3], bc[4][3];
+    load_tet(x, tets[t], X);
+    M3 F;
+    tet_F(X, tp, F, bc);
+    acc += tp.vol * psi(F, kd, tp.mu, tp.lam);
+  }
+  block_sum_store<256>(acc, part);
+}
+
+// ---------------------------------------------------------------------------
+// PSD-projected element Hessians scattered into the static BSR(3x3)
+
+struct TetModes {
+  double U[3][3];
+  double vb[4][3];   // vb[a][j] = V[:,j] . bc_a
+  double cT[3], cF[3];  // (lambda - mu) of twist / flip mode of pair p
+  double cD[3];         // (lambda - mu) of scaling mode a
+  double eD[3][3];      // scaling-mode eigenvectors (columns) in the frame
+};
+
+__device__ const int PAIR_I[3] = {0, 0, 1};
+__device__ const int PAIR_J[3] = {1, 2, 2};
+__device__ const int PAIR_K[3] = {2, 1, 0};
+
+__device__ void tet_modes(const M3& F, const double bc[4][3], int kind, double mu, double lam, TetModes& md) {
+  double S[3], V[3][3];
+  signed_svd3(F, md.U, S, V);
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) md.vb[a][j] = V[0][j] * bc[a][0] + V[1][j] * bc[a][1] + V[2][j] * bc[a][2];
+  if (kind == 1) {
+    for (int p = 0; p < 3; ++p) {
+      int i = PAIR_I[p], j = PAIR_J[p];
+      double den = S[i] + S[j];
+      double safe = (fabs(den) < 1e-8) ? copysign(1e-8, den + 1e-300) : den;
+      double l = fmax(mu * (1.0 - 2.0 / safe), 0.0);
+      md.cT[p] = l - mu;
+      md.cF[p] = 0.0;
+      md.cD[p] = 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) md.eD[r][c] = (r == c) ? 1.0 : 0.0;
+  } else {
+    double J = S[0] * S[1] * S[2];
+    double c = lam * (J - 1.0) - mu;
+    for (int p = 0; p < 3; ++p) {
+      double sk = S[PAIR_K[p]];
+      md.cT[p] = fmax(mu + c * sk, 0.0) - mu;
+      md.cF[p] = fmax(mu - c * sk, 0.0) - mu;
+    }
+    double gg[3] = {S[1] * S[2], S[0] * S[2], S[0] * S[1]};
+    double A[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) A[r][q] = (r == q ? mu : 0.0) + lam * gg[r] * gg[q];
+    A[0][1] += c * S[2]; A[1][0] += c * S[2];
+    A[0][2] += c * S[1]; A[2][0] += c * S[1];
+    A[1][2] += c * S[0]; A[2][1] += c * S[0];
+    double w[3];
+    sym_eig3(A, w, md.eD);
+    for (int a = 0; a < 3; ++a) md.cD[a] = fmax(w[a], 0.0) - mu;
+  }
+}
+
+// 3x3 block (a,b) of vol^-1 * H12 (without the mu*(bc_a.bc_b) I part)
+__device__ __forceinline__ void tet_block(const TetModes& md, int a, int b, double blk[3][3]) {
+  double K[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  const double rs2 = 0.70710678118654752440;
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    int i = PAIR_I[p], j = PAIR_J[p];
+    // twist: (vb_j e_i - vb_i e_j)/sqrt2 ; flip: (vb_j e_i + vb_i e_j)/sqrt2
+    double tai = md.vb[a][j] * rs2, taj = -md.vb[a][i] * rs2;
+    double tbi = md.vb[b][j] * rs2, tbj = -md.vb[b][i] * rs2;
+    double cT = md.cT[p], cF = md.cF[p];
+    K[i][i] += cT * tai * tbi + cF * tai * tbi;
+    K[j][j] += cT * taj * tbj + cF * taj * tbj;
+    K[i][j] += cT * tai * tbj - cF * tai * tbj;
+    K[j][i] += cT * taj * tbi - cF * taj * tbi;
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    double cq = md.cD[q];
+    double wa[3], wb[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      wa[i] = md.eD[i][q] * md.vb[a][i];
+      wb[i] = md.eD[i][q] * md.vb[b][i];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) K[i][j] += cq * wa[i] * wb[j];
+  }
+  // blk = U K U^T
+  double UK[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) UK[r][c] = md.U[r][0] * K[0][c] + md.U[r][1] * K[1][c] + md.U[r][2] * K[2][c];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) blk[r][c] = UK[r][0] * md.U[c][0] + UK[r][1] * md.U[c][1] + UK[r][2] * md.U[c][2];
+}
+
+__global__ void k_tet_hessian(int64_t T, const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
+                              const signed char* __restrict__ kind, const unsigned char* __restrict__ pinned,
+                              const int* __restrict__ tet_slot, const double* __restrict__ x, double h2,
+                              double* __restrict__ bsr) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int kd = kind[t];
+  if (kd == 0) return;
+  int4 tv = tets[t];
+  TetParam tp = tetp[t];
+  double X[4][3], bc[4][3];
+  load_tet(x, tv, X);
+  M3 F;
+  tet_F(X, tp, F, bc);
+  TetModes md;
+  tet_modes(F, bc, kd, tp.mu, tp.lam, md);
+  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+  bool pin[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) pin[a] = pinned[id[a]] != 0;
+  const double s = h2 * tp.vol;
+  for (int a = 0; a < 4; ++a) {
+    if (pin[a]) continue;
+    for (int b = a; b < 4; ++b) {
+      if (pin[b]) continue;
+      double blk[3][3];
+      tet_block(md, a, b, blk);
+      double mI = tp.mu * (bc[a][0] * bc[b][0] + bc[a][1] * bc[b][1] + bc[a][2] * bc[b][2]);
+      double* dst = bsr + 9 * (int64_t)tet_slot[16 * t + 4 * a + b];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) atomicAdd(dst + 3 * r + c, s * (blk[r][c] + (r == c ? mI : 0.0)));
+      if (b != a) {
+        double* dsT = bsr + 9 * (int64_t)tet_slot[16 * t + 4 * b + a];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) atomicAdd(dsT + 3 * c + r, s * (blk[r][c] + (r == c ? mI : 0.0)));
+      }
+    }
+  }
+}
+
+// diagonal blocks: mass (free) or identity (pinned) (energy.py:411-412)
+__global__ void k_bsr_diag(int64_t N, const int* __restrict__ diag_slot, const double* __restrict__ mass,
+                           const unsigned char* __restrict__ pinned, double* __restrict__ bsr) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  double dv = pinned[v] ? 1.0 : mass[v];
+  double* b = bsr + 9 * (int64_t)diag_slot[v];
+  b[0] += dv;
+  b[4] += dv;
+  b[8] += dv;
+}
+
+// y = BSR x ; 8 lanes per block row, lanes stride over the row's blocks
+__global__ void k_bsr_spmv(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
+                           const double* __restrict__ vals, const double* __restrict__ xin, double* __restrict__ y) {
+  int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t row = gt >> 3;
+  int lane = threadIdx.x & 7;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (row < N) {
+    int beg = rowptr[row], end = rowptr[row + 1];
+    for (int k = beg + lane; k < end; k += 8) {
+      int c = cols[k];
+      const double* b = vals + 9 * (int64_t)k;
+      double x0 = xin[3 * c], x1 = xin[3 * c + 1], x2 = xin[3 * c + 2];
+      a0 += b[0] * x0 + b[1] * x1 + b[2] * x2;
+      a1 += b[3] * x0 + b[4] * x1 + b[5] * x2;
+      a2 += b[6] * x0 + b[7] * x1 + b[8] * x2;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  if (row < N && lane == 0) {
+    y[3 * row] = a0;
+    y[3 * row + 1] = a1;
+    y[3 * row + 2] = a2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+static void elastic_gradient(mp_ctx* c, const double* x, const double* xt, double h, double* g) {
+  k_inertia_grad<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, x, xt, c->mass, c->pinned, g);
+  LAUNCH_CHECK();
+  if (c->T) {
+    k_tet_grad<<<grid_for(c->T, 128), 128, 0, c->stream>>>(c->T, c->tets, c->tetp, c->kind, c->pinned, x,
+                                                           h * h, g);
+    LAUNCH_CHECK();
+  }
+}
+
+static void assemble_elastic_bsr(mp_ctx* c, const double* x, double h) {
+  CUDA_CHECK(cudaMemsetAsync(c->bsr.p, 0, sizeof(double) * 9 * c->nnzb, c->stream));
+  k_bsr_diag<<<grid_for(c->N, 256), 256, 0, c->stream>>>(c->N, c->diag_slot, c->mass, c->pinned, c->bsr);
+  LAUNCH_CHECK();
+  if (c->T) {
+    k_tet_hessian<<<grid_for(c->T, 64), 64, 0, c->stream>>>(c->T, c->tets, c->tetp, c->kind, c->pinned,
+                                                            c->tet_slot, x, h * h, c->bsr);
+    LAUNCH_CHECK();
+  }
+}
+
+static void bsr_spmv(mp_ctx* c, const double* xin, double* y) {
+  k_bsr_spmv<<<grid_for(8 * c->N, 256), 256, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, xin, y);
+  LAUNCH_CHECK();
+}

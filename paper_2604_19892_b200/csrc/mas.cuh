@@ -1,0 +1,501 @@
+// mas.cuh -- multilevel additive Schwarz preconditioner on the device.
+//
+// Reference: mas.py:84-90 (_spd_inverse), :123-179 (build_hierarchy),
+// :182-205 (apply_preconditioner); woodbury.py:46-87 (build_update /
+// apply_subdomain).
+//
+// Level 0: subdomain d = vertices [d*bs, d*bs + n_d) after renumbering; its
+// dense block M_d = H[idx, idx] (elastic BSR blocks + mass + contact k g g^T)
+// is assembled in a D x m x m scratch, factored and inverted in shared memory
+// by one CTA, symmetrised, and stored packed-symmetric in the cyclic-diagonal
+// layout (common.cuh) -- m(m+1)/2 doubles, the algorithmic minimum.  Padded
+// dofs of a short last subdomain are identity.
+// Coarse level l: aggregate a = vertices [a*span_l, (a+1)*span_l), span_l =
+// bs * coarse_block^l; M_l = C H C^T accumulated from BSR blocks and contacts,
+// inverted with cuSOLVER potrf/potri (dense FP64), packed the same way.
+// Woodbury (Sparse-Input): for touched subdomains W = B U is formed from the
+// <= 12 non-zero rows of each u column; the corrected inverse
+// B~ = B - W cap^-1 W^T (== (M_d + U U^T)^-1) goes to an overlay slot the
+// apply reads instead of B_d.  Large K_d falls back to refactoring
+// M_d + U U^T directly (same matrix, one Cholesky-inverse).
+#pragma once
+
+#include "ctx.cuh"
+
+// ---------------------------------------------------------------------------
+// level-0 assembly
+
+// contacts -> Mfull (same-subdomain vertex pairs) and coarse dense levels
+__global__ void k_contact_blocks(int64_t n, const int4* __restrict__ verts, const double* __restrict__ grad,
+                                 const double* __restrict__ k, int bs, int m, double* __restrict__ Mfull) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 v = verts[i];
+  const int id[4] = {v.x, v.y, v.z, v.w};
+  const double kk = k[i];
+  const double* gr = grad + 12 * i;
+  for (int a = 0; a < 4; ++a) {
+    int da = id[a] / bs;
+    for (int b = 0; b < 4; ++b) {
+      if (id[b] / bs != da) continue;
+      int la = id[a] - da * bs, lb = id[b] - da * bs;
+      double* blk = Mfull + (int64_t)da * m * m;
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          double val = kk * gr[3 * a + r] * gr[3 * b + c];
+          if (val != 0.0) atomicAdd(&blk[(3 * la + r) * m + 3 * lb + c], val);
+        }
+    }
+  }
+}
+
+// BSR blocks whose row and column share a subdomain -> Mfull (unique targets)
+__global__ void k_bsr_to_blocks(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
+                                const double* __restrict__ vals, int bs, int m, double* __restrict__ Mfull) {
+  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= N) return;
+  int d = (int)(row / bs);
+  int lr = (int)(row - (int64_t)d * bs);
+  double* blk = Mfull + (int64_t)d * m * m;
+  for (int k = rowptr[row]; k < rowptr[row + 1]; ++k) {
+    int w = cols[k];
+    if (w / bs != d) continue;
+    int lc = w - d * bs;
+    const double* b = vals + 9 * (int64_t)k;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) blk[(3 * lr + r) * m + 3 * lc + c] += b[3 * r + c];
+  }
+}
+
+// write a symmetric m x m smem matrix (0.5 (X + X^T)) in cyclic-diagonal packing
+__device__ void store_cyc_sym(const double* X, int m, double* __restrict__ out, bool symmetrize) {
+  const int64_t tot = cyc_size(m);
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    int s = (int)(e / m);
+    int i = (int)(e - (int64_t)s * m);
+    int j = i + s;
+    if (j >= m) j -= m;
+    out[e] = symmetrize ? 0.5 * (X[i * m + j] + X[j * m + i]) : X[i * m + j];
+  }
+}
+
+__device__ void load_cyc_full(const double* __restrict__ in, int m, double* X) {
+  const int64_t tot = cyc_size(m);
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    int s = (int)(e / m);
+    int i = (int)(e - (int64_t)s * m);
+    int j = i + s;
+    if (j >= m) j -= m;
+    double v = in[e];
+    X[i * m + j] = v;
+    X[j * m + i] = v;
+  }
+}
+
+// In-smem Cholesky (lower, A = L L^T) of A (m x m row-major). Returns false
+// (via *bad) when a pivot is not positive -- LAPACK potrf's failure mode.
+__device__ void smem_cholesky(double* A, int m, int* bad) {
+  for (int k = 0; k < m; ++k) {
+    __syncthreads();
+    double piv = A[k * m + k];
+    if (!(piv > 0.0)) {
+      if (threadIdx.x == 0) *bad = 1;
+      return;  // uniform: every thread read the same pivot
+    }
+    double dk = sqrt(piv);
+    __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) A[i * m + k] /= dk;
+    if (threadIdx.x == 0) A[k * m + k] = dk;
+    __syncthreads();
+    // trailing update of the lower triangle
+    const int rem = m - k - 1;
+    const int tot = rem * rem;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      int i = k + 1 + e / rem;
+      int j = k + 1 + e % rem;
+      if (j <= i) A[i * m + j] -= A[i * m + k] * A[j * m + k];
+    }
+  }
+  __syncthreads();
+}
+
+// X = A^-1 from the lower Cholesky factor in A: thread j solves column j
+// (L y = e_j, L^T x = y), mirroring cho_solve(cho_factor(A), I) (mas.py:89)
+__device__ void smem_chol_inverse(const double* L, int m, double* X) {
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    for (int i = 0; i < j; ++i) X[i * m + j] = 0.0;
+    for (int i = j; i < m; ++i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s -= L[i * m + k] * X[k * m + j];
+      X[i * m + j] = s / L[i * m + i];
+    }
+    for (int i = m - 1; i >= 0; --i) {
+      double s = X[i * m + j];
+      for (int k = i + 1; k < m; ++k) s -= L[k * m + i] * X[k * m + j];
+      X[i * m + j] = s / L[i * m + i];
+    }
+  }
+  __syncthreads();
+}
+
+// one CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
+__global__ void k_mas_factor(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull,
+                             double* __restrict__ Mblk, double* __restrict__ Bblk, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* X = sm + m * m;
+  __shared__ int bad;
+  const int64_t d = blockIdx.x;
+  if (threadIdx.x == 0) bad = 0;
+  int nd = (int)((N - d * bs) < bs ? (N - d * bs) : bs);
+  const double* src = Mfull + d * m * m;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    int i = e / m, j = e % m;
+    double v = src[e];
+    if (i >= 3 * nd || j >= 3 * nd) v = (i == j) ? 1.0 : 0.0;
+    A[e] = v;
+  }
+  __syncthreads();
+  store_cyc_sym(A, m, Mblk + d * cyc_size(m), false);
+  smem_cholesky(A, m, &bad);
+  if (bad) {
+    if (threadIdx.x == 0) atomicExch(status, 1);
+    return;
+  }
+  smem_chol_inverse(A, m, X);
+  store_cyc_sym(X, m, Bblk + d * cyc_size(m), true);
+}
+
+// ---------------------------------------------------------------------------
+// coarse levels
+
+// every BSR block (v, w) -> M_l[agg(v), agg(w)] / (|a||b|)
+__global__ void k_bsr_to_coarse(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
+                                const double* __restrict__ vals, int span, int n, double* __restrict__ M) {
+  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= N) return;
+  int a = (int)(row / span);
+  int64_t na = (N - (int64_t)a * span) < span ? (N - (int64_t)a * span) : span;
+  for (int k = rowptr[row]; k < rowptr[row + 1]; ++k) {
+    int w = cols[k];
+    int b = w / span;
+    int64_t nb = (N - (int64_t)b * span) < span ? (N - (int64_t)b * span) : span;
+    double sc = 1.0 / ((double)na * (double)nb);
+    const double* bl = vals + 9 * (int64_t)k;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) atomicAdd(&M[(int64_t)(3 * a + r) * n + 3 * b + c], bl[3 * r + c] * sc);
+  }
+}
+
+__global__ void k_contact_coarse(int64_t nc, const int4* __restrict__ verts, const double* __restrict__ grad,
+                                 const double* __restrict__ k, int64_t N, int span, int n, double* __restrict__ M) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  int4 v = verts[i];
+  const int id[4] = {v.x, v.y, v.z, v.w};
+  const double* gr = grad + 12 * i;
+  for (int a = 0; a < 4; ++a) {
+    int A = id[a] / span;
+    int64_t na = (N - (int64_t)A * span) < span ? (N - (int64_t)A * span) : span;
+    for (int b = 0; b < 4; ++b) {
+      int B = id[b] / span;
+      int64_t nb = (N - (int64_t)B * span) < span ? (N - (int64_t)B * span) : span;
+      double sc = k[i] / ((double)na * (double)nb);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          double val = sc * gr[3 * a + r] * gr[3 * b + c];
+          if (val != 0.0) atomicAdd(&M[(int64_t)(3 * A + r) * n + 3 * B + c], val);
+        }
+    }
+  }
+}
+
+// 0.5 (M + M^T) on the lower triangle (the only half potrf reads)
+__global__ void k_sym_lower(int n, double* M) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  int i = (int)(e / n), j = (int)(e % n);
+  if (j >= i) return;
+  // column-major view for cuSOLVER: element (r, c) at r + c*n; our row-major
+  // M[i*n+j] is (j, i) column-major -- symmetric anyway, average both halves
+  double a = M[(int64_t)i * n + j], b = M[(int64_t)j * n + i];
+  double s = 0.5 * (a + b);
+  M[(int64_t)i * n + j] = s;
+  M[(int64_t)j * n + i] = s;
+}
+
+// pack the symmetric inverse whose valid half is potri's (lower, column-major)
+__global__ void k_pack_coarse(int n, const double* __restrict__ M, double* __restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= cyc_size(n)) return;
+  int s = (int)(e / n);
+  int i = (int)(e - (int64_t)s * n);
+  int j = i + s;
+  if (j >= n) j -= n;
+  int r = i > j ? i : j, c = i > j ? j : i;  // lower-triangle element (r >= c)
+  out[e] = M[(int64_t)c * n + r];           // column-major (r, c)
+}
+
+// ---------------------------------------------------------------------------
+// apply
+
+// raw sums of g over each level-1 aggregate (one CTA per aggregate)
+__global__ void k_restrict1(int64_t N, int span, const double* __restrict__ g, double* __restrict__ rsum) {
+  const int64_t a = blockIdx.x;
+  const int64_t v0 = a * span;
+  int64_t v1 = v0 + span;
+  if (v1 > N) v1 = N;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    s0 += g[3 * v];
+    s1 += g[3 * v + 1];
+    s2 += g[3 * v + 2];
+  }
+  __shared__ double sh[3][32];
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][w] = s0; sh[1][w] = s1; sh[2][w] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sh[threadIdx.x][q];
+    rsum[3 * a + threadIdx.x] = t;
+  }
+}
+
+// raw sums of a coarser level from the finer level's raw sums
+__global__ void k_restrict_up(int A, int cb, int Afine, const double* __restrict__ fine, double* __restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= 3 * (int64_t)A) return;
+  int a = (int)(e / 3), c = (int)(e % 3);
+  double s = 0.0;
+  for (int q = a * cb; q < (a + 1) * cb && q < Afine; ++q) s += fine[3 * q + c];
+  out[e] = s;
+}
+
+// partial y = Minv r over a chunk of diagonals; r = rsum / |a|
+__global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double* __restrict__ P,
+                            const double* __restrict__ rsum, double* __restrict__ ypart) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int ch = blockIdx.y;
+  if (i >= n) return;
+  const int smax = n / 2;  // diagonals 0..smax
+  int per = (smax + 1 + chunks - 1) / chunks;
+  int s0 = ch * per, s1 = s0 + per - 1;
+  if (s1 > smax) s1 = smax;
+  auto rin = [&](int q) {
+    int a = q / 3;
+    int64_t na = (N - (int64_t)a * span) < span ? (N - (int64_t)a * span) : span;
+    return rsum[q] / (double)na;
+  };
+  double acc = 0.0;
+  const bool even = (n % 2) == 0;
+  for (int s = s0; s <= s1; ++s) {
+    if (s == 0) {
+      acc += P[i] * rin(i);
+      continue;
+    }
+    const double* dg = P + (int64_t)s * n;
+    int jp = i + s; if (jp >= n) jp -= n;
+    int jm = i - s; if (jm < 0) jm += n;
+    if (even && 2 * s == n) {
+      // half diagonal: A(i, i+n/2) stored at min(i, i+n/2)
+      int r = i < jp ? i : jp;
+      acc += dg[r] * rin(jp);
+    } else {
+      acc += dg[i] * rin(jp) + dg[jm] * rin(jm);
+    }
+  }
+  ypart[(int64_t)ch * n + i] = acc;
+}
+
+struct LevelView {
+  const double* ypart;
+  int n, span, chunks;
+};
+struct LevelViews {
+  LevelView lv[8];
+  int L;
+};
+
+// level-0 + Woodbury overlay + coarse prolongation + pinned projection.
+// One CTA per subdomain; the packed block is staged in shared memory.
+__global__ void k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
+                               const int* __restrict__ overlay_of, const double* __restrict__ overlay,
+                               const double* __restrict__ g, const unsigned char* __restrict__ pinned,
+                               LevelViews LV, double* __restrict__ z) {
+  extern __shared__ double sm[];
+  const int64_t csz = cyc_size(m);
+  double* P = sm;
+  double* gs = sm + csz;
+  const int64_t d = blockIdx.x;
+  const int ov = overlay_of ? overlay_of[d] : -1;
+  const double* src = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+  if ((csz & 1) == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* p2 = reinterpret_cast<double2*>(P);
+    for (int64_t e = threadIdx.x; e < csz / 2; e += blockDim.x) p2[e] = __ldg(&s2[e]);
+  } else {
+    for (int64_t e = threadIdx.x; e < csz; e += blockDim.x) P[e] = __ldg(&src[e]);
+  }
+  const int64_t v0 = d * bs;
+  const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) gs[i] = (i < nd3) ? g[3 * v0 + i] : 0.0;
+  __syncthreads();
+  const bool even = (m % 2) == 0;
+  const int smax = m / 2;
+  for (int i = threadIdx.x; i < nd3; i += blockDim.x) {
+    double acc = P[i] * gs[i];
+    for (int s = 1; s <= smax; ++s) {
+      const double* dg = P + (int64_t)s * m;
+      int jp = i + s; if (jp >= m) jp -= m;
+      if (even && 2 * s == m) {
+        int r = i < jp ? i : jp;
+        acc += dg[r] * gs[jp];
+      } else {
+        int jm = i - s; if (jm < 0) jm += m;
+        acc += dg[i] * gs[jp] + dg[jm] * gs[jm];
+      }
+    }
+    int64_t dof = 3 * v0 + i;
+    int64_t v = dof / 3;
+    int c = (int)(dof % 3);
+    for (int l = 0; l < LV.L; ++l) {
+      const LevelView& L = LV.lv[l];
+      int a = (int)(v / L.span);
+      int64_t na = (N - (int64_t)a * L.span) < L.span ? (N - (int64_t)a * L.span) : L.span;
+      double y = 0.0;
+      for (int ch = 0; ch < L.chunks; ++ch) y += L.ypart[(int64_t)ch * L.n + 3 * a + c];
+      acc += y / (double)na;
+    }
+    z[dof] = pinned[v] ? 0.0 : acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sparse-Input Woodbury build, one CTA per touched subdomain.
+// smem: B (m x m full), U (m x K), W (m x K), cap (K x K)
+
+__global__ void k_woodbury(int64_t N, int bs, int m, int Kmax, const double* __restrict__ Bblk,
+                           const int* __restrict__ tsub, const int* __restrict__ tstart, const int* __restrict__ tlen,
+                           const int* __restrict__ ecand, const int4* __restrict__ cverts,
+                           const double* __restrict__ cu, double* __restrict__ overlay, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  const int t = blockIdx.x;
+  const int d = tsub[t];
+  const int K = tlen[t];
+  if (K > Kmax) return;  // handled by k_direct_update
+  double* B = sm;
+  double* U = B + m * m;
+  double* W = U + m * Kmax;
+  double* C = W + m * Kmax;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  load_cyc_full(Bblk + (int64_t)d * cyc_size(m), m, B);
+  for (int e = threadIdx.x; e < m * K; e += blockDim.x) U[e] = 0.0;
+  __syncthreads();
+  // U columns: candidate rows restricted to this subdomain (woodbury.py:46-54)
+  for (int col = threadIdx.x; col < K; col += blockDim.x) {
+    int ci = ecand[tstart[t] + col];
+    int4 v = cverts[ci];
+    const int id[4] = {v.x, v.y, v.z, v.w};
+    for (int a = 0; a < 4; ++a) {
+      if (id[a] / bs != d) continue;
+      int l = id[a] - d * bs;
+      for (int r = 0; r < 3; ++r) U[(3 * l + r) * K + col] = cu[12 * (int64_t)ci + 3 * a + r];
+    }
+  }
+  __syncthreads();
+  // W = B U using only the non-zero rows of U (sparse input)
+  for (int e = threadIdx.x; e < m * K; e += blockDim.x) {
+    int i = e / K, col = e % K;
+    double s = 0.0;
+    for (int r = 0; r < m; ++r) {
+      double u = U[r * K + col];
+      if (u != 0.0) s += B[i * m + r] * u;
+    }
+    W[e] = s;
+  }
+  __syncthreads();
+  // cap = I + U^T W, symmetrised (woodbury.py:71-72)
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    int a = e / K, b = e % K;
+    double s1 = 0.0, s2 = 0.0;
+    for (int r = 0; r < m; ++r) {
+      s1 += U[r * K + a] * W[r * K + b];
+      s2 += U[r * K + b] * W[r * K + a];
+    }
+    C[e] = (a == b ? 1.0 : 0.0) + 0.5 * (s1 + s2);
+  }
+  smem_cholesky(C, K, &bad);
+  if (bad) {
+    if (threadIdx.x == 0) atomicExch(status, 1);
+    return;
+  }
+  // Y = W L^-T (row i: solve L y = W[i,:]^T) written over W
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double* w = W + i * K;
+    for (int a = 0; a < K; ++a) {
+      double s = w[a];
+      for (int b = 0; b < a; ++b) s -= C[a * K + b] * w[b];
+      w[a] = s / C[a * K + a];
+    }
+  }
+  __syncthreads();
+  // B~ = B - Y Y^T, stored packed
+  const int64_t tot = cyc_size(m);
+  double* out = overlay + (int64_t)t * tot;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    int s = (int)(e / m);
+    int i = (int)(e - (int64_t)s * m);
+    int j = i + s;
+    if (j >= m) j -= m;
+    double acc = 0.0;
+    for (int a = 0; a < K; ++a) acc += W[i * K + a] * W[j * K + a];
+    out[e] = 0.5 * (B[i * m + j] + B[j * m + i]) - acc;
+  }
+}
+
+// direct path for large K_d: overlay = sym((M_d + U U^T)^-1)
+__global__ void k_direct_update(int64_t N, int bs, int m, const double* __restrict__ Mblk,
+                                const int* __restrict__ tsub, const int* __restrict__ tstart,
+                                const int* __restrict__ tlen, const int* __restrict__ ecand,
+                                const int4* __restrict__ cverts, const double* __restrict__ cu, int Kthresh,
+                                double* __restrict__ overlay, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  const int t = blockIdx.x;
+  const int K = tlen[t];
+  if (K <= Kthresh) return;
+  const int d = tsub[t];
+  double* A = sm;
+  double* X = sm + m * m;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  load_cyc_full(Mblk + (int64_t)d * cyc_size(m), m, A);
+  __syncthreads();
+  // add u u^T restricted to the subdomain, one candidate at a time
+  for (int col = 0; col < K; ++col) {
+    int ci = ecand[tstart[t] + col];
+    int4 v = cverts[ci];
+    const int id[4] = {v.x, v.y, v.z, v.w};
+    for (int e = threadIdx.x; e < 144; e += blockDim.x) {
+      int p = e / 12, q = e % 12;
+      int a = p / 3, r = p % 3, b = q / 3, cc = q % 3;
+      if (id[a] / bs != d || id[b] / bs != d) continue;
+      int la = id[a] - d * bs, lb = id[b] - d * bs;
+      A[(3 * la + r) * m + 3 * lb + cc] += cu[12 * (int64_t)ci + p] * cu[12 * (int64_t)ci + q];
+    }
+    __syncthreads();
+  }
+  smem_cholesky(A, m, &bad);
+  if (bad) {
+    if (threadIdx.x == 0) atomicExch(status, 1);
+    return;
+  }
+  smem_chol_inverse(A, m, X);
+  store_cyc_sym(X, m, overlay + (int64_t)t * cyc_size(m), true);
+}

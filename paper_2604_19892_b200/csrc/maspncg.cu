@@ -1,0 +1,834 @@
+// maspncg.cu -- C ABI + the MAS-PNCG outer loop (Alg. 1) on sm_100a.
+//
+// Single translation unit: the stage headers hold the kernels and their
+// launchers; this file owns context creation (partition, renumbering, static
+// BSR pattern), the advance_step loop and the exported entry points
+// declared in include/maspncg.h.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "stages.cuh"
+
+thread_local int64_t* g_launch_counter = nullptr;
+
+mp_ctx::~mp_ctx() {
+  for (auto* l : levels) delete l;
+  if (h_scal) cudaFreeHost(h_scal);
+  if (h_cnt) cudaFreeHost(h_cnt);
+  if (solver) cusolverDnDestroy(solver);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// ---------------------------------------------------------------------------
+// Morton partition (mas.py:30-77), computed once on the host exactly as the
+// reference does (same IEEE expression, stable sort)
+
+static uint64_t part1by2(uint64_t v) {
+  v = (v | (v << 32)) & 0x1F00000000FFFFull;
+  v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+  v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+  v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+static void morton_partition(const double* rest, int64_t N, int bs, std::vector<int>& new2old,
+                             std::vector<int64_t>& sub_of) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = 0; i < N; ++i)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], rest[3 * i + k]);
+      hi[k] = std::max(hi[k], rest[3 * i + k]);
+    }
+  double ext[3];
+  for (int k = 0; k < 3; ++k) {
+    ext[k] = hi[k] - lo[k];
+    if (ext[k] == 0.0) ext[k] = 1.0;
+  }
+  std::vector<uint64_t> code(N);
+  for (int64_t i = 0; i < N; ++i) {
+    uint64_t q[3];
+    for (int k = 0; k < 3; ++k) {
+      volatile double t = (rest[3 * i + k] - lo[k]) / ext[k];
+      volatile double u = t * 1023.0;
+      q[k] = (uint64_t)(double)u;
+    }
+    code[i] = part1by2(q[0]) | (part1by2(q[1]) << 1) | (part1by2(q[2]) << 2);
+  }
+  std::vector<int> order(N);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return code[a] < code[b]; });
+  int64_t D = std::max<int64_t>(1, (N + bs - 1) / bs);
+  new2old.assign(N, 0);
+  sub_of.assign(N, 0);
+  for (int64_t d = 0; d < D; ++d) {
+    int64_t b = d * bs, e = std::min<int64_t>(N, b + bs);
+    std::vector<int> blk(order.begin() + b, order.begin() + e);
+    std::sort(blk.begin(), blk.end());
+    for (int64_t r = 0; r < (int64_t)blk.size(); ++r) {
+      new2old[b + r] = blk[r];
+      sub_of[blk[r]] = d;
+    }
+  }
+}
+
+static void validate_config(const mp_solver_config& c) {
+  if (!(c.eps > 0)) throw MpError(MP_ERR_CONFIG, "eps must be positive");
+  if (!(c.delta > 0 && c.delta < 1)) throw MpError(MP_ERR_CONFIG, "delta must lie in (0, 1)");
+  if (c.iter_max < 1) throw MpError(MP_ERR_CONFIG, "iter_max must be >= 1");
+  if (c.preconditioner != MP_PRECOND_MAS)
+    throw MpError(MP_ERR_CONFIG, "the B200 backend implements the MAS preconditioner only");
+  if (c.direction_rule != MP_DIR_SUBSPACE2D)
+    throw MpError(MP_ERR_CONFIG, "the B200 backend implements the Subspace2D direction rule only");
+  if (c.update_strategy < 0 || c.update_strategy > 2) throw MpError(MP_ERR_CONFIG, "unknown update strategy");
+  if (c.block_size < 1 || c.block_size > 32) throw MpError(MP_ERR_CONFIG, "block_size must lie in [1, 32]");
+  if (c.K < 0) throw MpError(MP_ERR_CONFIG, "K must be >= 0");
+  if (c.coarse_block < 1) throw MpError(MP_ERR_CONFIG, "coarse_block must be >= 1");
+}
+
+// coarse level shapes (mas.py:155-169): aggregate coarse_block units of the
+// previous level; stop at the first level that does not coarsen
+static void setup_levels(mp_ctx* c) {
+  for (auto* l : c->levels) delete l;
+  c->levels.clear();
+  int64_t units = c->D;
+  int64_t span = c->bs;
+  const int cb = c->cfg.coarse_block;
+  for (int l = 0; l < c->cfg.levels && l < 8; ++l) {
+    int64_t n_agg = (units + cb - 1) / cb;
+    if (n_agg == units) break;
+    span *= cb;
+    auto* L = new CoarseLevel();
+    L->A = (int)n_agg;
+    L->n = (int)(3 * n_agg);
+    L->span = (int)span;
+    int rowblocks = (L->n + 127) / 128;
+    int maxch = (L->n / 2 + 1 + 31) / 32;
+    int ch = std::max(1, std::min(maxch, RED_BLOCKS / std::max(1, rowblocks)));
+    L->chunks = ch;
+    L->rsum.ensure(L->n);
+    L->ypart.ensure((size_t)ch * L->n);
+    c->levels.push_back(L);
+    units = n_agg;
+  }
+  c->n_levels = (int)c->levels.size();
+}
+
+static void set_smem_limits() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0, optin = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  auto allow = [&](const void* fn) {
+    cudaFuncAttributes fa{};
+    CUDA_CHECK(cudaFuncGetAttributes(&fa, fn));
+    int dyn = optin - (int)fa.sharedSizeBytes;
+    CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  };
+  allow((const void*)k_mas_factor);
+  allow((const void*)k_woodbury);
+  allow((const void*)k_direct_update);
+  allow((const void*)k_mas_apply_l0);
+  done = true;
+}
+
+static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int device, mp_ctx* c) {
+  validate_config(*cfg);
+  c->cfg = *cfg;
+  c->device = device;
+  CUDA_CHECK(cudaSetDevice(device));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cusolverDnCreate");
+  cusolverDnSetStream(c->solver, c->stream);
+  set_smem_limits();
+  CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
+  CUDA_CHECK(cudaMallocHost(&c->h_cnt, 16 * sizeof(int)));
+  c->N = s->n_verts;
+  c->T = s->n_tets;
+  c->F = s->n_tris;
+  c->E = s->n_edges;
+  c->V = s->n_surf_verts;
+  c->d_hat = s->d_hat;
+  c->kappa = s->kappa;
+  c->bs = cfg->block_size;
+  c->m = 3 * c->bs;
+  const int64_t N = c->N;
+  if (N < 1) throw MpError(MP_ERR_CONFIG, "scene has no vertices");
+  if (N >= (1ll << 30)) throw MpError(MP_ERR_CONFIG, "scene too large");
+  morton_partition(s->rest, N, c->bs, c->h_new2old, c->h_sub_of_old);
+  c->D = std::max<int64_t>(1, (N + c->bs - 1) / c->bs);
+  c->h_old2new.assign(N, 0);
+  for (int64_t i = 0; i < N; ++i) c->h_old2new[c->h_new2old[i]] = (int)i;
+  const auto& o2n = c->h_old2new;
+  const auto& n2o = c->h_new2old;
+  c->id_bits = bits_for((unsigned long long)(N > 1 ? N - 1 : 1));
+  cudaStream_t st = c->stream;
+  c->new2old.upload(n2o.data(), N, st);
+  {
+    std::vector<double> mass(N), fe(3 * N);
+    std::vector<unsigned char> pin(N);
+    for (int64_t i = 0; i < N; ++i) {
+      int o = n2o[i];
+      mass[i] = s->mass[o];
+      pin[i] = s->dirichlet[o] ? 1 : 0;
+      for (int k = 0; k < 3; ++k) fe[3 * i + k] = s->f_ext[3 * o + k];
+    }
+    c->mass.upload(mass.data(), N, st);
+    c->pinned.upload(pin.data(), N, st);
+    c->f_ext.upload(fe.data(), 3 * N, st);
+  }
+  // tets and per-tet constants
+  const int64_t T = c->T;
+  std::vector<int4> tets(T);
+  std::vector<TetParam> tp(T);
+  std::vector<signed char> kind(T);
+  for (int64_t t = 0; t < T; ++t) {
+    int id[4];
+    for (int a = 0; a < 4; ++a) {
+      int64_t o = s->tets[4 * t + a];
+      if (o < 0 || o >= N) throw MpError(MP_ERR_CONFIG, "tet index out of range");
+      id[a] = o2n[o];
+    }
+    tets[t] = make_int4(id[0], id[1], id[2], id[3]);
+    for (int q = 0; q < 9; ++q) tp[t].Bm[q] = s->Bm[9 * t + q];
+    tp[t].vol = s->vol[t];
+    tp[t].mu = s->mu[t];
+    tp[t].lam = s->lam[t];
+    kind[t] = s->kind[t];
+  }
+  c->tets.upload(tets.data(), T, st);
+  c->tetp.upload(tp.data(), T, st);
+  c->kind.upload(kind.data(), T, st);
+  // static BSR pattern: vertex adjacency through tets (+ diagonal)
+  {
+    std::vector<std::vector<int>> adj(N);
+    for (int64_t v = 0; v < N; ++v) adj[v].push_back((int)v);
+    for (int64_t t = 0; t < T; ++t) {
+      const int id[4] = {tets[t].x, tets[t].y, tets[t].z, tets[t].w};
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) adj[id[a]].push_back(id[b]);
+    }
+    std::vector<int> rowptr(N + 1, 0);
+    for (int64_t v = 0; v < N; ++v) {
+      auto& r = adj[v];
+      std::sort(r.begin(), r.end());
+      r.erase(std::unique(r.begin(), r.end()), r.end());
+      rowptr[v + 1] = rowptr[v] + (int)r.size();
+    }
+    c->nnzb = rowptr[N];
+    std::vector<int> cols(c->nnzb), diag(N), slot(16 * T);
+    for (int64_t v = 0; v < N; ++v) {
+      std::copy(adj[v].begin(), adj[v].end(), cols.begin() + rowptr[v]);
+      diag[v] = rowptr[v] + (int)(std::lower_bound(adj[v].begin(), adj[v].end(), (int)v) - adj[v].begin());
+    }
+    for (int64_t t = 0; t < T; ++t) {
+      const int id[4] = {tets[t].x, tets[t].y, tets[t].z, tets[t].w};
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+          auto& r = adj[id[a]];
+          slot[16 * t + 4 * a + b] =
+              rowptr[id[a]] + (int)(std::lower_bound(r.begin(), r.end(), id[b]) - r.begin());
+        }
+    }
+    c->rowptr.upload(rowptr.data(), N + 1, st);
+    c->cols.upload(cols.data(), c->nnzb, st);
+    c->diag_slot.upload(diag.data(), N, st);
+    c->tet_slot.upload(slot.data(), 16 * T, st);
+    c->bsr.ensure(9 * (size_t)c->nnzb);
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  // surface
+  {
+    std::vector<int> tri(3 * c->F), tri_sorted(3 * c->F), edge(2 * c->E), sv(c->V);
+    for (int64_t f = 0; f < c->F; ++f) {
+      int64_t o[3] = {s->tris[3 * f], s->tris[3 * f + 1], s->tris[3 * f + 2]};
+      for (int k = 0; k < 3; ++k) tri[3 * f + k] = o2n[o[k]];
+      std::sort(o, o + 3);
+      for (int k = 0; k < 3; ++k) tri_sorted[3 * f + k] = o2n[o[k]];
+    }
+    for (int64_t e = 0; e < 2 * c->E; ++e) edge[e] = o2n[s->edges[e]];
+    for (int64_t v = 0; v < c->V; ++v) sv[v] = o2n[s->surf_verts[v]];
+    c->tri.upload(tri.data(), 3 * c->F, st);
+    c->tri_sorted.upload(tri_sorted.data(), 3 * c->F, st);
+    c->edge.upload(edge.data(), 2 * c->E, st);
+    c->sverts.upload(sv.data(), c->V, st);
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  const size_t n3 = 3 * (size_t)N;
+  for (DBuf<double>* b : {&c->x, &c->xt, &c->vel, &c->g, &c->z, &c->p, &c->Hp, &c->p_prev, &c->Hp_prev, &c->z_prev,
+                          &c->hv, &c->x_start, &c->x_best, &c->tmp, &c->tmp2})
+    b->ensure(n3);
+  c->counters.ensure(16);
+  c->dscal.ensure(64);
+  c->solver_info.ensure(1);
+  c->alpha_d.ensure(c->D);
+  setup_levels(c);
+}
+
+// ---------------------------------------------------------------------------
+// advance_step (solver.py:296-458)
+
+struct LoopResult {
+  std::vector<mp_iter_record> recs;
+  bool converged = false;
+  uint32_t flags = 0;
+};
+
+using Clock = std::chrono::steady_clock;
+static double ms_since(Clock::time_point a) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - a).count();
+}
+
+// 2-norm condition number of a 2x2 matrix (np.linalg.cond)
+static double cond2(double a, double b, double c, double d) {
+  double E = 0.5 * (a + d), F = 0.5 * (a - d), G = 0.5 * (c + b), H = 0.5 * (c - b);
+  double Q = std::sqrt(E * E + H * H), R = std::sqrt(F * F + G * G);
+  double s1 = Q + R, s2 = std::fabs(Q - R);
+  if (s2 == 0.0) return INFINITY;
+  return s1 / s2;
+}
+
+// LAPACK gesv on 2x2 (partial pivoting, reciprocal pivot scaling)
+static void solve2(double A[2][2], double b[2], double* x0, double* x1) {
+  double a00 = A[0][0], a01 = A[0][1], a10 = A[1][0], a11 = A[1][1], b0 = b[0], b1 = b[1];
+  if (std::fabs(a10) > std::fabs(a00)) {
+    std::swap(a00, a10);
+    std::swap(a01, a11);
+    std::swap(b0, b1);
+  }
+  double l = a10 * (1.0 / a00);
+  double u11 = a11 - l * a01;
+  double y1 = b1 - l * b0;
+  *x1 = y1 / u11;
+  *x0 = (b0 - a01 * (*x1)) / a00;
+}
+
+static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
+  const mp_solver_config& cfg = c->cfg;
+  const int64_t n3 = 3 * c->N;
+  cudaStream_t st = c->stream;
+  CUDA_CHECK(cudaMemcpyAsync(c->x_start.p, c->x.p, n3 * 8, cudaMemcpyDeviceToDevice, st));
+  CUDA_CHECK(cudaMemcpyAsync(c->x_best.p, c->x.p, n3 * 8, cudaMemcpyDeviceToDevice, st));
+  const bool full_every = cfg.update_strategy == MP_UPDATE_FULLREBUILD;
+  bool restart = true;
+  bool have_prev = false;   // p_prev / Hp_prev / z_prev valid
+  double best = INFINITY;
+  R.recs.clear();
+  R.converged = false;
+  for (int64_t k = 0; k < cfg.iter_max; ++k) {
+    auto t0 = Clock::now();
+    const bool rebuild = restart || full_every;
+    constraint_set(c, c->x);
+    if (rebuild) {
+      snapshot(c, c->x, h, true);
+    } else {
+      update_build(c);
+    }
+    gradient(c, c->x, c->xt, h, c->g);
+    precond_apply(c, c->g, c->z, true);
+    sync_stream(c);
+    auto t1 = Clock::now();
+
+    hvp(c, c->z, c->hv, !rebuild);
+    DotSpec S{};
+    S.n = 0;
+    auto add = [&](const double* a, const double* b) {
+      S.a[S.n] = a;
+      S.b[S.n] = b;
+      return S.n++;
+    };
+    int i_zz = add(c->z, c->z), i_gg = add(c->g, c->g), i_zg = add(c->z, c->g), i_zv = add(c->z, c->hv);
+    int i_zHp = -1, i_pv = -1, i_pHp = -1, i_pg = -1, i_gzp = -1;
+    if (have_prev) {
+      i_zHp = add(c->z, c->Hp_prev);
+      i_pv = add(c->p_prev, c->hv);
+      i_pHp = add(c->p_prev, c->Hp_prev);
+      i_pg = add(c->p_prev, c->g);
+      i_gzp = add(c->g, c->z_prev);
+    }
+    multidot(c, n3, S);
+    double dots[MAX_DOTS];
+    std::memcpy(dots, c->h_scal, sizeof(double) * S.n);
+    const double z_norm = std::sqrt(dots[i_zz]);
+    const double grad_norm = std::sqrt(dots[i_gg]);
+    const double zg = dots[i_zg], zv = dots[i_zv];
+    if (z_norm < best) {
+      best = z_norm;
+      CUDA_CHECK(cudaMemcpyAsync(c->x_best.p, c->x.p, n3 * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    double mu = 0.0, nu = 0.0;
+    double pinf = 0.0;
+    if (z_norm == 0.0) {
+      CUDA_CHECK(cudaMemsetAsync(c->p.p, 0, n3 * 8, st));
+      CUDA_CHECK(cudaMemsetAsync(c->Hp.p, 0, n3 * 8, st));
+    } else if (restart || !have_prev) {
+      if (zv <= 0.0) throw MpError(MP_ERR_MODEL_NOT_SPD, "z.Hz <= 0 at restart");
+      mu = zg / zv;
+      nu = 0.0;
+      form_direction(c, -mu, 0.0, nullptr, nullptr);
+      pinf = c->h_scal[1];
+    } else {
+      // solve_2d_subspace (solver.py:147-161)
+      const double zHz = zv;
+      if (zHz <= 0.0) throw MpError(MP_ERR_MODEL_NOT_SPD, "z.Hz <= 0 in subspace solve");
+      double A[2][2] = {{zHz, -dots[i_zHp]}, {-dots[i_pv], dots[i_pHp]}};
+      double b[2] = {zg, -dots[i_pg]};
+      if (cond2(A[0][0], A[0][1], A[1][0], A[1][1]) > 1e12) {
+        mu = b[0] / zHz;
+        nu = 0.0;
+      } else {
+        solve2(A, b, &mu, &nu);
+      }
+      form_direction(c, -mu, nu, c->p_prev, c->Hp_prev);
+      double gp = c->h_scal[0];
+      pinf = c->h_scal[1];
+      if (gp >= 0.0 && z_norm > 0.0) {
+        if (zv <= 0.0) throw MpError(MP_ERR_MODEL_NOT_SPD, "z.Hz <= 0 in fallback");
+        mu = zg / zv;
+        nu = 0.0;
+        form_direction(c, -mu, 0.0, nullptr, nullptr);
+        pinf = c->h_scal[1];
+      }
+    }
+    auto t2 = Clock::now();
+    double min_alpha = 1.0;
+    if (pinf > 0.0) {
+      CcdResult cr = ccd_clamp(c, c->x, c->p, pinf, cfg.ccd_per_subdomain != 0, c->tmp);
+      min_alpha = cr.min_alpha;
+      std::swap(c->x.p, c->tmp.p);
+    }
+    sync_stream(c);
+    auto t3 = Clock::now();
+    mp_iter_record rec{};
+    rec.k = k;
+    rec.grad_norm = grad_norm;
+    rec.z_norm = z_norm;
+    rec.r = 0.0;
+    rec.restart = restart ? 1 : 0;
+    rec.n_contacts = (int32_t)c->cur.count;
+    rec.mu = mu;
+    rec.nu = nu;
+    rec.min_alpha = min_alpha;
+    rec.t_grad_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    rec.t_dir_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    rec.t_ccd_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
+    rec.n_candidates = (int32_t)(rebuild ? 0 : c->n_cand);
+    rec.n_ccd_pairs = (int32_t)c->n_ccd;
+    const bool converged_now = z_norm <= cfg.eps;
+    if (converged_now && (restart || full_every)) {
+      R.recs.push_back(rec);
+      R.converged = true;
+      break;
+    }
+    if (converged_now) {
+      restart = true;
+    } else {
+      double r = 0.0;
+      if (have_prev) {
+        if (zg <= 0.0) throw MpError(MP_ERR_PRECOND_NOT_SPD, "g.z <= 0 in restart ratio");
+        r = std::fabs(dots[i_gzp]) / zg;
+      }
+      rec.r = r;
+      restart = r > cfg.delta;
+    }
+    R.recs.push_back(rec);
+    std::swap(c->z_prev.p, c->z.p);
+    std::swap(c->p_prev.p, c->p.p);
+    std::swap(c->Hp_prev.p, c->Hp.p);
+    have_prev = true;
+  }
+  if (!R.converged) {
+    R.flags |= MP_FLAG_NOT_CONVERGED;
+    CUDA_CHECK(cudaMemcpyAsync(c->x.p, c->x_best.p, n3 * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  k_velocity<<<grid_for(n3, 256), 256, 0, st>>>(c->N, c->x, c->x_start, h, c->pinned, c->vel);
+  LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+static const char* status_codes[] = {"ok",
+                                     "penetration-detected",
+                                     "non-spd-subdomain",
+                                     "capacitance-not-spd",
+                                     "model-not-spd",
+                                     "precond-not-spd",
+                                     "non-spd-block",
+                                     "degenerate-primitive",
+                                     "config-error",
+                                     "capacity-overflow",
+                                     "cuda-error"};
+
+template <typename Fn>
+static int guarded(mp_ctx* c, Fn&& fn) {
+  g_launch_counter = c ? &c->launches : nullptr;
+  try {
+    if (c) CUDA_CHECK(cudaSetDevice(c->device));
+    fn();
+    return MP_OK;
+  } catch (const MpError& e) {
+    if (c) c->last_error = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what();
+    return MP_ERR_CUDA;
+  }
+}
+
+static void upload_vec_new(mp_ctx* c, const double* host, double* dev) {
+  const int64_t n3 = 3 * c->N;
+  c->tmp2.ensure(n3);
+  CUDA_CHECK(cudaMemcpyAsync(c->tmp2.p, host, n3 * 8, cudaMemcpyHostToDevice, c->stream));
+  k_to_new<<<grid_for(n3, 256), 256, 0, c->stream>>>(c->N, c->new2old, c->tmp2, dev);
+  LAUNCH_CHECK();
+}
+
+static void download_vec_old(mp_ctx* c, const double* dev, double* host) {
+  const int64_t n3 = 3 * c->N;
+  k_to_old<<<grid_for(n3, 256), 256, 0, c->stream>>>(c->N, c->new2old, dev, c->tmp2);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemcpyAsync(host, c->tmp2.p, n3 * 8, cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+}
+
+extern "C" {
+
+const char* mp_status_code(int status) {
+  if (status < 0 || status > MP_ERR_CUDA) return "sim-error";
+  return status_codes[status];
+}
+
+const char* mp_last_error(mp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+void* mp_stream(mp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int64_t mp_launch_count(mp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+static thread_local std::string g_create_error;
+const char* mp_create_error(void) { return g_create_error.c_str(); }
+
+int mp_create(const mp_scene_desc* scene, const mp_solver_config* cfg, int device, mp_ctx** out) {
+  *out = nullptr;
+  mp_ctx* c = new mp_ctx();
+  int st = guarded(c, [&] { create_ctx(scene, cfg, device, c); });
+  if (st != MP_OK) {
+    g_create_error = c->last_error;
+    delete c;
+    return st;
+  }
+  *out = c;
+  return MP_OK;
+}
+
+void mp_destroy(mp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+int mp_set_config(mp_ctx* c, const mp_solver_config* cfg) {
+  return guarded(c, [&] {
+    validate_config(*cfg);
+    if (cfg->block_size != c->cfg.block_size)
+      throw MpError(MP_ERR_CONFIG, "block_size is fixed per context (partition); create a new context");
+    c->cfg = *cfg;
+    setup_levels(c);
+    c->have_mas = false;
+  });
+}
+
+int mp_partition_host(const double* rest, int64_t n, int32_t block_size, int64_t* subdomain_of) {
+  if (n < 1 || block_size < 1) return MP_ERR_CONFIG;
+  try {
+    std::vector<int> n2o;
+    std::vector<int64_t> sub;
+    morton_partition(rest, n, block_size, n2o, sub);
+    std::memcpy(subdomain_of, sub.data(), sizeof(int64_t) * n);
+  } catch (...) {
+    return MP_ERR_CONFIG;
+  }
+  return MP_OK;
+}
+
+int mp_partition(mp_ctx* c, int64_t* D, int64_t* subdomain_of) {
+  return guarded(c, [&] {
+    *D = c->D;
+    if (subdomain_of) std::memcpy(subdomain_of, c->h_sub_of_old.data(), sizeof(int64_t) * c->N);
+  });
+}
+
+static void fill_records(const LoopResult& R, mp_iter_record* recs, int64_t cap, int64_t* n_recs,
+                         int32_t* converged, uint32_t* flags) {
+  int64_t n = (int64_t)R.recs.size();
+  if (recs) std::memcpy(recs, R.recs.data(), sizeof(mp_iter_record) * std::min(n, cap));
+  if (n_recs) *n_recs = n;
+  if (converged) *converged = R.converged ? 1 : 0;
+  if (flags) *flags = R.flags;
+}
+
+int mp_advance(mp_ctx* c, const double* x, const double* v, const double* x_tilde, double h, double* x_out,
+               double* v_out, mp_iter_record* recs, int64_t cap, int64_t* n_recs, int32_t* converged,
+               uint32_t* flags) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    upload_vec_new(c, x_tilde, c->xt);
+    LoopResult R;
+    advance_loop(c, h, R);
+    download_vec_old(c, c->x, x_out);
+    download_vec_old(c, c->vel, v_out);
+    fill_records(R, recs, cap, n_recs, converged, flags);
+  });
+}
+
+int mp_step(mp_ctx* c, const double* x, const double* v, double h, double* x_out, double* v_out,
+            mp_iter_record* recs, int64_t cap, int64_t* n_recs, int32_t* converged, uint32_t* flags) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    upload_vec_new(c, v, c->vel);
+    k_prepare<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, c->x, c->vel, c->mass, c->f_ext, c->pinned, h,
+                                                              c->xt);
+    LAUNCH_CHECK();
+    LoopResult R;
+    advance_loop(c, h, R);
+    download_vec_old(c, c->x, x_out);
+    download_vec_old(c, c->vel, v_out);
+    fill_records(R, recs, cap, n_recs, converged, flags);
+  });
+}
+
+// device-resident variant: x, v stay on the device between calls (bench)
+int mp_step_device(mp_ctx* c, double h, mp_iter_record* recs, int64_t cap, int64_t* n_recs, int32_t* converged,
+                   uint32_t* flags) {
+  return guarded(c, [&] {
+    k_prepare<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, c->x, c->vel, c->mass, c->f_ext, c->pinned, h,
+                                                              c->xt);
+    LAUNCH_CHECK();
+    LoopResult R;
+    advance_loop(c, h, R);
+    fill_records(R, recs, cap, n_recs, converged, flags);
+  });
+}
+
+int mp_set_state(mp_ctx* c, const double* x, const double* v) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    upload_vec_new(c, v, c->vel);
+    sync_stream(c);
+  });
+}
+
+int mp_get_state(mp_ctx* c, double* x, double* v) {
+  return guarded(c, [&] {
+    if (x) download_vec_old(c, c->x, x);
+    if (v) download_vec_old(c, c->vel, v);
+  });
+}
+
+int mp_broad_phase(mp_ctx* c, const double* x, double motion_bound, double d_hat, int64_t* pt, int64_t pt_cap,
+                   int64_t* n_pt, int64_t* ee, int64_t ee_cap, int64_t* n_ee) {
+  return guarded(c, [&] {
+    *n_pt = 0;
+    *n_ee = 0;
+    if (c->F == 0) return;
+    upload_vec_new(c, x, c->x);
+    const double gap = d_hat + 2.0 * motion_bound;
+    GridBuild B = build_grid(c, c->x, gap);
+    // PT and EE separately so their raw lists stay apart
+    for (int pass = 0; pass < 2; ++pass) {
+      size_t cap = std::max<size_t>(c->cand_a.n, 4096);
+      for (int attempt = 0; attempt < 4; ++attempt) {
+        c->cand_a.ensure(cap);
+        c->cand_b.ensure(cap);
+        BpOut O{};
+        O.a = c->cand_a;
+        O.b = c->cand_b;
+        O.cap = (int64_t)c->cand_a.n;
+        O.counter = c->counters.p;
+        CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(int), c->stream));
+        ContactParams CP{};
+        CcdParams CC{};
+        if (pass == 0 && c->V && B.n_tri_keys) {
+          k_query_pt<BP_RAW><<<grid_for(c->V, 128), 128, 0, c->stream>>>(c->V, c->sverts, c->tri, c->tri_sorted,
+                                                                          c->x, B.G, B.tri_keys, B.tri_prim,
+                                                                          B.n_tri_keys, c->box_lo, c->box_hi, O, CP,
+                                                                          CC);
+          LAUNCH_CHECK();
+        }
+        if (pass == 1 && c->E && B.n_edge_keys) {
+          k_query_ee<BP_RAW><<<grid_for(c->E, 128), 128, 0, c->stream>>>(c->E, c->F, c->edge, c->x, B.G,
+                                                                          B.edge_keys, B.edge_prim, B.n_edge_keys,
+                                                                          c->box_lo, c->box_hi, O, CP, CC);
+          LAUNCH_CHECK();
+        }
+        int n = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&n, c->counters.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        sync_stream(c);
+        if ((size_t)n > c->cand_a.n) {
+          cap = (size_t)n + 1024;
+          continue;
+        }
+        std::vector<int> a(n), b(n);
+        CUDA_CHECK(cudaMemcpyAsync(a.data(), c->cand_a.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_CHECK(cudaMemcpyAsync(b.data(), c->cand_b.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        sync_stream(c);
+        std::vector<std::pair<int64_t, int64_t>> rows(n);
+        for (int i = 0; i < n; ++i) {
+          if (pass == 0) rows[i] = {c->h_new2old[a[i]], b[i]};
+          else rows[i] = {a[i], b[i]};
+        }
+        std::sort(rows.begin(), rows.end());
+        if (pass == 0) {
+          *n_pt = n;
+          if (pt)
+            for (int i = 0; i < n && i < pt_cap; ++i) {
+              pt[2 * i] = rows[i].first;
+              pt[2 * i + 1] = rows[i].second;
+            }
+        } else {
+          *n_ee = n;
+          if (ee)
+            for (int i = 0; i < n && i < ee_cap; ++i) {
+              ee[2 * i] = rows[i].first;
+              ee[2 * i + 1] = rows[i].second;
+            }
+        }
+        break;
+      }
+    }
+  });
+}
+
+static void download_table(mp_ctx* c, PairTable& t, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt,
+                           double* d, double* grad, double* k) {
+  const int64_t m = t.count;
+  *n = m;
+  if (m == 0 || cap < m) return;
+  std::vector<int4> v(m);
+  std::vector<int> ip(m);
+  CUDA_CHECK(cudaMemcpyAsync(v.data(), t.verts.p, m * sizeof(int4), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaMemcpyAsync(ip.data(), t.is_pt.p, m * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (d) CUDA_CHECK(cudaMemcpyAsync(d, t.d.p, m * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (grad) CUDA_CHECK(cudaMemcpyAsync(grad, t.grad.p, m * 96, cudaMemcpyDeviceToHost, c->stream));
+  if (k) CUDA_CHECK(cudaMemcpyAsync(k, t.k.p, m * 8, cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  for (int64_t i = 0; i < m; ++i) {
+    const int id[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    if (verts)
+      for (int a = 0; a < 4; ++a) verts[4 * i + a] = c->h_new2old[id[a]];
+    if (is_pt) is_pt[i] = (uint8_t)ip[i];
+  }
+}
+
+int mp_constraint_set(mp_ctx* c, const double* x, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt,
+                      double* d, double* grad, double* k) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    constraint_set(c, c->x);
+    download_table(c, c->cur, cap, n, verts, is_pt, d, grad, k);
+  });
+}
+
+int mp_gradient(mp_ctx* c, const double* x, const double* x_tilde, double h, double* g) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    upload_vec_new(c, x_tilde, c->xt);
+    constraint_set(c, c->x);
+    gradient(c, c->x, c->xt, h, c->g);
+    download_vec_old(c, c->g, g);
+  });
+}
+
+int mp_energy(mp_ctx* c, const double* x, const double* x_tilde, double h, double* e) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    upload_vec_new(c, x_tilde, c->xt);
+    constraint_set(c, c->x);
+    *e = energy(c, c->x, c->xt, h);
+  });
+}
+
+int mp_snapshot(mp_ctx* c, const double* x, double h, int build_mas) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    constraint_set(c, c->x);
+    snapshot(c, c->x, h, build_mas != 0);
+    sync_stream(c);
+  });
+}
+
+int mp_hvp(mp_ctx* c, const double* vec, int with_updates, double* out) {
+  return guarded(c, [&] {
+    if (!c->have_snapshot) throw MpError(MP_ERR_CONFIG, "no snapshot: call mp_snapshot first");
+    upload_vec_new(c, vec, c->tmp);
+    hvp(c, c->tmp, c->hv, with_updates != 0);
+    download_vec_old(c, c->hv, out);
+  });
+}
+
+int mp_precond_apply(mp_ctx* c, const double* g, int with_updates, double* z) {
+  return guarded(c, [&] {
+    if (!c->have_mas) throw MpError(MP_ERR_CONFIG, "no MAS hierarchy: call mp_snapshot(build_mas=1) first");
+    upload_vec_new(c, g, c->g);
+    precond_apply(c, c->g, c->z, with_updates != 0);
+    download_vec_old(c, c->z, z);
+  });
+}
+
+int mp_update_at(mp_ctx* c, const double* x, int64_t* n_candidates, int64_t* n_touched) {
+  return guarded(c, [&] {
+    if (!c->have_snapshot) throw MpError(MP_ERR_CONFIG, "no snapshot: call mp_snapshot first");
+    upload_vec_new(c, x, c->tmp);
+    constraint_set(c, c->tmp);
+    update_build(c);
+    sync_stream(c);
+    if (n_candidates) *n_candidates = c->n_cand;
+    if (n_touched) *n_touched = c->n_touched;
+  });
+}
+
+int mp_ccd(mp_ctx* c, const double* x, const double* p, double* alpha_d, double* x_new, double* min_alpha,
+           int32_t* certified, int64_t* n_pairs) {
+  return guarded(c, [&] {
+    upload_vec_new(c, x, c->x);
+    upload_vec_new(c, p, c->p);
+    // max |p| over all components (ccd.py:225), from the caller's array
+    const int64_t n3 = 3 * c->N;
+    double pinf = 0.0;
+    for (int64_t i = 0; i < n3; ++i) pinf = std::max(pinf, std::fabs(p[i]));
+    CcdResult R = ccd_clamp(c, c->x, c->p, pinf, c->cfg.ccd_per_subdomain != 0, c->tmp);
+    if (alpha_d)
+      CUDA_CHECK(cudaMemcpyAsync(alpha_d, c->alpha_d.p, c->D * 8, cudaMemcpyDeviceToHost, c->stream));
+    download_vec_old(c, c->tmp, x_new);
+    *min_alpha = R.min_alpha;
+    *certified = R.certified ? 1 : 0;
+    *n_pairs = R.n_pairs;
+  });
+}
+
+int mp_ccd_pairs(mp_ctx* c, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt, double* alpha) {
+  return guarded(c, [&] {
+    const int64_t m = c->n_ccd;
+    *n = m;
+    if (m == 0 || cap < m) return;
+    std::vector<int4> v(m);
+    std::vector<int> ip(m);
+    CUDA_CHECK(cudaMemcpyAsync(v.data(), c->ccd_verts.p, m * sizeof(int4), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(ip.data(), c->ccd_ispt.p, m * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (alpha) CUDA_CHECK(cudaMemcpyAsync(alpha, c->ccd_alpha.p, m * 8, cudaMemcpyDeviceToHost, c->stream));
+    sync_stream(c);
+    for (int64_t i = 0; i < m; ++i) {
+      const int id[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+      if (verts)
+        for (int a = 0; a < 4; ++a) verts[4 * i + a] = c->h_new2old[id[a]];
+      if (is_pt) is_pt[i] = (uint8_t)ip[i];
+    }
+  });
+}
+
+}  // extern "C"

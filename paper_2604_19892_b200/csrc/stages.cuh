@@ -1,0 +1,258 @@
+// stages.cuh -- host drivers of the device stages: gradient, energy,
+// snapshot (H_base + MAS build), update (classify / Top-K / Woodbury),
+// preconditioner apply and HVP.
+#pragma once
+
+#include "ccd.cuh"
+#include "elastic.cuh"
+#include "mas.cuh"
+#include "ops.cuh"
+
+#define WOODBURY_KMAX 48
+
+// energy.gradient (energy.py:357-370) with the current constraint set
+static void gradient(mp_ctx* c, const double* x, const double* xt, double h, double* g) {
+  elastic_gradient(c, x, xt, h, g);
+  if (c->cur.count) {
+    k_contact_grad<<<grid_for(c->cur.count, 128), 128, 0, c->stream>>>(c->cur.count, c->cur.verts, c->cur.d,
+                                                                      c->cur.grad, c->pinned, c->d_hat, c->kappa, g);
+    LAUNCH_CHECK();
+  }
+}
+
+// energy.incremental_potential (energy.py:346-354)
+static double energy(mp_ctx* c, const double* x, const double* xt, double h) {
+  const int nb = 64;
+  c->red_part.ensure(3 * nb);
+  CUDA_CHECK(cudaMemsetAsync(c->red_part.p, 0, sizeof(double) * 3 * nb, c->stream));
+  k_inertia_energy<<<nb, 256, 0, c->stream>>>(c->N, x, xt, c->mass, c->red_part.p);
+  LAUNCH_CHECK();
+  if (c->T) {
+    k_tet_energy<<<nb, 256, 0, c->stream>>>(c->T, c->tets, c->tetp, c->kind, x, c->red_part.p + nb);
+    LAUNCH_CHECK();
+  }
+  if (c->cur.count) {
+    k_contact_energy<<<nb, 256, 0, c->stream>>>(c->cur.count, c->cur.d, c->d_hat, c->kappa, c->red_part.p + 2 * nb);
+    LAUNCH_CHECK();
+  }
+  std::vector<double> part(3 * nb);
+  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * 3 * nb, cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < 3; ++q)
+    for (int b = 0; b < nb; ++b) s[q] += part[q * nb + b];
+  return 0.5 * s[0] + h * h * s[1] + s[2];
+}
+
+static void copy_table(mp_ctx* c, PairTable& s, PairTable& d) {
+  int64_t n = s.count;
+  d.ensure(n > 0 ? n : 1);
+  d.count = n;
+  if (!n) return;
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  };
+  cp(d.khi.p, s.khi.p, n * 8);
+  cp(d.klo.p, s.klo.p, n * 8);
+  cp(d.verts.p, s.verts.p, n * sizeof(int4));
+  cp(d.d.p, s.d.p, n * 8);
+  cp(d.k.p, s.k.p, n * 8);
+  cp(d.nrm.p, s.nrm.p, n * 8);
+  cp(d.grad.p, s.grad.p, n * 96);
+  cp(d.is_pt.p, s.is_pt.p, n * 4);
+}
+
+static int read_status(mp_ctx* c, int* dev) {
+  int h = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&h, dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  return h;
+}
+
+// build_hierarchy (mas.py:138-179) from the BSR + base contacts
+static void mas_build(mp_ctx* c) {
+  const int m = c->m;
+  const int64_t D = c->D;
+  c->Mfull.zero((size_t)D * m * m, c->stream);
+  c->Bblk.ensure((size_t)D * cyc_size(m));
+  c->Mblk.ensure((size_t)D * cyc_size(m));
+  if (c->base.count) {
+    k_contact_blocks<<<grid_for(c->base.count, 128), 128, 0, c->stream>>>(c->base.count, c->base.verts,
+                                                                         c->base.grad, c->base.k, c->bs, m, c->Mfull);
+    LAUNCH_CHECK();
+  }
+  k_bsr_to_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, c->bs, m, c->Mfull);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, sizeof(int), c->stream));
+  const size_t smem = sizeof(double) * 2 * m * m;
+  k_mas_factor<<<(unsigned)D, 256, smem, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
+                                                       c->counters.p + 3);
+  LAUNCH_CHECK();
+  if (read_status(c, c->counters.p + 3)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
+  for (int l = 0; l < c->n_levels; ++l) {
+    CoarseLevel& L = *c->levels[l];
+    L.dense.zero((size_t)L.n * L.n, c->stream);
+    k_bsr_to_coarse<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, L.span, L.n,
+                                                                L.dense);
+    LAUNCH_CHECK();
+    if (c->base.count) {
+      k_contact_coarse<<<grid_for(c->base.count, 128), 128, 0, c->stream>>>(
+          c->base.count, c->base.verts, c->base.grad, c->base.k, c->N, L.span, L.n, L.dense);
+      LAUNCH_CHECK();
+    }
+    k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, c->stream>>>(L.n, L.dense);
+    LAUNCH_CHECK();
+    int lwork = 0;
+    if (cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, "cusolver potrf buffer");
+    int lwork2 = 0;
+    if (cusolverDnDpotri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, &lwork2) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, "cusolver potri buffer");
+    c->solver_work.ensure((size_t)std::max(lwork, lwork2) + 1);
+    if (cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, c->solver_work, lwork,
+                         c->solver_info) != CUSOLVER_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, "cusolver potrf");
+    ++c->launches;
+    if (read_status(c, c->solver_info)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
+    if (cusolverDnDpotri(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, c->solver_work, lwork2,
+                         c->solver_info) != CUSOLVER_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, "cusolver potri");
+    ++c->launches;
+    L.inv.ensure((size_t)cyc_size(L.n));
+    k_pack_coarse<<<grid_for(cyc_size(L.n), 256), 256, 0, c->stream>>>(L.n, L.dense, L.inv);
+    LAUNCH_CHECK();
+  }
+  c->have_mas = true;
+}
+
+// rebuild branch of advance_step (solver.py:323-335): base := cur at x,
+// H_base = assemble_base_hessian, MAS hierarchy
+static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
+  copy_table(c, c->cur, c->base);
+  assemble_elastic_bsr(c, x, h);
+  c->have_snapshot = true;
+  c->have_mas = false;
+  c->have_updates = false;
+  c->n_cand = 0;
+  c->n_touched = 0;
+  if (build_mas) mas_build(c);
+}
+
+// non-rebuild branch (solver.py:337-346): classify_all, select_top_k,
+// build_update, against the snapshot; cur must hold the constraint set at x
+static void update_build(mp_ctx* c) {
+  classify_all(c, c->cfg.eps_rot);
+  c->have_updates = false;
+  c->n_touched = 0;
+  if (c->cfg.update_strategy == MP_UPDATE_FREEZE || c->n_cand == 0 || !c->have_mas) return;
+  const int64_t nc = c->n_cand;
+  c->ent_count.ensure(nc + 1);
+  c->ent_off.ensure(nc + 1);
+  k_topk_count<<<grid_for(nc, 128), 128, 0, c->stream>>>(nc, c->cand_verts, c->cand_u, c->bs, c->ent_count);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemsetAsync(c->ent_count.p + nc, 0, sizeof(int), c->stream));
+  exclusive_scan(c, c->ent_count, c->ent_off, nc + 1);
+  int ne = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&ne, c->ent_off.p + nc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  if (ne == 0) return;
+  c->ent_sub.ensure(ne); c->ent_cand.ensure(ne); c->ent_key.ensure(ne);
+  c->ent_sub2.ensure(ne); c->ent_cand2.ensure(ne); c->ent_key2.ensure(ne);
+  c->sort_idx.ensure(ne); c->sort_idx2.ensure(ne); c->sort_k1.ensure(ne); c->sort_k2.ensure(ne);
+  k_topk_fill<<<grid_for(nc, 128), 128, 0, c->stream>>>(nc, c->cand_verts, c->cand_u, c->cand_ds, c->bs, c->ent_off,
+                                                        c->ent_sub, c->ent_cand, c->ent_key);
+  LAUNCH_CHECK();
+  // stable LSD: by descending delta_s, then by subdomain
+  k_iota<<<grid_for(ne, 256), 256, 0, c->stream>>>(c->sort_idx, ne);
+  LAUNCH_CHECK();
+  sort_pairs_u64(c, c->ent_key, c->ent_key2, c->sort_idx, c->sort_idx2, ne, 64);
+  // subdomain key of the permuted entries
+  k_gather_sub_key<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->ent_sub, c->sort_idx2, c->sort_k1);
+  LAUNCH_CHECK();
+  sort_pairs_u64(c, c->sort_k1, c->sort_k2, c->sort_idx2, c->sort_idx, ne, bits_for((unsigned long long)c->D));
+  k_gather_entries<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->sort_idx, c->ent_sub, c->ent_cand, c->ent_sub2,
+                                                             c->ent_cand2);
+  LAUNCH_CHECK();
+  // runs -> touched subdomains
+  c->ent_count.ensure(ne + 1);
+  c->ent_off.ensure(ne + 1);
+  k_topk_runs<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->ent_sub2, c->ent_count);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemsetAsync(c->ent_count.p + ne, 0, sizeof(int), c->stream));
+  exclusive_scan(c, c->ent_count, c->ent_off, ne + 1);
+  int nt = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&nt, c->ent_off.p + ne, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  c->touched_sub.ensure(nt); c->touched_start.ensure(nt); c->touched_len.ensure(nt);
+  c->overlay_of.ensure(c->D);
+  CUDA_CHECK(cudaMemsetAsync(c->overlay_of.p, 0xff, sizeof(int) * c->D, c->stream));  // -1
+  k_topk_touched<<<grid_for(ne, 256), 256, 0, c->stream>>>(ne, c->ent_sub2, c->ent_count, c->ent_off, c->cfg.K,
+                                                           c->touched_sub, c->touched_start, c->touched_len,
+                                                           c->overlay_of);
+  LAUNCH_CHECK();
+  c->n_touched = nt;
+  const int m = c->m;
+  c->overlay.ensure((size_t)nt * cyc_size(m));
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 4, 0, sizeof(int), c->stream));
+  const int kw = c->cfg.K < WOODBURY_KMAX ? c->cfg.K : WOODBURY_KMAX;
+  const size_t smem_w = sizeof(double) * ((size_t)m * m + 2 * (size_t)m * kw + (size_t)kw * kw);
+  k_woodbury<<<nt, 256, smem_w, c->stream>>>(c->N, c->bs, m, kw, c->Bblk, c->touched_sub, c->touched_start,
+                                             c->touched_len, c->ent_cand2, c->cand_verts, c->cand_u, c->overlay,
+                                             c->counters.p + 4);
+  LAUNCH_CHECK();
+  if (c->cfg.K > WOODBURY_KMAX) {
+    const size_t smem_d = sizeof(double) * 2 * (size_t)m * m;
+    k_direct_update<<<nt, 256, smem_d, c->stream>>>(c->N, c->bs, m, c->Mblk, c->touched_sub, c->touched_start,
+                                                    c->touched_len, c->ent_cand2, c->cand_verts, c->cand_u,
+                                                    WOODBURY_KMAX, c->overlay, c->counters.p + 4);
+    LAUNCH_CHECK();
+  }
+  if (read_status(c, c->counters.p + 4)) throw MpError(MP_ERR_CAPACITANCE, "capacitance not SPD");
+  c->have_updates = nt > 0;
+}
+
+// mas.apply_preconditioner + z[pinned] = 0
+static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updates) {
+  LevelViews LV{};
+  LV.L = c->n_levels;
+  for (int l = 0; l < c->n_levels; ++l) {
+    CoarseLevel& L = *c->levels[l];
+    if (l == 0) {
+      k_restrict1<<<L.A, 128, 0, c->stream>>>(c->N, L.span, g, L.rsum);
+    } else {
+      CoarseLevel& F = *c->levels[l - 1];
+      k_restrict_up<<<grid_for(3 * (int64_t)L.A, 128), 128, 0, c->stream>>>(L.A, c->cfg.coarse_block, F.A, F.rsum,
+                                                                             L.rsum);
+    }
+    LAUNCH_CHECK();
+    dim3 grid(grid_for(L.n, 128), L.chunks);
+    k_coarse_mv<<<grid, 128, 0, c->stream>>>(L.n, c->N, L.span, L.chunks, L.inv, L.rsum, L.ypart);
+    LAUNCH_CHECK();
+    LV.lv[l] = LevelView{L.ypart, L.n, L.span, L.chunks};
+  }
+  const int m = c->m;
+  const int threads = ((m + 31) / 32) * 32;
+  const size_t smem = sizeof(double) * (cyc_size(m) + m);
+  const bool ov = with_updates && c->have_updates;
+  k_mas_apply_l0<<<(unsigned)c->D, threads, smem, c->stream>>>(c->D, c->N, c->bs, m, c->Bblk,
+                                                               ov ? c->overlay_of.p : nullptr, c->overlay, g,
+                                                               c->pinned, LV, z);
+  LAUNCH_CHECK();
+}
+
+// HessianModel.hvp (energy.py:435-440): H_base v + sum u (u^T v)
+static void hvp(mp_ctx* c, const double* vec, double* out, bool with_cands) {
+  bsr_spmv(c, vec, out);
+  if (c->base.count) {
+    k_rank1_apply<<<grid_for(c->base.count, 128), 128, 0, c->stream>>>(c->base.count, c->base.verts, c->base.grad,
+                                                                       c->base.k, vec, out);
+    LAUNCH_CHECK();
+  }
+  if (with_cands && c->n_cand) {
+    k_rank1_apply<<<grid_for(c->n_cand, 128), 128, 0, c->stream>>>(c->n_cand, c->cand_verts, c->cand_u, nullptr,
+                                                                   vec, out);
+    LAUNCH_CHECK();
+  }
+}

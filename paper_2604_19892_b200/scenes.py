@@ -1,0 +1,143 @@
+"""Synthetic scene generators for parity tests and the benchmark.
+
+Every builder takes an optional ``mods=(geometry, energy, solver)`` triple so
+the same scene can be built with this package or -- in the golden-fixture
+script only -- with the reference package, which has the same names
+(`pkg/tests/test_acceptance.py:37-78` for the object-list convention).
+
+Configs (BASELINE.json ``configs``):
+
+* ``c1_cube``  -- floor slab + soft SNH cube ``cells^3`` (8^3: 737 V, 3,078 T)
+* ``c2_stack`` -- floor + 8 cubes (17^3 cells each) stacked 2x2x2 with 1e-3 gaps
+  (46,664 V, 235,830 T), SNH E=1e5, d_hat=2e-3, kappa=1e4, h=0.01
+* small reference-shaped scenes used by the golden fixtures: ``drop``
+  (scenes/drop.ini), ``stacked_boxes`` (test_acceptance.py:369-388),
+  ``locking`` (test_acceptance.py:488-499).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _mods(mods):
+    if mods is None:
+        from . import energy, geometry, solver
+
+        return geometry, energy, solver
+    return mods
+
+
+def build_scene(objs, d_hat, kappa, gravity=(0.0, 0.0, -9.81), mods=None):
+    """Concatenate object meshes into one Scene.
+
+    objs: dicts with mesh, translate, material ('arap'|'snh'), young, poisson,
+    density, pinned (whole object)."""
+    geo, en, sol = _mods(mods)
+    verts, tets, pin, kinds, mus, lams, rhos = [], [], [], [], [], [], []
+    off = 0
+    for ob in objs:
+        m = ob["mesh"]
+        verts.append(m.rest_positions + np.asarray(ob.get("translate", (0.0, 0.0, 0.0))))
+        tets.append(m.tets + off)
+        pin.append(np.full(len(m.rest_positions), bool(ob.get("pinned", False))))
+        T = len(m.tets)
+        mu, lam = en.lame_parameters(ob.get("young", 1e5), ob.get("poisson", 0.3))
+        kinds.append(np.full(T, 1 if ob.get("material", "arap") == "arap" else 2, dtype=np.int8))
+        mus.append(np.full(T, mu))
+        lams.append(np.full(T, lam))
+        rhos.append(np.full(T, ob.get("density", 1000.0)))
+        off += len(m.rest_positions)
+    mesh = geo.TetMesh(rest_positions=np.vstack(verts), tets=np.vstack(tets), dirichlet=np.concatenate(pin))
+    elastic = en.ElasticModel.from_arrays(mesh, np.concatenate(kinds), np.concatenate(mus), np.concatenate(lams))
+    mass = en.lumped_masses(mesh, np.concatenate(rhos))
+    return sol.Scene(
+        mesh=mesh, surface=geo.SurfaceMesh.from_tet_mesh(mesh), elastic=elastic, mass=mass,
+        dirichlet=mesh.dirichlet, d_hat=d_hat, kappa=kappa,
+        f_ext=(mass[:, None] * np.asarray(gravity)).ravel(),
+    )
+
+
+def floor(size=(1.0, 1.0, 0.1), mods=None):
+    geo, _, _ = _mods(mods)
+    return {
+        "mesh": geo.make_box_mesh(1, 1, 1, size),
+        "translate": (-size[0] / 2, -size[1] / 2, -size[2]),
+        "material": "arap", "young": 1e6, "pinned": True,
+    }
+
+
+def drop(mods=None):
+    """scenes/drop.ini: one SNH tet over a pinned slab."""
+    geo, _, _ = _mods(mods)
+    objs = [floor((1.0, 1.0, 0.1), mods),
+            {"mesh": geo.make_single_tet(0.2), "translate": (-0.05, -0.05, 0.05), "material": "snh",
+             "young": 5e4, "poisson": 0.3, "density": 1000.0}]
+    return build_scene(objs, d_hat=2e-3, kappa=1e4, mods=mods)
+
+
+def stacked_boxes(mods=None):
+    """test_acceptance.py:369-388 (three stiff 2x2x2 boxes pressing in)."""
+    geo, _, _ = _mods(mods)
+    box = geo.make_box_mesh(2, 2, 2, (0.3, 0.3, 0.3))
+    objs = [floor((1.2, 1.2, 0.1), mods)]
+    z = 0.0036
+    for i, gap in enumerate((0.0036, 0.0036, 0.0040)):
+        if i:
+            z += 0.3 + gap
+        objs.append({"mesh": box, "translate": (-0.15, -0.15, z), "material": "arap", "young": 1e7,
+                     "density": 1000.0})
+    return build_scene(objs, d_hat=4e-3, kappa=2e4, mods=mods)
+
+
+def stacked_boxes_v0(scene):
+    v0 = np.zeros((scene.mesh.n_vertices, 3))
+    v0[8:, 2] = -0.05
+    return v0.ravel()
+
+
+def locking(mods=None):
+    """test_acceptance.py:488-499."""
+    geo, _, _ = _mods(mods)
+    box = geo.make_box_mesh(1, 1, 1, (0.2, 0.2, 0.2))
+    objs = [floor((1.2, 1.2, 0.1), mods),
+            {"mesh": box, "translate": (-0.35, -0.35, 0.001), "material": "arap", "young": 2e5},
+            {"mesh": box, "translate": (0.15, 0.15, 0.15), "material": "arap", "young": 2e5}]
+    return build_scene(objs, d_hat=3e-3, kappa=1e4, mods=mods)
+
+
+def c1_cube(cells=8, young=5e4, material="snh", gap=0.01, mods=None):
+    """Config 1: pinned floor + soft cube of cells^3 (0.2 m), SURVEY 8(d) C1."""
+    geo, _, _ = _mods(mods)
+    cube = geo.make_box_mesh(cells, cells, cells, (0.2, 0.2, 0.2))
+    objs = [floor((1.0, 1.0, 0.1), mods),
+            {"mesh": cube, "translate": (-0.1, -0.1, gap), "material": material, "young": young,
+             "poisson": 0.3, "density": 1000.0}]
+    return build_scene(objs, d_hat=2e-3, kappa=1e4, mods=mods)
+
+
+def c2_stack(cells=17, young=1e5, gap=1e-3, mods=None):
+    """Config 2: 8 soft SNH cubes (cells^3, 0.2 m) stacked 2x2x2 above a pinned
+    1.2 x 1.2 x 0.1 floor, 1e-3 gaps (46,664 V / 235,830 T at cells=17)."""
+    geo, _, _ = _mods(mods)
+    cube = geo.make_box_mesh(cells, cells, cells, (0.2, 0.2, 0.2))
+    objs = [floor((1.2, 1.2, 0.1), mods)]
+    for iz in range(2):
+        for iy in range(2):
+            for ix in range(2):
+                objs.append({
+                    "mesh": cube,
+                    "translate": (-0.2 - 0.5 * gap + ix * (0.2 + gap), -0.2 - 0.5 * gap + iy * (0.2 + gap),
+                                  gap + iz * (0.2 + gap)),
+                    "material": "snh", "young": young, "poisson": 0.3, "density": 1000.0,
+                })
+    return build_scene(objs, d_hat=2e-3, kappa=1e4, mods=mods)
+
+
+SCENES = {
+    "drop": drop,
+    "stacked_boxes": stacked_boxes,
+    "locking": locking,
+    "c1_cube": c1_cube,
+    "c2_stack": c2_stack,
+}
