@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MAS-PNCG solver inner loop (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A *step* is one simulated frame: ``solver.step`` = prepare_step +
+advance_step (Alg. 1, `pkg/src/ipcsim/solver.py:296-464`) of the config-2
+scene (8 soft SNH cubes stacked on a pinned floor, 46,664 V / 235,830 T,
+BASELINE.json ``configs[1]``), every PNCG iteration on the device.
+
+Metric: PNCG iterations per second (whole job), with sec/frame alongside.
+Iterations/s is measured directly on a bounded sample by both arms; the
+per-frame iteration counts of the two arms agree within +-5% (the parity
+tests), so the ratio of the two is the solver speed-up.
+
+* ``value``  -- device-resident frames (state resident in HBM, CUDA events on
+  the context stream around each frame, L2 flushed between frames).
+* ``e2e``    -- the same frames through the public API
+  ``solver.step(scene, x, v, h, cfg)`` with host (pinned) numpy buffers: the
+  H2D of x, v and the D2H of x, v are inside the timed region.
+* ``roofline`` -- the MAS apply stage (north-star roofline kernel #1),
+  algorithmic bytes per launch / CUDA-event launch time measured inside the
+  timed frames; ``roofline_gradient`` the same for the gradient stage.
+* ``cpu_baseline`` -- the numpy oracle (oracle/, a CPU restatement of the
+  reference's algorithm) on a bounded sample of the same workload, rank 0.
+
+N > 1 (torchrun): every rank simulates its own replica of the scene on its
+own GPU ("replicas only": config 2 is a single-GPU scene per the north
+star); ``value`` = all ranks' iterations / max-over-ranks time.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port; the Python reference itself cannot travel to the GPU box) on
+the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SCENE_DESC = ("c2_stack: 8 SNH cubes (17^3 cells, 0.2 m, E=1e5) stacked 2x2x2 with 1e-3 gaps on a pinned "
+              "1.2x1.2x0.1 floor; 46,664 V / 235,830 T / 27,756 surface tris; h=0.01, d_hat=2e-3, kappa=1e4; "
+              "SolverConfig defaults (K=8, levels=2, coarse_block=4, block 32)")
+H = 0.01
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(sample_iters=None, budget_s=20.0):
+    """The oracle (numpy CPU restatement of the reference, oracle/) on a
+    bounded sample of the workload: PNCG iterations of frame 1 from rest,
+    single process.  Returns the cpu_baseline object."""
+    from oracle import solver as osolver
+
+    from paper_2604_19892_b200 import scenes
+
+    scene = scenes.c2_stack(mods=osolver.MODS)
+    cfg = osolver.SolverConfig()
+    x = scene.mesh.rest_positions.ravel().copy()
+    v = np.zeros_like(x)
+    iters, elapsed = osolver.timed_iterations(scene, x, v, H, cfg, budget_s=budget_s, max_iters=sample_iters)
+    return {
+        "value": iters / elapsed, "unit": "iters/s", "cores": 1, "kind": "port",
+        "sample": f"{iters} PNCG iterations of frame 1 of the same scene (from rest) by the numpy oracle, "
+                  f"{elapsed:.1f} s, single process, OMP/BLAS threads=1",
+    }
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    per = []
+    total_it = 0
+    total_s = 0.0
+    budget = max(5.0, 60.0 / max(1, args.steps))
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline(budget_s=budget if s >= args.warmup else 3.0)
+        it = int(cb["sample"].split()[0])
+        if s >= args.warmup:
+            per.append(cb["value"])
+            total_it += it
+            total_s += it / cb["value"]
+    value = total_it / total_s
+    line = {
+        "impl": "reference", "metric": "PNCG iters/sec", "value": value, "unit": "iters/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": SCENE_DESC, "sample": "each step = PNCG iterations of frame 1 for a bounded "
+                                                     f"~{budget:.0f} s budget"},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "port",
+                         "sample": f"{total_it} PNCG iterations over {args.steps} steps"},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_19892_b200 import scenes, solver
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def allmax(v):
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(v):
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    scene = scenes.c2_stack()
+    cfg = solver.SolverConfig()
+    if args.iter_max:
+        cfg.iter_max = args.iter_max
+    ctx = scene.context(cfg, device=local)
+    x0 = scene.mesh.rest_positions.ravel().copy()
+    ctx.set_state(x0, np.zeros_like(x0))
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    for _ in range(args.warmup):
+        ctx.step_device(H)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident frames ----
+    sampler = ClockSampler()
+    if rank == 0:
+        sampler.start()
+    ctx.stage_timing(True)
+    launches0 = ctx.launches
+    total_ms = 0.0
+    iters = 0
+    frames = []
+    for _ in range(args.steps):
+        flush.fill_(1)  # evict L2 between frames (outside the timed interval)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        recs, conv, _ = ctx.step_device(H)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        total_ms += ms
+        iters += len(recs)
+        frames.append({"iters": len(recs), "ms": round(ms, 3), "converged": conv,
+                       "restarts": int(sum(r.restart for r in recs))})
+    launches = ctx.launches - launches0
+    stats = ctx.stage_stats()
+    ctx.stage_timing(False)
+    clocks = sampler.stop() if rank == 0 else None
+    t_max = allmax(total_ms)
+    all_iters = allsum(float(iters))
+
+    # ---- e2e: the public API with host buffers ----
+    x_h, v_h = ctx.get_state()
+    xp = torch.empty(x_h.size, dtype=torch.float64).pin_memory().numpy()
+    vp = torch.empty(v_h.size, dtype=torch.float64).pin_memory().numpy()
+    xp[:] = x_h
+    vp[:] = v_h
+    e2e_s = 0.0
+    e2e_iters = 0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        st, tr = solver.step(scene, xp, vp, H, cfg)
+        xp[:] = st.x  # the next frame's host input
+        vp[:] = st.v
+        e2e_s += time.perf_counter() - t0
+        e2e_iters += tr.iterations
+        barrier()
+    e2e_s = allmax(e2e_s)
+    e2e_all = allsum(float(e2e_iters))
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+
+    def roof(name, kernels):
+        ms, cnt, b = stats[name]
+        if cnt == 0 or ms <= 0:
+            return None
+        ach = (b / cnt) / (ms / cnt * 1e-3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get(name)
+        return {"bound": "hbm", "kernel": kernels, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": traffic, "bytes_per_launch": round(b / cnt),
+                "us_per_launch": round(1e3 * ms / cnt, 2), "launches": cnt, "peak_kind": peak_kind}
+
+    stage_share = {k: {"ms": round(v[0], 2), "count": v[1], "share": round(v[0] / max(total_ms, 1e-9), 4)}
+                   for k, v in stats.items()}
+    n3 = 3 * scene.mesh.n_vertices
+    line = {
+        "metric": "PNCG iters/sec", "value": all_iters / (t_max * 1e-3), "unit": "iters/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": SCENE_DESC, "step": "one frame (prepare_step + advance_step)",
+                   "l2": "flushed between timed frames (512 MiB write)",
+                   "parallelism": "replicas" if ws > 1 else "single-gpu", "iter_max": cfg.iter_max},
+        "sec_per_frame": t_max * 1e-3 / args.steps,
+        "frames": frames,
+        "e2e": {"value": e2e_all / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": 2 * 8 * n3,
+                "d2h_bytes_per_step": 2 * 8 * n3, "sec_per_frame": e2e_s / args.steps,
+                "api": "paper_2604_19892_b200.solver.step(scene, x, v, h, cfg) with pinned numpy x, v"},
+        "roofline": roof("mas_apply", "MAS apply: k_restrict1 + k_coarse_mv + k_mas_apply_l0"),
+        "roofline_gradient": roof("gradient", "gradient: k_inertia_grad + k_tet_grad + k_contact_grad"),
+        "roofline_hvp": roof("hvp", "HVP: k_bsr_spmv + k_rank1_apply"),
+        "stages": stage_share,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline()
+        except Exception as e:  # reported, never silently replaced
+            line["cpu_baseline"] = {"value": None, "unavailable": repr(e)[:200]}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--iter-max", type=int, default=0, help="cap PNCG iterations per frame (0 = reference default)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,25 @@ int mp_ccd_pairs(mp_ctx* ctx, int64_t cap, int64_t* n, int64_t* verts, uint8_t* 
 /* Number of kernels this context has launched since creation. */
 int64_t mp_launch_count(mp_ctx* ctx);
 
+/* Per-stage CUDA-event timing on the context stream (bench / profiling).
+ * mp_stage_timing(ctx, 1) resets and enables; every later stage launch is
+ * bracketed by events.  mp_stage_stats returns, for one stage, the summed
+ * device time, the number of timed invocations and the summed ALGORITHMIC
+ * bytes of those invocations (compulsory unique HBM traffic). */
+enum {
+  MP_STAGE_GRADIENT = 0,       /* energy.gradient          energy.py:357-370 */
+  MP_STAGE_MAS_APPLY = 1,      /* mas.apply_preconditioner mas.py:182-205    */
+  MP_STAGE_HVP = 2,            /* HessianModel.hvp         energy.py:435-440 */
+  MP_STAGE_CONSTRAINT_SET = 3, /* broad phase + constraint set contact.py:116-165 */
+  MP_STAGE_HESSIAN = 4,        /* assemble_base_hessian    energy.py:373-413 */
+  MP_STAGE_MAS_BUILD = 5,      /* build_hierarchy          mas.py:138-179    */
+  MP_STAGE_UPDATE = 6,         /* classify/top-K/Woodbury  solver.py:337-346 */
+  MP_STAGE_CCD = 7,            /* CCD clamp                solver.py:268-280 */
+  MP_STAGE_COUNT = 8
+};
+int mp_stage_timing(mp_ctx* ctx, int enable);
+int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
+
 /* Message of the last failed mp_create on this thread. */
 const char* mp_create_error(void);
 

@@ -53,8 +53,10 @@ class IterRecordC(C.Structure):
 EXPORTS = (
     "mp_create", "mp_destroy", "mp_set_config", "mp_status_code", "mp_last_error", "mp_stream", "mp_partition",
     "mp_step", "mp_advance", "mp_broad_phase", "mp_constraint_set", "mp_gradient", "mp_energy", "mp_snapshot",
-    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_launch_count",
+    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_launch_count", "mp_stage_timing", "mp_stage_stats",
 )
+
+STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd")
 
 _lib = None
 
@@ -104,6 +106,8 @@ def load_library():
     lib.mp_precond_apply.argtypes = [vp, _f64p, C.c_int, _f64p]
     lib.mp_update_at.argtypes = [vp, _f64p, _i64p, _i64p]
     lib.mp_ccd.argtypes = [vp, _f64p, _f64p, _f64p, _f64p, _f64p, C.POINTER(C.c_int32), _i64p]
+    lib.mp_stage_timing.argtypes = [vp, C.c_int]
+    lib.mp_stage_stats.argtypes = [vp, C.c_int, _f64p, _i64p, _f64p]
     _lib = lib
     return lib
 
@@ -239,6 +243,19 @@ class NativeContext:
         self._check(self.lib.mp_step_device(self.h, C.c_double(h), recs, cap, C.byref(n), C.byref(conv),
                                             C.byref(flags)))
         return [recs[i] for i in range(min(n.value, cap))], bool(conv.value), int(flags.value)
+
+    # ---- per-stage CUDA-event timing ----
+    def stage_timing(self, enable=True):
+        self._check(self.lib.mp_stage_timing(self.h, int(enable)))
+
+    def stage_stats(self):
+        """{stage: (total_ms, count, algorithmic_bytes)} since stage_timing(True)."""
+        out = {}
+        for i, name in enumerate(STAGES):
+            ms, cnt, b = C.c_double(), C.c_int64(), C.c_double()
+            self._check(self.lib.mp_stage_stats(self.h, i, C.byref(ms), C.byref(cnt), C.byref(b)))
+            out[name] = (ms.value, int(cnt.value), b.value)
+        return out
 
     # ---- stage taps ----
     def broad_phase(self, x, motion_bound, d_hat):

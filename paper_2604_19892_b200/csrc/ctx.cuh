@@ -80,8 +80,22 @@ struct CoarseLevel {
   int chunks = 1;
 };
 
+// CUDA-event timer of one solver stage on the context stream.  Events are
+// recorded around the stage's launches; the elapsed time is folded in lazily
+// (at the next begin or at readout), after the loop's own per-iteration sync,
+// so timing adds no host stall.
+struct StageTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool pending = false;
+  double total_ms = 0.0;
+  double bytes = 0.0;   // algorithmic bytes of all timed launches
+  int64_t count = 0;
+};
+
 struct mp_ctx {
   int device = 0;
+  bool timing = false;
+  StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
   std::string last_error;
@@ -175,3 +189,32 @@ struct mp_ctx {
 
   ~mp_ctx();
 };
+
+static void timer_fold(StageTimer& t) {
+  if (!t.pending) return;
+  CUDA_CHECK(cudaEventSynchronize(t.b));
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, t.a, t.b));
+  t.total_ms += ms;
+  t.count += 1;
+  t.pending = false;
+}
+
+static void timer_begin(mp_ctx* c, int id) {
+  if (!c->timing) return;
+  StageTimer& t = c->timers[id];
+  timer_fold(t);
+  if (!t.a) {
+    CUDA_CHECK(cudaEventCreate(&t.a));
+    CUDA_CHECK(cudaEventCreate(&t.b));
+  }
+  CUDA_CHECK(cudaEventRecord(t.a, c->stream));
+}
+
+static void timer_end(mp_ctx* c, int id, double bytes) {
+  if (!c->timing) return;
+  StageTimer& t = c->timers[id];
+  CUDA_CHECK(cudaEventRecord(t.b, c->stream));
+  t.pending = true;
+  t.bytes += bytes;
+}

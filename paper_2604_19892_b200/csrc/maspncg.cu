@@ -18,6 +18,10 @@ mp_ctx::~mp_ctx() {
   for (auto* l : levels) delete l;
   if (h_scal) cudaFreeHost(h_scal);
   if (h_cnt) cudaFreeHost(h_cnt);
+  for (auto& t : timers) {
+    if (t.a) cudaEventDestroy(t.a);
+    if (t.b) cudaEventDestroy(t.b);
+  }
   if (solver) cusolverDnDestroy(solver);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -322,18 +326,28 @@ static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
   for (int64_t k = 0; k < cfg.iter_max; ++k) {
     auto t0 = Clock::now();
     const bool rebuild = restart || full_every;
+    timer_begin(c, MP_STAGE_CONSTRAINT_SET);
     constraint_set(c, c->x);
+    timer_end(c, MP_STAGE_CONSTRAINT_SET, 0.0);
     if (rebuild) {
       snapshot(c, c->x, h, true);
     } else {
+      timer_begin(c, MP_STAGE_UPDATE);
       update_build(c);
+      timer_end(c, MP_STAGE_UPDATE, 0.0);
     }
+    timer_begin(c, MP_STAGE_GRADIENT);
     gradient(c, c->x, c->xt, h, c->g);
+    timer_end(c, MP_STAGE_GRADIENT, gradient_bytes(c));
+    timer_begin(c, MP_STAGE_MAS_APPLY);
     precond_apply(c, c->g, c->z, true);
+    timer_end(c, MP_STAGE_MAS_APPLY, mas_apply_bytes(c));
     sync_stream(c);
     auto t1 = Clock::now();
 
+    timer_begin(c, MP_STAGE_HVP);
     hvp(c, c->z, c->hv, !rebuild);
+    timer_end(c, MP_STAGE_HVP, hvp_bytes(c, !rebuild));
     DotSpec S{};
     S.n = 0;
     auto add = [&](const double* a, const double* b) {
@@ -397,7 +411,9 @@ static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
     auto t2 = Clock::now();
     double min_alpha = 1.0;
     if (pinf > 0.0) {
+      timer_begin(c, MP_STAGE_CCD);
       CcdResult cr = ccd_clamp(c, c->x, c->p, pinf, cfg.ccd_per_subdomain != 0, c->tmp);
+      timer_end(c, MP_STAGE_CCD, 0.0);
       min_alpha = cr.min_alpha;
       std::swap(c->x.p, c->tmp.p);
     }
@@ -508,6 +524,29 @@ const char* mp_last_error(mp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : 
 void* mp_stream(mp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 int64_t mp_launch_count(mp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int mp_stage_timing(mp_ctx* c, int enable) {
+  return guarded(c, [&] {
+    for (auto& t : c->timers) {
+      timer_fold(t);
+      t.total_ms = 0.0;
+      t.bytes = 0.0;
+      t.count = 0;
+    }
+    c->timing = enable != 0;
+  });
+}
+
+int mp_stage_stats(mp_ctx* c, int stage, double* total_ms, int64_t* count, double* bytes) {
+  return guarded(c, [&] {
+    if (stage < 0 || stage >= MP_STAGE_COUNT) throw MpError(MP_ERR_CONFIG, "unknown stage");
+    StageTimer& t = c->timers[stage];
+    timer_fold(t);
+    if (total_ms) *total_ms = t.total_ms;
+    if (count) *count = t.count;
+    if (bytes) *bytes = t.bytes;
+  });
+}
 
 static thread_local std::string g_create_error;
 const char* mp_create_error(void) { return g_create_error.c_str(); }

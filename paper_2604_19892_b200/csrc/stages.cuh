@@ -10,6 +10,25 @@
 
 #define WOODBURY_KMAX 48
 
+// ALGORITHMIC bytes per stage invocation: compulsory
+// unique HBM traffic, FP64 = 8 B, ids int32.
+static double gradient_bytes(const mp_ctx* c) {
+  return 81.0 * c->N + 113.0 * c->T + 17.0 * c->cur.count;
+}
+static double mas_apply_bytes(const mp_ctx* c) {
+  double b = 8.0 * (double)c->D * (double)cyc_size(c->m) + 48.0 * c->N;
+  for (int l = 0; l < c->n_levels; ++l) b += 8.0 * (double)cyc_size(c->levels[l]->n);
+  return b;
+}
+static double hvp_bytes(const mp_ctx* c, bool with_cands) {
+  double pairs = (double)c->base.count + (with_cands ? (double)c->n_cand : 0.0);
+  return 76.0 * c->nnzb + 4.0 * (c->N + 1) + 48.0 * c->N + 116.0 * pairs;
+}
+static double hessian_bytes(const mp_ctx* c) {
+  return 33.0 * c->N + 113.0 * c->T + 72.0 * c->nnzb;
+}
+
+
 // energy.gradient (energy.py:357-370) with the current constraint set
 static void gradient(mp_ctx* c, const double* x, const double* xt, double h, double* g) {
   elastic_gradient(c, x, xt, h, g);
@@ -130,14 +149,20 @@ static void mas_build(mp_ctx* c) {
 // rebuild branch of advance_step (solver.py:323-335): base := cur at x,
 // H_base = assemble_base_hessian, MAS hierarchy
 static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
+  timer_begin(c, MP_STAGE_HESSIAN);
   copy_table(c, c->cur, c->base);
   assemble_elastic_bsr(c, x, h);
+  timer_end(c, MP_STAGE_HESSIAN, hessian_bytes(c));
   c->have_snapshot = true;
   c->have_mas = false;
   c->have_updates = false;
   c->n_cand = 0;
   c->n_touched = 0;
-  if (build_mas) mas_build(c);
+  if (build_mas) {
+    timer_begin(c, MP_STAGE_MAS_BUILD);
+    mas_build(c);
+    timer_end(c, MP_STAGE_MAS_BUILD, 0.0);
+  }
 }
 
 // non-rebuild branch (solver.py:337-346): classify_all, select_top_k,

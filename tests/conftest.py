@@ -9,6 +9,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 GOLDEN = Path(__file__).resolve().parent / "golden"
 GOLDEN_SCENES = ("drop", "locking", "stacked_k8", "stacked_k256", "cube3_capped")
+BP_FIXTURES = ("bp_cube8",)
 
 
 def pytest_configure(config):

@@ -237,7 +237,34 @@ def run_scene(name, scene, frames, cfg, v0=None, h=0.01, taps=True):
           f"taps={ {k: len(v) for k, v in tap.rec.items()} }", flush=True)
 
 
+def broad_phase_cases(name="bp_cube8", cells=8):
+    """Broad-phase-only fixture at C1 size (the 8^3 soft cube on its floor):
+    jittered iterates pushed into the floor's contact zone, several motion
+    bounds, both the constraint-set (mb = 0, d_hat) and the CCD (mb, 0) calls."""
+    scene = scenes.c1_cube(cells, mods=MODS)
+    rng = np.random.default_rng(20260823)
+    rest = scene.mesh.rest_positions
+    free = ~scene.dirichlet
+    data = dict(scene_arrays(scene))
+    cases = []
+    for i, (drop, jit, mb, dh) in enumerate([(0.0, 0.0, 0.0, 2e-3), (0.0095, 1e-4, 0.0, 2e-3),
+                                              (0.0095, 1e-4, 3e-3, 0.0), (0.0099, 3e-4, 1e-2, 0.0),
+                                              (0.0099, 3e-4, 0.0, 2e-3), (0.0, 2e-3, 0.0, 2e-2),
+                                              (0.0099, 1e-3, 3e-2, 0.0), (0.0099, 1e-3, 0.0, 1e-2)]):
+        x = rest.copy()
+        x[free, 2] -= drop
+        x[free] += jit * rng.standard_normal((free.sum(), 3))
+        pt, ee = geo.broad_phase(x, scene.surface, mb, dh)
+        cases.append(dict(x=x.ravel(), mb=mb, d_hat=dh, pt=pt, ee=ee))
+        print(f"{name} case {i}: pt={len(pt)} ee={len(ee)}", flush=True)
+    data.update(flatten_taps({"broad_phase": cases}))
+    np.savez_compressed(OUT / f"{name}.npz", **data)
+
+
 def main():
+    if "--bp" in sys.argv:
+        broad_phase_cases()
+        return
     run_scene("drop", scenes.drop(MODS), 25, sol.SolverConfig())
     s = scenes.locking(MODS)
     nv = s.mesh.n_vertices
