@@ -176,6 +176,35 @@ def _ref_cells(lo, hi, cell):
     return np.floor(lo / cell).astype(np.int64), np.floor(hi / cell).astype(np.int64)
 
 
+_CHUNK = 1 << 23  # candidate pairs per filtering pass (bounded memory)
+
+
+def _chunks(per):
+    """[start, stop) item ranges whose summed candidate counts stay near
+    _CHUNK (at least one item each)."""
+    cum = np.cumsum(per)
+    start, n = 0, len(per)
+    while start < n:
+        base = cum[start - 1] if start else 0
+        stop = max(int(np.searchsorted(cum, base + _CHUNK, "right")), start + 1)
+        yield start, min(stop, n)
+        start = stop
+
+
+def _ee_filter(a, b, edges, e_lo, e_hi, gap, pad, cell):
+    i, j = np.minimum(a, b), np.maximum(a, b)
+    sel = i < j
+    i, j = i[sel], j[sel]
+    ei, ej = edges[i], edges[j]
+    ok = ~np.any(ej[:, :, None] == ei[:, None, :], axis=(1, 2))
+    ok &= np.all(e_lo[i] <= e_hi[j] + gap, axis=1) & np.all(e_lo[j] <= e_hi[i] + gap, axis=1)
+    i, j = i[ok], j[ok]
+    q0, q1 = _ref_cells(e_lo[i] - pad, e_hi[i] + pad, cell)
+    i0, i1 = _ref_cells(e_lo[j] - pad, e_hi[j] + pad, cell)
+    ok = np.all((q0 <= i1) & (i0 <= q1), axis=1)
+    return np.stack([i[ok], j[ok]], axis=1).astype(np.int64)
+
+
 def broad_phase(x, tris, edges, surf_verts, motion_bound, d_hat):
     """Sorted unique (v, tri) and (edge i, edge j) candidate pairs, exactly
     the reference's `broad_phase` output (`geometry.py:443-503`)."""
@@ -205,19 +234,25 @@ def broad_phase(x, tris, edges, surf_verts, motion_bound, d_hat):
     lo_i = np.searchsorted(keys, vkey, "left")
     hi_i = np.searchsorted(keys, vkey, "right")
     cnt = hi_i - lo_i
-    qi = np.repeat(np.arange(len(surf_verts)), cnt)
-    ti = prim[_ranges(lo_i, cnt)]
-    if len(big):
-        qi = np.concatenate([qi, np.repeat(np.arange(len(surf_verts)), len(big))])
-        ti = np.concatenate([ti, np.tile(big, len(surf_verts))])
-    v = surf_verts[qi]
-    p = x[v]
-    ok = ~np.any(tris[ti] == v[:, None], axis=1)
-    ok &= np.all(p >= tri_lo[ti] - gap, axis=1) & np.all(p <= tri_hi[ti] + gap, axis=1)
-    q0, q1 = _ref_cells(p - pad, p + pad, cell)
-    i0, i1 = _ref_cells(tri_lo[ti] - pad, tri_hi[ti] + pad, cell)
-    ok &= np.all((q0 <= i1) & (i0 <= q1), axis=1)
-    pt = np.unique(np.stack([v[ok], ti[ok]], axis=1).astype(np.int64), axis=0)
+    bigc = len(big)
+    out = []
+    for start, stop in _chunks(cnt + bigc):  # bounded-memory query batches
+        qs = np.arange(start, stop)
+        qi = np.repeat(qs, cnt[qs])
+        ti = prim[_ranges(lo_i[qs], cnt[qs])]
+        if bigc:
+            qi = np.concatenate([qi, np.repeat(qs, bigc)])
+            ti = np.concatenate([ti, np.tile(big, len(qs))])
+        v = surf_verts[qi]
+        p = x[v]
+        ok = ~np.any(tris[ti] == v[:, None], axis=1)
+        ok &= np.all(p >= tri_lo[ti] - gap, axis=1) & np.all(p <= tri_hi[ti] + gap, axis=1)
+        v, ti, p = v[ok], ti[ok], p[ok]
+        q0, q1 = _ref_cells(p - pad, p + pad, cell)
+        i0, i1 = _ref_cells(tri_lo[ti] - pad, tri_hi[ti] + pad, cell)
+        ok = np.all((q0 <= i1) & (i0 <= q1), axis=1)
+        out.append(np.stack([v[ok], ti[ok]], axis=1).astype(np.int64))
+    pt = np.unique(np.concatenate(out), axis=0) if out else np.zeros((0, 2), np.int64)
 
     # ---- edge-edge ----
     E = len(edges)
@@ -231,22 +266,16 @@ def broad_phase(x, tris, edges, surf_verts, motion_bound, d_hat):
     starts = np.flatnonzero(np.r_[True, keys[1:] != keys[:-1]])
     gsize = np.diff(np.r_[starts, len(keys)])
     pos = np.arange(len(keys))
-    gend = np.repeat(starts + gsize, gsize)
-    later = gend - pos - 1  # partners after this entry in its cell
-    a = np.repeat(prim, later)
-    b = prim[_ranges(pos + 1, later)]
-    if len(big):
-        a = np.concatenate([a, np.repeat(big, E)])
-        b = np.concatenate([b, np.tile(np.arange(E), len(big))])
-    i, j = np.minimum(a, b), np.maximum(a, b)
-    sel = i < j
-    code = np.unique(i[sel] * E + j[sel])
-    i, j = code // E, code % E
-    ei, ej = edges[i], edges[j]
-    ok = ~np.any(ej[:, :, None] == ei[:, None, :], axis=(1, 2))
-    ok &= np.all(e_lo[i] <= e_hi[j] + gap, axis=1) & np.all(e_lo[j] <= e_hi[i] + gap, axis=1)
-    q0, q1 = _ref_cells(e_lo[i] - pad, e_hi[i] + pad, cell)
-    i0, i1 = _ref_cells(e_lo[j] - pad, e_hi[j] + pad, cell)
-    ok &= np.all((q0 <= i1) & (i0 <= q1), axis=1)
-    ee = np.stack([i[ok], j[ok]], axis=1).astype(np.int64)
+    later = np.repeat(starts + gsize, gsize) - pos - 1  # partners after this entry in its cell
+    out = []
+    for start, stop in _chunks(later):
+        es = np.arange(start, stop)
+        a = np.repeat(prim[es], later[es])
+        b = prim[_ranges(es + 1, later[es])]
+        out.append(_ee_filter(a, b, edges, e_lo, e_hi, gap, pad, cell))
+    for start, stop in _chunks(np.full(len(big), E)):  # oversized edges vs all
+        bb = big[start:stop]
+        out.append(_ee_filter(np.repeat(bb, E), np.tile(np.arange(E), len(bb)), edges, e_lo, e_hi, gap, pad,
+                              cell))
+    ee = np.unique(np.concatenate(out), axis=0) if out else np.zeros((0, 2), np.int64)
     return pt.reshape(-1, 2), ee.reshape(-1, 2)

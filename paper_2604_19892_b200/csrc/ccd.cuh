@@ -189,8 +189,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
   k_fill<<<grid_for(c->D, 256), 256, 0, c->stream>>>(c->alpha_d, c->D, 1.0);
   LAUNCH_CHECK();
   if (c->F > 0) {
-    const double gap = 0.0 + 2.0 * pinf;
-    GridBuild B = build_grid(c, x, gap);
+    BpGrid B = build_bp(c, x, pinf, 0.0);
     ContactParams CP{};
     CcdParams CC{p, c->cfg.alpha_l, c->bs};
     if (c->ccd_verts.n < 4096) {
@@ -200,7 +199,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       BpOut O{};
       O.verts = c->ccd_verts; O.ccd_ispt = c->ccd_ispt; O.alpha_pair = c->ccd_alpha; O.alpha_d = c->alpha_d;
       O.cap = (int64_t)c->ccd_verts.n;
-      int64_t n = run_queries<BP_CCD>(c, x, B, O, CP, CC, nullptr);
+      int64_t n = run_bp<BP_CCD>(c, x, B, O, CP, CC, nullptr);
       if (n <= O.cap) {
         R.n_pairs = n;
         break;

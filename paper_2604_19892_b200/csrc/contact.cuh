@@ -23,55 +23,68 @@
 
 enum { BP_RAW = 0, BP_CONTACT = 1, BP_CCD = 2 };
 
-struct Grid {
+// ---------------------------------------------------------------------------
+// dense cell grid (our own cell size, independent of the reference's)
+
+struct CellGrid {
   double o[3];
-  double c;
-  long long n[3];
+  double h;
+  int n[3];
 };
 
-__device__ __forceinline__ long long cell_coord(double v, double o, double c, long long n) {
-  double q = floor((v - o) / c);
-  long long i = (long long)q;
-  if (!(q >= 0.0)) i = 0;  // also catches NaN
-  if (i > n - 1) i = n - 1;
-  return i;
+__device__ __forceinline__ int cg_coord(double v, double o, double h, int n) {
+  double q = floor((v - o) / h);  // monotone in v: box tests imply cell hits
+  if (!(q >= 0.0)) return 0;      // also catches NaN
+  if (q > (double)(n - 1)) return n - 1;
+  return (int)q;
 }
 
-__device__ __forceinline__ long long cell_key(const Grid& G, long long ix, long long iy, long long iz) {
-  return (ix * G.n[1] + iy) * G.n[2] + iz;
-}
+__device__ __forceinline__ int cg_id(const CellGrid& G, int a, int b, int c) { return (a * G.n[1] + b) * G.n[2] + c; }
 
-// primitive boxes: prim < F -> triangle filter box [lo-gap, hi+gap];
-// prim >= F -> edge box [lo, hi+gap]
+// Primitive boxes.  prim < F: triangle; raw box [lo, hi] of its vertices
+// and filter box [lo - gap, hi + gap].  prim >= F: edge; raw box and the
+// join box [lo, hi + gap].  The largest raw-box diagonal (the reference's
+// grid cell candidate, geometry.py:462-465) is max-reduced into *diag_max.
 __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, const int* __restrict__ edge,
                              const double* __restrict__ x, double gap, double* __restrict__ lo,
-                             double* __restrict__ hi) {
+                             double* __restrict__ hi, double* __restrict__ rlo, double* __restrict__ rhi,
+                             double* __restrict__ diag_max) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= F + E) return;
-  double l[3], h[3];
-  if (i < F) {
-    int a = tri[3 * i], b = tri[3 * i + 1], c = tri[3 * i + 2];
+  double dg = 0.0;
+  if (i < F + E) {
+    double l[3], h[3];
+    if (i < F) {
+      int a = tri[3 * i], b = tri[3 * i + 1], c = tri[3 * i + 2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double xa = x[3 * a + k], xb = x[3 * b + k], xc = x[3 * c + k];
+        l[k] = fmin(fmin(xa, xb), xc);
+        h[k] = fmax(fmax(xa, xb), xc);
+      }
+    } else {
+      int64_t e = i - F;
+      int a = edge[2 * e], b = edge[2 * e + 1];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double xa = x[3 * a + k], xb = x[3 * b + k];
+        l[k] = fmin(xa, xb);
+        h[k] = fmax(xa, xb);
+      }
+    }
+    double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      double xa = x[3 * a + k], xb = x[3 * b + k], xc = x[3 * c + k];
-      l[k] = fmin(fmin(xa, xb), xc) - gap;
-      h[k] = fmax(fmax(xa, xb), xc) + gap;
+      double dk = RSUB(h[k], l[k]);
+      s = (k == 0) ? RMUL(dk, dk) : RADD(s, RMUL(dk, dk));
+      rlo[3 * i + k] = l[k];
+      rhi[3 * i + k] = h[k];
+      lo[3 * i + k] = (i < F) ? RSUB(l[k], gap) : l[k];
+      hi[3 * i + k] = RADD(h[k], gap);
     }
-  } else {
-    int64_t e = i - F;
-    int a = edge[2 * e], b = edge[2 * e + 1];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      double xa = x[3 * a + k], xb = x[3 * b + k];
-      l[k] = fmin(xa, xb);
-      h[k] = fmax(xa, xb) + gap;
-    }
+    dg = __dsqrt_rn(s);
   }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    lo[3 * i + k] = l[k];
-    hi[3 * i + k] = h[k];
-  }
+  dg = warp_max(dg);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(diag_max, dg);
 }
 
 // stats for the grid: [0..2] min lo, [3..5] max hi, [6] sum of max extents
@@ -107,49 +120,107 @@ __global__ void k_box_stats(int64_t P, const double* __restrict__ lo, const doub
   }
 }
 
-__device__ __forceinline__ void box_cells(const Grid& G, const double* lo, const double* hi, long long c0[3],
-                                          long long c1[3]) {
+__device__ __forceinline__ void box_span(const CellGrid& G, const double* lo, const double* hi, int c0[3],
+                                         int c1[3]) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    c0[k] = cell_coord(lo[k], G.o[k], G.c, G.n[k]);
-    c1[k] = cell_coord(hi[k], G.o[k], G.c, G.n[k]);
+    c0[k] = cg_coord(lo[k], G.o[k], G.h, G.n[k]);
+    c1[k] = cg_coord(hi[k], G.o[k], G.h, G.n[k]);
   }
 }
 
-__global__ void k_cell_count(int64_t P0, int64_t P, Grid G, const double* __restrict__ lo,
-                             const double* __restrict__ hi, int* __restrict__ cnt) {
+// number of grid cells each primitive box covers
+__global__ void k_cell_span(int64_t P, CellGrid G, const double* __restrict__ lo, const double* __restrict__ hi,
+                            int* __restrict__ cnt) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= P) return;
-  long long c0[3], c1[3];
-  box_cells(G, lo + 3 * (P0 + i), hi + 3 * (P0 + i), c0, c1);
-  long long n = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
+  int c0[3], c1[3];
+  box_span(G, lo + 3 * i, hi + 3 * i, c0, c1);
+  long long n = (long long)(c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
   cnt[i] = (int)(n > (1 << 30) ? (1 << 30) : n);
 }
 
-__global__ void k_cell_fill(int64_t P0, int64_t P, Grid G, const double* __restrict__ lo,
-                            const double* __restrict__ hi, const int* __restrict__ off,
-                            unsigned long long* __restrict__ keys, int* __restrict__ prim) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  long long c0[3], c1[3];
-  box_cells(G, lo + 3 * (P0 + i), hi + 3 * (P0 + i), c0, c1);
-  int o = off[i];
-  for (long long a = c0[0]; a <= c1[0]; ++a)
-    for (long long b = c0[1]; b <= c1[1]; ++b)
-      for (long long c = c0[2]; c <= c1[2]; ++c) {
-        keys[o] = (unsigned long long)cell_key(G, a, b, c);
-        prim[o] = (int)i;
-        ++o;
-      }
+__device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
+  int l = 0, r = n;
+  while (l < r) {
+    int m = (l + r) >> 1;
+    if (a[m] <= k) l = m + 1; else r = m;
+  }
+  return l;
 }
 
-__device__ __forceinline__ int lower_bound_u64(const unsigned long long* a, int n, unsigned long long k) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < k) lo = mid + 1; else hi = mid;
+// one thread per (primitive, covered cell) entry: its cell id and the
+// per-cell histograms (triangles and edges separately)
+__global__ void k_entry_hist(int64_t total, int64_t P, int64_t F, CellGrid G, const int* __restrict__ off,
+                             const double* __restrict__ lo, const double* __restrict__ hi, int* __restrict__ ecell,
+                             int* __restrict__ tri_cnt, int* __restrict__ edge_cnt) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int p = upper_bound_i32(off, (int)P + 1, (int)e) - 1;
+  int r = (int)e - off[p];
+  int c0[3], c1[3];
+  box_span(G, lo + 3 * (int64_t)p, hi + 3 * (int64_t)p, c0, c1);
+  int sx = c1[0] - c0[0] + 1, sy = c1[1] - c0[1] + 1;
+  int a = c0[0] + r % sx, b = c0[1] + (r / sx) % sy, c = c0[2] + r / (sx * sy);
+  int cell = cg_id(G, a, b, c);
+  ecell[e] = cell;
+  atomicAdd(p < F ? &tri_cnt[cell] : &edge_cnt[cell], 1);
+}
+
+__global__ void k_entry_fill(int64_t total, int64_t P, int64_t F, const int* __restrict__ off,
+                             const int* __restrict__ ecell, const int* __restrict__ tri_start,
+                             const int* __restrict__ edge_start, int* __restrict__ tri_cur,
+                             int* __restrict__ edge_cur, int* __restrict__ tri_ent, int* __restrict__ edge_ent) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int p = upper_bound_i32(off, (int)P + 1, (int)e) - 1;
+  int cell = ecell[e];
+  if (p < F) tri_ent[tri_start[cell] + atomicAdd(&tri_cur[cell], 1)] = p;
+  else edge_ent[edge_start[cell] + atomicAdd(&edge_cur[cell], 1)] = p - (int)F;
+}
+
+// surface vertices: one cell each
+__global__ void k_point_hist(int64_t V, const int* __restrict__ sverts, const double* __restrict__ x, CellGrid G,
+                             int* __restrict__ pcell, int* __restrict__ pt_cnt) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= V) return;
+  int v = sverts[q];
+  int cell = cg_id(G, cg_coord(x[3 * v], G.o[0], G.h, G.n[0]), cg_coord(x[3 * v + 1], G.o[1], G.h, G.n[1]),
+                   cg_coord(x[3 * v + 2], G.o[2], G.h, G.n[2]));
+  pcell[q] = cell;
+  atomicAdd(&pt_cnt[cell], 1);
+}
+
+__global__ void k_point_fill(int64_t V, const int* __restrict__ pcell, const int* __restrict__ pt_start,
+                             int* __restrict__ pt_cur, int* __restrict__ pt_ent) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= V) return;
+  int cell = pcell[q];
+  pt_ent[pt_start[cell] + atomicAdd(&pt_cur[cell], 1)] = (int)q;
+}
+
+// work lists: cells holding points and triangles; cells holding >= 2 edges
+__global__ void k_cell_lists(int ncell, const int* __restrict__ pt_start, const int* __restrict__ tri_start,
+                             const int* __restrict__ edge_start, int* __restrict__ cells_pt,
+                             int* __restrict__ cells_ee, int* __restrict__ ncount) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  bool a = false, b = false;
+  if (c < ncell) {
+    a = (pt_start[c + 1] > pt_start[c]) && (tri_start[c + 1] > tri_start[c]);
+    b = (edge_start[c + 1] - edge_start[c]) >= 2;
   }
-  return lo;
+  const int lane = threadIdx.x & 31;
+  unsigned ma = __ballot_sync(0xffffffffu, a), mb = __ballot_sync(0xffffffffu, b);
+  int ba = 0, bb = 0;
+  if (lane == 0) {
+    if (ma) ba = atomicAdd(&ncount[0], __popc(ma));
+    if (mb) bb = atomicAdd(&ncount[1], __popc(mb));
+  }
+  ba = __shfl_sync(0xffffffffu, ba, 0);
+  bb = __shfl_sync(0xffffffffu, bb, 0);
+  unsigned below = (1u << lane) - 1u;
+  if (a) cells_pt[ba + __popc(ma & below)] = c;
+  if (b) cells_ee[bb + __popc(mb & below)] = c;
 }
 
 struct BpOut {
@@ -193,16 +264,14 @@ struct ContactParams {
   KeyCtx key;
 };
 
-// emit one active constraint (contact.py:139-165) into the scratch table
-__device__ void emit_contact(const BpOut& O, const ContactParams& CP, int type, const int vid[4], double d,
-                             double gr[12]) {
+// write one active constraint (contact.py:139-165) into slot of the scratch table
+__device__ void write_contact(const BpOut& O, const ContactParams& CP, int slot, int type, const int vid[4], double d,
+                              double gr[12]) {
 #pragma unroll
   for (int a = 0; a < 4; ++a)
     if (CP.pinned[vid[a]]) {
       gr[3 * a] = 0.0; gr[3 * a + 1] = 0.0; gr[3 * a + 2] = 0.0;
     }
-  int slot = atomicAdd(&O.counter[0], 1);
-  if (slot >= O.cap) return;
   double s = 0.0;
 #pragma unroll
   for (int q = 0; q < 12; ++q) s += gr[q] * gr[q];
@@ -229,130 +298,192 @@ struct CcdParams {
 
 __device__ double ccd_pair_alpha(const double* x, const double* p, const int vid[4], bool is_pt, double alpha_l);
 
-// PT query: one thread per surface vertex, single cell
+// one CCD candidate: certified pair step (ccd.py:255-281) into the pair
+// list, min-reduced into its vertices' subdomains (ccd.py:284-294)
+__device__ __forceinline__ void write_ccd(const BpOut& O, const CcdParams& CC, const double* x, int slot,
+                                          const int vid[4], bool is_pt) {
+  O.verts[slot] = make_int4(vid[0], vid[1], vid[2], vid[3]);
+  O.ccd_ispt[slot] = is_pt ? 1 : 0;
+  double al = ccd_pair_alpha(x, CC.p, vid, is_pt, CC.alpha_l);
+  O.alpha_pair[slot] = al;
+  if (al < 1.0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid[r] / CC.bs], al);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cell-centric queries: one warp per work cell, lanes stride over the cell's
+// candidate pairs, warp-aggregated output slots.
+
+// the reference hash grid's reachability (geometry.py:417-440, 465-475):
+// query box [q_lo - pad, q_hi + pad] and inserted box [b_lo - pad, b_hi + pad]
+// share a reference cell on every axis
+struct RefGrid {
+  double cell, pad;
+};
+
+__device__ __forceinline__ bool ref_reach(const RefGrid& R, const double* qlo, const double* qhi, const double* blo,
+                                          const double* bhi) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double q0 = floor(RDIV(RSUB(qlo[k], R.pad), R.cell)), q1 = floor(RDIV(RADD(qhi[k], R.pad), R.cell));
+    double i0 = floor(RDIV(RSUB(blo[k], R.pad), R.cell)), i1 = floor(RDIV(RADD(bhi[k], R.pad), R.cell));
+    if (!(q0 <= i1 && i0 <= q1)) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ int warp_slot(bool emit, int* counter) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, emit);
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+struct BpTables {
+  CellGrid G;
+  RefGrid R;
+  const int *pt_start, *pt_ent, *tri_start, *tri_ent, *edge_start, *edge_ent;
+  const int *cells_pt, *cells_ee, *ncount;
+  const double *lo, *hi, *rlo, *rhi;  // (F+E)*3: filter/join boxes and raw boxes
+};
+
+// PT pairs (geometry.py:478-487): points of the cell x triangles whose
+// filter box covers the cell -- each passing pair is met exactly once
 template <int MODE>
-__global__ void k_query_pt(int64_t V, const int* __restrict__ sverts, const int* __restrict__ tri,
-                           const int* __restrict__ tri_sorted, const double* __restrict__ x, Grid G,
-                           const unsigned long long* __restrict__ keys, const int* __restrict__ prim, int nkeys,
-                           const double* __restrict__ lo, const double* __restrict__ hi, BpOut O,
-                           ContactParams CP, CcdParams CC) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= V) return;
-  int v = sverts[q];
-  double pv[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
-  unsigned long long key = (unsigned long long)cell_key(G, cell_coord(pv[0], G.o[0], G.c, G.n[0]),
-                                                       cell_coord(pv[1], G.o[1], G.c, G.n[1]),
-                                                       cell_coord(pv[2], G.o[2], G.c, G.n[2]));
-  int k0 = lower_bound_u64(keys, nkeys, key);
-  for (int kk = k0; kk < nkeys && keys[kk] == key; ++kk) {
-    int t = prim[kk];
-    int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
-    if (a == v || b == v || c == v) continue;
-    const double* l = lo + 3 * (int64_t)t;
-    const double* h = hi + 3 * (int64_t)t;
-    if (!(pv[0] >= l[0] && pv[1] >= l[1] && pv[2] >= l[2] && pv[0] <= h[0] && pv[1] <= h[1] && pv[2] <= h[2]))
-      continue;
-    if (MODE == BP_RAW) {
-      int slot = atomicAdd(&O.counter[0], 1);
-      if (slot < O.cap) {
-        O.a[slot] = v;
-        O.b[slot] = t;
+__global__ void __launch_bounds__(256) k_bp_pt(BpTables T, const int* __restrict__ sverts, const int* __restrict__ tri,
+                                               const int* __restrict__ tri_sorted, const double* __restrict__ x,
+                                               BpOut O, ContactParams CP, CcdParams CC) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int ncells = T.ncount[0];
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ncells; w += nw) {
+    const int cell = T.cells_pt[w];
+    const int ps = T.pt_start[cell], np = T.pt_start[cell + 1] - ps;
+    const int ts = T.tri_start[cell], nt = T.tri_start[cell + 1] - ts;
+    const int64_t npairs = (int64_t)np * nt;
+    for (int64_t b0 = 0; b0 < npairs; b0 += 32) {
+      const int64_t q = b0 + lane;
+      bool pass = false;
+      int v = 0, t = 0;
+      double pv[3] = {0.0, 0.0, 0.0};
+      if (q < npairs) {
+        v = sverts[T.pt_ent[ps + (int)(q / nt)]];
+        t = T.tri_ent[ts + (int)(q % nt)];
+        const int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
+        pv[0] = x[3 * v]; pv[1] = x[3 * v + 1]; pv[2] = x[3 * v + 2];
+        const double* l = T.lo + 3 * (int64_t)t;
+        const double* h = T.hi + 3 * (int64_t)t;
+        pass = a != v && b != v && c != v && pv[0] >= l[0] && pv[1] >= l[1] && pv[2] >= l[2] && pv[0] <= h[0] &&
+               pv[1] <= h[1] && pv[2] <= h[2];
+        pass = pass && ref_reach(T.R, pv, pv, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t);
       }
-    } else if (MODE == BP_CONTACT) {
-      // distances against the triangle sorted by original id (contact.py:133-135)
-      int s0 = tri_sorted[3 * t], s1 = tri_sorted[3 * t + 1], s2 = tri_sorted[3 * t + 2];
-      double X0[3], X1[3], X2[3], gr[12];
+      if (MODE == BP_RAW) {
+        int slot = warp_slot(pass, O.counter);
+        if (pass && slot < O.cap) {
+          O.a[slot] = v;
+          O.b[slot] = t;
+        }
+      } else if (MODE == BP_CONTACT) {
+        // distance against the triangle sorted by original id (contact.py:133-135)
+        double d = 0.0, gr[12];
+        int vid[4] = {v, 0, 0, 0};
+        if (pass) {
+          vid[1] = tri_sorted[3 * t]; vid[2] = tri_sorted[3 * t + 1]; vid[3] = tri_sorted[3 * t + 2];
+          double X0[3], X1[3], X2[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        X0[k] = x[3 * s0 + k]; X1[k] = x[3 * s1 + k]; X2[k] = x[3 * s2 + k];
-      }
-      double d = pt_distance(pv, X0, X1, X2, gr);
-      if (d <= 0.0) O.counter[1] = 1;
-      else if (d < CP.d_hat) {
-        int vid[4] = {v, s0, s1, s2};
-        emit_contact(O, CP, 1, vid, d, gr);
-      }
-    } else {
-      int vid[4] = {v, a, b, c};  // CCD keeps surface order (ccd.py:229-231)
-      int slot = atomicAdd(&O.counter[0], 1);
-      if (slot < O.cap) {
-        O.verts[slot] = make_int4(v, a, b, c);
-        O.ccd_ispt[slot] = 1;
-        double al = ccd_pair_alpha(x, CC.p, vid, true, CC.alpha_l);
-        O.alpha_pair[slot] = al;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid[r] / CC.bs], al);
+          for (int k = 0; k < 3; ++k) {
+            X0[k] = x[3 * vid[1] + k]; X1[k] = x[3 * vid[2] + k]; X2[k] = x[3 * vid[3] + k];
+          }
+          d = pt_distance(pv, X0, X1, X2, gr);
+          if (d <= 0.0) O.counter[1] = 1;
+        }
+        const bool emit = pass && d > 0.0 && d < CP.d_hat;
+        int slot = warp_slot(emit, O.counter);
+        if (emit && slot < O.cap) write_contact(O, CP, slot, 1, vid, d, gr);
+      } else {
+        int slot = warp_slot(pass, O.counter);
+        if (pass && slot < O.cap) {
+          const int vid[4] = {v, tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};  // surface order (ccd.py:229-231)
+          write_ccd(O, CC, x, slot, vid, true);
+        }
       }
     }
   }
 }
 
-// EE query: one thread per edge, all its cells, dedup by intersection corner
+// EE pairs (geometry.py:489-499): all pairs of join boxes sharing the cell,
+// reported only in the cell holding the low corner of their intersection
 template <int MODE>
-__global__ void k_query_ee(int64_t E, int64_t F, const int* __restrict__ edge, const double* __restrict__ x, Grid G,
-                           const unsigned long long* __restrict__ keys, const int* __restrict__ prim, int nkeys,
-                           const double* __restrict__ lo, const double* __restrict__ hi, BpOut O,
-                           ContactParams CP, CcdParams CC) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= E) return;
-  const double* li = lo + 3 * (F + i);
-  const double* hi_i = hi + 3 * (F + i);
-  int ia = edge[2 * i], ib = edge[2 * i + 1];
-  long long c0[3], c1[3];
-  box_cells(G, li, hi_i, c0, c1);
-  for (long long ax = c0[0]; ax <= c1[0]; ++ax)
-    for (long long ay = c0[1]; ay <= c1[1]; ++ay)
-      for (long long az = c0[2]; az <= c1[2]; ++az) {
-        unsigned long long key = (unsigned long long)cell_key(G, ax, ay, az);
-        int k0 = lower_bound_u64(keys, nkeys, key);
-        for (int kk = k0; kk < nkeys && keys[kk] == key; ++kk) {
-          int j = prim[kk];
-          if (j <= i) continue;
-          int ja = edge[2 * j], jb = edge[2 * j + 1];
-          if (ia == ja || ia == jb || ib == ja || ib == jb) continue;
-          const double* lj = lo + 3 * (F + j);
-          const double* hj = hi + 3 * (F + j);
-          bool ok = true;
+__global__ void __launch_bounds__(256) k_bp_ee(BpTables T, const int* __restrict__ edge, const double* __restrict__ x,
+                                               int64_t F, BpOut O, ContactParams CP, CcdParams CC) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int ncells = T.ncount[1];
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ncells; w += nw) {
+    const int cell = T.cells_ee[w];
+    const int cz = cell % T.G.n[2], cy = (cell / T.G.n[2]) % T.G.n[1], cx = cell / (T.G.n[2] * T.G.n[1]);
+    const int es = T.edge_start[cell];
+    const int64_t k = T.edge_start[cell + 1] - es;
+    const int64_t npairs = k * (k - 1) / 2;
+    for (int64_t b0 = 0; b0 < npairs; b0 += 32) {
+      const int64_t q = b0 + lane;
+      bool pass = false;
+      int i = 0, j = 0, ia = 0, ib = 0, ja = 0, jb = 0;
+      if (q < npairs) {
+        // upper-triangle index -> (r, s), r < s
+        int64_t r = k - 2 - (int64_t)floor(sqrt((double)(-8 * q + 4 * k * (k - 1) - 7)) / 2.0 - 0.5);
+        int64_t s = q + r + 1 - k * (k - 1) / 2 + (k - r) * ((k - r) - 1) / 2;
+        int e1 = T.edge_ent[es + (int)r], e2 = T.edge_ent[es + (int)s];
+        i = min(e1, e2);
+        j = max(e1, e2);
+        ia = edge[2 * i]; ib = edge[2 * i + 1]; ja = edge[2 * j]; jb = edge[2 * j + 1];
+        const double* li = T.lo + 3 * (F + i);
+        const double* hi_i = T.hi + 3 * (F + i);
+        const double* lj = T.lo + 3 * (F + j);
+        const double* hj = T.hi + 3 * (F + j);
+        pass = !(ia == ja || ia == jb || ib == ja || ib == jb);
 #pragma unroll
-          for (int k = 0; k < 3; ++k) ok = ok && (li[k] <= hj[k]) && (lj[k] <= hi_i[k]);
-          if (!ok) continue;
-          // report only in the cell of the intersection's low corner
-          if (cell_coord(fmax(li[0], lj[0]), G.o[0], G.c, G.n[0]) != ax ||
-              cell_coord(fmax(li[1], lj[1]), G.o[1], G.c, G.n[1]) != ay ||
-              cell_coord(fmax(li[2], lj[2]), G.o[2], G.c, G.n[2]) != az)
-            continue;
-          if (MODE == BP_RAW) {
-            int slot = atomicAdd(&O.counter[0], 1);
-            if (slot < O.cap) {
-              O.a[slot] = (int)i;
-              O.b[slot] = j;
-            }
-          } else if (MODE == BP_CONTACT) {
-            double A0[3], A1[3], B0[3], B1[3], gr[12];
+        for (int kk = 0; kk < 3; ++kk) pass = pass && (li[kk] <= hj[kk]) && (lj[kk] <= hi_i[kk]);
+        pass = pass && cg_coord(fmax(li[0], lj[0]), T.G.o[0], T.G.h, T.G.n[0]) == cx &&
+               cg_coord(fmax(li[1], lj[1]), T.G.o[1], T.G.h, T.G.n[1]) == cy &&
+               cg_coord(fmax(li[2], lj[2]), T.G.o[2], T.G.h, T.G.n[2]) == cz;
+        pass = pass && ref_reach(T.R, T.rlo + 3 * (F + i), T.rhi + 3 * (F + i), T.rlo + 3 * (F + j),
+                                 T.rhi + 3 * (F + j));
+      }
+      if (MODE == BP_RAW) {
+        int slot = warp_slot(pass, O.counter);
+        if (pass && slot < O.cap) {
+          O.a[slot] = i;
+          O.b[slot] = j;
+        }
+      } else if (MODE == BP_CONTACT) {
+        double d = 0.0, gr[12];
+        const int vid[4] = {ia, ib, ja, jb};
+        if (pass) {
+          double A0[3], A1[3], B0[3], B1[3];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              A0[k] = x[3 * ia + k]; A1[k] = x[3 * ib + k]; B0[k] = x[3 * ja + k]; B1[k] = x[3 * jb + k];
-            }
-            double d = ee_distance(A0, A1, B0, B1, gr);
-            if (d <= 0.0) O.counter[1] = 1;
-            else if (d < CP.d_hat) {
-              int vid[4] = {ia, ib, ja, jb};
-              emit_contact(O, CP, 0, vid, d, gr);
-            }
-          } else {
-            int vid[4] = {ia, ib, ja, jb};
-            int slot = atomicAdd(&O.counter[0], 1);
-            if (slot < O.cap) {
-              O.verts[slot] = make_int4(ia, ib, ja, jb);
-              O.ccd_ispt[slot] = 0;
-              double al = ccd_pair_alpha(x, CC.p, vid, false, CC.alpha_l);
-              O.alpha_pair[slot] = al;
-#pragma unroll
-              for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid[r] / CC.bs], al);
-            }
+          for (int kk = 0; kk < 3; ++kk) {
+            A0[kk] = x[3 * ia + kk]; A1[kk] = x[3 * ib + kk]; B0[kk] = x[3 * ja + kk]; B1[kk] = x[3 * jb + kk];
           }
+          d = ee_distance(A0, A1, B0, B1, gr);
+          if (d <= 0.0) O.counter[1] = 1;
+        }
+        const bool emit = pass && d > 0.0 && d < CP.d_hat;
+        int slot = warp_slot(emit, O.counter);
+        if (emit && slot < O.cap) write_contact(O, CP, slot, 0, vid, d, gr);
+      } else {
+        int slot = warp_slot(pass, O.counter);
+        if (pass && slot < O.cap) {
+          const int vid[4] = {ia, ib, ja, jb};
+          write_ccd(O, CC, x, slot, vid, false);
         }
       }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -387,44 +518,38 @@ static int bits_for(unsigned long long v) {
 }
 
 // ---------------------------------------------------------------------------
-// grid build
+// broad-phase build (host driver)
 
-struct GridBuild {
-  Grid G;
-  int n_tri_keys = 0, n_edge_keys = 0;
-  unsigned long long* tri_keys = nullptr;
-  int* tri_prim = nullptr;
-  unsigned long long* edge_keys = nullptr;
-  int* edge_prim = nullptr;
+struct BpGrid {
+  BpTables T{};
+  int ncell = 0;
+  int64_t F = 0;
+  bool empty = true;
 };
 
 static void sync_stream(mp_ctx* c) { CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
 
-__global__ void k_sub_const(int* a, int64_t n, int v) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) a[i] -= v;
-}
-
-static void rebase_edge_prims(mp_ctx* c, GridBuild& B) {
-  if (B.n_edge_keys) {
-    k_sub_const<<<grid_for(B.n_edge_keys, 256), 256, 0, c->stream>>>(B.edge_prim, B.n_edge_keys, (int)c->F);
-    LAUNCH_CHECK();
-  }
-}
-
-static GridBuild build_grid(mp_ctx* c, const double* x, double gap) {
-  GridBuild B;
+// Everything one broad-phase call needs at (x, mb, d_hat): boxes, the dense
+// cell tables of triangles / edges / surface points and the work lists.
+static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
+  BpGrid B;
+  B.F = c->F;
   const int64_t P = c->F + c->E;
-  c->box_lo.ensure(3 * P);
-  c->box_hi.ensure(3 * P);
-  k_prim_boxes<<<grid_for(P, 256), 256, 0, c->stream>>>(c->F, c->E, c->tri, c->edge, x, gap, c->box_lo, c->box_hi);
+  if (c->F == 0 || P == 0) return B;
+  const double gap = d_hat + 2.0 * mb;
+  cudaStream_t st = c->stream;
+  c->box_lo.ensure(3 * P); c->box_hi.ensure(3 * P); c->box_rlo.ensure(3 * P); c->box_rhi.ensure(3 * P);
+  CUDA_CHECK(cudaMemsetAsync(c->dscal.p + 40, 0, sizeof(double), st));
+  k_prim_boxes<<<grid_for(P, 256), 256, 0, st>>>(c->F, c->E, c->tri, c->edge, x, gap, c->box_lo, c->box_hi,
+                                                  c->box_rlo, c->box_rhi, c->dscal.p + 40);
   LAUNCH_CHECK();
   const int nb = 64;
-  c->red_part.ensure(7 * nb);
-  k_box_stats<<<nb, 256, 0, c->stream>>>(P, c->box_lo, c->box_hi, c->red_part);
+  c->red_part.ensure(7 * nb + 1);
+  k_box_stats<<<nb, 256, 0, st>>>(P, c->box_lo, c->box_hi, c->red_part);
   LAUNCH_CHECK();
-  std::vector<double> part(7 * nb);
-  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * 7 * nb, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_CHECK(cudaMemcpyAsync(c->red_part.p + 7 * nb, c->dscal.p + 40, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  std::vector<double> part(7 * nb + 1);
+  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * (7 * nb + 1), cudaMemcpyDeviceToHost, st));
   sync_stream(c);
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0;
   for (int b = 0; b < nb; ++b) {
@@ -434,83 +559,114 @@ static GridBuild build_grid(mp_ctx* c, const double* x, double gap) {
     }
     ext += part[7 * b + 6];
   }
+  // the reference's cell and pad (geometry.py:465-466)
+  B.T.R.cell = fmax(part[7 * nb], d_hat + mb);
+  B.T.R.pad = 0.5 * d_hat + mb;
   double span = fmax(fmax(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
-  double cell = ext / (double)(P > 0 ? P : 1);
-  if (!(cell > 0.0) || !std::isfinite(cell)) cell = span > 0.0 ? span : 1.0;
-  cell = fmax(cell, span * 1e-6);
-  if (!(cell > 0.0)) cell = 1.0;
+  double h = ext / (double)P;  // mean box extent
+  if (!(h > 0.0) || !std::isfinite(h)) h = span > 0.0 ? span : 1.0;
+  h = fmax(h, span * 1e-6);
+  if (!(h > 0.0)) h = 1.0;
+  const double max_cells = fmax(1 << 18, fmin(1 << 24, 16.0 * (double)(P + c->V)));
   c->cell_cnt.ensure(P + 1);
   c->cell_off.ensure(P + 1);
-  int64_t total = 0;
-  for (int attempt = 0; attempt < 40; ++attempt) {
-    Grid& G = B.G;
-    G.c = cell;
+  int total = 0, ncell = 0;
+  for (int attempt = 0; attempt < 60; ++attempt, h *= 1.5) {
+    CellGrid& G = B.T.G;
+    G.h = h;
+    double cells = 1.0;
     for (int k = 0; k < 3; ++k) {
       G.o[k] = mn[k];
-      double nk = floor((mx[k] - mn[k]) / cell) + 1.0;
+      double nk = floor((mx[k] - mn[k]) / h) + 1.0;
       if (!(nk >= 1.0)) nk = 1.0;
-      G.n[k] = (long long)fmin(nk, 1048576.0);
+      G.n[k] = (int)fmin(nk, 1 << 20);
+      cells *= (double)G.n[k];
     }
-    if (P == 0) break;
-    k_cell_count<<<grid_for(P, 256), 256, 0, c->stream>>>(0, P, G, c->box_lo, c->box_hi, c->cell_cnt);
+    if (cells > max_cells) continue;
+    ncell = (int)cells;
+    k_cell_span<<<grid_for(P, 256), 256, 0, st>>>(P, G, c->box_lo, c->box_hi, c->cell_cnt);
     LAUNCH_CHECK();
-    CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + P, 0, sizeof(int), c->stream));
+    CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + P, 0, sizeof(int), st));
     exclusive_scan(c, c->cell_cnt, c->cell_off, P + 1);
-    int tot = 0, ftot = 0;
-    CUDA_CHECK(cudaMemcpyAsync(&tot, c->cell_off.p + P, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_CHECK(cudaMemcpyAsync(&ftot, c->cell_off.p + c->F, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 4, c->cell_off.p + P, sizeof(int), cudaMemcpyDeviceToHost, st));
     sync_stream(c);
-    total = tot;
-    if (tot >= 0 && tot <= 48 * P + 1024) {
-      B.n_tri_keys = ftot;
-      B.n_edge_keys = tot - ftot;
-      break;
-    }
-    cell *= 2.0;
+    total = c->h_cnt[4];
+    if (total >= 0 && (int64_t)total <= 64 * P + 4096) break;
   }
-  if (P == 0) return B;
-  c->cell_key.ensure(total + 1);
-  c->cell_key2.ensure(total + 1);
-  c->cell_prim.ensure(total + 1);
-  c->cell_prim2.ensure(total + 1);
-  // tris occupy [0, ftot), edges [ftot, total): fill with per-class offsets
-  k_cell_fill<<<grid_for(P, 256), 256, 0, c->stream>>>(0, P, B.G, c->box_lo, c->box_hi, c->cell_off, c->cell_key,
-                                                       c->cell_prim);
+  B.ncell = ncell;
+  const int64_t V = c->V;
+  auto& g = c->grid;
+  for (DBuf<int>* b : {&g.tri_cnt, &g.tri_start, &g.edge_cnt, &g.edge_start, &g.pt_cnt, &g.pt_start})
+    b->ensure((size_t)ncell + 1);
+  g.cells_pt.ensure(ncell);
+  g.cells_ee.ensure(ncell);
+  g.ecell.ensure((size_t)total + 1);
+  g.tri_ent.ensure((size_t)total + 1);
+  g.edge_ent.ensure((size_t)total + 1);
+  g.pcell.ensure(V + 1);
+  g.pt_ent.ensure(V + 1);
+  for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
+    CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * ((size_t)ncell + 1), st));
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 8, 0, 2 * sizeof(int), st));
+  if (total) {
+    k_entry_hist<<<grid_for(total, 256), 256, 0, st>>>(total, P, c->F, B.T.G, c->cell_off, c->box_lo, c->box_hi,
+                                                       g.ecell, g.tri_cnt, g.edge_cnt);
+    LAUNCH_CHECK();
+  }
+  if (V) {
+    k_point_hist<<<grid_for(V, 256), 256, 0, st>>>(V, c->sverts, x, B.T.G, g.pcell, g.pt_cnt);
+    LAUNCH_CHECK();
+  }
+  exclusive_scan(c, g.tri_cnt, g.tri_start, ncell + 1);
+  exclusive_scan(c, g.edge_cnt, g.edge_start, ncell + 1);
+  exclusive_scan(c, g.pt_cnt, g.pt_start, ncell + 1);
+  // the counts become per-cell fill cursors
+  for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
+    CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * ((size_t)ncell + 1), st));
+  if (total) {
+    k_entry_fill<<<grid_for(total, 256), 256, 0, st>>>(total, P, c->F, c->cell_off, g.ecell, g.tri_start,
+                                                       g.edge_start, g.tri_cnt, g.edge_cnt, g.tri_ent, g.edge_ent);
+    LAUNCH_CHECK();
+  }
+  if (V) {
+    k_point_fill<<<grid_for(V, 256), 256, 0, st>>>(V, g.pcell, g.pt_start, g.pt_cnt, g.pt_ent);
+    LAUNCH_CHECK();
+  }
+  k_cell_lists<<<grid_for(ncell, 256), 256, 0, st>>>(ncell, g.pt_start, g.tri_start, g.edge_start, g.cells_pt,
+                                                      g.cells_ee, c->counters.p + 8);
   LAUNCH_CHECK();
-  // edge prim ids are stored as (F + e): rebase to e after sort
-  unsigned long long maxkey = (unsigned long long)(B.G.n[0] * B.G.n[1] * B.G.n[2]);
-  int kb = bits_for(maxkey);
-  if (B.n_tri_keys)
-    sort_pairs_u64(c, c->cell_key.p, c->cell_key2.p, c->cell_prim.p, c->cell_prim2.p, B.n_tri_keys, kb);
-  if (B.n_edge_keys)
-    sort_pairs_u64(c, c->cell_key.p + B.n_tri_keys, c->cell_key2.p + B.n_tri_keys, c->cell_prim.p + B.n_tri_keys,
-                   c->cell_prim2.p + B.n_tri_keys, B.n_edge_keys, kb);
-  B.tri_keys = c->cell_key2.p;
-  B.tri_prim = c->cell_prim2.p;
-  B.edge_keys = c->cell_key2.p + B.n_tri_keys;
-  B.edge_prim = c->cell_prim2.p + B.n_tri_keys;
-  rebase_edge_prims(c, B);
+  BpTables& T = B.T;
+  T.pt_start = g.pt_start; T.pt_ent = g.pt_ent;
+  T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
+  T.edge_start = g.edge_start; T.edge_ent = g.edge_ent;
+  T.cells_pt = g.cells_pt; T.cells_ee = g.cells_ee; T.ncount = c->counters.p + 8;
+  T.lo = c->box_lo; T.hi = c->box_hi; T.rlo = c->box_rlo; T.rhi = c->box_rhi;
+  B.empty = false;
   return B;
 }
 
+static unsigned bp_blocks(mp_ctx* c) {
+  static int sms = 0;
+  if (!sms) CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  return (unsigned)(sms * 8);  // 8 x 256-thread CTAs per SM, persistent warps
+}
 
-// Runs both queries in MODE with capacity retry.  Returns emitted count.
+// Run the PT (which & 1) and EE (which & 2) queries in MODE; returns the
+// number of emitted records (may exceed O.cap: caller grows and retries).
 template <int MODE>
-static int64_t run_queries(mp_ctx* c, const double* x, GridBuild& B, BpOut O, ContactParams CP, CcdParams CC,
-                           int* penetration) {
+static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
+                      int* penetration, int which = 3) {
   CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(int), c->stream));
   O.counter = c->counters.p;
-  if (c->V && B.n_tri_keys) {
-    k_query_pt<MODE><<<grid_for(c->V, 128), 128, 0, c->stream>>>(c->V, c->sverts, c->tri, c->tri_sorted, x, B.G,
-                                                                  B.tri_keys, B.tri_prim, B.n_tri_keys, c->box_lo,
-                                                                  c->box_hi, O, CP, CC);
-    LAUNCH_CHECK();
-  }
-  if (c->E && B.n_edge_keys) {
-    k_query_ee<MODE><<<grid_for(c->E, 128), 128, 0, c->stream>>>(c->E, c->F, c->edge, x, B.G, B.edge_keys,
-                                                                  B.edge_prim, B.n_edge_keys, c->box_lo, c->box_hi,
-                                                                  O, CP, CC);
-    LAUNCH_CHECK();
+  if (!B.empty) {
+    if ((which & 1) && c->V) {
+      k_bp_pt<MODE><<<bp_blocks(c), 256, 0, c->stream>>>(B.T, c->sverts, c->tri, c->tri_sorted, x, O, CP, CC);
+      LAUNCH_CHECK();
+    }
+    if ((which & 2) && c->E > 1) {
+      k_bp_ee<MODE><<<bp_blocks(c), 256, 0, c->stream>>>(B.T, c->edge, x, B.F, O, CP, CC);
+      LAUNCH_CHECK();
+    }
   }
   CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
@@ -583,14 +739,14 @@ static BpOut table_out(PairTable& t) {
 static void constraint_set(mp_ctx* c, const double* x) {
   c->cur.count = 0;
   if (c->F == 0) return;
-  GridBuild B = build_grid(c, x, c->d_hat);  // gap = d_hat + 2*0
+  BpGrid B = build_bp(c, x, 0.0, c->d_hat);
   ContactParams CP{c->d_hat, c->kappa, c->pinned, KeyCtx{c->new2old, c->id_bits}};
   CcdParams CC{};
   if (c->scratch.d.n < 1024) c->scratch.ensure(1024);
   for (int attempt = 0; attempt < 4; ++attempt) {
     BpOut O = table_out(c->scratch);
     int pen = 0;
-    int64_t n = run_queries<BP_CONTACT>(c, x, B, O, CP, CC, &pen);
+    int64_t n = run_bp<BP_CONTACT>(c, x, B, O, CP, CC, &pen);
     if (pen) throw MpError(MP_ERR_PENETRATION, "contact distance <= 0");
     if (n <= O.cap) {
       sort_table_into(c, c->scratch, c->cur, n);

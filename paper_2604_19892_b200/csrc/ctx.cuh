@@ -69,6 +69,14 @@ struct PairTable {
   }
 };
 
+// dense cell tables of the broad phase (contact.cuh build_bp)
+struct BpGridBufs {
+  DBuf<int> tri_cnt, tri_start, edge_cnt, edge_start, pt_cnt, pt_start;  // (ncell+1)
+  DBuf<int> cells_pt, cells_ee;                                          // work lists
+  DBuf<int> ecell, tri_ent, edge_ent;                                    // (entries)
+  DBuf<int> pcell, pt_ent;                                               // (V)
+};
+
 struct CoarseLevel {
   int A = 0;          // aggregates
   int n = 0;          // 3A dofs
@@ -156,10 +164,10 @@ struct mp_ctx {
   bool have_updates = false;
 
   // ---- broad phase scratch ----
-  DBuf<double> box_lo, box_hi;   // (F+E)*3
-  DBuf<int> cell_cnt, cell_off;
-  DBuf<unsigned long long> cell_key, cell_key2;
-  DBuf<int> cell_prim, cell_prim2;
+  DBuf<double> box_lo, box_hi;   // (F+E)*3 filter / join boxes
+  DBuf<double> box_rlo, box_rhi; // (F+E)*3 raw primitive boxes
+  DBuf<int> cell_cnt, cell_off;  // per-primitive covered-cell counts / offsets
+  BpGridBufs grid;
   DBuf<int> cand_a, cand_b;      // raw broad-phase pairs (taps)
   DBuf<int> counters;            // device counters
   DBuf<double> dscal;            // device scalars

@@ -676,8 +676,7 @@ int mp_broad_phase(mp_ctx* c, const double* x, double motion_bound, double d_hat
     *n_ee = 0;
     if (c->F == 0) return;
     upload_vec_new(c, x, c->x);
-    const double gap = d_hat + 2.0 * motion_bound;
-    GridBuild B = build_grid(c, c->x, gap);
+    BpGrid B = build_bp(c, c->x, motion_bound, d_hat);
     // PT and EE separately so their raw lists stay apart
     for (int pass = 0; pass < 2; ++pass) {
       size_t cap = std::max<size_t>(c->cand_a.n, 4096);
@@ -688,26 +687,10 @@ int mp_broad_phase(mp_ctx* c, const double* x, double motion_bound, double d_hat
         O.a = c->cand_a;
         O.b = c->cand_b;
         O.cap = (int64_t)c->cand_a.n;
-        O.counter = c->counters.p;
-        CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(int), c->stream));
         ContactParams CP{};
         CcdParams CC{};
-        if (pass == 0 && c->V && B.n_tri_keys) {
-          k_query_pt<BP_RAW><<<grid_for(c->V, 128), 128, 0, c->stream>>>(c->V, c->sverts, c->tri, c->tri_sorted,
-                                                                          c->x, B.G, B.tri_keys, B.tri_prim,
-                                                                          B.n_tri_keys, c->box_lo, c->box_hi, O, CP,
-                                                                          CC);
-          LAUNCH_CHECK();
-        }
-        if (pass == 1 && c->E && B.n_edge_keys) {
-          k_query_ee<BP_RAW><<<grid_for(c->E, 128), 128, 0, c->stream>>>(c->E, c->F, c->edge, c->x, B.G,
-                                                                          B.edge_keys, B.edge_prim, B.n_edge_keys,
-                                                                          c->box_lo, c->box_hi, O, CP, CC);
-          LAUNCH_CHECK();
-        }
-        int n = 0;
-        CUDA_CHECK(cudaMemcpyAsync(&n, c->counters.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        sync_stream(c);
+        int64_t n64 = run_bp<BP_RAW>(c, c->x, B, O, CP, CC, nullptr, pass == 0 ? 1 : 2);
+        int n = (int)n64;
         if ((size_t)n > c->cand_a.n) {
           cap = (size_t)n + 1024;
           continue;
