@@ -166,9 +166,14 @@ int mp_precond_apply(mp_ctx* ctx, const double* g, int with_updates, double* z);
 int mp_update_at(mp_ctx* ctx, const double* x, int64_t* n_candidates, int64_t* n_touched);
 
 /* ccd.per_subdomain_steps + certify_mixed + _apply_ccd (ccd.py:221-320,
- * solver.py:268-280): alpha_d (D,), x_new (3N), min alpha, certificate. */
+ * solver.py:268-280): alpha_d (D,), x_new (3N), min alpha, certificate.
+ * exact_set != 0 enumerates (and keeps, for mp_ccd_pairs) the reference's
+ * full candidate set, *n_pairs = its size; exact_set == 0 is the solver's
+ * tight enumeration (same alpha_d / min / certificate, *n_pairs = pairs
+ * enumerated). */
 int mp_ccd(mp_ctx* ctx, const double* x, const double* p, double* alpha_d,
-           double* x_new, double* min_alpha, int32_t* certified, int64_t* n_pairs);
+           double* x_new, double* min_alpha, int32_t* certified, int64_t* n_pairs,
+           int32_t exact_set);
 
 /* The CCD candidate pairs of the last mp_ccd / iteration with their
  * certified steps (ccd.py:244-281 alpha_pair); rows (v,t0,t1,t2) or

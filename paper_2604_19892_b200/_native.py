@@ -105,7 +105,7 @@ def load_library():
     lib.mp_hvp.argtypes = [vp, _f64p, C.c_int, _f64p]
     lib.mp_precond_apply.argtypes = [vp, _f64p, C.c_int, _f64p]
     lib.mp_update_at.argtypes = [vp, _f64p, _i64p, _i64p]
-    lib.mp_ccd.argtypes = [vp, _f64p, _f64p, _f64p, _f64p, _f64p, C.POINTER(C.c_int32), _i64p]
+    lib.mp_ccd.argtypes = [vp, _f64p, _f64p, _f64p, _f64p, _f64p, C.POINTER(C.c_int32), _i64p, C.c_int32]
     lib.mp_stage_timing.argtypes = [vp, C.c_int]
     lib.mp_stage_stats.argtypes = [vp, C.c_int, _f64p, _i64p, _f64p]
     _lib = lib
@@ -311,7 +311,7 @@ class NativeContext:
         self._check(self.lib.mp_update_at(self.h, _ptr(self._vec(x)), C.byref(nc), C.byref(nt)))
         return nc.value, nt.value
 
-    def ccd(self, x, p):
+    def ccd(self, x, p, exact_set=True):
         D, _ = self.partition()
         alpha_d = np.empty(D)
         x_new = np.empty(3 * self.n)
@@ -319,7 +319,7 @@ class NativeContext:
         cert = C.c_int32()
         npairs = C.c_int64()
         self._check(self.lib.mp_ccd(self.h, _ptr(self._vec(x)), _ptr(self._vec(p)), _ptr(alpha_d), _ptr(x_new),
-                                    C.byref(ma), C.byref(cert), C.byref(npairs)))
+                                    C.byref(ma), C.byref(cert), C.byref(npairs), int(bool(exact_set))))
         return alpha_d, x_new, ma.value, bool(cert.value), npairs.value
 
     def ccd_pairs(self):

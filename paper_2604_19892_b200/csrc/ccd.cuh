@@ -97,8 +97,27 @@ __device__ __forceinline__ double ccd_distance(const double X[4][3], bool is_pt)
   return is_pt ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
 }
 
-// pair_steps for one pair (ccd.py:255-281)
-__device__ double ccd_pair_alpha(const double* x, const double* p, const int vid[4], bool is_pt, double alpha_l) {
+// certify_mixed's per-pair test (ccd.py:309-320) on X, P (P = p_mix rows)
+__device__ __forceinline__ bool ccd_cert_test(const double X[4][3], const double P[4][3], bool is_pt, double d,
+                                              double speed, const double* co_or_null) {
+  double lhs = (speed > 0.0) ? RMUL(1.0 - CCD_S, d) : INFINITY;
+  if ((lhs >= speed) && (d > 0.0)) return true;
+  double co[4];
+  if (co_or_null) {
+    co[0] = co_or_null[0]; co[1] = co_or_null[1]; co[2] = co_or_null[2]; co[3] = co_or_null[3];
+  } else {
+    ccd_coeffs(X, P, co);
+  }
+  double w = ccd_window(co);
+  double f1 = RADD(RADD(RADD(co[0], co[1]), co[2]), co[3]);
+  return (w >= 1.0) && (co[3] != 0.0) && (RMUL(f1, co[3]) > 0.0);
+}
+
+// pair_steps for one pair (ccd.py:255-281).  *cert_p: the certify_mixed test
+// of this pair under the UNSCALED p (valid as the certificate when every
+// alpha_d ends up 1, i.e. p_mix == p).
+__device__ double ccd_pair_alpha(const double* x, const double* p, const int vid[4], bool is_pt, double alpha_l,
+                                 bool* cert_p) {
   double X[4][3], P[4][3];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -126,10 +145,27 @@ __device__ double ccd_pair_alpha(const double* x, const double* p, const int vid
     }
     bis = al;
   }
+  if (cert_p) *cert_p = ccd_cert_test(X, P, is_pt, d, speed, co);
   return fmin(fmax(alb, bis), 1.0);
 }
 
-// certify_mixed (ccd.py:297-320): flag[0] cleared when any pair fails
+// certify_mixed for one pair under p_mix = alpha_d[sub] p (ccd.py:297-320)
+__device__ bool ccd_certify_pair(const double* x, const double* p, const double* alpha_d, int bs, const int vid[4],
+                                 bool is_pt) {
+  double X[4][3], P[4][3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double s = alpha_d[vid[a] / bs];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      X[a][k] = x[3 * vid[a] + k];
+      P[a][k] = s * p[3 * vid[a] + k];
+    }
+  }
+  return ccd_cert_test(X, P, is_pt, ccd_distance(X, is_pt), ccd_speed(P, is_pt), nullptr);
+}
+
+// certify_mixed over a stored pair list: *fail set when any pair fails
 __global__ void k_ccd_certify(int64_t n, const int4* __restrict__ verts, const int* __restrict__ is_pt,
                               const double* __restrict__ x, const double* __restrict__ p,
                               const double* __restrict__ alpha_d, int bs, int* __restrict__ fail) {
@@ -137,28 +173,62 @@ __global__ void k_ccd_certify(int64_t n, const int4* __restrict__ verts, const i
   if (i >= n) return;
   int4 v = verts[i];
   const int id[4] = {v.x, v.y, v.z, v.w};
-  double X[4][3], P[4][3];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    double s = alpha_d[id[a] / bs];
+  if (!ccd_certify_pair(x, p, alpha_d, bs, id, is_pt[i] != 0)) atomicExch(fail, 1);
+}
+
+// Tight CCD enumeration bound.  For any constant c, the reference's
+// relative-displacement bound of a pair (ccd.py:172-179) satisfies
+//   speed <= 4 max_a |p_a - c|,
+// so a pair with 0.9 d >= speed -- which gets alpha_pair = 1 exactly and
+// passes certify_mixed's first test -- is any pair whose distance exceeds
+// (4 / 0.9) max_a |p_a - c|.  Inflating every vertex by 4.5 |p_v - c| (c =
+// component midrange) therefore enumerates every pair that can move alpha_d,
+// the global min or the certificate; the reference's own membership test is
+// still applied to each enumerated pair.  s = alpha_d scaling (p_mix) or 1.
+__global__ void k_motion_midrange(int64_t N, int bs, const double* __restrict__ p, const double* __restrict__ alpha_d,
+                                  double* __restrict__ out) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t v = threadIdx.x; v < N; v += blockDim.x) {
+    double s = alpha_d ? alpha_d[v / bs] : 1.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      X[a][k] = x[3 * id[a] + k];
-      P[a][k] = s * p[3 * id[a] + k];
+      double q = s * p[3 * v + k];
+      mn[k] = fmin(mn[k], q);
+      mx[k] = fmax(mx[k], q);
     }
   }
-  const bool pt = is_pt[i] != 0;
-  double d = ccd_distance(X, pt);
-  double speed = ccd_speed(P, pt);
-  double lhs = (speed > 0.0) ? RMUL(1.0 - CCD_S, d) : INFINITY;
-  bool ok = (lhs >= speed) && (d > 0.0);
-  if (ok) return;
-  double co[4];
-  ccd_coeffs(X, P, co);
-  double w = ccd_window(co);
-  double f1 = RADD(RADD(RADD(co[0], co[1]), co[2]), co[3]);
-  bool ok_sign = (w >= 1.0) && (co[3] != 0.0) && (RMUL(f1, co[3]) > 0.0);
-  if (!ok_sign) atomicExch(fail, 1);
+  __shared__ double sh[6][32];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double a = -warp_max(-mn[k]), b = warp_max(mx[k]);
+    if ((threadIdx.x & 31) == 0) {
+      sh[k][threadIdx.x >> 5] = a;
+      sh[3 + k][threadIdx.x >> 5] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double a = INFINITY, b = -INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a = fmin(a, sh[threadIdx.x][w]);
+      b = fmax(b, sh[3 + threadIdx.x][w]);
+    }
+    out[threadIdx.x] = 0.5 * (a + b);
+  }
+}
+
+__global__ void k_motion_infl(int64_t N, int bs, const double* __restrict__ p, const double* __restrict__ alpha_d,
+                              const double* __restrict__ mid, double* __restrict__ infl) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  double s = alpha_d ? alpha_d[v / bs] : 1.0;
+  double r = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double q = s * p[3 * v + k] - mid[k];
+    r += q * q;
+  }
+  infl[v] = 4.5 * sqrt(r) * (1.0 + 1e-12) + 1e-12;
 }
 
 // x_new = x + alpha_d[sub] p   (mixed)  or  x + alpha p  (global)
@@ -181,60 +251,94 @@ struct CcdResult {
   int64_t n_pairs;
 };
 
-// collect_pairs + per_subdomain_steps (+ certify when per_subdomain);
-// leaves alpha_d in c->alpha_d.  x_out receives the clamped position.
+// collect_pairs + per_subdomain_steps (+ certify_mixed when per_subdomain);
+// leaves alpha_d in c->alpha_d; x_out receives the clamped position.
+// exact_set: enumerate the reference's full candidate set and store it (the
+// stage tap); otherwise the tight set (k_motion_infl), which yields the same
+// alpha_d, global min and certificate.
 static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double pinf, bool per_subdomain,
-                           double* x_out) {
+                           double* x_out, bool exact_set = false) {
   CcdResult R{1.0, true, 0};
-  k_fill<<<grid_for(c->D, 256), 256, 0, c->stream>>>(c->alpha_d, c->D, 1.0);
+  cudaStream_t st = c->stream;
+  k_fill<<<grid_for(c->D, 256), 256, 0, st>>>(c->alpha_d, c->D, 1.0);
   LAUNCH_CHECK();
+  double* d_min = c->dscal.p + 41;
+  double* d_mid = c->dscal.p + 44;
+  k_fill<<<1, 32, 0, st>>>(d_min, 1, 1.0);
+  LAUNCH_CHECK();
+  int cert_fail_p = 0;
   if (c->F > 0) {
-    BpGrid B = build_bp(c, x, pinf, 0.0);
+    const double* infl = nullptr;
+    if (!exact_set) {
+      c->infl.ensure(c->N);
+      k_motion_midrange<<<1, 1024, 0, st>>>(c->N, c->bs, p, nullptr, d_mid);
+      LAUNCH_CHECK();
+      k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, nullptr, d_mid, c->infl);
+      LAUNCH_CHECK();
+      infl = c->infl;
+    }
+    BpGrid B = build_bp(c, x, pinf, 0.0, infl);
     ContactParams CP{};
     CcdParams CC{p, c->cfg.alpha_l, c->bs};
-    if (c->ccd_verts.n < 4096) {
+    if (exact_set && c->ccd_verts.n < 4096) {
       c->ccd_verts.ensure(4096); c->ccd_ispt.ensure(4096); c->ccd_alpha.ensure(4096);
     }
     for (int attempt = 0; attempt < 4; ++attempt) {
       BpOut O{};
-      O.verts = c->ccd_verts; O.ccd_ispt = c->ccd_ispt; O.alpha_pair = c->ccd_alpha; O.alpha_d = c->alpha_d;
-      O.cap = (int64_t)c->ccd_verts.n;
-      int64_t n = run_bp<BP_CCD>(c, x, B, O, CP, CC, nullptr);
-      if (n <= O.cap) {
+      if (exact_set) {
+        O.verts = c->ccd_verts; O.ccd_ispt = c->ccd_ispt; O.alpha_pair = c->ccd_alpha;
+        O.cap = (int64_t)c->ccd_verts.n;
+      }
+      O.alpha_d = c->alpha_d;
+      O.min_alpha = d_min;
+      int64_t n = run_bp<BP_CCD>(c, x, B, O, CP, CC, &cert_fail_p);
+      if (!exact_set || n <= O.cap) {
         R.n_pairs = n;
         break;
       }
       size_t cap = (size_t)(n * 1.5) + 4096;
       c->ccd_verts.ensure(cap); c->ccd_ispt.ensure(cap); c->ccd_alpha.ensure(cap);
-      k_fill<<<grid_for(c->D, 256), 256, 0, c->stream>>>(c->alpha_d, c->D, 1.0);
+      k_fill<<<grid_for(c->D, 256), 256, 0, st>>>(c->alpha_d, c->D, 1.0);
+      LAUNCH_CHECK();
+      k_fill<<<1, 32, 0, st>>>(d_min, 1, 1.0);
       LAUNCH_CHECK();
       if (attempt == 3) throw MpError(MP_ERR_CAPACITY, "ccd pair capacity retry failed");
     }
-  }
-  c->n_ccd = R.n_pairs;
-  if (R.n_pairs > 0) {
-    // global min over pairs (deterministic: min is order independent)
-    size_t bytes = 0;
-    cub::DeviceReduce::Min(nullptr, bytes, c->ccd_alpha.p, c->dscal.p, (int)R.n_pairs, c->stream);
-    void* tmp = cub_temp(c, bytes);
-    cub::DeviceReduce::Min(tmp, bytes, c->ccd_alpha.p, c->dscal.p, (int)R.n_pairs, c->stream);
-    LAUNCH_CHECK();
-    CUDA_CHECK(cudaMemsetAsync(c->counters.p + 2, 0, sizeof(int), c->stream));
-    if (per_subdomain) {
-      k_ccd_certify<<<grid_for(R.n_pairs, 128), 128, 0, c->stream>>>(R.n_pairs, c->ccd_verts, c->ccd_ispt, x, p,
-                                                                    c->alpha_d, c->bs, c->counters.p + 2);
-      LAUNCH_CHECK();
-    }
-    CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->dscal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 2, c->counters.p + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(c->h_scal, d_min, sizeof(double), cudaMemcpyDeviceToHost, st));
     sync_stream(c);
     R.min_alpha = c->h_scal[0];
-    R.certified = c->h_cnt[2] == 0;
+    if (per_subdomain && R.n_pairs > 0) {
+      if (R.min_alpha == 1.0) {
+        // every alpha_d is 1: p_mix == p, the certificate was evaluated inline
+        R.certified = cert_fail_p == 0;
+      } else if (exact_set) {
+        CUDA_CHECK(cudaMemsetAsync(c->counters.p + 2, 0, sizeof(int), st));
+        k_ccd_certify<<<grid_for(R.n_pairs, 128), 128, 0, st>>>(R.n_pairs, c->ccd_verts, c->ccd_ispt, x, p,
+                                                                c->alpha_d, c->bs, c->counters.p + 2);
+        LAUNCH_CHECK();
+        CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 2, c->counters.p + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+        sync_stream(c);
+        R.certified = c->h_cnt[2] == 0;
+      } else {
+        k_motion_midrange<<<1, 1024, 0, st>>>(c->N, c->bs, p, c->alpha_d, d_mid);
+        LAUNCH_CHECK();
+        k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, c->alpha_d, d_mid, c->infl);
+        LAUNCH_CHECK();
+        BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl);
+        BpOut O{};
+        O.alpha_d = c->alpha_d;
+        int fail = 0;
+        run_bp<BP_CERT>(c, x, B2, O, CP, CC, &fail);
+        R.certified = fail == 0;
+      }
+    }
   }
+  c->n_ccd = exact_set ? R.n_pairs : 0;
+  c->n_ccd_seen = R.n_pairs;
   if (per_subdomain && R.certified) {
-    k_ccd_update<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, c->bs, x, p, c->alpha_d, 0.0, x_out);
+    k_ccd_update<<<grid_for(3 * c->N, 256), 256, 0, st>>>(c->N, c->bs, x, p, c->alpha_d, 0.0, x_out);
   } else {
-    k_ccd_update<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, c->bs, x, p, nullptr, R.min_alpha, x_out);
+    k_ccd_update<<<grid_for(3 * c->N, 256), 256, 0, st>>>(c->N, c->bs, x, p, nullptr, R.min_alpha, x_out);
   }
   LAUNCH_CHECK();
   return R;

@@ -21,10 +21,20 @@
 #include "ctx.cuh"
 #include "geom.cuh"
 
-enum { BP_RAW = 0, BP_CONTACT = 1, BP_CCD = 2 };
+enum { BP_RAW = 0, BP_CONTACT = 1, BP_CCD = 2, BP_CERT = 3 };
 
 // ---------------------------------------------------------------------------
 // dense cell grid (our own cell size, independent of the reference's)
+//
+// Objects inserted in the grid: triangles [0, F), edges [F, F+E) and surface
+// points [F+E, F+E+V), each with an ENUMERATION box.  Reference mode
+// (infl == nullptr): triangle box = the reference's PT filter box
+// [lo - gap, hi + gap], edge box = the EE join box [lo, hi + gap], point box
+// = the point.  Tight CCD mode (infl != nullptr, per-vertex inflation):
+// every box is the raw box grown by its vertices' largest inflation.  A
+// candidate pair is met in every cell both boxes cover and reported only in
+// the cell of the low corner of the box intersection.  The reference's own
+// membership test is then applied to the pair exactly (queries below).
 
 struct CellGrid {
   double o[3];
@@ -33,7 +43,7 @@ struct CellGrid {
 };
 
 __device__ __forceinline__ int cg_coord(double v, double o, double h, int n) {
-  double q = floor((v - o) / h);  // monotone in v: box tests imply cell hits
+  double q = floor((v - o) / h);  // monotone in v: box overlap implies a shared cell
   if (!(q >= 0.0)) return 0;      // also catches NaN
   if (q > (double)(n - 1)) return n - 1;
   return (int)q;
@@ -41,20 +51,22 @@ __device__ __forceinline__ int cg_coord(double v, double o, double h, int n) {
 
 __device__ __forceinline__ int cg_id(const CellGrid& G, int a, int b, int c) { return (a * G.n[1] + b) * G.n[2] + c; }
 
-// Primitive boxes.  prim < F: triangle; raw box [lo, hi] of its vertices
-// and filter box [lo - gap, hi + gap].  prim >= F: edge; raw box and the
-// join box [lo, hi + gap].  The largest raw-box diagonal (the reference's
-// grid cell candidate, geometry.py:462-465) is max-reduced into *diag_max.
+// Boxes of triangles and edges: raw (rlo, rhi); reference filter (flo, fhi:
+// triangle [lo - gap, hi + gap], edge [lo, hi + gap]); enumeration (elo,
+// ehi).  The largest raw-box diagonal (the reference's grid cell candidate,
+// geometry.py:462-465, same IEEE expression) is max-reduced into *diag_max.
 __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, const int* __restrict__ edge,
-                             const double* __restrict__ x, double gap, double* __restrict__ lo,
-                             double* __restrict__ hi, double* __restrict__ rlo, double* __restrict__ rhi,
+                             const double* __restrict__ x, double gap, const double* __restrict__ infl,
+                             double* __restrict__ rlo, double* __restrict__ rhi, double* __restrict__ flo,
+                             double* __restrict__ fhi, double* __restrict__ elo, double* __restrict__ ehi,
                              double* __restrict__ diag_max) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double dg = 0.0;
   if (i < F + E) {
-    double l[3], h[3];
+    double l[3], h[3], inf = 0.0;
     if (i < F) {
       int a = tri[3 * i], b = tri[3 * i + 1], c = tri[3 * i + 2];
+      if (infl) inf = fmax(fmax(infl[a], infl[b]), infl[c]);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double xa = x[3 * a + k], xb = x[3 * b + k], xc = x[3 * c + k];
@@ -64,6 +76,7 @@ __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, 
     } else {
       int64_t e = i - F;
       int a = edge[2 * e], b = edge[2 * e + 1];
+      if (infl) inf = fmax(infl[a], infl[b]);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double xa = x[3 * a + k], xb = x[3 * b + k];
@@ -76,15 +89,33 @@ __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, 
     for (int k = 0; k < 3; ++k) {
       double dk = RSUB(h[k], l[k]);
       s = (k == 0) ? RMUL(dk, dk) : RADD(s, RMUL(dk, dk));
+      const double fl = (i < F) ? RSUB(l[k], gap) : l[k];
+      const double fh = RADD(h[k], gap);
       rlo[3 * i + k] = l[k];
       rhi[3 * i + k] = h[k];
-      lo[3 * i + k] = (i < F) ? RSUB(l[k], gap) : l[k];
-      hi[3 * i + k] = RADD(h[k], gap);
+      flo[3 * i + k] = fl;
+      fhi[3 * i + k] = fh;
+      elo[3 * i + k] = infl ? l[k] - inf : fl;
+      ehi[3 * i + k] = infl ? h[k] + inf : fh;
     }
     dg = __dsqrt_rn(s);
   }
   dg = warp_max(dg);
   if ((threadIdx.x & 31) == 0) atomic_max_nonneg(diag_max, dg);
+}
+
+// enumeration boxes of the surface points (object ids F+E+q)
+__global__ void k_point_boxes(int64_t V, const int* __restrict__ sverts, const double* __restrict__ x,
+                              const double* __restrict__ infl, double* __restrict__ elo, double* __restrict__ ehi) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= V) return;
+  int v = sverts[q];
+  double e = infl ? infl[v] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    elo[3 * q + k] = x[3 * v + k] - e;
+    ehi[3 * q + k] = x[3 * v + k] + e;
+  }
 }
 
 // stats for the grid: [0..2] min lo, [3..5] max hi, [6] sum of max extents
@@ -129,15 +160,15 @@ __device__ __forceinline__ void box_span(const CellGrid& G, const double* lo, co
   }
 }
 
-// number of grid cells each primitive box covers
-__global__ void k_cell_span(int64_t P, CellGrid G, const double* __restrict__ lo, const double* __restrict__ hi,
+// number of grid cells each object box covers
+__global__ void k_cell_span(int64_t n, CellGrid G, const double* __restrict__ lo, const double* __restrict__ hi,
                             int* __restrict__ cnt) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= P) return;
+  if (i >= n) return;
   int c0[3], c1[3];
   box_span(G, lo + 3 * i, hi + 3 * i, c0, c1);
-  long long n = (long long)(c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
-  cnt[i] = (int)(n > (1 << 30) ? (1 << 30) : n);
+  long long m = (long long)(c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
+  cnt[i] = (int)(m > (1 << 30) ? (1 << 30) : m);
 }
 
 __device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
@@ -149,54 +180,36 @@ __device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
   return l;
 }
 
-// one thread per (primitive, covered cell) entry: its cell id and the
-// per-cell histograms (triangles and edges separately)
-__global__ void k_entry_hist(int64_t total, int64_t P, int64_t F, CellGrid G, const int* __restrict__ off,
-                             const double* __restrict__ lo, const double* __restrict__ hi, int* __restrict__ ecell,
-                             int* __restrict__ tri_cnt, int* __restrict__ edge_cnt) {
+// one thread per (object, covered cell) entry: its cell and the per-class
+// per-cell histograms (class 0 triangles, 1 edges, 2 points)
+__global__ void k_entry_hist(int64_t total, int64_t nobj, int64_t F, int64_t P, CellGrid G,
+                             const int* __restrict__ off, const double* __restrict__ lo, const double* __restrict__ hi,
+                             int* __restrict__ ecell, int* __restrict__ tri_cnt, int* __restrict__ edge_cnt,
+                             int* __restrict__ pt_cnt) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= total) return;
-  int p = upper_bound_i32(off, (int)P + 1, (int)e) - 1;
+  int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
   int r = (int)e - off[p];
   int c0[3], c1[3];
   box_span(G, lo + 3 * (int64_t)p, hi + 3 * (int64_t)p, c0, c1);
   int sx = c1[0] - c0[0] + 1, sy = c1[1] - c0[1] + 1;
-  int a = c0[0] + r % sx, b = c0[1] + (r / sx) % sy, c = c0[2] + r / (sx * sy);
-  int cell = cg_id(G, a, b, c);
+  int cell = cg_id(G, c0[0] + r % sx, c0[1] + (r / sx) % sy, c0[2] + r / (sx * sy));
   ecell[e] = cell;
-  atomicAdd(p < F ? &tri_cnt[cell] : &edge_cnt[cell], 1);
+  atomicAdd(p < F ? &tri_cnt[cell] : (p < P ? &edge_cnt[cell] : &pt_cnt[cell]), 1);
 }
 
-__global__ void k_entry_fill(int64_t total, int64_t P, int64_t F, const int* __restrict__ off,
+__global__ void k_entry_fill(int64_t total, int64_t nobj, int64_t F, int64_t P, const int* __restrict__ off,
                              const int* __restrict__ ecell, const int* __restrict__ tri_start,
-                             const int* __restrict__ edge_start, int* __restrict__ tri_cur,
-                             int* __restrict__ edge_cur, int* __restrict__ tri_ent, int* __restrict__ edge_ent) {
+                             const int* __restrict__ edge_start, const int* __restrict__ pt_start,
+                             int* __restrict__ tri_cur, int* __restrict__ edge_cur, int* __restrict__ pt_cur,
+                             int* __restrict__ tri_ent, int* __restrict__ edge_ent, int* __restrict__ pt_ent) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= total) return;
-  int p = upper_bound_i32(off, (int)P + 1, (int)e) - 1;
+  int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
   int cell = ecell[e];
   if (p < F) tri_ent[tri_start[cell] + atomicAdd(&tri_cur[cell], 1)] = p;
-  else edge_ent[edge_start[cell] + atomicAdd(&edge_cur[cell], 1)] = p - (int)F;
-}
-
-// surface vertices: one cell each
-__global__ void k_point_hist(int64_t V, const int* __restrict__ sverts, const double* __restrict__ x, CellGrid G,
-                             int* __restrict__ pcell, int* __restrict__ pt_cnt) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= V) return;
-  int v = sverts[q];
-  int cell = cg_id(G, cg_coord(x[3 * v], G.o[0], G.h, G.n[0]), cg_coord(x[3 * v + 1], G.o[1], G.h, G.n[1]),
-                   cg_coord(x[3 * v + 2], G.o[2], G.h, G.n[2]));
-  pcell[q] = cell;
-  atomicAdd(&pt_cnt[cell], 1);
-}
-
-__global__ void k_point_fill(int64_t V, const int* __restrict__ pcell, const int* __restrict__ pt_start,
-                             int* __restrict__ pt_cur, int* __restrict__ pt_ent) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= V) return;
-  int cell = pcell[q];
-  pt_ent[pt_start[cell] + atomicAdd(&pt_cur[cell], 1)] = (int)q;
+  else if (p < P) edge_ent[edge_start[cell] + atomicAdd(&edge_cur[cell], 1)] = p - (int)F;
+  else pt_ent[pt_start[cell] + atomicAdd(&pt_cur[cell], 1)] = p - (int)P;
 }
 
 // work lists: cells holding points and triangles; cells holding >= 2 edges
@@ -236,12 +249,13 @@ struct BpOut {
   double* nrm;
   double* grad;
   int* is_pt;
-  // ccd mode
+  // ccd / certificate modes (verts == nullptr: no pair list is stored)
   double* alpha_pair;
   double* alpha_d;
+  double* min_alpha;  // global min over pairs (atomic)
   int* ccd_ispt;
   // common
-  int* counter;    // [0] = emitted, [1] = penetration flag
+  int* counter;    // [0] = reported pairs, [1] = flag (penetration / failed certificate)
   int64_t cap;
 };
 
@@ -296,21 +310,12 @@ struct CcdParams {
   int bs;
 };
 
-__device__ double ccd_pair_alpha(const double* x, const double* p, const int vid[4], bool is_pt, double alpha_l);
+__device__ double ccd_pair_alpha(const double* x, const double* p, const int vid[4], bool is_pt, double alpha_l,
+                                 bool* cert_p);
+__device__ bool ccd_certify_pair(const double* x, const double* p, const double* alpha_d, int bs, const int vid[4],
+                                 bool is_pt);
 
-// one CCD candidate: certified pair step (ccd.py:255-281) into the pair
-// list, min-reduced into its vertices' subdomains (ccd.py:284-294)
-__device__ __forceinline__ void write_ccd(const BpOut& O, const CcdParams& CC, const double* x, int slot,
-                                          const int vid[4], bool is_pt) {
-  O.verts[slot] = make_int4(vid[0], vid[1], vid[2], vid[3]);
-  O.ccd_ispt[slot] = is_pt ? 1 : 0;
-  double al = ccd_pair_alpha(x, CC.p, vid, is_pt, CC.alpha_l);
-  O.alpha_pair[slot] = al;
-  if (al < 1.0) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid[r] / CC.bs], al);
-  }
-}
+
 
 // ---------------------------------------------------------------------------
 // cell-centric queries: one warp per work cell, lanes stride over the cell's
@@ -348,15 +353,69 @@ struct BpTables {
   RefGrid R;
   const int *pt_start, *pt_ent, *tri_start, *tri_ent, *edge_start, *edge_ent;
   const int *cells_pt, *cells_ee, *ncount;
-  const double *lo, *hi, *rlo, *rhi;  // (F+E)*3: filter/join boxes and raw boxes
+  const double *flo, *fhi, *rlo, *rhi;  // (F+E)*3 reference filter / raw boxes
+  const double *elo, *ehi;              // (F+E+V)*3 enumeration boxes
 };
 
-// PT pairs (geometry.py:478-487): points of the cell x triangles whose
-// filter box covers the cell -- each passing pair is met exactly once
+__device__ __forceinline__ bool boxes_meet(const double* al, const double* ah, const double* bl, const double* bh) {
+  return al[0] <= bh[0] && bl[0] <= ah[0] && al[1] <= bh[1] && bl[1] <= ah[1] && al[2] <= bh[2] && bl[2] <= ah[2];
+}
+
+// the pair is reported in exactly one cell: the one holding the low corner
+// of the intersection of the two enumeration boxes
+__device__ __forceinline__ bool owns_corner(const CellGrid& G, int cell, const double* al, const double* bl) {
+  const int cz = cell % G.n[2], cy = (cell / G.n[2]) % G.n[1], cx = cell / (G.n[2] * G.n[1]);
+  return cg_coord(fmax(al[0], bl[0]), G.o[0], G.h, G.n[0]) == cx &&
+         cg_coord(fmax(al[1], bl[1]), G.o[1], G.h, G.n[1]) == cy &&
+         cg_coord(fmax(al[2], bl[2]), G.o[2], G.h, G.n[2]) == cz;
+}
+
+// per-pair work of the non-raw modes
+template <int MODE>
+__device__ __forceinline__ void pair_work(const BpOut& O, const ContactParams& CP, const CcdParams& CC,
+                                          const double* x, bool pass, int type, int vid[4], int vid_ccd[4]) {
+  if (MODE == BP_CONTACT) {
+    double d = 0.0, gr[12];
+    if (pass) {
+      double X[4][3];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
+      d = type ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
+      if (d <= 0.0) O.counter[1] = 1;
+    }
+    const bool emit = pass && d > 0.0 && d < CP.d_hat;
+    int slot = warp_slot(emit, O.counter);
+    if (emit && slot < O.cap) write_contact(O, CP, slot, type, vid, d, gr);
+  } else if (MODE == BP_CCD) {
+    int slot = warp_slot(pass, O.counter);
+    if (pass) {
+      bool cert_p = true;
+      double al = ccd_pair_alpha(x, CC.p, vid_ccd, type != 0, CC.alpha_l, &cert_p);
+      if (al < 1.0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid_ccd[r] / CC.bs], al);
+        atomic_min_nonneg(O.min_alpha, al);
+      }
+      if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
+      if (O.verts && slot < O.cap) {
+        O.verts[slot] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
+        O.ccd_ispt[slot] = type;
+        O.alpha_pair[slot] = al;
+      }
+    }
+  } else if (MODE == BP_CERT) {
+    warp_slot(pass, O.counter);
+    if (pass && !ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, type != 0)) O.counter[1] = 1;
+  }
+}
+
+// PT pairs (geometry.py:478-487)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_bp_pt(BpTables T, const int* __restrict__ sverts, const int* __restrict__ tri,
                                                const int* __restrict__ tri_sorted, const double* __restrict__ x,
-                                               BpOut O, ContactParams CP, CcdParams CC) {
+                                               int64_t PE, BpOut O, ContactParams CP, CcdParams CC) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int ncells = T.ncount[0];
@@ -368,18 +427,24 @@ __global__ void __launch_bounds__(256) k_bp_pt(BpTables T, const int* __restrict
     for (int64_t b0 = 0; b0 < npairs; b0 += 32) {
       const int64_t q = b0 + lane;
       bool pass = false;
-      int v = 0, t = 0;
-      double pv[3] = {0.0, 0.0, 0.0};
+      int v = 0, t = 0, a = 0, b = 0, c = 0;
       if (q < npairs) {
-        v = sverts[T.pt_ent[ps + (int)(q / nt)]];
+        const int qi = T.pt_ent[ps + (int)(q / nt)];
+        v = sverts[qi];
         t = T.tri_ent[ts + (int)(q % nt)];
-        const int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
-        pv[0] = x[3 * v]; pv[1] = x[3 * v + 1]; pv[2] = x[3 * v + 2];
-        const double* l = T.lo + 3 * (int64_t)t;
-        const double* h = T.hi + 3 * (int64_t)t;
-        pass = a != v && b != v && c != v && pv[0] >= l[0] && pv[1] >= l[1] && pv[2] >= l[2] && pv[0] <= h[0] &&
-               pv[1] <= h[1] && pv[2] <= h[2];
-        pass = pass && ref_reach(T.R, pv, pv, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t);
+        a = tri[3 * t]; b = tri[3 * t + 1]; c = tri[3 * t + 2];
+        const double* pl = T.elo + 3 * (PE + qi);
+        const double* ph = T.ehi + 3 * (PE + qi);
+        const double* tl = T.elo + 3 * (int64_t)t;
+        const double* th = T.ehi + 3 * (int64_t)t;
+        pass = a != v && b != v && c != v && boxes_meet(pl, ph, tl, th) && owns_corner(T.G, cell, pl, tl);
+        if (pass) {
+          const double pv[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
+          const double* l = T.flo + 3 * (int64_t)t;
+          const double* h = T.fhi + 3 * (int64_t)t;
+          pass = pv[0] >= l[0] && pv[1] >= l[1] && pv[2] >= l[2] && pv[0] <= h[0] && pv[1] <= h[1] && pv[2] <= h[2];
+          pass = pass && ref_reach(T.R, pv, pv, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t);
+        }
       }
       if (MODE == BP_RAW) {
         int slot = warp_slot(pass, O.counter);
@@ -387,36 +452,20 @@ __global__ void __launch_bounds__(256) k_bp_pt(BpTables T, const int* __restrict
           O.a[slot] = v;
           O.b[slot] = t;
         }
-      } else if (MODE == BP_CONTACT) {
-        // distance against the triangle sorted by original id (contact.py:133-135)
-        double d = 0.0, gr[12];
-        int vid[4] = {v, 0, 0, 0};
-        if (pass) {
-          vid[1] = tri_sorted[3 * t]; vid[2] = tri_sorted[3 * t + 1]; vid[3] = tri_sorted[3 * t + 2];
-          double X0[3], X1[3], X2[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            X0[k] = x[3 * vid[1] + k]; X1[k] = x[3 * vid[2] + k]; X2[k] = x[3 * vid[3] + k];
-          }
-          d = pt_distance(pv, X0, X1, X2, gr);
-          if (d <= 0.0) O.counter[1] = 1;
-        }
-        const bool emit = pass && d > 0.0 && d < CP.d_hat;
-        int slot = warp_slot(emit, O.counter);
-        if (emit && slot < O.cap) write_contact(O, CP, slot, 1, vid, d, gr);
       } else {
-        int slot = warp_slot(pass, O.counter);
-        if (pass && slot < O.cap) {
-          const int vid[4] = {v, tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};  // surface order (ccd.py:229-231)
-          write_ccd(O, CC, x, slot, vid, true);
+        // constraint set: triangle sorted by original id (contact.py:133-135);
+        // CCD: surface order (ccd.py:229-231)
+        int vid[4] = {v, 0, 0, 0}, vid_ccd[4] = {v, a, b, c};
+        if (MODE == BP_CONTACT && q < npairs) {
+          vid[1] = tri_sorted[3 * t]; vid[2] = tri_sorted[3 * t + 1]; vid[3] = tri_sorted[3 * t + 2];
         }
+        pair_work<MODE>(O, CP, CC, x, pass, 1, vid, vid_ccd);
       }
     }
   }
 }
 
-// EE pairs (geometry.py:489-499): all pairs of join boxes sharing the cell,
-// reported only in the cell holding the low corner of their intersection
+// EE pairs (geometry.py:489-499)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_bp_ee(BpTables T, const int* __restrict__ edge, const double* __restrict__ x,
                                                int64_t F, BpOut O, ContactParams CP, CcdParams CC) {
@@ -425,14 +474,14 @@ __global__ void __launch_bounds__(256) k_bp_ee(BpTables T, const int* __restrict
   const int ncells = T.ncount[1];
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ncells; w += nw) {
     const int cell = T.cells_ee[w];
-    const int cz = cell % T.G.n[2], cy = (cell / T.G.n[2]) % T.G.n[1], cx = cell / (T.G.n[2] * T.G.n[1]);
     const int es = T.edge_start[cell];
     const int64_t k = T.edge_start[cell + 1] - es;
     const int64_t npairs = k * (k - 1) / 2;
     for (int64_t b0 = 0; b0 < npairs; b0 += 32) {
       const int64_t q = b0 + lane;
       bool pass = false;
-      int i = 0, j = 0, ia = 0, ib = 0, ja = 0, jb = 0;
+      int i = 0, j = 0;
+      int vid[4] = {0, 0, 0, 0};
       if (q < npairs) {
         // upper-triangle index -> (r, s), r < s
         int64_t r = k - 2 - (int64_t)floor(sqrt((double)(-8 * q + 4 * k * (k - 1) - 7)) / 2.0 - 0.5);
@@ -440,19 +489,21 @@ __global__ void __launch_bounds__(256) k_bp_ee(BpTables T, const int* __restrict
         int e1 = T.edge_ent[es + (int)r], e2 = T.edge_ent[es + (int)s];
         i = min(e1, e2);
         j = max(e1, e2);
-        ia = edge[2 * i]; ib = edge[2 * i + 1]; ja = edge[2 * j]; jb = edge[2 * j + 1];
-        const double* li = T.lo + 3 * (F + i);
-        const double* hi_i = T.hi + 3 * (F + i);
-        const double* lj = T.lo + 3 * (F + j);
-        const double* hj = T.hi + 3 * (F + j);
-        pass = !(ia == ja || ia == jb || ib == ja || ib == jb);
+        vid[0] = edge[2 * i]; vid[1] = edge[2 * i + 1]; vid[2] = edge[2 * j]; vid[3] = edge[2 * j + 1];
+        const double* eli = T.elo + 3 * (F + i);
+        const double* elj = T.elo + 3 * (F + j);
+        pass = !(vid[0] == vid[2] || vid[0] == vid[3] || vid[1] == vid[2] || vid[1] == vid[3]) &&
+               boxes_meet(eli, T.ehi + 3 * (F + i), elj, T.ehi + 3 * (F + j)) && owns_corner(T.G, cell, eli, elj);
+        if (pass) {
+          const double* li = T.flo + 3 * (F + i);
+          const double* hi_i = T.fhi + 3 * (F + i);
+          const double* lj = T.flo + 3 * (F + j);
+          const double* hj = T.fhi + 3 * (F + j);
 #pragma unroll
-        for (int kk = 0; kk < 3; ++kk) pass = pass && (li[kk] <= hj[kk]) && (lj[kk] <= hi_i[kk]);
-        pass = pass && cg_coord(fmax(li[0], lj[0]), T.G.o[0], T.G.h, T.G.n[0]) == cx &&
-               cg_coord(fmax(li[1], lj[1]), T.G.o[1], T.G.h, T.G.n[1]) == cy &&
-               cg_coord(fmax(li[2], lj[2]), T.G.o[2], T.G.h, T.G.n[2]) == cz;
-        pass = pass && ref_reach(T.R, T.rlo + 3 * (F + i), T.rhi + 3 * (F + i), T.rlo + 3 * (F + j),
-                                 T.rhi + 3 * (F + j));
+          for (int kk = 0; kk < 3; ++kk) pass = pass && (li[kk] <= hj[kk]) && (lj[kk] <= hi_i[kk]);
+          pass = pass && ref_reach(T.R, T.rlo + 3 * (F + i), T.rhi + 3 * (F + i), T.rlo + 3 * (F + j),
+                                   T.rhi + 3 * (F + j));
+        }
       }
       if (MODE == BP_RAW) {
         int slot = warp_slot(pass, O.counter);
@@ -460,27 +511,8 @@ __global__ void __launch_bounds__(256) k_bp_ee(BpTables T, const int* __restrict
           O.a[slot] = i;
           O.b[slot] = j;
         }
-      } else if (MODE == BP_CONTACT) {
-        double d = 0.0, gr[12];
-        const int vid[4] = {ia, ib, ja, jb};
-        if (pass) {
-          double A0[3], A1[3], B0[3], B1[3];
-#pragma unroll
-          for (int kk = 0; kk < 3; ++kk) {
-            A0[kk] = x[3 * ia + kk]; A1[kk] = x[3 * ib + kk]; B0[kk] = x[3 * ja + kk]; B1[kk] = x[3 * jb + kk];
-          }
-          d = ee_distance(A0, A1, B0, B1, gr);
-          if (d <= 0.0) O.counter[1] = 1;
-        }
-        const bool emit = pass && d > 0.0 && d < CP.d_hat;
-        int slot = warp_slot(emit, O.counter);
-        if (emit && slot < O.cap) write_contact(O, CP, slot, 0, vid, d, gr);
       } else {
-        int slot = warp_slot(pass, O.counter);
-        if (pass && slot < O.cap) {
-          const int vid[4] = {ia, ib, ja, jb};
-          write_ccd(O, CC, x, slot, vid, false);
-        }
+        pair_work<MODE>(O, CP, CC, x, pass, 0, vid, vid);
       }
     }
   }
@@ -523,29 +555,40 @@ static int bits_for(unsigned long long v) {
 struct BpGrid {
   BpTables T{};
   int ncell = 0;
-  int64_t F = 0;
+  int64_t F = 0, PE = 0;
   bool empty = true;
 };
 
 static void sync_stream(mp_ctx* c) { CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
 
-// Everything one broad-phase call needs at (x, mb, d_hat): boxes, the dense
+// Everything one broad-phase call at (x, mb, d_hat) needs: boxes, the dense
 // cell tables of triangles / edges / surface points and the work lists.
-static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
+// infl (per vertex, device) switches to tight enumeration boxes.
+static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, const double* infl = nullptr) {
   BpGrid B;
   B.F = c->F;
   const int64_t P = c->F + c->E;
+  const int64_t V = c->V;
+  const int64_t nobj = P + V;
+  B.PE = P;
   if (c->F == 0 || P == 0) return B;
   const double gap = d_hat + 2.0 * mb;
   cudaStream_t st = c->stream;
-  c->box_lo.ensure(3 * P); c->box_hi.ensure(3 * P); c->box_rlo.ensure(3 * P); c->box_rhi.ensure(3 * P);
+  for (DBuf<double>* b : {&c->box_rlo, &c->box_rhi, &c->box_flo, &c->box_fhi}) b->ensure(3 * P);
+  c->box_elo.ensure(3 * nobj);
+  c->box_ehi.ensure(3 * nobj);
   CUDA_CHECK(cudaMemsetAsync(c->dscal.p + 40, 0, sizeof(double), st));
-  k_prim_boxes<<<grid_for(P, 256), 256, 0, st>>>(c->F, c->E, c->tri, c->edge, x, gap, c->box_lo, c->box_hi,
-                                                  c->box_rlo, c->box_rhi, c->dscal.p + 40);
+  k_prim_boxes<<<grid_for(P, 256), 256, 0, st>>>(c->F, c->E, c->tri, c->edge, x, gap, infl, c->box_rlo, c->box_rhi,
+                                                  c->box_flo, c->box_fhi, c->box_elo, c->box_ehi, c->dscal.p + 40);
   LAUNCH_CHECK();
+  if (V) {
+    k_point_boxes<<<grid_for(V, 256), 256, 0, st>>>(V, c->sverts, x, infl, c->box_elo.p + 3 * P,
+                                                     c->box_ehi.p + 3 * P);
+    LAUNCH_CHECK();
+  }
   const int nb = 64;
   c->red_part.ensure(7 * nb + 1);
-  k_box_stats<<<nb, 256, 0, st>>>(P, c->box_lo, c->box_hi, c->red_part);
+  k_box_stats<<<nb, 256, 0, st>>>(P, c->box_elo, c->box_ehi, c->red_part);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemcpyAsync(c->red_part.p + 7 * nb, c->dscal.p + 40, sizeof(double), cudaMemcpyDeviceToDevice, st));
   std::vector<double> part(7 * nb + 1);
@@ -563,13 +606,13 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
   B.T.R.cell = fmax(part[7 * nb], d_hat + mb);
   B.T.R.pad = 0.5 * d_hat + mb;
   double span = fmax(fmax(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
-  double h = ext / (double)P;  // mean box extent
+  double h = ext / (double)P;  // mean enumeration-box extent
   if (!(h > 0.0) || !std::isfinite(h)) h = span > 0.0 ? span : 1.0;
   h = fmax(h, span * 1e-6);
   if (!(h > 0.0)) h = 1.0;
-  const double max_cells = fmax(1 << 18, fmin(1 << 24, 16.0 * (double)(P + c->V)));
-  c->cell_cnt.ensure(P + 1);
-  c->cell_off.ensure(P + 1);
+  const double max_cells = fmax(1 << 18, fmin(1 << 24, 16.0 * (double)nobj));
+  c->cell_cnt.ensure(nobj + 1);
+  c->cell_off.ensure(nobj + 1);
   int total = 0, ncell = 0;
   for (int attempt = 0; attempt < 60; ++attempt, h *= 1.5) {
     CellGrid& G = B.T.G;
@@ -584,17 +627,16 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
     }
     if (cells > max_cells) continue;
     ncell = (int)cells;
-    k_cell_span<<<grid_for(P, 256), 256, 0, st>>>(P, G, c->box_lo, c->box_hi, c->cell_cnt);
+    k_cell_span<<<grid_for(nobj, 256), 256, 0, st>>>(nobj, G, c->box_elo, c->box_ehi, c->cell_cnt);
     LAUNCH_CHECK();
-    CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + P, 0, sizeof(int), st));
-    exclusive_scan(c, c->cell_cnt, c->cell_off, P + 1);
-    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 4, c->cell_off.p + P, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + nobj, 0, sizeof(int), st));
+    exclusive_scan(c, c->cell_cnt, c->cell_off, nobj + 1);
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 4, c->cell_off.p + nobj, sizeof(int), cudaMemcpyDeviceToHost, st));
     sync_stream(c);
     total = c->h_cnt[4];
-    if (total >= 0 && (int64_t)total <= 64 * P + 4096) break;
+    if (total >= 0 && (int64_t)total <= 32 * nobj + 4096) break;
   }
   B.ncell = ncell;
-  const int64_t V = c->V;
   auto& g = c->grid;
   for (DBuf<int>* b : {&g.tri_cnt, &g.tri_start, &g.edge_cnt, &g.edge_start, &g.pt_cnt, &g.pt_start})
     b->ensure((size_t)ncell + 1);
@@ -603,18 +645,13 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
   g.ecell.ensure((size_t)total + 1);
   g.tri_ent.ensure((size_t)total + 1);
   g.edge_ent.ensure((size_t)total + 1);
-  g.pcell.ensure(V + 1);
-  g.pt_ent.ensure(V + 1);
+  g.pt_ent.ensure((size_t)total + 1);
   for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * ((size_t)ncell + 1), st));
   CUDA_CHECK(cudaMemsetAsync(c->counters.p + 8, 0, 2 * sizeof(int), st));
   if (total) {
-    k_entry_hist<<<grid_for(total, 256), 256, 0, st>>>(total, P, c->F, B.T.G, c->cell_off, c->box_lo, c->box_hi,
-                                                       g.ecell, g.tri_cnt, g.edge_cnt);
-    LAUNCH_CHECK();
-  }
-  if (V) {
-    k_point_hist<<<grid_for(V, 256), 256, 0, st>>>(V, c->sverts, x, B.T.G, g.pcell, g.pt_cnt);
+    k_entry_hist<<<grid_for(total, 256), 256, 0, st>>>(total, nobj, c->F, P, B.T.G, c->cell_off, c->box_elo,
+                                                       c->box_ehi, g.ecell, g.tri_cnt, g.edge_cnt, g.pt_cnt);
     LAUNCH_CHECK();
   }
   exclusive_scan(c, g.tri_cnt, g.tri_start, ncell + 1);
@@ -624,12 +661,9 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
   for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * ((size_t)ncell + 1), st));
   if (total) {
-    k_entry_fill<<<grid_for(total, 256), 256, 0, st>>>(total, P, c->F, c->cell_off, g.ecell, g.tri_start,
-                                                       g.edge_start, g.tri_cnt, g.edge_cnt, g.tri_ent, g.edge_ent);
-    LAUNCH_CHECK();
-  }
-  if (V) {
-    k_point_fill<<<grid_for(V, 256), 256, 0, st>>>(V, g.pcell, g.pt_start, g.pt_cnt, g.pt_ent);
+    k_entry_fill<<<grid_for(total, 256), 256, 0, st>>>(total, nobj, c->F, P, c->cell_off, g.ecell, g.tri_start,
+                                                       g.edge_start, g.pt_start, g.tri_cnt, g.edge_cnt, g.pt_cnt,
+                                                       g.tri_ent, g.edge_ent, g.pt_ent);
     LAUNCH_CHECK();
   }
   k_cell_lists<<<grid_for(ncell, 256), 256, 0, st>>>(ncell, g.pt_start, g.tri_start, g.edge_start, g.cells_pt,
@@ -640,7 +674,8 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat) {
   T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
   T.edge_start = g.edge_start; T.edge_ent = g.edge_ent;
   T.cells_pt = g.cells_pt; T.cells_ee = g.cells_ee; T.ncount = c->counters.p + 8;
-  T.lo = c->box_lo; T.hi = c->box_hi; T.rlo = c->box_rlo; T.rhi = c->box_rhi;
+  T.flo = c->box_flo; T.fhi = c->box_fhi; T.rlo = c->box_rlo; T.rhi = c->box_rhi;
+  T.elo = c->box_elo; T.ehi = c->box_ehi;
   B.empty = false;
   return B;
 }
@@ -651,16 +686,18 @@ static unsigned bp_blocks(mp_ctx* c) {
   return (unsigned)(sms * 8);  // 8 x 256-thread CTAs per SM, persistent warps
 }
 
-// Run the PT (which & 1) and EE (which & 2) queries in MODE; returns the
-// number of emitted records (may exceed O.cap: caller grows and retries).
+// Run the PT (which & 1) and EE (which & 2) queries in MODE.  Returns the
+// number of reported pairs (may exceed O.cap: the caller grows and retries);
+// *flag = counters[1] (penetration / failed certificate).
 template <int MODE>
 static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
-                      int* penetration, int which = 3) {
+                      int* flag, int which = 3) {
   CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(int), c->stream));
   O.counter = c->counters.p;
   if (!B.empty) {
     if ((which & 1) && c->V) {
-      k_bp_pt<MODE><<<bp_blocks(c), 256, 0, c->stream>>>(B.T, c->sverts, c->tri, c->tri_sorted, x, O, CP, CC);
+      k_bp_pt<MODE><<<bp_blocks(c), 256, 0, c->stream>>>(B.T, c->sverts, c->tri, c->tri_sorted, x, B.PE, O, CP,
+                                                          CC);
       LAUNCH_CHECK();
     }
     if ((which & 2) && c->E > 1) {
@@ -670,7 +707,7 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
   }
   CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
-  if (penetration) *penetration = c->h_cnt[1];
+  if (flag) *flag = c->h_cnt[1];
   return c->h_cnt[0];
 }
 

@@ -73,8 +73,7 @@ struct PairTable {
 struct BpGridBufs {
   DBuf<int> tri_cnt, tri_start, edge_cnt, edge_start, pt_cnt, pt_start;  // (ncell+1)
   DBuf<int> cells_pt, cells_ee;                                          // work lists
-  DBuf<int> ecell, tri_ent, edge_ent;                                    // (entries)
-  DBuf<int> pcell, pt_ent;                                               // (V)
+  DBuf<int> ecell, tri_ent, edge_ent, pt_ent;                            // (entries)
 };
 
 struct CoarseLevel {
@@ -164,8 +163,10 @@ struct mp_ctx {
   bool have_updates = false;
 
   // ---- broad phase scratch ----
-  DBuf<double> box_lo, box_hi;   // (F+E)*3 filter / join boxes
+  DBuf<double> box_flo, box_fhi; // (F+E)*3 reference filter / join boxes
   DBuf<double> box_rlo, box_rhi; // (F+E)*3 raw primitive boxes
+  DBuf<double> box_elo, box_ehi; // (F+E+V)*3 enumeration boxes
+  DBuf<double> infl;             // (N) per-vertex CCD inflation
   DBuf<int> cell_cnt, cell_off;  // per-primitive covered-cell counts / offsets
   BpGridBufs grid;
   DBuf<int> cand_a, cand_b;      // raw broad-phase pairs (taps)
@@ -189,7 +190,8 @@ struct mp_ctx {
   DBuf<int> ccd_ispt;
   DBuf<double> ccd_alpha;   // per pair
   DBuf<double> alpha_d;     // (D)
-  int64_t n_ccd = 0;
+  int64_t n_ccd = 0;        // stored pair list length (exact-set taps)
+  int64_t n_ccd_seen = 0;   // pairs enumerated by the last CCD
 
   // pinned host staging for scalars
   double* h_scal = nullptr;

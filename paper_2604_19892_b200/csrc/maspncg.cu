@@ -433,7 +433,7 @@ static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
     rec.t_dir_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
     rec.t_ccd_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
     rec.n_candidates = (int32_t)(rebuild ? 0 : c->n_cand);
-    rec.n_ccd_pairs = (int32_t)c->n_ccd;
+    rec.n_ccd_pairs = (int32_t)c->n_ccd_seen;
     const bool converged_now = z_norm <= cfg.eps;
     if (converged_now && (restart || full_every)) {
       R.recs.push_back(rec);
@@ -815,7 +815,7 @@ int mp_update_at(mp_ctx* c, const double* x, int64_t* n_candidates, int64_t* n_t
 }
 
 int mp_ccd(mp_ctx* c, const double* x, const double* p, double* alpha_d, double* x_new, double* min_alpha,
-           int32_t* certified, int64_t* n_pairs) {
+           int32_t* certified, int64_t* n_pairs, int32_t exact_set) {
   return guarded(c, [&] {
     upload_vec_new(c, x, c->x);
     upload_vec_new(c, p, c->p);
@@ -823,7 +823,7 @@ int mp_ccd(mp_ctx* c, const double* x, const double* p, double* alpha_d, double*
     const int64_t n3 = 3 * c->N;
     double pinf = 0.0;
     for (int64_t i = 0; i < n3; ++i) pinf = std::max(pinf, std::fabs(p[i]));
-    CcdResult R = ccd_clamp(c, c->x, c->p, pinf, c->cfg.ccd_per_subdomain != 0, c->tmp);
+    CcdResult R = ccd_clamp(c, c->x, c->p, pinf, c->cfg.ccd_per_subdomain != 0, c->tmp, exact_set != 0);
     if (alpha_d)
       CUDA_CHECK(cudaMemcpyAsync(alpha_d, c->alpha_d.p, c->D * 8, cudaMemcpyDeviceToHost, c->stream));
     download_vec_old(c, c->tmp, x_new);
