@@ -126,14 +126,23 @@ __device__ double ccd_pair_alpha(const double* x, const double* p, const int vid
       X[a][k] = x[3 * vid[a] + k];
       P[a][k] = p[3 * vid[a] + k];
     }
-  double co[4];
-  ccd_coeffs(X, P, co);
   double d = ccd_distance(X, is_pt);
   double speed = ccd_speed(P, is_pt);
   const double one_s = 1.0 - CCD_S;
   double lb = (speed > 0.0) ? RDIV(RMUL(one_s, d), speed) : INFINITY;
   if (!(d > 0.0)) lb = 0.0;
   double alb = fmin(lb, 1.0);
+  // alb == 1: alpha_hat <= 1 rules the bisection out, alpha_pair = 1, and the
+  // cubic is only needed if certify_mixed's distance test fails
+  if (alb >= 1.0) {
+    if (cert_p) {
+      double lhs = (speed > 0.0) ? RMUL(one_s, d) : INFINITY;
+      *cert_p = ((lhs >= speed) && (d > 0.0)) ? true : ccd_cert_test(X, P, is_pt, d, speed, nullptr);
+    }
+    return 1.0;
+  }
+  double co[4];
+  ccd_coeffs(X, P, co);
   double ahat = fmin(1.0, ccd_window(co));
   double bis = 0.0;
   if (alb < ahat && co[3] != 0.0) {

@@ -166,6 +166,98 @@ __global__ void k_mas_factor(int64_t D, int64_t N, int bs, int m, const double* 
   store_cyc_sym(X, m, Bblk + d * cyc_size(m), true);
 }
 
+// One CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
+// (mas.py:84-90).  The inverse is formed by the symmetric sweep operator
+// (Gauss-Jordan without pivoting, stable for SPD): after sweeping every
+// pivot the matrix holds -M^-1.  Its pivots are the Schur-complement
+// diagonals, i.e. the squared Cholesky pivots, so "pivot <= 0" is exactly
+// cho_factor's non-SPD failure.  The m x m matrix lives in registers, a
+// 6 x 6 tile per thread on a 16 x 16 thread grid (m <= 96); each step
+// broadcasts the old pivot row through shared memory (double-buffered, one
+// barrier per step).  Symmetry is preserved bit-exactly (every update uses
+// the same products), so the row is also the pivot column.
+#define SWEEP_T 6
+__global__ void __launch_bounds__(256, 2)
+k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull, double* __restrict__ Mblk,
+            double* __restrict__ Bblk, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* S = sm;                 // m*m staging
+  double* rowk = sm + m * m;      // 2 x 96 broadcast rows
+  const int64_t d = blockIdx.x;
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  const int nd = (int)((N - d * bs) < bs ? (N - d * bs) : bs);
+  const double* src = Mfull + d * (int64_t)m * m;
+  for (int e = tid; e < m * m; e += blockDim.x) {
+    int i = e / m, j = e - (e / m) * m;
+    double v = src[e];
+    if (i >= 3 * nd || j >= 3 * nd) v = (i == j) ? 1.0 : 0.0;
+    S[e] = v;
+  }
+  for (int e = tid; e < 2 * 96; e += blockDim.x) rowk[e] = 0.0;
+  __syncthreads();
+  store_cyc_sym(S, m, Mblk + d * cyc_size(m), false);
+  double R[SWEEP_T][SWEEP_T];
+#pragma unroll
+  for (int a = 0; a < SWEEP_T; ++a)
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b) {
+      int i = tr + 16 * a, j = tc + 16 * b;
+      R[a][b] = (i < m && j < m) ? S[i * m + j] : 0.0;
+    }
+  bool bad = false;
+  for (int k = 0; k < m; ++k) {
+    double* rk = rowk + (k & 1) * 96;
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a)
+      if (tr + 16 * a == k) {
+#pragma unroll
+        for (int b = 0; b < SWEEP_T; ++b)
+          if (tc + 16 * b < m) rk[tc + 16 * b] = R[a][b];
+      }
+    __syncthreads();
+    const double piv = rk[k];
+    if (!(piv > 0.0)) {
+      bad = true;  // uniform across the CTA
+      break;
+    }
+    const double inv = 1.0 / piv;
+    double ci[SWEEP_T], cj[SWEEP_T];
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a) {
+      ci[a] = rk[min(tr + 16 * a, 95)] * inv;
+      cj[a] = rk[min(tc + 16 * a, 95)];
+    }
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a) {
+      const int i = tr + 16 * a;
+#pragma unroll
+      for (int b = 0; b < SWEEP_T; ++b) {
+        const int j = tc + 16 * b;
+        double r = R[a][b];
+        if (i != k && j != k) r = fma(-ci[a], cj[b], r);
+        else if (i == k && j == k) r = -inv;
+        else if (i == k) r = cj[b] * inv;
+        else r = ci[a];
+        R[a][b] = r;
+      }
+    }
+  }
+  if (bad) {
+    if (tid == 0) atomicExch(status, 1);
+    return;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < SWEEP_T; ++a)
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b) {
+      int i = tr + 16 * a, j = tc + 16 * b;
+      if (i < m && j < m) S[i * m + j] = -R[a][b];
+    }
+  __syncthreads();
+  store_cyc_sym(S, m, Bblk + d * cyc_size(m), true);
+}
+
 // ---------------------------------------------------------------------------
 // coarse levels
 

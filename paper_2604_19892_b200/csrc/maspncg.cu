@@ -134,6 +134,7 @@ static void set_smem_limits() {
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
   };
   allow((const void*)k_mas_factor);
+  allow((const void*)k_mas_sweep);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
   allow((const void*)k_mas_apply_l0);

@@ -103,9 +103,9 @@ static void mas_build(mp_ctx* c) {
   k_bsr_to_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, c->bs, m, c->Mfull);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, sizeof(int), c->stream));
-  const size_t smem = sizeof(double) * 2 * m * m;
-  k_mas_factor<<<(unsigned)D, 256, smem, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
-                                                       c->counters.p + 3);
+  const size_t smem = sizeof(double) * ((size_t)m * m + 2 * 96);
+  k_mas_sweep<<<(unsigned)D, 256, smem, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
+                                                      c->counters.p + 3);
   LAUNCH_CHECK();
   if (read_status(c, c->counters.p + 3)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
   for (int l = 0; l < c->n_levels; ++l) {
