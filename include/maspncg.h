@@ -101,7 +101,10 @@ typedef struct mp_iter_record {
   double t_dir_ms;
   double t_ccd_ms;
   int32_t n_candidates;    /* rank-one update candidates (non-rebuild)    */
-  int32_t n_ccd_pairs;     /* CCD candidate pairs                         */
+  int32_t n_ccd_pairs;     /* CCD candidate pairs enumerated              */
+  int32_t ccd_certified;   /* certify_mixed outcome (1 = mixed step kept) */
+  int32_t pad_;
+  double energy;           /* incremental potential at the iterate (NaN unless enabled) */
 } mp_iter_record;
 
 #define MP_FLAG_NOT_CONVERGED 1u
@@ -200,6 +203,13 @@ enum {
   MP_STAGE_COUNT = 8
 };
 int mp_stage_timing(mp_ctx* ctx, int enable);
+
+/* Solver options beyond SolverConfig.  MP_OPT_CCD_EXACT_SET: enumerate the
+ * reference's full CCD candidate set inside the loop (default 0: the tight
+ * set, same results).  MP_OPT_RECORD_ENERGY: evaluate the incremental
+ * potential at every iterate into mp_iter_record.energy (default 0). */
+enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2 };
+int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 
 /* Message of the last failed mp_create on this thread. */

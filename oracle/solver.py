@@ -129,6 +129,7 @@ class Record:
     nu: float
     min_alpha: float
     energy: float = float("nan")
+    certified: bool = True
 
 
 @dataclass
@@ -199,11 +200,12 @@ def advance(scene, x, x_tilde, h, cfg: SolverConfig, deadline=None, with_energy=
                 mu, nu = zg / zv, 0.0
                 p, Hp = -mu * z, -mu * v
         energy = ophys.incremental_potential(scene, x, x_tilde, h, cs) if with_energy else float("nan")
+        cert = True
         if np.any(p):
-            x, min_alpha, _, _, _ = occd.clamp(scene, part, x, p, cfg.ccd_per_subdomain, cfg.alpha_l)
+            x, min_alpha, _, cert, _ = occd.clamp(scene, part, x, p, cfg.ccd_per_subdomain, cfg.alpha_l)
         else:
             min_alpha = 1.0
-        rec = Record(k, g_norm, z_norm, 0.0, restart, float(mu), float(nu), float(min_alpha), energy)
+        rec = Record(k, g_norm, z_norm, 0.0, restart, float(mu), float(nu), float(min_alpha), energy, bool(cert))
         tr.records.append(rec)
         conv = z_norm <= cfg.eps
         if conv and (restart or full):

@@ -47,13 +47,14 @@ class IterRecordC(C.Structure):
         ("restart", C.c_int32), ("n_contacts", C.c_int32), ("mu", C.c_double), ("nu", C.c_double),
         ("min_alpha", C.c_double), ("t_grad_ms", C.c_double), ("t_dir_ms", C.c_double),
         ("t_ccd_ms", C.c_double), ("n_candidates", C.c_int32), ("n_ccd_pairs", C.c_int32),
+        ("ccd_certified", C.c_int32), ("pad_", C.c_int32), ("energy", C.c_double),
     ]
 
 
 EXPORTS = (
     "mp_create", "mp_destroy", "mp_set_config", "mp_status_code", "mp_last_error", "mp_stream", "mp_partition",
     "mp_step", "mp_advance", "mp_broad_phase", "mp_constraint_set", "mp_gradient", "mp_energy", "mp_snapshot",
-    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_launch_count", "mp_stage_timing", "mp_stage_stats",
+    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
 )
 
 STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd")
@@ -107,6 +108,7 @@ def load_library():
     lib.mp_update_at.argtypes = [vp, _f64p, _i64p, _i64p]
     lib.mp_ccd.argtypes = [vp, _f64p, _f64p, _f64p, _f64p, _f64p, C.POINTER(C.c_int32), _i64p, C.c_int32]
     lib.mp_stage_timing.argtypes = [vp, C.c_int]
+    lib.mp_set_option.argtypes = [vp, C.c_int, C.c_int64]
     lib.mp_stage_stats.argtypes = [vp, C.c_int, _f64p, _i64p, _f64p]
     _lib = lib
     return lib
@@ -243,6 +245,10 @@ class NativeContext:
         self._check(self.lib.mp_step_device(self.h, C.c_double(h), recs, cap, C.byref(n), C.byref(conv),
                                             C.byref(flags)))
         return [recs[i] for i in range(min(n.value, cap))], bool(conv.value), int(flags.value)
+
+    def set_option(self, option, value):
+        """MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2 (include/maspncg.h)."""
+        self._check(self.lib.mp_set_option(self.h, int(option), int(value)))
 
     # ---- per-stage CUDA-event timing ----
     def stage_timing(self, enable=True):

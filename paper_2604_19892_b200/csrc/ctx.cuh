@@ -102,6 +102,8 @@ struct StageTimer {
 struct mp_ctx {
   int device = 0;
   bool timing = false;
+  bool ccd_exact_set = false;
+  bool record_energy = false;
   StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;

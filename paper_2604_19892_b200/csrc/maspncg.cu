@@ -411,11 +411,14 @@ static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
     }
     auto t2 = Clock::now();
     double min_alpha = 1.0;
+    bool certified = true;
+    const double e_iter = c->record_energy ? energy(c, c->x, c->xt, h) : NAN;
     if (pinf > 0.0) {
       timer_begin(c, MP_STAGE_CCD);
-      CcdResult cr = ccd_clamp(c, c->x, c->p, pinf, cfg.ccd_per_subdomain != 0, c->tmp);
+      CcdResult cr = ccd_clamp(c, c->x, c->p, pinf, cfg.ccd_per_subdomain != 0, c->tmp, c->ccd_exact_set);
       timer_end(c, MP_STAGE_CCD, 0.0);
       min_alpha = cr.min_alpha;
+      certified = cr.certified;
       std::swap(c->x.p, c->tmp.p);
     }
     sync_stream(c);
@@ -435,6 +438,8 @@ static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
     rec.t_ccd_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
     rec.n_candidates = (int32_t)(rebuild ? 0 : c->n_cand);
     rec.n_ccd_pairs = (int32_t)c->n_ccd_seen;
+    rec.ccd_certified = certified ? 1 : 0;
+    rec.energy = e_iter;
     const bool converged_now = z_norm <= cfg.eps;
     if (converged_now && (restart || full_every)) {
       R.recs.push_back(rec);
@@ -535,6 +540,14 @@ int mp_stage_timing(mp_ctx* c, int enable) {
       t.count = 0;
     }
     c->timing = enable != 0;
+  });
+}
+
+int mp_set_option(mp_ctx* c, int option, int64_t value) {
+  return guarded(c, [&] {
+    if (option == MP_OPT_CCD_EXACT_SET) c->ccd_exact_set = value != 0;
+    else if (option == MP_OPT_RECORD_ENERGY) c->record_energy = value != 0;
+    else throw MpError(MP_ERR_CONFIG, "unknown option");
   });
 }
 

@@ -164,6 +164,8 @@ class IterRecord:
     n_contacts: int = 0
     n_candidates: int = 0
     n_ccd_pairs: int = 0
+    ccd_certified: bool = True
+    energy: float = float("nan")
 
 
 @dataclass
@@ -184,6 +186,7 @@ def _trace(recs, converged, flags) -> SolverTrace:
             k=int(r.k), grad_norm=r.grad_norm, z_norm=r.z_norm, r=r.r, restart=bool(r.restart), mu=r.mu,
             nu=r.nu, min_alpha=r.min_alpha, t_grad_ms=r.t_grad_ms, t_dir_ms=r.t_dir_ms, t_ccd_ms=r.t_ccd_ms,
             n_contacts=int(r.n_contacts), n_candidates=int(r.n_candidates), n_ccd_pairs=int(r.n_ccd_pairs),
+            ccd_certified=bool(r.ccd_certified), energy=float(r.energy),
         ))
     if flags & 1:
         out.flags.append("not-converged")
