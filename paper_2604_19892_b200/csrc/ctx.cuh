@@ -9,6 +9,7 @@
 // reference's B_d dof order (ascending original id, mas.py:74).
 #pragma once
 
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <string>
@@ -107,6 +108,7 @@ struct mp_ctx {
   StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
+  cublasHandle_t blas = nullptr;
   std::string last_error;
   int64_t launches = 0;
 
@@ -183,6 +185,7 @@ struct mp_ctx {
   std::vector<CoarseLevel*> levels;
   int n_levels = 0;
   DBuf<double> solver_work;
+  DBuf<double> dn_col, dn_W, dn_P;   // blocked dense sweep scratch
   DBuf<int> solver_info;
   bool have_snapshot = false;
   bool have_mas = false;

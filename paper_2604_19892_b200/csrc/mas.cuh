@@ -177,25 +177,14 @@ __global__ void k_mas_factor(int64_t D, int64_t N, int bs, int m, const double* 
 // barrier per step).  Symmetry is preserved bit-exactly (every update uses
 // the same products), so the row is also the pivot column.
 #define SWEEP_T 6
-__global__ void __launch_bounds__(256, 2)
-k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull, double* __restrict__ Mblk,
-            double* __restrict__ Bblk, int* __restrict__ status) {
-  extern __shared__ double sm[];
-  double* S = sm;                 // m*m staging
-  double* rowk = sm + m * m;      // 2 x 96 broadcast rows
-  const int64_t d = blockIdx.x;
+
+// Sweep every pivot of the m x m (m <= 96) symmetric matrix staged in smem
+// S (row-major); on return S holds -S^-1.  rowk: 2 x 96 smem scratch.
+// Returns false (uniformly) when a pivot is not positive.
+__device__ bool sweep_core(double* S, int m, double* rowk) {
   const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
-  const int nd = (int)((N - d * bs) < bs ? (N - d * bs) : bs);
-  const double* src = Mfull + d * (int64_t)m * m;
-  for (int e = tid; e < m * m; e += blockDim.x) {
-    int i = e / m, j = e - (e / m) * m;
-    double v = src[e];
-    if (i >= 3 * nd || j >= 3 * nd) v = (i == j) ? 1.0 : 0.0;
-    S[e] = v;
-  }
   for (int e = tid; e < 2 * 96; e += blockDim.x) rowk[e] = 0.0;
   __syncthreads();
-  store_cyc_sym(S, m, Mblk + d * cyc_size(m), false);
   double R[SWEEP_T][SWEEP_T];
 #pragma unroll
   for (int a = 0; a < SWEEP_T; ++a)
@@ -204,7 +193,6 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mful
       int i = tr + 16 * a, j = tc + 16 * b;
       R[a][b] = (i < m && j < m) ? S[i * m + j] : 0.0;
     }
-  bool bad = false;
   for (int k = 0; k < m; ++k) {
     double* rk = rowk + (k & 1) * 96;
 #pragma unroll
@@ -216,10 +204,7 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mful
       }
     __syncthreads();
     const double piv = rk[k];
-    if (!(piv > 0.0)) {
-      bad = true;  // uniform across the CTA
-      break;
-    }
+    if (!(piv > 0.0)) return false;  // uniform across the CTA
     const double inv = 1.0 / piv;
     double ci[SWEEP_T], cj[SWEEP_T];
 #pragma unroll
@@ -242,20 +227,87 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mful
       }
     }
   }
-  if (bad) {
-    if (tid == 0) atomicExch(status, 1);
-    return;
-  }
   __syncthreads();
 #pragma unroll
   for (int a = 0; a < SWEEP_T; ++a)
 #pragma unroll
     for (int b = 0; b < SWEEP_T; ++b) {
       int i = tr + 16 * a, j = tc + 16 * b;
-      if (i < m && j < m) S[i * m + j] = -R[a][b];
+      if (i < m && j < m) S[i * m + j] = R[a][b];
     }
   __syncthreads();
+  return true;
+}
+
+// One CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
+// (mas.py:84-90).  The inverse is formed by the symmetric sweep operator
+// (Gauss-Jordan without pivoting, stable for SPD): after sweeping every
+// pivot the matrix holds -M^-1.  Its pivots are the Schur-complement
+// diagonals, i.e. the squared Cholesky pivots, so "pivot <= 0" is exactly
+// cho_factor's non-SPD failure.  The m x m matrix lives in registers, a
+// 6 x 6 tile per thread on a 16 x 16 thread grid (m <= 96); each step
+// broadcasts the old pivot row through shared memory (double-buffered, one
+// barrier per step).  Symmetry is preserved bit-exactly (every update uses
+// the same products), so the row is also the pivot column.
+__global__ void __launch_bounds__(256, 2)
+k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull, double* __restrict__ Mblk,
+            double* __restrict__ Bblk, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* S = sm;                 // m*m staging
+  double* rowk = sm + m * m;      // 2 x 96 broadcast rows
+  const int64_t d = blockIdx.x;
+  const int nd = (int)((N - d * bs) < bs ? (N - d * bs) : bs);
+  const double* src = Mfull + d * (int64_t)m * m;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    int i = e / m, j = e - (e / m) * m;
+    double v = src[e];
+    if (i >= 3 * nd || j >= 3 * nd) v = (i == j) ? 1.0 : 0.0;
+    S[e] = v;
+  }
+  __syncthreads();
+  store_cyc_sym(S, m, Mblk + d * cyc_size(m), false);
+  if (!sweep_core(S, m, rowk)) {
+    if (threadIdx.x == 0) atomicExch(status, 1);
+    return;
+  }
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = -S[e];
+  __syncthreads();
   store_cyc_sym(S, m, Bblk + d * cyc_size(m), true);
+}
+
+// Pivot block of the blocked dense sweep: out (kb x kb) = -P^-1 for the
+// diagonal block P = A[k0:k0+kb, k0:k0+kb] of the n x n matrix A (lda = n).
+__global__ void __launch_bounds__(256, 1)
+k_block_sweep(int kb, const double* __restrict__ A, int lda, int k0, double* __restrict__ out,
+              int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* S = sm;
+  double* rowk = sm + kb * kb;
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    int i = e / kb, j = e - (e / kb) * kb;
+    S[e] = A[(int64_t)(k0 + j) * lda + k0 + i];
+  }
+  __syncthreads();
+  if (!sweep_core(S, kb, rowk)) {
+    if (threadIdx.x == 0) atomicExch(status, 1);
+    return;
+  }
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) out[e] = S[e];
+}
+
+// after the rank-kb update: block column/row K <- W (= A_iK P^-1), A_KK <- -P^-1
+__global__ void k_block_fix(int n, int kb, int k0, const double* __restrict__ W, const double* __restrict__ Pm,
+                            double* __restrict__ A) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * kb) return;
+  int i = (int)(e % n), c = (int)(e / n);  // W is n x kb column-major
+  double w = W[e];
+  if (i >= k0 && i < k0 + kb) {
+    A[(int64_t)(k0 + c) * n + i] = Pm[(i - k0) * kb + c];
+  } else {
+    A[(int64_t)(k0 + c) * n + i] = w;  // A[i, k0+c]
+    A[(int64_t)i * n + k0 + c] = w;    // A[k0+c, i]
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -317,6 +369,17 @@ __global__ void k_sym_lower(int n, double* M) {
 }
 
 // pack the symmetric inverse whose valid half is potri's (lower, column-major)
+// pack sym(-A) (A = -M^-1 after the blocked sweep) in the cyclic layout
+__global__ void k_pack_neg_sym(int n, const double* __restrict__ A, double* __restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= cyc_size(n)) return;
+  int s = (int)(e / n);
+  int i = (int)(e - (int64_t)s * n);
+  int j = i + s;
+  if (j >= n) j -= n;
+  out[e] = -0.5 * (A[(int64_t)j * n + i] + A[(int64_t)i * n + j]);
+}
+
 __global__ void k_pack_coarse(int n, const double* __restrict__ M, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= cyc_size(n)) return;

@@ -23,6 +23,7 @@ mp_ctx::~mp_ctx() {
     if (t.b) cudaEventDestroy(t.b);
   }
   if (solver) cusolverDnDestroy(solver);
+  if (blas) cublasDestroy(blas);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -135,6 +136,7 @@ static void set_smem_limits() {
   };
   allow((const void*)k_mas_factor);
   allow((const void*)k_mas_sweep);
+  allow((const void*)k_block_sweep);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
   allow((const void*)k_mas_apply_l0);
@@ -149,6 +151,8 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cusolverDnCreate");
   cusolverDnSetStream(c->solver, c->stream);
+  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate");
+  cublasSetStream(c->blas, c->stream);
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
   CUDA_CHECK(cudaMallocHost(&c->h_cnt, 16 * sizeof(int)));

@@ -88,6 +88,46 @@ static int read_status(mp_ctx* c, int* dev) {
   return h;
 }
 
+// sym(A^-1) of a dense SPD n x n matrix (column-major, both halves valid),
+// packed in the cyclic layout -- the coarse-level _spd_inverse (mas.py:84-90,
+// :167).  Blocked symmetric sweep: for each 96-wide pivot block K,
+//   P^-1 by the in-smem sweep (k_block_sweep, non-SPD pivots flagged),
+//   W = A[:,K] P^-1 (DGEMM), A -= W A[:,K]^T (rank-96 DGEMM update),
+//   A[:,K] = A[K,:]^T = W, A[K,K] = -P^-1 (k_block_fix);
+// after every block A = -M^-1.  cuBLAS DGEMM carries the O(n^3) work.
+static void dense_spd_inverse(mp_ctx* c, int n, double* A, double* packed) {
+  const int nb = 96;
+  cudaStream_t st = c->stream;
+  c->dn_col.ensure((size_t)n * nb);
+  c->dn_W.ensure((size_t)n * nb);
+  c->dn_P.ensure((size_t)nb * nb);
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 5, 0, sizeof(int), st));
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  for (int k0 = 0; k0 < n; k0 += nb) {
+    const int kb = std::min(nb, n - k0);
+    k_block_sweep<<<1, 256, sizeof(double) * ((size_t)kb * kb + 2 * 96), st>>>(kb, A, n, k0, c->dn_P,
+                                                                                c->counters.p + 5);
+    LAUNCH_CHECK();
+    CUDA_CHECK(cudaMemcpyAsync(c->dn_col.p, A + (size_t)k0 * n, sizeof(double) * (size_t)n * kb,
+                               cudaMemcpyDeviceToDevice, st));
+    // W = -colK * (-P^-1)
+    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, kb, kb, &mone, c->dn_col, n, c->dn_P, kb, &zero,
+                    c->dn_W, n) != CUBLAS_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, "cublasDgemm (coarse W)");
+    // A -= W colK^T
+    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_T, n, n, kb, &mone, c->dn_W, n, c->dn_col, n, &one, A, n) !=
+        CUBLAS_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, "cublasDgemm (coarse update)");
+    c->launches += 2;
+    k_block_fix<<<grid_for((int64_t)n * kb, 256), 256, 0, st>>>(n, kb, k0, c->dn_W, c->dn_P, A);
+    LAUNCH_CHECK();
+  }
+  (void)one;
+  k_pack_neg_sym<<<grid_for(cyc_size(n), 256), 256, 0, st>>>(n, A, packed);
+  LAUNCH_CHECK();
+  if (read_status(c, c->counters.p + 5)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
+}
+
 // build_hierarchy (mas.py:138-179) from the BSR + base contacts
 static void mas_build(mp_ctx* c) {
   const int m = c->m;
@@ -121,27 +161,8 @@ static void mas_build(mp_ctx* c) {
     }
     k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, c->stream>>>(L.n, L.dense);
     LAUNCH_CHECK();
-    int lwork = 0;
-    if (cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, &lwork) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, "cusolver potrf buffer");
-    int lwork2 = 0;
-    if (cusolverDnDpotri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, &lwork2) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, "cusolver potri buffer");
-    c->solver_work.ensure((size_t)std::max(lwork, lwork2) + 1);
-    if (cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, c->solver_work, lwork,
-                         c->solver_info) != CUSOLVER_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, "cusolver potrf");
-    ++c->launches;
-    if (read_status(c, c->solver_info)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
-    if (cusolverDnDpotri(c->solver, CUBLAS_FILL_MODE_LOWER, L.n, L.dense, L.n, c->solver_work, lwork2,
-                         c->solver_info) != CUSOLVER_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, "cusolver potri");
-    ++c->launches;
     L.inv.ensure((size_t)cyc_size(L.n));
-    k_pack_coarse<<<grid_for(cyc_size(L.n), 256), 256, 0, c->stream>>>(L.n, L.dense, L.inv);
-    LAUNCH_CHECK();
+    dense_spd_inverse(c, L.n, L.dense, L.inv);
   }
   c->have_mas = true;
 }
