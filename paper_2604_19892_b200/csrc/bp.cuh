@@ -1,0 +1,728 @@
+// bp.cuh -- broad phase (geometry.py:443-503) on a hierarchical grid, fused
+// with the per-pair work of its three callers (constraint set, CCD steps,
+// certificate).
+//
+// Membership is the reference's, applied exactly to every enumerated pair:
+//   PT (v, t):  v not in t and lo_t - gap <= x_v <= hi_t + gap (componentwise)
+//   EE (i, j):  i < j, no shared vertex, lo_i <= hi_j + gap, lo_j <= hi_i + gap
+// with gap = d_hat + 2 mb, AND the reference hash grid must reach the pair
+// (cell = max(largest primitive diagonal, d_hat + mb), boxes padded by
+// d_hat / 2 + mb; geometry.py:417-440, 462-475).  The enumeration itself uses
+// our own grid (below) over boxes that provably contain every such pair.
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include "ctx.cuh"
+#include "geom.cuh"
+
+enum { BP_RAW = 0, BP_CONTACT = 1, BP_CCD = 2, BP_CERT = 3 };
+
+struct BpOut {
+  // raw tap mode
+  int* a;
+  int* b;
+  // contact mode: scratch pair table
+  unsigned long long* khi;
+  unsigned long long* klo;
+  int4* verts;
+  double* d;
+  double* k;
+  double* nrm;
+  double* grad;
+  int* is_pt;
+  // ccd / certificate modes (verts == nullptr: no pair list is stored)
+  double* alpha_pair;
+  double* alpha_d;
+  double* min_alpha;  // global min over pairs (atomic)
+  int* ccd_ispt;
+  // common
+  int* counter;    // [0] = reported pairs, [1] = flag (penetration / failed certificate), [2] = stored
+  int64_t cap;
+};
+
+struct KeyCtx {
+  const int* new2old;
+  int bits;
+};
+
+__device__ __forceinline__ void make_key(const KeyCtx& K, int type, int i0, int i1, int i2, int i3,
+                                         unsigned long long* hi, unsigned long long* lo) {
+  unsigned long long b = (unsigned long long)K.bits;
+  *hi = ((unsigned long long)type << (2 * b)) | ((unsigned long long)K.new2old[i0] << b) |
+        (unsigned long long)K.new2old[i1];
+  *lo = ((unsigned long long)K.new2old[i2] << b) | (unsigned long long)K.new2old[i3];
+}
+
+struct ContactParams {
+  double d_hat, kappa;
+  const unsigned char* pinned;
+  KeyCtx key;
+};
+
+// write one active constraint (contact.py:139-165) into slot of the scratch table
+__device__ void write_contact(const BpOut& O, const ContactParams& CP, int slot, int type, const int vid[4], double d,
+                              double gr[12]) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+    if (CP.pinned[vid[a]]) {
+      gr[3 * a] = 0.0; gr[3 * a + 1] = 0.0; gr[3 * a + 2] = 0.0;
+    }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 12; ++q) s += gr[q] * gr[q];
+  double ddb;
+  barrier3(d, CP.d_hat, CP.kappa, nullptr, nullptr, &ddb);
+  unsigned long long hi, lo;
+  make_key(CP.key, type, vid[0], vid[1], vid[2], vid[3], &hi, &lo);
+  O.khi[slot] = hi;
+  O.klo[slot] = lo;
+  O.verts[slot] = make_int4(vid[0], vid[1], vid[2], vid[3]);
+  O.d[slot] = d;
+  O.k[slot] = ddb;
+  O.nrm[slot] = sqrt(s);
+  O.is_pt[slot] = type;
+#pragma unroll
+  for (int q = 0; q < 12; ++q) O.grad[12 * (int64_t)slot + q] = gr[q];
+}
+
+struct CcdParams {
+  const double* p;
+  double alpha_l;
+  int bs;
+};
+
+__device__ double ccd_pair_alpha(const double* x, const double* p, const int vid[4], bool is_pt, double alpha_l,
+                                 bool* cert_p);
+__device__ bool ccd_certify_pair(const double* x, const double* p, const double* alpha_d, int bs, const int vid[4],
+                                 bool is_pt);
+
+
+
+
+// ---------------------------------------------------------------------------
+// CUB helpers
+
+static void* cub_temp(mp_ctx* c, size_t bytes) {
+  c->cub_tmp.ensure(bytes + 256);
+  return c->cub_tmp.p;
+}
+
+static void exclusive_scan(mp_ctx* c, const int* in, int* out, int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, c->stream);
+  void* tmp = cub_temp(c, bytes);
+  cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)n, c->stream);
+  LAUNCH_CHECK();
+}
+
+static void sort_pairs_u64(mp_ctx* c, const unsigned long long* kin, unsigned long long* kout, const int* vin,
+                           int* vout, int64_t n, int end_bit) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, c->stream);
+  void* tmp = cub_temp(c, bytes);
+  cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, c->stream);
+  LAUNCH_CHECK();
+}
+
+static int bits_for(unsigned long long v) {
+  int b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+
+static void sync_stream(mp_ctx* c) { CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
+
+// Boxes of triangles and edges: raw (rlo, rhi); reference filter (flo, fhi:
+// triangle [lo - gap, hi + gap], edge [lo, hi + gap]); enumeration (elo,
+// ehi).  The largest raw-box diagonal (the reference's grid cell candidate,
+// geometry.py:462-465, same IEEE expression) is max-reduced into *diag_max.
+__global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, const int* __restrict__ edge,
+                             const double* __restrict__ x, double gap, const double* __restrict__ infl,
+                             double* __restrict__ rlo, double* __restrict__ rhi, double* __restrict__ flo,
+                             double* __restrict__ fhi, double* __restrict__ elo, double* __restrict__ ehi,
+                             double* __restrict__ diag_max) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double dg = 0.0;
+  if (i < F + E) {
+    double l[3], h[3], inf = 0.0;
+    if (i < F) {
+      int a = tri[3 * i], b = tri[3 * i + 1], c = tri[3 * i + 2];
+      if (infl) inf = fmax(fmax(infl[a], infl[b]), infl[c]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double xa = x[3 * a + k], xb = x[3 * b + k], xc = x[3 * c + k];
+        l[k] = fmin(fmin(xa, xb), xc);
+        h[k] = fmax(fmax(xa, xb), xc);
+      }
+    } else {
+      int64_t e = i - F;
+      int a = edge[2 * e], b = edge[2 * e + 1];
+      if (infl) inf = fmax(infl[a], infl[b]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double xa = x[3 * a + k], xb = x[3 * b + k];
+        l[k] = fmin(xa, xb);
+        h[k] = fmax(xa, xb);
+      }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double dk = RSUB(h[k], l[k]);
+      s = (k == 0) ? RMUL(dk, dk) : RADD(s, RMUL(dk, dk));
+      const double fl = (i < F) ? RSUB(l[k], gap) : l[k];
+      const double fh = RADD(h[k], gap);
+      rlo[3 * i + k] = l[k];
+      rhi[3 * i + k] = h[k];
+      flo[3 * i + k] = fl;
+      fhi[3 * i + k] = fh;
+      elo[3 * i + k] = infl ? l[k] - inf : fl;
+      ehi[3 * i + k] = infl ? h[k] + inf : fh;
+    }
+    dg = __dsqrt_rn(s);
+  }
+  dg = warp_max(dg);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(diag_max, dg);
+}
+
+// enumeration boxes of the surface points (object ids F+E+q)
+__global__ void k_point_boxes(int64_t V, const int* __restrict__ sverts, const double* __restrict__ x,
+                              const double* __restrict__ infl, double* __restrict__ elo, double* __restrict__ ehi) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= V) return;
+  int v = sverts[q];
+  double e = infl ? infl[v] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    elo[3 * q + k] = x[3 * v + k] - e;
+    ehi[3 * q + k] = x[3 * v + k] + e;
+  }
+}
+
+// stats for the grid: [0..2] min lo, [3..5] max hi, [6] sum of max extents
+__global__ void k_box_stats(int64_t P, const double* __restrict__ lo, const double* __restrict__ hi,
+                            double* __restrict__ part) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    double e = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double l = lo[3 * i + k], h = hi[3 * i + k];
+      mn[k] = fmin(mn[k], l);
+      mx[k] = fmax(mx[k], h);
+      e = fmax(e, h - l);
+    }
+    ext += e;
+  }
+  __shared__ double sh[7][8];
+  double vals[7] = {-mn[0], -mn[1], -mn[2], mx[0], mx[1], mx[2], ext};
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    double v = vals[q];
+    v = (q < 6) ? warp_max(v) : warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 7; ++q) {
+      double v = sh[q][0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = (q < 6) ? fmax(v, sh[q][w]) : v + sh[q][w];
+      part[7 * blockIdx.x + q] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// hierarchical uniform grid
+//
+// Level l has cell size h_l = h0 * 2^l (exact scaling) over the scene box.
+// Every object lives at the lowest level whose cell is at least as large as
+// its enumeration box, so it covers <= 2 cells per axis there (<= 8 entries).
+// A pair is found by the object of LOWER level querying the partner's level
+// (or, at equal levels, by the lower index for EE): the query walks levels
+// >= its own, <= 8 cells each, and meets only objects inserted at that
+// level.  Small objects therefore find large ones (the floor slab, boxes of
+// fast CCD vertices) without the large ones enumerating anything, and a pair
+// is reported once: in the cell holding the low corner of the intersection
+// of the two boxes, at the partner's level.
+
+#define HG_MAX_LEVELS 24
+
+struct HGrid {
+  double o[3];
+  double h0;
+  int nlev;
+  int n[HG_MAX_LEVELS][3];
+  int off[HG_MAX_LEVELS + 1];  // first global cell id of each level
+};
+
+__device__ __forceinline__ double hg_h(const HGrid& G, int l) { return ldexp(G.h0, l); }
+
+__device__ __forceinline__ int hg_coord(double v, double o, double h, int n) {
+  double q = floor((v - o) / h);  // monotone in v: box overlap implies a shared cell
+  if (!(q >= 0.0)) return 0;      // also catches NaN
+  if (q > (double)(n - 1)) return n - 1;
+  return (int)q;
+}
+
+__device__ __forceinline__ void hg_span(const HGrid& G, int l, const double* lo, const double* hi, int c0[3],
+                                        int c1[3]) {
+  const double h = hg_h(G, l);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c0[k] = hg_coord(lo[k], G.o[k], h, G.n[l][k]);
+    c1[k] = hg_coord(hi[k], G.o[k], h, G.n[l][k]);
+  }
+}
+
+__device__ __forceinline__ int hg_cell(const HGrid& G, int l, int a, int b, int c) {
+  return G.off[l] + (a * G.n[l][1] + b) * G.n[l][2] + c;
+}
+
+// the pair belongs to cell (a, b, c) of level l iff the low corner of the
+// intersection of the two boxes lies in it
+__device__ __forceinline__ bool hg_owns(const HGrid& G, int l, int a, int b, int c, const double* al,
+                                        const double* bl) {
+  const double h = hg_h(G, l);
+  return hg_coord(fmax(al[0], bl[0]), G.o[0], h, G.n[l][0]) == a &&
+         hg_coord(fmax(al[1], bl[1]), G.o[1], h, G.n[l][1]) == b &&
+         hg_coord(fmax(al[2], bl[2]), G.o[2], h, G.n[l][2]) == c;
+}
+
+__device__ __forceinline__ bool boxes_meet(const double* al, const double* ah, const double* bl, const double* bh) {
+  return al[0] <= bh[0] && bl[0] <= ah[0] && al[1] <= bh[1] && bl[1] <= ah[1] && al[2] <= bh[2] && bl[2] <= ah[2];
+}
+
+
+// level of every object and the number of cells it covers there
+__global__ void k_obj_level(int64_t nobj, HGrid G, const double* __restrict__ lo, const double* __restrict__ hi,
+                            int* __restrict__ level, int* __restrict__ cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nobj) return;
+  const double* l0 = lo + 3 * i;
+  const double* h0 = hi + 3 * i;
+  double ext = fmax(fmax(h0[0] - l0[0], h0[1] - l0[1]), h0[2] - l0[2]);
+  int l = 0;
+  while (l < G.nlev - 1 && ext > hg_h(G, l)) ++l;
+  int c0[3], c1[3];
+  hg_span(G, l, l0, h0, c0, c1);
+  level[i] = l;
+  cnt[i] = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
+}
+
+__device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
+  int l = 0, r = n;
+  while (l < r) {
+    int m = (l + r) >> 1;
+    if (a[m] <= k) l = m + 1; else r = m;
+  }
+  return l;
+}
+
+// one thread per (object, covered cell) entry: its global cell id and the
+// per-class histograms (0 triangles, 1 edges, 2 points)
+__global__ void k_entry_hist(int64_t total, int64_t nobj, int64_t F, int64_t P, HGrid G, const int* __restrict__ off,
+                             const int* __restrict__ level, const double* __restrict__ lo,
+                             const double* __restrict__ hi, int* __restrict__ ecell, int* __restrict__ tri_cnt,
+                             int* __restrict__ edge_cnt, int* __restrict__ pt_cnt) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
+  int r = (int)e - off[p];
+  int l = level[p];
+  int c0[3], c1[3];
+  hg_span(G, l, lo + 3 * (int64_t)p, hi + 3 * (int64_t)p, c0, c1);
+  int sx = c1[0] - c0[0] + 1, sy = c1[1] - c0[1] + 1;
+  int cell = hg_cell(G, l, c0[0] + r % sx, c0[1] + (r / sx) % sy, c0[2] + r / (sx * sy));
+  ecell[e] = cell;
+  atomicAdd(p < F ? &tri_cnt[cell] : (p < P ? &edge_cnt[cell] : &pt_cnt[cell]), 1);
+}
+
+__global__ void k_entry_fill(int64_t total, int64_t nobj, int64_t F, int64_t P, const int* __restrict__ off,
+                             const int* __restrict__ ecell, const int* __restrict__ tri_start,
+                             const int* __restrict__ edge_start, const int* __restrict__ pt_start,
+                             int* __restrict__ tri_cur, int* __restrict__ edge_cur, int* __restrict__ pt_cur,
+                             int* __restrict__ tri_ent, int* __restrict__ edge_ent, int* __restrict__ pt_ent) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
+  int cell = ecell[e];
+  if (p < F) tri_ent[tri_start[cell] + atomicAdd(&tri_cur[cell], 1)] = p;
+  else if (p < P) edge_ent[edge_start[cell] + atomicAdd(&edge_cur[cell], 1)] = p - (int)F;
+  else pt_ent[pt_start[cell] + atomicAdd(&pt_cur[cell], 1)] = p - (int)P;
+}
+
+// ---------------------------------------------------------------------------
+// queries
+
+// the reference hash grid's reachability (geometry.py:417-440, 465-475):
+// query box [q_lo - pad, q_hi + pad] and inserted box [b_lo - pad, b_hi + pad]
+// share a reference cell on every axis
+struct RefGrid {
+  double cell, pad;
+};
+
+__device__ __forceinline__ bool ref_reach(const RefGrid& R, const double* qlo, const double* qhi, const double* blo,
+                                          const double* bhi) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double q0 = floor(RDIV(RSUB(qlo[k], R.pad), R.cell)), q1 = floor(RDIV(RADD(qhi[k], R.pad), R.cell));
+    double i0 = floor(RDIV(RSUB(blo[k], R.pad), R.cell)), i1 = floor(RDIV(RADD(bhi[k], R.pad), R.cell));
+    if (!(q0 <= i1 && i0 <= q1)) return false;
+  }
+  return true;
+}
+
+struct BpTables {
+  HGrid G;
+  RefGrid R;
+  const int *pt_start, *pt_ent, *tri_start, *tri_ent, *edge_start, *edge_ent;
+  const int* level;                     // (F+E+V)
+  const double *flo, *fhi, *rlo, *rhi;  // (F+E)*3 reference filter / raw boxes
+  const double *elo, *ehi;              // (F+E+V)*3 enumeration boxes
+  int64_t F, P;                         // object id bases: edges at F, points at P
+};
+
+// mode work on one reference pair; returns 1 if the pair counts
+template <int MODE>
+__device__ __forceinline__ int pair_work(const BpOut& O, const ContactParams& CP, const CcdParams& CC,
+                                         const double* x, int type, const int vid[4], const int vid_ccd[4], int ra,
+                                         int rb) {
+  if (MODE == BP_RAW) {
+    int slot = atomicAdd(&O.counter[0], 1);
+    if (slot < O.cap) {
+      O.a[slot] = ra;
+      O.b[slot] = rb;
+    }
+    return 0;
+  } else if (MODE == BP_CONTACT) {
+    double X[4][3], gr[12];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
+    double d = type ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
+    if (d <= 0.0) {
+      O.counter[1] = 1;
+    } else if (d < CP.d_hat) {
+      int slot = atomicAdd(&O.counter[0], 1);
+      if (slot < O.cap) write_contact(O, CP, slot, type, vid, d, gr);
+    }
+    return 0;
+  } else if (MODE == BP_CCD) {
+    bool cert_p = true;
+    double al = ccd_pair_alpha(x, CC.p, vid_ccd, type != 0, CC.alpha_l, &cert_p);
+    if (al < 1.0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid_ccd[r] / CC.bs], al);
+      atomic_min_nonneg(O.min_alpha, al);
+    }
+    if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
+    if (O.verts) {
+      int slot = atomicAdd(&O.counter[2], 1);
+      if (slot < O.cap) {
+        O.verts[slot] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
+        O.ccd_ispt[slot] = type;
+        O.alpha_pair[slot] = al;
+      }
+    }
+    return 1;
+  } else {  // BP_CERT
+    if (!ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, type != 0)) O.counter[1] = 1;
+    return 1;
+  }
+}
+
+// PT filter + reachability (geometry.py:478-487) for point v against triangle t
+__device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const double* x, int v, int t) {
+  const double pv[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
+  const double* l = T.flo + 3 * (int64_t)t;
+  const double* h = T.fhi + 3 * (int64_t)t;
+  if (!(pv[0] >= l[0] && pv[1] >= l[1] && pv[2] >= l[2] && pv[0] <= h[0] && pv[1] <= h[1] && pv[2] <= h[2]))
+    return false;
+  return ref_reach(T.R, pv, pv, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t);
+}
+
+template <int MODE>
+__device__ __forceinline__ int pt_pair(const BpTables& T, const BpOut& O, const ContactParams& CP,
+                                       const CcdParams& CC, const double* x, const int* tri, const int* tri_sorted,
+                                       int v, int t) {
+  const int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
+  if (a == v || b == v || c == v) return 0;
+  if (!pt_ref_pass(T, x, v, t)) return 0;
+  // constraint set: triangle sorted by original id (contact.py:133-135);
+  // CCD: surface order (ccd.py:229-231)
+  int vid[4] = {v, a, b, c};
+  if (MODE == BP_CONTACT) {
+    vid[1] = tri_sorted[3 * t]; vid[2] = tri_sorted[3 * t + 1]; vid[3] = tri_sorted[3 * t + 2];
+  }
+  const int vid_ccd[4] = {v, a, b, c};
+  return pair_work<MODE>(O, CP, CC, x, 1, vid, vid_ccd, v, t);
+}
+
+// points query the triangles of every level >= their own
+template <int MODE>
+__global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const int* __restrict__ sverts,
+                                                   const int* __restrict__ tri, const int* __restrict__ tri_sorted,
+                                                   const double* __restrict__ x, BpOut O, ContactParams CP,
+                                                   CcdParams CC) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= V) return;
+  const int v = sverts[q];
+  const double* pl = T.elo + 3 * (T.P + q);
+  const double* ph = T.ehi + 3 * (T.P + q);
+  int cnt = 0;
+  for (int l = T.level[T.P + q]; l < T.G.nlev; ++l) {
+    int c0[3], c1[3];
+    hg_span(T.G, l, pl, ph, c0, c1);
+    for (int a = c0[0]; a <= c1[0]; ++a)
+      for (int b = c0[1]; b <= c1[1]; ++b)
+        for (int c = c0[2]; c <= c1[2]; ++c) {
+          const int cell = hg_cell(T.G, l, a, b, c);
+          for (int e = T.tri_start[cell]; e < T.tri_start[cell + 1]; ++e) {
+            const int t = T.tri_ent[e];
+            const double* tl = T.elo + 3 * (int64_t)t;
+            if (!boxes_meet(pl, ph, tl, T.ehi + 3 * (int64_t)t) || !hg_owns(T.G, l, a, b, c, pl, tl)) continue;
+            cnt += pt_pair<MODE>(T, O, CP, CC, x, tri, tri_sorted, v, t);
+          }
+        }
+  }
+  if (cnt) atomicAdd(&O.counter[0], cnt);
+}
+
+// triangles query the points of every level above their own
+template <int MODE>
+__global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const int* __restrict__ sverts,
+                                                 const int* __restrict__ tri, const int* __restrict__ tri_sorted,
+                                                 const double* __restrict__ x, BpOut O, ContactParams CP,
+                                                 CcdParams CC) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= F) return;
+  const double* tl = T.elo + 3 * t;
+  const double* th = T.ehi + 3 * t;
+  int cnt = 0;
+  for (int l = T.level[t] + 1; l < T.G.nlev; ++l) {
+    int c0[3], c1[3];
+    hg_span(T.G, l, tl, th, c0, c1);
+    for (int a = c0[0]; a <= c1[0]; ++a)
+      for (int b = c0[1]; b <= c1[1]; ++b)
+        for (int c = c0[2]; c <= c1[2]; ++c) {
+          const int cell = hg_cell(T.G, l, a, b, c);
+          for (int e = T.pt_start[cell]; e < T.pt_start[cell + 1]; ++e) {
+            const int q = T.pt_ent[e];
+            const double* pl = T.elo + 3 * (T.P + q);
+            if (!boxes_meet(pl, T.ehi + 3 * (T.P + q), tl, th) || !hg_owns(T.G, l, a, b, c, pl, tl)) continue;
+            cnt += pt_pair<MODE>(T, O, CP, CC, x, tri, tri_sorted, sverts[q], (int)t);
+          }
+        }
+  }
+  if (cnt) atomicAdd(&O.counter[0], cnt);
+}
+
+// edges query the edges of every level >= their own (equal level: higher index)
+template <int MODE>
+__global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const int* __restrict__ edge,
+                                                  const double* __restrict__ x, BpOut O, ContactParams CP,
+                                                  CcdParams CC) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const int lv = T.level[T.F + i];
+  const double* il = T.elo + 3 * (T.F + i);
+  const double* ih = T.ehi + 3 * (T.F + i);
+  const int ia = edge[2 * i], ib = edge[2 * i + 1];
+  int cnt = 0;
+  for (int l = lv; l < T.G.nlev; ++l) {
+    int c0[3], c1[3];
+    hg_span(T.G, l, il, ih, c0, c1);
+    for (int a = c0[0]; a <= c1[0]; ++a)
+      for (int b = c0[1]; b <= c1[1]; ++b)
+        for (int c = c0[2]; c <= c1[2]; ++c) {
+          const int cell = hg_cell(T.G, l, a, b, c);
+          for (int e = T.edge_start[cell]; e < T.edge_start[cell + 1]; ++e) {
+            const int j = T.edge_ent[e];
+            if (l == lv && j <= i) continue;
+            const double* jl = T.elo + 3 * (T.F + j);
+            if (!boxes_meet(il, ih, jl, T.ehi + 3 * (T.F + j)) || !hg_owns(T.G, l, a, b, c, il, jl)) continue;
+            const int ja = edge[2 * j], jb = edge[2 * j + 1];
+            if (ia == ja || ia == jb || ib == ja || ib == jb) continue;
+            const int lo_e = min((int)i, j), hi_e = max((int)i, j);
+            // reference join filter on (lo_e, hi_e) (geometry.py:491-499)
+            const double* li = T.flo + 3 * (T.F + lo_e);
+            const double* hi_i = T.fhi + 3 * (T.F + lo_e);
+            const double* lj = T.flo + 3 * (T.F + hi_e);
+            const double* hj = T.fhi + 3 * (T.F + hi_e);
+            bool pass = true;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) pass = pass && (li[k] <= hj[k]) && (lj[k] <= hi_i[k]);
+            if (!pass) continue;
+            if (!ref_reach(T.R, T.rlo + 3 * (T.F + lo_e), T.rhi + 3 * (T.F + lo_e), T.rlo + 3 * (T.F + hi_e),
+                           T.rhi + 3 * (T.F + hi_e)))
+              continue;
+            const int vid[4] = {edge[2 * lo_e], edge[2 * lo_e + 1], edge[2 * hi_e], edge[2 * hi_e + 1]};
+            cnt += pair_work<MODE>(O, CP, CC, x, 0, vid, vid, lo_e, hi_e);
+          }
+        }
+  }
+  if (cnt) atomicAdd(&O.counter[0], cnt);
+}
+
+// ---------------------------------------------------------------------------
+// broad-phase build (host driver)
+
+struct BpGrid {
+  BpTables T{};
+  bool empty = true;
+};
+
+// Everything one broad-phase call at (x, mb, d_hat) needs: boxes, levels and
+// the per-level cell tables of triangles / edges / surface points.
+// infl (per vertex, device) switches to tight enumeration boxes.
+static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, const double* infl = nullptr) {
+  BpGrid B;
+  const int64_t F = c->F, P = c->F + c->E, V = c->V, nobj = P + V;
+  B.T.F = F;
+  B.T.P = P;
+  if (F == 0) return B;
+  const double gap = d_hat + 2.0 * mb;
+  cudaStream_t st = c->stream;
+  for (DBuf<double>* b : {&c->box_rlo, &c->box_rhi, &c->box_flo, &c->box_fhi}) b->ensure(3 * P);
+  c->box_elo.ensure(3 * nobj);
+  c->box_ehi.ensure(3 * nobj);
+  CUDA_CHECK(cudaMemsetAsync(c->dscal.p + 40, 0, sizeof(double), st));
+  k_prim_boxes<<<grid_for(P, 256), 256, 0, st>>>(F, c->E, c->tri, c->edge, x, gap, infl, c->box_rlo, c->box_rhi,
+                                                  c->box_flo, c->box_fhi, c->box_elo, c->box_ehi, c->dscal.p + 40);
+  LAUNCH_CHECK();
+  if (V) {
+    k_point_boxes<<<grid_for(V, 256), 256, 0, st>>>(V, c->sverts, x, infl, c->box_elo.p + 3 * P,
+                                                     c->box_ehi.p + 3 * P);
+    LAUNCH_CHECK();
+  }
+  const int nb = 64;
+  c->red_part.ensure(7 * nb + 1);
+  k_box_stats<<<nb, 256, 0, st>>>(P, c->box_elo, c->box_ehi, c->red_part);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemcpyAsync(c->red_part.p + 7 * nb, c->dscal.p + 40, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  std::vector<double> part(7 * nb + 1);
+  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * (7 * nb + 1), cudaMemcpyDeviceToHost, st));
+  sync_stream(c);
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = fmin(mn[k], -part[7 * b + k]);
+      mx[k] = fmax(mx[k], part[7 * b + 3 + k]);
+    }
+    ext += part[7 * b + 6];
+  }
+  // the reference's cell and pad (geometry.py:465-466)
+  B.T.R.cell = fmax(part[7 * nb], d_hat + mb);
+  B.T.R.pad = 0.5 * d_hat + mb;
+  // level 0: about the mean primitive extent, at most ~4M cells
+  double span = fmax(fmax(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
+  if (!(span > 0.0) || !std::isfinite(span)) span = 1.0;
+  double h0 = ext / (double)P;
+  if (!(h0 > 0.0) || !std::isfinite(h0)) h0 = span;
+  h0 = fmax(h0, span * 1e-6);
+  HGrid& G = B.T.G;
+  for (;;) {
+    double cells0 = 1.0;
+    for (int k = 0; k < 3; ++k) cells0 *= floor((mx[k] - mn[k]) / h0) + 1.0;
+    if (cells0 <= (double)(1 << 22)) break;
+    h0 *= 2.0;
+  }
+  G.h0 = h0;
+  for (int k = 0; k < 3; ++k) G.o[k] = mn[k];
+  int64_t tot_cells = 0;
+  G.nlev = 0;
+  for (int l = 0; l < HG_MAX_LEVELS; ++l) {
+    const double h = ldexp(h0, l);
+    int one = 1;
+    for (int k = 0; k < 3; ++k) {
+      double nk = floor((mx[k] - mn[k]) / h) + 1.0;
+      if (!(nk >= 1.0)) nk = 1.0;
+      G.n[l][k] = (int)nk;
+      one = one && (G.n[l][k] <= 2);
+    }
+    G.off[l] = (int)tot_cells;
+    tot_cells += (int64_t)G.n[l][0] * G.n[l][1] * G.n[l][2];
+    G.nlev = l + 1;
+    if (one && h >= span) break;
+  }
+  G.off[G.nlev] = (int)tot_cells;
+  auto& g = c->grid;
+  g.level.ensure(nobj);
+  c->cell_cnt.ensure(nobj + 1);
+  c->cell_off.ensure(nobj + 1);
+  k_obj_level<<<grid_for(nobj, 256), 256, 0, st>>>(nobj, G, c->box_elo, c->box_ehi, g.level, c->cell_cnt);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + nobj, 0, sizeof(int), st));
+  exclusive_scan(c, c->cell_cnt, c->cell_off, nobj + 1);
+  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 4, c->cell_off.p + nobj, sizeof(int), cudaMemcpyDeviceToHost, st));
+  sync_stream(c);
+  const int total = c->h_cnt[4];
+  const size_t ncell = (size_t)tot_cells;
+  for (DBuf<int>* b : {&g.tri_cnt, &g.tri_start, &g.edge_cnt, &g.edge_start, &g.pt_cnt, &g.pt_start})
+    b->ensure(ncell + 1);
+  g.ecell.ensure((size_t)total + 1);
+  g.tri_ent.ensure((size_t)total + 1);
+  g.edge_ent.ensure((size_t)total + 1);
+  g.pt_ent.ensure((size_t)total + 1);
+  for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
+    CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
+  if (total) {
+    k_entry_hist<<<grid_for(total, 256), 256, 0, st>>>(total, nobj, F, P, G, c->cell_off, g.level, c->box_elo,
+                                                       c->box_ehi, g.ecell, g.tri_cnt, g.edge_cnt, g.pt_cnt);
+    LAUNCH_CHECK();
+  }
+  exclusive_scan(c, g.tri_cnt, g.tri_start, ncell + 1);
+  exclusive_scan(c, g.edge_cnt, g.edge_start, ncell + 1);
+  exclusive_scan(c, g.pt_cnt, g.pt_start, ncell + 1);
+  // the counts become per-cell fill cursors
+  for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
+    CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
+  if (total) {
+    k_entry_fill<<<grid_for(total, 256), 256, 0, st>>>(total, nobj, F, P, c->cell_off, g.ecell, g.tri_start,
+                                                       g.edge_start, g.pt_start, g.tri_cnt, g.edge_cnt, g.pt_cnt,
+                                                       g.tri_ent, g.edge_ent, g.pt_ent);
+    LAUNCH_CHECK();
+  }
+  BpTables& T = B.T;
+  T.pt_start = g.pt_start; T.pt_ent = g.pt_ent;
+  T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
+  T.edge_start = g.edge_start; T.edge_ent = g.edge_ent;
+  T.level = g.level;
+  T.flo = c->box_flo; T.fhi = c->box_fhi; T.rlo = c->box_rlo; T.rhi = c->box_rhi;
+  T.elo = c->box_elo; T.ehi = c->box_ehi;
+  B.empty = false;
+  return B;
+}
+
+// Run the PT (which & 1) and EE (which & 2) queries in MODE.  Returns the
+// number of reported pairs (RAW / CONTACT: may exceed O.cap, the caller grows
+// and retries; CCD / CERT: pairs evaluated); *flag = counters[1]
+// (penetration / failed certificate); counters[2] = stored CCD pairs.
+template <int MODE>
+static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
+                      int* flag, int which = 3) {
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
+  O.counter = c->counters.p;
+  if (!B.empty) {
+    if ((which & 1) && c->V) {
+      k_hq_points<MODE><<<grid_for(c->V, 128), 128, 0, c->stream>>>(B.T, c->V, c->sverts, c->tri, c->tri_sorted, x,
+                                                                      O, CP, CC);
+      LAUNCH_CHECK();
+      k_hq_tris<MODE><<<grid_for(c->F, 128), 128, 0, c->stream>>>(B.T, c->F, c->sverts, c->tri, c->tri_sorted, x, O,
+                                                                    CP, CC);
+      LAUNCH_CHECK();
+    }
+    if ((which & 2) && c->E > 1) {
+      k_hq_edges<MODE><<<grid_for(c->E, 128), 128, 0, c->stream>>>(B.T, c->E, c->edge, x, O, CP, CC);
+      LAUNCH_CHECK();
+    }
+  }
+  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  if (flag) *flag = c->h_cnt[1];
+  return (MODE == BP_CCD && O.verts) ? std::max<int64_t>(c->h_cnt[0], c->h_cnt[2]) : c->h_cnt[0];
+}

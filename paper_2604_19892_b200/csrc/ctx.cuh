@@ -70,10 +70,10 @@ struct PairTable {
   }
 };
 
-// dense cell tables of the broad phase (contact.cuh build_bp)
+// per-level cell tables of the broad phase (bp.cuh build_bp)
 struct BpGridBufs {
   DBuf<int> tri_cnt, tri_start, edge_cnt, edge_start, pt_cnt, pt_start;  // (ncell+1)
-  DBuf<int> cells_pt, cells_ee;                                          // work lists
+  DBuf<int> level;                                                       // (objects)
   DBuf<int> ecell, tri_ent, edge_ent, pt_ent;                            // (entries)
 };
 
