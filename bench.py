@@ -51,10 +51,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-SCENE_DESC = ("c2_stack: 8 SNH cubes (17^3 cells, 0.2 m, E=1e5) stacked 2x2x2 with 1e-3 gaps on a pinned "
-              "1.2x1.2x0.1 floor; 46,664 V / 235,830 T / 27,756 surface tris; h=0.01, d_hat=2e-3, kappa=1e4; "
-              "SolverConfig defaults (K=8, levels=2, coarse_block=4, block 32)")
+SCENE_DESC = ("c2_stack: 8 SNH cubes (17^3 cells, 0.2 m, E=1e5) stacked 2x2x2 with 5e-3 gaps on a pinned "
+              "1.2x1.2x0.1 floor, released from rest (contacts form from frame 2); 46,664 V / 235,830 T / "
+              "27,756 surface tris; h=0.01, d_hat=2e-3, kappa=1e4; SolverConfig defaults (K=8, levels=2, "
+              "coarse_block=4, block 32) except iter_max")
 H = 0.01
+GAP = 5e-3
+ITER_MAX = 500
 
 
 def _peaks():
@@ -119,23 +122,27 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_baseline(sample_iters=None, budget_s=20.0):
+def cpu_baseline(sample_iters=None, budget_s=30.0, threads=1):
     """The oracle (numpy CPU restatement of the reference, oracle/) on a
-    bounded sample of the workload: PNCG iterations of frame 1 from rest,
-    single process.  Returns the cpu_baseline object."""
+    bounded sample of the workload: PNCG iterations of frame 1 from rest
+    within a wall-clock budget, BLAS limited to `threads`.  Returns the
+    cpu_baseline object."""
+    from threadpoolctl import threadpool_limits
+
     from oracle import solver as osolver
 
     from paper_2604_19892_b200 import scenes
 
-    scene = scenes.c2_stack(mods=osolver.MODS)
-    cfg = osolver.SolverConfig()
-    x = scene.mesh.rest_positions.ravel().copy()
+    scene = osolver.Scene.from_scene(scenes.c2_stack(gap=GAP))
+    cfg = osolver.SolverConfig(iter_max=ITER_MAX)
+    x = scene.rest.ravel().copy()
     v = np.zeros_like(x)
-    iters, elapsed = osolver.timed_iterations(scene, x, v, H, cfg, budget_s=budget_s, max_iters=sample_iters)
+    with threadpool_limits(limits=threads):
+        iters, elapsed = osolver.timed_iterations(scene, x, v, H, cfg, budget_s=budget_s, max_iters=sample_iters)
     return {
-        "value": iters / elapsed, "unit": "iters/s", "cores": 1, "kind": "port",
+        "value": iters / elapsed, "unit": "iters/s", "cores": threads, "kind": "port",
         "sample": f"{iters} PNCG iterations of frame 1 of the same scene (from rest) by the numpy oracle, "
-                  f"{elapsed:.1f} s, single process, OMP/BLAS threads=1",
+                  f"{elapsed:.1f} s, single process, BLAS threads={threads}",
     }
 
 
@@ -144,13 +151,13 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    threads = os.cpu_count() or 1
     per = []
     total_it = 0
     total_s = 0.0
     budget = max(5.0, 60.0 / max(1, args.steps))
     for s in range(args.warmup + args.steps):
-        cb = cpu_baseline(budget_s=budget if s >= args.warmup else 3.0)
+        cb = cpu_baseline(budget_s=budget if s >= args.warmup else 3.0, threads=threads)
         it = int(cb["sample"].split()[0])
         if s >= args.warmup:
             per.append(cb["value"])
@@ -163,7 +170,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": SCENE_DESC, "sample": "each step = PNCG iterations of frame 1 for a bounded "
                                                      f"~{budget:.0f} s budget"},
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "port",
                          "sample": f"{total_it} PNCG iterations over {args.steps} steps"},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -199,10 +206,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    scene = scenes.c2_stack()
-    cfg = solver.SolverConfig()
-    if args.iter_max:
-        cfg.iter_max = args.iter_max
+    scene = scenes.c2_stack(gap=GAP)
+    cfg = solver.SolverConfig(iter_max=args.iter_max or ITER_MAX)
     ctx = scene.context(cfg, device=local)
     x0 = scene.mesh.rest_positions.ravel().copy()
     ctx.set_state(x0, np.zeros_like(x0))
@@ -326,7 +331,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--iter-max", type=int, default=0, help="cap PNCG iterations per frame (0 = reference default)")
+    ap.add_argument("--iter-max", type=int, default=0, help=f"PNCG iterations cap per frame (default {ITER_MAX})")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

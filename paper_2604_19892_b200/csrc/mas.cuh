@@ -69,10 +69,10 @@ __global__ void k_bsr_to_blocks(int64_t N, const int* __restrict__ rowptr, const
 
 // write a symmetric m x m smem matrix (0.5 (X + X^T)) in cyclic-diagonal packing
 __device__ void store_cyc_sym(const double* X, int m, double* __restrict__ out, bool symmetrize) {
-  const int64_t tot = cyc_size(m);
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-    int s = (int)(e / m);
-    int i = (int)(e - (int64_t)s * m);
+  const int tot = (int)cyc_size(m);
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    int s = e / m;
+    int i = e - s * m;
     int j = i + s;
     if (j >= m) j -= m;
     out[e] = symmetrize ? 0.5 * (X[i * m + j] + X[j * m + i]) : X[i * m + j];
@@ -212,20 +212,23 @@ __device__ bool sweep_core(double* S, int m, double* rowk) {
       ci[a] = rk[min(tr + 16 * a, 95)] * inv;
       cj[a] = rk[min(tc + 16 * a, 95)];
     }
+    // rank-one update of every element (row / column k patched below)
 #pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a) {
-      const int i = tr + 16 * a;
+    for (int a = 0; a < SWEEP_T; ++a)
 #pragma unroll
-      for (int b = 0; b < SWEEP_T; ++b) {
-        const int j = tc + 16 * b;
-        double r = R[a][b];
-        if (i != k && j != k) r = fma(-ci[a], cj[b], r);
-        else if (i == k && j == k) r = -inv;
-        else if (i == k) r = cj[b] * inv;
-        else r = ci[a];
-        R[a][b] = r;
+      for (int b = 0; b < SWEEP_T; ++b) R[a][b] = fma(-ci[a], cj[b], R[a][b]);
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a)
+      if (tr + 16 * a == k) {
+#pragma unroll
+        for (int b = 0; b < SWEEP_T; ++b) R[a][b] = cj[b] * inv;
       }
-    }
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b)
+      if (tc + 16 * b == k) {
+#pragma unroll
+        for (int a = 0; a < SWEEP_T; ++a) R[a][b] = (tr + 16 * a == k) ? -inv : ci[a];
+      }
   }
   __syncthreads();
 #pragma unroll
