@@ -252,7 +252,7 @@ __global__ void k_box_stats(int64_t P, const double* __restrict__ lo, const doub
 
 struct HGrid {
   double o[3];
-  double h0;
+  double h0, inv_h0;
   int nlev;
   int n[HG_MAX_LEVELS][3];
   int off[HG_MAX_LEVELS + 1];  // first global cell id of each level
@@ -260,20 +260,22 @@ struct HGrid {
 
 __device__ __forceinline__ double hg_h(const HGrid& G, int l) { return ldexp(G.h0, l); }
 
-__device__ __forceinline__ int hg_coord(double v, double o, double h, int n) {
-  double q = floor((v - o) / h);  // monotone in v: box overlap implies a shared cell
-  if (!(q >= 0.0)) return 0;      // also catches NaN
-  if (q > (double)(n - 1)) return n - 1;
+// cell coordinate at level l: floor((v - o) / h_l), evaluated as a product
+// with the exact power-of-two scaled reciprocal; the same monotone function
+// is used for every object, query and corner, which is all consistency needs
+__device__ __forceinline__ int hg_coord(const HGrid& G, int l, int k, double v) {
+  double q = floor((v - G.o[k]) * ldexp(G.inv_h0, -l));
+  if (!(q >= 0.0)) return 0;  // also catches NaN
+  if (q > (double)(G.n[l][k] - 1)) return G.n[l][k] - 1;
   return (int)q;
 }
 
 __device__ __forceinline__ void hg_span(const HGrid& G, int l, const double* lo, const double* hi, int c0[3],
                                         int c1[3]) {
-  const double h = hg_h(G, l);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    c0[k] = hg_coord(lo[k], G.o[k], h, G.n[l][k]);
-    c1[k] = hg_coord(hi[k], G.o[k], h, G.n[l][k]);
+    c0[k] = hg_coord(G, l, k, lo[k]);
+    c1[k] = hg_coord(G, l, k, hi[k]);
   }
 }
 
@@ -285,16 +287,50 @@ __device__ __forceinline__ int hg_cell(const HGrid& G, int l, int a, int b, int 
 // intersection of the two boxes lies in it
 __device__ __forceinline__ bool hg_owns(const HGrid& G, int l, int a, int b, int c, const double* al,
                                         const double* bl) {
-  const double h = hg_h(G, l);
-  return hg_coord(fmax(al[0], bl[0]), G.o[0], h, G.n[l][0]) == a &&
-         hg_coord(fmax(al[1], bl[1]), G.o[1], h, G.n[l][1]) == b &&
-         hg_coord(fmax(al[2], bl[2]), G.o[2], h, G.n[l][2]) == c;
+  return hg_coord(G, l, 0, fmax(al[0], bl[0])) == a && hg_coord(G, l, 1, fmax(al[1], bl[1])) == b &&
+         hg_coord(G, l, 2, fmax(al[2], bl[2])) == c;
 }
 
 __device__ __forceinline__ bool boxes_meet(const double* al, const double* ah, const double* bl, const double* bh) {
   return al[0] <= bh[0] && bl[0] <= ah[0] && al[1] <= bh[1] && bl[1] <= ah[1] && al[2] <= bh[2] && bl[2] <= ah[2];
 }
 
+
+// the reference hash grid's cell range of every object
+// (floor((lo - pad) / cell), floor((hi + pad) / cell); geometry.py:421-423,
+// same IEEE expressions): triangles / edges from their raw boxes, points
+// from their position.  Two objects are reachable in the reference grid iff
+// their ranges overlap on every axis.
+__global__ void k_ref_cells(int64_t P, int64_t V, const int* __restrict__ sverts, const double* __restrict__ x,
+                            const double* __restrict__ rlo, const double* __restrict__ rhi, double pad, double cell,
+                            int* __restrict__ rc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= P + V) return;
+  double lo[3], hi[3];
+  if (i < P) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = rlo[3 * i + k];
+      hi[k] = rhi[3 * i + k];
+    }
+  } else {
+    const int v = sverts[i - P];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) lo[k] = hi[k] = x[3 * v + k];
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double a = floor(RDIV(RSUB(lo[k], pad), cell)), b = floor(RDIV(RADD(hi[k], pad), cell));
+    rc[6 * i + k] = (int)fmax(fmin(a, 1e9), -1e9);
+    rc[6 * i + 3 + k] = (int)fmax(fmin(b, 1e9), -1e9);
+  }
+}
+
+__device__ __forceinline__ bool ref_reach(const int* __restrict__ rc, int64_t a, int64_t b) {
+  const int* A = rc + 6 * a;
+  const int* B = rc + 6 * b;
+  return A[0] <= B[3] && B[0] <= A[3] && A[1] <= B[4] && B[1] <= A[4] && A[2] <= B[5] && B[2] <= A[5];
+}
 
 // level of every object and the number of cells it covers there
 __global__ void k_obj_level(int64_t nobj, HGrid G, const double* __restrict__ lo, const double* __restrict__ hi,
@@ -355,125 +391,43 @@ __global__ void k_entry_fill(int64_t total, int64_t nobj, int64_t F, int64_t P, 
 }
 
 // ---------------------------------------------------------------------------
-// queries
-
-// the reference hash grid's reachability (geometry.py:417-440, 465-475):
-// query box [q_lo - pad, q_hi + pad] and inserted box [b_lo - pad, b_hi + pad]
-// share a reference cell on every axis
-struct RefGrid {
-  double cell, pad;
-};
-
-__device__ __forceinline__ bool ref_reach(const RefGrid& R, const double* qlo, const double* qhi, const double* blo,
-                                          const double* bhi) {
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    double q0 = floor(RDIV(RSUB(qlo[k], R.pad), R.cell)), q1 = floor(RDIV(RADD(qhi[k], R.pad), R.cell));
-    double i0 = floor(RDIV(RSUB(blo[k], R.pad), R.cell)), i1 = floor(RDIV(RADD(bhi[k], R.pad), R.cell));
-    if (!(q0 <= i1 && i0 <= q1)) return false;
-  }
-  return true;
-}
+// enumeration: count pass, scan, fill pass -> reference pair list
+//   PT pairs (v, t): v = surface vertex (device id), t = triangle index
+//   EE pairs (i, j): edge indices, i < j
 
 struct BpTables {
   HGrid G;
-  RefGrid R;
   const int *pt_start, *pt_ent, *tri_start, *tri_ent, *edge_start, *edge_ent;
   const int* level;                     // (F+E+V)
-  const double *flo, *fhi, *rlo, *rhi;  // (F+E)*3 reference filter / raw boxes
+  const int* rc;                        // (F+E+V)*6 reference-grid cell ranges
+  const double *flo, *fhi;              // (F+E)*3 reference filter / join boxes
   const double *elo, *ehi;              // (F+E+V)*3 enumeration boxes
   int64_t F, P;                         // object id bases: edges at F, points at P
 };
 
-// mode work on one reference pair; returns 1 if the pair counts
-template <int MODE>
-__device__ __forceinline__ int pair_work(const BpOut& O, const ContactParams& CP, const CcdParams& CC,
-                                         const double* x, int type, const int vid[4], const int vid_ccd[4], int ra,
-                                         int rb) {
-  if (MODE == BP_RAW) {
-    int slot = atomicAdd(&O.counter[0], 1);
-    if (slot < O.cap) {
-      O.a[slot] = ra;
-      O.b[slot] = rb;
-    }
-    return 0;
-  } else if (MODE == BP_CONTACT) {
-    double X[4][3], gr[12];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
-    double d = type ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
-    if (d <= 0.0) {
-      O.counter[1] = 1;
-    } else if (d < CP.d_hat) {
-      int slot = atomicAdd(&O.counter[0], 1);
-      if (slot < O.cap) write_contact(O, CP, slot, type, vid, d, gr);
-    }
-    return 0;
-  } else if (MODE == BP_CCD) {
-    bool cert_p = true;
-    double al = ccd_pair_alpha(x, CC.p, vid_ccd, type != 0, CC.alpha_l, &cert_p);
-    if (al < 1.0) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid_ccd[r] / CC.bs], al);
-      atomic_min_nonneg(O.min_alpha, al);
-    }
-    if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
-    if (O.verts) {
-      int slot = atomicAdd(&O.counter[2], 1);
-      if (slot < O.cap) {
-        O.verts[slot] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
-        O.ccd_ispt[slot] = type;
-        O.alpha_pair[slot] = al;
-      }
-    }
-    return 1;
-  } else {  // BP_CERT
-    if (!ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, type != 0)) O.counter[1] = 1;
-    return 1;
-  }
-}
-
-// PT filter + reachability (geometry.py:478-487) for point v against triangle t
-__device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const double* x, int v, int t) {
-  const double pv[3] = {x[3 * v], x[3 * v + 1], x[3 * v + 2]};
+// PT filter (geometry.py:484-486) + reference reachability, point q vs tri t
+__device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, const double* x, int v, int64_t q,
+                                            int t) {
+  if (tri[3 * t] == v || tri[3 * t + 1] == v || tri[3 * t + 2] == v) return false;
   const double* l = T.flo + 3 * (int64_t)t;
   const double* h = T.fhi + 3 * (int64_t)t;
-  if (!(pv[0] >= l[0] && pv[1] >= l[1] && pv[2] >= l[2] && pv[0] <= h[0] && pv[1] <= h[1] && pv[2] <= h[2]))
-    return false;
-  return ref_reach(T.R, pv, pv, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t);
-}
-
-template <int MODE>
-__device__ __forceinline__ int pt_pair(const BpTables& T, const BpOut& O, const ContactParams& CP,
-                                       const CcdParams& CC, const double* x, const int* tri, const int* tri_sorted,
-                                       int v, int t) {
-  const int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
-  if (a == v || b == v || c == v) return 0;
-  if (!pt_ref_pass(T, x, v, t)) return 0;
-  // constraint set: triangle sorted by original id (contact.py:133-135);
-  // CCD: surface order (ccd.py:229-231)
-  int vid[4] = {v, a, b, c};
-  if (MODE == BP_CONTACT) {
-    vid[1] = tri_sorted[3 * t]; vid[2] = tri_sorted[3 * t + 1]; vid[3] = tri_sorted[3 * t + 2];
-  }
-  const int vid_ccd[4] = {v, a, b, c};
-  return pair_work<MODE>(O, CP, CC, x, 1, vid, vid_ccd, v, t);
+  const double p0 = x[3 * v], p1 = x[3 * v + 1], p2 = x[3 * v + 2];
+  if (!(p0 >= l[0] && p1 >= l[1] && p2 >= l[2] && p0 <= h[0] && p1 <= h[1] && p2 <= h[2])) return false;
+  return ref_reach(T.rc, T.P + q, t);
 }
 
 // points query the triangles of every level >= their own
-template <int MODE>
+template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const int* __restrict__ sverts,
-                                                   const int* __restrict__ tri, const int* __restrict__ tri_sorted,
-                                                   const double* __restrict__ x, BpOut O, ContactParams CP,
-                                                   CcdParams CC) {
+                                                   const int* __restrict__ tri, const double* __restrict__ x,
+                                                   int* __restrict__ cnt, const int* __restrict__ off,
+                                                   int* __restrict__ pa, int* __restrict__ pb) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= V) return;
   const int v = sverts[q];
   const double* pl = T.elo + 3 * (T.P + q);
   const double* ph = T.ehi + 3 * (T.P + q);
-  int cnt = 0;
+  int n = 0, o = FILL ? off[q] : 0;
   for (int l = T.level[T.P + q]; l < T.G.nlev; ++l) {
     int c0[3], c1[3];
     hg_span(T.G, l, pl, ph, c0, c1);
@@ -485,24 +439,29 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
             const int t = T.tri_ent[e];
             const double* tl = T.elo + 3 * (int64_t)t;
             if (!boxes_meet(pl, ph, tl, T.ehi + 3 * (int64_t)t) || !hg_owns(T.G, l, a, b, c, pl, tl)) continue;
-            cnt += pt_pair<MODE>(T, O, CP, CC, x, tri, tri_sorted, v, t);
+            if (!pt_ref_pass(T, tri, x, v, q, t)) continue;
+            if (FILL) {
+              pa[o + n] = v;
+              pb[o + n] = t;
+            }
+            ++n;
           }
         }
   }
-  if (cnt) atomicAdd(&O.counter[0], cnt);
+  if (!FILL) cnt[q] = n;
 }
 
 // triangles query the points of every level above their own
-template <int MODE>
+template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const int* __restrict__ sverts,
-                                                 const int* __restrict__ tri, const int* __restrict__ tri_sorted,
-                                                 const double* __restrict__ x, BpOut O, ContactParams CP,
-                                                 CcdParams CC) {
+                                                 const int* __restrict__ tri, const double* __restrict__ x,
+                                                 int* __restrict__ cnt, const int* __restrict__ off,
+                                                 int* __restrict__ pa, int* __restrict__ pb) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= F) return;
   const double* tl = T.elo + 3 * t;
   const double* th = T.ehi + 3 * t;
-  int cnt = 0;
+  int n = 0, o = FILL ? off[t] : 0;
   for (int l = T.level[t] + 1; l < T.G.nlev; ++l) {
     int c0[3], c1[3];
     hg_span(T.G, l, tl, th, c0, c1);
@@ -514,25 +473,31 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
             const int q = T.pt_ent[e];
             const double* pl = T.elo + 3 * (T.P + q);
             if (!boxes_meet(pl, T.ehi + 3 * (T.P + q), tl, th) || !hg_owns(T.G, l, a, b, c, pl, tl)) continue;
-            cnt += pt_pair<MODE>(T, O, CP, CC, x, tri, tri_sorted, sverts[q], (int)t);
+            const int v = sverts[q];
+            if (!pt_ref_pass(T, tri, x, v, q, (int)t)) continue;
+            if (FILL) {
+              pa[o + n] = v;
+              pb[o + n] = (int)t;
+            }
+            ++n;
           }
         }
   }
-  if (cnt) atomicAdd(&O.counter[0], cnt);
+  if (!FILL) cnt[t] = n;
 }
 
 // edges query the edges of every level >= their own (equal level: higher index)
-template <int MODE>
+template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const int* __restrict__ edge,
-                                                  const double* __restrict__ x, BpOut O, ContactParams CP,
-                                                  CcdParams CC) {
+                                                  int* __restrict__ cnt, const int* __restrict__ off,
+                                                  int* __restrict__ pa, int* __restrict__ pb) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= E) return;
   const int lv = T.level[T.F + i];
   const double* il = T.elo + 3 * (T.F + i);
   const double* ih = T.ehi + 3 * (T.F + i);
   const int ia = edge[2 * i], ib = edge[2 * i + 1];
-  int cnt = 0;
+  int n = 0, o = FILL ? off[i] : 0;
   for (int l = lv; l < T.G.nlev; ++l) {
     int c0[3], c1[3];
     hg_span(T.G, l, il, ih, c0, c1);
@@ -547,25 +512,93 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
             if (!boxes_meet(il, ih, jl, T.ehi + 3 * (T.F + j)) || !hg_owns(T.G, l, a, b, c, il, jl)) continue;
             const int ja = edge[2 * j], jb = edge[2 * j + 1];
             if (ia == ja || ia == jb || ib == ja || ib == jb) continue;
-            const int lo_e = min((int)i, j), hi_e = max((int)i, j);
-            // reference join filter on (lo_e, hi_e) (geometry.py:491-499)
-            const double* li = T.flo + 3 * (T.F + lo_e);
-            const double* hi_i = T.fhi + 3 * (T.F + lo_e);
-            const double* lj = T.flo + 3 * (T.F + hi_e);
-            const double* hj = T.fhi + 3 * (T.F + hi_e);
-            bool pass = true;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) pass = pass && (li[k] <= hj[k]) && (lj[k] <= hi_i[k]);
-            if (!pass) continue;
-            if (!ref_reach(T.R, T.rlo + 3 * (T.F + lo_e), T.rhi + 3 * (T.F + lo_e), T.rlo + 3 * (T.F + hi_e),
-                           T.rhi + 3 * (T.F + hi_e)))
+            // reference join filter (geometry.py:495-498) + reachability
+            const double* li = T.flo + 3 * (T.F + i);
+            const double* hi_i = T.fhi + 3 * (T.F + i);
+            const double* lj = T.flo + 3 * (T.F + j);
+            const double* hj = T.fhi + 3 * (T.F + j);
+            if (!(li[0] <= hj[0] && li[1] <= hj[1] && li[2] <= hj[2] && lj[0] <= hi_i[0] && lj[1] <= hi_i[1] &&
+                  lj[2] <= hi_i[2]))
               continue;
-            const int vid[4] = {edge[2 * lo_e], edge[2 * lo_e + 1], edge[2 * hi_e], edge[2 * hi_e + 1]};
-            cnt += pair_work<MODE>(O, CP, CC, x, 0, vid, vid, lo_e, hi_e);
+            if (!ref_reach(T.rc, T.F + i, T.F + j)) continue;
+            if (FILL) {
+              pa[o + n] = min((int)i, j);
+              pb[o + n] = max((int)i, j);
+            }
+            ++n;
           }
         }
   }
-  if (cnt) atomicAdd(&O.counter[0], cnt);
+  if (!FILL) cnt[i] = n;
+}
+
+// ---------------------------------------------------------------------------
+// per-pair work over the list: pairs [0, n_pt) are PT, [n_pt, n) are EE
+
+__device__ __forceinline__ int warp_slot(bool emit, int* counter) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, emit);
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_pairs(int64_t n_pt, int64_t n, const int* __restrict__ pa,
+                                               const int* __restrict__ pb, const int* __restrict__ tri,
+                                               const int* __restrict__ tri_sorted, const int* __restrict__ edge,
+                                               const double* __restrict__ x, BpOut O, ContactParams CP,
+                                               CcdParams CC) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  const bool is_pt = i < n_pt;
+  int vid[4] = {0, 0, 0, 0}, vid_ccd[4] = {0, 0, 0, 0};
+  if (live) {
+    const int a = pa[i], b = pb[i];
+    if (is_pt) {
+      vid_ccd[0] = a; vid_ccd[1] = tri[3 * b]; vid_ccd[2] = tri[3 * b + 1]; vid_ccd[3] = tri[3 * b + 2];
+      // constraint set: triangle sorted by original id (contact.py:133-135);
+      // CCD: surface order (ccd.py:229-231)
+      vid[0] = a; vid[1] = tri_sorted[3 * b]; vid[2] = tri_sorted[3 * b + 1]; vid[3] = tri_sorted[3 * b + 2];
+    } else {
+      vid_ccd[0] = vid[0] = edge[2 * a]; vid_ccd[1] = vid[1] = edge[2 * a + 1];
+      vid_ccd[2] = vid[2] = edge[2 * b]; vid_ccd[3] = vid[3] = edge[2 * b + 1];
+    }
+  }
+  if (MODE == BP_CONTACT) {
+    double d = 0.0, gr[12];
+    if (live) {
+      double X[4][3];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
+      d = is_pt ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
+      if (d <= 0.0) O.counter[1] = 1;
+    }
+    const bool emit = live && d > 0.0 && d < CP.d_hat;
+    const int slot = warp_slot(emit, O.counter);
+    if (emit && slot < O.cap) write_contact(O, CP, slot, is_pt ? 1 : 0, vid, d, gr);
+  } else if (MODE == BP_CCD) {
+    if (!live) return;
+    bool cert_p = true;
+    double al = ccd_pair_alpha(x, CC.p, vid_ccd, is_pt, CC.alpha_l, &cert_p);
+    if (al < 1.0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid_ccd[r] / CC.bs], al);
+      atomic_min_nonneg(O.min_alpha, al);
+    }
+    if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
+    if (O.verts && i < O.cap) {
+      O.verts[i] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
+      O.ccd_ispt[i] = is_pt ? 1 : 0;
+      O.alpha_pair[i] = al;
+    }
+  } else if (MODE == BP_CERT) {
+    if (!live) return;
+    if (!ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, is_pt)) O.counter[1] = 1;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -576,9 +609,9 @@ struct BpGrid {
   bool empty = true;
 };
 
-// Everything one broad-phase call at (x, mb, d_hat) needs: boxes, levels and
-// the per-level cell tables of triangles / edges / surface points.
-// infl (per vertex, device) switches to tight enumeration boxes.
+// Everything one broad-phase call at (x, mb, d_hat) needs: boxes, levels,
+// reference cell ranges and the per-level cell tables of triangles / edges /
+// surface points.  infl (per vertex, device) switches to tight enumeration.
 static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, const double* infl = nullptr) {
   BpGrid B;
   const int64_t F = c->F, P = c->F + c->E, V = c->V, nobj = P + V;
@@ -615,9 +648,14 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
     }
     ext += part[7 * b + 6];
   }
-  // the reference's cell and pad (geometry.py:465-466)
-  B.T.R.cell = fmax(part[7 * nb], d_hat + mb);
-  B.T.R.pad = 0.5 * d_hat + mb;
+  auto& g = c->grid;
+  // the reference's cell and pad (geometry.py:465-466) -> per-object ranges
+  const double ref_cell = fmax(part[7 * nb], d_hat + mb);
+  const double ref_pad = 0.5 * d_hat + mb;
+  g.rc.ensure(6 * nobj);
+  k_ref_cells<<<grid_for(nobj, 256), 256, 0, st>>>(P, V, c->sverts, x, c->box_rlo, c->box_rhi, ref_pad, ref_cell,
+                                                   g.rc);
+  LAUNCH_CHECK();
   // level 0: about the mean primitive extent, at most ~4M cells
   double span = fmax(fmax(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
   if (!(span > 0.0) || !std::isfinite(span)) span = 1.0;
@@ -632,25 +670,26 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
     h0 *= 2.0;
   }
   G.h0 = h0;
+  G.inv_h0 = 1.0 / h0;
   for (int k = 0; k < 3; ++k) G.o[k] = mn[k];
   int64_t tot_cells = 0;
   G.nlev = 0;
   for (int l = 0; l < HG_MAX_LEVELS; ++l) {
     const double h = ldexp(h0, l);
-    int one = 1;
+    int small = 1;
     for (int k = 0; k < 3; ++k) {
-      double nk = floor((mx[k] - mn[k]) / h) + 1.0;
+      // as many cells as hg_coord can return (it clamps into [0, n-1])
+      double nk = floor((mx[k] - mn[k]) * ldexp(G.inv_h0, -l)) + 1.0;
       if (!(nk >= 1.0)) nk = 1.0;
       G.n[l][k] = (int)nk;
-      one = one && (G.n[l][k] <= 2);
+      small = small && (G.n[l][k] <= 2);
     }
     G.off[l] = (int)tot_cells;
     tot_cells += (int64_t)G.n[l][0] * G.n[l][1] * G.n[l][2];
     G.nlev = l + 1;
-    if (one && h >= span) break;
+    if (small && h >= span) break;
   }
   G.off[G.nlev] = (int)tot_cells;
-  auto& g = c->grid;
   g.level.ensure(nobj);
   c->cell_cnt.ensure(nobj + 1);
   c->cell_off.ensure(nobj + 1);
@@ -692,37 +731,83 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
   T.edge_start = g.edge_start; T.edge_ent = g.edge_ent;
   T.level = g.level;
-  T.flo = c->box_flo; T.fhi = c->box_fhi; T.rlo = c->box_rlo; T.rhi = c->box_rhi;
+  T.rc = g.rc;
+  T.flo = c->box_flo; T.fhi = c->box_fhi;
   T.elo = c->box_elo; T.ehi = c->box_ehi;
   B.empty = false;
   return B;
 }
 
-// Run the PT (which & 1) and EE (which & 2) queries in MODE.  Returns the
-// number of reported pairs (RAW / CONTACT: may exceed O.cap, the caller grows
-// and retries; CCD / CERT: pairs evaluated); *flag = counters[1]
-// (penetration / failed certificate); counters[2] = stored CCD pairs.
+// The reference pair list of the grid (PT if which & 1, EE if which & 2):
+// count pass, exclusive scan, fill pass.  Deterministic order: points' pairs,
+// then triangles' pairs (both PT), then edges' pairs.  Returns (n_pt, n).
+static std::pair<int64_t, int64_t> collect_pairs(mp_ctx* c, const double* x, const BpGrid& B, int which) {
+  if (B.empty) return {0, 0};
+  const int64_t V = c->V, F = c->F, E = c->E;
+  const int64_t nq = V + F + E;
+  auto& g = c->grid;
+  g.qcnt.ensure(nq + 1);
+  g.qoff.ensure(nq + 1);
+  cudaStream_t st = c->stream;
+  CUDA_CHECK(cudaMemsetAsync(g.qcnt.p, 0, sizeof(int) * (nq + 1), st));
+  if ((which & 1) && V) {
+    k_hq_points<false><<<grid_for(V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr, nullptr,
+                                                          nullptr);
+    LAUNCH_CHECK();
+    k_hq_tris<false><<<grid_for(F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr, nullptr,
+                                                        nullptr);
+    LAUNCH_CHECK();
+  }
+  if ((which & 2) && E > 1) {
+    k_hq_edges<false><<<grid_for(E, 128), 128, 0, st>>>(B.T, E, c->edge, g.qcnt.p + V + F, nullptr, nullptr,
+                                                         nullptr);
+    LAUNCH_CHECK();
+  }
+  exclusive_scan(c, g.qcnt, g.qoff, nq + 1);
+  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, g.qoff.p + V + F, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 6, g.qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, st));
+  sync_stream(c);
+  const int64_t n_pt = c->h_cnt[5], n = c->h_cnt[6];
+  g.pa.ensure(n + 1);
+  g.pb.ensure(n + 1);
+  if ((which & 1) && V && n_pt) {
+    k_hq_points<true><<<grid_for(V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa, g.pb);
+    LAUNCH_CHECK();
+    k_hq_tris<true><<<grid_for(F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, g.qoff.p + V, g.pa,
+                                                       g.pb);
+    LAUNCH_CHECK();
+  }
+  if ((which & 2) && E > 1 && n > n_pt) {
+    k_hq_edges<true><<<grid_for(E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa, g.pb);
+    LAUNCH_CHECK();
+  }
+  return {n_pt, n};
+}
+
+// Broad phase + the per-pair work of MODE.  Returns the number of reference
+// pairs (CONTACT: active constraints emitted, may exceed O.cap -- the
+// caller grows and retries); *flag = counters[1] (penetration / failed
+// certificate).  RAW leaves the list in c->grid.pa / pb and returns n,
+// with *n_pt_out the PT prefix length.
 template <int MODE>
 static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
-                      int* flag, int which = 3) {
+                      int* flag, int which = 3, int64_t* n_pt_out = nullptr) {
   CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
   O.counter = c->counters.p;
-  if (!B.empty) {
-    if ((which & 1) && c->V) {
-      k_hq_points<MODE><<<grid_for(c->V, 128), 128, 0, c->stream>>>(B.T, c->V, c->sverts, c->tri, c->tri_sorted, x,
-                                                                      O, CP, CC);
-      LAUNCH_CHECK();
-      k_hq_tris<MODE><<<grid_for(c->F, 128), 128, 0, c->stream>>>(B.T, c->F, c->sverts, c->tri, c->tri_sorted, x, O,
-                                                                    CP, CC);
-      LAUNCH_CHECK();
-    }
-    if ((which & 2) && c->E > 1) {
-      k_hq_edges<MODE><<<grid_for(c->E, 128), 128, 0, c->stream>>>(B.T, c->E, c->edge, x, O, CP, CC);
-      LAUNCH_CHECK();
-    }
+  auto nn = collect_pairs(c, x, B, which);
+  const int64_t n_pt = nn.first, n = nn.second;
+  if (n_pt_out) *n_pt_out = n_pt;
+  if (MODE == BP_RAW) {
+    if (flag) *flag = 0;
+    return n;
+  }
+  if (n) {
+    k_pairs<MODE><<<grid_for(n, 256), 256, 0, c->stream>>>(n_pt, n, c->grid.pa, c->grid.pb, c->tri, c->tri_sorted,
+                                                            c->edge, x, O, CP, CC);
+    LAUNCH_CHECK();
   }
   CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
   if (flag) *flag = c->h_cnt[1];
-  return (MODE == BP_CCD && O.verts) ? std::max<int64_t>(c->h_cnt[0], c->h_cnt[2]) : c->h_cnt[0];
+  return MODE == BP_CONTACT ? c->h_cnt[0] : n;
 }

@@ -74,6 +74,9 @@ struct PairTable {
 struct BpGridBufs {
   DBuf<int> tri_cnt, tri_start, edge_cnt, edge_start, pt_cnt, pt_start;  // (ncell+1)
   DBuf<int> level;                                                       // (objects)
+  DBuf<int> rc;                                                          // (objects*6) reference cells
+  DBuf<int> qcnt, qoff;                                                  // per-query pair counts
+  DBuf<int> pa, pb;                                                      // reference pair list
   DBuf<int> ecell, tri_ent, edge_ent, pt_ent;                            // (entries)
 };
 

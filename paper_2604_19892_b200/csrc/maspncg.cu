@@ -695,52 +695,35 @@ int mp_broad_phase(mp_ctx* c, const double* x, double motion_bound, double d_hat
     if (c->F == 0) return;
     upload_vec_new(c, x, c->x);
     BpGrid B = build_bp(c, c->x, motion_bound, d_hat);
-    // PT and EE separately so their raw lists stay apart
-    for (int pass = 0; pass < 2; ++pass) {
-      size_t cap = std::max<size_t>(c->cand_a.n, 4096);
-      for (int attempt = 0; attempt < 4; ++attempt) {
-        c->cand_a.ensure(cap);
-        c->cand_b.ensure(cap);
-        BpOut O{};
-        O.a = c->cand_a;
-        O.b = c->cand_b;
-        O.cap = (int64_t)c->cand_a.n;
-        ContactParams CP{};
-        CcdParams CC{};
-        int64_t n64 = run_bp<BP_RAW>(c, c->x, B, O, CP, CC, nullptr, pass == 0 ? 1 : 2);
-        int n = (int)n64;
-        if ((size_t)n > c->cand_a.n) {
-          cap = (size_t)n + 1024;
-          continue;
-        }
-        std::vector<int> a(n), b(n);
-        CUDA_CHECK(cudaMemcpyAsync(a.data(), c->cand_a.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_CHECK(cudaMemcpyAsync(b.data(), c->cand_b.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
-        sync_stream(c);
-        std::vector<std::pair<int64_t, int64_t>> rows(n);
-        for (int i = 0; i < n; ++i) {
-          if (pass == 0) rows[i] = {c->h_new2old[a[i]], b[i]};
-          else rows[i] = {a[i], b[i]};
-        }
-        std::sort(rows.begin(), rows.end());
-        if (pass == 0) {
-          *n_pt = n;
-          if (pt)
-            for (int i = 0; i < n && i < pt_cap; ++i) {
-              pt[2 * i] = rows[i].first;
-              pt[2 * i + 1] = rows[i].second;
-            }
-        } else {
-          *n_ee = n;
-          if (ee)
-            for (int i = 0; i < n && i < ee_cap; ++i) {
-              ee[2 * i] = rows[i].first;
-              ee[2 * i + 1] = rows[i].second;
-            }
-        }
-        break;
-      }
+    int64_t npt = 0;
+    BpOut O{};
+    ContactParams CP{};
+    CcdParams CC{};
+    const int64_t n = run_bp<BP_RAW>(c, c->x, B, O, CP, CC, nullptr, 3, &npt);
+    std::vector<int> a(n), b(n);
+    if (n) {
+      CUDA_CHECK(cudaMemcpyAsync(a.data(), c->grid.pa.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaMemcpyAsync(b.data(), c->grid.pb.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      sync_stream(c);
     }
+    // PT rows (original vertex id, triangle), EE rows (edge i, edge j); sorted
+    std::vector<std::pair<int64_t, int64_t>> pt_rows(npt), ee_rows(n - npt);
+    for (int64_t i = 0; i < npt; ++i) pt_rows[i] = {c->h_new2old[a[i]], b[i]};
+    for (int64_t i = npt; i < n; ++i) ee_rows[i - npt] = {a[i], b[i]};
+    std::sort(pt_rows.begin(), pt_rows.end());
+    std::sort(ee_rows.begin(), ee_rows.end());
+    *n_pt = (int64_t)pt_rows.size();
+    *n_ee = (int64_t)ee_rows.size();
+    if (pt)
+      for (int64_t i = 0; i < *n_pt && i < pt_cap; ++i) {
+        pt[2 * i] = pt_rows[i].first;
+        pt[2 * i + 1] = pt_rows[i].second;
+      }
+    if (ee)
+      for (int64_t i = 0; i < *n_ee && i < ee_cap; ++i) {
+        ee[2 * i] = ee_rows[i].first;
+        ee[2 * i + 1] = ee_rows[i].second;
+      }
   });
 }
 
