@@ -581,16 +581,22 @@ __global__ void __launch_bounds__(256) k_pairs(int64_t n_pt, int64_t n, const in
     const int slot = warp_slot(emit, O.counter);
     if (emit && slot < O.cap) write_contact(O, CP, slot, is_pt ? 1 : 0, vid, d, gr);
   } else if (MODE == BP_CCD) {
-    if (!live) return;
     bool cert_p = true;
-    double al = ccd_pair_alpha(x, CC.p, vid_ccd, is_pt, CC.alpha_l, &cert_p);
-    if (al < 1.0) {
+    double al = live ? ccd_pair_alpha(x, CC.p, vid_ccd, is_pt, CC.alpha_l, &cert_p) : 1.0;
+    if (live && al < 1.0) {
+      // read before the atomic: once a subdomain's minimum has settled most
+      // pairs cannot lower it, so contended atomics stay rare
 #pragma unroll
-      for (int r = 0; r < 4; ++r) atomic_min_nonneg(&O.alpha_d[vid_ccd[r] / CC.bs], al);
-      atomic_min_nonneg(O.min_alpha, al);
+      for (int r = 0; r < 4; ++r) {
+        double* ad = &O.alpha_d[vid_ccd[r] / CC.bs];
+        if (al < *(volatile double*)ad) atomic_min_nonneg(ad, al);
+      }
     }
+    // global minimum: warp minimum first, one filtered atomic per warp
+    double wm = warp_min_all(al);
+    if ((threadIdx.x & 31) == 0 && wm < *(volatile double*)O.min_alpha) atomic_min_nonneg(O.min_alpha, wm);
     if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
-    if (O.verts && i < O.cap) {
+    if (live && O.verts && i < O.cap) {
       O.verts[i] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
       O.ccd_ispt[i] = is_pt ? 1 : 0;
       O.alpha_pair[i] = al;

@@ -87,7 +87,7 @@ struct CoarseLevel {
   DBuf<double> dense; // n*n scratch (cuSOLVER workspace matrix)
   DBuf<double> inv;   // cyc_size(n) packed inverse
   DBuf<double> rsum;  // 3A restricted sums
-  DBuf<double> ypart; // chunks * n partial matvec results
+  DBuf<double> ypart; // n: M_l^-1 r accumulated over diagonal chunks
   int chunks = 1;
 };
 

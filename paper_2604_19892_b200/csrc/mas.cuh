@@ -435,9 +435,10 @@ __global__ void k_restrict_up(int A, int cb, int Afine, const double* __restrict
   out[e] = s;
 }
 
-// partial y = Minv r over a chunk of diagonals; r = rsum / |a|
+// y += Minv r over a chunk of diagonals (atomic accumulation; y zeroed by the
+// caller); r = rsum / |a|.  Many small chunks keep every SM busy.
 __global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double* __restrict__ P,
-                            const double* __restrict__ rsum, double* __restrict__ ypart) {
+                            const double* __restrict__ rsum, double* __restrict__ y) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y;
   if (i >= n) return;
@@ -445,6 +446,7 @@ __global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double
   int per = (smax + 1 + chunks - 1) / chunks;
   int s0 = ch * per, s1 = s0 + per - 1;
   if (s1 > smax) s1 = smax;
+  if (s0 > s1) return;
   auto rin = [&](int q) {
     int a = q / 3;
     int64_t na = (N - (int64_t)a * span) < span ? (N - (int64_t)a * span) : span;
@@ -465,15 +467,15 @@ __global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double
       int r = i < jp ? i : jp;
       acc += dg[r] * rin(jp);
     } else {
-      acc += dg[i] * rin(jp) + dg[jm] * rin(jm);
+      acc += __ldg(dg + i) * rin(jp) + __ldg(dg + jm) * rin(jm);
     }
   }
-  ypart[(int64_t)ch * n + i] = acc;
+  atomicAdd(&y[i], acc);
 }
 
 struct LevelView {
-  const double* ypart;
-  int n, span, chunks;
+  const double* y;
+  int n, span;
 };
 struct LevelViews {
   LevelView lv[8];
@@ -481,57 +483,56 @@ struct LevelViews {
 };
 
 // level-0 + Woodbury overlay + coarse prolongation + pinned projection.
-// One CTA per subdomain; the packed block is staged in shared memory.
-__global__ void k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
-                               const int* __restrict__ overlay_of, const double* __restrict__ overlay,
-                               const double* __restrict__ g, const unsigned char* __restrict__ pinned,
-                               LevelViews LV, double* __restrict__ z) {
-  extern __shared__ double sm[];
-  const int64_t csz = cyc_size(m);
-  double* P = sm;
-  double* gs = sm + csz;
-  const int64_t d = blockIdx.x;
-  const int ov = overlay_of ? overlay_of[d] : -1;
-  const double* src = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
-  if ((csz & 1) == 0) {
-    const double2* s2 = reinterpret_cast<const double2*>(src);
-    double2* p2 = reinterpret_cast<double2*>(P);
-    for (int64_t e = threadIdx.x; e < csz / 2; e += blockDim.x) p2[e] = __ldg(&s2[e]);
-  } else {
-    for (int64_t e = threadIdx.x; e < csz; e += blockDim.x) P[e] = __ldg(&src[e]);
-  }
+// APPLY_SPB subdomains per CTA, one thread per block row; the packed
+// diagonals are streamed from global memory (thread i reads diag_s[i] and
+// diag_s[(i - s) mod m]: two coalesced reads of the same lines, the second
+// an L1 hit), so there is no shared-memory staging of the block and
+// occupancy is register-limited only.
+#define APPLY_SPB 2
+__global__ void __launch_bounds__(APPLY_SPB * 96)
+k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
+               const int* __restrict__ overlay_of, const double* __restrict__ overlay, const double* __restrict__ g,
+               const unsigned char* __restrict__ pinned, LevelViews LV, double* __restrict__ z) {
+  __shared__ double gsh[APPLY_SPB][96];
+  const int sl = threadIdx.x / 96;
+  const int i = threadIdx.x - sl * 96;
+  const int64_t d = (int64_t)blockIdx.x * APPLY_SPB + sl;
+  const bool valid = d < D;
   const int64_t v0 = d * bs;
-  const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
-  for (int i = threadIdx.x; i < m; i += blockDim.x) gs[i] = (i < nd3) ? g[3 * v0 + i] : 0.0;
+  const int nd3 = valid ? 3 * (int)((N - v0) < bs ? (N - v0) : bs) : 0;
+  if (i < m) gsh[sl][i] = (i < nd3) ? g[3 * v0 + i] : 0.0;
   __syncthreads();
-  const bool even = (m % 2) == 0;
+  if (i >= nd3) return;
+  const int64_t csz = cyc_size(m);
+  const int ov = overlay_of ? overlay_of[d] : -1;
+  const double* P = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+  const double* gs = gsh[sl];
   const int smax = m / 2;
-  for (int i = threadIdx.x; i < nd3; i += blockDim.x) {
-    double acc = P[i] * gs[i];
-    for (int s = 1; s <= smax; ++s) {
-      const double* dg = P + (int64_t)s * m;
-      int jp = i + s; if (jp >= m) jp -= m;
-      if (even && 2 * s == m) {
-        int r = i < jp ? i : jp;
-        acc += dg[r] * gs[jp];
-      } else {
-        int jm = i - s; if (jm < 0) jm += m;
-        acc += dg[i] * gs[jp] + dg[jm] * gs[jm];
-      }
-    }
-    int64_t dof = 3 * v0 + i;
-    int64_t v = dof / 3;
-    int c = (int)(dof % 3);
-    for (int l = 0; l < LV.L; ++l) {
-      const LevelView& L = LV.lv[l];
-      int a = (int)(v / L.span);
-      int64_t na = (N - (int64_t)a * L.span) < L.span ? (N - (int64_t)a * L.span) : L.span;
-      double y = 0.0;
-      for (int ch = 0; ch < L.chunks; ++ch) y += L.ypart[(int64_t)ch * L.n + 3 * a + c];
-      acc += y / (double)na;
-    }
-    z[dof] = pinned[v] ? 0.0 : acc;
+  const bool even = (m % 2) == 0;
+  double acc = __ldg(P + i) * gs[i];
+  const int s_full = even ? smax - 1 : smax;  // full diagonals 1..s_full
+#pragma unroll 4
+  for (int s = 1; s <= s_full; ++s) {
+    const double* dg = P + (int64_t)s * m;
+    int jp = i + s; if (jp >= m) jp -= m;
+    int jm = i - s; if (jm < 0) jm += m;
+    acc += __ldg(dg + i) * gs[jp] + __ldg(dg + jm) * gs[jm];
   }
+  if (even) {
+    const double* dg = P + (int64_t)smax * m;
+    int jp = i + smax; if (jp >= m) jp -= m;
+    acc += __ldg(dg + (i < jp ? i : jp)) * gs[jp];
+  }
+  const int64_t dof = 3 * v0 + i;
+  const int64_t v = dof / 3;
+  const int c = (int)(dof % 3);
+  for (int l = 0; l < LV.L; ++l) {
+    const LevelView& L = LV.lv[l];
+    int a = (int)(v / L.span);
+    int64_t na = (N - (int64_t)a * L.span) < L.span ? (N - (int64_t)a * L.span) : L.span;
+    acc += L.y[3 * a + c] / (double)na;
+  }
+  z[dof] = pinned[v] ? 0.0 : acc;
 }
 
 // ---------------------------------------------------------------------------

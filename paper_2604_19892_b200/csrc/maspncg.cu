@@ -110,12 +110,13 @@ static void setup_levels(mp_ctx* c) {
     L->A = (int)n_agg;
     L->n = (int)(3 * n_agg);
     L->span = (int)span;
+    // ~4 blocks per SM over (row block, diagonal chunk), >= 4 diagonals each
     int rowblocks = (L->n + 127) / 128;
-    int maxch = (L->n / 2 + 1 + 31) / 32;
-    int ch = std::max(1, std::min(maxch, RED_BLOCKS / std::max(1, rowblocks)));
+    int maxch = std::max(1, (L->n / 2 + 1) / 4);
+    int ch = std::max(1, std::min(maxch, 4 * 148 / std::max(1, rowblocks)));
     L->chunks = ch;
     L->rsum.ensure(L->n);
-    L->ypart.ensure((size_t)ch * L->n);
+    L->ypart.ensure((size_t)L->n);
     c->levels.push_back(L);
     units = n_agg;
   }
@@ -139,7 +140,6 @@ static void set_smem_limits() {
   allow((const void*)k_block_sweep);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
-  allow((const void*)k_mas_apply_l0);
   done = true;
 }
 

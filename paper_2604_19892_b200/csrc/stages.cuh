@@ -273,18 +273,15 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
                                                                              L.rsum);
     }
     LAUNCH_CHECK();
+    CUDA_CHECK(cudaMemsetAsync(L.ypart.p, 0, sizeof(double) * L.n, c->stream));
     dim3 grid(grid_for(L.n, 128), L.chunks);
     k_coarse_mv<<<grid, 128, 0, c->stream>>>(L.n, c->N, L.span, L.chunks, L.inv, L.rsum, L.ypart);
     LAUNCH_CHECK();
-    LV.lv[l] = LevelView{L.ypart, L.n, L.span, L.chunks};
+    LV.lv[l] = LevelView{L.ypart, L.n, L.span};
   }
-  const int m = c->m;
-  const int threads = ((m + 31) / 32) * 32;
-  const size_t smem = sizeof(double) * (cyc_size(m) + m);
   const bool ov = with_updates && c->have_updates;
-  k_mas_apply_l0<<<(unsigned)c->D, threads, smem, c->stream>>>(c->D, c->N, c->bs, m, c->Bblk,
-                                                               ov ? c->overlay_of.p : nullptr, c->overlay, g,
-                                                               c->pinned, LV, z);
+  k_mas_apply_l0<<<(unsigned)((c->D + APPLY_SPB - 1) / APPLY_SPB), APPLY_SPB * 96, 0, c->stream>>>(
+      c->D, c->N, c->bs, c->m, c->Bblk, ov ? c->overlay_of.p : nullptr, c->overlay, g, c->pinned, LV, z);
   LAUNCH_CHECK();
 }
 
