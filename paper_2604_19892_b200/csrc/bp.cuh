@@ -333,8 +333,9 @@ __device__ __forceinline__ bool ref_reach(const int* __restrict__ rc, int64_t a,
 }
 
 // level of every object and the number of cells it covers there
-__global__ void k_obj_level(int64_t nobj, HGrid G, const double* __restrict__ lo, const double* __restrict__ hi,
-                            int* __restrict__ level, int* __restrict__ cnt) {
+__global__ void k_obj_level(int64_t nobj, int64_t F, int64_t P, HGrid G, const double* __restrict__ lo,
+                            const double* __restrict__ hi, int* __restrict__ level, int* __restrict__ cnt,
+                            unsigned* __restrict__ lmask) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nobj) return;
   const double* l0 = lo + 3 * i;
@@ -346,6 +347,10 @@ __global__ void k_obj_level(int64_t nobj, HGrid G, const double* __restrict__ lo
   hg_span(G, l, l0, h0, c0, c1);
   level[i] = l;
   cnt[i] = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
+  // which levels hold any triangle / edge / point (queries skip empty ones)
+  const int cls = i < F ? 0 : (i < P ? 1 : 2);
+  const unsigned bit = 1u << l;
+  if ((__ldg(lmask + cls) & bit) == 0) atomicOr(lmask + cls, bit);
 }
 
 __device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
@@ -399,6 +404,7 @@ struct BpTables {
   HGrid G;
   const int *pt_start, *pt_ent, *tri_start, *tri_ent, *edge_start, *edge_ent;
   const int* level;                     // (F+E+V)
+  const unsigned* lmask;                // [3] levels holding triangles / edges / points
   const int* rc;                        // (F+E+V)*6 reference-grid cell ranges
   const double *flo, *fhi;              // (F+E)*3 reference filter / join boxes
   const double *elo, *ehi;              // (F+E+V)*3 enumeration boxes
@@ -428,7 +434,9 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
   const double* pl = T.elo + 3 * (T.P + q);
   const double* ph = T.ehi + 3 * (T.P + q);
   int n = 0, o = FILL ? off[q] : 0;
+  const unsigned mask = T.lmask[0];
   for (int l = T.level[T.P + q]; l < T.G.nlev; ++l) {
+    if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_span(T.G, l, pl, ph, c0, c1);
     for (int a = c0[0]; a <= c1[0]; ++a)
@@ -462,7 +470,9 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
   const double* tl = T.elo + 3 * t;
   const double* th = T.ehi + 3 * t;
   int n = 0, o = FILL ? off[t] : 0;
+  const unsigned mask = T.lmask[2];
   for (int l = T.level[t] + 1; l < T.G.nlev; ++l) {
+    if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_span(T.G, l, tl, th, c0, c1);
     for (int a = c0[0]; a <= c1[0]; ++a)
@@ -498,7 +508,9 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
   const double* ih = T.ehi + 3 * (T.F + i);
   const int ia = edge[2 * i], ib = edge[2 * i + 1];
   int n = 0, o = FILL ? off[i] : 0;
+  const unsigned mask = T.lmask[1];
   for (int l = lv; l < T.G.nlev; ++l) {
+    if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_span(T.G, l, il, ih, c0, c1);
     for (int a = c0[0]; a <= c1[0]; ++a)
@@ -699,7 +711,10 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   g.level.ensure(nobj);
   c->cell_cnt.ensure(nobj + 1);
   c->cell_off.ensure(nobj + 1);
-  k_obj_level<<<grid_for(nobj, 256), 256, 0, st>>>(nobj, G, c->box_elo, c->box_ehi, g.level, c->cell_cnt);
+  unsigned* lmask = (unsigned*)(c->counters.p + 12);
+  CUDA_CHECK(cudaMemsetAsync(lmask, 0, 3 * sizeof(unsigned), st));
+  k_obj_level<<<grid_for(nobj, 256), 256, 0, st>>>(nobj, F, P, G, c->box_elo, c->box_ehi, g.level, c->cell_cnt,
+                                                   lmask);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + nobj, 0, sizeof(int), st));
   exclusive_scan(c, c->cell_cnt, c->cell_off, nobj + 1);
@@ -737,6 +752,7 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
   T.edge_start = g.edge_start; T.edge_ent = g.edge_ent;
   T.level = g.level;
+  T.lmask = lmask;
   T.rc = g.rc;
   T.flo = c->box_flo; T.fhi = c->box_fhi;
   T.elo = c->box_elo; T.ehi = c->box_ehi;

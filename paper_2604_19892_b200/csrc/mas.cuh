@@ -482,57 +482,115 @@ struct LevelViews {
   int L;
 };
 
-// level-0 + Woodbury overlay + coarse prolongation + pinned projection.
-// APPLY_SPB subdomains per CTA, one thread per block row; the packed
-// diagonals are streamed from global memory (thread i reads diag_s[i] and
-// diag_s[(i - s) mod m]: two coalesced reads of the same lines, the second
-// an L1 hit), so there is no shared-memory staging of the block and
-// occupancy is register-limited only.
-#define APPLY_SPB 2
-__global__ void __launch_bounds__(APPLY_SPB * 96)
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Level-0 + Woodbury overlay + coarse prolongation + pinned projection
+// (mas.py:196-205, solver.py:351-352).  Persistent CTAs walk the subdomains;
+// each packed block (m(m+1)/2 doubles, 37 KB at m = 96) is streamed into
+// shared memory by one TMA bulk copy, double-buffered so the next block's
+// copy overlaps this block's matvec.  One thread per block row reads the
+// cyclic diagonals diag_s[i], diag_s[(i-s) mod m] from shared memory.
+#define APPLY_THREADS 128
+__global__ void __launch_bounds__(APPLY_THREADS)
 k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
                const int* __restrict__ overlay_of, const double* __restrict__ overlay, const double* __restrict__ g,
                const unsigned char* __restrict__ pinned, LevelViews LV, double* __restrict__ z) {
-  __shared__ double gsh[APPLY_SPB][96];
-  const int sl = threadIdx.x / 96;
-  const int i = threadIdx.x - sl * 96;
-  const int64_t d = (int64_t)blockIdx.x * APPLY_SPB + sl;
-  const bool valid = d < D;
-  const int64_t v0 = d * bs;
-  const int nd3 = valid ? 3 * (int)((N - v0) < bs ? (N - v0) : bs) : 0;
-  if (i < m) gsh[sl][i] = (i < nd3) ? g[3 * v0 + i] : 0.0;
-  __syncthreads();
-  if (i >= nd3) return;
+  extern __shared__ __align__(16) double sm[];
   const int64_t csz = cyc_size(m);
-  const int ov = overlay_of ? overlay_of[d] : -1;
-  const double* P = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
-  const double* gs = gsh[sl];
+  const int64_t cpad = (csz + 1) & ~1ll;  // 16-byte aligned stages
+  double* buf[2] = {sm, sm + cpad};
+  double* gsh = sm + 2 * cpad;
+  __shared__ __align__(8) unsigned long long bar[2];
+  const int tid = threadIdx.x;
+  const unsigned bytes = (unsigned)(csz * sizeof(double));
+  auto src_of = [&](int64_t d) -> const double* {
+    const int ov = overlay_of ? overlay_of[d] : -1;
+    return (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int64_t d = blockIdx.x;
+  if (tid == 0 && d < D) {
+    mbar_expect_tx(&bar[0], bytes);
+    bulk_g2s(buf[0], src_of(d), bytes, &bar[0]);
+  }
   const int smax = m / 2;
   const bool even = (m % 2) == 0;
-  double acc = __ldg(P + i) * gs[i];
-  const int s_full = even ? smax - 1 : smax;  // full diagonals 1..s_full
+  const int s_full = even ? smax - 1 : smax;
+  for (int it = 0; d < D; d += gridDim.x, ++it) {
+    const int st = it & 1;
+    const int64_t dn = d + gridDim.x;
+    if (tid == 0 && dn < D) {  // prefetch the next block into the other stage
+      mbar_expect_tx(&bar[st ^ 1], bytes);
+      bulk_g2s(buf[st ^ 1], src_of(dn), bytes, &bar[st ^ 1]);
+    }
+    const int64_t v0 = d * bs;
+    const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
+    if (tid < m) gsh[tid] = (tid < nd3) ? g[3 * v0 + tid] : 0.0;
+    __syncthreads();
+    mbar_wait(&bar[st], (unsigned)((it >> 1) & 1));
+    const int i = tid;
+    if (i < nd3) {
+      const double* P = buf[st];
+      double acc = P[i] * gsh[i];
 #pragma unroll 4
-  for (int s = 1; s <= s_full; ++s) {
-    const double* dg = P + (int64_t)s * m;
-    int jp = i + s; if (jp >= m) jp -= m;
-    int jm = i - s; if (jm < 0) jm += m;
-    acc += __ldg(dg + i) * gs[jp] + __ldg(dg + jm) * gs[jm];
+      for (int s = 1; s <= s_full; ++s) {
+        const double* dg = P + (int64_t)s * m;
+        int jp = i + s; if (jp >= m) jp -= m;
+        int jm = i - s; if (jm < 0) jm += m;
+        acc += dg[i] * gsh[jp] + dg[jm] * gsh[jm];
+      }
+      if (even) {
+        const double* dg = P + (int64_t)smax * m;
+        int jp = i + smax; if (jp >= m) jp -= m;
+        acc += dg[i < jp ? i : jp] * gsh[jp];
+      }
+      const int64_t dof = 3 * v0 + i;
+      const int64_t v = dof / 3;
+      const int c = (int)(dof % 3);
+      for (int l = 0; l < LV.L; ++l) {
+        const LevelView& L = LV.lv[l];
+        int a = (int)(v / L.span);
+        int64_t na = (N - (int64_t)a * L.span) < L.span ? (N - (int64_t)a * L.span) : L.span;
+        acc += L.y[3 * a + c] / (double)na;
+      }
+      z[dof] = pinned[v] ? 0.0 : acc;
+    }
+    __syncthreads();  // stage st is free for the prefetch two iterations on
   }
-  if (even) {
-    const double* dg = P + (int64_t)smax * m;
-    int jp = i + smax; if (jp >= m) jp -= m;
-    acc += __ldg(dg + (i < jp ? i : jp)) * gs[jp];
-  }
-  const int64_t dof = 3 * v0 + i;
-  const int64_t v = dof / 3;
-  const int c = (int)(dof % 3);
-  for (int l = 0; l < LV.L; ++l) {
-    const LevelView& L = LV.lv[l];
-    int a = (int)(v / L.span);
-    int64_t na = (N - (int64_t)a * L.span) < L.span ? (N - (int64_t)a * L.span) : L.span;
-    acc += L.y[3 * a + c] / (double)na;
-  }
-  z[dof] = pinned[v] ? 0.0 : acc;
 }
 
 // ---------------------------------------------------------------------------

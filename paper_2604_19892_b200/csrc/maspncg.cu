@@ -137,6 +137,7 @@ static void set_smem_limits() {
   };
   allow((const void*)k_mas_factor);
   allow((const void*)k_mas_sweep);
+  allow((const void*)k_mas_apply_l0);
   allow((const void*)k_block_sweep);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);

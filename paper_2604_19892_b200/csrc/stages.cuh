@@ -280,8 +280,12 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
     LV.lv[l] = LevelView{L.ypart, L.n, L.span};
   }
   const bool ov = with_updates && c->have_updates;
-  k_mas_apply_l0<<<(unsigned)((c->D + APPLY_SPB - 1) / APPLY_SPB), APPLY_SPB * 96, 0, c->stream>>>(
-      c->D, c->N, c->bs, c->m, c->Bblk, ov ? c->overlay_of.p : nullptr, c->overlay, g, c->pinned, LV, z);
+  const int64_t cpad = (cyc_size(c->m) + 1) & ~1ll;
+  const size_t smem = sizeof(double) * (2 * cpad + 96);
+  const unsigned grid = (unsigned)std::min<int64_t>(c->D, 3 * 148);
+  k_mas_apply_l0<<<grid, APPLY_THREADS, smem, c->stream>>>(c->D, c->N, c->bs, c->m, c->Bblk,
+                                                           ov ? c->overlay_of.p : nullptr, c->overlay, g, c->pinned,
+                                                           LV, z);
   LAUNCH_CHECK();
 }
 
