@@ -422,18 +422,38 @@ __device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, c
   return ref_reach(T.rc, T.P + q, t);
 }
 
+// One warp per query object: lanes stride over the entries of each visited
+// cell, so a query meeting thousands of candidates (a fast CCD vertex, the
+// floor slab) is spread over 32 lanes.  Every lane runs the same loop trip
+// counts, so ballots are safe; the fill pass writes a query's pairs in entry
+// order at the offsets of the count pass (deterministic list).
+#define WARP_FULL 0xffffffffu
+
+__device__ __forceinline__ void warp_emit(bool pass, int lane, int& n, int o, int a, int b, bool fill, int* pa,
+                                          int* pb) {
+  const unsigned m = __ballot_sync(WARP_FULL, pass);
+  if (fill && pass) {
+    const int pos = o + n + __popc(m & ((1u << lane) - 1u));
+    pa[pos] = a;
+    pb[pos] = b;
+  }
+  n += __popc(m);
+}
+
 // points query the triangles of every level >= their own
 template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const int* __restrict__ sverts,
                                                    const int* __restrict__ tri, const double* __restrict__ x,
                                                    int* __restrict__ cnt, const int* __restrict__ off,
                                                    int* __restrict__ pa, int* __restrict__ pb) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= V) return;
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= V) return;  // warp-uniform
   const int v = sverts[q];
   const double* pl = T.elo + 3 * (T.P + q);
   const double* ph = T.ehi + 3 * (T.P + q);
-  int n = 0, o = FILL ? off[q] : 0;
+  int n = 0;
+  const int o = FILL ? off[q] : 0;
   const unsigned mask = T.lmask[0];
   for (int l = T.level[T.P + q]; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
@@ -443,20 +463,22 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
       for (int b = c0[1]; b <= c1[1]; ++b)
         for (int c = c0[2]; c <= c1[2]; ++c) {
           const int cell = hg_cell(T.G, l, a, b, c);
-          for (int e = T.tri_start[cell]; e < T.tri_start[cell + 1]; ++e) {
-            const int t = T.tri_ent[e];
-            const double* tl = T.elo + 3 * (int64_t)t;
-            if (!boxes_meet(pl, ph, tl, T.ehi + 3 * (int64_t)t) || !hg_owns(T.G, l, a, b, c, pl, tl)) continue;
-            if (!pt_ref_pass(T, tri, x, v, q, t)) continue;
-            if (FILL) {
-              pa[o + n] = v;
-              pb[o + n] = t;
+          const int e0 = T.tri_start[cell], e1 = T.tri_start[cell + 1];
+          for (int base = e0; base < e1; base += 32) {
+            const int e = base + lane;
+            bool pass = false;
+            int t = 0;
+            if (e < e1) {
+              t = T.tri_ent[e];
+              const double* tl = T.elo + 3 * (int64_t)t;
+              pass = boxes_meet(pl, ph, tl, T.ehi + 3 * (int64_t)t) && hg_owns(T.G, l, a, b, c, pl, tl) &&
+                     pt_ref_pass(T, tri, x, v, q, t);
             }
-            ++n;
+            warp_emit(pass, lane, n, o, v, t, FILL, pa, pb);
           }
         }
   }
-  if (!FILL) cnt[q] = n;
+  if (!FILL && lane == 0) cnt[q] = n;
 }
 
 // triangles query the points of every level above their own
@@ -465,11 +487,13 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
                                                  const int* __restrict__ tri, const double* __restrict__ x,
                                                  int* __restrict__ cnt, const int* __restrict__ off,
                                                  int* __restrict__ pa, int* __restrict__ pb) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= F) return;
   const double* tl = T.elo + 3 * t;
   const double* th = T.ehi + 3 * t;
-  int n = 0, o = FILL ? off[t] : 0;
+  int n = 0;
+  const int o = FILL ? off[t] : 0;
   const unsigned mask = T.lmask[2];
   for (int l = T.level[t] + 1; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
@@ -479,21 +503,23 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
       for (int b = c0[1]; b <= c1[1]; ++b)
         for (int c = c0[2]; c <= c1[2]; ++c) {
           const int cell = hg_cell(T.G, l, a, b, c);
-          for (int e = T.pt_start[cell]; e < T.pt_start[cell + 1]; ++e) {
-            const int q = T.pt_ent[e];
-            const double* pl = T.elo + 3 * (T.P + q);
-            if (!boxes_meet(pl, T.ehi + 3 * (T.P + q), tl, th) || !hg_owns(T.G, l, a, b, c, pl, tl)) continue;
-            const int v = sverts[q];
-            if (!pt_ref_pass(T, tri, x, v, q, (int)t)) continue;
-            if (FILL) {
-              pa[o + n] = v;
-              pb[o + n] = (int)t;
+          const int e0 = T.pt_start[cell], e1 = T.pt_start[cell + 1];
+          for (int base = e0; base < e1; base += 32) {
+            const int e = base + lane;
+            bool pass = false;
+            int v = 0;
+            if (e < e1) {
+              const int q = T.pt_ent[e];
+              const double* pl = T.elo + 3 * (T.P + q);
+              v = sverts[q];
+              pass = boxes_meet(pl, T.ehi + 3 * (T.P + q), tl, th) && hg_owns(T.G, l, a, b, c, pl, tl) &&
+                     pt_ref_pass(T, tri, x, v, q, (int)t);
             }
-            ++n;
+            warp_emit(pass, lane, n, o, v, (int)t, FILL, pa, pb);
           }
         }
   }
-  if (!FILL) cnt[t] = n;
+  if (!FILL && lane == 0) cnt[t] = n;
 }
 
 // edges query the edges of every level >= their own (equal level: higher index)
@@ -501,13 +527,17 @@ template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const int* __restrict__ edge,
                                                   int* __restrict__ cnt, const int* __restrict__ off,
                                                   int* __restrict__ pa, int* __restrict__ pb) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= E) return;
   const int lv = T.level[T.F + i];
   const double* il = T.elo + 3 * (T.F + i);
   const double* ih = T.ehi + 3 * (T.F + i);
+  const double* fli = T.flo + 3 * (T.F + i);
+  const double* fhi = T.fhi + 3 * (T.F + i);
   const int ia = edge[2 * i], ib = edge[2 * i + 1];
-  int n = 0, o = FILL ? off[i] : 0;
+  int n = 0;
+  const int o = FILL ? off[i] : 0;
   const unsigned mask = T.lmask[1];
   for (int l = lv; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
@@ -517,31 +547,31 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
       for (int b = c0[1]; b <= c1[1]; ++b)
         for (int c = c0[2]; c <= c1[2]; ++c) {
           const int cell = hg_cell(T.G, l, a, b, c);
-          for (int e = T.edge_start[cell]; e < T.edge_start[cell + 1]; ++e) {
-            const int j = T.edge_ent[e];
-            if (l == lv && j <= i) continue;
-            const double* jl = T.elo + 3 * (T.F + j);
-            if (!boxes_meet(il, ih, jl, T.ehi + 3 * (T.F + j)) || !hg_owns(T.G, l, a, b, c, il, jl)) continue;
-            const int ja = edge[2 * j], jb = edge[2 * j + 1];
-            if (ia == ja || ia == jb || ib == ja || ib == jb) continue;
-            // reference join filter (geometry.py:495-498) + reachability
-            const double* li = T.flo + 3 * (T.F + i);
-            const double* hi_i = T.fhi + 3 * (T.F + i);
-            const double* lj = T.flo + 3 * (T.F + j);
-            const double* hj = T.fhi + 3 * (T.F + j);
-            if (!(li[0] <= hj[0] && li[1] <= hj[1] && li[2] <= hj[2] && lj[0] <= hi_i[0] && lj[1] <= hi_i[1] &&
-                  lj[2] <= hi_i[2]))
-              continue;
-            if (!ref_reach(T.rc, T.F + i, T.F + j)) continue;
-            if (FILL) {
-              pa[o + n] = min((int)i, j);
-              pb[o + n] = max((int)i, j);
+          const int e0 = T.edge_start[cell], e1 = T.edge_start[cell + 1];
+          for (int base = e0; base < e1; base += 32) {
+            const int e = base + lane;
+            bool pass = false;
+            int j = 0;
+            if (e < e1) {
+              j = T.edge_ent[e];
+              const double* jl = T.elo + 3 * (T.F + j);
+              pass = !(l == lv && j <= (int)i) && boxes_meet(il, ih, jl, T.ehi + 3 * (T.F + j)) &&
+                     hg_owns(T.G, l, a, b, c, il, jl);
+              if (pass) {
+                const int ja = edge[2 * j], jb = edge[2 * j + 1];
+                const double* flj = T.flo + 3 * (T.F + j);
+                const double* fhj = T.fhi + 3 * (T.F + j);
+                // reference join filter (geometry.py:491-498) + reachability
+                pass = !(ia == ja || ia == jb || ib == ja || ib == jb) && fli[0] <= fhj[0] &&
+                       fli[1] <= fhj[1] && fli[2] <= fhj[2] && flj[0] <= fhi[0] && flj[1] <= fhi[1] &&
+                       flj[2] <= fhi[2] && ref_reach(T.rc, T.F + i, T.F + j);
+              }
             }
-            ++n;
+            warp_emit(pass, lane, n, o, min((int)i, j), max((int)i, j), FILL, pa, pb);
           }
         }
   }
-  if (!FILL) cnt[i] = n;
+  if (!FILL && lane == 0) cnt[i] = n;
 }
 
 // ---------------------------------------------------------------------------
@@ -773,15 +803,15 @@ static std::pair<int64_t, int64_t> collect_pairs(mp_ctx* c, const double* x, con
   cudaStream_t st = c->stream;
   CUDA_CHECK(cudaMemsetAsync(g.qcnt.p, 0, sizeof(int) * (nq + 1), st));
   if ((which & 1) && V) {
-    k_hq_points<false><<<grid_for(V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr, nullptr,
+    k_hq_points<false><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr, nullptr,
                                                           nullptr);
     LAUNCH_CHECK();
-    k_hq_tris<false><<<grid_for(F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr, nullptr,
+    k_hq_tris<false><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr, nullptr,
                                                         nullptr);
     LAUNCH_CHECK();
   }
   if ((which & 2) && E > 1) {
-    k_hq_edges<false><<<grid_for(E, 128), 128, 0, st>>>(B.T, E, c->edge, g.qcnt.p + V + F, nullptr, nullptr,
+    k_hq_edges<false><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, g.qcnt.p + V + F, nullptr, nullptr,
                                                          nullptr);
     LAUNCH_CHECK();
   }
@@ -793,14 +823,14 @@ static std::pair<int64_t, int64_t> collect_pairs(mp_ctx* c, const double* x, con
   g.pa.ensure(n + 1);
   g.pb.ensure(n + 1);
   if ((which & 1) && V && n_pt) {
-    k_hq_points<true><<<grid_for(V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa, g.pb);
+    k_hq_points<true><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa, g.pb);
     LAUNCH_CHECK();
-    k_hq_tris<true><<<grid_for(F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, g.qoff.p + V, g.pa,
+    k_hq_tris<true><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, g.qoff.p + V, g.pa,
                                                        g.pb);
     LAUNCH_CHECK();
   }
   if ((which & 2) && E > 1 && n > n_pt) {
-    k_hq_edges<true><<<grid_for(E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa, g.pb);
+    k_hq_edges<true><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa, g.pb);
     LAUNCH_CHECK();
   }
   return {n_pt, n};
