@@ -84,11 +84,21 @@ struct CoarseLevel {
   int A = 0;          // aggregates
   int n = 0;          // 3A dofs
   int span = 0;       // vertices per aggregate (last may be short)
-  DBuf<double> dense; // n*n scratch (cuSOLVER workspace matrix)
+  DBuf<double> dense; // n*n Galerkin matrix, swept in place
   DBuf<double> inv;   // cyc_size(n) packed inverse
   DBuf<double> rsum;  // 3A restricted sums
   DBuf<double> ypart; // n: M_l^-1 r accumulated over diagonal chunks
+  DBuf<double> dn_col, dn_W, dn_P;  // blocked-sweep scratch
   int chunks = 1;
+  // each coarse level is built on its own stream, concurrently with level 0
+  cudaStream_t st = nullptr;
+  cudaEvent_t done = nullptr;
+  cublasHandle_t blas = nullptr;
+  ~CoarseLevel() {
+    if (blas) cublasDestroy(blas);
+    if (done) cudaEventDestroy(done);
+    if (st) cudaStreamDestroy(st);
+  }
 };
 
 // CUDA-event timer of one solver stage on the context stream.  Events are
@@ -188,7 +198,7 @@ struct mp_ctx {
   std::vector<CoarseLevel*> levels;
   int n_levels = 0;
   DBuf<double> solver_work;
-  DBuf<double> dn_col, dn_W, dn_P;   // blocked dense sweep scratch
+  cudaEvent_t ev_bsr = nullptr;     // H_base ready (coarse streams wait on it)
   DBuf<int> solver_info;
   bool have_snapshot = false;
   bool have_mas = false;

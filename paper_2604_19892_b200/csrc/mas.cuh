@@ -178,6 +178,17 @@ __global__ void k_mas_factor(int64_t D, int64_t N, int bs, int m, const double* 
 // the same products), so the row is also the pivot column.
 #define SWEEP_T 6
 
+// 1/a to ~1 ulp: MUFU reciprocal seed + two Newton steps (the IEEE division
+// sits on the sweep's serial critical path)
+__device__ __forceinline__ double fast_rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Sweep every pivot of the m x m (m <= 96) symmetric matrix staged in smem
 // S (row-major); on return S holds -S^-1.  rowk: 2 x 96 smem scratch.
 // Returns false (uniformly) when a pivot is not positive.
@@ -205,7 +216,7 @@ __device__ bool sweep_core(double* S, int m, double* rowk) {
     __syncthreads();
     const double piv = rk[k];
     if (!(piv > 0.0)) return false;  // uniform across the CTA
-    const double inv = 1.0 / piv;
+    const double inv = fast_rcp(piv);
     double ci[SWEEP_T], cj[SWEEP_T];
 #pragma unroll
     for (int a = 0; a < SWEEP_T; ++a) {

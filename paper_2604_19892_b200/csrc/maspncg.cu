@@ -24,6 +24,7 @@ mp_ctx::~mp_ctx() {
   }
   if (solver) cusolverDnDestroy(solver);
   if (blas) cublasDestroy(blas);
+  if (ev_bsr) cudaEventDestroy(ev_bsr);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -117,6 +118,10 @@ static void setup_levels(mp_ctx* c) {
     L->chunks = ch;
     L->rsum.ensure(L->n);
     L->ypart.ensure((size_t)L->n);
+    CUDA_CHECK(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
+    if (cublasCreate(&L->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate (coarse)");
+    cublasSetStream(L->blas, L->st);
     c->levels.push_back(L);
     units = n_agg;
   }
@@ -154,6 +159,7 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   cusolverDnSetStream(c->solver, c->stream);
   if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate");
   cublasSetStream(c->blas, c->stream);
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bsr, cudaEventDisableTiming));
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
   CUDA_CHECK(cudaMallocHost(&c->h_cnt, 16 * sizeof(int)));

@@ -88,50 +88,70 @@ static int read_status(mp_ctx* c, int* dev) {
   return h;
 }
 
-// sym(A^-1) of a dense SPD n x n matrix (column-major, both halves valid),
-// packed in the cyclic layout -- the coarse-level _spd_inverse (mas.py:84-90,
+// sym(M^-1) of a coarse level's dense SPD matrix (column-major, both halves
+// valid), packed in the cyclic layout, on the level's own stream -- the coarse-level _spd_inverse (mas.py:84-90,
 // :167).  Blocked symmetric sweep: for each 96-wide pivot block K,
 //   P^-1 by the in-smem sweep (k_block_sweep, non-SPD pivots flagged),
 //   W = A[:,K] P^-1 (DGEMM), A -= W A[:,K]^T (rank-96 DGEMM update),
 //   A[:,K] = A[K,:]^T = W, A[K,K] = -P^-1 (k_block_fix);
 // after every block A = -M^-1.  cuBLAS DGEMM carries the O(n^3) work.
-static void dense_spd_inverse(mp_ctx* c, int n, double* A, double* packed) {
+static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   const int nb = 96;
-  cudaStream_t st = c->stream;
-  c->dn_col.ensure((size_t)n * nb);
-  c->dn_W.ensure((size_t)n * nb);
-  c->dn_P.ensure((size_t)nb * nb);
-  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 5, 0, sizeof(int), st));
+  const int n = L.n;
+  double* A = L.dense;
+  cudaStream_t st = L.st;
+  L.dn_col.ensure((size_t)n * nb);
+  L.dn_W.ensure((size_t)n * nb);
+  L.dn_P.ensure((size_t)nb * nb);
   const double one = 1.0, mone = -1.0, zero = 0.0;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int kb = std::min(nb, n - k0);
-    k_block_sweep<<<1, 256, sizeof(double) * ((size_t)kb * kb + 2 * 96), st>>>(kb, A, n, k0, c->dn_P,
-                                                                                c->counters.p + 5);
+    k_block_sweep<<<1, 256, sizeof(double) * ((size_t)kb * kb + 2 * 96), st>>>(kb, A, n, k0, L.dn_P, status);
     LAUNCH_CHECK();
-    CUDA_CHECK(cudaMemcpyAsync(c->dn_col.p, A + (size_t)k0 * n, sizeof(double) * (size_t)n * kb,
+    CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A + (size_t)k0 * n, sizeof(double) * (size_t)n * kb,
                                cudaMemcpyDeviceToDevice, st));
     // W = -colK * (-P^-1)
-    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, kb, kb, &mone, c->dn_col, n, c->dn_P, kb, &zero,
-                    c->dn_W, n) != CUBLAS_STATUS_SUCCESS)
+    if (cublasDgemm(L.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, kb, kb, &mone, L.dn_col, n, L.dn_P, kb, &zero, L.dn_W, n) !=
+        CUBLAS_STATUS_SUCCESS)
       throw MpError(MP_ERR_CUDA, "cublasDgemm (coarse W)");
     // A -= W colK^T
-    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_T, n, n, kb, &mone, c->dn_W, n, c->dn_col, n, &one, A, n) !=
+    if (cublasDgemm(L.blas, CUBLAS_OP_N, CUBLAS_OP_T, n, n, kb, &mone, L.dn_W, n, L.dn_col, n, &one, A, n) !=
         CUBLAS_STATUS_SUCCESS)
       throw MpError(MP_ERR_CUDA, "cublasDgemm (coarse update)");
     c->launches += 2;
-    k_block_fix<<<grid_for((int64_t)n * kb, 256), 256, 0, st>>>(n, kb, k0, c->dn_W, c->dn_P, A);
+    k_block_fix<<<grid_for((int64_t)n * kb, 256), 256, 0, st>>>(n, kb, k0, L.dn_W, L.dn_P, A);
     LAUNCH_CHECK();
   }
-  (void)one;
-  k_pack_neg_sym<<<grid_for(cyc_size(n), 256), 256, 0, st>>>(n, A, packed);
+  k_pack_neg_sym<<<grid_for(cyc_size(n), 256), 256, 0, st>>>(n, A, L.inv);
   LAUNCH_CHECK();
-  if (read_status(c, c->counters.p + 5)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
 }
 
 // build_hierarchy (mas.py:138-179) from the BSR + base contacts
 static void mas_build(mp_ctx* c) {
   const int m = c->m;
   const int64_t D = c->D;
+  // coarse levels: own streams, concurrent with the level-0 blocks below
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, 8 * sizeof(int), c->stream));
+  CUDA_CHECK(cudaEventRecord(c->ev_bsr, c->stream));
+  for (int l = 0; l < c->n_levels; ++l) {
+    CoarseLevel& L = *c->levels[l];
+    cudaStream_t st = L.st;
+    CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_bsr, 0));
+    L.dense.zero((size_t)L.n * L.n, st);
+    k_bsr_to_coarse<<<grid_for(c->N, 128), 128, 0, st>>>(c->N, c->rowptr, c->cols, c->bsr, L.span, L.n, L.dense);
+    LAUNCH_CHECK();
+    if (c->base.count) {
+      k_contact_coarse<<<grid_for(c->base.count, 128), 128, 0, st>>>(c->base.count, c->base.verts, c->base.grad,
+                                                                      c->base.k, c->N, L.span, L.n, L.dense);
+      LAUNCH_CHECK();
+    }
+    k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense);
+    LAUNCH_CHECK();
+    L.inv.ensure((size_t)cyc_size(L.n));
+    dense_spd_inverse(c, L, c->counters.p + 4 + std::min(l, 3));
+    CUDA_CHECK(cudaEventRecord(L.done, st));
+  }
+  // level 0
   c->Mfull.zero((size_t)D * m * m, c->stream);
   c->Bblk.ensure((size_t)D * cyc_size(m));
   c->Mblk.ensure((size_t)D * cyc_size(m));
@@ -142,28 +162,17 @@ static void mas_build(mp_ctx* c) {
   }
   k_bsr_to_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, c->bs, m, c->Mfull);
   LAUNCH_CHECK();
-  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, sizeof(int), c->stream));
   const size_t smem = sizeof(double) * ((size_t)m * m + 2 * 96);
   k_mas_sweep<<<(unsigned)D, 256, smem, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
                                                       c->counters.p + 3);
   LAUNCH_CHECK();
-  if (read_status(c, c->counters.p + 3)) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
-  for (int l = 0; l < c->n_levels; ++l) {
-    CoarseLevel& L = *c->levels[l];
-    L.dense.zero((size_t)L.n * L.n, c->stream);
-    k_bsr_to_coarse<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, L.span, L.n,
-                                                                L.dense);
-    LAUNCH_CHECK();
-    if (c->base.count) {
-      k_contact_coarse<<<grid_for(c->base.count, 128), 128, 0, c->stream>>>(
-          c->base.count, c->base.verts, c->base.grad, c->base.k, c->N, L.span, L.n, L.dense);
-      LAUNCH_CHECK();
-    }
-    k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, c->stream>>>(L.n, L.dense);
-    LAUNCH_CHECK();
-    L.inv.ensure((size_t)cyc_size(L.n));
-    dense_spd_inverse(c, L.n, L.dense, L.inv);
-  }
+  for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
+  // one readback of every level's non-SPD flag (counters 3..7)
+  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 8, c->counters.p + 3, 5 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync_stream(c);
+  if (c->h_cnt[8]) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
+  for (int q = 1; q < 5; ++q)
+    if (c->h_cnt[8 + q]) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
   c->have_mas = true;
 }
 
