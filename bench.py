@@ -179,32 +179,16 @@ def run_reference(args):
 
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     from paper_2604_19892_b200 import scenes, solver
 
-    ws, rank, local = _dist()
+    from paper_2604_19892_b200.replicas import ReplicaGroup
+
+    _, _, local = _dist()
     torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if ws > 1:
-            dist.barrier()
-
-    def allmax(v):
-        if ws == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def allsum(v):
-        if ws == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    grp = ReplicaGroup.from_env("nccl")
+    ws, rank = grp.world_size, grp.rank
+    barrier, allmax, allsum = grp.barrier, grp.allmax, grp.allsum
 
     scene = scenes.c2_stack(gap=GAP)
     cfg = solver.SolverConfig(iter_max=args.iter_max or ITER_MAX)
@@ -273,8 +257,7 @@ def run_ours(args):
     e2e_all = allsum(float(e2e_iters))
 
     if rank != 0:
-        if ws > 1:
-            dist.destroy_process_group()
+        grp.close()
         return
 
     peaks, peak_kind = _peaks()
@@ -308,7 +291,9 @@ def run_ours(args):
         "e2e": {"value": e2e_all / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": 2 * 8 * n3,
                 "d2h_bytes_per_step": 2 * 8 * n3, "sec_per_frame": e2e_s / args.steps,
                 "api": "paper_2604_19892_b200.solver.step(scene, x, v, h, cfg) with pinned numpy x, v"},
-        "roofline": roof("mas_apply", "MAS apply: k_restrict1 + k_coarse_mv + k_mas_apply_l0"),
+        "roofline": roof("mas_apply_l0", "k_mas_apply_l0 (level-0 block matvec + Woodbury overlay + coarse "
+                                          "prolongation + pinned projection; TMA-staged packed blocks)"),
+        "roofline_mas_stage": roof("mas_apply", "MAS apply stage: k_restrict1 + k_coarse_mv x2 + k_mas_apply_l0"),
         "roofline_gradient": roof("gradient", "gradient: k_inertia_grad + k_tet_grad + k_contact_grad"),
         "roofline_hvp": roof("hvp", "HVP: k_bsr_spmv + k_rank1_apply"),
         "stages": stage_share,
@@ -321,8 +306,7 @@ def run_ours(args):
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "unavailable": repr(e)[:200]}
     print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    grp.close()
 
 
 def main():

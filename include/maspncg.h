@@ -200,7 +200,8 @@ enum {
   MP_STAGE_MAS_BUILD = 5,      /* build_hierarchy          mas.py:138-179    */
   MP_STAGE_UPDATE = 6,         /* classify/top-K/Woodbury  solver.py:337-346 */
   MP_STAGE_CCD = 7,            /* CCD clamp                solver.py:268-280 */
-  MP_STAGE_COUNT = 8
+  MP_STAGE_MAS_L0 = 8,         /* the level-0 kernel of the MAS apply alone   */
+  MP_STAGE_COUNT = 9
 };
 int mp_stage_timing(mp_ctx* ctx, int enable);
 

@@ -297,8 +297,9 @@ k_block_sweep(int kb, const double* __restrict__ A, int lda, int k0, double* __r
   extern __shared__ double sm[];
   double* S = sm;
   double* rowk = sm + kb * kb;
+  // coalesced along the column; A is symmetric so the staged layout is too
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    int i = e / kb, j = e - (e / kb) * kb;
+    int j = e / kb, i = e - j * kb;
     S[e] = A[(int64_t)(k0 + j) * lda + k0 + i];
   }
   __syncthreads();
@@ -530,7 +531,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 // shared memory by one TMA bulk copy, double-buffered so the next block's
 // copy overlaps this block's matvec.  One thread per block row reads the
 // cyclic diagonals diag_s[i], diag_s[(i-s) mod m] from shared memory.
-#define APPLY_THREADS 128
+#define APPLY_THREADS 192  // two 96-thread groups split the diagonals of a block
+#define APPLY_CHUNKS 4      // bulk copies per block (more TMA requests in flight)
 __global__ void __launch_bounds__(APPLY_THREADS)
 k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
                const int* __restrict__ overlay_of, const double* __restrict__ overlay, const double* __restrict__ g,
@@ -539,13 +541,23 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
   const int64_t csz = cyc_size(m);
   const int64_t cpad = (csz + 1) & ~1ll;  // 16-byte aligned stages
   double* buf[2] = {sm, sm + cpad};
-  double* gsh = sm + 2 * cpad;
+  double* gsh = sm + 2 * cpad;       // 96
+  double* part = gsh + 96;           // 96 partial sums of the second group
   __shared__ __align__(8) unsigned long long bar[2];
   const int tid = threadIdx.x;
-  const unsigned bytes = (unsigned)(csz * sizeof(double));
-  auto src_of = [&](int64_t d) -> const double* {
+  const int grp = tid >= 96 ? 1 : 0;
+  const int i = tid - 96 * grp;
+  // chunk boundaries in doubles, multiples of 2 (16 B)
+  const int64_t chunk = ((csz + APPLY_CHUNKS - 1) / APPLY_CHUNKS + 1) & ~1ll;
+  auto issue = [&](int stage, int64_t d) {
     const int ov = overlay_of ? overlay_of[d] : -1;
-    return (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+    const double* src = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+    mbar_expect_tx(&bar[stage], (unsigned)(csz * sizeof(double)));
+    for (int q = 0; q < APPLY_CHUNKS; ++q) {
+      const int64_t b0 = q * chunk;
+      const int64_t b1 = (b0 + chunk < csz) ? b0 + chunk : csz;
+      if (b1 > b0) bulk_g2s(buf[stage] + b0, src + b0, (unsigned)((b1 - b0) * sizeof(double)), &bar[stage]);
+    }
   };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -554,41 +566,42 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
   }
   __syncthreads();
   int64_t d = blockIdx.x;
-  if (tid == 0 && d < D) {
-    mbar_expect_tx(&bar[0], bytes);
-    bulk_g2s(buf[0], src_of(d), bytes, &bar[0]);
-  }
+  if (tid == 0 && d < D) issue(0, d);
   const int smax = m / 2;
   const bool even = (m % 2) == 0;
   const int s_full = even ? smax - 1 : smax;
+  const int s_mid = s_full / 2;  // group 0: 1..s_mid, group 1: s_mid+1..s_full (+ half diagonal)
   for (int it = 0; d < D; d += gridDim.x, ++it) {
     const int st = it & 1;
     const int64_t dn = d + gridDim.x;
-    if (tid == 0 && dn < D) {  // prefetch the next block into the other stage
-      mbar_expect_tx(&bar[st ^ 1], bytes);
-      bulk_g2s(buf[st ^ 1], src_of(dn), bytes, &bar[st ^ 1]);
-    }
+    if (tid == 0 && dn < D) issue(st ^ 1, dn);  // prefetch the next block into the other stage
     const int64_t v0 = d * bs;
     const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
     if (tid < m) gsh[tid] = (tid < nd3) ? g[3 * v0 + tid] : 0.0;
     __syncthreads();
     mbar_wait(&bar[st], (unsigned)((it >> 1) & 1));
-    const int i = tid;
+    const double* P = buf[st];
+    double acc = 0.0;
     if (i < nd3) {
-      const double* P = buf[st];
-      double acc = P[i] * gsh[i];
+      const int s0 = grp ? s_mid + 1 : 1, s1 = grp ? s_full : s_mid;
+      if (!grp) acc = P[i] * gsh[i];
 #pragma unroll 4
-      for (int s = 1; s <= s_full; ++s) {
+      for (int s = s0; s <= s1; ++s) {
         const double* dg = P + (int64_t)s * m;
         int jp = i + s; if (jp >= m) jp -= m;
         int jm = i - s; if (jm < 0) jm += m;
         acc += dg[i] * gsh[jp] + dg[jm] * gsh[jm];
       }
-      if (even) {
+      if (grp && even) {
         const double* dg = P + (int64_t)smax * m;
         int jp = i + smax; if (jp >= m) jp -= m;
         acc += dg[i < jp ? i : jp] * gsh[jp];
       }
+      if (grp) part[i] = acc;
+    }
+    __syncthreads();
+    if (!grp && i < nd3) {
+      acc += part[i];
       const int64_t dof = 3 * v0 + i;
       const int64_t v = dof / 3;
       const int c = (int)(dof % 3);
@@ -600,7 +613,9 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
       }
       z[dof] = pinned[v] ? 0.0 : acc;
     }
-    __syncthreads();  // stage st is free for the prefetch two iterations on
+    // stage st and gsh / part are reused: the next iteration's first barrier
+    // orders these reads before any overwrite (the prefetch into st waits
+    // for it + 2, issued after that barrier)
   }
 }
 

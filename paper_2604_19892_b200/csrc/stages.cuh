@@ -290,12 +290,18 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   }
   const bool ov = with_updates && c->have_updates;
   const int64_t cpad = (cyc_size(c->m) + 1) & ~1ll;
-  const size_t smem = sizeof(double) * (2 * cpad + 96);
+  const size_t smem = sizeof(double) * (2 * cpad + 2 * 96);
   const unsigned grid = (unsigned)std::min<int64_t>(c->D, 3 * 148);
+  timer_begin(c, MP_STAGE_MAS_L0);
   k_mas_apply_l0<<<grid, APPLY_THREADS, smem, c->stream>>>(c->D, c->N, c->bs, c->m, c->Bblk,
                                                            ov ? c->overlay_of.p : nullptr, c->overlay, g, c->pinned,
                                                            LV, z);
   LAUNCH_CHECK();
+  // algorithmic bytes of this kernel: every packed block once, g and z,
+  // the coarse corrections it reads (3 A_l doubles per level)
+  double l0_bytes = 8.0 * (double)c->D * (double)cyc_size(c->m) + 48.0 * c->N;
+  for (int l = 0; l < c->n_levels; ++l) l0_bytes += 8.0 * c->levels[l]->n;
+  timer_end(c, MP_STAGE_MAS_L0, l0_bytes);
 }
 
 // HessianModel.hvp (energy.py:435-440): H_base v + sum u (u^T v)
