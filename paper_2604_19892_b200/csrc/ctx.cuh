@@ -86,7 +86,8 @@ struct CoarseLevel {
   int span = 0;       // vertices per aggregate (last may be short)
   DBuf<double> dense; // n*n Galerkin matrix, swept in place
   DBuf<double> inv;   // cyc_size(n) packed inverse
-  DBuf<double> rsum;  // 3A restricted sums
+  DBuf<double> rsum;  // 3A restricted raw sums
+  DBuf<double> r;     // 3A restriction C_l g (averages)
   DBuf<double> ypart; // n: M_l^-1 r accumulated over diagonal chunks
   DBuf<double> dn_col, dn_W, dn_P;  // blocked-sweep scratch
   int chunks = 1;
@@ -118,6 +119,9 @@ struct mp_ctx {
   bool timing = false;
   bool ccd_exact_set = false;
   bool record_energy = false;
+  bool apply_tma = true;     // level-0 apply staging: TMA bulk (true) or cp.async
+  int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
+  int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
   StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;

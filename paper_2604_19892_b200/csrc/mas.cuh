@@ -409,8 +409,11 @@ __global__ void k_pack_coarse(int n, const double* __restrict__ M, double* __res
 // ---------------------------------------------------------------------------
 // apply
 
-// raw sums of g over each level-1 aggregate (one CTA per aggregate)
-__global__ void k_restrict1(int64_t N, int span, const double* __restrict__ g, double* __restrict__ rsum) {
+// raw sums of g over each level-1 aggregate (one CTA per aggregate) and the
+// restriction r = C g = raw sum * (1 / |a|) (the reference's aggregation
+// weights 1/len(verts), mas.py:123-135)
+__global__ void k_restrict1(int64_t N, int span, const double* __restrict__ g, double* __restrict__ rsum,
+                            double* __restrict__ r) {
   const int64_t a = blockIdx.x;
   const int64_t v0 = a * span;
   int64_t v1 = v0 + span;
@@ -434,23 +437,28 @@ __global__ void k_restrict1(int64_t N, int span, const double* __restrict__ g, d
     double t = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sh[threadIdx.x][q];
     rsum[3 * a + threadIdx.x] = t;
+    r[3 * a + threadIdx.x] = t * (1.0 / (double)(v1 - v0));
   }
 }
 
-// raw sums of a coarser level from the finer level's raw sums
-__global__ void k_restrict_up(int A, int cb, int Afine, const double* __restrict__ fine, double* __restrict__ out) {
+// raw sums of a coarser level from the finer level's raw sums, and its r
+__global__ void k_restrict_up(int A, int cb, int Afine, int64_t N, int span, const double* __restrict__ fine,
+                              double* __restrict__ out, double* __restrict__ r) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= 3 * (int64_t)A) return;
   int a = (int)(e / 3), c = (int)(e % 3);
   double s = 0.0;
   for (int q = a * cb; q < (a + 1) * cb && q < Afine; ++q) s += fine[3 * q + c];
   out[e] = s;
+  const int64_t v0 = (int64_t)a * span;
+  const int64_t na = (N - v0) < span ? (N - v0) : span;
+  r[e] = s * (1.0 / (double)na);
 }
 
 // y += Minv r over a chunk of diagonals (atomic accumulation; y zeroed by the
 // caller); r = rsum / |a|.  Many small chunks keep every SM busy.
-__global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double* __restrict__ P,
-                            const double* __restrict__ rsum, double* __restrict__ y) {
+__global__ void k_coarse_mv(int n, int chunks, const double* __restrict__ P, const double* __restrict__ r,
+                            double* __restrict__ y) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y;
   if (i >= n) return;
@@ -459,16 +467,11 @@ __global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double
   int s0 = ch * per, s1 = s0 + per - 1;
   if (s1 > smax) s1 = smax;
   if (s0 > s1) return;
-  auto rin = [&](int q) {
-    int a = q / 3;
-    int64_t na = (N - (int64_t)a * span) < span ? (N - (int64_t)a * span) : span;
-    return rsum[q] / (double)na;
-  };
   double acc = 0.0;
   const bool even = (n % 2) == 0;
   for (int s = s0; s <= s1; ++s) {
     if (s == 0) {
-      acc += P[i] * rin(i);
+      acc += P[i] * r[i];
       continue;
     }
     const double* dg = P + (int64_t)s * n;
@@ -476,10 +479,9 @@ __global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double
     int jm = i - s; if (jm < 0) jm += n;
     if (even && 2 * s == n) {
       // half diagonal: A(i, i+n/2) stored at min(i, i+n/2)
-      int r = i < jp ? i : jp;
-      acc += dg[r] * rin(jp);
+      acc += dg[i < jp ? i : jp] * r[jp];
     } else {
-      acc += __ldg(dg + i) * rin(jp) + __ldg(dg + jm) * rin(jm);
+      acc += __ldg(dg + i) * r[jp] + __ldg(dg + jm) * r[jm];
     }
   }
   atomicAdd(&y[i], acc);
@@ -487,7 +489,7 @@ __global__ void k_coarse_mv(int n, int64_t N, int span, int chunks, const double
 
 struct LevelView {
   const double* y;
-  int n, span;
+  int n, span, ratio;  // ratio = span / bs: subdomains per aggregate
 };
 struct LevelViews {
   LevelView lv[8];
@@ -533,6 +535,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 // cyclic diagonals diag_s[i], diag_s[(i-s) mod m] from shared memory.
 #define APPLY_THREADS 192  // two 96-thread groups split the diagonals of a block
 #define APPLY_CHUNKS 4      // bulk copies per block (more TMA requests in flight)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// USE_TMA: one elected thread streams each packed block with cp.async.bulk
+// (TMA, completes on an mbarrier); otherwise every thread issues 16-byte
+// cp.async (LDGSTS) copies -- same double buffering, more requests in flight.
+template <bool USE_TMA, int STAGES>
 __global__ void __launch_bounds__(APPLY_THREADS)
 k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
                const int* __restrict__ overlay_of, const double* __restrict__ overlay, const double* __restrict__ g,
@@ -540,18 +556,23 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
   extern __shared__ __align__(16) double sm[];
   const int64_t csz = cyc_size(m);
   const int64_t cpad = (csz + 1) & ~1ll;  // 16-byte aligned stages
-  double* buf[2] = {sm, sm + cpad};
-  double* gsh = sm + 2 * cpad;       // 96
+  double* buf[STAGES];
+#pragma unroll
+  for (int q = 0; q < STAGES; ++q) buf[q] = sm + q * cpad;
+  double* gsh = sm + STAGES * cpad;  // 96
   double* part = gsh + 96;           // 96 partial sums of the second group
-  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ __align__(8) unsigned long long bar[STAGES];
   const int tid = threadIdx.x;
   const int grp = tid >= 96 ? 1 : 0;
   const int i = tid - 96 * grp;
   // chunk boundaries in doubles, multiples of 2 (16 B)
   const int64_t chunk = ((csz + APPLY_CHUNKS - 1) / APPLY_CHUNKS + 1) & ~1ll;
-  auto issue = [&](int stage, int64_t d) {
+  auto src_of = [&](int64_t d) -> const double* {
     const int ov = overlay_of ? overlay_of[d] : -1;
-    const double* src = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+    return (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+  };
+  auto issue = [&](int stage, int64_t d) {  // TMA: thread 0 only
+    const double* src = src_of(d);
     mbar_expect_tx(&bar[stage], (unsigned)(csz * sizeof(double)));
     for (int q = 0; q < APPLY_CHUNKS; ++q) {
       const int64_t b0 = q * chunk;
@@ -559,27 +580,54 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
       if (b1 > b0) bulk_g2s(buf[stage] + b0, src + b0, (unsigned)((b1 - b0) * sizeof(double)), &bar[stage]);
     }
   };
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+  auto issue_async = [&](int stage, int64_t d) {  // LDGSTS: every thread
+    const double* src = src_of(d);
+    const int64_t n16 = csz / 2;  // 16-byte chunks (csz is even for m = 96)
+    for (int64_t e = tid; e < n16; e += APPLY_THREADS) cp_async16(buf[stage] + 2 * e, src + 2 * e);
+    if ((csz & 1) && tid == 0) buf[stage][csz - 1] = src[csz - 1];
+    cp_async_commit();
+  };
+  if (USE_TMA && tid == 0) {
+    for (int q = 0; q < STAGES; ++q) mbar_init(&bar[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
+  // prologue: the first STAGES-1 blocks of this CTA
+  for (int q = 0; q < STAGES - 1; ++q) {
+    const int64_t dq = blockIdx.x + (int64_t)q * gridDim.x;
+    if (USE_TMA) {
+      if (tid == 0 && dq < D) issue(q, dq);
+    } else {
+      if (dq < D) issue_async(q, dq);
+      else cp_async_commit();
+    }
+  }
   int64_t d = blockIdx.x;
-  if (tid == 0 && d < D) issue(0, d);
   const int smax = m / 2;
   const bool even = (m % 2) == 0;
   const int s_full = even ? smax - 1 : smax;
   const int s_mid = s_full / 2;  // group 0: 1..s_mid, group 1: s_mid+1..s_full (+ half diagonal)
   for (int it = 0; d < D; d += gridDim.x, ++it) {
-    const int st = it & 1;
-    const int64_t dn = d + gridDim.x;
-    if (tid == 0 && dn < D) issue(st ^ 1, dn);  // prefetch the next block into the other stage
+    const int st = it % STAGES;
+    const int64_t dn = d + (int64_t)(STAGES - 1) * gridDim.x;
+    const int sn = (it + STAGES - 1) % STAGES;
+    // prefetch STAGES-1 blocks ahead into the stage freed by iteration it-1
+    if (USE_TMA) {
+      if (tid == 0 && dn < D) issue(sn, dn);
+    } else {
+      if (dn < D) issue_async(sn, dn);
+      else cp_async_commit();  // empty group keeps the wait_group count uniform
+    }
     const int64_t v0 = d * bs;
     const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
     if (tid < m) gsh[tid] = (tid < nd3) ? g[3 * v0 + tid] : 0.0;
-    __syncthreads();
-    mbar_wait(&bar[st], (unsigned)((it >> 1) & 1));
+    if (USE_TMA) {
+      __syncthreads();
+      mbar_wait(&bar[st], (unsigned)((it / STAGES) & 1));
+    } else {
+      cp_async_wait<STAGES - 1>();  // this block's group has landed (prefetches may still fly)
+      __syncthreads();
+    }
     const double* P = buf[st];
     double acc = 0.0;
     if (i < nd3) {
@@ -602,14 +650,15 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
     __syncthreads();
     if (!grp && i < nd3) {
       acc += part[i];
+      // prolongation C^T y: y of the vertex's aggregate times 1/|a|
       const int64_t dof = 3 * v0 + i;
-      const int64_t v = dof / 3;
-      const int c = (int)(dof % 3);
+      const int64_t v = v0 + i / 3;
+      const int c = i - 3 * (i / 3);
       for (int l = 0; l < LV.L; ++l) {
         const LevelView& L = LV.lv[l];
-        int a = (int)(v / L.span);
-        int64_t na = (N - (int64_t)a * L.span) < L.span ? (N - (int64_t)a * L.span) : L.span;
-        acc += L.y[3 * a + c] / (double)na;
+        const int64_t a = d / L.ratio;
+        const int64_t na = (N - a * L.span) < L.span ? (N - a * L.span) : L.span;
+        acc += L.y[3 * a + c] * (1.0 / (double)na);
       }
       z[dof] = pinned[v] ? 0.0 : acc;
     }

@@ -117,6 +117,7 @@ static void setup_levels(mp_ctx* c) {
     int ch = std::max(1, std::min(maxch, 4 * 148 / std::max(1, rowblocks)));
     L->chunks = ch;
     L->rsum.ensure(L->n);
+    L->r.ensure(L->n);
     L->ypart.ensure((size_t)L->n);
     CUDA_CHECK(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
@@ -142,7 +143,10 @@ static void set_smem_limits() {
   };
   allow((const void*)k_mas_factor);
   allow((const void*)k_mas_sweep);
-  allow((const void*)k_mas_apply_l0);
+  allow((const void*)k_mas_apply_l0<true, 2>);
+  allow((const void*)k_mas_apply_l0<false, 2>);
+  allow((const void*)k_mas_apply_l0<true, 3>);
+  allow((const void*)k_mas_apply_l0<false, 3>);
   allow((const void*)k_block_sweep);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
@@ -558,6 +562,9 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
   return guarded(c, [&] {
     if (option == MP_OPT_CCD_EXACT_SET) c->ccd_exact_set = value != 0;
     else if (option == MP_OPT_RECORD_ENERGY) c->record_energy = value != 0;
+    else if (option == MP_OPT_APPLY_TMA) c->apply_tma = value != 0;
+    else if (option == MP_OPT_APPLY_STAGES) c->apply_stages = value == 3 ? 3 : 2;
+    else if (option == MP_OPT_APPLY_CTAS) c->apply_ctas_per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, value));
     else throw MpError(MP_ERR_CONFIG, "unknown option");
   });
 }

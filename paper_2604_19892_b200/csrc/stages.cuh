@@ -275,27 +275,35 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   for (int l = 0; l < c->n_levels; ++l) {
     CoarseLevel& L = *c->levels[l];
     if (l == 0) {
-      k_restrict1<<<L.A, 128, 0, c->stream>>>(c->N, L.span, g, L.rsum);
+      k_restrict1<<<L.A, 128, 0, c->stream>>>(c->N, L.span, g, L.rsum, L.r);
     } else {
       CoarseLevel& F = *c->levels[l - 1];
-      k_restrict_up<<<grid_for(3 * (int64_t)L.A, 128), 128, 0, c->stream>>>(L.A, c->cfg.coarse_block, F.A, F.rsum,
-                                                                             L.rsum);
+      k_restrict_up<<<grid_for(3 * (int64_t)L.A, 128), 128, 0, c->stream>>>(L.A, c->cfg.coarse_block, F.A, c->N,
+                                                                             L.span, F.rsum, L.rsum, L.r);
     }
     LAUNCH_CHECK();
     CUDA_CHECK(cudaMemsetAsync(L.ypart.p, 0, sizeof(double) * L.n, c->stream));
     dim3 grid(grid_for(L.n, 128), L.chunks);
-    k_coarse_mv<<<grid, 128, 0, c->stream>>>(L.n, c->N, L.span, L.chunks, L.inv, L.rsum, L.ypart);
+    k_coarse_mv<<<grid, 128, 0, c->stream>>>(L.n, L.chunks, L.inv, L.r, L.ypart);
     LAUNCH_CHECK();
-    LV.lv[l] = LevelView{L.ypart, L.n, L.span};
+    LV.lv[l] = LevelView{L.ypart, L.n, L.span, L.span / c->bs};
   }
   const bool ov = with_updates && c->have_updates;
   const int64_t cpad = (cyc_size(c->m) + 1) & ~1ll;
-  const size_t smem = sizeof(double) * (2 * cpad + 2 * 96);
-  const unsigned grid = (unsigned)std::min<int64_t>(c->D, 3 * 148);
+  const int stages = c->apply_stages == 3 ? 3 : 2;
+  const size_t smem = sizeof(double) * (stages * cpad + 2 * 96);
+  const unsigned grid = (unsigned)std::min<int64_t>(c->D, (int64_t)c->apply_ctas_per_sm * 148);
   timer_begin(c, MP_STAGE_MAS_L0);
-  k_mas_apply_l0<<<grid, APPLY_THREADS, smem, c->stream>>>(c->D, c->N, c->bs, c->m, c->Bblk,
-                                                           ov ? c->overlay_of.p : nullptr, c->overlay, g, c->pinned,
-                                                           LV, z);
+  const int* ovp = ov ? c->overlay_of.p : nullptr;
+#define L0_ARGS c->D, c->N, c->bs, c->m, c->Bblk, ovp, c->overlay, g, c->pinned, LV, z
+  if (c->apply_tma) {
+    if (stages == 3) k_mas_apply_l0<true, 3><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
+    else k_mas_apply_l0<true, 2><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
+  } else {
+    if (stages == 3) k_mas_apply_l0<false, 3><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
+    else k_mas_apply_l0<false, 2><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
+  }
+#undef L0_ARGS
   LAUNCH_CHECK();
   // algorithmic bytes of this kernel: every packed block once, g and z,
   // the coarse corrections it reads (3 A_l doubles per level)
