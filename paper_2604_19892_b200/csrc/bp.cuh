@@ -364,12 +364,13 @@ __device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
 
 // one thread per (object, covered cell) entry: its global cell id and the
 // per-class histograms (0 triangles, 1 edges, 2 points)
-__global__ void k_entry_hist(int64_t total, int64_t nobj, int64_t F, int64_t P, HGrid G, const int* __restrict__ off,
+__global__ void k_entry_hist(const int* __restrict__ total_dev, int64_t nobj, int64_t F, int64_t P, HGrid G,
+                             const int* __restrict__ off,
                              const int* __restrict__ level, const double* __restrict__ lo,
                              const double* __restrict__ hi, int* __restrict__ ecell, int* __restrict__ tri_cnt,
                              int* __restrict__ edge_cnt, int* __restrict__ pt_cnt) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= total) return;
+  if (e >= *total_dev) return;
   int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
   int r = (int)e - off[p];
   int l = level[p];
@@ -381,13 +382,14 @@ __global__ void k_entry_hist(int64_t total, int64_t nobj, int64_t F, int64_t P, 
   atomicAdd(p < F ? &tri_cnt[cell] : (p < P ? &edge_cnt[cell] : &pt_cnt[cell]), 1);
 }
 
-__global__ void k_entry_fill(int64_t total, int64_t nobj, int64_t F, int64_t P, const int* __restrict__ off,
+__global__ void k_entry_fill(const int* __restrict__ total_dev, int64_t nobj, int64_t F, int64_t P,
+                             const int* __restrict__ off,
                              const int* __restrict__ ecell, const int* __restrict__ tri_start,
                              const int* __restrict__ edge_start, const int* __restrict__ pt_start,
                              int* __restrict__ tri_cur, int* __restrict__ edge_cur, int* __restrict__ pt_cur,
                              int* __restrict__ tri_ent, int* __restrict__ edge_ent, int* __restrict__ pt_ent) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= total) return;
+  if (e >= *total_dev) return;
   int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
   int cell = ecell[e];
   if (p < F) tri_ent[tri_start[cell] + atomicAdd(&tri_cur[cell], 1)] = p;
@@ -430,12 +432,14 @@ __device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, c
 #define WARP_FULL 0xffffffffu
 
 __device__ __forceinline__ void warp_emit(bool pass, int lane, int& n, int o, int a, int b, bool fill, int* pa,
-                                          int* pb) {
+                                          int* pb, int64_t cap) {
   const unsigned m = __ballot_sync(WARP_FULL, pass);
   if (fill && pass) {
-    const int pos = o + n + __popc(m & ((1u << lane) - 1u));
-    pa[pos] = a;
-    pb[pos] = b;
+    const int64_t pos = (int64_t)o + n + __popc(m & ((1u << lane) - 1u));
+    if (pos < cap) {
+      pa[pos] = a;
+      pb[pos] = b;
+    }
   }
   n += __popc(m);
 }
@@ -445,7 +449,7 @@ template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const int* __restrict__ sverts,
                                                    const int* __restrict__ tri, const double* __restrict__ x,
                                                    int* __restrict__ cnt, const int* __restrict__ off,
-                                                   int* __restrict__ pa, int* __restrict__ pb) {
+                                                   int* __restrict__ pa, int* __restrict__ pb, int64_t cap) {
   const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (q >= V) return;  // warp-uniform
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
               pass = boxes_meet(pl, ph, tl, T.ehi + 3 * (int64_t)t) && hg_owns(T.G, l, a, b, c, pl, tl) &&
                      pt_ref_pass(T, tri, x, v, q, t);
             }
-            warp_emit(pass, lane, n, o, v, t, FILL, pa, pb);
+            warp_emit(pass, lane, n, o, v, t, FILL, pa, pb, cap);
           }
         }
   }
@@ -486,7 +490,7 @@ template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const int* __restrict__ sverts,
                                                  const int* __restrict__ tri, const double* __restrict__ x,
                                                  int* __restrict__ cnt, const int* __restrict__ off,
-                                                 int* __restrict__ pa, int* __restrict__ pb) {
+                                                 int* __restrict__ pa, int* __restrict__ pb, int64_t cap) {
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= F) return;
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
               pass = boxes_meet(pl, T.ehi + 3 * (T.P + q), tl, th) && hg_owns(T.G, l, a, b, c, pl, tl) &&
                      pt_ref_pass(T, tri, x, v, q, (int)t);
             }
-            warp_emit(pass, lane, n, o, v, (int)t, FILL, pa, pb);
+            warp_emit(pass, lane, n, o, v, (int)t, FILL, pa, pb, cap);
           }
         }
   }
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
 template <bool FILL>
 __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const int* __restrict__ edge,
                                                   int* __restrict__ cnt, const int* __restrict__ off,
-                                                  int* __restrict__ pa, int* __restrict__ pb) {
+                                                  int* __restrict__ pa, int* __restrict__ pb, int64_t cap) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= E) return;
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
                        flj[2] <= fhi[2] && ref_reach(T.rc, T.F + i, T.F + j);
               }
             }
-            warp_emit(pass, lane, n, o, min((int)i, j), max((int)i, j), FILL, pa, pb);
+            warp_emit(pass, lane, n, o, min((int)i, j), max((int)i, j), FILL, pa, pb, cap);
           }
         }
   }
@@ -587,65 +591,71 @@ __device__ __forceinline__ int warp_slot(bool emit, int* counter) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_pairs(int64_t n_pt, int64_t n, const int* __restrict__ pa,
-                                               const int* __restrict__ pb, const int* __restrict__ tri,
-                                               const int* __restrict__ tri_sorted, const int* __restrict__ edge,
-                                               const double* __restrict__ x, BpOut O, ContactParams CP,
-                                               CcdParams CC) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool live = i < n;
-  const bool is_pt = i < n_pt;
-  int vid[4] = {0, 0, 0, 0}, vid_ccd[4] = {0, 0, 0, 0};
-  if (live) {
-    const int a = pa[i], b = pb[i];
-    if (is_pt) {
-      vid_ccd[0] = a; vid_ccd[1] = tri[3 * b]; vid_ccd[2] = tri[3 * b + 1]; vid_ccd[3] = tri[3 * b + 2];
-      // constraint set: triangle sorted by original id (contact.py:133-135);
-      // CCD: surface order (ccd.py:229-231)
-      vid[0] = a; vid[1] = tri_sorted[3 * b]; vid[2] = tri_sorted[3 * b + 1]; vid[3] = tri_sorted[3 * b + 2];
-    } else {
-      vid_ccd[0] = vid[0] = edge[2 * a]; vid_ccd[1] = vid[1] = edge[2 * a + 1];
-      vid_ccd[2] = vid[2] = edge[2 * b]; vid_ccd[3] = vid[3] = edge[2 * b + 1];
-    }
-  }
-  if (MODE == BP_CONTACT) {
-    double d = 0.0, gr[12];
+__global__ void __launch_bounds__(256) k_pairs(const int* __restrict__ n_pt_dev, const int* __restrict__ n_dev,
+                                               int64_t cap, const int* __restrict__ pa, const int* __restrict__ pb,
+                                               const int* __restrict__ tri, const int* __restrict__ tri_sorted,
+                                               const int* __restrict__ edge, const double* __restrict__ x, BpOut O,
+                                               ContactParams CP, CcdParams CC) {
+  const int64_t n_pt = *n_pt_dev;
+  const int64_t n = *n_dev < cap ? *n_dev : cap;  // n > cap: the caller grows and reruns
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the CONTACT emission ballots across the warp)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x - lane); base < n; base += stride) {
+    const int64_t i = base + lane;
+    const bool live = i < n;
+    const bool is_pt = i < n_pt;
+    int vid[4] = {0, 0, 0, 0}, vid_ccd[4] = {0, 0, 0, 0};
     if (live) {
-      double X[4][3];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
-      d = is_pt ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
-      if (d <= 0.0) O.counter[1] = 1;
-    }
-    const bool emit = live && d > 0.0 && d < CP.d_hat;
-    const int slot = warp_slot(emit, O.counter);
-    if (emit && slot < O.cap) write_contact(O, CP, slot, is_pt ? 1 : 0, vid, d, gr);
-  } else if (MODE == BP_CCD) {
-    bool cert_p = true;
-    double al = live ? ccd_pair_alpha(x, CC.p, vid_ccd, is_pt, CC.alpha_l, &cert_p) : 1.0;
-    if (live && al < 1.0) {
-      // read before the atomic: once a subdomain's minimum has settled most
-      // pairs cannot lower it, so contended atomics stay rare
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        double* ad = &O.alpha_d[vid_ccd[r] / CC.bs];
-        if (al < *(volatile double*)ad) atomic_min_nonneg(ad, al);
+      const int a = pa[i], b = pb[i];
+      if (is_pt) {
+        vid_ccd[0] = a; vid_ccd[1] = tri[3 * b]; vid_ccd[2] = tri[3 * b + 1]; vid_ccd[3] = tri[3 * b + 2];
+        // constraint set: triangle sorted by original id (contact.py:133-135);
+        // CCD: surface order (ccd.py:229-231)
+        vid[0] = a; vid[1] = tri_sorted[3 * b]; vid[2] = tri_sorted[3 * b + 1]; vid[3] = tri_sorted[3 * b + 2];
+      } else {
+        vid_ccd[0] = vid[0] = edge[2 * a]; vid_ccd[1] = vid[1] = edge[2 * a + 1];
+        vid_ccd[2] = vid[2] = edge[2 * b]; vid_ccd[3] = vid[3] = edge[2 * b + 1];
       }
     }
-    // global minimum: warp minimum first, one filtered atomic per warp
-    double wm = warp_min_all(al);
-    if ((threadIdx.x & 31) == 0 && wm < *(volatile double*)O.min_alpha) atomic_min_nonneg(O.min_alpha, wm);
-    if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
-    if (live && O.verts && i < O.cap) {
-      O.verts[i] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
-      O.ccd_ispt[i] = is_pt ? 1 : 0;
-      O.alpha_pair[i] = al;
+    if (MODE == BP_CONTACT) {
+      double d = 0.0, gr[12];
+      if (live) {
+        double X[4][3];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
+        d = is_pt ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
+        if (d <= 0.0) O.counter[1] = 1;
+      }
+      const bool emit = live && d > 0.0 && d < CP.d_hat;
+      const int slot = warp_slot(emit, O.counter);
+      if (emit && slot < O.cap) write_contact(O, CP, slot, is_pt ? 1 : 0, vid, d, gr);
+    } else if (MODE == BP_CCD) {
+      bool cert_p = true;
+      const double al = live ? ccd_pair_alpha(x, CC.p, vid_ccd, is_pt, CC.alpha_l, &cert_p) : 1.0;
+      if (live && al < 1.0) {
+        // read before the atomic: once a subdomain's minimum has settled most
+        // pairs cannot lower it, so contended atomics stay rare
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double* ad = &O.alpha_d[vid_ccd[r] / CC.bs];
+          if (al < *(volatile double*)ad) atomic_min_nonneg(ad, al);
+        }
+      }
+      // global minimum: warp minimum first, one filtered atomic per warp
+      const double wm = warp_min_all(al);
+      if (lane == 0 && wm < *(volatile double*)O.min_alpha) atomic_min_nonneg(O.min_alpha, wm);
+      if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
+      if (live && O.verts && i < O.cap) {
+        O.verts[i] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
+        O.ccd_ispt[i] = is_pt ? 1 : 0;
+        O.alpha_pair[i] = al;
+      }
+    } else if (MODE == BP_CERT) {
+      if (live && !ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, is_pt)) O.counter[1] = 1;
     }
-  } else if (MODE == BP_CERT) {
-    if (!live) return;
-    if (!ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, is_pt)) O.counter[1] = 1;
   }
 }
 
@@ -748,35 +758,32 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + nobj, 0, sizeof(int), st));
   exclusive_scan(c, c->cell_cnt, c->cell_off, nobj + 1);
-  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 4, c->cell_off.p + nobj, sizeof(int), cudaMemcpyDeviceToHost, st));
-  sync_stream(c);
-  const int total = c->h_cnt[4];
+  // every object covers <= 2 cells per axis at its level: <= 8 entries each,
+  // so the entry arrays are sized without reading the total back
+  const int64_t total_cap = 8 * nobj;
+  const int* total_dev = c->cell_off.p + nobj;
   const size_t ncell = (size_t)tot_cells;
   for (DBuf<int>* b : {&g.tri_cnt, &g.tri_start, &g.edge_cnt, &g.edge_start, &g.pt_cnt, &g.pt_start})
     b->ensure(ncell + 1);
-  g.ecell.ensure((size_t)total + 1);
-  g.tri_ent.ensure((size_t)total + 1);
-  g.edge_ent.ensure((size_t)total + 1);
-  g.pt_ent.ensure((size_t)total + 1);
+  g.ecell.ensure((size_t)total_cap + 1);
+  g.tri_ent.ensure((size_t)total_cap + 1);
+  g.edge_ent.ensure((size_t)total_cap + 1);
+  g.pt_ent.ensure((size_t)total_cap + 1);
   for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
-  if (total) {
-    k_entry_hist<<<grid_for(total, 256), 256, 0, st>>>(total, nobj, F, P, G, c->cell_off, g.level, c->box_elo,
-                                                       c->box_ehi, g.ecell, g.tri_cnt, g.edge_cnt, g.pt_cnt);
-    LAUNCH_CHECK();
-  }
+  k_entry_hist<<<grid_for(total_cap, 256), 256, 0, st>>>(total_dev, nobj, F, P, G, c->cell_off, g.level, c->box_elo,
+                                                         c->box_ehi, g.ecell, g.tri_cnt, g.edge_cnt, g.pt_cnt);
+  LAUNCH_CHECK();
   exclusive_scan(c, g.tri_cnt, g.tri_start, ncell + 1);
   exclusive_scan(c, g.edge_cnt, g.edge_start, ncell + 1);
   exclusive_scan(c, g.pt_cnt, g.pt_start, ncell + 1);
   // the counts become per-cell fill cursors
   for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
-  if (total) {
-    k_entry_fill<<<grid_for(total, 256), 256, 0, st>>>(total, nobj, F, P, c->cell_off, g.ecell, g.tri_start,
-                                                       g.edge_start, g.pt_start, g.tri_cnt, g.edge_cnt, g.pt_cnt,
-                                                       g.tri_ent, g.edge_ent, g.pt_ent);
-    LAUNCH_CHECK();
-  }
+  k_entry_fill<<<grid_for(total_cap, 256), 256, 0, st>>>(total_dev, nobj, F, P, c->cell_off, g.ecell, g.tri_start,
+                                                         g.edge_start, g.pt_start, g.tri_cnt, g.edge_cnt, g.pt_cnt,
+                                                         g.tri_ent, g.edge_ent, g.pt_ent);
+  LAUNCH_CHECK();
   BpTables& T = B.T;
   T.pt_start = g.pt_start; T.pt_ent = g.pt_ent;
   T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
@@ -791,10 +798,11 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
 }
 
 // The reference pair list of the grid (PT if which & 1, EE if which & 2):
-// count pass, exclusive scan, fill pass.  Deterministic order: points' pairs,
-// then triangles' pairs (both PT), then edges' pairs.  Returns (n_pt, n).
-static std::pair<int64_t, int64_t> collect_pairs(mp_ctx* c, const double* x, const BpGrid& B, int which) {
-  if (B.empty) return {0, 0};
+// count pass, exclusive scan, fill pass into the current capacity -- no host
+// sync; the counts stay on the device (qoff[V+F] = PT pairs, qoff[V+F+E] =
+// all) and the caller checks the capacity at its own readback.  Deterministic
+// order: points' pairs, then triangles' pairs (both PT), then edges' pairs.
+static void collect_pairs(mp_ctx* c, const double* x, const BpGrid& B, int which) {
   const int64_t V = c->V, F = c->F, E = c->E;
   const int64_t nq = V + F + E;
   auto& g = c->grid;
@@ -802,38 +810,42 @@ static std::pair<int64_t, int64_t> collect_pairs(mp_ctx* c, const double* x, con
   g.qoff.ensure(nq + 1);
   cudaStream_t st = c->stream;
   CUDA_CHECK(cudaMemsetAsync(g.qcnt.p, 0, sizeof(int) * (nq + 1), st));
+  if (B.empty) {
+    CUDA_CHECK(cudaMemsetAsync(g.qoff.p, 0, sizeof(int) * (nq + 1), st));
+    return;
+  }
+  if (g.pa.n < 1024) {
+    g.pa.ensure(1 << 16);
+    g.pb.ensure(1 << 16);
+  }
+  const int64_t cap = (int64_t)std::min(g.pa.n, g.pb.n);
   if ((which & 1) && V) {
-    k_hq_points<false><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr, nullptr,
-                                                          nullptr);
+    k_hq_points<false><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr,
+                                                               nullptr, nullptr, 0);
     LAUNCH_CHECK();
-    k_hq_tris<false><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr, nullptr,
-                                                        nullptr);
+    k_hq_tris<false><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr,
+                                                             nullptr, nullptr, 0);
     LAUNCH_CHECK();
   }
   if ((which & 2) && E > 1) {
     k_hq_edges<false><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, g.qcnt.p + V + F, nullptr, nullptr,
-                                                         nullptr);
+                                                              nullptr, 0);
     LAUNCH_CHECK();
   }
   exclusive_scan(c, g.qcnt, g.qoff, nq + 1);
-  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, g.qoff.p + V + F, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 6, g.qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, st));
-  sync_stream(c);
-  const int64_t n_pt = c->h_cnt[5], n = c->h_cnt[6];
-  g.pa.ensure(n + 1);
-  g.pb.ensure(n + 1);
-  if ((which & 1) && V && n_pt) {
-    k_hq_points<true><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa, g.pb);
+  if ((which & 1) && V) {
+    k_hq_points<true><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa,
+                                                              g.pb, cap);
     LAUNCH_CHECK();
     k_hq_tris<true><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, g.qoff.p + V, g.pa,
-                                                       g.pb);
+                                                            g.pb, cap);
     LAUNCH_CHECK();
   }
-  if ((which & 2) && E > 1 && n > n_pt) {
-    k_hq_edges<true><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa, g.pb);
+  if ((which & 2) && E > 1) {
+    k_hq_edges<true><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa, g.pb,
+                                                             cap);
     LAUNCH_CHECK();
   }
-  return {n_pt, n};
 }
 
 // Broad phase + the per-pair work of MODE.  Returns the number of reference
@@ -844,22 +856,33 @@ static std::pair<int64_t, int64_t> collect_pairs(mp_ctx* c, const double* x, con
 template <int MODE>
 static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
                       int* flag, int which = 3, int64_t* n_pt_out = nullptr) {
-  CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
-  O.counter = c->counters.p;
-  auto nn = collect_pairs(c, x, B, which);
-  const int64_t n_pt = nn.first, n = nn.second;
-  if (n_pt_out) *n_pt_out = n_pt;
-  if (MODE == BP_RAW) {
-    if (flag) *flag = 0;
-    return n;
+  const int64_t V = c->V, F = c->F, E = c->E, nq = V + F + E;
+  auto& g = c->grid;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
+    O.counter = c->counters.p;
+    collect_pairs(c, x, B, which);
+    const int64_t cap = (int64_t)std::min(g.pa.n, g.pb.n);
+    if (MODE != BP_RAW && !B.empty) {
+      int sms = 148;
+      k_pairs<MODE><<<(unsigned)(8 * sms), 256, 0, c->stream>>>(g.qoff.p + V + F, g.qoff.p + nq, cap, g.pa, g.pb,
+                                                                  c->tri, c->tri_sorted, c->edge, x, O, CP, CC);
+      LAUNCH_CHECK();
+    }
+    // one readback: the mode's counters and the pair-list sizes
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, g.qoff.p + V + F, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 6, g.qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync_stream(c);
+    const int64_t n_pt = c->h_cnt[5], n = c->h_cnt[6];
+    if (n > cap) {  // the list did not fit: grow and rerun (results are idempotent)
+      g.pa.ensure((size_t)(n * 1.25) + 1024);
+      g.pb.ensure((size_t)(n * 1.25) + 1024);
+      continue;
+    }
+    if (n_pt_out) *n_pt_out = n_pt;
+    if (flag) *flag = MODE == BP_RAW ? 0 : c->h_cnt[1];
+    return MODE == BP_CONTACT ? c->h_cnt[0] : n;
   }
-  if (n) {
-    k_pairs<MODE><<<grid_for(n, 256), 256, 0, c->stream>>>(n_pt, n, c->grid.pa, c->grid.pb, c->tri, c->tri_sorted,
-                                                            c->edge, x, O, CP, CC);
-    LAUNCH_CHECK();
-  }
-  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  sync_stream(c);
-  if (flag) *flag = c->h_cnt[1];
-  return MODE == BP_CONTACT ? c->h_cnt[0] : n;
+  throw MpError(MP_ERR_CAPACITY, "broad-phase pair list capacity retry failed");
 }
