@@ -166,16 +166,6 @@ __global__ void k_mas_factor(int64_t D, int64_t N, int bs, int m, const double* 
   store_cyc_sym(X, m, Bblk + d * cyc_size(m), true);
 }
 
-// One CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
-// (mas.py:84-90).  The inverse is formed by the symmetric sweep operator
-// (Gauss-Jordan without pivoting, stable for SPD): after sweeping every
-// pivot the matrix holds -M^-1.  Its pivots are the Schur-complement
-// diagonals, i.e. the squared Cholesky pivots, so "pivot <= 0" is exactly
-// cho_factor's non-SPD failure.  The m x m matrix lives in registers, a
-// 6 x 6 tile per thread on a 16 x 16 thread grid (m <= 96); each step
-// broadcasts the old pivot row through shared memory (double-buffered, one
-// barrier per step).  Symmetry is preserved bit-exactly (every update uses
-// the same products), so the row is also the pivot column.
 #define SWEEP_T 6
 
 // 1/a to ~1 ulp: MUFU reciprocal seed + two Newton steps (the IEEE division
@@ -192,6 +182,42 @@ __device__ __forceinline__ double fast_rcp(double a) {
 // Sweep every pivot of the m x m (m <= 96) symmetric matrix staged in smem
 // S (row-major); on return S holds -S^-1.  rowk: 2 x 96 smem scratch.
 // Returns false (uniformly) when a pivot is not positive.
+//
+// Per step the common path is 12 LDS, 6 DMUL and 36 DFMA per thread; only
+// the 16 threads holding row k and the 16 holding column k take a
+// (warp-divergent, compile-time indexed) fix-up branch, and the owners of
+// row k+1 publish it for the next step right after their update.
+
+template <int A>
+__device__ __forceinline__ void publish_row(const double (&R)[SWEEP_T][SWEEP_T], double* rk, int tc, int m) {
+#pragma unroll
+  for (int b = 0; b < SWEEP_T; ++b)
+    if (tc + 16 * b < m) rk[tc + 16 * b] = R[A][b];
+}
+
+__device__ __forceinline__ void publish(const double (&R)[SWEEP_T][SWEEP_T], int a, double* rk, int tc, int m) {
+  switch (a) {
+    case 0: publish_row<0>(R, rk, tc, m); break;
+    case 1: publish_row<1>(R, rk, tc, m); break;
+    case 2: publish_row<2>(R, rk, tc, m); break;
+    case 3: publish_row<3>(R, rk, tc, m); break;
+    case 4: publish_row<4>(R, rk, tc, m); break;
+    default: publish_row<5>(R, rk, tc, m); break;
+  }
+}
+
+template <int A>
+__device__ __forceinline__ void fix_row(double (&R)[SWEEP_T][SWEEP_T], const double (&cj)[SWEEP_T], double inv) {
+#pragma unroll
+  for (int b = 0; b < SWEEP_T; ++b) R[A][b] = cj[b] * inv;
+}
+
+template <int B>
+__device__ __forceinline__ void fix_col(double (&R)[SWEEP_T][SWEEP_T], const double (&ci)[SWEEP_T]) {
+#pragma unroll
+  for (int a = 0; a < SWEEP_T; ++a) R[a][B] = ci[a];
+}
+
 __device__ bool sweep_core(double* S, int m, double* rowk) {
   const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
   for (int e = tid; e < 2 * 96; e += blockDim.x) rowk[e] = 0.0;
@@ -204,15 +230,9 @@ __device__ bool sweep_core(double* S, int m, double* rowk) {
       int i = tr + 16 * a, j = tc + 16 * b;
       R[a][b] = (i < m && j < m) ? S[i * m + j] : 0.0;
     }
+  if (tr == 0) publish(R, 0, rowk, tc, m);  // row 0 for step 0
   for (int k = 0; k < m; ++k) {
     double* rk = rowk + (k & 1) * 96;
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a)
-      if (tr + 16 * a == k) {
-#pragma unroll
-        for (int b = 0; b < SWEEP_T; ++b)
-          if (tc + 16 * b < m) rk[tc + 16 * b] = R[a][b];
-      }
     __syncthreads();
     const double piv = rk[k];
     if (!(piv > 0.0)) return false;  // uniform across the CTA
@@ -223,23 +243,35 @@ __device__ bool sweep_core(double* S, int m, double* rowk) {
       ci[a] = rk[min(tr + 16 * a, 95)] * inv;
       cj[a] = rk[min(tc + 16 * a, 95)];
     }
-    // rank-one update of every element (row / column k patched below)
+    // rank-one update of every element (row / column k fixed below)
 #pragma unroll
     for (int a = 0; a < SWEEP_T; ++a)
 #pragma unroll
       for (int b = 0; b < SWEEP_T; ++b) R[a][b] = fma(-ci[a], cj[b], R[a][b]);
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a)
-      if (tr + 16 * a == k) {
-#pragma unroll
-        for (int b = 0; b < SWEEP_T; ++b) R[a][b] = cj[b] * inv;
+    const int kr = k & 15, ka = k >> 4;
+    if (tr == kr) {  // this thread holds part of row k: A_kj <- A_kj / piv
+      switch (ka) {
+        case 0: fix_row<0>(R, cj, inv); break;
+        case 1: fix_row<1>(R, cj, inv); break;
+        case 2: fix_row<2>(R, cj, inv); break;
+        case 3: fix_row<3>(R, cj, inv); break;
+        case 4: fix_row<4>(R, cj, inv); break;
+        default: fix_row<5>(R, cj, inv); break;
       }
-#pragma unroll
-    for (int b = 0; b < SWEEP_T; ++b)
-      if (tc + 16 * b == k) {
-#pragma unroll
-        for (int a = 0; a < SWEEP_T; ++a) R[a][b] = (tr + 16 * a == k) ? -inv : ci[a];
+    }
+    if (tc == kr) {  // column k: A_ik <- A_ik / piv, and A_kk <- -1 / piv
+      switch (ka) {
+        case 0: fix_col<0>(R, ci); if (tr == kr) R[0][0] = -inv; break;
+        case 1: fix_col<1>(R, ci); if (tr == kr) R[1][1] = -inv; break;
+        case 2: fix_col<2>(R, ci); if (tr == kr) R[2][2] = -inv; break;
+        case 3: fix_col<3>(R, ci); if (tr == kr) R[3][3] = -inv; break;
+        case 4: fix_col<4>(R, ci); if (tr == kr) R[4][4] = -inv; break;
+        default: fix_col<5>(R, ci); if (tr == kr) R[5][5] = -inv; break;
       }
+    }
+    // publish row k+1 (already updated) into the other buffer
+    const int k1 = k + 1;
+    if (k1 < m && tr == (k1 & 15)) publish(R, k1 >> 4, rowk + (k1 & 1) * 96, tc, m);
   }
   __syncthreads();
 #pragma unroll
