@@ -218,17 +218,17 @@ __device__ __forceinline__ void fix_col(double (&R)[SWEEP_T][SWEEP_T], const dou
   for (int a = 0; a < SWEEP_T; ++a) R[a][B] = ci[a];
 }
 
-__device__ bool sweep_core(double* S, int m, double* rowk) {
+// The matrix lives in R (thread (tr, tc) holds rows tr + 16a, columns
+// tc + 16b); LOAD(i, j) supplies the input, all 36 loads issued at once.
+template <class LOAD>
+__device__ bool sweep_regs(LOAD load, int m, double* rowk, double (&R)[SWEEP_T][SWEEP_T]) {
   const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
-  for (int e = tid; e < 2 * 96; e += blockDim.x) rowk[e] = 0.0;
-  __syncthreads();
-  double R[SWEEP_T][SWEEP_T];
 #pragma unroll
   for (int a = 0; a < SWEEP_T; ++a)
 #pragma unroll
     for (int b = 0; b < SWEEP_T; ++b) {
       int i = tr + 16 * a, j = tc + 16 * b;
-      R[a][b] = (i < m && j < m) ? S[i * m + j] : 0.0;
+      R[a][b] = (i < m && j < m) ? load(i, j) : 0.0;
     }
   if (tr == 0) publish(R, 0, rowk, tc, m);  // row 0 for step 0
   for (int k = 0; k < m; ++k) {
@@ -273,16 +273,15 @@ __device__ bool sweep_core(double* S, int m, double* rowk) {
     const int k1 = k + 1;
     if (k1 < m && tr == (k1 & 15)) publish(R, k1 >> 4, rowk + (k1 & 1) * 96, tc, m);
   }
-  __syncthreads();
-#pragma unroll
-  for (int a = 0; a < SWEEP_T; ++a)
-#pragma unroll
-    for (int b = 0; b < SWEEP_T; ++b) {
-      int i = tr + 16 * a, j = tc + 16 * b;
-      if (i < m && j < m) S[i * m + j] = R[a][b];
-    }
-  __syncthreads();
   return true;
+}
+
+// element (i, j) of a symmetric m x m matrix is the stored representative
+// of the cyclic-diagonal packing (common.cuh) at position cyc_index(m, i, j)
+__device__ __forceinline__ bool cyc_rep(int m, int i, int j) {
+  int s = j - i;
+  if (s < 0) s += m;
+  return 2 * s < m || (2 * s == m && i < j);
 }
 
 // One CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
@@ -293,32 +292,39 @@ __device__ bool sweep_core(double* S, int m, double* rowk) {
 // cho_factor's non-SPD failure.  The m x m matrix lives in registers, a
 // 6 x 6 tile per thread on a 16 x 16 thread grid (m <= 96); each step
 // broadcasts the old pivot row through shared memory (double-buffered, one
-// barrier per step).  Symmetry is preserved bit-exactly (every update uses
-// the same products), so the row is also the pivot column.
+// barrier per step).  The matrix stays symmetric to rounding, so the
+// broadcast pivot row doubles as the pivot column.
 __global__ void __launch_bounds__(256, 2)
 k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull, double* __restrict__ Mblk,
             double* __restrict__ Bblk, int* __restrict__ status) {
-  extern __shared__ double sm[];
-  double* S = sm;                 // m*m staging
-  double* rowk = sm + m * m;      // 2 x 96 broadcast rows
+  __shared__ double rowk[2 * 96];
   const int64_t d = blockIdx.x;
-  const int nd = (int)((N - d * bs) < bs ? (N - d * bs) : bs);
+  const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
+  const int nd3 = 3 * (int)((N - d * bs) < bs ? (N - d * bs) : bs);
   const double* src = Mfull + d * (int64_t)m * m;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int i = e / m, j = e - (e / m) * m;
-    double v = src[e];
-    if (i >= 3 * nd || j >= 3 * nd) v = (i == j) ? 1.0 : 0.0;
-    S[e] = v;
-  }
-  __syncthreads();
-  store_cyc_sym(S, m, Mblk + d * cyc_size(m), false);
-  if (!sweep_core(S, m, rowk)) {
+  const int64_t csz = cyc_size(m);
+  double* mout = Mblk + d * csz;
+  double R[SWEEP_T][SWEEP_T];
+  // M_d (padding rows of a short last subdomain = identity), packed into Mblk
+  auto load = [&](int i, int j) -> double {
+    double v = (i >= nd3 || j >= nd3) ? ((i == j) ? 1.0 : 0.0) : __ldg(src + i * m + j);
+    if (cyc_rep(m, i, j)) mout[cyc_index(m, i, j)] = v;
+    return v;
+  };
+  if (!sweep_regs(load, m, rowk, R)) {
     if (threadIdx.x == 0) atomicExch(status, 1);
     return;
   }
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = -S[e];
-  __syncthreads();
-  store_cyc_sym(S, m, Bblk + d * cyc_size(m), true);
+  // B_d = -R; R is symmetric to rounding (1 ulp), the representative of each
+  // symmetric pair is stored (the reference averages the two, mas.py:90)
+  double* bout = Bblk + d * csz;
+#pragma unroll
+  for (int a = 0; a < SWEEP_T; ++a)
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b) {
+      const int i = tr + 16 * a, j = tc + 16 * b;
+      if (i < m && j < m && cyc_rep(m, i, j)) bout[cyc_index(m, i, j)] = -R[a][b];
+    }
 }
 
 // Pivot block of the blocked dense sweep: out (kb x kb) = -P^-1 for the
@@ -326,20 +332,21 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mful
 __global__ void __launch_bounds__(256, 1)
 k_block_sweep(int kb, const double* __restrict__ A, int lda, int k0, double* __restrict__ out,
               int* __restrict__ status) {
-  extern __shared__ double sm[];
-  double* S = sm;
-  double* rowk = sm + kb * kb;
-  // coalesced along the column; A is symmetric so the staged layout is too
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-    int j = e / kb, i = e - j * kb;
-    S[e] = A[(int64_t)(k0 + j) * lda + k0 + i];
-  }
-  __syncthreads();
-  if (!sweep_core(S, kb, rowk)) {
+  __shared__ double rowk[2 * 96];
+  const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
+  double R[SWEEP_T][SWEEP_T];
+  auto load = [&](int i, int j) -> double { return __ldg(A + (int64_t)(k0 + j) * lda + k0 + i); };
+  if (!sweep_regs(load, kb, rowk, R)) {
     if (threadIdx.x == 0) atomicExch(status, 1);
     return;
   }
-  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) out[e] = S[e];
+#pragma unroll
+  for (int a = 0; a < SWEEP_T; ++a)
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b) {
+      const int i = tr + 16 * a, j = tc + 16 * b;
+      if (i < kb && j < kb) out[i * kb + j] = R[a][b];
+    }
 }
 
 // after the rank-kb update: block column/row K <- W (= A_iK P^-1), A_KK <- -P^-1

@@ -142,12 +142,10 @@ static void set_smem_limits() {
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
   };
   allow((const void*)k_mas_factor);
-  allow((const void*)k_mas_sweep);
   allow((const void*)k_mas_apply_l0<true, 2>);
   allow((const void*)k_mas_apply_l0<false, 2>);
   allow((const void*)k_mas_apply_l0<true, 3>);
   allow((const void*)k_mas_apply_l0<false, 3>);
-  allow((const void*)k_block_sweep);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
   done = true;

@@ -106,7 +106,7 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   const double one = 1.0, mone = -1.0, zero = 0.0;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int kb = std::min(nb, n - k0);
-    k_block_sweep<<<1, 256, sizeof(double) * ((size_t)kb * kb + 2 * 96), st>>>(kb, A, n, k0, L.dn_P, status);
+    k_block_sweep<<<1, 256, 0, st>>>(kb, A, n, k0, L.dn_P, status);
     LAUNCH_CHECK();
     CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A + (size_t)k0 * n, sizeof(double) * (size_t)n * kb,
                                cudaMemcpyDeviceToDevice, st));
@@ -162,9 +162,8 @@ static void mas_build(mp_ctx* c) {
   }
   k_bsr_to_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, c->bs, m, c->Mfull);
   LAUNCH_CHECK();
-  const size_t smem = sizeof(double) * ((size_t)m * m + 2 * 96);
-  k_mas_sweep<<<(unsigned)D, 256, smem, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
-                                                      c->counters.p + 3);
+  k_mas_sweep<<<(unsigned)D, 256, 0, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
+                                                    c->counters.p + 3);
   LAUNCH_CHECK();
   for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
   // one readback of every level's non-SPD flag (counters 3..7)
