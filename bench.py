@@ -202,6 +202,9 @@ def run_ours(args):
         ctx.step_device(H)
     torch.cuda.synchronize()
 
+    # the e2e leg replays the same frames from this state
+    x_start_h, v_start_h = ctx.get_state()
+
     # ---- timed: device-resident frames ----
     sampler = ClockSampler()
     if rank == 0:
@@ -234,12 +237,11 @@ def run_ours(args):
     t_max = allmax(total_ms)
     all_iters = allsum(float(iters))
 
-    # ---- e2e: the public API with host buffers ----
-    x_h, v_h = ctx.get_state()
-    xp = torch.empty(x_h.size, dtype=torch.float64).pin_memory().numpy()
-    vp = torch.empty(v_h.size, dtype=torch.float64).pin_memory().numpy()
-    xp[:] = x_h
-    vp[:] = v_h
+    # ---- e2e: the same frames through the public API with host buffers ----
+    xp = torch.empty(x_start_h.size, dtype=torch.float64).pin_memory().numpy()
+    vp = torch.empty(v_start_h.size, dtype=torch.float64).pin_memory().numpy()
+    xp[:] = x_start_h
+    vp[:] = v_start_h
     e2e_s = 0.0
     e2e_iters = 0
     for _ in range(args.steps):
@@ -290,6 +292,8 @@ def run_ours(args):
         "frames": frames,
         "e2e": {"value": e2e_all / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": 2 * 8 * n3,
                 "d2h_bytes_per_step": 2 * 8 * n3, "sec_per_frame": e2e_s / args.steps,
+                "frames": "the timed frames replayed from the same start state (iteration counts may differ "
+                          "slightly: FP64 atomics make contact frames chaotic)",
                 "api": "paper_2604_19892_b200.solver.step(scene, x, v, h, cfg) with pinned numpy x, v"},
         "roofline": roof("mas_apply_l0", "k_mas_apply_l0 (level-0 block matvec + Woodbury overlay + coarse "
                                           "prolongation + pinned projection; TMA-staged packed blocks)"),

@@ -347,10 +347,16 @@ __global__ void k_obj_level(int64_t nobj, int64_t F, int64_t P, HGrid G, const d
   hg_span(G, l, l0, h0, c0, c1);
   level[i] = l;
   cnt[i] = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
-  // which levels hold any triangle / edge / point (queries skip empty ones)
+  // which levels hold any triangle / edge / point (queries skip empty ones):
+  // OR-reduced per warp, one atomic per warp and class
   const int cls = i < F ? 0 : (i < P ? 1 : 2);
   const unsigned bit = 1u << l;
-  if ((__ldg(lmask + cls) & bit) == 0) atomicOr(lmask + cls, bit);
+  const unsigned live = __activemask();
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const unsigned w = __reduce_or_sync(live, cls == q ? bit : 0u);
+    if (w && (threadIdx.x & 31) == (__ffs(live) - 1)) atomicOr(lmask + q, w);
+  }
 }
 
 __device__ __forceinline__ int upper_bound_i32(const int* a, int n, int k) {
