@@ -367,59 +367,21 @@ __global__ void k_block_fix(int n, int kb, int k0, const double* __restrict__ W,
 // ---------------------------------------------------------------------------
 // coarse levels
 
-// every BSR block (v, w) -> M_l[agg(v), agg(w)] / (|a||b|).  One CTA per row
-// aggregate A: its rows' blocks are accumulated per column aggregate B in a
-// small shared-memory table (shared atomics), then flushed with one global
-// atomic per entry -- instead of one contended global atomic per block.
-#define COARSE_SLOTS 64
-__global__ void __launch_bounds__(256) k_bsr_to_coarse(int64_t N, const int* __restrict__ rowptr,
-                                                       const int* __restrict__ cols, const double* __restrict__ vals,
-                                                       int span, int n, double* __restrict__ M) {
-  __shared__ int key[COARSE_SLOTS];
-  __shared__ double acc[COARSE_SLOTS][9];
-  __shared__ int overflow;
-  const int A = blockIdx.x;
-  for (int q = threadIdx.x; q < COARSE_SLOTS; q += blockDim.x) key[q] = -1;
-  for (int q = threadIdx.x; q < COARSE_SLOTS * 9; q += blockDim.x) (&acc[0][0])[q] = 0.0;
-  if (threadIdx.x == 0) overflow = 0;
-  __syncthreads();
-  const int64_t v0 = (int64_t)A * span;
-  const int64_t v1 = (v0 + span) < N ? (v0 + span) : N;
-  const int64_t na = v1 - v0;
-  for (int64_t row = v0 + threadIdx.x; row < v1; row += blockDim.x) {
-    for (int k = rowptr[row]; k < rowptr[row + 1]; ++k) {
-      const int B = cols[k] / span;
-      const double* bl = vals + 9 * (int64_t)k;
-      // open-addressing slot of B
-      int h = B & (COARSE_SLOTS - 1), slot = -1;
-      for (int probe = 0; probe < COARSE_SLOTS; ++probe) {
-        const int cur = atomicCAS(&key[h], -1, B);
-        if (cur == -1 || cur == B) {
-          slot = h;
-          break;
-        }
-        h = (h + 1) & (COARSE_SLOTS - 1);
-      }
-      if (slot >= 0) {
-#pragma unroll
-        for (int q = 0; q < 9; ++q) atomicAdd(&acc[slot][q], bl[q]);
-      } else {  // table full: direct global accumulation (never in practice)
-        const int64_t nb = (N - (int64_t)B * span) < span ? (N - (int64_t)B * span) : span;
-        const double sc = 1.0 / ((double)na * (double)nb);
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) atomicAdd(&M[(int64_t)(3 * A + r) * n + 3 * B + c], bl[3 * r + c] * sc);
-        overflow = 1;
-      }
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < COARSE_SLOTS * 9; e += blockDim.x) {
-    const int q = e / 9, rc = e - 9 * q;
-    const int B = key[q];
-    if (B < 0) continue;
-    const int64_t nb = (N - (int64_t)B * span) < span ? (N - (int64_t)B * span) : span;
-    const double sc = 1.0 / ((double)na * (double)nb);
-    atomicAdd(&M[(int64_t)(3 * A + rc / 3) * n + 3 * B + rc % 3], acc[q][rc] * sc);
+// every BSR block (v, w) -> M_l[agg(v), agg(w)] / (|a||b|)
+__global__ void k_bsr_to_coarse(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
+                                const double* __restrict__ vals, int span, int n, double* __restrict__ M) {
+  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= N) return;
+  int a = (int)(row / span);
+  int64_t na = (N - (int64_t)a * span) < span ? (N - (int64_t)a * span) : span;
+  for (int k = rowptr[row]; k < rowptr[row + 1]; ++k) {
+    int w = cols[k];
+    int b = w / span;
+    int64_t nb = (N - (int64_t)b * span) < span ? (N - (int64_t)b * span) : span;
+    double sc = 1.0 / ((double)na * (double)nb);
+    const double* bl = vals + 9 * (int64_t)k;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) atomicAdd(&M[(int64_t)(3 * a + r) * n + 3 * b + c], bl[3 * r + c] * sc);
   }
 }
 

@@ -138,7 +138,7 @@ static void mas_build(mp_ctx* c) {
     cudaStream_t st = L.st;
     CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_bsr, 0));
     L.dense.zero((size_t)L.n * L.n, st);
-    k_bsr_to_coarse<<<L.A, 256, 0, st>>>(c->N, c->rowptr, c->cols, c->bsr, L.span, L.n, L.dense);
+    k_bsr_to_coarse<<<grid_for(c->N, 128), 128, 0, st>>>(c->N, c->rowptr, c->cols, c->bsr, L.span, L.n, L.dense);
     LAUNCH_CHECK();
     if (c->base.count) {
       k_contact_coarse<<<grid_for(c->base.count, 128), 128, 0, st>>>(c->base.count, c->base.verts, c->base.grad,
