@@ -131,6 +131,7 @@ struct mp_ctx {
 
   // ---- sizes ----
   int64_t N = 0, T = 0, F = 0, E = 0, V = 0;
+  int64_t T_snh = 0, T_arap = 0;  // tets are stored SNH [0, T_snh), ARAP next, then none
   int bs = 32;   // partition block size
   int m = 96;    // dofs per (padded) subdomain block = 3*bs
   int64_t D = 0; // subdomains

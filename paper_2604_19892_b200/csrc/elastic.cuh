@@ -98,22 +98,22 @@ __global__ void k_inertia_grad(int64_t N, const double* __restrict__ x, const do
   g[i] = pinned[v] ? 0.0 : mass[v] * (x[i] - xt[i]);
 }
 
-__global__ void k_tet_grad(int64_t T, const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
-                           const signed char* __restrict__ kind, const unsigned char* __restrict__ pinned,
-                           const double* __restrict__ x, double h2, double* __restrict__ g) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  int kd = kind[t];
-  if (kd == 0) return;
-  int4 tv = tets[t];
-  TetParam tp = tetp[t];
+template <int KIND>
+__global__ void __launch_bounds__(128) k_tet_grad(int64_t t0, int64_t nt, const int4* __restrict__ tets,
+                                                  const TetParam* __restrict__ tetp,
+                                                  const unsigned char* __restrict__ pinned,
+                                                  const double* __restrict__ x, double h2, double* __restrict__ g) {
+  const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= t0 + nt) return;
+  const int4 tv = tets[t];
+  const TetParam tp = tetp[t];
   double X[4][3], bc[4][3];
   load_tet(x, tv, X);
   M3 F;
   tet_F(X, tp, F, bc);
-  M3 P = piola(F, kd, tp.mu, tp.lam);
+  const M3 P = piola(F, KIND, tp.mu, tp.lam);
   const int id[4] = {tv.x, tv.y, tv.z, tv.w};
-  double s = h2 * tp.vol;
+  const double s = h2 * tp.vol;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     if (pinned[id[a]]) continue;
@@ -137,18 +137,18 @@ __global__ void k_inertia_energy(int64_t N, const double* __restrict__ x, const 
   block_sum_store<256>(acc, part);
 }
 
-__global__ void k_tet_energy(int64_t T, const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
-                             const signed char* __restrict__ kind, const double* __restrict__ x, double* part) {
+template <int KIND>
+__global__ void k_tet_energy(int64_t t0, int64_t nt, const int4* __restrict__ tets,
+                             const TetParam* __restrict__ tetp, const double* __restrict__ x, double* part) {
   double acc = 0.0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
-    int kd = kind[t];
-    if (kd == 0) continue;
+  for (int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < t0 + nt;
+       t += (int64_t)gridDim.x * blockDim.x) {
     TetParam tp = tetp[t];
     double X[4][3], bc[4][3];
     load_tet(x, tets[t], X);
     M3 F;
     tet_F(X, tp, F, bc);
-    acc += tp.vol * psi(F, kd, tp.mu, tp.lam);
+    acc += tp.vol * psi(F, KIND, tp.mu, tp.lam);
   }
   block_sum_store<256>(acc, part);
 }
@@ -254,14 +254,14 @@ __device__ __forceinline__ void tet_block(const TetModes& md, int a, int b, doub
     for (int c = 0; c < 3; ++c) blk[r][c] = UK[r][0] * md.U[c][0] + UK[r][1] * md.U[c][1] + UK[r][2] * md.U[c][2];
 }
 
-__global__ void k_tet_hessian(int64_t T, const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
-                              const signed char* __restrict__ kind, const unsigned char* __restrict__ pinned,
+template <int KIND>
+__global__ void k_tet_hessian(int64_t t0, int64_t nt, const int4* __restrict__ tets,
+                              const TetParam* __restrict__ tetp, const unsigned char* __restrict__ pinned,
                               const int* __restrict__ tet_slot, const double* __restrict__ x, double h2,
                               double* __restrict__ bsr) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  int kd = kind[t];
-  if (kd == 0) return;
+  const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= t0 + nt) return;
+  const int kd = KIND;
   int4 tv = tets[t];
   TetParam tp = tetp[t];
   double X[4][3], bc[4][3];
@@ -347,9 +347,14 @@ __global__ void k_bsr_spmv(int64_t N, const int* __restrict__ rowptr, const int*
 static void elastic_gradient(mp_ctx* c, const double* x, const double* xt, double h, double* g) {
   k_inertia_grad<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, x, xt, c->mass, c->pinned, g);
   LAUNCH_CHECK();
-  if (c->T) {
-    k_tet_grad<<<grid_for(c->T, 128), 128, 0, c->stream>>>(c->T, c->tets, c->tetp, c->kind, c->pinned, x,
-                                                           h * h, g);
+  if (c->T_snh) {
+    k_tet_grad<2><<<grid_for(c->T_snh, 128), 128, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned, x,
+                                                                  h * h, g);
+    LAUNCH_CHECK();
+  }
+  if (c->T_arap) {
+    k_tet_grad<1><<<grid_for(c->T_arap, 128), 128, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp,
+                                                                   c->pinned, x, h * h, g);
     LAUNCH_CHECK();
   }
 }
@@ -358,9 +363,14 @@ static void assemble_elastic_bsr(mp_ctx* c, const double* x, double h) {
   CUDA_CHECK(cudaMemsetAsync(c->bsr.p, 0, sizeof(double) * 9 * c->nnzb, c->stream));
   k_bsr_diag<<<grid_for(c->N, 256), 256, 0, c->stream>>>(c->N, c->diag_slot, c->mass, c->pinned, c->bsr);
   LAUNCH_CHECK();
-  if (c->T) {
-    k_tet_hessian<<<grid_for(c->T, 64), 64, 0, c->stream>>>(c->T, c->tets, c->tetp, c->kind, c->pinned,
-                                                            c->tet_slot, x, h * h, c->bsr);
+  if (c->T_snh) {
+    k_tet_hessian<2><<<grid_for(c->T_snh, 64), 64, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned,
+                                                                   c->tet_slot, x, h * h, c->bsr);
+    LAUNCH_CHECK();
+  }
+  if (c->T_arap) {
+    k_tet_hessian<1><<<grid_for(c->T_arap, 64), 64, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp,
+                                                                    c->pinned, c->tet_slot, x, h * h, c->bsr);
     LAUNCH_CHECK();
   }
 }

@@ -201,22 +201,32 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   }
   // tets and per-tet constants
   const int64_t T = c->T;
+  // tets grouped by material (SNH, then ARAP, then none) so every kernel
+  // runs a kind-specialised instantiation over a contiguous range
+  std::vector<int64_t> torder(T);
+  std::iota(torder.begin(), torder.end(), (int64_t)0);
+  auto rank_of = [&](int64_t t) { return s->kind[t] == 2 ? 0 : (s->kind[t] == 1 ? 1 : 2); };
+  std::stable_sort(torder.begin(), torder.end(), [&](int64_t a, int64_t b) { return rank_of(a) < rank_of(b); });
   std::vector<int4> tets(T);
   std::vector<TetParam> tp(T);
   std::vector<signed char> kind(T);
+  c->T_snh = c->T_arap = 0;
   for (int64_t t = 0; t < T; ++t) {
+    const int64_t u = torder[t];
     int id[4];
     for (int a = 0; a < 4; ++a) {
-      int64_t o = s->tets[4 * t + a];
+      int64_t o = s->tets[4 * u + a];
       if (o < 0 || o >= N) throw MpError(MP_ERR_CONFIG, "tet index out of range");
       id[a] = o2n[o];
     }
     tets[t] = make_int4(id[0], id[1], id[2], id[3]);
-    for (int q = 0; q < 9; ++q) tp[t].Bm[q] = s->Bm[9 * t + q];
-    tp[t].vol = s->vol[t];
-    tp[t].mu = s->mu[t];
-    tp[t].lam = s->lam[t];
-    kind[t] = s->kind[t];
+    for (int q = 0; q < 9; ++q) tp[t].Bm[q] = s->Bm[9 * u + q];
+    tp[t].vol = s->vol[u];
+    tp[t].mu = s->mu[u];
+    tp[t].lam = s->lam[u];
+    kind[t] = s->kind[u];
+    if (kind[t] == 2) ++c->T_snh;
+    else if (kind[t] == 1) ++c->T_arap;
   }
   c->tets.upload(tets.data(), T, st);
   c->tetp.upload(tp.data(), T, st);

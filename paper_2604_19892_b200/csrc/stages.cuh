@@ -42,25 +42,29 @@ static void gradient(mp_ctx* c, const double* x, const double* xt, double h, dou
 // energy.incremental_potential (energy.py:346-354)
 static double energy(mp_ctx* c, const double* x, const double* xt, double h) {
   const int nb = 64;
-  c->red_part.ensure(3 * nb);
-  CUDA_CHECK(cudaMemsetAsync(c->red_part.p, 0, sizeof(double) * 3 * nb, c->stream));
+  c->red_part.ensure(4 * nb);
+  CUDA_CHECK(cudaMemsetAsync(c->red_part.p, 0, sizeof(double) * 4 * nb, c->stream));
   k_inertia_energy<<<nb, 256, 0, c->stream>>>(c->N, x, xt, c->mass, c->red_part.p);
   LAUNCH_CHECK();
-  if (c->T) {
-    k_tet_energy<<<nb, 256, 0, c->stream>>>(c->T, c->tets, c->tetp, c->kind, x, c->red_part.p + nb);
+  if (c->T_snh) {
+    k_tet_energy<2><<<nb, 256, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, x, c->red_part.p + nb);
+    LAUNCH_CHECK();
+  }
+  if (c->T_arap) {
+    k_tet_energy<1><<<nb, 256, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp, x, c->red_part.p + 3 * nb);
     LAUNCH_CHECK();
   }
   if (c->cur.count) {
     k_contact_energy<<<nb, 256, 0, c->stream>>>(c->cur.count, c->cur.d, c->d_hat, c->kappa, c->red_part.p + 2 * nb);
     LAUNCH_CHECK();
   }
-  std::vector<double> part(3 * nb);
-  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * 3 * nb, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<double> part(4 * nb);
+  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
-  double s[3] = {0.0, 0.0, 0.0};
-  for (int q = 0; q < 3; ++q)
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int q = 0; q < 4; ++q)
     for (int b = 0; b < nb; ++b) s[q] += part[q * nb + b];
-  return 0.5 * s[0] + h * h * s[1] + s[2];
+  return 0.5 * s[0] + h * h * (s[1] + s[3]) + s[2];
 }
 
 static void copy_table(mp_ctx* c, PairTable& s, PairTable& d) {
