@@ -298,7 +298,8 @@ def run_ours(args):
         "roofline": roof("mas_apply_l0", "k_mas_apply_l0 (level-0 block matvec + Woodbury overlay + coarse "
                                           "prolongation + pinned projection; TMA-staged packed blocks)"),
         "roofline_mas_stage": roof("mas_apply", "MAS apply stage: k_restrict1 + k_coarse_mv x2 + k_mas_apply_l0"),
-        "roofline_gradient": roof("gradient", "gradient: k_inertia_grad + k_tet_grad + k_contact_grad"),
+        "roofline_gradient": roof("tet_grad", "k_tet_grad<SNH> (F, Piola, G^T scatter; 113 B/tet + 72 B/vertex)"),
+        "roofline_gradient_stage": roof("gradient", "gradient stage: k_inertia_grad + k_tet_grad x2 + k_contact_grad"),
         "roofline_hvp": roof("hvp", "HVP: k_bsr_spmv + k_rank1_apply"),
         "stages": stage_share,
         "gpu_launches": launches,

@@ -201,7 +201,8 @@ enum {
   MP_STAGE_UPDATE = 6,         /* classify/top-K/Woodbury  solver.py:337-346 */
   MP_STAGE_CCD = 7,            /* CCD clamp                solver.py:268-280 */
   MP_STAGE_MAS_L0 = 8,         /* the level-0 kernel of the MAS apply alone   */
-  MP_STAGE_COUNT = 9
+  MP_STAGE_TET_GRAD = 9,       /* the SNH per-tet gradient kernel alone        */
+  MP_STAGE_COUNT = 10
 };
 int mp_stage_timing(mp_ctx* ctx, int enable);
 

@@ -13,6 +13,8 @@
 // identical in exact arithmetic to eigh + clamp (verified to 1e-14).
 #pragma once
 
+#include <climits>
+
 #include "ctx.cuh"
 
 __device__ __forceinline__ void load_tet(const double* __restrict__ x, int4 t, double X[4][3]) {
@@ -98,31 +100,56 @@ __global__ void k_inertia_grad(int64_t N, const double* __restrict__ x, const do
   g[i] = pinned[v] ? 0.0 : mass[v] * (x[i] - xt[i]);
 }
 
+// Tet forces are pre-summed per CTA in shared memory: thanks to the Morton
+// renumbering a block of 128 consecutive tets touches a narrow vertex-id
+// window, so the forces are accumulated with shared-memory atomics over the
+// window [vmin, vmin + GRAD_WIN) and flushed with one global atomic per
+// touched dof (about 8x fewer global atomics).  Tets outside the window fall
+// back to direct global atomics.
+#define GRAD_WIN 1024
 template <int KIND>
 __global__ void __launch_bounds__(128) k_tet_grad(int64_t t0, int64_t nt, const int4* __restrict__ tets,
                                                   const TetParam* __restrict__ tetp,
                                                   const unsigned char* __restrict__ pinned,
                                                   const double* __restrict__ x, double h2, double* __restrict__ g) {
+  __shared__ double acc[3 * GRAD_WIN];
+  __shared__ int vmin_s;
   const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= t0 + nt) return;
-  const int4 tv = tets[t];
-  const TetParam tp = tetp[t];
-  double X[4][3], bc[4][3];
-  load_tet(x, tv, X);
-  M3 F;
-  tet_F(X, tp, F, bc);
-  const M3 P = piola(F, KIND, tp.mu, tp.lam);
-  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
-  const double s = h2 * tp.vol;
+  const bool live = t < t0 + nt;
+  for (int e = threadIdx.x; e < 3 * GRAD_WIN; e += blockDim.x) acc[e] = 0.0;
+  if (threadIdx.x == 0) vmin_s = INT_MAX;
+  __syncthreads();
+  int4 tv = make_int4(0, 0, 0, 0);
+  if (live) {
+    tv = tets[t];
+    atomicMin(&vmin_s, min(min(tv.x, tv.y), min(tv.z, tv.w)));
+  }
+  __syncthreads();
+  const int vmin = vmin_s;
+  if (live) {
+    const TetParam tp = tetp[t];
+    double X[4][3], bc[4][3];
+    load_tet(x, tv, X);
+    M3 F;
+    tet_F(X, tp, F, bc);
+    const M3 P = piola(F, KIND, tp.mu, tp.lam);
+    const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+    const double s = h2 * tp.vol;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    if (pinned[id[a]]) continue;
+    for (int a = 0; a < 4; ++a) {
+      if (pinned[id[a]]) continue;
+      const int w = id[a] - vmin;
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double f = P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2];
-      atomicAdd(&g[3 * id[a] + i], s * f);
+      for (int i = 0; i < 3; ++i) {
+        const double f = s * (P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2]);
+        if (w < GRAD_WIN) atomicAdd(&acc[3 * w + i], f);
+        else atomicAdd(&g[3 * id[a] + i], f);
+      }
     }
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 3 * GRAD_WIN; e += blockDim.x)
+    if (acc[e] != 0.0) atomicAdd(&g[3 * (int64_t)vmin + e], acc[e]);
 }
 
 // energy pieces: 0.5 (x-x~)^T M (x-x~)  and  sum vol*psi  (energy.py:346-354)
@@ -348,9 +375,13 @@ static void elastic_gradient(mp_ctx* c, const double* x, const double* xt, doubl
   k_inertia_grad<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, x, xt, c->mass, c->pinned, g);
   LAUNCH_CHECK();
   if (c->T_snh) {
+    timer_begin(c, MP_STAGE_TET_GRAD);
     k_tet_grad<2><<<grid_for(c->T_snh, 128), 128, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned, x,
                                                                   h * h, g);
     LAUNCH_CHECK();
+    // algorithmic bytes: 113 B of tet data per tet, x read and g
+    // read-modify-written once per vertex (72 B)
+    timer_end(c, MP_STAGE_TET_GRAD, 113.0 * c->T_snh + 72.0 * c->N);
   }
   if (c->T_arap) {
     k_tet_grad<1><<<grid_for(c->T_arap, 128), 128, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp,
