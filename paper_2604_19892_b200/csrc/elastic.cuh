@@ -100,56 +100,29 @@ __global__ void k_inertia_grad(int64_t N, const double* __restrict__ x, const do
   g[i] = pinned[v] ? 0.0 : mass[v] * (x[i] - xt[i]);
 }
 
-// Tet forces are pre-summed per CTA in shared memory: thanks to the Morton
-// renumbering a block of 128 consecutive tets touches a narrow vertex-id
-// window, so the forces are accumulated with shared-memory atomics over the
-// window [vmin, vmin + GRAD_WIN) and flushed with one global atomic per
-// touched dof (about 8x fewer global atomics).  Tets outside the window fall
-// back to direct global atomics.
-#define GRAD_WIN 1024
 template <int KIND>
 __global__ void __launch_bounds__(128) k_tet_grad(int64_t t0, int64_t nt, const int4* __restrict__ tets,
                                                   const TetParam* __restrict__ tetp,
                                                   const unsigned char* __restrict__ pinned,
                                                   const double* __restrict__ x, double h2, double* __restrict__ g) {
-  __shared__ double acc[3 * GRAD_WIN];
-  __shared__ int vmin_s;
   const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool live = t < t0 + nt;
-  for (int e = threadIdx.x; e < 3 * GRAD_WIN; e += blockDim.x) acc[e] = 0.0;
-  if (threadIdx.x == 0) vmin_s = INT_MAX;
-  __syncthreads();
-  int4 tv = make_int4(0, 0, 0, 0);
-  if (live) {
-    tv = tets[t];
-    atomicMin(&vmin_s, min(min(tv.x, tv.y), min(tv.z, tv.w)));
-  }
-  __syncthreads();
-  const int vmin = vmin_s;
-  if (live) {
-    const TetParam tp = tetp[t];
-    double X[4][3], bc[4][3];
-    load_tet(x, tv, X);
-    M3 F;
-    tet_F(X, tp, F, bc);
-    const M3 P = piola(F, KIND, tp.mu, tp.lam);
-    const int id[4] = {tv.x, tv.y, tv.z, tv.w};
-    const double s = h2 * tp.vol;
+  if (t >= t0 + nt) return;
+  const int4 tv = tets[t];
+  const TetParam tp = tetp[t];
+  double X[4][3], bc[4][3];
+  load_tet(x, tv, X);
+  M3 F;
+  tet_F(X, tp, F, bc);
+  const M3 P = piola(F, KIND, tp.mu, tp.lam);
+  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+  const double s = h2 * tp.vol;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      if (pinned[id[a]]) continue;
-      const int w = id[a] - vmin;
+  for (int a = 0; a < 4; ++a) {
+    if (pinned[id[a]]) continue;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double f = s * (P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2]);
-        if (w < GRAD_WIN) atomicAdd(&acc[3 * w + i], f);
-        else atomicAdd(&g[3 * id[a] + i], f);
-      }
-    }
+    for (int i = 0; i < 3; ++i)
+      atomicAdd(&g[3 * id[a] + i], s * (P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2]));
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 3 * GRAD_WIN; e += blockDim.x)
-    if (acc[e] != 0.0) atomicAdd(&g[3 * (int64_t)vmin + e], acc[e]);
 }
 
 // energy pieces: 0.5 (x-x~)^T M (x-x~)  and  sum vol*psi  (energy.py:346-354)
