@@ -1,0 +1,92 @@
+"""Closed-loop parity of the sm_100a solver against the CPU oracle for the
+SolverConfig options the reference exposes but the golden runs do not
+cover: update strategies (Woodbury / Freeze / FullRebuild), per-subdomain vs
+global CCD, MAS depth (levels, coarse_block) and block size
+(`solver.py:48-77`, `mas.py:138-179`, `solver.py:268-280`).
+
+Frames are short and well conditioned (stacked boxes, K = 256, and the drop
+scene), so iteration counts are compared within +-5% (at least +-1) and the
+final positions within 1e-6 relative.  Also: the error paths keep the
+reference's codes.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_config, load_golden, rel_err, scene_from_golden
+
+from oracle import solver as osol
+
+pytestmark = pytest.mark.gpu
+
+OPTIONS = [
+    {"update_strategy": "Freeze"},
+    {"update_strategy": "FullRebuild"},
+    {"ccd_per_subdomain": False},
+    {"levels": 0},
+    {"levels": 1, "coarse_block": 2},
+    {"block_size": 16},
+    {"block_size": 8, "levels": 3, "coarse_block": 3},
+]
+
+
+def _ocfg(cfg):
+    return osol.SolverConfig(eps=cfg.eps, delta=cfg.delta, iter_max=cfg.iter_max, K=cfg.K, block_size=cfg.block_size,
+                             levels=cfg.levels, coarse_block=cfg.coarse_block,
+                             ccd_per_subdomain=cfg.ccd_per_subdomain, update_strategy=cfg.update_strategy)
+
+
+@pytest.mark.parametrize("name", ["stacked_k256", "drop"])
+@pytest.mark.parametrize("opt", OPTIONS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
+def test_options_match_oracle(name, opt):
+    from paper_2604_19892_b200 import solver
+
+    g = load_golden(name)
+    cfg = golden_config(g)
+    for k, v in opt.items():
+        setattr(cfg, k, v)
+    cfg.iter_max = 400
+    scene = scene_from_golden(g)
+    osc = osol.Scene.from_golden(g)
+    x, v, h = g["rest"].ravel().copy(), g["v0"].copy(), float(g["h"])
+    ox, ov = x.copy(), v.copy()
+    for f in range(2):
+        st, tr = solver.step(scene, x, v, h, cfg)
+        ox, ov, otr = osol.step(osc, ox, ov, h, _ocfg(cfg))
+        assert abs(tr.iterations - otr.iterations) <= max(1, round(0.05 * otr.iterations)), \
+            (f, tr.iterations, otr.iterations)
+        assert tr.converged == otr.converged
+        assert rel_err(st.x, ox) <= 1e-6, (f, rel_err(st.x, ox))
+        x, v = st.x, st.v
+
+
+def test_penetration_raises_reference_code():
+    from paper_2604_19892_b200 import solver
+    from paper_2604_19892_b200.errors import PenetrationError
+
+    g = load_golden("drop")
+    scene = scene_from_golden(g)
+    ctx = scene.context(golden_config(g))
+    x = g["rest"].reshape(-1, 3).copy()
+    # drop the tet through the floor slab: a vertex ends up on a floor face
+    free = ~g["dirichlet"].astype(bool)
+    x[free, 2] = 0.0
+    x[free, :2] = 0.0
+    with pytest.raises(PenetrationError) as e:
+        ctx.constraint_set(x.ravel())
+    assert e.value.code == "penetration-detected"
+    _ = solver
+
+
+def test_unsupported_rules_are_config_errors():
+    from paper_2604_19892_b200 import solver
+    from paper_2604_19892_b200.errors import ConfigError
+
+    g = load_golden("drop")
+    scene = scene_from_golden(g)
+    x, v = g["rest"].ravel(), np.zeros(g["rest"].size)
+    for bad in ({"preconditioner": "Jacobi"}, {"direction_rule": "FR"}, {"delta": 1.5}, {"iter_max": 0}):
+        cfg = solver.SolverConfig(**bad)
+        with pytest.raises(ConfigError) as e:
+            solver.step(scene, x, v, 0.01, cfg)
+        assert e.value.code == "config-error"
