@@ -276,6 +276,122 @@ __device__ bool sweep_regs(LOAD load, int m, double* rowk, double (&R)[SWEEP_T][
   return true;
 }
 
+// Blocked sweep (6 panels of 16 pivots) for the coarse-level pivot blocks,
+// where one CTA runs alone on the critical path.  Panel K = tile row/column
+// K of the register layout.  Per panel: the 16 x 16 pivot block P is staged
+// in smem and swept by warp 0 alone (warp-level broadcasts, no CTA barrier
+// inside the 16 pivot steps); W = A_:K P^-1 (column panel and P^-1 staged
+// in smem, rows padded to SWEEP_LD doubles against bank conflicts); the
+// rank-16 update A_ij -= W_i. A_jK. for i, j outside K (400 FMA per thread,
+// no barrier); block row / column K <- W^T / W.  Same sweep operator
+// (A <- -A^-1 after every panel).  Rows >= m are identity padding.
+#define SWEEP_LD 17
+#define SWEEP_SMEM (40 + 256 + 2 * 96 * SWEEP_LD)
+template <class LOAD>
+__device__ bool sweep_blocked(LOAD load, int m, double* sm, double (&R)[SWEEP_T][SWEEP_T]) {
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  double* pk = sm;                    // 2 x 16 pivot-row broadcast, [32] = SPD flag
+  double* pm = sm + 40;               // 16 x 16 (-P^-1)
+  double* acol = pm + 256;            // 96 x 16: A(i, 16K + d), row stride SWEEP_LD
+  double* wsm = acol + 96 * SWEEP_LD; // 96 x 16: W(i, c), row stride SWEEP_LD
+#pragma unroll
+  for (int a = 0; a < SWEEP_T; ++a)
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b) {
+      int i = tr + 16 * a, j = tc + 16 * b;
+      R[a][b] = (i < m && j < m) ? load(i, j) : (i == j ? 1.0 : 0.0);
+    }
+  const int np = (m + 15) >> 4;
+#pragma unroll
+  for (int K = 0; K < SWEEP_T; ++K) {
+    if (K >= np) break;
+    // (1) pivot block P = R[K][K], swept by warp 0 (lane l: row l/2,
+    //     columns 8 (l%2) .. +8)
+    pm[tr * 16 + tc] = R[K][K];
+    __syncthreads();
+    if (tid < 32) {
+      const int lane = tid, r = lane >> 1, c0 = (lane & 1) * 8;
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = pm[r * 16 + c0 + q];
+      bool ok = true;
+      for (int k = 0; k < 16; ++k) {
+        double* row = pk + (k & 1) * 16;
+        if (r == k) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) row[c0 + q] = v[q];
+        }
+        __syncwarp();
+        const double piv = row[k];
+        if (!(piv > 0.0)) {
+          ok = false;
+          break;  // uniform across the warp
+        }
+        const double inv = fast_rcp(piv);
+        const double ci = row[r] * inv;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c = c0 + q;
+          const double cj = row[c];
+          double t = fma(-ci, cj, v[q]);
+          if (r == k) t = cj * inv;
+          if (c == k) t = (r == k) ? -inv : ci;
+          v[q] = t;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pm[r * 16 + c0 + q] = v[q];
+      if (lane == 0) pk[32] = ok ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (pk[32] == 0.0) return false;  // uniform across the CTA
+    R[K][K] = pm[tr * 16 + tc];
+    // (2) stage the column panel A(i, K.) for i outside K; -P^-1 is in pm
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a)
+      if (a != K) acol[(tr + 16 * a) * SWEEP_LD + tc] = R[a][K];
+    __syncthreads();
+    // (3) W(i, c) = A_iK P^-1 = -sum_d A(i, Kd) pm(d, c), c = tc
+    double w[SWEEP_T];
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a) {
+      w[a] = 0.0;
+      if (a == K) continue;
+      const double* ar = acol + (tr + 16 * a) * SWEEP_LD;
+#pragma unroll
+      for (int d = 0; d < 16; ++d) w[a] = fma(-ar[d], pm[d * 16 + tc], w[a]);
+      wsm[(tr + 16 * a) * SWEEP_LD + tc] = w[a];
+    }
+    __syncthreads();
+    // (4) A_ij -= W(i, .) . A(j, K.) for i, j outside K
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      double wi[SWEEP_T], aj[SWEEP_T];
+#pragma unroll
+      for (int a = 0; a < SWEEP_T; ++a) {
+        wi[a] = (a == K) ? 0.0 : wsm[(tr + 16 * a) * SWEEP_LD + d];
+        aj[a] = (a == K) ? 0.0 : acol[(tc + 16 * a) * SWEEP_LD + d];
+      }
+#pragma unroll
+      for (int a = 0; a < SWEEP_T; ++a) {
+        if (a == K) continue;
+#pragma unroll
+        for (int b = 0; b < SWEEP_T; ++b)
+          if (b != K) R[a][b] = fma(-wi[a], aj[b], R[a][b]);
+      }
+    }
+    // (5) block column K <- W, block row K <- W^T
+#pragma unroll
+    for (int a = 0; a < SWEEP_T; ++a)
+      if (a != K) R[a][K] = w[a];
+#pragma unroll
+    for (int b = 0; b < SWEEP_T; ++b)
+      if (b != K) R[K][b] = wsm[(tc + 16 * b) * SWEEP_LD + tr];
+    __syncthreads();  // acol / wsm / pm are rewritten by the next panel
+  }
+  return true;
+}
+
 // element (i, j) of a symmetric m x m matrix is the stored representative
 // of the cyclic-diagonal packing (common.cuh) at position cyc_index(m, i, j)
 __device__ __forceinline__ bool cyc_rep(int m, int i, int j) {
@@ -332,11 +448,11 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mful
 __global__ void __launch_bounds__(256, 1)
 k_block_sweep(int kb, const double* __restrict__ A, int lda, int k0, double* __restrict__ out,
               int* __restrict__ status) {
-  __shared__ double rowk[2 * 96];
+  __shared__ double swsm[SWEEP_SMEM];
   const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
   double R[SWEEP_T][SWEEP_T];
   auto load = [&](int i, int j) -> double { return __ldg(A + (int64_t)(k0 + j) * lda + k0 + i); };
-  if (!sweep_regs(load, kb, rowk, R)) {
+  if (!sweep_blocked(load, kb, swsm, R)) {
     if (threadIdx.x == 0) atomicExch(status, 1);
     return;
   }
