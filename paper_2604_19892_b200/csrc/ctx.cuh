@@ -89,16 +89,19 @@ struct CoarseLevel {
   DBuf<double> rsum;  // 3A restricted raw sums
   DBuf<double> r;     // 3A restriction C_l g (averages)
   DBuf<double> ypart; // n: M_l^-1 r accumulated over diagonal chunks
-  DBuf<double> dn_col, dn_W, dn_P;  // blocked-sweep scratch
+  DBuf<double> dn_col, dn_W, dn_P, dn_Pn;  // blocked-sweep scratch
   int chunks = 1;
-  // each coarse level is built on its own stream, concurrently with level 0
-  cudaStream_t st = nullptr;
-  cudaEvent_t done = nullptr;
+  // each coarse level is built on its own stream (st2: lookahead updates),
+  // concurrently with level 0
+  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaEvent_t done = nullptr, ev_w = nullptr, ev_u = nullptr;
   cublasHandle_t blas = nullptr;
   ~CoarseLevel() {
     if (blas) cublasDestroy(blas);
-    if (done) cudaEventDestroy(done);
+    for (cudaEvent_t e : {done, ev_w, ev_u})
+      if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
+    if (st2) cudaStreamDestroy(st2);
   }
 };
 

@@ -120,7 +120,10 @@ static void setup_levels(mp_ctx* c) {
     L->r.ensure(L->n);
     L->ypart.ensure((size_t)L->n);
     CUDA_CHECK(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&L->st2, cudaStreamNonBlocking));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_w, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_u, cudaEventDisableTiming));
     if (cublasCreate(&L->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate (coarse)");
     cublasSetStream(L->blas, L->st);
     c->levels.push_back(L);

@@ -103,29 +103,58 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   const int nb = 96;
   const int n = L.n;
   double* A = L.dense;
-  cudaStream_t st = L.st;
+  cudaStream_t st = L.st, st2 = L.st2;
   L.dn_col.ensure((size_t)n * nb);
   L.dn_W.ensure((size_t)n * nb);
-  L.dn_P.ensure((size_t)nb * nb);
+  L.dn_P.ensure(2 * (size_t)nb * nb);
+  L.dn_Pn.ensure((size_t)nb * nb);
   const double one = 1.0, mone = -1.0, zero = 0.0;
-  for (int k0 = 0; k0 < n; k0 += nb) {
-    const int kb = std::min(nb, n - k0);
-    k_block_sweep<<<1, 256, 0, st>>>(kb, A, n, k0, L.dn_P, status);
-    LAUNCH_CHECK();
-    CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A + (size_t)k0 * n, sizeof(double) * (size_t)n * kb,
-                               cudaMemcpyDeviceToDevice, st));
+  auto gemm = [&](cudaStream_t s, cublasOperation_t tb, int mm, int nn, int kk, const double* alpha,
+                  const double* Am, int lda, const double* Bm, int ldb, const double* beta, double* Cm, int ldc,
+                  const char* what) {
+    cublasSetStream(L.blas, s);
+    if (cublasDgemm(L.blas, CUBLAS_OP_N, tb, mm, nn, kk, alpha, Am, lda, Bm, ldb, beta, Cm, ldc) !=
+        CUBLAS_STATUS_SUCCESS)
+      throw MpError(MP_ERR_CUDA, what);
+    ++c->launches;
+  };
+  // Lookahead: the next pivot block is updated first (a kb x kb x kb GEMM)
+  // and swept on st while the rank-kb update of the whole matrix runs on st2.
+  const int nblk = (n + nb - 1) / nb;
+  k_block_sweep<<<1, 256, 0, st>>>(std::min(nb, n), A, n, 0, L.dn_P, status);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A, sizeof(double) * (size_t)n * std::min(nb, n), cudaMemcpyDeviceToDevice,
+                             st));
+  for (int K = 0; K < nblk; ++K) {
+    const int k0 = K * nb, kb = std::min(nb, n - k0);
+    double* Pk = L.dn_P.p + (size_t)(K & 1) * nb * nb;
     // W = -colK * (-P^-1)
-    if (cublasDgemm(L.blas, CUBLAS_OP_N, CUBLAS_OP_N, n, kb, kb, &mone, L.dn_col, n, L.dn_P, kb, &zero, L.dn_W, n) !=
-        CUBLAS_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, "cublasDgemm (coarse W)");
-    // A -= W colK^T
-    if (cublasDgemm(L.blas, CUBLAS_OP_N, CUBLAS_OP_T, n, n, kb, &mone, L.dn_W, n, L.dn_col, n, &one, A, n) !=
-        CUBLAS_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, "cublasDgemm (coarse update)");
-    c->launches += 2;
-    k_block_fix<<<grid_for((int64_t)n * kb, 256), 256, 0, st>>>(n, kb, k0, L.dn_W, L.dn_P, A);
+    gemm(st, CUBLAS_OP_N, n, kb, kb, &mone, L.dn_col, n, Pk, kb, &zero, L.dn_W, n, "cublasDgemm (coarse W)");
+    const int k1 = k0 + kb, kb1 = std::min(nb, n - k1);
+    if (K + 1 < nblk) {
+      // next pivot block, updated ahead: A(K+1, K+1) - W(K+1 rows) colK(K+1 rows)^T
+      CUDA_CHECK(cudaMemcpy2DAsync(L.dn_Pn.p, sizeof(double) * kb1, A + (size_t)k1 * n + k1, sizeof(double) * n,
+                                   sizeof(double) * kb1, kb1, cudaMemcpyDeviceToDevice, st));
+      gemm(st, CUBLAS_OP_T, kb1, kb1, kb, &mone, L.dn_W.p + k1, n, L.dn_col.p + k1, n, &one, L.dn_Pn, kb1,
+           "cublasDgemm (coarse lookahead)");
+    }
+    CUDA_CHECK(cudaEventRecord(L.ev_w, st));
+    // whole-matrix update, fix-up of block K and the next column panel: st2
+    CUDA_CHECK(cudaStreamWaitEvent(st2, L.ev_w, 0));
+    gemm(st2, CUBLAS_OP_T, n, n, kb, &mone, L.dn_W, n, L.dn_col, n, &one, A, n, "cublasDgemm (coarse update)");
+    k_block_fix<<<grid_for((int64_t)n * kb, 256), 256, 0, st2>>>(n, kb, k0, L.dn_W, Pk, A);
     LAUNCH_CHECK();
+    if (K + 1 < nblk)
+      CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A + (size_t)k1 * n, sizeof(double) * (size_t)n * kb1,
+                                 cudaMemcpyDeviceToDevice, st2));
+    CUDA_CHECK(cudaEventRecord(L.ev_u, st2));
+    if (K + 1 < nblk) {
+      k_block_sweep<<<1, 256, 0, st>>>(kb1, L.dn_Pn, kb1, 0, L.dn_P.p + (size_t)((K + 1) & 1) * nb * nb, status);
+      LAUNCH_CHECK();
+    }
+    CUDA_CHECK(cudaStreamWaitEvent(st, L.ev_u, 0));
   }
+  cublasSetStream(L.blas, st);
   k_pack_neg_sym<<<grid_for(cyc_size(n), 256), 256, 0, st>>>(n, A, L.inv);
   LAUNCH_CHECK();
 }
