@@ -212,9 +212,12 @@ int mp_stage_timing(mp_ctx* ctx, int enable);
  * potential at every iterate into mp_iter_record.energy (default 0).
  * MP_OPT_APPLY_TMA: stage level-0 MAS blocks with TMA bulk copies (1,
  * default) or per-thread cp.async (0); MP_OPT_APPLY_STAGES (2 or 3) and
- * MP_OPT_APPLY_CTAS (persistent CTAs per SM) tune its pipeline; same results. */
+ * MP_OPT_APPLY_CTAS (persistent CTAs per SM) tune its pipeline; same results.
+ * MP_OPT_BP_FUSED: constraint-set / CCD / certificate pair work fused into
+ * the grid enumeration (1, default) or over a stored pair list (0); same
+ * results. */
 enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3, MP_OPT_APPLY_STAGES = 4,
-       MP_OPT_APPLY_CTAS = 5 };
+       MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6 };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 

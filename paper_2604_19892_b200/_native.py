@@ -247,7 +247,8 @@ class NativeContext:
         return [recs[i] for i in range(min(n.value, cap))], bool(conv.value), int(flags.value)
 
     def set_option(self, option, value):
-        """MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2 (include/maspncg.h)."""
+        """MP_OPT_* of include/maspncg.h (CCD_EXACT_SET 1, RECORD_ENERGY 2, APPLY_TMA 3,
+        APPLY_STAGES 4, APPLY_CTAS 5, BP_FUSED 6)."""
         self._check(self.lib.mp_set_option(self.h, int(option), int(value)))
 
     # ---- per-stage CUDA-event timing ----

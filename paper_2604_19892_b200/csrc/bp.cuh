@@ -393,14 +393,133 @@ __global__ void k_entry_fill(const int* __restrict__ total_dev, int64_t nobj, in
                              const int* __restrict__ ecell, const int* __restrict__ tri_start,
                              const int* __restrict__ edge_start, const int* __restrict__ pt_start,
                              int* __restrict__ tri_cur, int* __restrict__ edge_cur, int* __restrict__ pt_cur,
-                             int* __restrict__ tri_ent, int* __restrict__ edge_ent, int* __restrict__ pt_ent) {
+                             int* __restrict__ tri_ent, int* __restrict__ edge_ent, int* __restrict__ pt_ent,
+                             const double* __restrict__ elo, const double* __restrict__ ehi,
+                             double* __restrict__ tri_box, double* __restrict__ edge_box,
+                             double* __restrict__ pt_box) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= *total_dev) return;
   int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
   int cell = ecell[e];
-  if (p < F) tri_ent[tri_start[cell] + atomicAdd(&tri_cur[cell], 1)] = p;
-  else if (p < P) edge_ent[edge_start[cell] + atomicAdd(&edge_cur[cell], 1)] = p - (int)F;
-  else pt_ent[pt_start[cell] + atomicAdd(&pt_cur[cell], 1)] = p - (int)P;
+  int pos;
+  double* box;
+  if (p < F) {
+    pos = tri_start[cell] + atomicAdd(&tri_cur[cell], 1);
+    tri_ent[pos] = p;
+    box = tri_box;
+  } else if (p < P) {
+    pos = edge_start[cell] + atomicAdd(&edge_cur[cell], 1);
+    edge_ent[pos] = p - (int)F;
+    box = edge_box;
+  } else {
+    pos = pt_start[cell] + atomicAdd(&pt_cur[cell], 1);
+    pt_ent[pos] = p - (int)P;
+    box = pt_box;
+  }
+  // the box travels with the entry: the query lanes read it coalesced
+  double* b = box + 6 * (int64_t)pos;
+  const double* l = elo + 3 * (int64_t)p;
+  const double* h = ehi + 3 * (int64_t)p;
+  reinterpret_cast<double2*>(b)[0] = make_double2(l[0], l[1]);
+  reinterpret_cast<double2*>(b)[1] = make_double2(l[2], h[0]);
+  reinterpret_cast<double2*>(b)[2] = make_double2(h[1], h[2]);
+}
+
+// ---------------------------------------------------------------------------
+// per-pair work of each mode.  pair_work is called by all 32 lanes of a warp
+// (ballots / warp minimum inside); live lanes carry one reference pair:
+// PT (a = surface vertex device id, b = triangle), EE (a < b edge indices).
+
+__device__ __forceinline__ int warp_slot(bool emit, int* counter) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, emit);
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+struct PairArgs {
+  const int* tri;         // surface order (CCD, ccd.py:229-231)
+  const int* tri_sorted;  // rows sorted by original id (constraint set, contact.py:133-135)
+  const int* edge;
+  const double* x;
+  BpOut O;
+  ContactParams CP;
+  CcdParams CC;
+  unsigned long long* n_pairs;  // fused enumeration: reference pairs seen
+};
+
+template <int MODE>
+__device__ __forceinline__ void pair_work(bool live, bool is_pt, int a, int b, int64_t i, const PairArgs& A) {
+  const int lane = threadIdx.x & 31;
+  const BpOut& O = A.O;
+  const double* x = A.x;
+  int vid[4] = {0, 0, 0, 0}, vid_ccd[4] = {0, 0, 0, 0};
+  if (live) {
+    if (is_pt) {
+      vid_ccd[0] = a; vid_ccd[1] = A.tri[3 * b]; vid_ccd[2] = A.tri[3 * b + 1]; vid_ccd[3] = A.tri[3 * b + 2];
+      vid[0] = a; vid[1] = A.tri_sorted[3 * b]; vid[2] = A.tri_sorted[3 * b + 1]; vid[3] = A.tri_sorted[3 * b + 2];
+    } else {
+      vid_ccd[0] = vid[0] = A.edge[2 * a]; vid_ccd[1] = vid[1] = A.edge[2 * a + 1];
+      vid_ccd[2] = vid[2] = A.edge[2 * b]; vid_ccd[3] = vid[3] = A.edge[2 * b + 1];
+    }
+  }
+  if (MODE == BP_CONTACT) {
+    double d = 0.0, gr[12];
+    if (live) {
+      double X[4][3];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) X[r][k] = x[3 * vid[r] + k];
+      d = is_pt ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
+      if (d <= 0.0) O.counter[1] = 1;
+    }
+    const bool emit = live && d > 0.0 && d < A.CP.d_hat;
+    const int slot = warp_slot(emit, O.counter);
+    if (emit && slot < O.cap) write_contact(O, A.CP, slot, is_pt ? 1 : 0, vid, d, gr);
+  } else if (MODE == BP_CCD) {
+    bool cert_p = true;
+    const double al = live ? ccd_pair_alpha(x, A.CC.p, vid_ccd, is_pt, A.CC.alpha_l, &cert_p) : 1.0;
+    if (live && al < 1.0) {
+      // read before the atomic: once a subdomain's minimum has settled most
+      // pairs cannot lower it, so contended atomics stay rare
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double* ad = &O.alpha_d[vid_ccd[r] / A.CC.bs];
+        if (al < *(volatile double*)ad) atomic_min_nonneg(ad, al);
+      }
+    }
+    // global minimum: warp minimum first, one filtered atomic per warp
+    const double wm = warp_min_all(al);
+    if (lane == 0 && wm < *(volatile double*)O.min_alpha) atomic_min_nonneg(O.min_alpha, wm);
+    if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
+    if (live && O.verts && i >= 0 && i < O.cap) {
+      O.verts[i] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
+      O.ccd_ispt[i] = is_pt ? 1 : 0;
+      O.alpha_pair[i] = al;
+    }
+  } else if (MODE == BP_CERT) {
+    if (live && !ccd_certify_pair(x, A.CC.p, O.alpha_d, A.CC.bs, vid_ccd, is_pt)) O.counter[1] = 1;
+  }
+}
+
+// the stored list: pairs [0, n_pt) are PT, [n_pt, n) are EE
+template <int MODE>
+__global__ void __launch_bounds__(256) k_pairs(const int* __restrict__ n_pt_dev, const int* __restrict__ n_dev,
+                                               int64_t cap, const int* __restrict__ pa, const int* __restrict__ pb,
+                                               PairArgs A) {
+  const int64_t n_pt = *n_pt_dev;
+  const int64_t n = *n_dev < cap ? *n_dev : cap;  // n > cap: the caller grows and reruns
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (pair_work ballots across the warp)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x - lane); base < n; base += stride) {
+    const int64_t i = base + lane;
+    const bool live = i < n;
+    pair_work<MODE>(live, i < n_pt, live ? pa[i] : 0, live ? pb[i] : 0, i, A);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -411,6 +530,7 @@ __global__ void k_entry_fill(const int* __restrict__ total_dev, int64_t nobj, in
 struct BpTables {
   HGrid G;
   const int *pt_start, *pt_ent, *tri_start, *tri_ent, *edge_start, *edge_ent;
+  const double *pt_box, *tri_box, *edge_box;  // per entry (lo, hi)
   const int* level;                     // (F+E+V)
   const unsigned* lmask;                // [3] levels holding triangles / edges / points
   const int* rc;                        // (F+E+V)*6 reference-grid cell ranges
@@ -437,25 +557,62 @@ __device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, c
 // order at the offsets of the count pass (deterministic list).
 #define WARP_FULL 0xffffffffu
 
-__device__ __forceinline__ void warp_emit(bool pass, int lane, int& n, int o, int a, int b, bool fill, int* pa,
-                                          int* pb, int64_t cap) {
+// EM: HQ_COUNT / HQ_FILL build the stored list (count pass, scan, fill
+// pass); a BP mode fuses the per-pair work into the enumeration instead --
+// order-free consumers only (CCD / certificate minima and flags, contacts
+// that are key-sorted afterwards): passing pairs queue in shared memory and
+// are worked 32 at a time, so no list is written and no count pass runs.
+enum { HQ_COUNT = -2, HQ_FILL = -1 };
+#define HQ_QUEUE 64
+
+template <int EM>
+__device__ __forceinline__ void hq_emit(bool pass, bool is_pt, int lane, int& n, int o, int a, int b, int* pa, int* pb,
+                                        int64_t cap, int2* q, int& qn, const PairArgs& A) {
   const unsigned m = __ballot_sync(WARP_FULL, pass);
-  if (fill && pass) {
-    const int64_t pos = (int64_t)o + n + __popc(m & ((1u << lane) - 1u));
-    if (pos < cap) {
-      pa[pos] = a;
-      pb[pos] = b;
+  const int rank = __popc(m & ((1u << lane) - 1u));
+  if (EM == HQ_FILL) {
+    if (pass) {
+      const int64_t pos = (int64_t)o + n + rank;
+      if (pos < cap) {
+        pa[pos] = a;
+        pb[pos] = b;
+      }
+    }
+  } else if (EM >= 0) {
+    if (pass) q[qn + rank] = make_int2(a, b);
+    qn += __popc(m);
+    if (qn >= 32) {
+      __syncwarp();
+      qn -= 32;
+      const int2 pr = q[qn + lane];
+      __syncwarp();
+      pair_work<(EM >= 0 ? EM : 0)>(true, is_pt, pr.x, pr.y, -1, A);
     }
   }
   n += __popc(m);
 }
 
+template <int EM>
+__device__ __forceinline__ void hq_finish(bool is_pt, int lane, int n, int* cnt, int2* q, int qn, const PairArgs& A) {
+  if (EM == HQ_COUNT) {
+    if (lane == 0) *cnt = n;
+  } else if (EM >= 0) {
+    __syncwarp();
+    if (qn > 0) {
+      const int2 pr = q[lane < qn ? lane : 0];
+      pair_work<(EM >= 0 ? EM : 0)>(lane < qn, is_pt, pr.x, pr.y, -1, A);
+    }
+    if (lane == 0 && n) atomicAdd(A.n_pairs, (unsigned long long)n);
+  }
+}
+
 // points query the triangles of every level >= their own
-template <bool FILL>
+template <int EM>
 __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const int* __restrict__ sverts,
                                                    const int* __restrict__ tri, const double* __restrict__ x,
                                                    int* __restrict__ cnt, const int* __restrict__ off,
-                                                   int* __restrict__ pa, int* __restrict__ pb, int64_t cap) {
+                                                   int* __restrict__ pa, int* __restrict__ pb, int64_t cap,
+                                                   PairArgs A) {
   const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (q >= V) return;  // warp-uniform
@@ -463,7 +620,10 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
   const double* pl = T.elo + 3 * (T.P + q);
   const double* ph = T.ehi + 3 * (T.P + q);
   int n = 0;
-  const int o = FILL ? off[q] : 0;
+  const int o = EM == HQ_FILL ? off[q] : 0;
+  __shared__ int2 qbuf[4][HQ_QUEUE];
+  int2* Q = qbuf[threadIdx.x >> 5];
+  int qn = 0;
   const unsigned mask = T.lmask[0];
   for (int l = T.level[T.P + q]; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
@@ -480,30 +640,34 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
             int t = 0;
             if (e < e1) {
               t = T.tri_ent[e];
-              const double* tl = T.elo + 3 * (int64_t)t;
-              pass = boxes_meet(pl, ph, tl, T.ehi + 3 * (int64_t)t) && hg_owns(T.G, l, a, b, c, pl, tl) &&
+              const double* tl = T.tri_box + 6 * (int64_t)e;
+              pass = boxes_meet(pl, ph, tl, tl + 3) && hg_owns(T.G, l, a, b, c, pl, tl) &&
                      pt_ref_pass(T, tri, x, v, q, t);
             }
-            warp_emit(pass, lane, n, o, v, t, FILL, pa, pb, cap);
+            hq_emit<EM>(pass, true, lane, n, o, v, t, pa, pb, cap, Q, qn, A);
           }
         }
   }
-  if (!FILL && lane == 0) cnt[q] = n;
+  hq_finish<EM>(true, lane, n, cnt ? cnt + q : nullptr, Q, qn, A);
 }
 
 // triangles query the points of every level above their own
-template <bool FILL>
+template <int EM>
 __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const int* __restrict__ sverts,
                                                  const int* __restrict__ tri, const double* __restrict__ x,
                                                  int* __restrict__ cnt, const int* __restrict__ off,
-                                                 int* __restrict__ pa, int* __restrict__ pb, int64_t cap) {
+                                                 int* __restrict__ pa, int* __restrict__ pb, int64_t cap,
+                                                 PairArgs A) {
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= F) return;
   const double* tl = T.elo + 3 * t;
   const double* th = T.ehi + 3 * t;
   int n = 0;
-  const int o = FILL ? off[t] : 0;
+  const int o = EM == HQ_FILL ? off[t] : 0;
+  __shared__ int2 qbuf[4][HQ_QUEUE];
+  int2* Q = qbuf[threadIdx.x >> 5];
+  int qn = 0;
   const unsigned mask = T.lmask[2];
   for (int l = T.level[t] + 1; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
@@ -520,23 +684,24 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
             int v = 0;
             if (e < e1) {
               const int q = T.pt_ent[e];
-              const double* pl = T.elo + 3 * (T.P + q);
+              const double* pl = T.pt_box + 6 * (int64_t)e;
               v = sverts[q];
-              pass = boxes_meet(pl, T.ehi + 3 * (T.P + q), tl, th) && hg_owns(T.G, l, a, b, c, pl, tl) &&
+              pass = boxes_meet(pl, pl + 3, tl, th) && hg_owns(T.G, l, a, b, c, pl, tl) &&
                      pt_ref_pass(T, tri, x, v, q, (int)t);
             }
-            warp_emit(pass, lane, n, o, v, (int)t, FILL, pa, pb, cap);
+            hq_emit<EM>(pass, true, lane, n, o, v, (int)t, pa, pb, cap, Q, qn, A);
           }
         }
   }
-  if (!FILL && lane == 0) cnt[t] = n;
+  hq_finish<EM>(true, lane, n, cnt ? cnt + t : nullptr, Q, qn, A);
 }
 
 // edges query the edges of every level >= their own (equal level: higher index)
-template <bool FILL>
+template <int EM>
 __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const int* __restrict__ edge,
                                                   int* __restrict__ cnt, const int* __restrict__ off,
-                                                  int* __restrict__ pa, int* __restrict__ pb, int64_t cap) {
+                                                  int* __restrict__ pa, int* __restrict__ pb, int64_t cap,
+                                                  PairArgs A) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= E) return;
@@ -547,7 +712,10 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
   const double* fhi = T.fhi + 3 * (T.F + i);
   const int ia = edge[2 * i], ib = edge[2 * i + 1];
   int n = 0;
-  const int o = FILL ? off[i] : 0;
+  const int o = EM == HQ_FILL ? off[i] : 0;
+  __shared__ int2 qbuf[4][HQ_QUEUE];
+  int2* Q = qbuf[threadIdx.x >> 5];
+  int qn = 0;
   const unsigned mask = T.lmask[1];
   for (int l = lv; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
@@ -564,8 +732,8 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
             int j = 0;
             if (e < e1) {
               j = T.edge_ent[e];
-              const double* jl = T.elo + 3 * (T.F + j);
-              pass = !(l == lv && j <= (int)i) && boxes_meet(il, ih, jl, T.ehi + 3 * (T.F + j)) &&
+              const double* jl = T.edge_box + 6 * (int64_t)e;
+              pass = !(l == lv && j <= (int)i) && boxes_meet(il, ih, jl, jl + 3) &&
                      hg_owns(T.G, l, a, b, c, il, jl);
               if (pass) {
                 const int ja = edge[2 * j], jb = edge[2 * j + 1];
@@ -577,92 +745,11 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
                        flj[2] <= fhi[2] && ref_reach(T.rc, T.F + i, T.F + j);
               }
             }
-            warp_emit(pass, lane, n, o, min((int)i, j), max((int)i, j), FILL, pa, pb, cap);
+            hq_emit<EM>(pass, false, lane, n, o, min((int)i, j), max((int)i, j), pa, pb, cap, Q, qn, A);
           }
         }
   }
-  if (!FILL && lane == 0) cnt[i] = n;
-}
-
-// ---------------------------------------------------------------------------
-// per-pair work over the list: pairs [0, n_pt) are PT, [n_pt, n) are EE
-
-__device__ __forceinline__ int warp_slot(bool emit, int* counter) {
-  const int lane = threadIdx.x & 31;
-  unsigned m = __ballot_sync(0xffffffffu, emit);
-  int base = 0;
-  if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  return base + __popc(m & ((1u << lane) - 1u));
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(256) k_pairs(const int* __restrict__ n_pt_dev, const int* __restrict__ n_dev,
-                                               int64_t cap, const int* __restrict__ pa, const int* __restrict__ pb,
-                                               const int* __restrict__ tri, const int* __restrict__ tri_sorted,
-                                               const int* __restrict__ edge, const double* __restrict__ x, BpOut O,
-                                               ContactParams CP, CcdParams CC) {
-  const int64_t n_pt = *n_pt_dev;
-  const int64_t n = *n_dev < cap ? *n_dev : cap;  // n > cap: the caller grows and reruns
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // warp-uniform trip count (the CONTACT emission ballots across the warp)
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x - lane); base < n; base += stride) {
-    const int64_t i = base + lane;
-    const bool live = i < n;
-    const bool is_pt = i < n_pt;
-    int vid[4] = {0, 0, 0, 0}, vid_ccd[4] = {0, 0, 0, 0};
-    if (live) {
-      const int a = pa[i], b = pb[i];
-      if (is_pt) {
-        vid_ccd[0] = a; vid_ccd[1] = tri[3 * b]; vid_ccd[2] = tri[3 * b + 1]; vid_ccd[3] = tri[3 * b + 2];
-        // constraint set: triangle sorted by original id (contact.py:133-135);
-        // CCD: surface order (ccd.py:229-231)
-        vid[0] = a; vid[1] = tri_sorted[3 * b]; vid[2] = tri_sorted[3 * b + 1]; vid[3] = tri_sorted[3 * b + 2];
-      } else {
-        vid_ccd[0] = vid[0] = edge[2 * a]; vid_ccd[1] = vid[1] = edge[2 * a + 1];
-        vid_ccd[2] = vid[2] = edge[2 * b]; vid_ccd[3] = vid[3] = edge[2 * b + 1];
-      }
-    }
-    if (MODE == BP_CONTACT) {
-      double d = 0.0, gr[12];
-      if (live) {
-        double X[4][3];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) X[a][k] = x[3 * vid[a] + k];
-        d = is_pt ? pt_distance(X[0], X[1], X[2], X[3], gr) : ee_distance(X[0], X[1], X[2], X[3], gr);
-        if (d <= 0.0) O.counter[1] = 1;
-      }
-      const bool emit = live && d > 0.0 && d < CP.d_hat;
-      const int slot = warp_slot(emit, O.counter);
-      if (emit && slot < O.cap) write_contact(O, CP, slot, is_pt ? 1 : 0, vid, d, gr);
-    } else if (MODE == BP_CCD) {
-      bool cert_p = true;
-      const double al = live ? ccd_pair_alpha(x, CC.p, vid_ccd, is_pt, CC.alpha_l, &cert_p) : 1.0;
-      if (live && al < 1.0) {
-        // read before the atomic: once a subdomain's minimum has settled most
-        // pairs cannot lower it, so contended atomics stay rare
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          double* ad = &O.alpha_d[vid_ccd[r] / CC.bs];
-          if (al < *(volatile double*)ad) atomic_min_nonneg(ad, al);
-        }
-      }
-      // global minimum: warp minimum first, one filtered atomic per warp
-      const double wm = warp_min_all(al);
-      if (lane == 0 && wm < *(volatile double*)O.min_alpha) atomic_min_nonneg(O.min_alpha, wm);
-      if (!cert_p) O.counter[1] = 1;  // certificate under the unscaled p fails
-      if (live && O.verts && i < O.cap) {
-        O.verts[i] = make_int4(vid_ccd[0], vid_ccd[1], vid_ccd[2], vid_ccd[3]);
-        O.ccd_ispt[i] = is_pt ? 1 : 0;
-        O.alpha_pair[i] = al;
-      }
-    } else if (MODE == BP_CERT) {
-      if (live && !ccd_certify_pair(x, CC.p, O.alpha_d, CC.bs, vid_ccd, is_pt)) O.counter[1] = 1;
-    }
-  }
+  hq_finish<EM>(false, lane, n, cnt ? cnt + i : nullptr, Q, qn, A);
 }
 
 // ---------------------------------------------------------------------------
@@ -775,6 +862,9 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   g.tri_ent.ensure((size_t)total_cap + 1);
   g.edge_ent.ensure((size_t)total_cap + 1);
   g.pt_ent.ensure((size_t)total_cap + 1);
+  g.tri_box.ensure(48 * (size_t)F + 6);
+  g.edge_box.ensure(48 * (size_t)c->E + 6);
+  g.pt_box.ensure(48 * (size_t)V + 6);
   for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
   k_entry_hist<<<grid_for(total_cap, 256), 256, 0, st>>>(total_dev, nobj, F, P, G, c->cell_off, g.level, c->box_elo,
@@ -788,9 +878,11 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
   k_entry_fill<<<grid_for(total_cap, 256), 256, 0, st>>>(total_dev, nobj, F, P, c->cell_off, g.ecell, g.tri_start,
                                                          g.edge_start, g.pt_start, g.tri_cnt, g.edge_cnt, g.pt_cnt,
-                                                         g.tri_ent, g.edge_ent, g.pt_ent);
+                                                         g.tri_ent, g.edge_ent, g.pt_ent, c->box_elo, c->box_ehi,
+                                                         g.tri_box, g.edge_box, g.pt_box);
   LAUNCH_CHECK();
   BpTables& T = B.T;
+  T.tri_box = g.tri_box; T.edge_box = g.edge_box; T.pt_box = g.pt_box;
   T.pt_start = g.pt_start; T.pt_ent = g.pt_ent;
   T.tri_start = g.tri_start; T.tri_ent = g.tri_ent;
   T.edge_start = g.edge_start; T.edge_ent = g.edge_ent;
@@ -826,30 +918,30 @@ static void collect_pairs(mp_ctx* c, const double* x, const BpGrid& B, int which
   }
   const int64_t cap = (int64_t)std::min(g.pa.n, g.pb.n);
   if ((which & 1) && V) {
-    k_hq_points<false><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr,
-                                                               nullptr, nullptr, 0);
+    k_hq_points<HQ_COUNT><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, g.qcnt.p, nullptr,
+                                                                  nullptr, nullptr, 0, PairArgs{});
     LAUNCH_CHECK();
-    k_hq_tris<false><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr,
-                                                             nullptr, nullptr, 0);
+    k_hq_tris<HQ_COUNT><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, g.qcnt.p + V, nullptr,
+                                                                nullptr, nullptr, 0, PairArgs{});
     LAUNCH_CHECK();
   }
   if ((which & 2) && E > 1) {
-    k_hq_edges<false><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, g.qcnt.p + V + F, nullptr, nullptr,
-                                                              nullptr, 0);
+    k_hq_edges<HQ_COUNT><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, g.qcnt.p + V + F, nullptr, nullptr,
+                                                                 nullptr, 0, PairArgs{});
     LAUNCH_CHECK();
   }
   exclusive_scan(c, g.qcnt, g.qoff, nq + 1);
   if ((which & 1) && V) {
-    k_hq_points<true><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa,
-                                                              g.pb, cap);
+    k_hq_points<HQ_FILL><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa,
+                                                                 g.pb, cap, PairArgs{});
     LAUNCH_CHECK();
-    k_hq_tris<true><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, g.qoff.p + V, g.pa,
-                                                            g.pb, cap);
+    k_hq_tris<HQ_FILL><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, g.qoff.p + V,
+                                                               g.pa, g.pb, cap, PairArgs{});
     LAUNCH_CHECK();
   }
   if ((which & 2) && E > 1) {
-    k_hq_edges<true><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa, g.pb,
-                                                             cap);
+    k_hq_edges<HQ_FILL><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, g.qoff.p + V + F, g.pa,
+                                                                g.pb, cap, PairArgs{});
     LAUNCH_CHECK();
   }
 }
@@ -859,20 +951,57 @@ static void collect_pairs(mp_ctx* c, const double* x, const BpGrid& B, int which
 // caller grows and retries); *flag = counters[1] (penetration / failed
 // certificate).  RAW leaves the list in c->grid.pa / pb and returns n,
 // with *n_pt_out the PT prefix length.
+// Fused enumeration (MODE = CONTACT / CCD / CERT without a stored list): the
+// hq kernels do the per-pair work themselves; the pair count lands in
+// c->n_pairs_dev.
+template <int MODE>
+static void fused_pairs(mp_ctx* c, const double* x, const BpGrid& B, const PairArgs& A) {
+  const int64_t V = c->V, F = c->F, E = c->E;
+  cudaStream_t st = c->stream;
+  if (B.empty) return;
+  if (V) {
+    k_hq_points<MODE><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, nullptr,
+                                                              nullptr, nullptr, 0, A);
+    LAUNCH_CHECK();
+    k_hq_tris<MODE><<<grid_for(32 * F, 128), 128, 0, st>>>(B.T, F, c->sverts, c->tri, x, nullptr, nullptr, nullptr,
+                                                            nullptr, 0, A);
+    LAUNCH_CHECK();
+  }
+  if (E > 1) {
+    k_hq_edges<MODE><<<grid_for(32 * E, 128), 128, 0, st>>>(B.T, E, c->edge, nullptr, nullptr, nullptr, nullptr, 0,
+                                                             A);
+    LAUNCH_CHECK();
+  }
+}
+
 template <int MODE>
 static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
                       int* flag, int which = 3, int64_t* n_pt_out = nullptr) {
   const int64_t V = c->V, F = c->F, E = c->E, nq = V + F + E;
   auto& g = c->grid;
+  const bool fused = c->bp_fused && MODE != BP_RAW && which == 3 && !n_pt_out && !(MODE == BP_CCD && O.verts);
   for (int attempt = 0; attempt < 3; ++attempt) {
     CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
     O.counter = c->counters.p;
+    if (fused) {
+      // results are final after one pass (CONTACT: the caller checks O.cap)
+      c->n_pairs_dev.ensure(1);
+      CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), c->stream));
+      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, c->n_pairs_dev.p};
+      fused_pairs<MODE>(c, x, B, A);
+      CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 c->stream));
+      sync_stream(c);
+      if (flag) *flag = c->h_cnt[1];
+      return MODE == BP_CONTACT ? c->h_cnt[0] : (int64_t)*c->h_npairs;
+    }
     collect_pairs(c, x, B, which);
     const int64_t cap = (int64_t)std::min(g.pa.n, g.pb.n);
     if (MODE != BP_RAW && !B.empty) {
       int sms = 148;
-      k_pairs<MODE><<<(unsigned)(8 * sms), 256, 0, c->stream>>>(g.qoff.p + V + F, g.qoff.p + nq, cap, g.pa, g.pb,
-                                                                  c->tri, c->tri_sorted, c->edge, x, O, CP, CC);
+      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr};
+      k_pairs<MODE><<<(unsigned)(8 * sms), 256, 0, c->stream>>>(g.qoff.p + V + F, g.qoff.p + nq, cap, g.pa, g.pb, A);
       LAUNCH_CHECK();
     }
     // one readback: the mode's counters and the pair-list sizes

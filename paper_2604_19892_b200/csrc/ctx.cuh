@@ -78,6 +78,7 @@ struct BpGridBufs {
   DBuf<int> qcnt, qoff;                                                  // per-query pair counts
   DBuf<int> pa, pb;                                                      // reference pair list
   DBuf<int> ecell, tri_ent, edge_ent, pt_ent;                            // (entries)
+  DBuf<double> tri_box, edge_box, pt_box;  // (entries*6) the entry's enumeration box, in cell order
 };
 
 struct CoarseLevel {
@@ -125,6 +126,7 @@ struct mp_ctx {
   bool apply_tma = true;     // level-0 apply staging: TMA bulk (true) or cp.async
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
+  bool bp_fused = true;      // pair work fused into the grid enumeration
   StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
@@ -222,6 +224,8 @@ struct mp_ctx {
   // pinned host staging for scalars
   double* h_scal = nullptr;
   int* h_cnt = nullptr;
+  unsigned long long* h_npairs = nullptr;  // = h_scal[63]
+  DBuf<unsigned long long> n_pairs_dev;    // fused enumeration pair count
 
   ~mp_ctx();
 };

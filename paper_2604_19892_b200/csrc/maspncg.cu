@@ -119,8 +119,12 @@ static void setup_levels(mp_ctx* c) {
     L->rsum.ensure(L->n);
     L->r.ensure(L->n);
     L->ypart.ensure((size_t)L->n);
-    CUDA_CHECK(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
-    CUDA_CHECK(cudaStreamCreateWithFlags(&L->st2, cudaStreamNonBlocking));
+    // the coarse chain is the build's critical path: its CTAs go ahead of
+    // the level-0 sweep's queued CTAs
+    int prio_lo = 0, prio_hi = 0;
+    CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CUDA_CHECK(cudaStreamCreateWithPriority(&L->st, cudaStreamNonBlocking, prio_hi));
+    CUDA_CHECK(cudaStreamCreateWithPriority(&L->st2, cudaStreamNonBlocking, prio_hi));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_w, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_u, cudaEventDisableTiming));
@@ -168,6 +172,7 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
   CUDA_CHECK(cudaMallocHost(&c->h_cnt, 16 * sizeof(int)));
+  c->h_npairs = reinterpret_cast<unsigned long long*>(c->h_scal + 63);
   c->N = s->n_verts;
   c->T = s->n_tets;
   c->F = s->n_tris;
@@ -575,6 +580,7 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_RECORD_ENERGY) c->record_energy = value != 0;
     else if (option == MP_OPT_APPLY_TMA) c->apply_tma = value != 0;
     else if (option == MP_OPT_APPLY_STAGES) c->apply_stages = value == 3 ? 3 : 2;
+    else if (option == MP_OPT_BP_FUSED) c->bp_fused = value != 0;
     else if (option == MP_OPT_APPLY_CTAS) c->apply_ctas_per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, value));
     else throw MpError(MP_ERR_CONFIG, "unknown option");
   });
