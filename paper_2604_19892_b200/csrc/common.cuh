@@ -310,3 +310,24 @@ __host__ __device__ __forceinline__ int64_t cyc_index(int m, int i, int j) {
   if (2 * s == m) base = (i < j) ? i : j;  // half diagonal: A(r, r+m/2), r < m/2
   return (int64_t)s * m + base;
 }
+
+// Fixed-order warp gather: the lanes stride over incidences [b, e) of an
+// index list and sum buf[3 idx + 0..2]; a shfl_down tree leaves the total in
+// lane 0.  The partition and the tree are fixed, so the bits are reproducible,
+// and a vertex with thousands of incidences is spread over 32 lanes.
+__device__ __forceinline__ void warp_gather3(int b, int e, const int* __restrict__ idx,
+                                             const double* __restrict__ buf, double& s0, double& s1, double& s2) {
+  const int lane = threadIdx.x & 31;
+  s0 = s1 = s2 = 0.0;
+  for (int k = b + lane; k < e; k += 32) {
+    const double* f = buf + 3 * (int64_t)idx[k];
+    s0 += f[0]; s1 += f[1]; s2 += f[2];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_down_sync(0xffffffffu, s0, o);
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+}
+

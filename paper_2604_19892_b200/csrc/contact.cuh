@@ -57,6 +57,87 @@ static void sort_table_into(mp_ctx* c, PairTable& src, PairTable& dst, int64_t n
   LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// vertex -> incidence CSR of a 4-vertex row table (deterministic scatter)
+
+__global__ void k_inc_keys(int64_t n, const int4* __restrict__ verts, int* __restrict__ cnt, int* __restrict__ key,
+                           int* __restrict__ val) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= 4 * n) return;
+  const int4 v = verts[e >> 2];
+  const int a = (int)(e & 3);
+  const int id = a == 0 ? v.x : (a == 1 ? v.y : (a == 2 ? v.z : v.w));
+  key[e] = id;
+  val[e] = (int)e;
+  atomicAdd(&cnt[id], 1);  // integer counts: order-free
+}
+
+// I.off = per-vertex offsets, I.val2 = incidences 4i+a grouped by vertex,
+// ascending within a vertex (stable radix sort of ascending input)
+static void build_inc(mp_ctx* c, IncCSR& I, const int4* verts, int64_t n) {
+  const int64_t N = c->N;
+  I.cnt.ensure(N + 1);
+  I.off.ensure(N + 1);
+  CUDA_CHECK(cudaMemsetAsync(I.cnt.p, 0, sizeof(int) * (N + 1), c->stream));
+  if (n > 0) {
+    const size_t m = 4 * (size_t)n;
+    I.key.ensure(m); I.key2.ensure(m); I.val.ensure(m); I.val2.ensure(m);
+    k_inc_keys<<<grid_for((int64_t)m, 256), 256, 0, c->stream>>>(n, verts, I.cnt, I.key, I.val);
+    LAUNCH_CHECK();
+    sort_pairs_i32(c, I.key, I.key2, I.val, I.val2, (int64_t)m, c->id_bits);
+  }
+  exclusive_scan(c, I.cnt, I.off, N + 1);
+}
+
+// per-row contact gradient terms kappa b'(d) grad (pinned rows are zero)
+__global__ void k_contact_grad_rows(int64_t n, const double* __restrict__ d, const double* __restrict__ grad,
+                                    double dh, double kappa, double* __restrict__ cbuf) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double db;
+  barrier3(d[i], dh, kappa, nullptr, &db, nullptr);
+#pragma unroll
+  for (int q = 0; q < 12; ++q) cbuf[12 * i + q] = db * grad[12 * i + q];
+}
+
+// per-row rank-one terms s_i w_i (w_i . vec); s == nullptr -> 1
+__global__ void k_rank1_rows(int64_t n, const int4* __restrict__ verts, const double* __restrict__ w,
+                             const double* __restrict__ s, const double* __restrict__ vec, double* __restrict__ rbuf) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 v = verts[i];
+  const int id[4] = {v.x, v.y, v.z, v.w};
+  double dot = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dot += w[12 * i + 3 * a + k] * vec[3 * id[a] + k];
+  if (s) dot *= s[i];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) rbuf[12 * i + q] = w[12 * i + q] * dot;
+}
+
+// out[v] += (sum over A's incidences) + (sum over B's): one warp per vertex,
+// fixed-order gathers; pinned vertices' rows are zero in every table
+__global__ void k_inc_gather_add(int64_t N, const unsigned char* __restrict__ pinned,
+                                 const int* __restrict__ a_off, const int* __restrict__ a_val,
+                                 const double* __restrict__ a_buf, const int* __restrict__ b_off,
+                                 const int* __restrict__ b_val, const double* __restrict__ b_buf,
+                                 double* __restrict__ out) {
+  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= N || pinned[v]) return;  // warp-uniform
+  const bool ha = a_off && a_off[v + 1] > a_off[v], hb = b_off && b_off[v + 1] > b_off[v];
+  if (!ha && !hb) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+  if (ha) warp_gather3(a_off[v], a_off[v + 1], a_val, a_buf, a0, a1, a2);
+  if (hb) warp_gather3(b_off[v], b_off[v + 1], b_val, b_buf, b0, b1, b2);
+  if (lane) return;
+  out[3 * v] = (out[3 * v] + a0) + b0;
+  out[3 * v + 1] = (out[3 * v + 1] + a1) + b1;
+  out[3 * v + 2] = (out[3 * v + 2] + a2) + b2;
+}
+
 static BpOut table_out(PairTable& t) {
   BpOut O{};
   O.khi = t.khi; O.klo = t.klo; O.verts = t.verts; O.d = t.d; O.k = t.k; O.nrm = t.nrm; O.grad = t.grad;
@@ -80,6 +161,7 @@ static void constraint_set(mp_ctx* c, const double* x) {
     if (pen) throw MpError(MP_ERR_PENETRATION, "contact distance <= 0");
     if (n <= O.cap) {
       sort_table_into(c, c->scratch, c->cur, n);
+      build_inc(c, c->inc_cur, c->cur.verts, n);
       return;
     }
     c->scratch.ensure((size_t)(n * 1.5) + 1024);
@@ -90,23 +172,6 @@ static void constraint_set(mp_ctx* c, const double* x) {
 // ---------------------------------------------------------------------------
 // contact terms of gradient / energy / HVP
 
-__global__ void k_contact_grad(int64_t n, const int4* __restrict__ verts, const double* __restrict__ d,
-                               const double* __restrict__ grad, const unsigned char* __restrict__ pinned,
-                               double dh, double kappa, double* __restrict__ g) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double db;
-  barrier3(d[i], dh, kappa, nullptr, &db, nullptr);
-  int4 v = verts[i];
-  const int id[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    if (pinned[id[a]]) continue;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) atomicAdd(&g[3 * id[a] + k], db * grad[12 * i + 3 * a + k]);
-  }
-}
-
 __global__ void k_contact_energy(int64_t n, const double* __restrict__ d, double dh, double kappa, double* part) {
   double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -115,29 +180,6 @@ __global__ void k_contact_energy(int64_t n, const double* __restrict__ d, double
     acc += b;
   }
   block_sum_store<256>(acc, part);
-}
-
-// out += sum_i s_i w_i (w_i . vec) over rank-one terms; s == nullptr -> 1
-__global__ void k_rank1_apply(int64_t n, const int4* __restrict__ verts, const double* __restrict__ w,
-                              const double* __restrict__ s, const double* __restrict__ vec, double* __restrict__ out) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int4 v = verts[i];
-  const int id[4] = {v.x, v.y, v.z, v.w};
-  double dot = 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) dot += w[12 * i + 3 * a + k] * vec[3 * id[a] + k];
-  if (s) dot *= s[i];
-  if (dot == 0.0) return;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      double val = w[12 * i + 3 * a + k];
-      if (val != 0.0) atomicAdd(&out[3 * id[a] + k], val * dot);
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -233,6 +275,7 @@ static void classify_all(mp_ctx* c, double eps_rot) {
                                                            c->cur.verts, c->cur.grad, c->cand_verts, c->cand_u,
                                                            c->cand_ds);
   LAUNCH_CHECK();
+  build_inc(c, c->inc_cand, c->cand_verts, tot);
 }
 
 // ---------------------------------------------------------------------------

@@ -70,6 +70,11 @@ struct PairTable {
   }
 };
 
+struct IncCSR {
+  DBuf<int> cnt, off;        // (N+1)
+  DBuf<int> key, key2, val, val2;  // (4 rows): vertex keys, incidences (val2 sorted)
+};
+
 // per-level cell tables of the broad phase (bp.cuh build_bp)
 struct BpGridBufs {
   DBuf<int> tri_cnt, tri_start, edge_cnt, edge_start, pt_cnt, pt_start;  // (ncell+1)
@@ -89,17 +94,22 @@ struct CoarseLevel {
   DBuf<double> inv;   // cyc_size(n) packed inverse
   DBuf<double> rsum;  // 3A restricted raw sums
   DBuf<double> r;     // 3A restriction C_l g (averages)
-  DBuf<double> ypart; // n: M_l^-1 r accumulated over diagonal chunks
+  DBuf<double> ypart; // n: M_l^-1 r (sum of the diagonal chunks' partials, fixed order)
+  DBuf<double> ypc;   // chunks*n partials
+  DBuf<int> mv_cnt;   // per row block: chunks done (the last one reduces)
+  DBuf<unsigned long long> fx_acc;  // n*n*2: contact terms, 128-bit fixed point
+  DBuf<int> cb_key, cb_off, cb_slot;  // BSR -> M_l gather map: nonzero blocks A*nA+B, their slots
+  int nblk = 0;
   DBuf<double> dn_col, dn_W, dn_P, dn_Pn;  // blocked-sweep scratch
   int chunks = 1;
   // each coarse level is built on its own stream (st2: lookahead updates),
   // concurrently with level 0
   cudaStream_t st = nullptr, st2 = nullptr;
-  cudaEvent_t done = nullptr, ev_w = nullptr, ev_u = nullptr;
+  cudaEvent_t done = nullptr, ev_w = nullptr, ev_u = nullptr, ev_asm = nullptr;
   cublasHandle_t blas = nullptr;
   ~CoarseLevel() {
     if (blas) cublasDestroy(blas);
-    for (cudaEvent_t e : {done, ev_w, ev_u})
+    for (cudaEvent_t e : {done, ev_w, ev_u, ev_asm})
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
     if (st2) cudaStreamDestroy(st2);
@@ -160,6 +170,12 @@ struct mp_ctx {
   int64_t nnzb = 0;
   DBuf<int> rowptr, cols, tet_slot, diag_slot;
   DBuf<double> bsr;         // nnzb*9 values
+  std::vector<int> h_rowptr, h_cols;  // host copy of the pattern (coarse gather maps)
+  // deterministic assembly (fixed-order gathers instead of atomics)
+  DBuf<int> hs_off, hs_val, slot_row;  // BSR slot -> element blocks 16t+4a+b; slot -> row
+  DBuf<int> vt_off, vt_val;            // vertex -> tet corners 4t+a
+  DBuf<double> fbuf;                   // (T_el,4,3) per-corner elastic forces
+  DBuf<double> hbuf;                   // (T_el,10,9) element blocks a <= b
   // surface
   DBuf<int> tri;            // (F*3) new ids, surface order
   DBuf<int> tri_sorted;     // (F*3) new ids ordered by ascending original id
@@ -171,6 +187,11 @@ struct mp_ctx {
 
   // ---- contact sets ----
   PairTable cur, base, scratch;
+  // vertex -> incidences (4 row + corner, ascending) of cur / base / the
+  // update candidates: fixed-order per-vertex gathers instead of atomics
+  IncCSR inc_cur, inc_base, inc_cand;
+  DBuf<double> cbuf, rbuf_base, rbuf_cand;  // (rows, 12) per-row terms
+  DBuf<double> fx_scale;                   // coarse contact fixed-point unit
   DBuf<int> sort_idx, sort_idx2;
   DBuf<unsigned long long> sort_k1, sort_k2;
   DBuf<unsigned char> cub_tmp;

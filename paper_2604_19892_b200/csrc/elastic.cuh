@@ -103,8 +103,7 @@ __global__ void k_inertia_grad(int64_t N, const double* __restrict__ x, const do
 template <int KIND>
 __global__ void __launch_bounds__(128) k_tet_grad(int64_t t0, int64_t nt, const int4* __restrict__ tets,
                                                   const TetParam* __restrict__ tetp,
-                                                  const unsigned char* __restrict__ pinned,
-                                                  const double* __restrict__ x, double h2, double* __restrict__ g) {
+                                                  const double* __restrict__ x, double h2, double* __restrict__ fbuf) {
   const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= t0 + nt) return;
   const int4 tv = tets[t];
@@ -114,15 +113,40 @@ __global__ void __launch_bounds__(128) k_tet_grad(int64_t t0, int64_t nt, const 
   M3 F;
   tet_F(X, tp, F, bc);
   const M3 P = piola(F, KIND, tp.mu, tp.lam);
-  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
   const double s = h2 * tp.vol;
+  // per-corner forces; k_grad_gather sums them per vertex in a fixed order
+  double* f = fbuf + 12 * t;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    if (pinned[id[a]]) continue;
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-      atomicAdd(&g[3 * id[a] + i], s * (P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2]));
+      f[3 * a + i] = s * (P(i, 0) * bc[a][0] + P(i, 1) * bc[a][1] + P(i, 2) * bc[a][2]);
+}
+
+// g = M (x - x~) + the vertex's tet-corner forces + its contact terms
+// (fixed-order warp gathers, one warp per vertex); pinned entries 0
+// (energy.py:357-370)
+__global__ void k_grad_gather(int64_t N, const double* __restrict__ x, const double* __restrict__ xt,
+                              const double* __restrict__ mass, const unsigned char* __restrict__ pinned,
+                              const int* __restrict__ vt_off, const int* __restrict__ vt_val,
+                              const double* __restrict__ fbuf, const int* __restrict__ c_off,
+                              const int* __restrict__ c_val, const double* __restrict__ cbuf,
+                              double* __restrict__ g) {
+  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= N) return;  // warp-uniform
+  if (pinned[v]) {
+    if (lane < 3) g[3 * v + lane] = 0.0;
+    return;
   }
+  double e0, e1, e2, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  warp_gather3(vt_off[v], vt_off[v + 1], vt_val, fbuf, e0, e1, e2);
+  if (c_off) warp_gather3(c_off[v], c_off[v + 1], c_val, cbuf, c0, c1, c2);
+  if (lane) return;
+  const double mv = mass[v];
+  g[3 * v] = mv * (x[3 * v] - xt[3 * v]) + e0 + c0;
+  g[3 * v + 1] = mv * (x[3 * v + 1] - xt[3 * v + 1]) + e1 + c1;
+  g[3 * v + 2] = mv * (x[3 * v + 2] - xt[3 * v + 2]) + e2 + c2;
 }
 
 // energy pieces: 0.5 (x-x~)^T M (x-x~)  and  sum vol*psi  (energy.py:346-354)
@@ -254,11 +278,13 @@ __device__ __forceinline__ void tet_block(const TetModes& md, int a, int b, doub
     for (int c = 0; c < 3; ++c) blk[r][c] = UK[r][0] * md.U[c][0] + UK[r][1] * md.U[c][1] + UK[r][2] * md.U[c][2];
 }
 
+// index of the element block (a, b), a <= b, among the 10 stored per tet
+__device__ __forceinline__ int pair_index(int a, int b) { return a * (7 - a) / 2 + b; }
+
 template <int KIND>
 __global__ void k_tet_hessian(int64_t t0, int64_t nt, const int4* __restrict__ tets,
                               const TetParam* __restrict__ tetp, const unsigned char* __restrict__ pinned,
-                              const int* __restrict__ tet_slot, const double* __restrict__ x, double h2,
-                              double* __restrict__ bsr) {
+                              const double* __restrict__ x, double h2, double* __restrict__ hbuf) {
   const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= t0 + nt) return;
   const int kd = KIND;
@@ -275,6 +301,8 @@ __global__ void k_tet_hessian(int64_t t0, int64_t nt, const int4* __restrict__ t
 #pragma unroll
   for (int a = 0; a < 4; ++a) pin[a] = pinned[id[a]] != 0;
   const double s = h2 * tp.vol;
+  // element blocks a <= b into hbuf; k_hess_gather sums them per BSR slot
+  double* hb = hbuf + 90 * t;
   for (int a = 0; a < 4; ++a) {
     if (pin[a]) continue;
     for (int b = a; b < 4; ++b) {
@@ -282,32 +310,49 @@ __global__ void k_tet_hessian(int64_t t0, int64_t nt, const int4* __restrict__ t
       double blk[3][3];
       tet_block(md, a, b, blk);
       double mI = tp.mu * (bc[a][0] * bc[b][0] + bc[a][1] * bc[b][1] + bc[a][2] * bc[b][2]);
-      double* dst = bsr + 9 * (int64_t)tet_slot[16 * t + 4 * a + b];
+      double* dst = hb + 9 * pair_index(a, b);
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) atomicAdd(dst + 3 * r + c, s * (blk[r][c] + (r == c ? mI : 0.0)));
-      if (b != a) {
-        double* dsT = bsr + 9 * (int64_t)tet_slot[16 * t + 4 * b + a];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) atomicAdd(dsT + 3 * c + r, s * (blk[r][c] + (r == c ? mI : 0.0)));
-      }
+        for (int c = 0; c < 3; ++c) dst[3 * r + c] = s * (blk[r][c] + (r == c ? mI : 0.0));
     }
   }
 }
 
-// diagonal blocks: mass (free) or identity (pinned) (energy.py:411-412)
-__global__ void k_bsr_diag(int64_t N, const int* __restrict__ diag_slot, const double* __restrict__ mass,
-                           const unsigned char* __restrict__ pinned, double* __restrict__ bsr) {
-  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= N) return;
-  double dv = pinned[v] ? 1.0 : mass[v];
-  double* b = bsr + 9 * (int64_t)diag_slot[v];
-  b[0] += dv;
-  b[4] += dv;
-  b[8] += dv;
+// one thread per BSR slot: (mass | pinned identity on the diagonal) + its
+// element blocks in ascending (tet, a, b) order (energy.py:373-413)
+__global__ void k_hess_gather(int64_t nnzb, const int* __restrict__ slot_row, const int* __restrict__ cols,
+                              const int* __restrict__ hs_off, const int* __restrict__ hs_val,
+                              const double* __restrict__ hbuf, const double* __restrict__ mass,
+                              const unsigned char* __restrict__ pinned, double* __restrict__ bsr) {
+  int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (sl >= nnzb) return;
+  double acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+  const int v = slot_row[sl];
+  if (cols[sl] == v) {
+    const double dv = pinned[v] ? 1.0 : mass[v];
+    acc[0] = dv; acc[4] = dv; acc[8] = dv;
+  }
+  for (int k = hs_off[sl]; k < hs_off[sl + 1]; ++k) {
+    const int e = hs_val[k];
+    const int t = e >> 4, a = (e >> 2) & 3, b = e & 3;
+    if (a <= b) {
+      const double* blk = hbuf + 90 * (int64_t)t + 9 * pair_index(a, b);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += blk[q];
+    } else {
+      const double* blk = hbuf + 90 * (int64_t)t + 9 * pair_index(b, a);
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[3 * r + c] += blk[3 * c + r];
+    }
+  }
+  double* out = bsr + 9 * sl;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) out[q] = acc[q];
 }
 
 // y = BSR x ; 8 lanes per block row, lanes stride over the row's blocks
@@ -344,39 +389,43 @@ __global__ void k_bsr_spmv(int64_t N, const int* __restrict__ rowptr, const int*
 // ---------------------------------------------------------------------------
 // host launchers
 
-static void elastic_gradient(mp_ctx* c, const double* x, const double* xt, double h, double* g) {
-  k_inertia_grad<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, x, xt, c->mass, c->pinned, g);
-  LAUNCH_CHECK();
+// energy.gradient's elastic + inertia part (energy.py:357-370), with the
+// contact rows' terms when c_off is given (contact.cuh): per-corner / per-row
+// forces, then one fixed-order gather per vertex -- bitwise reproducible
+static void gradient_gather(mp_ctx* c, const double* x, const double* xt, double h, double* g, const int* c_off,
+                            const int* c_val, const double* cbuf) {
   if (c->T_snh) {
     timer_begin(c, MP_STAGE_TET_GRAD);
-    k_tet_grad<2><<<grid_for(c->T_snh, 128), 128, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned, x,
-                                                                  h * h, g);
+    k_tet_grad<2><<<grid_for(c->T_snh, 128), 128, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, x, h * h, c->fbuf);
     LAUNCH_CHECK();
-    // algorithmic bytes: 113 B of tet data per tet, x read and g
-    // read-modify-written once per vertex (72 B)
-    timer_end(c, MP_STAGE_TET_GRAD, 113.0 * c->T_snh + 72.0 * c->N);
+    // algorithmic bytes: 113 B of tet data per tet, x read and g written
+    // once per vertex (48 B)
+    timer_end(c, MP_STAGE_TET_GRAD, 113.0 * c->T_snh + 48.0 * c->N);
   }
   if (c->T_arap) {
-    k_tet_grad<1><<<grid_for(c->T_arap, 128), 128, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp,
-                                                                   c->pinned, x, h * h, g);
+    k_tet_grad<1><<<grid_for(c->T_arap, 128), 128, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp, x, h * h,
+                                                                   c->fbuf);
     LAUNCH_CHECK();
   }
+  k_grad_gather<<<grid_for(32 * c->N, 128), 128, 0, c->stream>>>(c->N, x, xt, c->mass, c->pinned, c->vt_off, c->vt_val,
+                                                            c->fbuf, c_off, c_val, cbuf, g);
+  LAUNCH_CHECK();
 }
 
 static void assemble_elastic_bsr(mp_ctx* c, const double* x, double h) {
-  CUDA_CHECK(cudaMemsetAsync(c->bsr.p, 0, sizeof(double) * 9 * c->nnzb, c->stream));
-  k_bsr_diag<<<grid_for(c->N, 256), 256, 0, c->stream>>>(c->N, c->diag_slot, c->mass, c->pinned, c->bsr);
-  LAUNCH_CHECK();
   if (c->T_snh) {
-    k_tet_hessian<2><<<grid_for(c->T_snh, 64), 64, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned,
-                                                                   c->tet_slot, x, h * h, c->bsr);
+    k_tet_hessian<2><<<grid_for(c->T_snh, 64), 64, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned, x,
+                                                                   h * h, c->hbuf);
     LAUNCH_CHECK();
   }
   if (c->T_arap) {
     k_tet_hessian<1><<<grid_for(c->T_arap, 64), 64, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp,
-                                                                    c->pinned, c->tet_slot, x, h * h, c->bsr);
+                                                                    c->pinned, x, h * h, c->hbuf);
     LAUNCH_CHECK();
   }
+  k_hess_gather<<<grid_for(c->nnzb, 128), 128, 0, c->stream>>>(c->nnzb, c->slot_row, c->cols, c->hs_off, c->hs_val,
+                                                               c->hbuf, c->mass, c->pinned, c->bsr);
+  LAUNCH_CHECK();
 }
 
 static void bsr_spmv(mp_ctx* c, const double* xin, double* y) {

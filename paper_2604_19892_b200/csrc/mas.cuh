@@ -25,46 +25,54 @@
 // ---------------------------------------------------------------------------
 // level-0 assembly
 
-// contacts -> Mfull (same-subdomain vertex pairs) and coarse dense levels
-__global__ void k_contact_blocks(int64_t n, const int4* __restrict__ verts, const double* __restrict__ grad,
-                                 const double* __restrict__ k, int bs, int m, double* __restrict__ Mfull) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int4 v = verts[i];
-  const int id[4] = {v.x, v.y, v.z, v.w};
-  const double kk = k[i];
-  const double* gr = grad + 12 * i;
-  for (int a = 0; a < 4; ++a) {
-    int da = id[a] / bs;
+// contacts -> Mfull (same-subdomain vertex pairs): one thread per vertex a
+// owns rows 3a..3a+2 of its subdomain block and adds its incidences' terms
+// in ascending (contact, partner) order -- no atomics, reproducible
+__global__ void k_contact_blocks(int64_t N, const unsigned char* __restrict__ pinned, const int* __restrict__ off,
+                                 const int* __restrict__ inc, const int4* __restrict__ verts,
+                                 const double* __restrict__ grad, const double* __restrict__ k, int bs, int m,
+                                 double* __restrict__ Mfull) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= N || pinned[v]) return;  // pinned rows of grad are zero
+  const int d = (int)(v / bs), la = (int)(v - (int64_t)d * bs);
+  double* blk = Mfull + (int64_t)d * m * m;
+  for (int q = off[v]; q < off[v + 1]; ++q) {
+    const int e = inc[q];
+    const int64_t i = e >> 2;
+    const int a = e & 3;
+    const int4 vv = verts[i];
+    const int id[4] = {vv.x, vv.y, vv.z, vv.w};
+    const double kk = k[i];
+    const double* ga = grad + 12 * i + 3 * a;
     for (int b = 0; b < 4; ++b) {
-      if (id[b] / bs != da) continue;
-      int la = id[a] - da * bs, lb = id[b] - da * bs;
-      double* blk = Mfull + (int64_t)da * m * m;
+      if (id[b] / bs != d) continue;
+      const int lb = id[b] - d * bs;
+      const double* gb = grad + 12 * i + 3 * b;
       for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) {
-          double val = kk * gr[3 * a + r] * gr[3 * b + c];
-          if (val != 0.0) atomicAdd(&blk[(3 * la + r) * m + 3 * lb + c], val);
+        for (int cc = 0; cc < 3; ++cc) {
+          double val = kk * ga[r] * gb[cc];
+          if (val != 0.0) blk[(3 * la + r) * m + 3 * lb + cc] += val;
         }
     }
   }
 }
 
-// BSR blocks whose row and column share a subdomain -> Mfull (unique targets)
-__global__ void k_bsr_to_blocks(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
+// BSR blocks whose row and column share a subdomain -> Mfull: one thread per
+// slot, unique targets (added after the contact terms, same stream)
+__global__ void k_bsr_to_blocks(int64_t nnzb, const int* __restrict__ slot_row, const int* __restrict__ cols,
                                 const double* __restrict__ vals, int bs, int m, double* __restrict__ Mfull) {
-  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (row >= N) return;
-  int d = (int)(row / bs);
-  int lr = (int)(row - (int64_t)d * bs);
-  double* blk = Mfull + (int64_t)d * m * m;
-  for (int k = rowptr[row]; k < rowptr[row + 1]; ++k) {
-    int w = cols[k];
-    if (w / bs != d) continue;
-    int lc = w - d * bs;
-    const double* b = vals + 9 * (int64_t)k;
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) blk[(3 * lr + r) * m + 3 * lc + c] += b[3 * r + c];
-  }
+  int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (sl >= nnzb) return;
+  const int v = slot_row[sl], w = cols[sl];
+  const int d = v / bs;
+  if (w / bs != d) return;
+  const int lr = v - d * bs, lc = w - d * bs;
+  double* blk = Mfull + (int64_t)d * m * m + (3 * lr) * m + 3 * lc;
+  const double* b = vals + 9 * sl;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) blk[r * m + c] += b[3 * r + c];
 }
 
 // write a symmetric m x m smem matrix (0.5 (X + X^T)) in cyclic-diagonal packing
@@ -483,56 +491,165 @@ __global__ void k_block_fix(int n, int kb, int k0, const double* __restrict__ W,
 // ---------------------------------------------------------------------------
 // coarse levels
 
-// every BSR block (v, w) -> M_l[agg(v), agg(w)] / (|a||b|)
-__global__ void k_bsr_to_coarse(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
-                                const double* __restrict__ vals, int span, int n, double* __restrict__ M) {
-  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (row >= N) return;
-  int a = (int)(row / span);
-  int64_t na = (N - (int64_t)a * span) < span ? (N - (int64_t)a * span) : span;
-  for (int k = rowptr[row]; k < rowptr[row + 1]; ++k) {
-    int w = cols[k];
-    int b = w / span;
-    int64_t nb = (N - (int64_t)b * span) < span ? (N - (int64_t)b * span) : span;
-    double sc = 1.0 / ((double)na * (double)nb);
-    const double* bl = vals + 9 * (int64_t)k;
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) atomicAdd(&M[(int64_t)(3 * a + r) * n + 3 * b + c], bl[3 * r + c] * sc);
+// M_l from the BSR by a static gather map: one warp per nonzero coarse block
+// (A, B) sums its BSR slots in ascending order (lanes strided, fixed shuffle
+// tree), then scales by 1/(|a||b|) -- no atomics, reproducible
+__global__ void k_coarse_gather(int nblk, const int* __restrict__ cb_key, const int* __restrict__ cb_off,
+                                const int* __restrict__ cb_slot, const double* __restrict__ bsr, int nA, int64_t N,
+                                int span, int n, double* __restrict__ M) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= nblk) return;
+  double acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+  for (int k = cb_off[w] + lane; k < cb_off[w + 1]; k += 32) {
+    const double* b = bsr + 9 * (int64_t)cb_slot[k];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += b[q];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += __shfl_down_sync(0xffffffffu, acc[q], o);
+  if (lane) return;
+  const int key = cb_key[w];
+  const int A = key / nA, B = key - (key / nA) * nA;
+  const int64_t na = (N - (int64_t)A * span) < span ? (N - (int64_t)A * span) : span;
+  const int64_t nb = (N - (int64_t)B * span) < span ? (N - (int64_t)B * span) : span;
+  const double sc = 1.0 / ((double)na * (double)nb);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) M[(int64_t)(3 * A + r) * n + 3 * B + c] = acc[3 * r + c] * sc;
+}
+
+// M_{l+1} from the finer level's dense M_l (contacts included): every coarse
+// 3x3 block sums the cb x cb fine blocks it covers, weighted |a_f||b_f| /
+// (|A||B|) -- the same Galerkin sum as from the BSR, from n_l^2 instead of
+// nnzb reads.  One thread per coarse entry, fine blocks in ascending order.
+__global__ void k_coarse_up(int nA, int cb, int nAf, const double* __restrict__ Mf, int nf, int64_t N, int span,
+                            int span_f, double* __restrict__ M) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int n = 3 * nA;
+  if (e >= (int64_t)n * n) return;
+  const int i = (int)(e / n), j = (int)(e - (int64_t)(e / n) * n);
+  const int A = i / 3, r = i - 3 * (i / 3), B = j / 3, c = j - 3 * (j / 3);
+  auto size = [&](int a, int sp) {
+    const int64_t s = N - (int64_t)a * sp;
+    return (double)(s < sp ? s : sp);
+  };
+  double acc = 0.0;
+  for (int af = A * cb; af < (A + 1) * cb && af < nAf; ++af) {
+    const double wa = size(af, span_f);
+    for (int bf = B * cb; bf < (B + 1) * cb && bf < nAf; ++bf)
+      acc += Mf[(int64_t)(3 * af + r) * nf + 3 * bf + c] * (wa * size(bf, span_f));
+  }
+  M[e] = acc / (size(A, span) * size(B, span));
+}
+
+// 128-bit fixed-point accumulation: integer addition is associative, so the
+// contact terms of the coarse levels sum to the same bits in any order.
+// y is in units of the call's fixed-point unit (|partial sums| < 2^120).
+__device__ __forceinline__ void fx_add(unsigned long long* p, double y) {
+  const double yi = rint(y);
+  if (yi == 0.0) return;
+  __int128 v;
+  const int e = ilogb(yi);
+  if (e < 62) {
+    v = (__int128)(long long)yi;
+  } else {
+    const long long m = (long long)scalbn(yi, 52 - e);  // exact 53-bit signed mantissa
+    v = (__int128)m * ((__int128)1 << (e - 52));
+  }
+  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  const unsigned long long old = atomicAdd(p, lo);
+  atomicAdd(p + 1, hi + (old + lo < old ? 1ull : 0ull));
+}
+
+__device__ __forceinline__ double fx_get(const unsigned long long* p) {
+  return (double)(long long)p[1] * 18446744073709551616.0 + (double)p[0];
+}
+
+// fixed-point unit from T = sum_i k_i |grad_i|^2 >= |any coarse contact entry|:
+// out[0] = 1 / unit, out[1] = unit = 2^(ilogb(T) + 1 - 120).  One block, fixed order.
+__global__ void k_fx_scale(int64_t nc, const double* __restrict__ k, const double* __restrict__ nrm,
+                           double* __restrict__ out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < nc; i += 256) s += fabs(k[i]) * nrm[i] * nrm[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double T = sh[0];
+    const int e = (T > 0.0 && isfinite(T)) ? ilogb(T) + 1 - 120 : 0;
+    out[0] = ldexp(1.0, -e);
+    out[1] = ldexp(1.0, e);
   }
 }
 
+// contacts -> the coarse level's 128-bit accumulators: k w_A w_B^T over the
+// contact's distinct aggregates, w_A = sum_{a in A} grad_a / |A| (the same
+// sum as k grad_a grad_b^T / (|A||B|) over vertex pairs)
 __global__ void k_contact_coarse(int64_t nc, const int4* __restrict__ verts, const double* __restrict__ grad,
-                                 const double* __restrict__ k, int64_t N, int span, int n, double* __restrict__ M) {
+                                 const double* __restrict__ k, int64_t N, int span, int n,
+                                 const double* __restrict__ fx, unsigned long long* __restrict__ acc) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nc) return;
   int4 v = verts[i];
   const int id[4] = {v.x, v.y, v.z, v.w};
   const double* gr = grad + 12 * i;
+  int agg[4];
+  double w[4][3];
+  int na = 0;
   for (int a = 0; a < 4; ++a) {
-    int A = id[a] / span;
-    int64_t na = (N - (int64_t)A * span) < span ? (N - (int64_t)A * span) : span;
-    for (int b = 0; b < 4; ++b) {
-      int B = id[b] / span;
-      int64_t nb = (N - (int64_t)B * span) < span ? (N - (int64_t)B * span) : span;
-      double sc = k[i] / ((double)na * (double)nb);
+    const int A = id[a] / span;
+    int q = 0;
+    while (q < na && agg[q] != A) ++q;
+    if (q == na) {
+      agg[na] = A;
+      w[na][0] = w[na][1] = w[na][2] = 0.0;
+      ++na;
+    }
+    w[q][0] += gr[3 * a]; w[q][1] += gr[3 * a + 1]; w[q][2] += gr[3 * a + 2];
+  }
+  for (int q = 0; q < na; ++q) {
+    const int64_t sz = (N - (int64_t)agg[q] * span) < span ? (N - (int64_t)agg[q] * span) : span;
+    const double inv = 1.0 / (double)sz;
+    w[q][0] *= inv; w[q][1] *= inv; w[q][2] *= inv;
+  }
+  const double s = k[i] * fx[0];
+  for (int qa = 0; qa < na; ++qa)
+    for (int qb = 0; qb < na; ++qb)
       for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c) {
-          double val = sc * gr[3 * a + r] * gr[3 * b + c];
-          if (val != 0.0) atomicAdd(&M[(int64_t)(3 * A + r) * n + 3 * B + c], val);
+          const double val = s * w[qa][r] * w[qb][c];
+          if (val != 0.0) fx_add(acc + 2 * ((int64_t)(3 * agg[qa] + r) * n + 3 * agg[qb] + c), val);
         }
-    }
-  }
 }
 
 // 0.5 (M + M^T) on the lower triangle (the only half potrf reads)
-__global__ void k_sym_lower(int n, double* M) {
+// (plus the contact accumulators when acc != nullptr)
+__global__ void k_sym_lower(int n, double* M, const unsigned long long* __restrict__ acc,
+                            const double* __restrict__ fx) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * n) return;
   int i = (int)(e / n), j = (int)(e % n);
-  if (j >= i) return;
-  // column-major view for cuSOLVER: element (r, c) at r + c*n; our row-major
-  // M[i*n+j] is (j, i) column-major -- symmetric anyway, average both halves
-  double a = M[(int64_t)i * n + j], b = M[(int64_t)j * n + i];
+  if (j > i) return;
+  const int64_t ij = (int64_t)i * n + j, ji = (int64_t)j * n + i;
+  double a = M[ij], b = M[ji];
+  if (acc) {
+    a += fx_get(acc + 2 * ij) * fx[1];
+    b += fx_get(acc + 2 * ji) * fx[1];
+  }
+  if (j == i) {
+    M[ij] = a;
+    return;
+  }
   double s = 0.5 * (a + b);
   M[(int64_t)i * n + j] = s;
   M[(int64_t)j * n + i] = s;
@@ -610,36 +727,49 @@ __global__ void k_restrict_up(int A, int cb, int Afine, int64_t N, int span, con
   r[e] = s * (1.0 / (double)na);
 }
 
-// y += Minv r over a chunk of diagonals (atomic accumulation; y zeroed by the
-// caller); r = rsum / |a|.  Many small chunks keep every SM busy.
+// y = Minv r: each (row block, diagonal chunk) CTA writes its partial; the
+// row block's last CTA to finish sums the chunks in order (reproducible).
+// Many small chunks keep every SM busy.
 __global__ void k_coarse_mv(int n, int chunks, const double* __restrict__ P, const double* __restrict__ r,
-                            double* __restrict__ y) {
+                            double* __restrict__ ypc, double* __restrict__ y, int* __restrict__ done) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y;
-  if (i >= n) return;
   const int smax = n / 2;  // diagonals 0..smax
   int per = (smax + 1 + chunks - 1) / chunks;
   int s0 = ch * per, s1 = s0 + per - 1;
   if (s1 > smax) s1 = smax;
-  if (s0 > s1) return;
   double acc = 0.0;
   const bool even = (n % 2) == 0;
-  for (int s = s0; s <= s1; ++s) {
-    if (s == 0) {
-      acc += P[i] * r[i];
-      continue;
+  if (i < n) {
+    for (int s = s0; s <= s1; ++s) {
+      if (s == 0) {
+        acc += P[i] * r[i];
+        continue;
+      }
+      const double* dg = P + (int64_t)s * n;
+      int jp = i + s; if (jp >= n) jp -= n;
+      int jm = i - s; if (jm < 0) jm += n;
+      if (even && 2 * s == n) {
+        // half diagonal: A(i, i+n/2) stored at min(i, i+n/2)
+        acc += dg[i < jp ? i : jp] * r[jp];
+      } else {
+        acc += __ldg(dg + i) * r[jp] + __ldg(dg + jm) * r[jm];
+      }
     }
-    const double* dg = P + (int64_t)s * n;
-    int jp = i + s; if (jp >= n) jp -= n;
-    int jm = i - s; if (jm < 0) jm += n;
-    if (even && 2 * s == n) {
-      // half diagonal: A(i, i+n/2) stored at min(i, i+n/2)
-      acc += dg[i < jp ? i : jp] * r[jp];
-    } else {
-      acc += __ldg(dg + i) * r[jp] + __ldg(dg + jm) * r[jm];
-    }
+    ypc[(int64_t)ch * n + i] = acc;
   }
-  atomicAdd(&y[i], acc);
+  __threadfence();
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done + blockIdx.x, 1) == chunks - 1;
+  __syncthreads();
+  if (!last) return;
+  if (i < n) {
+    double s = 0.0;
+    for (int q = 0; q < chunks; ++q) s += __ldcg(ypc + (int64_t)q * n + i);
+    y[i] = s;
+  }
+  if (threadIdx.x == 0) done[blockIdx.x] = 0;  // ready for the next apply
 }
 
 struct LevelView {

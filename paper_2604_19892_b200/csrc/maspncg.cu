@@ -119,6 +119,37 @@ static void setup_levels(mp_ctx* c) {
     L->rsum.ensure(L->n);
     L->r.ensure(L->n);
     L->ypart.ensure((size_t)L->n);
+    L->ypc.ensure((size_t)ch * L->n);
+    L->mv_cnt.zero((size_t)rowblocks, c->stream);
+    // BSR -> M_l gather map (first coarse level only; the next levels sum
+    // the previous level's blocks): slots grouped by coarse block (A, B)
+    if (c->levels.empty()) {
+      const int64_t N = c->N;
+      const int nA = L->A;
+      std::vector<std::pair<int64_t, int>> ks;
+      ks.reserve(c->h_cols.size());
+      for (int64_t v = 0; v < N; ++v)
+        for (int k = c->h_rowptr[v]; k < c->h_rowptr[v + 1]; ++k)
+          ks.emplace_back((v / span) * nA + c->h_cols[k] / span, k);
+      std::stable_sort(ks.begin(), ks.end(),
+                       [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& b) { return a.first < b.first; });
+      std::vector<int> key, off, slot(ks.size());
+      for (size_t q = 0; q < ks.size(); ++q) {
+        if (q == 0 || ks[q].first != ks[q - 1].first) {
+          key.push_back((int)ks[q].first);
+          off.push_back((int)q);
+        }
+        slot[q] = ks[q].second;
+      }
+      off.push_back((int)ks.size());
+      L->nblk = (int)key.size();
+      if (L->nblk) {
+        L->cb_key.upload(key.data(), key.size(), c->stream);
+        L->cb_off.upload(off.data(), off.size(), c->stream);
+        L->cb_slot.upload(slot.data(), slot.size(), c->stream);
+      }
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
     // the coarse chain is the build's critical path: its CTAs go ahead of
     // the level-0 sweep's queued CTAs
     int prio_lo = 0, prio_hi = 0;
@@ -128,6 +159,7 @@ static void setup_levels(mp_ctx* c) {
     CUDA_CHECK(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_w, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_u, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_asm, cudaEventDisableTiming));
     if (cublasCreate(&L->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate (coarse)");
     cublasSetStream(L->blas, L->st);
     c->levels.push_back(L);
@@ -272,8 +304,49 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
     }
     c->rowptr.upload(rowptr.data(), N + 1, st);
     c->cols.upload(cols.data(), c->nnzb, st);
+    c->h_rowptr = rowptr;
+    c->h_cols = cols;
     c->diag_slot.upload(diag.data(), N, st);
     c->tet_slot.upload(slot.data(), 16 * T, st);
+    // Deterministic assembly maps (fixed summation order, no atomics):
+    //   BSR slot -> its element blocks 16t + 4a + b (t ascending), for the
+    //   Hessian gather; vertex -> its tet corners 4t + a, for the gradient.
+    // Tets of no material and pinned rows / columns contribute nothing.
+    const int64_t T_el = c->T_snh + c->T_arap;
+    std::vector<unsigned char> pinh(N);
+    for (int64_t i = 0; i < N; ++i) pinh[i] = s->dirichlet[n2o[i]] ? 1 : 0;
+    std::vector<int> hoff(c->nnzb + 1, 0), voff(N + 1, 0), srow(c->nnzb);
+    for (int64_t v = 0; v < N; ++v)
+      for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) srow[k] = (int)v;
+    for (int64_t t = 0; t < T_el; ++t) {
+      const int id[4] = {tets[t].x, tets[t].y, tets[t].z, tets[t].w};
+      for (int a = 0; a < 4; ++a) {
+        if (pinh[id[a]]) continue;
+        ++voff[id[a] + 1];
+        for (int b = 0; b < 4; ++b)
+          if (!pinh[id[b]]) ++hoff[slot[16 * t + 4 * a + b] + 1];
+      }
+    }
+    for (int64_t k = 0; k < c->nnzb; ++k) hoff[k + 1] += hoff[k];
+    for (int64_t v = 0; v < N; ++v) voff[v + 1] += voff[v];
+    std::vector<int> hval(hoff[c->nnzb]), vval(voff[N]);
+    std::vector<int> hcur(hoff.begin(), hoff.end() - 1), vcur(voff.begin(), voff.end() - 1);
+    for (int64_t t = 0; t < T_el; ++t) {
+      const int id[4] = {tets[t].x, tets[t].y, tets[t].z, tets[t].w};
+      for (int a = 0; a < 4; ++a) {
+        if (pinh[id[a]]) continue;
+        vval[vcur[id[a]]++] = (int)(4 * t + a);
+        for (int b = 0; b < 4; ++b)
+          if (!pinh[id[b]]) hval[hcur[slot[16 * t + 4 * a + b]]++] = (int)(16 * t + 4 * a + b);
+      }
+    }
+    c->hs_off.upload(hoff.data(), c->nnzb + 1, st);
+    c->hs_val.upload(hval.data(), std::max<size_t>(1, hval.size()), st);
+    c->slot_row.upload(srow.data(), c->nnzb, st);
+    c->vt_off.upload(voff.data(), N + 1, st);
+    c->vt_val.upload(vval.data(), std::max<size_t>(1, vval.size()), st);
+    c->fbuf.ensure(12 * (size_t)std::max<int64_t>(1, T_el));
+    c->hbuf.ensure(90 * (size_t)std::max<int64_t>(1, T_el));
     c->bsr.ensure(9 * (size_t)c->nnzb);
     CUDA_CHECK(cudaStreamSynchronize(st));
   }

@@ -31,12 +31,14 @@ static double hessian_bytes(const mp_ctx* c) {
 
 // energy.gradient (energy.py:357-370) with the current constraint set
 static void gradient(mp_ctx* c, const double* x, const double* xt, double h, double* g) {
-  elastic_gradient(c, x, xt, h, g);
-  if (c->cur.count) {
-    k_contact_grad<<<grid_for(c->cur.count, 128), 128, 0, c->stream>>>(c->cur.count, c->cur.verts, c->cur.d,
-                                                                      c->cur.grad, c->pinned, c->d_hat, c->kappa, g);
+  const int64_t nc = c->cur.count;
+  if (nc) {
+    c->cbuf.ensure(12 * (size_t)nc);
+    k_contact_grad_rows<<<grid_for(nc, 128), 128, 0, c->stream>>>(nc, c->cur.d, c->cur.grad, c->d_hat, c->kappa,
+                                                                   c->cbuf);
     LAUNCH_CHECK();
   }
+  gradient_gather(c, x, xt, h, g, nc ? c->inc_cur.off.p : nullptr, c->inc_cur.val2.p, c->cbuf.p);
 }
 
 // energy.incremental_potential (energy.py:346-354)
@@ -165,35 +167,66 @@ static void mas_build(mp_ctx* c) {
   const int64_t D = c->D;
   // coarse levels: own streams, concurrent with the level-0 blocks below
   CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, 8 * sizeof(int), c->stream));
+  const int64_t nc = c->base.count;
+  if (nc && c->n_levels) {
+    c->fx_scale.ensure(2);
+    k_fx_scale<<<1, 256, 0, c->stream>>>(nc, c->base.k, c->base.nrm, c->fx_scale);
+    LAUNCH_CHECK();
+  }
   CUDA_CHECK(cudaEventRecord(c->ev_bsr, c->stream));
+  // assembly: the first coarse level from the BSR (static gather map) plus
+  // the contact terms (fixed point); every further level from the previous
+  // level's dense matrix before that one is swept in place
   for (int l = 0; l < c->n_levels; ++l) {
     CoarseLevel& L = *c->levels[l];
     cudaStream_t st = L.st;
-    CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_bsr, 0));
-    L.dense.zero((size_t)L.n * L.n, st);
-    k_bsr_to_coarse<<<grid_for(c->N, 128), 128, 0, st>>>(c->N, c->rowptr, c->cols, c->bsr, L.span, L.n, L.dense);
-    LAUNCH_CHECK();
-    if (c->base.count) {
-      k_contact_coarse<<<grid_for(c->base.count, 128), 128, 0, st>>>(c->base.count, c->base.verts, c->base.grad,
-                                                                      c->base.k, c->N, L.span, L.n, L.dense);
+    if (l == 0) {
+      CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_bsr, 0));
+      L.dense.zero((size_t)L.n * L.n, st);
+      if (L.nblk) {
+        k_coarse_gather<<<grid_for(32 * (int64_t)L.nblk, 128), 128, 0, st>>>(L.nblk, L.cb_key, L.cb_off, L.cb_slot,
+                                                                             c->bsr, L.A, c->N, L.span, L.n, L.dense);
+        LAUNCH_CHECK();
+      }
+      if (nc) {
+        L.fx_acc.zero(2 * (size_t)L.n * L.n, st);
+        k_contact_coarse<<<grid_for(nc, 128), 128, 0, st>>>(nc, c->base.verts, c->base.grad, c->base.k, c->N,
+                                                            L.span, L.n, c->fx_scale, L.fx_acc);
+        LAUNCH_CHECK();
+      }
+      k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense, nc ? L.fx_acc.p : nullptr,
+                                                                     c->fx_scale.p);
+    } else {
+      CoarseLevel& F = *c->levels[l - 1];
+      CUDA_CHECK(cudaStreamWaitEvent(st, F.ev_asm, 0));
+      L.dense.ensure((size_t)L.n * L.n);
+      k_coarse_up<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.A, c->cfg.coarse_block, F.A, F.dense, F.n,
+                                                                     c->N, L.span, F.span, L.dense);
       LAUNCH_CHECK();
+      k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense, nullptr, nullptr);
     }
-    k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense);
     LAUNCH_CHECK();
+    CUDA_CHECK(cudaEventRecord(L.ev_asm, st));
+  }
+  for (int l = 0; l < c->n_levels; ++l) {
+    CoarseLevel& L = *c->levels[l];
+    if (l + 1 < c->n_levels) CUDA_CHECK(cudaStreamWaitEvent(L.st, c->levels[l + 1]->ev_asm, 0));
     L.inv.ensure((size_t)cyc_size(L.n));
     dense_spd_inverse(c, L, c->counters.p + 4 + std::min(l, 3));
-    CUDA_CHECK(cudaEventRecord(L.done, st));
+    CUDA_CHECK(cudaEventRecord(L.done, L.st));
   }
   // level 0
   c->Mfull.zero((size_t)D * m * m, c->stream);
   c->Bblk.ensure((size_t)D * cyc_size(m));
   c->Mblk.ensure((size_t)D * cyc_size(m));
-  if (c->base.count) {
-    k_contact_blocks<<<grid_for(c->base.count, 128), 128, 0, c->stream>>>(c->base.count, c->base.verts,
-                                                                         c->base.grad, c->base.k, c->bs, m, c->Mfull);
+  if (nc) {
+    k_contact_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->pinned, c->inc_base.off, c->inc_base.val2,
+                                                                 c->base.verts, c->base.grad, c->base.k, c->bs, m,
+                                                                 c->Mfull);
     LAUNCH_CHECK();
   }
-  k_bsr_to_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, c->bs, m, c->Mfull);
+  k_bsr_to_blocks<<<grid_for(c->nnzb, 128), 128, 0, c->stream>>>(c->nnzb, c->slot_row, c->cols, c->bsr, c->bs, m,
+                                                                 c->Mfull);
   LAUNCH_CHECK();
   k_mas_sweep<<<(unsigned)D, 256, 0, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
                                                     c->counters.p + 3);
@@ -213,6 +246,7 @@ static void mas_build(mp_ctx* c) {
 static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
   timer_begin(c, MP_STAGE_HESSIAN);
   copy_table(c, c->cur, c->base);
+  build_inc(c, c->inc_base, c->base.verts, c->base.count);
   assemble_elastic_bsr(c, x, h);
   timer_end(c, MP_STAGE_HESSIAN, hessian_bytes(c));
   c->have_snapshot = true;
@@ -314,9 +348,8 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
                                                                              L.span, F.rsum, L.rsum, L.r);
     }
     LAUNCH_CHECK();
-    CUDA_CHECK(cudaMemsetAsync(L.ypart.p, 0, sizeof(double) * L.n, c->stream));
     dim3 grid(grid_for(L.n, 128), L.chunks);
-    k_coarse_mv<<<grid, 128, 0, c->stream>>>(L.n, L.chunks, L.inv, L.r, L.ypart);
+    k_coarse_mv<<<grid, 128, 0, c->stream>>>(L.n, L.chunks, L.inv, L.r, L.ypc, L.ypart, L.mv_cnt);
     LAUNCH_CHECK();
     LV.lv[l] = LevelView{L.ypart, L.n, L.span, L.span / c->bs};
   }
@@ -347,14 +380,22 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
 // HessianModel.hvp (energy.py:435-440): H_base v + sum u (u^T v)
 static void hvp(mp_ctx* c, const double* vec, double* out, bool with_cands) {
   bsr_spmv(c, vec, out);
-  if (c->base.count) {
-    k_rank1_apply<<<grid_for(c->base.count, 128), 128, 0, c->stream>>>(c->base.count, c->base.verts, c->base.grad,
-                                                                       c->base.k, vec, out);
+  const int64_t nb = c->base.count, nq = with_cands ? c->n_cand : 0;
+  if (nb) {
+    c->rbuf_base.ensure(12 * (size_t)nb);
+    k_rank1_rows<<<grid_for(nb, 128), 128, 0, c->stream>>>(nb, c->base.verts, c->base.grad, c->base.k, vec,
+                                                           c->rbuf_base);
     LAUNCH_CHECK();
   }
-  if (with_cands && c->n_cand) {
-    k_rank1_apply<<<grid_for(c->n_cand, 128), 128, 0, c->stream>>>(c->n_cand, c->cand_verts, c->cand_u, nullptr,
-                                                                   vec, out);
+  if (nq) {
+    c->rbuf_cand.ensure(12 * (size_t)nq);
+    k_rank1_rows<<<grid_for(nq, 128), 128, 0, c->stream>>>(nq, c->cand_verts, c->cand_u, nullptr, vec, c->rbuf_cand);
+    LAUNCH_CHECK();
+  }
+  if (nb || nq) {
+    k_inc_gather_add<<<grid_for(32 * c->N, 128), 128, 0, c->stream>>>(
+        c->N, c->pinned, nb ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->rbuf_base.p, nq ? c->inc_cand.off.p : nullptr,
+        c->inc_cand.val2.p, c->rbuf_cand.p, out);
     LAUNCH_CHECK();
   }
 }
