@@ -248,14 +248,14 @@ __global__ void k_box_stats(int64_t P, const double* __restrict__ lo, const doub
 //
 // Level l has cell size h_l = h0 * 2^l (exact scaling) over the scene box.
 // Every object lives at the lowest level whose cell is at least as large as
-// its enumeration box, so it covers <= 2 cells per axis there (<= 8 entries).
+// its enumeration box, stored ONCE, in the cell holding its box's low corner.
 // A pair is found by the object of LOWER level querying the partner's level
 // (or, at equal levels, by the lower index for EE): the query walks levels
-// >= its own, <= 8 cells each, and meets only objects inserted at that
-// level.  Small objects therefore find large ones (the floor slab, boxes of
-// fast CCD vertices) without the large ones enumerating anything, and a pair
-// is reported once: in the cell holding the low corner of the intersection
-// of the two boxes, at the partner's level.
+// >= its own and visits the cells that can hold the low corner of a level-l
+// box meeting it ([lo - h_l, hi] per axis), so every candidate is met exactly
+// once -- no duplicate encounters to filter.  Small objects find large ones
+// (the floor slab, boxes of fast CCD vertices) without the large ones
+// enumerating anything.
 
 #define HG_MAX_LEVELS 24
 
@@ -288,16 +288,21 @@ __device__ __forceinline__ void hg_span(const HGrid& G, int l, const double* lo,
   }
 }
 
-__device__ __forceinline__ int hg_cell(const HGrid& G, int l, int a, int b, int c) {
-  return G.off[l] + (a * G.n[l][1] + b) * G.n[l][2] + c;
+// cells a query box must visit at level l to meet every level-l object whose
+// box it overlaps: objects are stored once, in the cell of their low corner,
+// and their extent is <= h_l, so that corner lies in [lo - h_l, hi]
+__device__ __forceinline__ void hg_query_span(const HGrid& G, int l, const double* lo, const double* hi, int c0[3],
+                                              int c1[3]) {
+  const double h = hg_h(G, l) * (1.0 + 1e-6);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c0[k] = hg_coord(G, l, k, lo[k] - h);
+    c1[k] = hg_coord(G, l, k, hi[k]);
+  }
 }
 
-// the pair belongs to cell (a, b, c) of level l iff the low corner of the
-// intersection of the two boxes lies in it
-__device__ __forceinline__ bool hg_owns(const HGrid& G, int l, int a, int b, int c, const double* al,
-                                        const double* bl) {
-  return hg_coord(G, l, 0, fmax(al[0], bl[0])) == a && hg_coord(G, l, 1, fmax(al[1], bl[1])) == b &&
-         hg_coord(G, l, 2, fmax(al[2], bl[2])) == c;
+__device__ __forceinline__ int hg_cell(const HGrid& G, int l, int a, int b, int c) {
+  return G.off[l] + (a * G.n[l][1] + b) * G.n[l][2] + c;
 }
 
 __device__ __forceinline__ bool boxes_meet(const double* al, const double* ah, const double* bl, const double* bh) {
@@ -352,10 +357,8 @@ __global__ void k_obj_level(int64_t nobj, int64_t F, int64_t P, HGrid G, const d
   double ext = fmax(fmax(h0[0] - l0[0], h0[1] - l0[1]), h0[2] - l0[2]);
   int l = 0;
   while (l < G.nlev - 1 && ext > hg_h(G, l)) ++l;
-  int c0[3], c1[3];
-  hg_span(G, l, l0, h0, c0, c1);
   level[i] = l;
-  cnt[i] = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
+  cnt[i] = 1;  // stored once, in the cell of its low corner
   // which levels hold any triangle / edge / point (queries skip empty ones):
   // OR-reduced per warp, one atomic per warp and class
   const int cls = i < F ? 0 : (i < P ? 1 : 2);
@@ -389,10 +392,9 @@ __global__ void k_entry_hist(const int* __restrict__ total_dev, int64_t nobj, in
   int p = upper_bound_i32(off, (int)nobj + 1, (int)e) - 1;
   int r = (int)e - off[p];
   int l = level[p];
-  int c0[3], c1[3];
-  hg_span(G, l, lo + 3 * (int64_t)p, hi + 3 * (int64_t)p, c0, c1);
-  int sx = c1[0] - c0[0] + 1, sy = c1[1] - c0[1] + 1;
-  int cell = hg_cell(G, l, c0[0] + r % sx, c0[1] + (r / sx) % sy, c0[2] + r / (sx * sy));
+  const double* o = lo + 3 * (int64_t)p;
+  (void)r;
+  int cell = hg_cell(G, l, hg_coord(G, l, 0, o[0]), hg_coord(G, l, 1, o[1]), hg_coord(G, l, 2, o[2]));
   ecell[e] = cell;
   atomicAdd(p < F ? &tri_cnt[cell] : (p < P ? &edge_cnt[cell] : &pt_cnt[cell]), 1);
 }
@@ -637,7 +639,7 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
   for (int l = T.level[T.P + q]; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
-    hg_span(T.G, l, pl, ph, c0, c1);
+    hg_query_span(T.G, l, pl, ph, c0, c1);
     for (int a = c0[0]; a <= c1[0]; ++a)
       for (int b = c0[1]; b <= c1[1]; ++b)
         for (int c = c0[2]; c <= c1[2]; ++c) {
@@ -650,7 +652,7 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
             if (e < e1) {
               t = T.tri_ent[e];
               const double* tl = T.tri_box + 6 * (int64_t)e;
-              pass = boxes_meet(pl, ph, tl, tl + 3) && hg_owns(T.G, l, a, b, c, pl, tl) &&
+              pass = boxes_meet(pl, ph, tl, tl + 3) &&
                      pt_ref_pass(T, tri, x, v, q, t);
             }
             hq_emit<EM>(pass, true, lane, n, o, v, t, pa, pb, cap, Q, qn, A);
@@ -681,7 +683,7 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
   for (int l = T.level[t] + 1; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
-    hg_span(T.G, l, tl, th, c0, c1);
+    hg_query_span(T.G, l, tl, th, c0, c1);
     for (int a = c0[0]; a <= c1[0]; ++a)
       for (int b = c0[1]; b <= c1[1]; ++b)
         for (int c = c0[2]; c <= c1[2]; ++c) {
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
               const int q = T.pt_ent[e];
               const double* pl = T.pt_box + 6 * (int64_t)e;
               v = sverts[q];
-              pass = boxes_meet(pl, pl + 3, tl, th) && hg_owns(T.G, l, a, b, c, pl, tl) &&
+              pass = boxes_meet(pl, pl + 3, tl, th) &&
                      pt_ref_pass(T, tri, x, v, q, (int)t);
             }
             hq_emit<EM>(pass, true, lane, n, o, v, (int)t, pa, pb, cap, Q, qn, A);
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
   for (int l = lv; l < T.G.nlev; ++l) {
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
-    hg_span(T.G, l, il, ih, c0, c1);
+    hg_query_span(T.G, l, il, ih, c0, c1);
     for (int a = c0[0]; a <= c1[0]; ++a)
       for (int b = c0[1]; b <= c1[1]; ++b)
         for (int c = c0[2]; c <= c1[2]; ++c) {
@@ -742,8 +744,7 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
             if (e < e1) {
               j = T.edge_ent[e];
               const double* jl = T.edge_box + 6 * (int64_t)e;
-              pass = !(l == lv && j <= (int)i) && boxes_meet(il, ih, jl, jl + 3) &&
-                     hg_owns(T.G, l, a, b, c, il, jl);
+              pass = !(l == lv && j <= (int)i) && boxes_meet(il, ih, jl, jl + 3);
               if (pass) {
                 const int ja = edge[2 * j], jb = edge[2 * j + 1];
                 const double* flj = T.flo + 3 * (T.F + j);
@@ -860,9 +861,9 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemsetAsync(c->cell_cnt.p + nobj, 0, sizeof(int), st));
   exclusive_scan(c, c->cell_cnt, c->cell_off, nobj + 1);
-  // every object covers <= 2 cells per axis at its level: <= 8 entries each,
+  // one entry per object,
   // so the entry arrays are sized without reading the total back
-  const int64_t total_cap = 8 * nobj;
+  const int64_t total_cap = nobj;
   const int* total_dev = c->cell_off.p + nobj;
   const size_t ncell = (size_t)tot_cells;
   for (DBuf<int>* b : {&g.tri_cnt, &g.tri_start, &g.edge_cnt, &g.edge_start, &g.pt_cnt, &g.pt_start})
@@ -871,9 +872,9 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   g.tri_ent.ensure((size_t)total_cap + 1);
   g.edge_ent.ensure((size_t)total_cap + 1);
   g.pt_ent.ensure((size_t)total_cap + 1);
-  g.tri_box.ensure(48 * (size_t)F + 6);
-  g.edge_box.ensure(48 * (size_t)c->E + 6);
-  g.pt_box.ensure(48 * (size_t)V + 6);
+  g.tri_box.ensure(6 * (size_t)F + 6);
+  g.edge_box.ensure(6 * (size_t)c->E + 6);
+  g.pt_box.ensure(6 * (size_t)V + 6);
   for (DBuf<int>* b : {&g.tri_cnt, &g.edge_cnt, &g.pt_cnt})
     CUDA_CHECK(cudaMemsetAsync(b->p, 0, sizeof(int) * (ncell + 1), st));
   k_entry_hist<<<grid_for(total_cap, 256), 256, 0, st>>>(total_dev, nobj, F, P, G, c->cell_off, g.level, c->box_elo,

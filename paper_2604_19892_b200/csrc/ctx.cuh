@@ -30,11 +30,15 @@ struct DBuf {
     p = nullptr;
     n = 0;
   }
-  // grow to at least `count` elements; contents are NOT preserved
+  // grow to at least `count` elements, geometrically (cudaFree / cudaMalloc
+  // synchronise the device: buffers sized by contact counts must not
+  // reallocate every time a count creeps up); contents are NOT preserved
   void ensure(size_t count) {
     if (count <= n && p) return;
+    const size_t grown = n + n / 2;
     release();
     size_t c = count < 1 ? 1 : count;
+    if (grown > c) c = grown;
     CUDA_CHECK(cudaMalloc(&p, c * sizeof(T)));
     n = c;
   }
