@@ -698,8 +698,11 @@ int mp_set_config(mp_ctx* c, const mp_solver_config* cfg) {
     validate_config(*cfg);
     if (cfg->block_size != c->cfg.block_size)
       throw MpError(MP_ERR_CONFIG, "block_size is fixed per context (partition); create a new context");
+    const bool relevel = cfg->levels != c->cfg.levels || cfg->coarse_block != c->cfg.coarse_block;
     c->cfg = *cfg;
-    setup_levels(c);
+    // the hierarchy (streams, handles, gather maps) only depends on the MAS
+    // depth; the per-call config of the Python API re-sets the rest freely
+    if (relevel) setup_levels(c);
     c->have_mas = false;
   });
 }
