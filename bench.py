@@ -278,8 +278,11 @@ def run_ours(args):
                 "frac": round(ach / hbm, 4), "traffic": traffic, "bytes_per_launch": round(b / cnt),
                 "us_per_launch": round(1e3 * ms / cnt, 2), "launches": cnt, "peak_kind": peak_kind}
 
+    host = {"loop_ms": round(stats["loop"][0], 2), "blocked_in_syncs_ms": round(stats["host_wait"][0], 2),
+            "syncs": stats["host_wait"][1],
+            "note": "host wall time of the advance loops and the part spent blocked on the stream"}
     stage_share = {k: {"ms": round(v[0], 2), "count": v[1], "share": round(v[0] / max(total_ms, 1e-9), 4)}
-                   for k, v in stats.items()}
+                   for k, v in stats.items() if k not in ("loop", "host_wait")}
     n3 = 3 * scene.mesh.n_vertices
     line = {
         "metric": "PNCG iters/sec", "value": all_iters / (t_max * 1e-3), "unit": "iters/s", "n_gpus": ws,
@@ -298,10 +301,12 @@ def run_ours(args):
         "roofline": roof("mas_apply_l0", "k_mas_apply_l0 (level-0 block matvec + Woodbury overlay + coarse "
                                           "prolongation + pinned projection; TMA-staged packed blocks)"),
         "roofline_mas_stage": roof("mas_apply", "MAS apply stage: k_restrict1 + k_coarse_mv x2 + k_mas_apply_l0"),
-        "roofline_gradient": roof("tet_grad", "k_tet_grad<SNH> (F, Piola, G^T scatter; 113 B/tet + 72 B/vertex)"),
-        "roofline_gradient_stage": roof("gradient", "gradient stage: k_inertia_grad + k_tet_grad x2 + k_contact_grad"),
-        "roofline_hvp": roof("hvp", "HVP: k_bsr_spmv + k_rank1_apply"),
+        "roofline_gradient": roof("tet_grad", "k_tet_grad<SNH> (F, Piola, per-corner forces; 113 B/tet + 48 B/vertex)"),
+        "roofline_gradient_stage": roof("gradient",
+                                        "gradient stage: k_contact_grad_rows + k_tet_grad x2 + k_grad_gather"),
+        "roofline_hvp": roof("hvp", "HVP: k_bsr_spmv + k_rank1_rows + k_inc_gather_add"),
         "stages": stage_share,
+        "host": host,
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -202,7 +202,9 @@ enum {
   MP_STAGE_CCD = 7,            /* CCD clamp                solver.py:268-280 */
   MP_STAGE_MAS_L0 = 8,         /* the level-0 kernel of the MAS apply alone   */
   MP_STAGE_TET_GRAD = 9,       /* the SNH per-tet gradient kernel alone        */
-  MP_STAGE_COUNT = 10
+  MP_STAGE_HOST_WAIT = 10,     /* host wall time blocked on the stream (syncs) */
+  MP_STAGE_LOOP = 11,          /* host wall time of advance_step loops         */
+  MP_STAGE_COUNT = 12
 };
 int mp_stage_timing(mp_ctx* ctx, int enable);
 

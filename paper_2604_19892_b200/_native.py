@@ -57,7 +57,8 @@ EXPORTS = (
     "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
 )
 
-STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd", "mas_apply_l0", "tet_grad")
+STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd", "mas_apply_l0",
+          "tet_grad", "host_wait", "loop")
 
 _lib = None
 

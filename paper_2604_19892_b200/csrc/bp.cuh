@@ -141,7 +141,6 @@ static int bits_for(unsigned long long v) {
 }
 
 
-static void sync_stream(mp_ctx* c) { CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
 
 // Boxes of triangles and edges: raw (rlo, rhi); reference filter (flo, fhi:
 // triangle [lo - gap, hi + gap], edge [lo, hi + gap]); enumeration (elo,

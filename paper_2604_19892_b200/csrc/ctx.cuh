@@ -13,6 +13,7 @@
 #include <cusolverDn.h>
 
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include "common.cuh"
@@ -247,6 +248,10 @@ struct mp_ctx {
   int64_t n_ccd_seen = 0;   // pairs enumerated by the last CCD
 
   // pinned host staging for scalars
+  double sync_wait_ms = 0.0;  // host time blocked in sync_stream (stage timing on)
+  int64_t n_sync = 0;
+  double loop_ms = 0.0;       // host wall time of advance loops (stage timing on)
+  int64_t n_loop = 0;
   double* h_scal = nullptr;
   int* h_cnt = nullptr;
   unsigned long long* h_npairs = nullptr;  // = h_scal[63]
@@ -254,6 +259,19 @@ struct mp_ctx {
 
   ~mp_ctx();
 };
+
+// every host wait on the context stream goes through here: with
+// MP_OPT stage timing on, the wall time spent blocked is accumulated
+static void sync_stream(mp_ctx* c) {
+  if (!c->timing) {
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->n_sync += 1;
+}
 
 static void timer_fold(StageTimer& t) {
   if (!t.pending) return;

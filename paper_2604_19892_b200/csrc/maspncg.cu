@@ -416,7 +416,18 @@ static void solve2(double A[2][2], double b[2], double* x0, double* x1) {
   *x0 = (b0 - a01 * (*x1)) / a00;
 }
 
+static void advance_loop_body(mp_ctx* c, double h, LoopResult& R);
+
 static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
+  const auto t0 = Clock::now();
+  advance_loop_body(c, h, R);
+  if (c->timing) {
+    c->loop_ms += ms_since(t0);
+    c->n_loop += 1;
+  }
+}
+
+static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
   const mp_solver_config& cfg = c->cfg;
   const int64_t n3 = 3 * c->N;
   cudaStream_t st = c->stream;
@@ -643,6 +654,10 @@ int mp_stage_timing(mp_ctx* c, int enable) {
       t.bytes = 0.0;
       t.count = 0;
     }
+    c->sync_wait_ms = 0.0;
+    c->n_sync = 0;
+    c->loop_ms = 0.0;
+    c->n_loop = 0;
     c->timing = enable != 0;
   });
 }
@@ -662,6 +677,13 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
 int mp_stage_stats(mp_ctx* c, int stage, double* total_ms, int64_t* count, double* bytes) {
   return guarded(c, [&] {
     if (stage < 0 || stage >= MP_STAGE_COUNT) throw MpError(MP_ERR_CONFIG, "unknown stage");
+    if (stage == MP_STAGE_HOST_WAIT || stage == MP_STAGE_LOOP) {
+      const bool w = stage == MP_STAGE_HOST_WAIT;
+      if (total_ms) *total_ms = w ? c->sync_wait_ms : c->loop_ms;
+      if (count) *count = w ? c->n_sync : c->n_loop;
+      if (bytes) *bytes = 0.0;
+      return;
+    }
     StageTimer& t = c->timers[stage];
     timer_fold(t);
     if (total_ms) *total_ms = t.total_ms;

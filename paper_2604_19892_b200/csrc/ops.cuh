@@ -62,7 +62,7 @@ static void multidot(mp_ctx* c, int64_t len, const DotSpec& S) {
   k_multidot_final<<<1, 32, 0, c->stream>>>(nb, S.n, c->red_part, c->dscal);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->dscal.p, sizeof(double) * S.n, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  sync_stream(c);
 }
 
 // p = a z + b pp ; Hp = a v + b Hpp ; partials of g.p and max|p|
@@ -125,7 +125,7 @@ static void form_direction(mp_ctx* c, double a, double b, const double* pp, cons
   k_form_dir_final<<<1, 32, 0, c->stream>>>(nb, c->red_part, c->dscal);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->dscal.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  sync_stream(c);
 }
 
 __global__ void k_velocity(int64_t N, const double* __restrict__ x, const double* __restrict__ x0, double h,
