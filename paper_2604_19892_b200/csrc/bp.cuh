@@ -458,6 +458,9 @@ struct PairArgs {
   ContactParams CP;
   CcdParams CC;
   unsigned long long* n_pairs;  // fused enumeration: reference pairs seen
+  // append enumeration (HQ_APPEND): this class's list and its counter
+  int *app_a, *app_b, *app_cnt;
+  int64_t app_cap;
 };
 
 template <int MODE>
@@ -532,6 +535,32 @@ __global__ void __launch_bounds__(256) k_pairs(const int* __restrict__ n_pt_dev,
   }
 }
 
+// the appended lists: PT pairs [0, n_pt) in (pa, pb), EE pairs in (ea, eb)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_pairs_app(const int* __restrict__ cnt, int64_t cap_pt, int64_t cap_ee,
+                                                   const int* __restrict__ pa, const int* __restrict__ pb,
+                                                   const int* __restrict__ ea, const int* __restrict__ eb,
+                                                   PairArgs A) {
+  const int64_t n_pt = cnt[0] < cap_pt ? cnt[0] : cap_pt;  // overflow: the caller grows and reruns
+  const int64_t n_ee = cnt[1] < cap_ee ? cnt[1] : cap_ee;
+  const int64_t n = n_pt + n_ee;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x - lane); base < n; base += stride) {
+    const int64_t i = base + lane;
+    const bool live = i < n, pt = i < n_pt;
+    int a = 0, b = 0;
+    if (live) {
+      if (pt) {
+        a = pa[i]; b = pb[i];
+      } else {
+        a = ea[i - n_pt]; b = eb[i - n_pt];
+      }
+    }
+    pair_work<MODE>(live, pt, a, b, -1, A);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // enumeration: count pass, scan, fill pass -> reference pair list
 //   PT pairs (v, t): v = surface vertex (device id), t = triangle index
@@ -572,7 +601,21 @@ __device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, c
 // order-free consumers only (CCD / certificate minima and flags, contacts
 // that are key-sorted afterwards): passing pairs queue in shared memory and
 // are worked 32 at a time, so no list is written and no count pass runs.
-enum { HQ_COUNT = -2, HQ_FILL = -1 };
+// HQ_APPEND writes an unordered list in one pass: warps queue their passing
+// pairs in shared memory and reserve 32 list slots per atomic -- for the
+// order-free CCD / certificate consumers, it saves the count pass.
+enum { HQ_APPEND = -3, HQ_COUNT = -2, HQ_FILL = -1 };
+
+__device__ __forceinline__ void hq_append_flush(int lane, int k, const int2* q, const PairArgs& A) {
+  int base = 0;
+  if (lane == 0) base = atomicAdd(A.app_cnt, k);
+  base = __shfl_sync(WARP_FULL, base, 0);
+  if (lane < k && (int64_t)base + lane < A.app_cap) {
+    const int2 pr = q[lane];
+    A.app_a[base + lane] = pr.x;
+    A.app_b[base + lane] = pr.y;
+  }
+}
 #define HQ_QUEUE 64
 
 template <int EM>
@@ -587,6 +630,15 @@ __device__ __forceinline__ void hq_emit(bool pass, bool is_pt, int lane, int& n,
         pa[pos] = a;
         pb[pos] = b;
       }
+    }
+  } else if (EM == HQ_APPEND) {
+    if (pass) q[qn + rank] = make_int2(a, b);
+    qn += __popc(m);
+    if (qn >= 32) {
+      __syncwarp();
+      qn -= 32;
+      hq_append_flush(lane, 32, q + qn, A);
+      __syncwarp();
     }
   } else if (EM >= 0) {
     if (pass) q[qn + rank] = make_int2(a, b);
@@ -606,6 +658,9 @@ template <int EM>
 __device__ __forceinline__ void hq_finish(bool is_pt, int lane, int n, int* cnt, int2* q, int qn, const PairArgs& A) {
   if (EM == HQ_COUNT) {
     if (lane == 0) *cnt = n;
+  } else if (EM == HQ_APPEND) {
+    __syncwarp();
+    if (qn > 0) hq_append_flush(lane, qn, q, A);
   } else if (EM >= 0) {
     __syncwarp();
     if (qn > 0) {
@@ -992,6 +1047,8 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
   // ~100 registers, and inlined into the enumeration it costs more occupancy
   // than the count pass it saves (measured: 362 vs 264 us per edge pass)
   const bool fused = c->bp_fused && MODE == BP_CONTACT && which == 3 && !n_pt_out;
+  // CCD / certificate without a stored per-pair output: one-pass unordered list
+  const bool append = c->bp_fused && (MODE == BP_CCD || MODE == BP_CERT) && which == 3 && !n_pt_out && !O.verts;
   for (int attempt = 0; attempt < 3; ++attempt) {
     CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
     O.counter = c->counters.p;
@@ -999,7 +1056,7 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
       // results are final after one pass (CONTACT: the caller checks O.cap)
       c->n_pairs_dev.ensure(1);
       CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), c->stream));
-      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, c->n_pairs_dev.p};
+      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, c->n_pairs_dev.p, nullptr, nullptr, nullptr, 0};
       fused_pairs<MODE>(c, x, B, A);
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -1008,11 +1065,49 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
       if (flag) *flag = c->h_cnt[1];
       return MODE == BP_CONTACT ? c->h_cnt[0] : (int64_t)*c->h_npairs;
     }
+    if (append) {
+      if (g.pa.n < 1024) { g.pa.ensure(1 << 16); g.pb.ensure(1 << 16); }
+      if (g.ea.n < 1024) { g.ea.ensure(1 << 16); g.eb.ensure(1 << 16); }
+      int* cnt = c->counters.p + 8;  // [8] PT, [9] EE appended
+      CUDA_CHECK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c->stream));
+      const int64_t cap_pt = (int64_t)std::min(g.pa.n, g.pb.n), cap_ee = (int64_t)std::min(g.ea.n, g.eb.n);
+      if (!B.empty) {
+        PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr, g.pa, g.pb, cnt, cap_pt};
+        if (V) {
+          k_hq_points<HQ_APPEND><<<grid_for(32 * V, 128), 128, 0, c->stream>>>(B.T, V, c->sverts, c->tri, x, nullptr,
+                                                                               nullptr, nullptr, nullptr, 0, A);
+          LAUNCH_CHECK();
+          k_hq_tris<HQ_APPEND><<<grid_for(32 * F, 128), 128, 0, c->stream>>>(B.T, F, c->sverts, c->tri, x, nullptr,
+                                                                             nullptr, nullptr, nullptr, 0, A);
+          LAUNCH_CHECK();
+        }
+        if (E > 1) {
+          PairArgs Ae = A;
+          Ae.app_a = g.ea; Ae.app_b = g.eb; Ae.app_cnt = cnt + 1; Ae.app_cap = cap_ee;
+          k_hq_edges<HQ_APPEND><<<grid_for(32 * E, 128), 128, 0, c->stream>>>(B.T, E, c->edge, nullptr, nullptr,
+                                                                              nullptr, nullptr, 0, Ae);
+          LAUNCH_CHECK();
+        }
+        k_pairs_app<MODE><<<8 * 148, 256, 0, c->stream>>>(cnt, cap_pt, cap_ee, g.pa, g.pb, g.ea, g.eb, A);
+        LAUNCH_CHECK();
+      }
+      CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      sync_stream(c);
+      const int64_t n_pt = c->h_cnt[5], n_ee = c->h_cnt[6];
+      if (n_pt > cap_pt || n_ee > cap_ee) {  // grow and rerun (minima / flags are idempotent)
+        if (n_pt > cap_pt) { g.pa.ensure((size_t)(n_pt * 1.25) + 1024); g.pb.ensure((size_t)(n_pt * 1.25) + 1024); }
+        if (n_ee > cap_ee) { g.ea.ensure((size_t)(n_ee * 1.25) + 1024); g.eb.ensure((size_t)(n_ee * 1.25) + 1024); }
+        continue;
+      }
+      if (flag) *flag = c->h_cnt[1];
+      return n_pt + n_ee;
+    }
     collect_pairs(c, x, B, which);
     const int64_t cap = (int64_t)std::min(g.pa.n, g.pb.n);
     if (MODE != BP_RAW && !B.empty) {
       int sms = 148;
-      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr};
+      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr, nullptr, nullptr, nullptr, 0};
       k_pairs<MODE><<<(unsigned)(8 * sms), 256, 0, c->stream>>>(g.qoff.p + V + F, g.qoff.p + nq, cap, g.pa, g.pb, A);
       LAUNCH_CHECK();
     }

@@ -86,7 +86,8 @@ struct BpGridBufs {
   DBuf<int> level;                                                       // (objects)
   DBuf<int> rc;                                                          // (objects*6) reference cells
   DBuf<int> qcnt, qoff;                                                  // per-query pair counts
-  DBuf<int> pa, pb;                                                      // reference pair list
+  DBuf<int> pa, pb;                                                      // reference pair list (PT in append mode)
+  DBuf<int> ea, eb;                                                      // append mode: EE list
   DBuf<int> ecell, tri_ent, edge_ent, pt_ent;                            // (entries)
   DBuf<double> tri_box, edge_box, pt_box;  // (entries*6) the entry's enumeration box, in cell order
 };
