@@ -212,8 +212,9 @@ int mp_stage_timing(mp_ctx* ctx, int enable);
  * reference's full CCD candidate set inside the loop (default 0: the tight
  * set, same results).  MP_OPT_RECORD_ENERGY: evaluate the incremental
  * potential at every iterate into mp_iter_record.energy (default 0).
- * MP_OPT_APPLY_TMA: stage level-0 MAS blocks with TMA bulk copies (1,
- * default) or per-thread cp.async (0); MP_OPT_APPLY_STAGES (2 or 3) and
+ * MP_OPT_APPLY_TMA: level-0 MAS apply variant -- 2 (default) direct
+ * streaming loads, one CTA per subdomain; 1 TMA bulk staging; 0 per-thread
+ * cp.async staging; MP_OPT_APPLY_STAGES (2 or 3) and
  * MP_OPT_APPLY_CTAS (persistent CTAs per SM) tune its pipeline; same results.
  * MP_OPT_BP_FUSED: constraint-set / CCD / certificate pair work fused into
  * the grid enumeration (1, default) or over a stored pair list (0); same

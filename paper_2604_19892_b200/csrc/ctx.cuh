@@ -139,7 +139,7 @@ struct mp_ctx {
   bool timing = false;
   bool ccd_exact_set = false;
   bool record_energy = false;
-  bool apply_tma = true;     // level-0 apply staging: TMA bulk (true) or cp.async
+  int apply_mode = 2;        // level-0 apply: 2 direct loads, 1 TMA-staged, 0 cp.async-staged
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
   bool bp_fused = true;      // pair work fused into the grid enumeration

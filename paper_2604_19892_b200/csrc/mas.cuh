@@ -953,6 +953,69 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
   }
 }
 
+// Direct variant (default): one CTA of 192 threads per subdomain, no staging
+// of the packed block -- thread i of group 0 / 1 streams diagonals 1..s_mid /
+// s_mid+1.. of row i straight from HBM (two unit-stride loads per diagonal
+// across the warp, 8 diagonals unrolled: 16 independent loads in flight per
+// thread).  The whole D-block grid is one wave (about 10 CTAs, 60 warps per
+// SM), so the loads of every block are in flight at once and no pipeline has
+// to fill or drain.  Same sums, same order as the staged variants.
+__global__ void __launch_bounds__(APPLY_THREADS)
+k_mas_apply_l0_direct(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
+                      const int* __restrict__ overlay_of, const double* __restrict__ overlay,
+                      const double* __restrict__ g, const unsigned char* __restrict__ pinned, LevelViews LV,
+                      double* __restrict__ z) {
+  __shared__ double gsh[96];
+  __shared__ double part[96];
+  const int64_t d = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int grp = tid >= 96 ? 1 : 0;
+  const int i = tid - 96 * grp;
+  const int64_t csz = cyc_size(m);
+  const int ov = overlay_of ? overlay_of[d] : -1;
+  const double* __restrict__ P = (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
+  const int64_t v0 = d * bs;
+  const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
+  if (tid < m) gsh[tid] = (tid < nd3) ? g[3 * v0 + tid] : 0.0;
+  __syncthreads();
+  const int smax = m / 2;
+  const bool even = (m % 2) == 0;
+  const int s_full = even ? smax - 1 : smax;
+  const int s_mid = s_full / 2;
+  double acc = 0.0;
+  if (i < nd3) {
+    const int s0 = grp ? s_mid + 1 : 1, s1 = grp ? s_full : s_mid;
+    if (!grp) acc = __ldcs(P + i) * gsh[i];
+#pragma unroll 8
+    for (int s = s0; s <= s1; ++s) {
+      const double* dg = P + (int64_t)s * m;
+      int jp = i + s; if (jp >= m) jp -= m;
+      int jm = i - s; if (jm < 0) jm += m;
+      acc += __ldcs(dg + i) * gsh[jp] + __ldcs(dg + jm) * gsh[jm];
+    }
+    if (grp && even) {
+      const double* dg = P + (int64_t)smax * m;
+      int jp = i + smax; if (jp >= m) jp -= m;
+      acc += __ldcs(dg + (i < jp ? i : jp)) * gsh[jp];
+    }
+    if (grp) part[i] = acc;
+  }
+  __syncthreads();
+  if (!grp && i < nd3) {
+    acc += part[i];
+    const int64_t dof = 3 * v0 + i;
+    const int64_t v = v0 + i / 3;
+    const int c = i - 3 * (i / 3);
+    for (int l = 0; l < LV.L; ++l) {
+      const LevelView& L = LV.lv[l];
+      const int64_t a = d / L.ratio;
+      const int64_t na = (N - a * L.span) < L.span ? (N - a * L.span) : L.span;
+      acc += L.y[3 * a + c] * (1.0 / (double)na);
+    }
+    z[dof] = pinned[v] ? 0.0 : acc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Sparse-Input Woodbury build, one CTA per touched subdomain.
 // smem: B (m x m full), U (m x K), W (m x K), cap (K x K)

@@ -361,7 +361,9 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   timer_begin(c, MP_STAGE_MAS_L0);
   const int* ovp = ov ? c->overlay_of.p : nullptr;
 #define L0_ARGS c->D, c->N, c->bs, c->m, c->Bblk, ovp, c->overlay, g, c->pinned, LV, z
-  if (c->apply_tma) {
+  if (c->apply_mode == 2) {
+    k_mas_apply_l0_direct<<<(unsigned)c->D, APPLY_THREADS, 0, c->stream>>>(L0_ARGS);
+  } else if (c->apply_mode == 1) {
     if (stages == 3) k_mas_apply_l0<true, 3><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
     else k_mas_apply_l0<true, 2><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
   } else {
