@@ -330,9 +330,11 @@ def run_ours(args):
                 "frames": "the timed frames replayed from the same start state (iteration counts may differ "
                           "slightly: FP64 atomics make contact frames chaotic)",
                 "api": "paper_2604_19892_b200.solver.step(scene, x, v, h, cfg) with pinned numpy x, v"},
-        "roofline": roof("mas_apply_l0", "k_mas_apply_l0 (level-0 block matvec + Woodbury overlay + coarse "
-                                          "prolongation + pinned projection; TMA-staged packed blocks)"),
-        "roofline_mas_stage": roof("mas_apply", "MAS apply stage: k_restrict1 + k_coarse_mv x2 + k_mas_apply_l0"),
+        "roofline": roof("mas_apply_l0", "k_mas_apply_l0_direct (level-0 packed block matvec + Woodbury overlay + "
+                                          "coarse prolongation + pinned projection; one CTA per subdomain, "
+                                          "streaming loads)"),
+        "roofline_mas_stage": roof("mas_apply",
+                                   "MAS apply stage: k_restrict1 + k_restrict_up + k_coarse_mv x2 + k_mas_apply_l0_direct"),
         "roofline_gradient": roof("tet_grad", "k_tet_grad<SNH> (F, Piola, per-corner forces; 113 B/tet + 48 B/vertex)"),
         "roofline_gradient_stage": roof("gradient",
                                         "gradient stage: k_contact_grad_rows + k_tet_grad x2 + k_grad_gather"),

@@ -194,10 +194,12 @@ __global__ void k_ccd_certify(int64_t n, const int4* __restrict__ verts, const i
 // component midrange) therefore enumerates every pair that can move alpha_d,
 // the global min or the certificate; the reference's own membership test is
 // still applied to each enumerated pair.  s = alpha_d scaling (p_mix) or 1.
+// component midrange of alpha_d-scaled p: blocks reduce min / max (order-
+// free) into partials; the last block to finish combines them
 __global__ void k_motion_midrange(int64_t N, int bs, const double* __restrict__ p, const double* __restrict__ alpha_d,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ part, int* __restrict__ done, double* __restrict__ out) {
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t v = threadIdx.x; v < N; v += blockDim.x) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x) {
     double s = alpha_d ? alpha_d[v / bs] : 1.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -207,6 +209,7 @@ __global__ void k_motion_midrange(int64_t N, int bs, const double* __restrict__ 
     }
   }
   __shared__ double sh[6][32];
+  __shared__ bool last;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     double a = -warp_max(-mn[k]), b = warp_max(mx[k]);
@@ -222,8 +225,23 @@ __global__ void k_motion_midrange(int64_t N, int bs, const double* __restrict__ 
       a = fmin(a, sh[threadIdx.x][w]);
       b = fmax(b, sh[3 + threadIdx.x][w]);
     }
+    part[6 * blockIdx.x + threadIdx.x] = a;
+    part[6 * blockIdx.x + 3 + threadIdx.x] = b;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x < 3) {
+    double a = INFINITY, b = -INFINITY;
+    for (int q = 0; q < (int)gridDim.x; ++q) {
+      a = fmin(a, __ldcg(part + 6 * q + threadIdx.x));
+      b = fmax(b, __ldcg(part + 6 * q + 3 + threadIdx.x));
+    }
     out[threadIdx.x] = 0.5 * (a + b);
   }
+  if (threadIdx.x == 0) *done = 0;
 }
 
 __global__ void k_motion_infl(int64_t N, int bs, const double* __restrict__ p, const double* __restrict__ alpha_d,
@@ -280,7 +298,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
     const double* infl = nullptr;
     if (!exact_set) {
       c->infl.ensure(c->N);
-      k_motion_midrange<<<1, 1024, 0, st>>>(c->N, c->bs, p, nullptr, d_mid);
+      k_motion_midrange<<<148, 256, 0, st>>>(c->N, c->bs, p, nullptr, c->mid_part, c->counters.p + 15, d_mid);
       LAUNCH_CHECK();
       k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, nullptr, d_mid, c->infl);
       LAUNCH_CHECK();
@@ -329,7 +347,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
         sync_stream(c);
         R.certified = c->h_cnt[2] == 0;
       } else {
-        k_motion_midrange<<<1, 1024, 0, st>>>(c->N, c->bs, p, c->alpha_d, d_mid);
+        k_motion_midrange<<<148, 256, 0, st>>>(c->N, c->bs, p, c->alpha_d, c->mid_part, c->counters.p + 15, d_mid);
         LAUNCH_CHECK();
         k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, c->alpha_d, d_mid, c->infl);
         LAUNCH_CHECK();

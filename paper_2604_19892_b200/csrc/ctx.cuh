@@ -198,6 +198,7 @@ struct mp_ctx {
   IncCSR inc_cur, inc_base, inc_cand;
   DBuf<double> cbuf, rbuf_base, rbuf_cand;  // (rows, 12) per-row terms
   DBuf<double> fx_scale;                   // coarse contact fixed-point unit
+  DBuf<double> mid_part;                   // (148, 6) CCD motion midrange partials
   DBuf<int> sort_idx, sort_idx2;
   DBuf<unsigned long long> sort_k1, sort_k2;
   DBuf<unsigned char> cub_tmp;

@@ -741,11 +741,28 @@ __global__ void k_coarse_mv(int n, int chunks, const double* __restrict__ P, con
   double acc = 0.0;
   const bool even = (n % 2) == 0;
   if (i < n) {
-    for (int s = s0; s <= s1; ++s) {
-      if (s == 0) {
-        acc += P[i] * r[i];
-        continue;
+    int s = s0;
+    if (s == 0) {
+      acc += P[i] * r[i];
+      s = 1;
+    }
+    const int s_hi = (even && s1 == n / 2) ? s1 - 1 : s1;  // full diagonals
+    // 4 diagonals per step, loads issued before use (latency, not a chain)
+    for (; s + 3 <= s_hi; s += 4) {
+      double a[4], b[4];
+      int jp[4], jm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        jp[u] = i + s + u; if (jp[u] >= n) jp[u] -= n;
+        jm[u] = i - s - u; if (jm[u] < 0) jm[u] += n;
+        const double* dg = P + (int64_t)(s + u) * n;
+        a[u] = __ldg(dg + i);
+        b[u] = __ldg(dg + jm[u]);
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += a[u] * r[jp[u]] + b[u] * r[jm[u]];
+    }
+    for (; s <= s1; ++s) {
       const double* dg = P + (int64_t)s * n;
       int jp = i + s; if (jp >= n) jp -= n;
       int jm = i - s; if (jm < 0) jm += n;
@@ -960,7 +977,7 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
 // thread).  The whole D-block grid is one wave (about 10 CTAs, 60 warps per
 // SM), so the loads of every block are in flight at once and no pipeline has
 // to fill or drain.  Same sums, same order as the staged variants.
-__global__ void __launch_bounds__(APPLY_THREADS)
+__global__ void __launch_bounds__(APPLY_THREADS, 10)
 k_mas_apply_l0_direct(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Bblk,
                       const int* __restrict__ overlay_of, const double* __restrict__ overlay,
                       const double* __restrict__ g, const unsigned char* __restrict__ pinned, LevelViews LV,
@@ -986,8 +1003,24 @@ k_mas_apply_l0_direct(int64_t D, int64_t N, int bs, int m, const double* __restr
   if (i < nd3) {
     const int s0 = grp ? s_mid + 1 : 1, s1 = grp ? s_full : s_mid;
     if (!grp) acc = __ldcs(P + i) * gsh[i];
-#pragma unroll 8
-    for (int s = s0; s <= s1; ++s) {
+    // 8 diagonals per step: all 16 loads issued before the first use, so a
+    // thread waits one memory latency per 8 diagonals, not per diagonal
+    int s = s0;
+    for (; s + 7 <= s1; s += 8) {
+      double a[8], b[8];
+      int jp[8], jm[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        jp[u] = i + s + u; if (jp[u] >= m) jp[u] -= m;
+        jm[u] = i - s - u; if (jm[u] < 0) jm[u] += m;
+        const double* dg = P + (int64_t)(s + u) * m;
+        a[u] = __ldcs(dg + i);
+        b[u] = __ldcs(dg + jm[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += a[u] * gsh[jp[u]] + b[u] * gsh[jm[u]];
+    }
+    for (; s <= s1; ++s) {
       const double* dg = P + (int64_t)s * m;
       int jp = i + s; if (jp >= m) jp -= m;
       int jm = i - s; if (jm < 0) jm += m;

@@ -371,7 +371,8 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   for (DBuf<double>* b : {&c->x, &c->xt, &c->vel, &c->g, &c->z, &c->p, &c->Hp, &c->p_prev, &c->Hp_prev, &c->z_prev,
                           &c->hv, &c->x_start, &c->x_best, &c->tmp, &c->tmp2})
     b->ensure(n3);
-  c->counters.ensure(16);
+  c->counters.zero(16, c->stream);
+  c->mid_part.ensure(6 * 148);
   c->dscal.ensure(64);
   c->solver_info.ensure(1);
   c->alpha_d.ensure(c->D);

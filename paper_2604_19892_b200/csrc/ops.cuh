@@ -44,12 +44,16 @@ __global__ void k_multidot(int64_t len, DotSpec S, double* __restrict__ part) {
 }
 
 // sum partials in block order; mode per slot: 0 sum, 1 max
+// one warp per dot: lanes stride over the block partials, fixed shuffle
+// tree (reproducible; a single thread walking 296 partials is latency bound)
 __global__ void k_multidot_final(int nblocks, int n, const double* __restrict__ part, double* __restrict__ out) {
-  int q = threadIdx.x;
-  if (q >= n) return;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (q >= n) return;  // warp-uniform
   double t = 0.0;
-  for (int b = 0; b < nblocks; ++b) t += part[b * MAX_DOTS + q];
-  out[q] = t;
+  for (int b = lane; b < nblocks; b += 32) t += part[b * MAX_DOTS + q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  if (lane == 0) out[q] = t;
 }
 
 // returns dots in c->h_scal[0..n)
@@ -59,7 +63,7 @@ static void multidot(mp_ctx* c, int64_t len, const DotSpec& S) {
   if (nb > RED_BLOCKS) nb = RED_BLOCKS;
   k_multidot<<<nb, RED_THREADS, 0, c->stream>>>(len, S, c->red_part);
   LAUNCH_CHECK();
-  k_multidot_final<<<1, 32, 0, c->stream>>>(nb, S.n, c->red_part, c->dscal);
+  k_multidot_final<<<1, 32 * MAX_DOTS, 0, c->stream>>>(nb, S.n, c->red_part, c->dscal);
   LAUNCH_CHECK();
   CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->dscal.p, sizeof(double) * S.n, cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
@@ -104,14 +108,21 @@ __global__ void k_form_dir(int64_t len, double a, double b, const double* __rest
 }
 
 __global__ void k_form_dir_final(int nblocks, const double* __restrict__ part, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
   double t = 0.0, m = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
+  for (int b = lane; b < nblocks; b += 32) {
     t += part[b * MAX_DOTS];
     m = fmax(m, part[b * MAX_DOTS + 1]);
   }
-  out[0] = t;
-  out[1] = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_down_sync(0xffffffffu, t, o);
+    m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  }
+  if (lane == 0) {
+    out[0] = t;
+    out[1] = m;
+  }
 }
 
 // p, Hp formed on device; returns (g.p, max|p|) in h_scal[0..1]
