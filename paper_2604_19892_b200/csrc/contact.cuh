@@ -149,6 +149,7 @@ static BpOut table_out(PairTable& t) {
 // compute_constraint_set at x (device, new order) into c->cur (key order)
 static void constraint_set(mp_ctx* c, const double* x) {
   c->cur.count = 0;
+  c->inc_cur_rows = -1;
   if (c->F == 0) return;
   BpGrid B = build_bp(c, x, 0.0, c->d_hat);
   ContactParams CP{c->d_hat, c->kappa, c->pinned, KeyCtx{c->new2old, c->id_bits}};
@@ -162,6 +163,7 @@ static void constraint_set(mp_ctx* c, const double* x) {
     if (n <= O.cap) {
       sort_table_into(c, c->scratch, c->cur, n);
       build_inc(c, c->inc_cur, c->cur.verts, n);
+      c->inc_cur_rows = n;
       return;
     }
     c->scratch.ensure((size_t)(n * 1.5) + 1024);

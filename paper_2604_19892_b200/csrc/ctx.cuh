@@ -196,6 +196,7 @@ struct mp_ctx {
   // vertex -> incidences (4 row + corner, ascending) of cur / base / the
   // update candidates: fixed-order per-vertex gathers instead of atomics
   IncCSR inc_cur, inc_base, inc_cand;
+  int64_t inc_cur_rows = -1;  // rows of cur that inc_cur indexes (-1: stale)
   DBuf<double> cbuf, rbuf_base, rbuf_cand;  // (rows, 12) per-row terms
   DBuf<double> fx_scale;                   // coarse contact fixed-point unit
   DBuf<double> mid_part;                   // (148, 6) CCD motion midrange partials

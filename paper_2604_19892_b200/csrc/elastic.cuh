@@ -335,7 +335,35 @@ __global__ void k_hess_gather(int64_t nnzb, const int* __restrict__ slot_row, co
     const double dv = pinned[v] ? 1.0 : mass[v];
     acc[0] = dv; acc[4] = dv; acc[8] = dv;
   }
-  for (int k = hs_off[sl]; k < hs_off[sl + 1]; ++k) {
+  const int k0 = hs_off[sl], k1 = hs_off[sl + 1];
+  // 4 element blocks per step, all loads issued before the adds (same order)
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    double v[4][9];
+    bool tr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = hs_val[k + u];
+      const int t = e >> 4, a = (e >> 2) & 3, b = e & 3;
+      tr[u] = a > b;
+      const double* blk = hbuf + 90 * (int64_t)t + 9 * (tr[u] ? pair_index(b, a) : pair_index(a, b));
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[u][q] = blk[q];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!tr[u]) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += v[u][q];
+      } else {
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[3 * r + c] += v[u][3 * c + r];
+      }
+    }
+  }
+  for (; k < k1; ++k) {
     const int e = hs_val[k];
     const int t = e >> 4, a = (e >> 2) & 3, b = e & 3;
     if (a <= b) {

@@ -246,7 +246,18 @@ static void mas_build(mp_ctx* c) {
 static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
   timer_begin(c, MP_STAGE_HESSIAN);
   copy_table(c, c->cur, c->base);
-  build_inc(c, c->inc_base, c->base.verts, c->base.count);
+  if (c->inc_cur_rows == c->cur.count && c->cur.count > 0) {
+    // base == cur row for row: its incidence CSR is cur's
+    const size_t m = 4 * (size_t)c->cur.count;
+    c->inc_base.off.ensure(c->N + 1);
+    c->inc_base.val2.ensure(m);
+    CUDA_CHECK(cudaMemcpyAsync(c->inc_base.off.p, c->inc_cur.off.p, sizeof(int) * (c->N + 1),
+                               cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(c->inc_base.val2.p, c->inc_cur.val2.p, sizeof(int) * m, cudaMemcpyDeviceToDevice,
+                               c->stream));
+  } else {
+    build_inc(c, c->inc_base, c->base.verts, c->base.count);
+  }
   assemble_elastic_bsr(c, x, h);
   timer_end(c, MP_STAGE_HESSIAN, hessian_bytes(c));
   c->have_snapshot = true;
