@@ -216,9 +216,10 @@ int mp_stage_timing(mp_ctx* ctx, int enable);
  * streaming loads, one CTA per subdomain; 1 TMA bulk staging; 0 per-thread
  * cp.async staging; MP_OPT_APPLY_STAGES (2 or 3) and
  * MP_OPT_APPLY_CTAS (persistent CTAs per SM) tune its pipeline; same results.
- * MP_OPT_BP_FUSED: constraint-set / CCD / certificate pair work fused into
- * the grid enumeration (1, default) or over a stored pair list (0); same
- * results. */
+ * MP_OPT_BP_FUSED: broad-phase enumeration for the constraint set, CCD and
+ * certificate -- 1 (default) one-pass unordered pair lists, 2 constraint-set
+ * pair work fused into the grid queries, 0 ordered count/scan/fill lists;
+ * same results. */
 enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3, MP_OPT_APPLY_STAGES = 4,
        MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6 };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);

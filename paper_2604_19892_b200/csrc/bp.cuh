@@ -1046,9 +1046,12 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
   // fused for the constraint set only: the CCD / certificate pair work needs
   // ~100 registers, and inlined into the enumeration it costs more occupancy
   // than the count pass it saves (measured: 362 vs 264 us per edge pass)
-  const bool fused = c->bp_fused && MODE == BP_CONTACT && which == 3 && !n_pt_out;
-  // CCD / certificate without a stored per-pair output: one-pass unordered list
-  const bool append = c->bp_fused && (MODE == BP_CCD || MODE == BP_CERT) && which == 3 && !n_pt_out && !O.verts;
+  const bool fused = c->bp_fused == 2 && MODE == BP_CONTACT && which == 3 && !n_pt_out;
+  // order-free consumers (contacts are key-sorted afterwards; CCD / the
+  // certificate reduce minima and flags) without a stored per-pair output:
+  // one-pass unordered list, then the pair kernel
+  const bool append = c->bp_fused == 1 && MODE != BP_RAW && which == 3 && !n_pt_out &&
+                      !(MODE == BP_CCD && O.verts);
   for (int attempt = 0; attempt < 3; ++attempt) {
     CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
     O.counter = c->counters.p;
@@ -1101,7 +1104,7 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
         continue;
       }
       if (flag) *flag = c->h_cnt[1];
-      return n_pt + n_ee;
+      return MODE == BP_CONTACT ? c->h_cnt[0] : n_pt + n_ee;  // CONTACT: constraints emitted
     }
     collect_pairs(c, x, B, which);
     const int64_t cap = (int64_t)std::min(g.pa.n, g.pb.n);

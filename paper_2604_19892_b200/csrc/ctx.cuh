@@ -142,7 +142,7 @@ struct mp_ctx {
   int apply_mode = 2;        // level-0 apply: 2 direct loads, 1 TMA-staged, 0 cp.async-staged
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
-  bool bp_fused = true;      // pair work fused into the grid enumeration
+  int bp_fused = 1;          // 1: one-pass unordered pair lists, 2: contact work fused into the queries, 0: ordered lists
   StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;

@@ -669,7 +669,7 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_RECORD_ENERGY) c->record_energy = value != 0;
     else if (option == MP_OPT_APPLY_TMA) c->apply_mode = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (option == MP_OPT_APPLY_STAGES) c->apply_stages = value == 3 ? 3 : 2;
-    else if (option == MP_OPT_BP_FUSED) c->bp_fused = value != 0;
+    else if (option == MP_OPT_BP_FUSED) c->bp_fused = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (option == MP_OPT_APPLY_CTAS) c->apply_ctas_per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, value));
     else throw MpError(MP_ERR_CONFIG, "unknown option");
   });

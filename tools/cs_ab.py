@@ -11,7 +11,7 @@ from paper_2604_19892_b200 import scenes, solver  # noqa: E402
 scene = scenes.c2_stack(gap=5e-3)
 ctx = scene.context(solver.SolverConfig())
 x = np.load("tools/_data/ccd_state.npz")["x"]
-for fused in (1, 0, 1, 0):
+for fused in (1, 2, 0, 1, 2):
     ctx.set_option(6, fused)
     for _ in range(3):
         ctx.constraint_set(x)
