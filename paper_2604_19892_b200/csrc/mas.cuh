@@ -459,7 +459,9 @@ k_block_sweep(int kb, const double* __restrict__ A, int lda, int k0, double* __r
   __shared__ double swsm[SWEEP_SMEM];
   const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
   double R[SWEEP_T][SWEEP_T];
-  auto load = [&](int i, int j) -> double { return __ldg(A + (int64_t)(k0 + j) * lda + k0 + i); };
+  // the pivot block is symmetric (to rounding of the lookahead GEMM): read
+  // it row-major so a warp's 16-column lanes load contiguous doubles
+  auto load = [&](int i, int j) -> double { return __ldg(A + (int64_t)(k0 + i) * lda + k0 + j); };
   if (!sweep_blocked(load, kb, swsm, R)) {
     if (threadIdx.x == 0) atomicExch(status, 1);
     return;
