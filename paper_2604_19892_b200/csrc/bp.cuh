@@ -1096,6 +1096,8 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
       }
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      if (c->rb_extra)  // the caller's scalar rides on this readback (h_scal[0])
+        CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       sync_stream(c);
       const int64_t n_pt = c->h_cnt[5], n_ee = c->h_cnt[6];
       if (n_pt > cap_pt || n_ee > cap_ee) {  // grow and rerun (minima / flags are idempotent)
@@ -1118,6 +1120,8 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
     CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, g.qoff.p + V + F, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 6, g.qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (c->rb_extra)
+      CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     sync_stream(c);
     const int64_t n_pt = c->h_cnt[5], n = c->h_cnt[6];
     if (n > cap) {  // the list did not fit: grow and rerun (results are idempotent)

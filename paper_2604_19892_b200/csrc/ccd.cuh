@@ -318,7 +318,9 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       }
       O.alpha_d = c->alpha_d;
       O.min_alpha = d_min;
+      c->rb_extra = d_min;  // read back with run_bp's counters: no extra sync
       int64_t n = run_bp<BP_CCD>(c, x, B, O, CP, CC, &cert_fail_p);
+      c->rb_extra = nullptr;
       if (!exact_set || n <= O.cap) {
         R.n_pairs = n;
         break;
@@ -331,8 +333,6 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       LAUNCH_CHECK();
       if (attempt == 3) throw MpError(MP_ERR_CAPACITY, "ccd pair capacity retry failed");
     }
-    CUDA_CHECK(cudaMemcpyAsync(c->h_scal, d_min, sizeof(double), cudaMemcpyDeviceToHost, st));
-    sync_stream(c);
     R.min_alpha = c->h_scal[0];
     if (per_subdomain && R.n_pairs > 0) {
       if (R.min_alpha == 1.0) {

@@ -258,6 +258,7 @@ struct mp_ctx {
   double* h_scal = nullptr;
   int* h_cnt = nullptr;
   unsigned long long* h_npairs = nullptr;  // = h_scal[63]
+  const double* rb_extra = nullptr;        // device scalar run_bp reads back into h_scal[0]
   DBuf<unsigned long long> n_pairs_dev;    // fused enumeration pair count
 
   ~mp_ctx();
