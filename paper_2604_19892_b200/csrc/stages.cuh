@@ -182,18 +182,22 @@ static void mas_build(mp_ctx* c) {
     cudaStream_t st = L.st;
     if (l == 0) {
       CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_bsr, 0));
+      if (nc) {
+        // contact terms on the level's second stream, beside the BSR gather
+        CUDA_CHECK(cudaStreamWaitEvent(L.st2, c->ev_bsr, 0));
+        L.fx_acc.zero(2 * (size_t)L.n * L.n, L.st2);
+        k_contact_coarse<<<grid_for(nc, 128), 128, 0, L.st2>>>(nc, c->base.verts, c->base.grad, c->base.k, c->N,
+                                                               L.span, L.n, c->fx_scale, L.fx_acc);
+        LAUNCH_CHECK();
+        CUDA_CHECK(cudaEventRecord(L.ev_w, L.st2));
+      }
       L.dense.zero((size_t)L.n * L.n, st);
       if (L.nblk) {
         k_coarse_gather<<<grid_for(32 * (int64_t)L.nblk, 128), 128, 0, st>>>(L.nblk, L.cb_key, L.cb_off, L.cb_slot,
                                                                              c->bsr, L.A, c->N, L.span, L.n, L.dense);
         LAUNCH_CHECK();
       }
-      if (nc) {
-        L.fx_acc.zero(2 * (size_t)L.n * L.n, st);
-        k_contact_coarse<<<grid_for(nc, 128), 128, 0, st>>>(nc, c->base.verts, c->base.grad, c->base.k, c->N,
-                                                            L.span, L.n, c->fx_scale, L.fx_acc);
-        LAUNCH_CHECK();
-      }
+      if (nc) CUDA_CHECK(cudaStreamWaitEvent(st, L.ev_w, 0));
       k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense, nc ? L.fx_acc.p : nullptr,
                                                                      c->fx_scale.p);
     } else {
