@@ -113,7 +113,13 @@ struct CoarseLevel {
   cudaStream_t st = nullptr, st2 = nullptr;
   cudaEvent_t done = nullptr, ev_w = nullptr, ev_u = nullptr, ev_asm = nullptr;
   cublasHandle_t blas = nullptr;
+  // the blocked inverse as a CUDA graph (stages.cuh dense_spd_inverse)
+  cudaGraphExec_t graph = nullptr;
+  const void* graph_key[7] = {};
+  int64_t graph_launches = 0;
+  bool graph_failed = false;
   ~CoarseLevel() {
+    if (graph) cudaGraphExecDestroy(graph);
     if (blas) cublasDestroy(blas);
     for (cudaEvent_t e : {done, ev_w, ev_u, ev_asm})
       if (e) cudaEventDestroy(e);

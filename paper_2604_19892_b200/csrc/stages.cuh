@@ -101,15 +101,11 @@ static int read_status(mp_ctx* c, int* dev) {
 //   W = A[:,K] P^-1 (DGEMM), A -= W A[:,K]^T (rank-96 DGEMM update),
 //   A[:,K] = A[K,:]^T = W, A[K,K] = -P^-1 (k_block_fix);
 // after every block A = -M^-1.  cuBLAS DGEMM carries the O(n^3) work.
-static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
+static void dense_spd_inverse_enqueue(mp_ctx* c, CoarseLevel& L, int* status) {
   const int nb = 96;
   const int n = L.n;
   double* A = L.dense;
   cudaStream_t st = L.st, st2 = L.st2;
-  L.dn_col.ensure((size_t)n * nb);
-  L.dn_W.ensure((size_t)n * nb);
-  L.dn_P.ensure(2 * (size_t)nb * nb);
-  L.dn_Pn.ensure((size_t)nb * nb);
   const double one = 1.0, mone = -1.0, zero = 0.0;
   auto gemm = [&](cudaStream_t s, cublasOperation_t tb, int mm, int nn, int kk, const double* alpha,
                   const double* Am, int lda, const double* Bm, int ldb, const double* beta, double* Cm, int ldc,
@@ -118,7 +114,7 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
     if (cublasDgemm(L.blas, CUBLAS_OP_N, tb, mm, nn, kk, alpha, Am, lda, Bm, ldb, beta, Cm, ldc) !=
         CUBLAS_STATUS_SUCCESS)
       throw MpError(MP_ERR_CUDA, what);
-    ++c->launches;
+    if (g_launch_counter) ++(*g_launch_counter);
   };
   // Lookahead: the next pivot block is updated first (a kb x kb x kb GEMM)
   // and swept on st while the rank-kb update of the whole matrix runs on st2.
@@ -159,6 +155,61 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   cublasSetStream(L.blas, st);
   k_pack_neg_sym<<<grid_for(cyc_size(n), 256), 256, 0, st>>>(n, A, L.inv);
   LAUNCH_CHECK();
+}
+
+// The blocked inverse is ~150 dependent launches and cuBLAS calls across two
+// streams per level -- enough host work to starve the GPU.  It is captured
+// once into a CUDA graph (re-captured if a buffer moved) and replayed with
+// one launch: the same kernels in the same order, so the same bits.
+static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
+  const int nb = 96;
+  const int n = L.n;
+  L.dn_col.ensure((size_t)n * nb);
+  L.dn_W.ensure((size_t)n * nb);
+  L.dn_P.ensure(2 * (size_t)nb * nb);
+  L.dn_Pn.ensure((size_t)nb * nb);
+  L.inv.ensure((size_t)cyc_size(n));
+  static const bool no_graph = getenv("MP_NO_COARSE_GRAPH") != nullptr;
+  if (no_graph || L.graph_failed) {
+    dense_spd_inverse_enqueue(c, L, status);
+    return;
+  }
+  const void* key[7] = {L.dense.p, L.dn_col.p, L.dn_W.p, L.dn_P.p, L.dn_Pn.p, L.inv.p, status};
+  bool same = L.graph != nullptr;
+  for (int q = 0; q < 7 && same; ++q) same = L.graph_key[q] == key[q];
+  if (!same) {
+    if (L.graph) {
+      cudaGraphExecDestroy(L.graph);
+      L.graph = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    int64_t* saved = g_launch_counter;
+    int64_t counted = 0;
+    g_launch_counter = &counted;
+    bool ok = cudaStreamBeginCapture(L.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        dense_spd_inverse_enqueue(c, L, status);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(L.st, &g) == cudaSuccess) && ok && g;
+    }
+    g_launch_counter = saved;
+    if (ok) ok = cudaGraphInstantiate(&L.graph, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {  // capture unsupported here: enqueue directly from now on
+      cudaGetLastError();
+      L.graph = nullptr;
+      L.graph_failed = true;
+      dense_spd_inverse_enqueue(c, L, status);
+      return;
+    }
+    for (int q = 0; q < 7; ++q) L.graph_key[q] = key[q];
+    L.graph_launches = counted;
+  }
+  CUDA_CHECK(cudaGraphLaunch(L.graph, L.st));
+  if (g_launch_counter) *g_launch_counter += L.graph_launches;
 }
 
 // build_hierarchy (mas.py:138-179) from the BSR + base contacts
