@@ -1,0 +1,58 @@
+"""Selectable implementation variants give the same bits.
+
+- MP_OPT_BP_FUSED (6): broad-phase enumeration for the constraint set, CCD
+  and certificate -- 1 one-pass unordered pair lists (default), 2 constraint-
+  set pair work fused into the grid queries, 0 ordered count/scan/fill lists.
+  All consumers are order-free (minima, flags, key-sorted contacts), so the
+  constraint set, alpha_d, the certificate and x_new must be bit-identical.
+- MP_OPT_APPLY_TMA (3): level-0 MAS apply -- 2 direct streaming loads
+  (default), 1 TMA-staged, 0 cp.async-staged: the same sums in the same
+  order, so z must be bit-identical.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_config, golden_taps, load_golden, scene_from_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["stacked_k256", "locking"])
+def test_broad_phase_modes_same_bits(name):
+    g = load_golden(name)
+    scene = scene_from_golden(g)
+    ctx = scene.context(golden_config(g))
+    rng = np.random.default_rng(3)
+    cases = [(t["x"], t["p"]) for t in golden_taps(g, "ccd")]
+    for x, p in list(cases):
+        cases.append((x, 4.0 * p + 0.5 * np.abs(p).max() * rng.standard_normal(p.shape)))
+    for x, p in cases:
+        out = []
+        for mode in (1, 2, 0):
+            ctx.set_option(6, mode)
+            cs = ctx.constraint_set(x)
+            ad, xn, ma, cert, n = ctx.ccd(x, p, exact_set=False)
+            out.append((cs, ad, xn, ma, cert, n))
+        ctx.set_option(6, 1)
+        ref = out[0]
+        for o in out[1:]:
+            for a, b in zip(ref[0], o[0]):
+                assert np.array_equal(np.asarray(a), np.asarray(b))
+            assert np.array_equal(ref[1], o[1]) and np.array_equal(ref[2], o[2])
+            assert ref[3] == o[3] and ref[4] == o[4] and ref[5] == o[5]
+
+
+def test_apply_modes_same_bits():
+    g = load_golden("stacked_k256")
+    scene = scene_from_golden(g)
+    ctx = scene.context(golden_config(g))
+    x = g["rest"].ravel().copy()
+    ctx.snapshot(x, float(g["h"]), build_mas=True)
+    r = np.random.default_rng(5).standard_normal(x.size)
+    zs = []
+    for mode in (2, 1, 0):
+        ctx.set_option(3, mode)
+        zs.append(ctx.precond_apply(r))
+    ctx.set_option(3, 2)
+    assert np.array_equal(zs[0], zs[1]) and np.array_equal(zs[0], zs[2])
