@@ -10,6 +10,10 @@ Configs (BASELINE.json ``configs``):
 * ``c1_cube``  -- floor slab + soft SNH cube ``cells^3`` (8^3: 737 V, 3,078 T)
 * ``c2_stack`` -- floor + 8 cubes (17^3 cells each) stacked 2x2x2 with 1e-3 gaps
   (46,664 V, 235,830 T), SNH E=1e5, d_hat=2e-3, kappa=1e4, h=0.01
+* ``c3_rod``   -- twisting soft SNH rod (8 x 8 x 2500 cells; 202,589 V / 960,006 T with the floor
+  at full size) released above a pinned floor with a linear twist-rate
+  field (``c3_rod_v0``): opposite ends spin in opposite senses, so the rod
+  winds up and presses on itself; SURVEY.md 8.0 C3
 * small reference-shaped scenes used by the golden fixtures: ``drop``
   (scenes/drop.ini), ``stacked_boxes`` (test_acceptance.py:369-388),
   ``locking`` (test_acceptance.py:488-499).
@@ -134,10 +138,38 @@ def c2_stack(cells=17, young=1e5, gap=1e-3, mods=None):
     return build_scene(objs, d_hat=2e-3, kappa=1e4, mods=mods)
 
 
+def c3_rod(cells=(2500, 8, 8), length=6.25, width=0.02, young=1e5, gap=2e-3, mods=None):
+    """Config 3 surrogate: a soft SNH rod along x (cells = (nx, ny, nz)) held
+    gap above a pinned floor; pair with ``c3_rod_v0`` for the twist."""
+    geo, _, _ = _mods(mods)
+    nx, ny, nz = cells
+    rod = geo.make_box_mesh(nx, ny, nz, (length, width, width))
+    objs = [floor((length + 0.4, 0.4, 0.1), mods),
+            {"mesh": rod, "translate": (-0.5 * length, -0.5 * width, gap), "material": "snh", "young": young,
+             "poisson": 0.3, "density": 1000.0}]
+    return build_scene(objs, d_hat=2e-3, kappa=1e4, mods=mods)
+
+
+def c3_rod_v0(scene, omega=20.0):
+    """Twist field: angular velocity about the rod axis varying linearly from
+    -omega at one end to +omega at the other; the pinned floor stays at rest."""
+    x = scene.mesh.rest_positions
+    rod = ~np.asarray(scene.dirichlet, dtype=bool)
+    xr = x[rod]
+    lo, hi = xr.min(axis=0), xr.max(axis=0)
+    c = 0.5 * (lo + hi)
+    w = omega * (2.0 * (xr[:, 0] - lo[0]) / max(hi[0] - lo[0], 1e-30) - 1.0)
+    v = np.zeros_like(x)
+    v[rod, 1] = -w * (xr[:, 2] - c[2])
+    v[rod, 2] = w * (xr[:, 1] - c[1])
+    return v.ravel()
+
+
 SCENES = {
     "drop": drop,
     "stacked_boxes": stacked_boxes,
     "locking": locking,
     "c1_cube": c1_cube,
     "c2_stack": c2_stack,
+    "c3_rod": c3_rod,
 }
