@@ -461,6 +461,7 @@ struct PairArgs {
   // append enumeration (HQ_APPEND): this class's list and its counter
   int *app_a, *app_b, *app_cnt;
   int64_t app_cap;
+  int app_ee;  // app_cnt is counters[9] (EE) rather than [8] (PT): the overflow flag sits at counters[10]
 };
 
 template <int MODE>
@@ -606,10 +607,19 @@ __device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, c
 // order-free CCD / certificate consumers, it saves the count pass.
 enum { HQ_APPEND = -3, HQ_COUNT = -2, HQ_FILL = -1 };
 
+// The 32-bit append counter must not wrap: past HQ_APPEND_LIMIT reservations
+// a warp raises app_cnt[2] and stops writing; the host then reruns the call in
+// the list-free fused mode (64-bit pair count).  Every slot below the limit
+// was written before any warp reached it, so the list stays memory-safe.
+#define HQ_APPEND_LIMIT (1 << 30)
 __device__ __forceinline__ void hq_append_flush(int lane, int k, const int2* q, const PairArgs& A) {
   int base = 0;
-  if (lane == 0) base = atomicAdd(A.app_cnt, k);
+  if (lane == 0) {
+    base = atomicAdd(A.app_cnt, k);
+    if (base < 0 || base > HQ_APPEND_LIMIT - k) atomicExch(A.app_cnt + (A.app_ee ? 1 : 2), 1);
+  }
   base = __shfl_sync(WARP_FULL, base, 0);
+  if (base < 0 || base > HQ_APPEND_LIMIT - k) return;
   if (lane < k && (int64_t)base + lane < A.app_cap) {
     const int2 pr = q[lane];
     A.app_a[base + lane] = pr.x;
@@ -1072,7 +1082,7 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
       if (g.pa.n < 1024) { g.pa.ensure(1 << 16); g.pb.ensure(1 << 16); }
       if (g.ea.n < 1024) { g.ea.ensure(1 << 16); g.eb.ensure(1 << 16); }
       int* cnt = c->counters.p + 8;  // [8] PT, [9] EE appended
-      CUDA_CHECK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c->stream));
+      CUDA_CHECK(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), c->stream));  // [10]: append overflow flag
       const int64_t cap_pt = (int64_t)std::min(g.pa.n, g.pb.n), cap_ee = (int64_t)std::min(g.ea.n, g.eb.n);
       if (!B.empty) {
         PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr, g.pa, g.pb, cnt, cap_pt};
@@ -1086,7 +1096,7 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
         }
         if (E > 1) {
           PairArgs Ae = A;
-          Ae.app_a = g.ea; Ae.app_b = g.eb; Ae.app_cnt = cnt + 1; Ae.app_cap = cap_ee;
+          Ae.app_a = g.ea; Ae.app_b = g.eb; Ae.app_cnt = cnt + 1; Ae.app_cap = cap_ee; Ae.app_ee = 1;
           k_hq_edges<HQ_APPEND><<<grid_for(32 * E, 128), 128, 0, c->stream>>>(B.T, E, c->edge, nullptr, nullptr,
                                                                               nullptr, nullptr, 0, Ae);
           LAUNCH_CHECK();
@@ -1095,10 +1105,23 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
         LAUNCH_CHECK();
       }
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       if (c->rb_extra)  // the caller's scalar rides on this readback (h_scal[0])
         CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       sync_stream(c);
+      if (c->h_cnt[7]) {  // >= 2^30 candidate pairs: no list; rerun list-free with a 64-bit count
+        CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), c->stream));
+        c->n_pairs_dev.ensure(1);
+        CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), c->stream));
+        PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, c->n_pairs_dev.p, nullptr, nullptr, nullptr, 0};
+        fused_pairs<MODE>(c, x, B, A);
+        CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        sync_stream(c);
+        if (flag) *flag = c->h_cnt[1];
+        return MODE == BP_CONTACT ? c->h_cnt[0] : (int64_t)*c->h_npairs;
+      }
       const int64_t n_pt = c->h_cnt[5], n_ee = c->h_cnt[6];
       if (n_pt > cap_pt || n_ee > cap_ee) {  // grow and rerun (minima / flags are idempotent)
         if (n_pt > cap_pt) { g.pa.ensure((size_t)(n_pt * 1.25) + 1024); g.pb.ensure((size_t)(n_pt * 1.25) + 1024); }

@@ -14,7 +14,8 @@ from paper_2604_19892_b200 import scenes, solver  # noqa: E402
 
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 iter_max = int(sys.argv[2]) if len(sys.argv) > 2 else 200
-scene = scenes.c3_rod()
+nx = int(sys.argv[3]) if len(sys.argv) > 3 else 2500
+scene = scenes.c3_rod(cells=(nx, 8, 8), length=6.25 * nx / 2500)
 cfg = solver.SolverConfig(iter_max=iter_max)
 ctx = scene.context(cfg, device=0)
 x0 = scene.mesh.rest_positions.ravel().copy()
@@ -34,5 +35,5 @@ for f in range(frames):
     ms = e0.elapsed_time(e1)
     out.append({"frame": f, "iters": len(recs), "ms": round(ms, 3), "iters_per_s": round(len(recs) / ms * 1e3, 1),
                 "converged": bool(conv)})
-print(json.dumps({"workload": "c3_rod 8x8x2500 cells SNH, omega=20 rad/s twist, h=0.01", "iter_max": iter_max,
+print(json.dumps({"workload": f"c3_rod 8x8x{nx} cells SNH, omega=20 rad/s twist, h=0.01", "iter_max": iter_max,
                   "frames": out}))
