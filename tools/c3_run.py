@@ -4,6 +4,7 @@ flushed between frames.  Not the bench headline (bench.py measures C2);
 a sizing/throughput probe for the next row of SURVEY.md 8."""
 
 import json
+import os
 import sys
 
 import numpy as np
@@ -16,7 +17,7 @@ frames = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 iter_max = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 nx = int(sys.argv[3]) if len(sys.argv) > 3 else 2500
 scene = scenes.c3_rod(cells=(nx, 8, 8), length=6.25 * nx / 2500)
-cfg = solver.SolverConfig(iter_max=iter_max)
+cfg = solver.SolverConfig(iter_max=iter_max, **json.loads(os.environ.get("C3_CFG", "{}")))
 ctx = scene.context(cfg, device=0)
 x0 = scene.mesh.rest_positions.ravel().copy()
 ctx.set_state(x0, scenes.c3_rod_v0(scene))
