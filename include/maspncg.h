@@ -101,7 +101,7 @@ typedef struct mp_iter_record {
   double t_dir_ms;
   double t_ccd_ms;
   int32_t n_candidates;    /* rank-one update candidates (non-rebuild)    */
-  int32_t n_ccd_pairs;     /* CCD candidate pairs enumerated              */
+  int32_t n_ccd_pairs;     /* CCD candidate pairs enumerated (saturates at INT32_MAX) */
   int32_t ccd_certified;   /* certify_mixed outcome (1 = mixed step kept) */
   int32_t pad_;
   double energy;           /* incremental potential at the iterate (NaN unless enabled) */
@@ -183,6 +183,12 @@ int mp_ccd(mp_ctx* ctx, const double* x, const double* p, double* alpha_d,
  * (a0,a1,b0,b1), original ids, unordered. */
 int mp_ccd_pairs(mp_ctx* ctx, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt, double* alpha);
 
+/* The assembled Galerkin matrix M_l = C_l H C_l^T (mas.py:155-168) of coarse
+ * level `level` (1-based) as it entered the last build's factorisation,
+ * row-major n x n; needs MP_OPT_KEEP_COARSE set before that build.  Pass
+ * out = NULL to query n. */
+int mp_coarse_matrix(mp_ctx* ctx, int level, double* out, int64_t cap, int64_t* n);
+
 /* Number of kernels this context has launched since creation. */
 int64_t mp_launch_count(mp_ctx* ctx);
 
@@ -221,12 +227,19 @@ int mp_stage_timing(mp_ctx* ctx, int enable);
  * pair work fused into the grid queries, 0 ordered count/scan/fill lists;
  * same results. */
 enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3, MP_OPT_APPLY_STAGES = 4,
-       MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6 };
+       MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6, MP_OPT_KEEP_COARSE = 7,
+       MP_OPT_APPEND_LIMIT = 8 /* test knob: process-wide one-pass list limit (default and max 2^30; <= 0 resets) */ };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 
 /* Message of the last failed mp_create on this thread. */
 const char* mp_create_error(void);
+
+/* The coarse-level dense inverse (mas.py:84-90 `_spd_inverse` as used at
+ * mas.py:167) on `device`, standalone: inv (n x n, row-major) = sym(A^-1)
+ * of the symmetric n x n row-major A; *not_spd = 1 (and inv undefined) where
+ * cho_factor would raise non-spd-subdomain.  Test / parity entry point. */
+int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t* not_spd);
 
 /* mas.partition_domain (mas.py:63-77) on the host, no GPU needed:
  * subdomain_of (n,) for a Morton partition into blocks of block_size. */

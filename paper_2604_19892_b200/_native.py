@@ -54,7 +54,7 @@ class IterRecordC(C.Structure):
 EXPORTS = (
     "mp_create", "mp_destroy", "mp_set_config", "mp_status_code", "mp_last_error", "mp_stream", "mp_partition",
     "mp_step", "mp_advance", "mp_broad_phase", "mp_constraint_set", "mp_gradient", "mp_energy", "mp_snapshot",
-    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
+    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_coarse_matrix", "mp_spd_inverse", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
 )
 
 STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd", "mas_apply_l0",
@@ -89,6 +89,7 @@ def load_library():
     lib.mp_launch_count.restype = C.c_int64
     lib.mp_partition.argtypes = [vp, _i64p, _i64p]
     lib.mp_partition_host.argtypes = [_f64p, C.c_int64, C.c_int32, _i64p]
+    lib.mp_spd_inverse.argtypes = [C.c_int, C.c_int64, _f64p, _f64p, C.POINTER(C.c_int32)]
     rec = C.POINTER(IterRecordC)
     step_tail = [_f64p, _f64p, rec, C.c_int64, _i64p, C.POINTER(C.c_int32), C.POINTER(C.c_uint32)]
     lib.mp_step.argtypes = [vp, _f64p, _f64p, C.c_double] + step_tail
@@ -108,6 +109,7 @@ def load_library():
     lib.mp_precond_apply.argtypes = [vp, _f64p, C.c_int, _f64p]
     lib.mp_update_at.argtypes = [vp, _f64p, _i64p, _i64p]
     lib.mp_ccd.argtypes = [vp, _f64p, _f64p, _f64p, _f64p, _f64p, C.POINTER(C.c_int32), _i64p, C.c_int32]
+    lib.mp_coarse_matrix.argtypes = [vp, C.c_int, _f64p, C.c_int64, _i64p]
     lib.mp_stage_timing.argtypes = [vp, C.c_int]
     lib.mp_set_option.argtypes = [vp, C.c_int, C.c_int64]
     lib.mp_stage_stats.argtypes = [vp, C.c_int, _f64p, _i64p, _f64p]
@@ -138,6 +140,19 @@ def partition_host(rest, block_size):
     out = np.zeros(len(rest), dtype=np.int64)
     raise_status(lib.mp_partition_host(_ptr(rest), len(rest), int(block_size), _ptr(out, C.c_int64)), "")
     return out
+
+
+def spd_inverse(A, device=0):
+    """The device coarse-level inverse (mas.py:84-90) of a dense symmetric
+    matrix: (sym(A^-1), not_spd)."""
+    lib = load_library()
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    out = np.empty((n, n))
+    flag = C.c_int32()
+    st = lib.mp_spd_inverse(int(device), n, _ptr(A), _ptr(out), C.byref(flag))
+    raise_status(st, "mp_spd_inverse failed")
+    return out, bool(flag.value)
 
 
 class NativeContext:
@@ -249,7 +264,7 @@ class NativeContext:
 
     def set_option(self, option, value):
         """MP_OPT_* of include/maspncg.h (CCD_EXACT_SET 1, RECORD_ENERGY 2, APPLY_TMA 3,
-        APPLY_STAGES 4, APPLY_CTAS 5, BP_FUSED 6)."""
+        APPLY_STAGES 4, APPLY_CTAS 5, BP_FUSED 6, KEEP_COARSE 7)."""
         self._check(self.lib.mp_set_option(self.h, int(option), int(value)))
 
     # ---- per-stage CUDA-event timing ----
@@ -329,6 +344,15 @@ class NativeContext:
         self._check(self.lib.mp_ccd(self.h, _ptr(self._vec(x)), _ptr(self._vec(p)), _ptr(alpha_d), _ptr(x_new),
                                     C.byref(ma), C.byref(cert), C.byref(npairs), int(bool(exact_set))))
         return alpha_d, x_new, ma.value, bool(cert.value), npairs.value
+
+    def coarse_matrix(self, level):
+        """Assembled Galerkin matrix of coarse level `level` (1-based) of the
+        last MAS build (set_option(MP_OPT_KEEP_COARSE=7, 1) before it)."""
+        n = C.c_int64()
+        self._check(self.lib.mp_coarse_matrix(self.h, int(level), None, 0, C.byref(n)))
+        out = np.empty((n.value, n.value))
+        self._check(self.lib.mp_coarse_matrix(self.h, int(level), _ptr(out), out.size, C.byref(n)))
+        return out
 
     def ccd_pairs(self):
         """(verts (Q,4) original ids, is_pt (Q,), alpha_pair (Q,)) of the last CCD."""

@@ -2,9 +2,8 @@
 
     python -m paper_2604_19892_b200.build_native
 
-One nvcc invocation: csrc/maspncg.cu (unity build) -> libmaspncg.so, linked
-against cuSOLVER (coarse-level dense factorisations) with the CUDA runtime
-static.  -lineinfo keeps ncu's source view mapped to our code.
+One nvcc invocation: csrc/maspncg.cu (unity build) -> libmaspncg.so with the
+CUDA runtime static.  -lineinfo keeps ncu's source view mapped to our code.
 """
 
 from __future__ import annotations
@@ -41,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         "-Xptxas", "-v" if verbose else "-O3",
         "-I", str(PKG.parent / "include"),
         "-o", str(LIB) + ".tmp", str(CSRC / "maspncg.cu"),
-        "-L", str(CUDA_HOME / "lib64"), "-lcusolver", "-lcublas", "-lcublasLt",
+        "-L", str(CUDA_HOME / "lib64"),
         "-Xlinker", f"-rpath,{CUDA_HOME / 'lib64'}",
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(256) k_pairs_app(const int* __restrict__ cnt, 
                                                    const int* __restrict__ pa, const int* __restrict__ pb,
                                                    const int* __restrict__ ea, const int* __restrict__ eb,
                                                    PairArgs A) {
+  if (cnt[2]) return;  // append counter hit HQ_APPEND_LIMIT: the list is partial, the caller reruns list-free
   const int64_t n_pt = cnt[0] < cap_pt ? cnt[0] : cap_pt;  // overflow: the caller grows and reruns
   const int64_t n_ee = cnt[1] < cap_ee ? cnt[1] : cap_ee;
   const int64_t n = n_pt + n_ee;
@@ -612,14 +613,18 @@ enum { HQ_APPEND = -3, HQ_COUNT = -2, HQ_FILL = -1 };
 // the list-free fused mode (64-bit pair count).  Every slot below the limit
 // was written before any warp reached it, so the list stays memory-safe.
 #define HQ_APPEND_LIMIT (1 << 30)
+// the limit the kernels apply (MP_OPT_APPEND_LIMIT lowers it so small scenes
+// exercise the list-free rerun in tests)
+__device__ int g_append_limit = HQ_APPEND_LIMIT;
 __device__ __forceinline__ void hq_append_flush(int lane, int k, const int2* q, const PairArgs& A) {
   int base = 0;
+  const int lim = g_append_limit;
   if (lane == 0) {
     base = atomicAdd(A.app_cnt, k);
-    if (base < 0 || base > HQ_APPEND_LIMIT - k) atomicExch(A.app_cnt + (A.app_ee ? 1 : 2), 1);
+    if (base < 0 || base > lim - k) atomicExch(A.app_cnt + (A.app_ee ? 1 : 2), 1);
   }
   base = __shfl_sync(WARP_FULL, base, 0);
-  if (base < 0 || base > HQ_APPEND_LIMIT - k) return;
+  if (base < 0 || base > lim - k) return;
   if (lane < k && (int64_t)base + lane < A.app_cap) {
     const int2 pr = q[lane];
     A.app_a[base + lane] = pr.x;
@@ -969,6 +974,17 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   return B;
 }
 
+// 64-bit sum of the per-query pair counts of the ordered list (each count is
+// a 32-bit non-negative int; their int32 scan wraps past 2^31 pairs)
+__global__ void k_sum_counts(int64_t n, const int* __restrict__ cnt, unsigned long long* __restrict__ total) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += (unsigned)cnt[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(total, s);
+}
+
 // The reference pair list of the grid (PT if which & 1, EE if which & 2):
 // count pass, exclusive scan, fill pass into the current capacity -- no host
 // sync; the counts stay on the device (qoff[V+F] = PT pairs, qoff[V+F+E] =
@@ -1004,6 +1020,12 @@ static void collect_pairs(mp_ctx* c, const double* x, const BpGrid& B, int which
                                                                  nullptr, 0, PairArgs{});
     LAUNCH_CHECK();
   }
+  // the int32 scan below must not wrap: a 64-bit total of the counts rides
+  // on the caller's readback (h_npairs) and is checked before the list is used
+  c->n_pairs_dev.ensure(1);
+  CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), st));
+  k_sum_counts<<<148, 256, 0, st>>>(nq, g.qcnt.p, c->n_pairs_dev.p);
+  LAUNCH_CHECK();
   exclusive_scan(c, g.qcnt, g.qoff, nq + 1);
   if ((which & 1) && V) {
     k_hq_points<HQ_FILL><<<grid_for(32 * V, 128), 128, 0, st>>>(B.T, V, c->sverts, c->tri, x, nullptr, g.qoff.p, g.pa,
@@ -1074,6 +1096,8 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                  c->stream));
+      if (c->rb_extra)
+        CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       sync_stream(c);
       if (flag) *flag = c->h_cnt[1];
       return MODE == BP_CONTACT ? c->h_cnt[0] : (int64_t)*c->h_npairs;
@@ -1118,6 +1142,8 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
         CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                    c->stream));
+        if (c->rb_extra)  // the caller's scalar (CCD minimum) as recomputed by this full pass
+          CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         sync_stream(c);
         if (flag) *flag = c->h_cnt[1];
         return MODE == BP_CONTACT ? c->h_cnt[0] : (int64_t)*c->h_npairs;
@@ -1145,7 +1171,13 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
     CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 6, g.qoff.p + nq, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (c->rb_extra)
       CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (!B.empty)
+      CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 c->stream));
     sync_stream(c);
+    if (!B.empty && *c->h_npairs > (unsigned long long)HQ_APPEND_LIMIT)
+      throw MpError(MP_ERR_CAPACITY, "ordered broad-phase list exceeds 2^30 pairs (the default one-pass "
+                                     "enumeration handles this size)");
     const int64_t n_pt = c->h_cnt[5], n = c->h_cnt[6];
     if (n > cap) {  // the list did not fit: grow and rerun (results are idempotent)
       g.pa.ensure((size_t)(n * 1.25) + 1024);

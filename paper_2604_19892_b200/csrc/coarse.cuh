@@ -1,0 +1,244 @@
+// coarse.cuh -- dense SPD inverse of a coarse MAS level, the coarse-level
+// _spd_inverse of the reference (mas.py:84-90 applied at mas.py:167), as ONE
+// persistent kernel: no library calls, one launch per level per rebuild.
+//
+// Algorithm: the symmetric sweep operator (Gauss-Jordan without pivoting,
+// stable for SPD) in 32-wide pivot panels.  After panel K is swept,
+//   A_KK <- -A_KK^-1,  A_IK <- W_I = A_IK A_KK^-1,  A_KI <- W_I^T,
+//   A_IJ <- A_IJ - W_I A_JK^T                          (I, J != K)
+// and after the last panel A = -M^-1.  Its pivots are the Schur-complement
+// diagonals (the squared Cholesky pivots), so "pivot <= 0" is exactly
+// cho_factor's non-SPD failure (mas.py:86-88).
+//
+// Layout: only the lower triangle of 32 x 32 tiles is kept, tile-major
+// (tile (I, J <= I) is 1024 contiguous doubles, row-major inside) -- n^2/2
+// doubles of traffic per panel instead of n^2.  A panel's old column
+// A_{., K} is kept in a double-buffered column buffer written by the
+// previous phase, so the in-place update of phase K never races with its
+// readers: one grid barrier per panel.
+//
+// Work split per phase: a unit = (row tile I, chunk of <= 8 column tiles);
+// a unit recomputes W_I (32 x 32 x 32, +1/8 work) and updates its tiles
+// with a 4 x 8 register tile per thread (12 shared loads per 32 FMA).
+// Every CTA sweeps the 32 x 32 pivot block itself (32 barrier steps):
+// redundant, but it saves a second grid barrier per panel.
+#pragma once
+
+#include "common.cuh"
+
+#define CS_TB 32       // tile edge (= pivot panel width)
+#define CS_CH 8        // column tiles per work unit
+#define CS_LD 33       // padded smem row stride
+#define CS_THREADS 256
+
+struct CoarseSweepArgs {
+  int n;                     // matrix order
+  int nT;                    // tiles per side (n padded to 32 nT)
+  int n_units;               // work units per phase
+  const int2* units;         // (row tile I, chunk c) per unit
+  const double* dense;       // n x n assembled M (row-major, both halves valid)
+  double* tiles;             // lower tiles, tile-major
+  double* colbuf;            // 2 x nT x 1024: panel column A_{I,K} (row-major (i, k))
+  double* inv;               // cyc_size(n) packed sym(M^-1)
+  int* status;               // set to 1 when a pivot is not positive
+  unsigned* bar;             // [0] arrival count, [1] generation
+};
+
+__device__ __forceinline__ int64_t cs_tile(int I, int J) { return ((int64_t)I * (I + 1) / 2 + J) * 1024; }
+
+// sense-free generation barrier over all CTAs of the (co-resident) grid
+__device__ __forceinline__ void cs_grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The whole CTA sweeps the 32 x 32 pivot block (row-major in global) ->
+// Pm = -P^-1 in smem (row-major, stride CS_LD).  Thread t holds row t/8,
+// columns 4(t%8)..+3 in registers; the matrix stays symmetric, so the pivot
+// row (double-buffered in rk, published by its owners after their update)
+// doubles as the pivot column: one barrier per pivot.  Returns false
+// (uniformly) when a pivot is not positive.  Reads bypass L1 (__ldcg): the
+// buffers are rewritten by other CTAs between grid barriers.
+__device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double* rk) {
+  const int t = threadIdx.x, i = t >> 3, j0 = (t & 7) * 4;
+  double v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = __ldcg(P + i * 32 + j0 + q);
+  if (i == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rk[j0 + q] = v[q];
+  for (int k = 0; k < 32; ++k) {
+    const double* r = rk + (k & 1) * 32;
+    __syncthreads();
+    const double piv = r[k];
+    if (!(piv > 0.0)) return false;  // uniform across the CTA
+    const double inv = 1.0 / piv;
+    const double cik = r[i] * inv;   // A_ik / A_kk (= A_ki / A_kk)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      const double ckj = r[j];
+      v[q] = (i == k) ? ((j == k) ? -inv : ckj * inv) : ((j == k) ? cik : fma(-cik, ckj, v[q]));
+    }
+    if (i == k + 1 && k + 1 < 32)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rk[((k + 1) & 1) * 32 + j0 + q] = v[q];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Pm[i * CS_LD + j0 + q] = v[q];
+  return true;
+}
+
+__global__ void __launch_bounds__(CS_THREADS, 2) k_coarse_sweep(CoarseSweepArgs A) {
+  extern __shared__ double cs_sm[];
+  double* Pm = cs_sm;                        // 32 x CS_LD: -A_KK^-1
+  double* Wsm = Pm + 32 * CS_LD;             // 32 x CS_LD: W_I, then own column tile
+  double* Csm = Wsm + 32 * CS_LD;            // 32 x CS_LD: own A_IK (row-major)
+  double* Bsm = Csm + 32 * CS_LD;            // CS_CH x 32 x CS_LD: A_JK^T (k-major) per column tile
+  const int tid = threadIdx.x;
+  const int n = A.n, nT = A.nT;
+  const int G = gridDim.x;
+
+  // ---- setup: lower tiles (identity padding) and the first panel column ----
+  {
+    const int64_t tot = (int64_t)nT * (nT + 1) / 2 * 1024;
+    for (int64_t e = blockIdx.x * (int64_t)CS_THREADS + tid; e < tot; e += (int64_t)G * CS_THREADS) {
+      const int64_t t = e >> 10;
+      const int w = (int)(e & 1023);
+      // tile index t -> (I, J): I(I+1)/2 <= t
+      int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((int64_t)(I + 1) * (I + 2) / 2 <= t) ++I;
+      while ((int64_t)I * (I + 1) / 2 > t) --I;
+      const int J = (int)(t - (int64_t)I * (I + 1) / 2);
+      const int i = 32 * I + (w >> 5), j = 32 * J + (w & 31);
+      const double v = (i < n && j < n) ? A.dense[(int64_t)i * n + j] : (i == j ? 1.0 : 0.0);
+      A.tiles[e] = v;
+      if (J == 0) A.colbuf[(int64_t)I * 1024 + w] = v;
+    }
+  }
+  cs_grid_sync(A.bar);
+
+  for (int K = 0; K < nT; ++K) {
+    const double* cur = A.colbuf + (int64_t)(K & 1) * nT * 1024;
+    double* nxt = A.colbuf + (int64_t)((K + 1) & 1) * nT * 1024;
+    // (1) every CTA sweeps the pivot block itself
+    const bool ok = cs_pivot_sweep(cur + (int64_t)K * 1024, Pm, Wsm);
+    __syncthreads();
+    if (!ok) {  // the same bits in every CTA: all leave at the same panel
+      if (blockIdx.x == 0 && tid == 0) atomicExch(A.status, 1);
+      return;
+    }
+    for (int u = blockIdx.x; u < A.n_units; u += G) {
+      const int2 uc = A.units[u];
+      const int I = uc.x, c = uc.y;
+      const int J0 = CS_CH * c, J1 = min(CS_CH * c + CS_CH, I + 1);
+      if (I == K) {  // the pivot row: only A_KK <- -P^-1
+        if (c == 0)
+          for (int w = tid; w < 1024; w += CS_THREADS) A.tiles[cs_tile(K, K) + w] = Pm[(w >> 5) * CS_LD + (w & 31)];
+        continue;
+      }
+      // (2) own column tile A_IK and the chunk's A_JK (transposed, k-major)
+      for (int w = tid; w < 1024; w += CS_THREADS) Csm[(w >> 5) * CS_LD + (w & 31)] = __ldcg(cur + (int64_t)I * 1024 + w);
+      for (int q = 0; q < J1 - J0; ++q) {
+        const double* src = cur + (int64_t)(J0 + q) * 1024;
+        double* dst = Bsm + q * 32 * CS_LD;
+        for (int w = tid; w < 1024; w += CS_THREADS) dst[(w & 31) * CS_LD + (w >> 5)] = __ldcg(src + w);
+      }
+      __syncthreads();
+      // (3) W_I = A_IK A_KK^-1 = -A_IK Pm (4 outputs per thread)
+      {
+        const int i = tid >> 3, j0 = (tid & 7) * 4;
+        double w4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+        for (int d = 0; d < 32; ++d) {
+          const double a = Csm[i * CS_LD + d];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w4[q] = fma(-a, Pm[d * CS_LD + j0 + q], w4[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Wsm[i * CS_LD + j0 + q] = w4[q];
+      }
+      __syncthreads();
+      // (4) the chunk's tiles: rows tr*4 + r, column tc of tile J0 + q
+      const int tr = tid >> 5, tc = tid & 31;
+      const int nq = J1 - J0;
+      double acc[4][CS_CH];
+#pragma unroll
+      for (int q = 0; q < CS_CH; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          acc[r][q] = (q < nq && J0 + q != K) ? __ldcg(A.tiles + cs_tile(I, J0 + q) + (tr * 4 + r) * 32 + tc) : 0.0;
+#pragma unroll 4
+      for (int d = 0; d < 32; ++d) {
+        double wv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) wv[r] = Wsm[(tr * 4 + r) * CS_LD + d];
+#pragma unroll
+        for (int q = 0; q < CS_CH; ++q) {
+          if (q < nq) {
+            const double b = Bsm[q * 32 * CS_LD + d * CS_LD + tc];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][q] = fma(-wv[r], b, acc[r][q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CS_CH; ++q) {
+        if (q >= nq) continue;
+        const int J = J0 + q;
+        double* T = A.tiles + cs_tile(I, J);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = tr * 4 + r;
+          const double v = (J == K) ? Wsm[i * CS_LD + tc] : acc[r][q];  // A_IK <- W_I (I > K)
+          T[i * 32 + tc] = v;
+          if (K + 1 < nT) {
+            if (J == K + 1) nxt[(int64_t)I * 1024 + i * 32 + tc] = v;       // A_{I,K+1}, I >= K+1
+            else if (I == K + 1) nxt[(int64_t)J * 1024 + tc * 32 + i] = v;  // A_{J,K+1} = A_{K+1,J}^T
+          }
+        }
+      }
+      // the pivot row's tile (K, I) <- W_I^T for I < K (row K owns no units)
+      if (I < K && c == 0) {
+        double* T = A.tiles + cs_tile(K, I);
+        for (int w = tid; w < 1024; w += CS_THREADS) {
+          const int i = w >> 5, j = w & 31;  // (K-row i, I-column j) = W_I(j, i)
+          T[w] = Wsm[j * CS_LD + i];
+        }
+        // A_{I,K+1} for I < K comes from row K+1 (handled above); A_{K,K+1}
+        // = W_{K+1}^T is written by row K+1's unit holding column K
+      }
+      __syncthreads();  // smem reused by the next unit
+    }
+    cs_grid_sync(A.bar);
+  }
+
+  // ---- pack sym(-A) in the cyclic layout (common.cuh) ----
+  const int64_t tot = cyc_size(n);
+  for (int64_t e = blockIdx.x * (int64_t)CS_THREADS + tid; e < tot; e += (int64_t)G * CS_THREADS) {
+    const int s = (int)(e / n);
+    const int i = (int)(e - (int64_t)s * n);
+    int j = i + s;
+    if (j >= n) j -= n;
+    const int r = i > j ? i : j, cc = i > j ? j : i;  // lower representative
+    const int I = r >> 5, J = cc >> 5;
+    double v = __ldcg(A.tiles + cs_tile(I, J) + (r & 31) * 32 + (cc & 31));
+    if (I == J) v = 0.5 * (v + __ldcg(A.tiles + cs_tile(I, J) + (cc & 31) * 32 + (r & 31)));
+    A.inv[e] = -v;
+  }
+}
+
+static size_t coarse_sweep_smem() { return sizeof(double) * (3 * 32 * CS_LD + CS_CH * 32 * CS_LD); }

@@ -9,8 +9,6 @@
 // reference's B_d dof order (ascending original id, mas.py:74).
 #pragma once
 
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 
 #include <string>
 #include <chrono>
@@ -97,6 +95,7 @@ struct CoarseLevel {
   int n = 0;          // 3A dofs
   int span = 0;       // vertices per aggregate (last may be short)
   DBuf<double> dense; // n*n Galerkin matrix, swept in place
+  DBuf<double> keep;  // n*n copy of the assembled matrix before the sweep (MP_OPT_KEEP_COARSE)
   DBuf<double> inv;   // cyc_size(n) packed inverse
   DBuf<double> rsum;  // 3A restricted raw sums
   DBuf<double> r;     // 3A restriction C_l g (averages)
@@ -106,21 +105,17 @@ struct CoarseLevel {
   DBuf<unsigned long long> fx_acc;  // n*n*2: contact terms, 128-bit fixed point
   DBuf<int> cb_key, cb_off, cb_slot;  // BSR -> M_l gather map: nonzero blocks A*nA+B, their slots
   int nblk = 0;
-  DBuf<double> dn_col, dn_W, dn_P, dn_Pn;  // blocked-sweep scratch
+  // the coarse inverse (coarse.cuh): work units, lower tiles, panel columns, grid barrier
+  DBuf<int2> cs_units;
+  int n_units = 0;
+  DBuf<double> cs_tiles, cs_col;
+  DBuf<unsigned> cs_bar;
   int chunks = 1;
-  // each coarse level is built on its own stream (st2: lookahead updates),
+  // each coarse level is built on its own stream (st2: its contact terms),
   // concurrently with level 0
   cudaStream_t st = nullptr, st2 = nullptr;
   cudaEvent_t done = nullptr, ev_w = nullptr, ev_u = nullptr, ev_asm = nullptr;
-  cublasHandle_t blas = nullptr;
-  // the blocked inverse as a CUDA graph (stages.cuh dense_spd_inverse)
-  cudaGraphExec_t graph = nullptr;
-  const void* graph_key[7] = {};
-  int64_t graph_launches = 0;
-  bool graph_failed = false;
   ~CoarseLevel() {
-    if (graph) cudaGraphExecDestroy(graph);
-    if (blas) cublasDestroy(blas);
     for (cudaEvent_t e : {done, ev_w, ev_u, ev_asm})
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
@@ -148,11 +143,10 @@ struct mp_ctx {
   int apply_mode = 2;        // level-0 apply: 2 direct loads, 1 TMA-staged, 0 cp.async-staged
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
+  bool keep_coarse = false;  // keep each coarse level's assembled matrix (mp_coarse_matrix)
   int bp_fused = 1;          // 1: one-pass unordered pair lists, 2: contact work fused into the queries, 0: ordered lists
   StageTimer timers[MP_STAGE_COUNT];
   cudaStream_t stream = nullptr;
-  cusolverDnHandle_t solver = nullptr;
-  cublasHandle_t blas = nullptr;
   std::string last_error;
   int64_t launches = 0;
 
@@ -242,9 +236,7 @@ struct mp_ctx {
   DBuf<double> Mfull;       // D * m*m scratch
   std::vector<CoarseLevel*> levels;
   int n_levels = 0;
-  DBuf<double> solver_work;
   cudaEvent_t ev_bsr = nullptr;     // H_base ready (coarse streams wait on it)
-  DBuf<int> solver_info;
   bool have_snapshot = false;
   bool have_mas = false;
 

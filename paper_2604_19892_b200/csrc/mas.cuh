@@ -146,33 +146,6 @@ __device__ void smem_chol_inverse(const double* L, int m, double* X) {
   __syncthreads();
 }
 
-// one CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
-__global__ void k_mas_factor(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull,
-                             double* __restrict__ Mblk, double* __restrict__ Bblk, int* __restrict__ status) {
-  extern __shared__ double sm[];
-  double* A = sm;
-  double* X = sm + m * m;
-  __shared__ int bad;
-  const int64_t d = blockIdx.x;
-  if (threadIdx.x == 0) bad = 0;
-  int nd = (int)((N - d * bs) < bs ? (N - d * bs) : bs);
-  const double* src = Mfull + d * m * m;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int i = e / m, j = e % m;
-    double v = src[e];
-    if (i >= 3 * nd || j >= 3 * nd) v = (i == j) ? 1.0 : 0.0;
-    A[e] = v;
-  }
-  __syncthreads();
-  store_cyc_sym(A, m, Mblk + d * cyc_size(m), false);
-  smem_cholesky(A, m, &bad);
-  if (bad) {
-    if (threadIdx.x == 0) atomicExch(status, 1);
-    return;
-  }
-  smem_chol_inverse(A, m, X);
-  store_cyc_sym(X, m, Bblk + d * cyc_size(m), true);
-}
 
 #define SWEEP_T 6
 
@@ -657,7 +630,6 @@ __global__ void k_sym_lower(int n, double* M, const unsigned long long* __restri
   M[(int64_t)j * n + i] = s;
 }
 
-// pack the symmetric inverse whose valid half is potri's (lower, column-major)
 // pack sym(-A) (A = -M^-1 after the blocked sweep) in the cyclic layout
 __global__ void k_pack_neg_sym(int n, const double* __restrict__ A, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -669,16 +641,6 @@ __global__ void k_pack_neg_sym(int n, const double* __restrict__ A, double* __re
   out[e] = -0.5 * (A[(int64_t)j * n + i] + A[(int64_t)i * n + j]);
 }
 
-__global__ void k_pack_coarse(int n, const double* __restrict__ M, double* __restrict__ out) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= cyc_size(n)) return;
-  int s = (int)(e / n);
-  int i = (int)(e - (int64_t)s * n);
-  int j = i + s;
-  if (j >= n) j -= n;
-  int r = i > j ? i : j, c = i > j ? j : i;  // lower-triangle element (r >= c)
-  out[e] = M[(int64_t)c * n + r];           // column-major (r, c)
-}
 
 // ---------------------------------------------------------------------------
 // apply

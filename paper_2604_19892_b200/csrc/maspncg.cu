@@ -22,8 +22,6 @@ mp_ctx::~mp_ctx() {
     if (t.a) cudaEventDestroy(t.a);
     if (t.b) cudaEventDestroy(t.b);
   }
-  if (solver) cusolverDnDestroy(solver);
-  if (blas) cublasDestroy(blas);
   if (ev_bsr) cudaEventDestroy(ev_bsr);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -160,8 +158,15 @@ static void setup_levels(mp_ctx* c) {
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_w, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_u, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_asm, cudaEventDisableTiming));
-    if (cublasCreate(&L->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate (coarse)");
-    cublasSetStream(L->blas, L->st);
+    {  // coarse-inverse work units: (row tile I, chunk of <= CS_CH column tiles J <= I)
+      const int nT = (L->n + CS_TB - 1) / CS_TB;
+      std::vector<int2> units;
+      for (int I = 0; I < nT; ++I)
+        for (int cch = 0; CS_CH * cch <= I; ++cch) units.push_back(make_int2(I, cch));
+      L->n_units = (int)units.size();
+      L->cs_units.upload(units.data(), units.size(), c->stream);
+      CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
     c->levels.push_back(L);
     units = n_agg;
   }
@@ -180,13 +185,13 @@ static void set_smem_limits() {
     int dyn = optin - (int)fa.sharedSizeBytes;
     CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
   };
-  allow((const void*)k_mas_factor);
   allow((const void*)k_mas_apply_l0<true, 2>);
   allow((const void*)k_mas_apply_l0<false, 2>);
   allow((const void*)k_mas_apply_l0<true, 3>);
   allow((const void*)k_mas_apply_l0<false, 3>);
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
+  allow((const void*)k_coarse_sweep);
   done = true;
 }
 
@@ -196,10 +201,6 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   c->device = device;
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cusolverDnCreate");
-  cusolverDnSetStream(c->solver, c->stream);
-  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw MpError(MP_ERR_CUDA, "cublasCreate");
-  cublasSetStream(c->blas, c->stream);
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bsr, cudaEventDisableTiming));
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
@@ -374,7 +375,6 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   c->counters.zero(16, c->stream);
   c->mid_part.ensure(6 * 148);
   c->dscal.ensure(64);
-  c->solver_info.ensure(1);
   c->alpha_d.ensure(c->D);
   setup_levels(c);
 }
@@ -553,7 +553,7 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     rec.t_dir_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
     rec.t_ccd_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
     rec.n_candidates = (int32_t)(rebuild ? 0 : c->n_cand);
-    rec.n_ccd_pairs = (int32_t)c->n_ccd_seen;
+    rec.n_ccd_pairs = (int32_t)std::min<int64_t>(c->n_ccd_seen, INT32_MAX);  // saturates (>2^31 at C3)
     rec.ccd_certified = certified ? 1 : 0;
     rec.energy = e_iter;
     const bool converged_now = z_norm <= cfg.eps;
@@ -670,6 +670,11 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_APPLY_TMA) c->apply_mode = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (option == MP_OPT_APPLY_STAGES) c->apply_stages = value == 3 ? 3 : 2;
     else if (option == MP_OPT_BP_FUSED) c->bp_fused = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
+    else if (option == MP_OPT_KEEP_COARSE) c->keep_coarse = value != 0;
+    else if (option == MP_OPT_APPEND_LIMIT) {
+      const int lim = (int)std::max<int64_t>(64, std::min<int64_t>(HQ_APPEND_LIMIT, value <= 0 ? HQ_APPEND_LIMIT : value));
+      CUDA_CHECK(cudaMemcpyToSymbol(g_append_limit, &lim, sizeof(int)));
+    }
     else if (option == MP_OPT_APPLY_CTAS) c->apply_ctas_per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, value));
     else throw MpError(MP_ERR_CONFIG, "unknown option");
   });
@@ -727,6 +732,44 @@ int mp_set_config(mp_ctx* c, const mp_solver_config* cfg) {
     // depth; the per-call config of the Python API re-sets the rest freely
     if (relevel) setup_levels(c);
     c->have_mas = false;
+  });
+}
+
+int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t* not_spd) {
+  static thread_local mp_ctx* tmp = nullptr;  // scratch context: streams + buffers of one coarse level
+  if (n < 1 || n > (1 << 15)) return MP_ERR_CONFIG;
+  if (!tmp) tmp = new mp_ctx();
+  return guarded(tmp, [&] {
+    mp_ctx* c = tmp;
+    c->device = device;
+    CUDA_CHECK(cudaSetDevice(device));
+    if (!c->stream) CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    set_smem_limits();
+    CoarseLevel L;
+    struct Unown {  // the stream belongs to the scratch context, not to L
+      CoarseLevel& l;
+      ~Unown() { l.st = nullptr; }
+    } unown{L};
+    L.n = (int)n;
+    L.st = c->stream;
+    const int nT = (L.n + CS_TB - 1) / CS_TB;
+    std::vector<int2> units;
+    for (int I = 0; I < nT; ++I)
+      for (int cch = 0; CS_CH * cch <= I; ++cch) units.push_back(make_int2(I, cch));
+    L.n_units = (int)units.size();
+    L.cs_units.upload(units.data(), units.size(), c->stream);
+    L.dense.upload(A, (size_t)n * n, c->stream);
+    c->counters.zero(16, c->stream);
+    dense_spd_inverse(c, L, c->counters.p);
+    std::vector<double> packed(cyc_size(L.n));
+    int flag = 0;
+    CUDA_CHECK(cudaMemcpyAsync(packed.data(), L.inv.p, sizeof(double) * packed.size(), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(&flag, c->counters.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    *not_spd = flag;
+    for (int i = 0; i < L.n; ++i)
+      for (int j = 0; j < L.n; ++j) inv[(int64_t)i * n + j] = packed[cyc_index(L.n, i, j)];
   });
 }
 
@@ -961,6 +1004,18 @@ int mp_ccd(mp_ctx* c, const double* x, const double* p, double* alpha_d, double*
     *min_alpha = R.min_alpha;
     *certified = R.certified ? 1 : 0;
     *n_pairs = R.n_pairs;
+  });
+}
+
+int mp_coarse_matrix(mp_ctx* c, int level, double* out, int64_t cap, int64_t* n) {
+  return guarded(c, [&] {
+    if (level < 1 || level > c->n_levels) throw MpError(MP_ERR_CONFIG, "no such coarse level");
+    CoarseLevel& L = *c->levels[level - 1];
+    *n = L.n;
+    if (!out || cap < (int64_t)L.n * L.n) return;
+    if (!c->keep_coarse || !L.keep.p) throw MpError(MP_ERR_CONFIG, "enable MP_OPT_KEEP_COARSE before the build");
+    for (auto* l : c->levels) CUDA_CHECK(cudaStreamSynchronize(l->st));
+    CUDA_CHECK(cudaMemcpy(out, L.keep.p, sizeof(double) * (size_t)L.n * L.n, cudaMemcpyDeviceToHost));
   });
 }
 

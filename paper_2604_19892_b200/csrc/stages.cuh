@@ -4,6 +4,7 @@
 #pragma once
 
 #include "ccd.cuh"
+#include "coarse.cuh"
 #include "elastic.cuh"
 #include "mas.cuh"
 #include "ops.cuh"
@@ -94,122 +95,32 @@ static int read_status(mp_ctx* c, int* dev) {
   return h;
 }
 
-// sym(M^-1) of a coarse level's dense SPD matrix (column-major, both halves
-// valid), packed in the cyclic layout, on the level's own stream -- the coarse-level _spd_inverse (mas.py:84-90,
-// :167).  Blocked symmetric sweep: for each 96-wide pivot block K,
-//   P^-1 by the in-smem sweep (k_block_sweep, non-SPD pivots flagged),
-//   W = A[:,K] P^-1 (DGEMM), A -= W A[:,K]^T (rank-96 DGEMM update),
-//   A[:,K] = A[K,:]^T = W, A[K,K] = -P^-1 (k_block_fix);
-// after every block A = -M^-1.  cuBLAS DGEMM carries the O(n^3) work.
-static void dense_spd_inverse_enqueue(mp_ctx* c, CoarseLevel& L, int* status) {
-  const int nb = 96;
-  const int n = L.n;
-  double* A = L.dense;
-  cudaStream_t st = L.st, st2 = L.st2;
-  const double one = 1.0, mone = -1.0, zero = 0.0;
-  auto gemm = [&](cudaStream_t s, cublasOperation_t tb, int mm, int nn, int kk, const double* alpha,
-                  const double* Am, int lda, const double* Bm, int ldb, const double* beta, double* Cm, int ldc,
-                  const char* what) {
-    cublasSetStream(L.blas, s);
-    if (cublasDgemm(L.blas, CUBLAS_OP_N, tb, mm, nn, kk, alpha, Am, lda, Bm, ldb, beta, Cm, ldc) !=
-        CUBLAS_STATUS_SUCCESS)
-      throw MpError(MP_ERR_CUDA, what);
-    if (g_launch_counter) ++(*g_launch_counter);
-  };
-  // Lookahead: the next pivot block is updated first (a kb x kb x kb GEMM)
-  // and swept on st while the rank-kb update of the whole matrix runs on st2.
-  const int nblk = (n + nb - 1) / nb;
-  k_block_sweep<<<1, 256, 0, st>>>(std::min(nb, n), A, n, 0, L.dn_P, status);
-  LAUNCH_CHECK();
-  CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A, sizeof(double) * (size_t)n * std::min(nb, n), cudaMemcpyDeviceToDevice,
-                             st));
-  for (int K = 0; K < nblk; ++K) {
-    const int k0 = K * nb, kb = std::min(nb, n - k0);
-    double* Pk = L.dn_P.p + (size_t)(K & 1) * nb * nb;
-    // W = -colK * (-P^-1)
-    gemm(st, CUBLAS_OP_N, n, kb, kb, &mone, L.dn_col, n, Pk, kb, &zero, L.dn_W, n, "cublasDgemm (coarse W)");
-    const int k1 = k0 + kb, kb1 = std::min(nb, n - k1);
-    if (K + 1 < nblk) {
-      // next pivot block, updated ahead: A(K+1, K+1) - W(K+1 rows) colK(K+1 rows)^T
-      CUDA_CHECK(cudaMemcpy2DAsync(L.dn_Pn.p, sizeof(double) * kb1, A + (size_t)k1 * n + k1, sizeof(double) * n,
-                                   sizeof(double) * kb1, kb1, cudaMemcpyDeviceToDevice, st));
-      gemm(st, CUBLAS_OP_T, kb1, kb1, kb, &mone, L.dn_W.p + k1, n, L.dn_col.p + k1, n, &one, L.dn_Pn, kb1,
-           "cublasDgemm (coarse lookahead)");
-    }
-    CUDA_CHECK(cudaEventRecord(L.ev_w, st));
-    // whole-matrix update, fix-up of block K and the next column panel: st2
-    CUDA_CHECK(cudaStreamWaitEvent(st2, L.ev_w, 0));
-    gemm(st2, CUBLAS_OP_T, n, n, kb, &mone, L.dn_W, n, L.dn_col, n, &one, A, n, "cublasDgemm (coarse update)");
-    k_block_fix<<<grid_for((int64_t)n * kb, 256), 256, 0, st2>>>(n, kb, k0, L.dn_W, Pk, A);
-    LAUNCH_CHECK();
-    if (K + 1 < nblk)
-      CUDA_CHECK(cudaMemcpyAsync(L.dn_col.p, A + (size_t)k1 * n, sizeof(double) * (size_t)n * kb1,
-                                 cudaMemcpyDeviceToDevice, st2));
-    CUDA_CHECK(cudaEventRecord(L.ev_u, st2));
-    if (K + 1 < nblk) {
-      k_block_sweep<<<1, 256, 0, st>>>(kb1, L.dn_Pn, kb1, 0, L.dn_P.p + (size_t)((K + 1) & 1) * nb * nb, status);
-      LAUNCH_CHECK();
-    }
-    CUDA_CHECK(cudaStreamWaitEvent(st, L.ev_u, 0));
-  }
-  cublasSetStream(L.blas, st);
-  k_pack_neg_sym<<<grid_for(cyc_size(n), 256), 256, 0, st>>>(n, A, L.inv);
-  LAUNCH_CHECK();
-}
-
-// The blocked inverse is ~150 dependent launches and cuBLAS calls across two
-// streams per level -- enough host work to starve the GPU.  It is captured
-// once into a CUDA graph (re-captured if a buffer moved) and replayed with
-// one launch: the same kernels in the same order, so the same bits.
+// sym(M^-1) of a coarse level's dense SPD matrix, packed in the cyclic
+// layout, on the level's own stream: the coarse-level _spd_inverse
+// (mas.py:84-90, :167) as one persistent cooperative kernel
+// (coarse.cuh k_coarse_sweep, one grid barrier per 32-pivot panel).
 static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
-  const int nb = 96;
-  const int n = L.n;
-  L.dn_col.ensure((size_t)n * nb);
-  L.dn_W.ensure((size_t)n * nb);
-  L.dn_P.ensure(2 * (size_t)nb * nb);
-  L.dn_Pn.ensure((size_t)nb * nb);
+  (void)c;
+  const int n = L.n, nT = (n + CS_TB - 1) / CS_TB;
   L.inv.ensure((size_t)cyc_size(n));
-  static const bool no_graph = getenv("MP_NO_COARSE_GRAPH") != nullptr;
-  if (no_graph || L.graph_failed) {
-    dense_spd_inverse_enqueue(c, L, status);
-    return;
+  L.cs_tiles.ensure((size_t)nT * (nT + 1) / 2 * 1024);
+  L.cs_col.ensure(2 * (size_t)nT * 1024);
+  L.cs_bar.zero(2, L.st);
+  static int max_ctas = 0;
+  if (!max_ctas) {
+    int dev = 0, sms = 0, per = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_sweep, CS_THREADS, coarse_sweep_smem()));
+    max_ctas = std::max(1, sms * std::max(1, per));
   }
-  const void* key[7] = {L.dense.p, L.dn_col.p, L.dn_W.p, L.dn_P.p, L.dn_Pn.p, L.inv.p, status};
-  bool same = L.graph != nullptr;
-  for (int q = 0; q < 7 && same; ++q) same = L.graph_key[q] == key[q];
-  if (!same) {
-    if (L.graph) {
-      cudaGraphExecDestroy(L.graph);
-      L.graph = nullptr;
-    }
-    cudaGraph_t g = nullptr;
-    int64_t* saved = g_launch_counter;
-    int64_t counted = 0;
-    g_launch_counter = &counted;
-    bool ok = cudaStreamBeginCapture(L.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-    if (ok) {
-      try {
-        dense_spd_inverse_enqueue(c, L, status);
-      } catch (...) {
-        ok = false;
-      }
-      ok = (cudaStreamEndCapture(L.st, &g) == cudaSuccess) && ok && g;
-    }
-    g_launch_counter = saved;
-    if (ok) ok = cudaGraphInstantiate(&L.graph, g, 0) == cudaSuccess;
-    if (g) cudaGraphDestroy(g);
-    if (!ok) {  // capture unsupported here: enqueue directly from now on
-      cudaGetLastError();
-      L.graph = nullptr;
-      L.graph_failed = true;
-      dense_spd_inverse_enqueue(c, L, status);
-      return;
-    }
-    for (int q = 0; q < 7; ++q) L.graph_key[q] = key[q];
-    L.graph_launches = counted;
-  }
-  CUDA_CHECK(cudaGraphLaunch(L.graph, L.st));
-  if (g_launch_counter) *g_launch_counter += L.graph_launches;
+  const int grid = std::max(1, std::min(L.n_units, max_ctas));
+  CoarseSweepArgs A{n, nT, L.n_units, L.cs_units.p, L.dense.p, L.cs_tiles.p, L.cs_col.p, L.inv.p, status,
+                    L.cs_bar.p};
+  void* args[] = {&A};
+  CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_coarse_sweep, dim3(grid), dim3(CS_THREADS), args,
+                                         coarse_sweep_smem(), L.st));
+  if (g_launch_counter) ++(*g_launch_counter);
 }
 
 // build_hierarchy (mas.py:138-179) from the BSR + base contacts
@@ -267,6 +178,11 @@ static void mas_build(mp_ctx* c) {
     CoarseLevel& L = *c->levels[l];
     if (l + 1 < c->n_levels) CUDA_CHECK(cudaStreamWaitEvent(L.st, c->levels[l + 1]->ev_asm, 0));
     L.inv.ensure((size_t)cyc_size(L.n));
+    if (c->keep_coarse) {
+      L.keep.ensure((size_t)L.n * L.n);
+      CUDA_CHECK(cudaMemcpyAsync(L.keep.p, L.dense.p, sizeof(double) * (size_t)L.n * L.n, cudaMemcpyDeviceToDevice,
+                                 L.st));
+    }
     dense_spd_inverse(c, L, c->counters.p + 4 + std::min(l, 3));
     CUDA_CHECK(cudaEventRecord(L.done, L.st));
   }

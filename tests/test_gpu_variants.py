@@ -56,3 +56,28 @@ def test_apply_modes_same_bits():
         zs.append(ctx.precond_apply(r))
     ctx.set_option(3, 2)
     assert np.array_equal(zs[0], zs[1]) and np.array_equal(zs[0], zs[2])
+
+
+@pytest.mark.parametrize("name", ["stacked_k256", "locking"])
+def test_append_overflow_rerun_same_bits(name):
+    """MP_OPT_APPEND_LIMIT (8) lowers the one-pass list's counter limit so a
+    small scene takes the >2^30-pairs path (list-free rerun with a 64-bit
+    count): alpha_d, the global minimum (read back from the rerun), the
+    certificate and x_new must equal the normal path's."""
+    g = load_golden(name)
+    scene = scene_from_golden(g)
+    ctx = scene.context(golden_config(g))
+    rng = np.random.default_rng(11)
+    cases = [(t["x"], t["p"]) for t in golden_taps(g, "ccd")]
+    for x, p in list(cases):
+        cases.append((x, 4.0 * p + 0.5 * np.abs(p).max() * rng.standard_normal(p.shape)))
+    try:
+        for x, p in cases:
+            ctx.set_option(8, 0)
+            ref = ctx.ccd(x, p, exact_set=False)
+            ctx.set_option(8, 64)
+            low = ctx.ccd(x, p, exact_set=False)
+            assert np.array_equal(ref[0], low[0]) and np.array_equal(ref[1], low[1])
+            assert ref[2] == low[2] and ref[3] == low[3]
+    finally:
+        ctx.set_option(8, 0)

@@ -14,7 +14,9 @@ cfg = solver.SolverConfig(iter_max=200, levels=levels)
 ctx = scene.context(cfg)
 x0 = scene.mesh.rest_positions.ravel().copy()
 ctx.set_state(x0, np.zeros_like(x0))
-if os.path.exists("tools/_data/ccd_state.npz"):
+if os.path.exists("tools/_data/c2_state_w5.npz"):  # the bench's first timed frame (tools/c2_dump.py)
+    x = np.load("tools/_data/c2_state_w5.npz")["x0"]
+elif os.path.exists("tools/_data/ccd_state.npz"):
     x = np.load("tools/_data/ccd_state.npz")["x"]
 else:
     for _ in range(4):  # reach contact
