@@ -42,7 +42,14 @@ struct CoarseSweepArgs {
   double* inv;               // cyc_size(n) packed sym(M^-1)
   int* status;               // set to 1 when a pivot is not positive
   unsigned* bar;             // [0] arrival count, [1] generation
+  int prof;                  // debug: CTA 0 prints per-phase %globaltimer splits (MP_CS_PROF)
 };
+
+__device__ __forceinline__ unsigned long long cs_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int64_t cs_tile(int I, int J) { return ((int64_t)I * (I + 1) / 2 + J) * 1024; }
 
@@ -58,7 +65,8 @@ __device__ __forceinline__ void cs_grid_sync(unsigned* bar) {
       __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
-      while (*gen == g) __nanosleep(64);
+      while (*gen == g) {
+      }
     }
     __threadfence();
   }
@@ -69,7 +77,8 @@ __device__ __forceinline__ void cs_grid_sync(unsigned* bar) {
 // Pm = -P^-1 in smem (row-major, stride CS_LD).  Thread t holds row t/8,
 // columns 4(t%8)..+3 in registers; the matrix stays symmetric, so the pivot
 // row (double-buffered in rk, published by its owners after their update)
-// doubles as the pivot column: one barrier per pivot.  Returns false
+// doubles as the pivot column: one barrier per pivot (~5 us for 32; a
+// one-warp shuffle-only variant measured 25-31 us).  Returns false
 // (uniformly) when a pivot is not positive.  Reads bypass L1 (__ldcg): the
 // buffers are rewritten by other CTAs between grid barriers.
 __device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double* rk) {
@@ -85,7 +94,12 @@ __device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double*
     __syncthreads();
     const double piv = r[k];
     if (!(piv > 0.0)) return false;  // uniform across the CTA
-    const double inv = 1.0 / piv;
+    double inv;  // 1/piv to ~1 ulp: MUFU seed + two Newton steps (the IEEE
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(piv));  // division sits on the serial path)
+    double e = fma(-piv, inv, 1.0);
+    inv = fma(inv, e, inv);
+    e = fma(-piv, inv, 1.0);
+    inv = fma(inv, e, inv);
     const double cik = r[i] * inv;   // A_ik / A_kk (= A_ki / A_kk)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -102,7 +116,23 @@ __device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double*
   return true;
 }
 
-__global__ void __launch_bounds__(CS_THREADS, 2) k_coarse_sweep(CoarseSweepArgs A) {
+// A unit's panel tiles into registers: pre[0] = A_IK, pre[1 + q] = A_{J0+q, K};
+// element w = tid + 256 s of each tile.  Unrolled, predicated: every load is
+// in flight at once.
+__device__ __forceinline__ void cs_load_unit(const double* __restrict__ cur, int2 uc, int K,
+                                             double (&pre)[1 + CS_CH][4]) {
+  const int I = uc.x, J0 = CS_CH * uc.y, nq = min(CS_CH, I + 1 - J0);
+  const bool live = I != K;
+#pragma unroll
+  for (int s4 = 0; s4 < 4; ++s4) {
+    const int w = threadIdx.x + CS_THREADS * s4;
+    pre[0][s4] = live ? __ldcg(cur + (int64_t)I * 1024 + w) : 0.0;
+#pragma unroll
+    for (int q = 0; q < CS_CH; ++q) pre[1 + q][s4] = (live && q < nq) ? __ldcg(cur + (int64_t)(J0 + q) * 1024 + w) : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs A) {
   extern __shared__ double cs_sm[];
   double* Pm = cs_sm;                        // 32 x CS_LD: -A_KK^-1
   double* Wsm = Pm + 32 * CS_LD;             // 32 x CS_LD: W_I, then own column tile
@@ -134,14 +164,21 @@ __global__ void __launch_bounds__(CS_THREADS, 2) k_coarse_sweep(CoarseSweepArgs 
   for (int K = 0; K < nT; ++K) {
     const double* cur = A.colbuf + (int64_t)(K & 1) * nT * 1024;
     double* nxt = A.colbuf + (int64_t)((K + 1) & 1) * nT * 1024;
+    // the first unit's panel tiles are fetched before the pivot sweep (all
+    // loads in flight in registers; the sweep hides their L2 latency)
+    double pre[1 + CS_CH][4];
+    const unsigned long long t0 = A.prof ? cs_now() : 0ull;
+    int u = blockIdx.x;
+    if (u < A.n_units) cs_load_unit(cur, A.units[u], K, pre);
     // (1) every CTA sweeps the pivot block itself
     const bool ok = cs_pivot_sweep(cur + (int64_t)K * 1024, Pm, Wsm);
     __syncthreads();
+    const unsigned long long t1 = A.prof ? cs_now() : 0ull;
     if (!ok) {  // the same bits in every CTA: all leave at the same panel
       if (blockIdx.x == 0 && tid == 0) atomicExch(A.status, 1);
       return;
     }
-    for (int u = blockIdx.x; u < A.n_units; u += G) {
+    for (; u < A.n_units; u += G) {
       const int2 uc = A.units[u];
       const int I = uc.x, c = uc.y;
       const int J0 = CS_CH * c, J1 = min(CS_CH * c + CS_CH, I + 1);
@@ -150,12 +187,15 @@ __global__ void __launch_bounds__(CS_THREADS, 2) k_coarse_sweep(CoarseSweepArgs 
           for (int w = tid; w < 1024; w += CS_THREADS) A.tiles[cs_tile(K, K) + w] = Pm[(w >> 5) * CS_LD + (w & 31)];
         continue;
       }
-      // (2) own column tile A_IK and the chunk's A_JK (transposed, k-major)
-      for (int w = tid; w < 1024; w += CS_THREADS) Csm[(w >> 5) * CS_LD + (w & 31)] = __ldcg(cur + (int64_t)I * 1024 + w);
-      for (int q = 0; q < J1 - J0; ++q) {
-        const double* src = cur + (int64_t)(J0 + q) * 1024;
-        double* dst = Bsm + q * 32 * CS_LD;
-        for (int w = tid; w < 1024; w += CS_THREADS) dst[(w & 31) * CS_LD + (w >> 5)] = __ldcg(src + w);
+      if (u != (int)blockIdx.x) cs_load_unit(cur, uc, K, pre);
+      // (2) own column tile A_IK (row-major) and the chunk's A_JK (transposed, k-major)
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int w = tid + CS_THREADS * s4;
+        Csm[(w >> 5) * CS_LD + (w & 31)] = pre[0][s4];
+#pragma unroll
+        for (int q = 0; q < CS_CH; ++q)
+          if (q < J1 - J0) Bsm[q * 32 * CS_LD + (w & 31) * CS_LD + (w >> 5)] = pre[1 + q][s4];
       }
       __syncthreads();
       // (3) W_I = A_IK A_KK^-1 = -A_IK Pm (4 outputs per thread)
@@ -223,7 +263,10 @@ __global__ void __launch_bounds__(CS_THREADS, 2) k_coarse_sweep(CoarseSweepArgs 
       }
       __syncthreads();  // smem reused by the next unit
     }
+    const unsigned long long t2 = A.prof ? cs_now() : 0ull;
     cs_grid_sync(A.bar);
+    if (A.prof && blockIdx.x == 0 && tid == 0 && K < 4)
+      printf("cs phase %d: sweep %llu ns, units %llu ns, barrier %llu ns\n", K, t1 - t0, t2 - t1, cs_now() - t2);
   }
 
   // ---- pack sym(-A) in the cyclic layout (common.cuh) ----

@@ -233,7 +233,6 @@ struct mp_ctx {
   // ---- MAS ----
   DBuf<double> Bblk;        // D * cyc(m) packed inverses
   DBuf<double> Mblk;        // D * cyc(m) packed subdomain blocks (direct refactor path)
-  DBuf<double> Mfull;       // D * m*m scratch
   std::vector<CoarseLevel*> levels;
   int n_levels = 0;
   cudaEvent_t ev_bsr = nullptr;     // H_base ready (coarse streams wait on it)

@@ -25,54 +25,62 @@
 // ---------------------------------------------------------------------------
 // level-0 assembly
 
-// contacts -> Mfull (same-subdomain vertex pairs): one thread per vertex a
-// owns rows 3a..3a+2 of its subdomain block and adds its incidences' terms
-// in ascending (contact, partner) order -- no atomics, reproducible
-__global__ void k_contact_blocks(int64_t N, const unsigned char* __restrict__ pinned, const int* __restrict__ off,
-                                 const int* __restrict__ inc, const int4* __restrict__ verts,
-                                 const double* __restrict__ grad, const double* __restrict__ k, int bs, int m,
-                                 double* __restrict__ Mfull) {
-  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= N || pinned[v]) return;  // pinned rows of grad are zero
-  const int d = (int)(v / bs), la = (int)(v - (int64_t)d * bs);
-  double* blk = Mfull + (int64_t)d * m * m;
-  for (int q = off[v]; q < off[v + 1]; ++q) {
-    const int e = inc[q];
-    const int64_t i = e >> 2;
-    const int a = e & 3;
-    const int4 vv = verts[i];
-    const int id[4] = {vv.x, vv.y, vv.z, vv.w};
-    const double kk = k[i];
-    const double* ga = grad + 12 * i + 3 * a;
-    for (int b = 0; b < 4; ++b) {
-      if (id[b] / bs != d) continue;
-      const int lb = id[b] - d * bs;
-      const double* gb = grad + 12 * i + 3 * b;
-      for (int r = 0; r < 3; ++r)
-        for (int cc = 0; cc < 3; ++cc) {
-          double val = kk * ga[r] * gb[cc];
-          if (val != 0.0) blk[(3 * la + r) * m + 3 * lb + cc] += val;
+// M_d assembled in shared memory (m x m, row stride m), by the subdomain's
+// own CTA: first the contact terms -- one thread per local vertex a owns
+// rows 3a..3a+2 and adds its incidences' k grad_a grad_b^T (b in the same
+// subdomain) in ascending (contact, partner) order -- then the BSR blocks
+// whose row and column both lie in the subdomain (unique targets).  No
+// atomics: the same sums in the same order on every run.
+__device__ void assemble_block_smem(int64_t d, int64_t N, int bs, int m, const unsigned char* __restrict__ pinned,
+                                    const int* __restrict__ off, const int* __restrict__ inc,
+                                    const int4* __restrict__ verts, const double* __restrict__ grad,
+                                    const double* __restrict__ k, const int* __restrict__ rowptr,
+                                    const int* __restrict__ slot_row, const int* __restrict__ cols,
+                                    const double* __restrict__ vals, double* S) {
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = 0.0;
+  __syncthreads();
+  const int64_t v0 = d * bs;
+  const int nd = (int)((N - v0) < bs ? (N - v0) : bs);
+  if (off && (int)threadIdx.x < nd) {
+    const int la = threadIdx.x;
+    const int64_t v = v0 + la;
+    if (!pinned[v]) {  // pinned rows of grad are zero
+      for (int q = off[v]; q < off[v + 1]; ++q) {
+        const int e = inc[q];
+        const int64_t i = e >> 2;
+        const int a = e & 3;
+        const int4 vv = verts[i];
+        const int id[4] = {vv.x, vv.y, vv.z, vv.w};
+        const double kk = k[i];
+        const double* ga = grad + 12 * i + 3 * a;
+        for (int b = 0; b < 4; ++b) {
+          if (id[b] / bs != d) continue;
+          const int lb = id[b] - (int)v0;
+          const double* gb = grad + 12 * i + 3 * b;
+          for (int r = 0; r < 3; ++r)
+            for (int cc = 0; cc < 3; ++cc) {
+              const double val = kk * ga[r] * gb[cc];
+              if (val != 0.0) S[(3 * la + r) * m + 3 * lb + cc] += val;
+            }
         }
+      }
     }
   }
-}
-
-// BSR blocks whose row and column share a subdomain -> Mfull: one thread per
-// slot, unique targets (added after the contact terms, same stream)
-__global__ void k_bsr_to_blocks(int64_t nnzb, const int* __restrict__ slot_row, const int* __restrict__ cols,
-                                const double* __restrict__ vals, int bs, int m, double* __restrict__ Mfull) {
-  int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (sl >= nnzb) return;
-  const int v = slot_row[sl], w = cols[sl];
-  const int d = v / bs;
-  if (w / bs != d) return;
-  const int lr = v - d * bs, lc = w - d * bs;
-  double* blk = Mfull + (int64_t)d * m * m + (3 * lr) * m + 3 * lc;
-  const double* b = vals + 9 * sl;
+  __syncthreads();
+  const int s0 = rowptr[v0], s1 = rowptr[v0 + nd];
+  for (int sl = s0 + threadIdx.x; sl < s1; sl += blockDim.x) {
+    const int w = cols[sl];
+    if (w < v0 || w >= v0 + nd) continue;
+    const int lr = slot_row[sl] - (int)v0;
+    const int lc = w - (int)v0;
+    const double* b = vals + 9 * (int64_t)sl;
+    double* dst = S + (3 * lr) * m + 3 * lc;
 #pragma unroll
-  for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) blk[r * m + c] += b[3 * r + c];
+      for (int c = 0; c < 3; ++c) dst[r * m + c] += b[3 * r + c];
+  }
+  __syncthreads();
 }
 
 // write a symmetric m x m smem matrix (0.5 (X + X^T)) in cyclic-diagonal packing
@@ -381,7 +389,8 @@ __device__ __forceinline__ bool cyc_rep(int m, int i, int j) {
   return 2 * s < m || (2 * s == m && i < j);
 }
 
-// One CTA per subdomain: Mfull[d] -> Mblk (packed) and Bblk = sym(M^-1)
+// One CTA per subdomain: M_d assembled in smem (BSR + contacts) -> Mblk
+// (packed) and Bblk = sym(M^-1)
 // (mas.py:84-90).  The inverse is formed by the symmetric sweep operator
 // (Gauss-Jordan without pivoting, stable for SPD): after sweeping every
 // pivot the matrix holds -M^-1.  Its pivots are the Schur-complement
@@ -392,19 +401,24 @@ __device__ __forceinline__ bool cyc_rep(int m, int i, int j) {
 // barrier per step).  The matrix stays symmetric to rounding, so the
 // broadcast pivot row doubles as the pivot column.
 __global__ void __launch_bounds__(256, 2)
-k_mas_sweep(int64_t D, int64_t N, int bs, int m, const double* __restrict__ Mfull, double* __restrict__ Mblk,
+k_mas_sweep(int64_t D, int64_t N, int bs, int m, const unsigned char* __restrict__ pinned,
+            const int* __restrict__ inc_off, const int* __restrict__ inc, const int4* __restrict__ cverts,
+            const double* __restrict__ cgrad, const double* __restrict__ ck, const int* __restrict__ rowptr,
+            const int* __restrict__ slot_row, const int* __restrict__ cols, const double* __restrict__ bsr,
+            double* __restrict__ Mblk,
             double* __restrict__ Bblk, int* __restrict__ status) {
+  extern __shared__ double msm[];  // m x m: M_d
   __shared__ double rowk[2 * 96];
   const int64_t d = blockIdx.x;
   const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
   const int nd3 = 3 * (int)((N - d * bs) < bs ? (N - d * bs) : bs);
-  const double* src = Mfull + d * (int64_t)m * m;
+  assemble_block_smem(d, N, bs, m, pinned, inc_off, inc, cverts, cgrad, ck, rowptr, slot_row, cols, bsr, msm);
   const int64_t csz = cyc_size(m);
   double* mout = Mblk + d * csz;
   double R[SWEEP_T][SWEEP_T];
   // M_d (padding rows of a short last subdomain = identity), packed into Mblk
   auto load = [&](int i, int j) -> double {
-    double v = (i >= nd3 || j >= nd3) ? ((i == j) ? 1.0 : 0.0) : __ldg(src + i * m + j);
+    double v = (i >= nd3 || j >= nd3) ? ((i == j) ? 1.0 : 0.0) : msm[i * m + j];
     if (cyc_rep(m, i, j)) mout[cyc_index(m, i, j)] = v;
     return v;
   };

@@ -192,6 +192,7 @@ static void set_smem_limits() {
   allow((const void*)k_woodbury);
   allow((const void*)k_direct_update);
   allow((const void*)k_coarse_sweep);
+  allow((const void*)k_mas_sweep);
   done = true;
 }
 

@@ -115,8 +115,9 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
     max_ctas = std::max(1, sms * std::max(1, per));
   }
   const int grid = std::max(1, std::min(L.n_units, max_ctas));
+  static const int prof = getenv("MP_CS_PROF") ? 1 : 0;
   CoarseSweepArgs A{n, nT, L.n_units, L.cs_units.p, L.dense.p, L.cs_tiles.p, L.cs_col.p, L.inv.p, status,
-                    L.cs_bar.p};
+                    L.cs_bar.p, prof};
   void* args[] = {&A};
   CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_coarse_sweep, dim3(grid), dim3(CS_THREADS), args,
                                          coarse_sweep_smem(), L.st));
@@ -186,21 +187,12 @@ static void mas_build(mp_ctx* c) {
     dense_spd_inverse(c, L, c->counters.p + 4 + std::min(l, 3));
     CUDA_CHECK(cudaEventRecord(L.done, L.st));
   }
-  // level 0
-  c->Mfull.zero((size_t)D * m * m, c->stream);
+  // level 0: one CTA per subdomain assembles M_d in smem and sweeps it
   c->Bblk.ensure((size_t)D * cyc_size(m));
   c->Mblk.ensure((size_t)D * cyc_size(m));
-  if (nc) {
-    k_contact_blocks<<<grid_for(c->N, 128), 128, 0, c->stream>>>(c->N, c->pinned, c->inc_base.off, c->inc_base.val2,
-                                                                 c->base.verts, c->base.grad, c->base.k, c->bs, m,
-                                                                 c->Mfull);
-    LAUNCH_CHECK();
-  }
-  k_bsr_to_blocks<<<grid_for(c->nnzb, 128), 128, 0, c->stream>>>(c->nnzb, c->slot_row, c->cols, c->bsr, c->bs, m,
-                                                                 c->Mfull);
-  LAUNCH_CHECK();
-  k_mas_sweep<<<(unsigned)D, 256, 0, c->stream>>>(D, c->N, c->bs, m, c->Mfull, c->Mblk, c->Bblk,
-                                                    c->counters.p + 3);
+  k_mas_sweep<<<(unsigned)D, 256, sizeof(double) * m * m, c->stream>>>(
+      D, c->N, c->bs, m, c->pinned, nc ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->base.verts,
+      c->base.grad, c->base.k, c->rowptr, c->slot_row, c->cols, c->bsr, c->Mblk, c->Bblk, c->counters.p + 3);
   LAUNCH_CHECK();
   for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
   // one readback of every level's non-SPD flag (counters 3..7)

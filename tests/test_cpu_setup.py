@@ -85,3 +85,20 @@ def test_native_partition_is_morton_blocks():
     assert sub.max() == 6
     counts = np.bincount(sub)
     assert sorted(counts) == [5] + [8] * 6
+
+
+def test_c2_bench_scene_bit_identical_to_reference():
+    """Our config-2 builder gives the reference-built bench scene bit for bit
+    (sha256 over every array, recorded by tests/golden/make_c2_golden.py)."""
+    import hashlib
+
+    import bench
+
+    s = scenes.c2_stack(gap=bench.GAP)
+    h = hashlib.sha256()
+    el, sf = s.elastic, s.surface
+    for a in (s.mesh.rest_positions, el.tets, el.Bm, el.vol, el.mu, el.lam, s.mass, s.dirichlet, s.f_ext,
+              sf.triangles, sf.edges, sf.vertices):
+        h.update(np.ascontiguousarray(a).tobytes())
+    with np.load(ROOT / "tests" / "golden" / "c2_bench.npz") as z:
+        assert h.hexdigest() == str(z["scene_sha256"])

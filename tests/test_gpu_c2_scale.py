@@ -1,0 +1,125 @@
+"""Parity at BENCH scale (config 2: 46,664 V / 235,830 T, coarse orders 1095
+and 276): every hot-path stage of the device against the REFERENCE's own
+outputs at the state where bench.py's first timed frame starts
+(tests/golden/make_c2_golden.py ran ipcsim on it; the state is the GPU's,
+dumped by tools/c2_dump.py).
+
+Bars (BASELINE north_star): contact pairs and the CCD-active subdomain set
+bit-exact; gradient, preconditioned vectors, HVP, energy within 1e-9
+relative (norm-wise, FP64)."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _load(name):
+    with np.load(GOLD / name, allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.fixture(scope="module")
+def c2():
+    import bench
+    from paper_2604_19892_b200 import scenes, solver
+
+    g = _load("c2_bench.npz")
+    scene = scenes.c2_stack(gap=bench.GAP)
+    ctx = scene.context(solver.SolverConfig(iter_max=bench.ITER_MAX))
+    return g, scene, ctx
+
+
+def _sorted_pairs(verts, d, k):
+    order = np.lexsort(verts.T[::-1])
+    return verts[order], d[order], k[order]
+
+
+@pytest.mark.gpu
+def test_c2_constraint_set_bit_exact(c2):
+    g, _, ctx = c2
+    verts, is_pt, d, grad, k = ctx.constraint_set(g["x0"])
+    assert len(d) == len(g["cs_d"])
+    # both are in the reference's key order (contact.py:98-113)
+    assert np.array_equal(verts, g["cs_verts"].astype(np.int64))
+    assert np.array_equal(d, g["cs_d"])
+    assert rel_err(k, g["cs_k"]) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_c2_gradient_energy(c2):
+    g, _, ctx = c2
+    h = float(g["h"])
+    assert rel_err(ctx.gradient(g["x0"], g["x_tilde"], h), g["g"]) <= 1e-9
+    e = ctx.energy(g["x0"], g["x_tilde"], h)
+    assert abs(e - float(g["energy"])) <= 1e-9 * abs(float(g["energy"]))
+
+
+@pytest.mark.gpu
+def test_c2_mas_build_apply_hvp(c2):
+    """build_hierarchy (level-0 96x96 blocks, coarse 1095 / 276 through the
+    persistent coarse kernel) + apply_preconditioner + HessianModel.hvp."""
+    g, _, ctx = c2
+    ctx.snapshot(g["x0"], float(g["h"]), build_mas=True)
+    z = ctx.precond_apply(g["g"])
+    assert rel_err(z, g["z"]) <= 1e-9
+    hv = ctx.hvp(g["z"])
+    assert rel_err(hv, g["hv"]) <= 1e-9
+    # the restart step's scalars (solver.py:362-379)
+    mu = float(z @ g["g"]) / float(z @ ctx.hvp(z))
+    assert abs(mu - float(g["mu"])) <= 1e-9 * abs(float(g["mu"]))
+
+
+@pytest.mark.gpu
+def test_c2_ccd_restart_step(c2):
+    g, _, ctx = c2
+    ad, xn, ma, cert, n = ctx.ccd(g["x0"], g["p"], exact_set=True)
+    assert n == int(g["ccd_pairs"])
+    assert np.array_equal(ad < 1.0, g["alpha_d"] < 1.0)
+    assert rel_err(ad, g["alpha_d"]) <= 1e-9
+    assert cert == bool(g["ccd_certified"]) and abs(ma - float(g["ccd_min_alpha"])) <= 1e-9
+    assert rel_err(xn, g["x1"]) <= 1e-12
+    # the solver's tight enumeration: same alpha_d / minimum / certificate
+    ad2, xn2, ma2, cert2, _ = ctx.ccd(g["x0"], g["p"], exact_set=False)
+    assert np.array_equal(ad, ad2) and np.array_equal(xn, xn2) and ma == ma2 and cert == cert2
+
+
+@pytest.mark.gpu
+def test_c2_ccd_clamped(c2):
+    """A 40x restart step: many subdomains clamp (alpha_d < 1)."""
+    path = GOLD / "c2_bench_ccd.npz"
+    if not path.exists():
+        pytest.skip("c2_bench_ccd.npz not generated")
+    g, _, ctx = c2
+    r = _load("c2_bench_ccd.npz")
+    p = float(r["scale"]) * g["p"]
+    ad, xn, ma, cert, n = ctx.ccd(g["x0"], p, exact_set=True)
+    assert n == int(r["n_pairs"])
+    assert np.array_equal(ad < 1.0, r["alpha_d"] < 1.0)  # the CCD-active set, bit-exact
+    assert rel_err(ad, r["alpha_d"]) <= 1e-9
+    assert cert == bool(r["certified"]) and abs(ma - float(r["min_alpha"])) <= 1e-9 * max(1.0, abs(ma))
+    assert rel_err(xn, r["x_new"]) <= 1e-9
+    ad2, xn2, ma2, cert2, _ = ctx.ccd(g["x0"], p, exact_set=False)
+    assert np.array_equal(ad, ad2) and np.array_equal(xn, xn2) and ma == ma2 and cert == cert2
+
+
+@pytest.mark.gpu
+def test_c2_update_branch(c2):
+    """The non-rebuild branch at x1 against the x0 snapshot: classify_all,
+    select_top_k (K=8), build_update (Sparse-Input Woodbury), then z and HVP
+    with the candidates (solver.py:336-346)."""
+    g, _, ctx = c2
+    h = float(g["h"])
+    ctx.snapshot(g["x0"], h, build_mas=True)
+    nc, nt = ctx.update_at(g["x1"])
+    assert nc == int(g["n_candidates"]) and nt == int(g["n_touched"])
+    assert rel_err(ctx.gradient(g["x1"], g["x_tilde"], h), g["g1"]) <= 1e-9
+    ctx.snapshot(g["x0"], h, build_mas=True)
+    ctx.update_at(g["x1"])
+    z1 = ctx.precond_apply(g["g1"], with_updates=True)
+    assert rel_err(z1, g["z1"]) <= 1e-9
+    assert rel_err(ctx.hvp(g["z1"], with_updates=True), g["hv1"]) <= 1e-9
