@@ -9,9 +9,10 @@ scene (8 soft SNH cubes stacked on a pinned floor, 46,664 V / 235,830 T,
 BASELINE.json ``configs[1]``), every PNCG iteration on the device.
 
 Metric: PNCG iterations per second (whole job), with sec/frame alongside.
-Iterations/s is measured directly on a bounded sample by both arms; the
-per-frame iteration counts of the two arms agree within +-5% (the parity
-tests), so the ratio of the two is the solver speed-up.
+Both arms time the SAME frames: bench frame 6 onwards from a committed start
+state (tests/golden/c2_bench.npz, this solver's own state after 5 frames from
+rest, where the reference's stage taps were recorded); the CPU arms measure
+iterations/s on a bounded prefix of frame 6.
 
 * ``value``  -- device-resident frames (state resident in HBM, CUDA events on
   the context stream around each frame, L2 flushed between frames).
@@ -30,7 +31,8 @@ star); ``value`` = all ranks' iterations / max-over-ranks time.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 oracle port; the Python reference itself cannot travel to the GPU box) on
-the same workload, rank 0 only.
+the same frame from the same start state, rank 0 only, with 1 BLAS thread
+and with every host thread (the faster is the line's value).
 """
 
 from __future__ import annotations
@@ -58,6 +60,18 @@ SCENE_DESC = ("c2_stack: 8 SNH cubes (17^3 cells, 0.2 m, E=1e5) stacked 2x2x2 wi
 H = 0.01
 GAP = 5e-3
 ITER_MAX = 500
+# The timed frames start from this committed state: the GPU's own state after
+# 5 frames from rest (tools/c2_dump.py; the solver is bitwise deterministic,
+# so every box reaches the same bits), at which the reference's stage taps
+# were recorded (tests/golden/make_c2_golden.py).  Both arms time frames
+# from here, so they time the same frames whatever --warmup is.
+START = ROOT / "tests" / "golden" / "c2_bench.npz"
+START_FRAME = 6  # 1-based: the frame after the 5 frames that produced START
+
+
+def start_state():
+    with np.load(START) as z:
+        return z["x0"].copy(), z["v0"].copy()
 
 
 def _peaks():
@@ -122,11 +136,11 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_baseline(sample_iters=None, budget_s=30.0, threads=1):
-    """The oracle (numpy CPU restatement of the reference, oracle/) on a
-    bounded sample of the workload: PNCG iterations of frame 1 from rest
-    within a wall-clock budget, BLAS limited to `threads`.  Returns the
-    cpu_baseline object."""
+def _oracle_frame(budget_s, threads):
+    """PNCG iterations of bench frame START_FRAME (from the committed start
+    state) by the numpy oracle within a wall-clock budget; the scene, its
+    partition and the start state are prepared outside the timed call.
+    Returns (iterations, seconds)."""
     from threadpoolctl import threadpool_limits
 
     from oracle import solver as osolver
@@ -135,43 +149,71 @@ def cpu_baseline(sample_iters=None, budget_s=30.0, threads=1):
 
     scene = osolver.Scene.from_scene(scenes.c2_stack(gap=GAP))
     cfg = osolver.SolverConfig(iter_max=ITER_MAX)
-    x = scene.rest.ravel().copy()
-    v = np.zeros_like(x)
+    scene.partition(cfg.block_size)
+    x, v = start_state()
     with threadpool_limits(limits=threads):
-        iters, elapsed = osolver.timed_iterations(scene, x, v, H, cfg, budget_s=budget_s, max_iters=sample_iters)
+        return osolver.timed_iterations(scene, x, v, H, cfg, budget_s=budget_s)
+
+
+def cpu_baseline(budget_s=30.0, threads=1):
+    """The oracle (numpy CPU restatement of the reference, oracle/) on a
+    bounded sample of the same workload: the first timed frame, from the same
+    start state, single BLAS thread (BLAS threading slows this
+    path down).  Returns the cpu_baseline object."""
+    iters, elapsed = _oracle_frame(budget_s, threads)
     return {
         "value": iters / elapsed, "unit": "iters/s", "cores": threads, "kind": "port",
-        "sample": f"{iters} PNCG iterations of frame 1 of the same scene (from rest) by the numpy oracle, "
-                  f"{elapsed:.1f} s, single process, BLAS threads={threads}",
+        "sample": f"the first {iters} PNCG iterations of bench frame {START_FRAME} (the GPU arm's first timed "
+                  f"frame, same start state) by the numpy oracle, {elapsed:.1f} s, single process, BLAS "
+                  f"threads={threads}; scene/partition built outside the timed call",
     }
 
 
+def _host_cpu():
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                info["model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU implementation."""
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port: the Python reference cannot travel to the GPU box) on the
+    SAME frames as the GPU arm: bench frame START_FRAME from the committed
+    start state, iterations/s over one continuous bounded sample.  Measured
+    with one BLAS thread (the fastest setting for this path) and, for the
+    record, with every host thread; `value` is the faster of the two."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    per = []
-    total_it = 0
-    total_s = 0.0
-    budget = max(5.0, 60.0 / max(1, args.steps))
-    for s in range(args.warmup + args.steps):
-        cb = cpu_baseline(budget_s=budget if s >= args.warmup else 3.0, threads=threads)
-        it = int(cb["sample"].split()[0])
-        if s >= args.warmup:
-            per.append(cb["value"])
-            total_it += it
-            total_s += it / cb["value"]
-    value = total_it / total_s
+    nthreads = os.cpu_count() or 1
+    for _ in range(max(0, min(args.warmup, 1))):
+        _oracle_frame(2.0, 1)  # imports, BLAS init
+    budget = float(min(200.0, max(60.0, 10.0 * args.steps)))
+    it1, s1 = _oracle_frame(budget, 1)
+    budget_all = min(40.0, budget / 3.0)
+    itn, sn = _oracle_frame(budget_all, nthreads)
+    v1, vn = it1 / s1, itn / sn
+    value, threads, it, sec = (v1, 1, it1, s1) if v1 >= vn else (vn, nthreads, itn, sn)
     line = {
         "impl": "reference", "metric": "PNCG iters/sec", "value": value, "unit": "iters/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / max(1, args.steps),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": SCENE_DESC, "sample": "each step = PNCG iterations of frame 1 for a bounded "
-                                                     f"~{budget:.0f} s budget"},
+        "config": {"workload": SCENE_DESC, "iter_max": ITER_MAX, "same_frames": True,
+                   "frames": f"bench frame {START_FRAME} from the committed start state (tests/golden/c2_bench.npz) "
+                             "-- the GPU arm's first timed frame",
+                   "sample": f"one continuous {sec:.0f} s sample ({it} PNCG iterations) split evenly over the "
+                             f"{args.steps} steps"},
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "port",
-                         "sample": f"{total_it} PNCG iterations over {args.steps} steps"},
+                         "sample": f"{it} PNCG iterations of frame {START_FRAME} in {sec:.1f} s",
+                         "threads_1": {"iters_per_s": v1, "iters": it1, "s": round(s1, 1)},
+                         f"threads_{nthreads}": {"iters_per_s": vn, "iters": itn, "s": round(sn, 1)},
+                         "host": _host_cpu()},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -201,9 +243,13 @@ def run_ours(args):
     for _ in range(args.warmup):
         ctx.step_device(H)
     torch.cuda.synchronize()
+    xw, vw = ctx.get_state()
 
-    # the e2e leg replays the same frames from this state
-    x_start_h, v_start_h = ctx.get_state()
+    # the timed frames (and the e2e leg) start from the committed state
+    x_start_h, v_start_h = start_state()
+    warm_equals_start = bool(args.warmup == START_FRAME - 1 and np.array_equal(xw, x_start_h)
+                             and np.array_equal(vw, v_start_h)) if args.warmup == START_FRAME - 1 else None
+    ctx.set_state(x_start_h, v_start_h)
     # dry run of the timed frames: the solver is bitwise deterministic, so
     # this grows every capacity-driven buffer (pair lists, contact tables) to
     # its final size -- the timed frames then allocate nothing
@@ -322,13 +368,16 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": SCENE_DESC, "step": "one frame (prepare_step + advance_step)",
                    "l2": "flushed between timed frames (512 MiB write)",
-                   "parallelism": "replicas" if ws > 1 else "single-gpu", "iter_max": cfg.iter_max},
+                   "parallelism": "replicas" if ws > 1 else "single-gpu", "iter_max": cfg.iter_max,
+                   "frames": f"frames {START_FRAME}..{START_FRAME + args.steps - 1} from the committed start state "
+                             "(tests/golden/c2_bench.npz = this solver's state after 5 frames from rest)",
+                   "warmup_reaches_start_state": warm_equals_start},
         "sec_per_frame": t_max * 1e-3 / args.steps,
         "frames": frames,
         "e2e": {"value": e2e_all / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": 2 * 8 * n3,
                 "d2h_bytes_per_step": 2 * 8 * n3, "sec_per_frame": e2e_s / args.steps,
-                "frames": "the timed frames replayed from the same start state (iteration counts may differ "
-                          "slightly: FP64 atomics make contact frames chaotic)",
+                "frames": "the timed frames replayed from the same start state (the solver is bitwise "
+                          "deterministic: the same iterations as the device-resident pass)",
                 "api": "paper_2604_19892_b200.solver.step(scene, x, v, h, cfg) with pinned numpy x, v"},
         "roofline": roof("mas_apply_l0", "k_mas_apply_l0_direct (level-0 packed block matvec + Woodbury overlay + "
                                           "coarse prolongation + pinned projection; one CTA per subdomain, "

@@ -114,6 +114,17 @@ typedef struct mp_ctx mp_ctx;
 /* Create a context on `device`: uploads the scene, builds the Morton
  * partition (mas.py:30-77), the static BSR pattern and surface tables. */
 int mp_create(const mp_scene_desc* scene, const mp_solver_config* cfg, int device, mp_ctx** out);
+/* A partitioned multi-GPU context ("group"): one shard
+ * per entry of dev_ids (entries may repeat a device -- the equivalence tests
+ * run two shards on one GPU), each owning a contiguous Morton range of
+ * level-1 aggregates (mas.py:63-77).  mp_step / mp_advance / mp_step_device /
+ * mp_set_state / mp_get_state run on every shard (one host thread each);
+ * the results are bitwise those of a single-GPU context.  The stage taps
+ * need a single-GPU context.  n_dev == 1 is mp_create. */
+int mp_create_multi(const mp_scene_desc* scene, const mp_solver_config* cfg, int n_dev, const int* dev_ids,
+                    mp_ctx** out);
+/* number of shards of a context (1 for mp_create) */
+int mp_shards(mp_ctx* ctx);
 void mp_destroy(mp_ctx* ctx);
 int mp_set_config(mp_ctx* ctx, const mp_solver_config* cfg);
 const char* mp_status_code(int status);
@@ -240,6 +251,14 @@ const char* mp_create_error(void);
  * of the symmetric n x n row-major A; *not_spd = 1 (and inv undefined) where
  * cho_factor would raise non-spd-subdomain.  Test / parity entry point. */
 int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t* not_spd);
+
+/* Host-only: the owned ranges shard `rank` of `nshards` gets in a group
+ * (mp_create_multi): out[0..1] vertices [v0, v1) (renumbered, subdomain
+ * order), out[2..3] subdomains, out[4..5] level-1 aggregates, out[6..7]
+ * reduction chunks.  The unit is the level-1 aggregate (coarse_block
+ * subdomains) when a coarse level is built, else the subdomain. */
+int mp_shard_range(int64_t n_verts, int32_t block_size, int32_t levels, int32_t coarse_block, int32_t rank,
+                   int32_t nshards, int64_t* out);
 
 /* mas.partition_domain (mas.py:63-77) on the host, no GPU needed:
  * subdomain_of (n,) for a Morton partition into blocks of block_size. */

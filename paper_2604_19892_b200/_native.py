@@ -52,9 +52,9 @@ class IterRecordC(C.Structure):
 
 
 EXPORTS = (
-    "mp_create", "mp_destroy", "mp_set_config", "mp_status_code", "mp_last_error", "mp_stream", "mp_partition",
+    "mp_create", "mp_create_multi", "mp_shards", "mp_destroy", "mp_set_config", "mp_status_code", "mp_last_error", "mp_stream", "mp_partition",
     "mp_step", "mp_advance", "mp_broad_phase", "mp_constraint_set", "mp_gradient", "mp_energy", "mp_snapshot",
-    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_coarse_matrix", "mp_spd_inverse", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
+    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_coarse_matrix", "mp_spd_inverse", "mp_shard_range", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
 )
 
 STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd", "mas_apply_l0",
@@ -75,6 +75,9 @@ def load_library():
     lib = C.CDLL(str(LIB_PATH))
     vp = C.c_void_p
     lib.mp_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(SolverConfigC), C.c_int, C.POINTER(vp)]
+    lib.mp_create_multi.argtypes = [C.POINTER(SceneDesc), C.POINTER(SolverConfigC), C.c_int, C.POINTER(C.c_int),
+                                    C.POINTER(vp)]
+    lib.mp_shards.argtypes = [vp]
     lib.mp_destroy.argtypes = [vp]
     lib.mp_destroy.restype = None
     lib.mp_set_config.argtypes = [vp, C.POINTER(SolverConfigC)]
@@ -89,6 +92,7 @@ def load_library():
     lib.mp_launch_count.restype = C.c_int64
     lib.mp_partition.argtypes = [vp, _i64p, _i64p]
     lib.mp_partition_host.argtypes = [_f64p, C.c_int64, C.c_int32, _i64p]
+    lib.mp_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p]
     lib.mp_spd_inverse.argtypes = [C.c_int, C.c_int64, _f64p, _f64p, C.POINTER(C.c_int32)]
     rec = C.POINTER(IterRecordC)
     step_tail = [_f64p, _f64p, rec, C.c_int64, _i64p, C.POINTER(C.c_int32), C.POINTER(C.c_uint32)]
@@ -142,6 +146,17 @@ def partition_host(rest, block_size):
     return out
 
 
+def shard_range(n_verts, block_size, levels, coarse_block, rank, nshards):
+    """Host-only mirror of a group shard's owned ranges (mp_shard_range):
+    dict of (lo, hi) for vertices, subdomains, aggregates and chunks."""
+    lib = load_library()
+    out = np.zeros(8, np.int64)
+    raise_status(lib.mp_shard_range(int(n_verts), int(block_size), int(levels), int(coarse_block), int(rank),
+                                    int(nshards), _ptr(out, C.c_int64)), "mp_shard_range")
+    return {"verts": (int(out[0]), int(out[1])), "subdomains": (int(out[2]), int(out[3])),
+            "aggregates": (int(out[4]), int(out[5])), "chunks": (int(out[6]), int(out[7]))}
+
+
 def spd_inverse(A, device=0):
     """The device coarse-level inverse (mas.py:84-90) of a dense symmetric
     matrix: (sym(A^-1), not_spd)."""
@@ -172,7 +187,11 @@ class NativeContext:
             surf_verts=_ptr(a["surf_verts"], C.c_int64), d_hat=float(a["d_hat"]), kappa=float(a["kappa"]),
         )
         h = C.c_void_p()
-        st = lib.mp_create(C.byref(desc), C.byref(cfg), int(device), C.byref(h))
+        if isinstance(device, (list, tuple)):  # partitioned multi-GPU group
+            ids = (C.c_int * len(device))(*[int(d) for d in device])
+            st = lib.mp_create_multi(C.byref(desc), C.byref(cfg), len(device), ids, C.byref(h))
+        else:
+            st = lib.mp_create(C.byref(desc), C.byref(cfg), int(device), C.byref(h))
         if st != 0:
             raise_status(st, lib.mp_create_error().decode())
         self.h = h
@@ -202,6 +221,10 @@ class NativeContext:
     @property
     def stream(self):
         return self.lib.mp_stream(self.h)
+
+    @property
+    def shards(self):
+        return int(self.lib.mp_shards(self.h))
 
     @property
     def launches(self):

@@ -42,6 +42,8 @@ struct CoarseSweepArgs {
   double* inv;               // cyc_size(n) packed sym(M^-1)
   int* status;               // set to 1 when a pivot is not positive
   unsigned* bar;             // [0] arrival count, [1] generation
+  double* pmbuf;             // nT x 1024: -A_KK^-1 of each panel, published by the lookahead CTA
+  double* dbuf;              // nT x 1024: diagonal tile (K+1, K+1) as phase K starts (lookahead input)
   int prof;                  // debug: CTA 0 prints per-phase %globaltimer splits (MP_CS_PROF)
 };
 
@@ -116,6 +118,20 @@ __device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double*
   return true;
 }
 
+// W = A_IK A_KK^-1 = -C Pm (C = A_IK row-major in smem), 4 outputs per thread
+__device__ __forceinline__ void cs_compute_W(const double* Csm, const double* Pm, double* Wsm) {
+  const int i = threadIdx.x >> 3, j0 = (threadIdx.x & 7) * 4;
+  double w4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int d = 0; d < 32; ++d) {
+    const double a = Csm[i * CS_LD + d];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w4[q] = fma(-a, Pm[d * CS_LD + j0 + q], w4[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Wsm[i * CS_LD + j0 + q] = w4[q];
+}
+
 // A unit's panel tiles into registers: pre[0] = A_IK, pre[1 + q] = A_{J0+q, K};
 // element w = tid + 256 s of each tile.  Unrolled, predicated: every load is
 // in flight at once.
@@ -157,6 +173,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
       const double v = (i < n && j < n) ? A.dense[(int64_t)i * n + j] : (i == j ? 1.0 : 0.0);
       A.tiles[e] = v;
       if (J == 0) A.colbuf[(int64_t)I * 1024 + w] = v;
+      if (J == I) A.dbuf[(int64_t)I * 1024 + w] = v;
     }
   }
   cs_grid_sync(A.bar);
@@ -164,21 +181,67 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
   for (int K = 0; K < nT; ++K) {
     const double* cur = A.colbuf + (int64_t)(K & 1) * nT * 1024;
     double* nxt = A.colbuf + (int64_t)((K + 1) & 1) * nT * 1024;
-    // the first unit's panel tiles are fetched before the pivot sweep (all
-    // loads in flight in registers; the sweep hides their L2 latency)
+    // CTA 0 is the lookahead CTA (when there are others): it publishes
+    // -A_{K+1,K+1}^-1 for the next phase; the units are spread over the rest
+    const int G1 = G > 1 ? G - 1 : 1;
+    const int self = G > 1 ? (int)blockIdx.x - 1 : 0;
+    // the first unit's panel tiles are fetched before the pivot block (all
+    // loads in flight in registers, hiding the L2 latency)
     double pre[1 + CS_CH][4];
     const unsigned long long t0 = A.prof ? cs_now() : 0ull;
-    int u = blockIdx.x;
-    if (u < A.n_units) cs_load_unit(cur, A.units[u], K, pre);
-    // (1) every CTA sweeps the pivot block itself
-    const bool ok = cs_pivot_sweep(cur + (int64_t)K * 1024, Pm, Wsm);
-    __syncthreads();
-    const unsigned long long t1 = A.prof ? cs_now() : 0ull;
-    if (!ok) {  // the same bits in every CTA: all leave at the same panel
-      if (blockIdx.x == 0 && tid == 0) atomicExch(A.status, 1);
-      return;
+    int u = self;
+    if (self >= 0 && u < A.n_units) cs_load_unit(cur, A.units[u], K, pre);
+    // (1) Pm = -A_KK^-1: swept by every CTA at K = 0, then published one phase ahead
+    if (K == 0) {
+      const bool ok0 = cs_pivot_sweep(cur, Pm, Wsm);
+      __syncthreads();
+      if (!ok0) {  // the same bits in every CTA: all leave together
+        if (blockIdx.x == 0 && tid == 0) atomicExch(A.status, 1);
+        return;
+      }
+    } else {
+      for (int w = tid; w < 1024; w += CS_THREADS) Pm[(w >> 5) * CS_LD + (w & 31)] = __ldcg(A.pmbuf + (int64_t)K * 1024 + w);
+      __syncthreads();
     }
-    for (; u < A.n_units; u += G) {
+    const unsigned long long t1 = A.prof ? cs_now() : 0ull;
+    // (1b) lookahead: the diagonal tile (K+1, K+1) after this phase's update
+    // -- the same operations in the same order as its owner unit, so the
+    // same bits -- swept at once; its inverse is the next phase's Pm
+    if (blockIdx.x == 0 && K + 1 < nT) {
+      const double* ck = cur + (int64_t)(K + 1) * 1024;  // A_{K+1,K}
+      for (int w = tid; w < 1024; w += CS_THREADS) {
+        const double a = __ldcg(ck + w);
+        Csm[(w >> 5) * CS_LD + (w & 31)] = a;
+        Bsm[(w & 31) * CS_LD + (w >> 5)] = a;
+      }
+      __syncthreads();
+      cs_compute_W(Csm, Pm, Wsm);
+      __syncthreads();
+      const int tr = tid >> 5, tc = tid & 31;
+      double acc[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = __ldcg(A.dbuf + (int64_t)(K + 1) * 1024 + (tr * 4 + r) * 32 + tc);
+#pragma unroll 4
+      for (int d = 0; d < 32; ++d) {
+        const double b = Bsm[d * CS_LD + tc];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r] = fma(-Wsm[(tr * 4 + r) * CS_LD + d], b, acc[r]);
+      }
+      double* scratch = A.pmbuf + (int64_t)(K + 1) * 1024;  // P' staged here, then overwritten by -P'^-1
+#pragma unroll
+      for (int r = 0; r < 4; ++r) scratch[(tr * 4 + r) * 32 + tc] = acc[r];
+      __syncthreads();
+      double* Pn = Bsm + 32 * CS_LD;
+      const bool okn = cs_pivot_sweep(scratch, Pn, Csm);
+      __syncthreads();
+      if (!okn) {
+        if (tid == 0) atomicExch(A.status, 1);  // every CTA leaves after this phase's barrier
+      } else {
+        for (int w = tid; w < 1024; w += CS_THREADS) scratch[w] = Pn[(w >> 5) * CS_LD + (w & 31)];
+      }
+      __syncthreads();
+    }
+    for (; self >= 0 && u < A.n_units; u += G1) {
       const int2 uc = A.units[u];
       const int I = uc.x, c = uc.y;
       const int J0 = CS_CH * c, J1 = min(CS_CH * c + CS_CH, I + 1);
@@ -187,7 +250,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
           for (int w = tid; w < 1024; w += CS_THREADS) A.tiles[cs_tile(K, K) + w] = Pm[(w >> 5) * CS_LD + (w & 31)];
         continue;
       }
-      if (u != (int)blockIdx.x) cs_load_unit(cur, uc, K, pre);
+      if (u != self) cs_load_unit(cur, uc, K, pre);
       // (2) own column tile A_IK (row-major) and the chunk's A_JK (transposed, k-major)
 #pragma unroll
       for (int s4 = 0; s4 < 4; ++s4) {
@@ -198,19 +261,8 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
           if (q < J1 - J0) Bsm[q * 32 * CS_LD + (w & 31) * CS_LD + (w >> 5)] = pre[1 + q][s4];
       }
       __syncthreads();
-      // (3) W_I = A_IK A_KK^-1 = -A_IK Pm (4 outputs per thread)
-      {
-        const int i = tid >> 3, j0 = (tid & 7) * 4;
-        double w4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
-        for (int d = 0; d < 32; ++d) {
-          const double a = Csm[i * CS_LD + d];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) w4[q] = fma(-a, Pm[d * CS_LD + j0 + q], w4[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Wsm[i * CS_LD + j0 + q] = w4[q];
-      }
+      // (3) W_I = A_IK A_KK^-1 = -A_IK Pm
+      cs_compute_W(Csm, Pm, Wsm);
       __syncthreads();
       // (4) the chunk's tiles: rows tr*4 + r, column tc of tile J0 + q
       const int tr = tid >> 5, tc = tid & 31;
@@ -245,6 +297,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
           const int i = tr * 4 + r;
           const double v = (J == K) ? Wsm[i * CS_LD + tc] : acc[r][q];  // A_IK <- W_I (I > K)
           T[i * 32 + tc] = v;
+          if (I == J && I == K + 2) A.dbuf[(int64_t)I * 1024 + i * 32 + tc] = v;  // next phase's lookahead input
           if (K + 1 < nT) {
             if (J == K + 1) nxt[(int64_t)I * 1024 + i * 32 + tc] = v;       // A_{I,K+1}, I >= K+1
             else if (I == K + 1) nxt[(int64_t)J * 1024 + tc * 32 + i] = v;  // A_{J,K+1} = A_{K+1,J}^T
@@ -265,8 +318,9 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
     }
     const unsigned long long t2 = A.prof ? cs_now() : 0ull;
     cs_grid_sync(A.bar);
-    if (A.prof && blockIdx.x == 0 && tid == 0 && K < 4)
-      printf("cs phase %d: sweep %llu ns, units %llu ns, barrier %llu ns\n", K, t1 - t0, t2 - t1, cs_now() - t2);
+    if (A.prof && blockIdx.x == 1 && tid == 0 && K < 4)
+      printf("cs phase %d: pivot %llu ns, units %llu ns, barrier %llu ns\n", K, t1 - t0, t2 - t1, cs_now() - t2);
+    if (*(volatile int*)A.status) return;  // the lookahead found a non-positive pivot: all leave
   }
 
   // ---- pack sym(-A) in the cyclic layout (common.cuh) ----

@@ -123,8 +123,8 @@ __global__ void k_inc_gather_add(int64_t N, const unsigned char* __restrict__ pi
                                  const int* __restrict__ a_off, const int* __restrict__ a_val,
                                  const double* __restrict__ a_buf, const int* __restrict__ b_off,
                                  const int* __restrict__ b_val, const double* __restrict__ b_buf,
-                                 double* __restrict__ out) {
-  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                                 double* __restrict__ out, int64_t v0) {
+  const int64_t v = v0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // rows [v0, N)
   const int lane = threadIdx.x & 31;
   if (v >= N || pinned[v]) return;  // warp-uniform
   const bool ha = a_off && a_off[v + 1] > a_off[v], hb = b_off && b_off[v + 1] > b_off[v];

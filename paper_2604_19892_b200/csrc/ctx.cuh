@@ -11,6 +11,10 @@
 
 
 #include <string>
+#include <thread>
+#include <mutex>
+#include <condition_variable>
+#include <atomic>
 #include <chrono>
 #include <vector>
 
@@ -108,7 +112,7 @@ struct CoarseLevel {
   // the coarse inverse (coarse.cuh): work units, lower tiles, panel columns, grid barrier
   DBuf<int2> cs_units;
   int n_units = 0;
-  DBuf<double> cs_tiles, cs_col;
+  DBuf<double> cs_tiles, cs_col, cs_pm, cs_diag;
   DBuf<unsigned> cs_bar;
   int chunks = 1;
   // each coarse level is built on its own stream (st2: its contact terms),
@@ -135,8 +139,21 @@ struct StageTimer {
   int64_t count = 0;
 };
 
+struct Group;
+
 struct mp_ctx {
   int device = 0;
+  // ---- shard of a multi-GPU group (group.cuh); one GPU: rank 0 of 1 owning everything ----
+  Group* grp = nullptr;
+  int rank = 0, nshards = 1;
+  int64_t own_v0 = 0, own_v1 = 0;  // owned vertices (aligned to level-1 aggregates)
+  int64_t own_d0 = 0, own_d1 = 0;  // owned subdomains
+  int64_t own_a0 = 0, own_a1 = 0;  // owned level-1 aggregates
+  int64_t chunk_v = 32;            // vertices per reduction chunk (= the alignment unit)
+  int64_t n_chunks = 1, own_c0 = 0, own_c1 = 1;
+  DBuf<double> chunk_part;         // n_chunks * MAX_DOTS chunk partials
+  std::vector<double> h_part;      // host copy (single shard) for the ordered chunk sum
+  int par_dots = 0, par_flags = 0; // double-buffer parities of the group's host exchange arrays
   bool timing = false;
   bool ccd_exact_set = false;
   bool record_energy = false;

@@ -131,10 +131,10 @@ __global__ void k_grad_gather(int64_t N, const double* __restrict__ x, const dou
                               const int* __restrict__ vt_off, const int* __restrict__ vt_val,
                               const double* __restrict__ fbuf, const int* __restrict__ c_off,
                               const int* __restrict__ c_val, const double* __restrict__ cbuf,
-                              double* __restrict__ g) {
-  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                              double* __restrict__ g, int64_t v0, int64_t v1) {
+  const int64_t v = v0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);  // [v0, v1): owned rows
   const int lane = threadIdx.x & 31;
-  if (v >= N) return;  // warp-uniform
+  if (v >= v1) return;  // warp-uniform
   if (pinned[v]) {
     if (lane < 3) g[3 * v + lane] = 0.0;
     return;
@@ -385,9 +385,10 @@ __global__ void k_hess_gather(int64_t nnzb, const int* __restrict__ slot_row, co
 
 // y = BSR x ; 8 lanes per block row, lanes stride over the row's blocks
 __global__ void k_bsr_spmv(int64_t N, const int* __restrict__ rowptr, const int* __restrict__ cols,
-                           const double* __restrict__ vals, const double* __restrict__ xin, double* __restrict__ y) {
+                           const double* __restrict__ vals, const double* __restrict__ xin, double* __restrict__ y,
+                           int64_t r0) {
   int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t row = gt >> 3;
+  int64_t row = r0 + (gt >> 3);  // N: end of the launch's row range [r0, N)
   int lane = threadIdx.x & 7;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (row < N) {
@@ -435,8 +436,8 @@ static void gradient_gather(mp_ctx* c, const double* x, const double* xt, double
                                                                    c->fbuf);
     LAUNCH_CHECK();
   }
-  k_grad_gather<<<grid_for(32 * c->N, 128), 128, 0, c->stream>>>(c->N, x, xt, c->mass, c->pinned, c->vt_off, c->vt_val,
-                                                            c->fbuf, c_off, c_val, cbuf, g);
+  k_grad_gather<<<grid_for(32 * (c->own_v1 - c->own_v0), 128), 128, 0, c->stream>>>(
+      c->N, x, xt, c->mass, c->pinned, c->vt_off, c->vt_val, c->fbuf, c_off, c_val, cbuf, g, c->own_v0, c->own_v1);
   LAUNCH_CHECK();
 }
 
@@ -457,6 +458,7 @@ static void assemble_elastic_bsr(mp_ctx* c, const double* x, double h) {
 }
 
 static void bsr_spmv(mp_ctx* c, const double* xin, double* y) {
-  k_bsr_spmv<<<grid_for(8 * c->N, 256), 256, 0, c->stream>>>(c->N, c->rowptr, c->cols, c->bsr, xin, y);
+  k_bsr_spmv<<<grid_for(8 * (c->own_v1 - c->own_v0), 256), 256, 0, c->stream>>>(c->own_v1, c->rowptr, c->cols, c->bsr,
+                                                                                 xin, y, c->own_v0);
   LAUNCH_CHECK();
 }

@@ -406,10 +406,10 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const unsigned char* __restrict
             const double* __restrict__ cgrad, const double* __restrict__ ck, const int* __restrict__ rowptr,
             const int* __restrict__ slot_row, const int* __restrict__ cols, const double* __restrict__ bsr,
             double* __restrict__ Mblk,
-            double* __restrict__ Bblk, int* __restrict__ status) {
+            double* __restrict__ Bblk, int* __restrict__ status, int64_t d0) {
   extern __shared__ double msm[];  // m x m: M_d
   __shared__ double rowk[2 * 96];
-  const int64_t d = blockIdx.x;
+  const int64_t d = d0 + blockIdx.x;  // d0: a shard's first owned subdomain
   const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
   const int nd3 = 3 * (int)((N - d * bs) < bs ? (N - d * bs) : bs);
   assemble_block_smem(d, N, bs, m, pinned, inc_off, inc, cverts, cgrad, ck, rowptr, slot_row, cols, bsr, msm);
@@ -663,8 +663,8 @@ __global__ void k_pack_neg_sym(int n, const double* __restrict__ A, double* __re
 // restriction r = C g = raw sum * (1 / |a|) (the reference's aggregation
 // weights 1/len(verts), mas.py:123-135)
 __global__ void k_restrict1(int64_t N, int span, const double* __restrict__ g, double* __restrict__ rsum,
-                            double* __restrict__ r) {
-  const int64_t a = blockIdx.x;
+                            double* __restrict__ r, int64_t a0) {
+  const int64_t a = a0 + blockIdx.x;  // a0: a shard's first owned aggregate
   const int64_t v0 = a * span;
   int64_t v1 = v0 + span;
   if (v1 > N) v1 = N;
@@ -774,6 +774,7 @@ struct LevelView {
 struct LevelViews {
   LevelView lv[8];
   int L;
+  int64_t d0;  // first subdomain of this launch (a shard's owned range; 0 on one GPU)
 };
 
 // ---------------------------------------------------------------------------
@@ -847,7 +848,8 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
   const int i = tid - 96 * grp;
   // chunk boundaries in doubles, multiples of 2 (16 B)
   const int64_t chunk = ((csz + APPLY_CHUNKS - 1) / APPLY_CHUNKS + 1) & ~1ll;
-  auto src_of = [&](int64_t d) -> const double* {
+  auto src_of = [&](int64_t dl) -> const double* {
+    const int64_t d = LV.d0 + dl;
     const int ov = overlay_of ? overlay_of[d] : -1;
     return (ov >= 0) ? overlay + (int64_t)ov * csz : Bblk + d * csz;
   };
@@ -898,7 +900,8 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
       if (dn < D) issue_async(sn, dn);
       else cp_async_commit();  // empty group keeps the wait_group count uniform
     }
-    const int64_t v0 = d * bs;
+    const int64_t da = LV.d0 + d;
+    const int64_t v0 = da * bs;
     const int nd3 = 3 * (int)((N - v0) < bs ? (N - v0) : bs);
     if (tid < m) gsh[tid] = (tid < nd3) ? g[3 * v0 + tid] : 0.0;
     if (USE_TMA) {
@@ -936,7 +939,7 @@ k_mas_apply_l0(int64_t D, int64_t N, int bs, int m, const double* __restrict__ B
       const int c = i - 3 * (i / 3);
       for (int l = 0; l < LV.L; ++l) {
         const LevelView& L = LV.lv[l];
-        const int64_t a = d / L.ratio;
+        const int64_t a = da / L.ratio;
         const int64_t na = (N - a * L.span) < L.span ? (N - a * L.span) : L.span;
         acc += L.y[3 * a + c] * (1.0 / (double)na);
       }
@@ -962,7 +965,7 @@ k_mas_apply_l0_direct(int64_t D, int64_t N, int bs, int m, const double* __restr
                       double* __restrict__ z) {
   __shared__ double gsh[96];
   __shared__ double part[96];
-  const int64_t d = blockIdx.x;
+  const int64_t d = LV.d0 + blockIdx.x;
   const int tid = threadIdx.x;
   const int grp = tid >= 96 ? 1 : 0;
   const int i = tid - 96 * grp;
@@ -1034,12 +1037,14 @@ k_mas_apply_l0_direct(int64_t D, int64_t N, int bs, int m, const double* __restr
 __global__ void k_woodbury(int64_t N, int bs, int m, int Kmax, const double* __restrict__ Bblk,
                            const int* __restrict__ tsub, const int* __restrict__ tstart, const int* __restrict__ tlen,
                            const int* __restrict__ ecand, const int4* __restrict__ cverts,
-                           const double* __restrict__ cu, double* __restrict__ overlay, int* __restrict__ status) {
+                           const double* __restrict__ cu, double* __restrict__ overlay, int* __restrict__ status,
+                           int64_t d0, int64_t d1) {
   extern __shared__ double sm[];
   const int t = blockIdx.x;
   const int d = tsub[t];
   const int K = tlen[t];
-  if (K > Kmax) return;  // handled by k_direct_update
+  if (K > Kmax) return;       // handled by k_direct_update
+  if (d < d0 || d >= d1) return;  // another shard's subdomain
   double* B = sm;
   double* U = B + m * m;
   double* W = U + m * Kmax;
@@ -1116,12 +1121,13 @@ __global__ void k_direct_update(int64_t N, int bs, int m, const double* __restri
                                 const int* __restrict__ tsub, const int* __restrict__ tstart,
                                 const int* __restrict__ tlen, const int* __restrict__ ecand,
                                 const int4* __restrict__ cverts, const double* __restrict__ cu, int Kthresh,
-                                double* __restrict__ overlay, int* __restrict__ status) {
+                                double* __restrict__ overlay, int* __restrict__ status, int64_t d0, int64_t d1) {
   extern __shared__ double sm[];
   const int t = blockIdx.x;
   const int K = tlen[t];
   if (K <= Kthresh) return;
   const int d = tsub[t];
+  if (d < d0 || d >= d1) return;  // another shard's subdomain
   double* A = sm;
   double* X = sm + m * m;
   __shared__ int bad;

@@ -15,6 +15,14 @@
 thread_local int64_t* g_launch_counter = nullptr;
 
 mp_ctx::~mp_ctx() {
+  if (grp && rank == 0) {  // the group's shard 0 owns the other shards and the group
+    for (size_t q = 1; q < grp->sh.size(); ++q) delete grp->sh[q];
+    for (int q = 0; q < GROUP_MAX; ++q) {
+      if (grp->ev[q]) cudaEventDestroy(grp->ev[q]);
+      if (grp->ev2[q]) cudaEventDestroy(grp->ev2[q]);
+    }
+    delete grp;
+  }
   for (auto* l : levels) delete l;
   if (h_scal) cudaFreeHost(h_scal);
   if (h_cnt) cudaFreeHost(h_cnt);
@@ -171,6 +179,7 @@ static void setup_levels(mp_ctx* c) {
     units = n_agg;
   }
   c->n_levels = (int)c->levels.size();
+  group_ranges(c, c->rank, c->nshards);  // owned ranges and reduction chunks follow the level-1 aggregates
 }
 
 static void set_smem_limits() {
@@ -422,7 +431,16 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R);
 
 static void advance_loop(mp_ctx* c, double h, LoopResult& R) {
   const auto t0 = Clock::now();
-  advance_loop_body(c, h, R);
+  if (c->nshards > 1) {
+    // every shard runs the loop (SPMD, lockstep); shard 0's records are the group's
+    run_shards(c, [&](mp_ctx* sc) {
+      LoopResult Rs;
+      advance_loop_body(sc, h, Rs);
+      if (sc->rank == 0) R = std::move(Rs);
+    });
+  } else {
+    advance_loop_body(c, h, R);
+  }
   if (c->timing) {
     c->loop_ms += ms_since(t0);
     c->n_loop += 1;
@@ -635,6 +653,34 @@ static void download_vec_old(mp_ctx* c, const double* dev, double* host) {
   sync_stream(c);
 }
 
+// sequential per-shard host work (uploads) on each shard's device
+template <class Fn>
+static void each_shard(mp_ctx* c, Fn&& fn) {
+  if (c->nshards <= 1 || !c->grp) {
+    fn(c);
+    return;
+  }
+  int64_t* saved = g_launch_counter;
+  for (mp_ctx* sc : c->grp->sh) {
+    CUDA_CHECK(cudaSetDevice(sc->device));
+    g_launch_counter = &sc->launches;
+    fn(sc);
+  }
+  g_launch_counter = saved;
+  CUDA_CHECK(cudaSetDevice(c->device));
+}
+
+static void prepare_on(mp_ctx* sc, double h) {
+  k_prepare<<<grid_for(3 * sc->N, 256), 256, 0, sc->stream>>>(sc->N, sc->x, sc->vel, sc->mass, sc->f_ext, sc->pinned,
+                                                              h, sc->xt);
+  LAUNCH_CHECK();
+}
+
+// stage taps evaluate one device stage on a whole scene: single-GPU contexts
+static void single_gpu_only(mp_ctx* c) {
+  if (c->nshards > 1) throw MpError(MP_ERR_CONFIG, "stage taps run on single-GPU contexts (mp_create)");
+}
+
 extern "C" {
 
 const char* mp_status_code(int status) {
@@ -646,7 +692,13 @@ const char* mp_last_error(mp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : 
 
 void* mp_stream(mp_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
-int64_t mp_launch_count(mp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t mp_launch_count(mp_ctx* ctx) {
+  if (!ctx) return 0;
+  if (!ctx->grp) return ctx->launches;
+  int64_t n = 0;
+  for (mp_ctx* sc : ctx->grp->sh) n += sc->launches;
+  return n;
+}
 
 int mp_stage_timing(mp_ctx* c, int enable) {
   return guarded(c, [&] {
@@ -715,8 +767,70 @@ int mp_create(const mp_scene_desc* scene, const mp_solver_config* cfg, int devic
   return MP_OK;
 }
 
+int mp_create_multi(const mp_scene_desc* scene, const mp_solver_config* cfg, int n_dev, const int* dev_ids,
+                    mp_ctx** out) {
+  *out = nullptr;
+  if (n_dev < 1 || n_dev > GROUP_MAX || !dev_ids) {
+    g_create_error = "n_dev must lie in [1, 16]";
+    return MP_ERR_CONFIG;
+  }
+  if (n_dev == 1) return mp_create(scene, cfg, dev_ids[0], out);
+  std::vector<mp_ctx*> sh(n_dev, nullptr);
+  for (int q = 0; q < n_dev; ++q) {
+    const int st = mp_create(scene, cfg, dev_ids[q], &sh[q]);
+    if (st != MP_OK) {
+      for (mp_ctx* s2 : sh)
+        if (s2) mp_destroy(s2);
+      return st;
+    }
+  }
+  Group* G = new Group();
+  G->sh = sh;
+  G->bar.n = n_dev;
+  int st = guarded(sh[0], [&] {
+    // peer access between distinct devices (exchanges are peer copies over NVLink)
+    for (int a = 0; a < n_dev; ++a)
+      for (int b = 0; b < n_dev; ++b) {
+        const int da = dev_ids[a], db = dev_ids[b];
+        if (da == db) continue;
+        int can = 0;
+        CUDA_CHECK(cudaDeviceCanAccessPeer(&can, da, db));
+        if (!can) continue;
+        CUDA_CHECK(cudaSetDevice(da));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_CHECK(e);
+        cudaGetLastError();
+      }
+    for (int q = 0; q < n_dev; ++q) {
+      CUDA_CHECK(cudaSetDevice(dev_ids[q]));
+      CUDA_CHECK(cudaEventCreateWithFlags(&G->ev[q], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&G->ev2[q], cudaEventDisableTiming));
+      sh[q]->grp = G;
+      sh[q]->rank = q;
+      sh[q]->nshards = n_dev;
+      group_ranges(sh[q], q, n_dev);
+    }
+    CUDA_CHECK(cudaSetDevice(dev_ids[0]));
+    const size_t np = (size_t)sh[0]->n_chunks * MAX_DOTS;
+    for (auto& hp : G->hpart) CUDA_CHECK(cudaMallocHost(&hp, sizeof(double) * np));
+  });
+  if (st != MP_OK) {
+    g_create_error = sh[0]->last_error;
+    mp_destroy(sh[0]);
+    return st;
+  }
+  *out = sh[0];
+  return MP_OK;
+}
+
 void mp_destroy(mp_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->grp && ctx->rank != 0) return;  // shards are owned by shard 0
+  if (ctx->grp)
+    for (mp_ctx* sc : ctx->grp->sh) {
+      cudaSetDevice(sc->device);
+      cudaStreamSynchronize(sc->stream);
+    }
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   delete ctx;
@@ -728,11 +842,19 @@ int mp_set_config(mp_ctx* c, const mp_solver_config* cfg) {
     if (cfg->block_size != c->cfg.block_size)
       throw MpError(MP_ERR_CONFIG, "block_size is fixed per context (partition); create a new context");
     const bool relevel = cfg->levels != c->cfg.levels || cfg->coarse_block != c->cfg.coarse_block;
-    c->cfg = *cfg;
-    // the hierarchy (streams, handles, gather maps) only depends on the MAS
-    // depth; the per-call config of the Python API re-sets the rest freely
-    if (relevel) setup_levels(c);
-    c->have_mas = false;
+    // the hierarchy (streams, gather maps) only depends on the MAS depth; the
+    // per-call config of the Python API re-sets the rest freely
+    each_shard(c, [&](mp_ctx* sc) {
+      sc->cfg = *cfg;
+      if (relevel) setup_levels(sc);
+      sc->have_mas = false;
+    });
+    if (relevel && c->grp) {  // the group's chunk partial buffers follow the new chunk count
+      for (auto& hp : c->grp->hpart) {
+        if (hp) cudaFreeHost(hp);
+        CUDA_CHECK(cudaMallocHost(&hp, sizeof(double) * (size_t)c->n_chunks * MAX_DOTS));
+      }
+    }
   });
 }
 
@@ -774,6 +896,29 @@ int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t*
   });
 }
 
+int mp_shard_range(int64_t n_verts, int32_t block_size, int32_t levels, int32_t coarse_block, int32_t rank,
+                   int32_t nshards, int64_t* out) {
+  if (n_verts < 1 || block_size < 1 || coarse_block < 1 || nshards < 1 || rank < 0 || rank >= nshards)
+    return MP_ERR_CONFIG;
+  // the unit group_ranges aligns to: the level-1 aggregate (mas.py:155-169)
+  // when one is built, else the subdomain
+  const int64_t D = (n_verts + block_size - 1) / block_size;
+  const bool coarse = levels >= 1 && (D + coarse_block - 1) / coarse_block != D;
+  const int64_t U = coarse ? (int64_t)block_size * coarse_block : (int64_t)block_size;
+  const int64_t NU = (n_verts + U - 1) / U;
+  const int64_t u0 = NU * rank / nshards, u1 = NU * (rank + 1) / nshards;
+  const int64_t v0 = std::min(n_verts, u0 * U), v1 = std::min(n_verts, u1 * U);
+  out[0] = v0;
+  out[1] = v1;
+  out[2] = v0 / block_size;
+  out[3] = (v1 + block_size - 1) / block_size;
+  out[4] = coarse ? u0 : 0;
+  out[5] = coarse ? u1 : 0;
+  out[6] = u0;  // reduction chunks
+  out[7] = u1;
+  return MP_OK;
+}
+
 int mp_partition_host(const double* rest, int64_t n, int32_t block_size, int64_t* subdomain_of) {
   if (n < 1 || block_size < 1) return MP_ERR_CONFIG;
   try {
@@ -807,8 +952,10 @@ int mp_advance(mp_ctx* c, const double* x, const double* v, const double* x_tild
                double* v_out, mp_iter_record* recs, int64_t cap, int64_t* n_recs, int32_t* converged,
                uint32_t* flags) {
   return guarded(c, [&] {
-    upload_vec_new(c, x, c->x);
-    upload_vec_new(c, x_tilde, c->xt);
+    each_shard(c, [&](mp_ctx* sc) {
+      upload_vec_new(sc, x, sc->x);
+      upload_vec_new(sc, x_tilde, sc->xt);
+    });
     LoopResult R;
     advance_loop(c, h, R);
     download_vec_old(c, c->x, x_out);
@@ -820,11 +967,11 @@ int mp_advance(mp_ctx* c, const double* x, const double* v, const double* x_tild
 int mp_step(mp_ctx* c, const double* x, const double* v, double h, double* x_out, double* v_out,
             mp_iter_record* recs, int64_t cap, int64_t* n_recs, int32_t* converged, uint32_t* flags) {
   return guarded(c, [&] {
-    upload_vec_new(c, x, c->x);
-    upload_vec_new(c, v, c->vel);
-    k_prepare<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, c->x, c->vel, c->mass, c->f_ext, c->pinned, h,
-                                                              c->xt);
-    LAUNCH_CHECK();
+    each_shard(c, [&](mp_ctx* sc) {
+      upload_vec_new(sc, x, sc->x);
+      upload_vec_new(sc, v, sc->vel);
+      prepare_on(sc, h);
+    });
     LoopResult R;
     advance_loop(c, h, R);
     download_vec_old(c, c->x, x_out);
@@ -837,9 +984,7 @@ int mp_step(mp_ctx* c, const double* x, const double* v, double h, double* x_out
 int mp_step_device(mp_ctx* c, double h, mp_iter_record* recs, int64_t cap, int64_t* n_recs, int32_t* converged,
                    uint32_t* flags) {
   return guarded(c, [&] {
-    k_prepare<<<grid_for(3 * c->N, 256), 256, 0, c->stream>>>(c->N, c->x, c->vel, c->mass, c->f_ext, c->pinned, h,
-                                                              c->xt);
-    LAUNCH_CHECK();
+    each_shard(c, [&](mp_ctx* sc) { prepare_on(sc, h); });
     LoopResult R;
     advance_loop(c, h, R);
     fill_records(R, recs, cap, n_recs, converged, flags);
@@ -848,9 +993,11 @@ int mp_step_device(mp_ctx* c, double h, mp_iter_record* recs, int64_t cap, int64
 
 int mp_set_state(mp_ctx* c, const double* x, const double* v) {
   return guarded(c, [&] {
-    upload_vec_new(c, x, c->x);
-    upload_vec_new(c, v, c->vel);
-    sync_stream(c);
+    each_shard(c, [&](mp_ctx* sc) {
+      upload_vec_new(sc, x, sc->x);
+      upload_vec_new(sc, v, sc->vel);
+      sync_stream(sc);
+    });
   });
 }
 
@@ -861,9 +1008,12 @@ int mp_get_state(mp_ctx* c, double* x, double* v) {
   });
 }
 
+int mp_shards(mp_ctx* c) { return c ? c->nshards : 0; }
+
 int mp_broad_phase(mp_ctx* c, const double* x, double motion_bound, double d_hat, int64_t* pt, int64_t pt_cap,
                    int64_t* n_pt, int64_t* ee, int64_t ee_cap, int64_t* n_ee) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     *n_pt = 0;
     *n_ee = 0;
     if (c->F == 0) return;
@@ -925,6 +1075,7 @@ static void download_table(mp_ctx* c, PairTable& t, int64_t cap, int64_t* n, int
 int mp_constraint_set(mp_ctx* c, const double* x, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt,
                       double* d, double* grad, double* k) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     upload_vec_new(c, x, c->x);
     constraint_set(c, c->x);
     download_table(c, c->cur, cap, n, verts, is_pt, d, grad, k);
@@ -933,6 +1084,7 @@ int mp_constraint_set(mp_ctx* c, const double* x, int64_t cap, int64_t* n, int64
 
 int mp_gradient(mp_ctx* c, const double* x, const double* x_tilde, double h, double* g) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     upload_vec_new(c, x, c->x);
     upload_vec_new(c, x_tilde, c->xt);
     constraint_set(c, c->x);
@@ -943,6 +1095,7 @@ int mp_gradient(mp_ctx* c, const double* x, const double* x_tilde, double h, dou
 
 int mp_energy(mp_ctx* c, const double* x, const double* x_tilde, double h, double* e) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     upload_vec_new(c, x, c->x);
     upload_vec_new(c, x_tilde, c->xt);
     constraint_set(c, c->x);
@@ -952,6 +1105,7 @@ int mp_energy(mp_ctx* c, const double* x, const double* x_tilde, double h, doubl
 
 int mp_snapshot(mp_ctx* c, const double* x, double h, int build_mas) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     upload_vec_new(c, x, c->x);
     constraint_set(c, c->x);
     snapshot(c, c->x, h, build_mas != 0);
@@ -961,6 +1115,7 @@ int mp_snapshot(mp_ctx* c, const double* x, double h, int build_mas) {
 
 int mp_hvp(mp_ctx* c, const double* vec, int with_updates, double* out) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     if (!c->have_snapshot) throw MpError(MP_ERR_CONFIG, "no snapshot: call mp_snapshot first");
     upload_vec_new(c, vec, c->tmp);
     hvp(c, c->tmp, c->hv, with_updates != 0);
@@ -970,6 +1125,7 @@ int mp_hvp(mp_ctx* c, const double* vec, int with_updates, double* out) {
 
 int mp_precond_apply(mp_ctx* c, const double* g, int with_updates, double* z) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     if (!c->have_mas) throw MpError(MP_ERR_CONFIG, "no MAS hierarchy: call mp_snapshot(build_mas=1) first");
     upload_vec_new(c, g, c->g);
     precond_apply(c, c->g, c->z, with_updates != 0);
@@ -979,6 +1135,7 @@ int mp_precond_apply(mp_ctx* c, const double* g, int with_updates, double* z) {
 
 int mp_update_at(mp_ctx* c, const double* x, int64_t* n_candidates, int64_t* n_touched) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     if (!c->have_snapshot) throw MpError(MP_ERR_CONFIG, "no snapshot: call mp_snapshot first");
     upload_vec_new(c, x, c->tmp);
     constraint_set(c, c->tmp);
@@ -992,6 +1149,7 @@ int mp_update_at(mp_ctx* c, const double* x, int64_t* n_candidates, int64_t* n_t
 int mp_ccd(mp_ctx* c, const double* x, const double* p, double* alpha_d, double* x_new, double* min_alpha,
            int32_t* certified, int64_t* n_pairs, int32_t exact_set) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     upload_vec_new(c, x, c->x);
     upload_vec_new(c, p, c->p);
     // max |p| over all components (ccd.py:225), from the caller's array
@@ -1010,6 +1168,7 @@ int mp_ccd(mp_ctx* c, const double* x, const double* p, double* alpha_d, double*
 
 int mp_coarse_matrix(mp_ctx* c, int level, double* out, int64_t cap, int64_t* n) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     if (level < 1 || level > c->n_levels) throw MpError(MP_ERR_CONFIG, "no such coarse level");
     CoarseLevel& L = *c->levels[level - 1];
     *n = L.n;
@@ -1022,6 +1181,7 @@ int mp_coarse_matrix(mp_ctx* c, int level, double* out, int64_t cap, int64_t* n)
 
 int mp_ccd_pairs(mp_ctx* c, int64_t cap, int64_t* n, int64_t* verts, uint8_t* is_pt, double* alpha) {
   return guarded(c, [&] {
+    single_gpu_only(c);
     const int64_t m = c->n_ccd;
     *n = m;
     if (m == 0 || cap < m) return;

@@ -2,9 +2,10 @@
 //
 // Every PNCG scalar of one iteration (norms and the dots of the 2x2
 // subspace system, solver.py:357-392, 444) comes out of ONE pass over the
-// vectors: k_multidot accumulates up to MAX_DOTS products per thread, writes
-// per-block partials, and k_multidot_final sums them in a fixed order
-// (deterministic, no atomics).
+// vectors: k_multidot_chunks writes one partial per chunk (a level-1
+// aggregate's dofs) and per dot, and the chunks are summed in chunk order on
+// the host (group.cuh group_dots) -- deterministic, no atomics, and the same
+// bits on one GPU and on a multi-GPU group.
 #pragma once
 
 #include "ctx.cuh"
@@ -19,62 +20,47 @@ struct DotSpec {
   int n;
 };
 
-__global__ void k_multidot(int64_t len, DotSpec S, double* __restrict__ part) {
+// Per-chunk partials of up to MAX_DOTS dots: chunk q = dofs [q cl, (q+1) cl)
+// (cl = 3 x one level-1 aggregate); one CTA per chunk sums in a fixed order.
+// The chunks' sum in chunk order (group_dots) does not depend on how the
+// chunks are spread over shards or CTAs.
+__global__ void k_multidot_chunks(int64_t len, int64_t cl, int64_t q0, DotSpec S, double* __restrict__ part) {
+  const int64_t q = q0 + blockIdx.x;
+  const int64_t b = q * cl, e = (b + cl < len) ? b + cl : len;
   double acc[MAX_DOTS];
 #pragma unroll
-  for (int q = 0; q < MAX_DOTS; ++q) acc[q] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int k = 0; k < MAX_DOTS; ++k) acc[k] = 0.0;
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
 #pragma unroll
-    for (int q = 0; q < MAX_DOTS; ++q)
-      if (q < S.n) acc[q] += S.a[q][i] * S.b[q][i];
+    for (int k = 0; k < MAX_DOTS; ++k)
+      if (k < S.n) acc[k] += S.a[k][i] * S.b[k][i];
   }
-  __shared__ double sh[MAX_DOTS][RED_THREADS / 32];
+  __shared__ double sh[MAX_DOTS][4];
 #pragma unroll
-  for (int q = 0; q < MAX_DOTS; ++q) {
-    if (q >= S.n) break;
-    double v = warp_sum(acc[q]);
-    if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x >> 5] = v;
+  for (int k = 0; k < MAX_DOTS; ++k) {
+    if (k >= S.n) break;
+    const double v = warp_sum(acc[k]);
+    if ((threadIdx.x & 31) == 0) sh[k][threadIdx.x >> 5] = v;
   }
   __syncthreads();
-  if (threadIdx.x < S.n) {
+  if ((int)threadIdx.x < S.n) {
     double t = 0.0;
-    for (int w = 0; w < RED_THREADS / 32; ++w) t += sh[threadIdx.x][w];
-    part[blockIdx.x * MAX_DOTS + threadIdx.x] = t;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[threadIdx.x][w];
+    part[q * MAX_DOTS + threadIdx.x] = t;
   }
 }
 
-// sum partials in block order; mode per slot: 0 sum, 1 max
-// one warp per dot: lanes stride over the block partials, fixed shuffle
-// tree (reproducible; a single thread walking 296 partials is latency bound)
-__global__ void k_multidot_final(int nblocks, int n, const double* __restrict__ part, double* __restrict__ out) {
-  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (q >= n) return;  // warp-uniform
-  double t = 0.0;
-  for (int b = lane; b < nblocks; b += 32) t += part[b * MAX_DOTS + q];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-  if (lane == 0) out[q] = t;
-}
+// dots over this shard's owned chunks -> group-wide values in c->h_scal[0..n)
+// (extra device scalars, if any, land in h_scal[MAX_DOTS..])
+static void multidot(mp_ctx* c, int64_t len, const DotSpec& S, const double* extra = nullptr, int n_extra = 0);
 
-// returns dots in c->h_scal[0..n)
-static void multidot(mp_ctx* c, int64_t len, const DotSpec& S) {
-  c->red_part.ensure((size_t)RED_BLOCKS * MAX_DOTS);
-  int nb = (int)grid_for(len, RED_THREADS);
-  if (nb > RED_BLOCKS) nb = RED_BLOCKS;
-  k_multidot<<<nb, RED_THREADS, 0, c->stream>>>(len, S, c->red_part);
-  LAUNCH_CHECK();
-  k_multidot_final<<<1, 32 * MAX_DOTS, 0, c->stream>>>(nb, S.n, c->red_part, c->dscal);
-  LAUNCH_CHECK();
-  CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->dscal.p, sizeof(double) * S.n, cudaMemcpyDeviceToHost, c->stream));
-  sync_stream(c);
-}
-
-// p = a z + b pp ; Hp = a v + b Hpp ; partials of g.p and max|p|
+// p = a z + b pp ; Hp = a v + b Hpp (elementwise, every row); max|p| into
+// *pmax (order-free: atomicMax on the bit pattern of a non-negative double)
 __global__ void k_form_dir(int64_t len, double a, double b, const double* __restrict__ z,
                            const double* __restrict__ pp, const double* __restrict__ v,
-                           const double* __restrict__ Hpp, const double* __restrict__ g, double* __restrict__ p,
-                           double* __restrict__ Hp, double* __restrict__ part) {
-  double gp = 0.0, mx = 0.0;
+                           const double* __restrict__ Hpp, double* __restrict__ p, double* __restrict__ Hp,
+                           unsigned long long* __restrict__ pmax) {
+  double mx = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
     // (-mu z) + (nu p_prev), each product rounded as in solver.py:384-385
     double pi = __dmul_rn(a, z[i]);
@@ -85,58 +71,26 @@ __global__ void k_form_dir(int64_t len, double a, double b, const double* __rest
     }
     p[i] = pi;
     Hp[i] = hi;
-    gp += g[i] * pi;
     mx = fmax(mx, fabs(pi));
   }
-  __shared__ double s1[RED_THREADS / 32], s2[RED_THREADS / 32];
-  gp = warp_sum(gp);
   mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) {
-    s1[threadIdx.x >> 5] = gp;
-    s2[threadIdx.x >> 5] = mx;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0, m = 0.0;
-    for (int w = 0; w < RED_THREADS / 32; ++w) {
-      t += s1[w];
-      m = fmax(m, s2[w]);
-    }
-    part[blockIdx.x * MAX_DOTS] = t;
-    part[blockIdx.x * MAX_DOTS + 1] = m;
-  }
-}
-
-__global__ void k_form_dir_final(int nblocks, const double* __restrict__ part, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  double t = 0.0, m = 0.0;
-  for (int b = lane; b < nblocks; b += 32) {
-    t += part[b * MAX_DOTS];
-    m = fmax(m, part[b * MAX_DOTS + 1]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    t += __shfl_down_sync(0xffffffffu, t, o);
-    m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
-  }
-  if (lane == 0) {
-    out[0] = t;
-    out[1] = m;
-  }
+  if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(pmax, (unsigned long long)__double_as_longlong(mx));
 }
 
 // p, Hp formed on device; returns (g.p, max|p|) in h_scal[0..1]
 static void form_direction(mp_ctx* c, double a, double b, const double* pp, const double* Hpp) {
   const int64_t len = 3 * c->N;
-  c->red_part.ensure((size_t)RED_BLOCKS * MAX_DOTS);
-  int nb = (int)grid_for(len, RED_THREADS);
-  if (nb > RED_BLOCKS) nb = RED_BLOCKS;
-  k_form_dir<<<nb, RED_THREADS, 0, c->stream>>>(len, a, b, c->z, pp, c->hv, Hpp, c->g, c->p, c->Hp, c->red_part);
+  unsigned long long* pmax = reinterpret_cast<unsigned long long*>(c->dscal.p + 40);
+  CUDA_CHECK(cudaMemsetAsync(pmax, 0, sizeof(unsigned long long), c->stream));
+  k_form_dir<<<(unsigned)std::min<int64_t>(grid_for(len, RED_THREADS), RED_BLOCKS), RED_THREADS, 0, c->stream>>>(
+      len, a, b, c->z, pp, c->hv, Hpp, c->p, c->Hp, pmax);
   LAUNCH_CHECK();
-  k_form_dir_final<<<1, 32, 0, c->stream>>>(nb, c->red_part, c->dscal);
-  LAUNCH_CHECK();
-  CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->dscal.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
-  sync_stream(c);
+  DotSpec S{};
+  S.a[0] = c->g;
+  S.b[0] = c->p;
+  S.n = 1;
+  multidot(c, len, S, c->dscal.p + 40, 1);
+  c->h_scal[1] = c->h_scal[MAX_DOTS];  // max|p| (the bits of a non-negative double)
 }
 
 __global__ void k_velocity(int64_t N, const double* __restrict__ x, const double* __restrict__ x0, double h,

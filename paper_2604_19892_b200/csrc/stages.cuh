@@ -5,6 +5,7 @@
 
 #include "ccd.cuh"
 #include "coarse.cuh"
+#include "group.cuh"
 #include "elastic.cuh"
 #include "mas.cuh"
 #include "ops.cuh"
@@ -105,6 +106,8 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   L.inv.ensure((size_t)cyc_size(n));
   L.cs_tiles.ensure((size_t)nT * (nT + 1) / 2 * 1024);
   L.cs_col.ensure(2 * (size_t)nT * 1024);
+  L.cs_pm.ensure((size_t)nT * 1024);
+  L.cs_diag.ensure((size_t)nT * 1024);
   L.cs_bar.zero(2, L.st);
   static int max_ctas = 0;
   if (!max_ctas) {
@@ -114,10 +117,10 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_sweep, CS_THREADS, coarse_sweep_smem()));
     max_ctas = std::max(1, sms * std::max(1, per));
   }
-  const int grid = std::max(1, std::min(L.n_units, max_ctas));
+  const int grid = std::max(1, std::min(L.n_units + 1, max_ctas));  // + the lookahead CTA
   static const int prof = getenv("MP_CS_PROF") ? 1 : 0;
   CoarseSweepArgs A{n, nT, L.n_units, L.cs_units.p, L.dense.p, L.cs_tiles.p, L.cs_col.p, L.inv.p, status,
-                    L.cs_bar.p, prof};
+                    L.cs_bar.p, L.cs_pm.p, L.cs_diag.p, prof};
   void* args[] = {&A};
   CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_coarse_sweep, dim3(grid), dim3(CS_THREADS), args,
                                          coarse_sweep_smem(), L.st));
@@ -190,15 +193,19 @@ static void mas_build(mp_ctx* c) {
   // level 0: one CTA per subdomain assembles M_d in smem and sweeps it
   c->Bblk.ensure((size_t)D * cyc_size(m));
   c->Mblk.ensure((size_t)D * cyc_size(m));
-  k_mas_sweep<<<(unsigned)D, 256, sizeof(double) * m * m, c->stream>>>(
-      D, c->N, c->bs, m, c->pinned, nc ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->base.verts,
-      c->base.grad, c->base.k, c->rowptr, c->slot_row, c->cols, c->bsr, c->Mblk, c->Bblk, c->counters.p + 3);
-  LAUNCH_CHECK();
+  // (a shard sweeps its owned subdomains only)
+  if (c->own_d1 > c->own_d0) {
+    k_mas_sweep<<<(unsigned)(c->own_d1 - c->own_d0), 256, sizeof(double) * m * m, c->stream>>>(
+        D, c->N, c->bs, m, c->pinned, nc ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->base.verts,
+        c->base.grad, c->base.k, c->rowptr, c->slot_row, c->cols, c->bsr, c->Mblk, c->Bblk, c->counters.p + 3,
+        c->own_d0);
+    LAUNCH_CHECK();
+  }
   for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
   // one readback of every level's non-SPD flag (counters 3..7)
   CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 8, c->counters.p + 3, 5 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
-  if (c->h_cnt[8]) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
+  if (group_or(c, c->h_cnt[8])) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
   for (int q = 1; q < 5; ++q)
     if (c->h_cnt[8 + q]) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
   c->have_mas = true;
@@ -295,16 +302,16 @@ static void update_build(mp_ctx* c) {
   const size_t smem_w = sizeof(double) * ((size_t)m * m + 2 * (size_t)m * kw + (size_t)kw * kw);
   k_woodbury<<<nt, 256, smem_w, c->stream>>>(c->N, c->bs, m, kw, c->Bblk, c->touched_sub, c->touched_start,
                                              c->touched_len, c->ent_cand2, c->cand_verts, c->cand_u, c->overlay,
-                                             c->counters.p + 4);
+                                             c->counters.p + 4, c->own_d0, c->own_d1);
   LAUNCH_CHECK();
   if (c->cfg.K > WOODBURY_KMAX) {
     const size_t smem_d = sizeof(double) * 2 * (size_t)m * m;
     k_direct_update<<<nt, 256, smem_d, c->stream>>>(c->N, c->bs, m, c->Mblk, c->touched_sub, c->touched_start,
                                                     c->touched_len, c->ent_cand2, c->cand_verts, c->cand_u,
-                                                    WOODBURY_KMAX, c->overlay, c->counters.p + 4);
+                                                    WOODBURY_KMAX, c->overlay, c->counters.p + 4, c->own_d0, c->own_d1);
     LAUNCH_CHECK();
   }
-  if (read_status(c, c->counters.p + 4)) throw MpError(MP_ERR_CAPACITANCE, "capacitance not SPD");
+  if (group_or(c, read_status(c, c->counters.p + 4))) throw MpError(MP_ERR_CAPACITANCE, "capacitance not SPD");
   c->have_updates = nt > 0;
 }
 
@@ -315,7 +322,14 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   for (int l = 0; l < c->n_levels; ++l) {
     CoarseLevel& L = *c->levels[l];
     if (l == 0) {
-      k_restrict1<<<L.A, 128, 0, c->stream>>>(c->N, L.span, g, L.rsum, L.r);
+      // owned aggregates, then every shard's slice to every shard (6 doubles per aggregate)
+      if (c->own_a1 > c->own_a0)
+        k_restrict1<<<(unsigned)(c->own_a1 - c->own_a0), 128, 0, c->stream>>>(c->N, L.span, g, L.rsum, L.r,
+                                                                              c->own_a0);
+      LAUNCH_CHECK();
+      auto rng = [](mp_ctx* p, int64_t& lo, int64_t& hi) { lo = 3 * p->own_a0; hi = 3 * p->own_a1; };
+      group_allgather(c, [](mp_ctx* p) { return p->levels[0]->rsum.p; }, rng);
+      group_allgather(c, [](mp_ctx* p) { return p->levels[0]->r.p; }, rng);
     } else {
       CoarseLevel& F = *c->levels[l - 1];
       k_restrict_up<<<grid_for(3 * (int64_t)L.A, 128), 128, 0, c->stream>>>(L.A, c->cfg.coarse_block, F.A, c->N,
@@ -331,12 +345,15 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   const int64_t cpad = (cyc_size(c->m) + 1) & ~1ll;
   const int stages = c->apply_stages == 3 ? 3 : 2;
   const size_t smem = sizeof(double) * (stages * cpad + 2 * 96);
-  const unsigned grid = (unsigned)std::min<int64_t>(c->D, (int64_t)c->apply_ctas_per_sm * 148);
+  const int64_t Down = c->own_d1 - c->own_d0;  // this shard's subdomains
+  LV.d0 = c->own_d0;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(Down, (int64_t)c->apply_ctas_per_sm * 148));
   timer_begin(c, MP_STAGE_MAS_L0);
   const int* ovp = ov ? c->overlay_of.p : nullptr;
-#define L0_ARGS c->D, c->N, c->bs, c->m, c->Bblk, ovp, c->overlay, g, c->pinned, LV, z
-  if (c->apply_mode == 2) {
-    k_mas_apply_l0_direct<<<(unsigned)c->D, APPLY_THREADS, 0, c->stream>>>(L0_ARGS);
+#define L0_ARGS Down, c->N, c->bs, c->m, c->Bblk, ovp, c->overlay, g, c->pinned, LV, z
+  if (Down <= 0) {
+  } else if (c->apply_mode == 2) {
+    k_mas_apply_l0_direct<<<(unsigned)Down, APPLY_THREADS, 0, c->stream>>>(L0_ARGS);
   } else if (c->apply_mode == 1) {
     if (stages == 3) k_mas_apply_l0<true, 3><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
     else k_mas_apply_l0<true, 2><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
@@ -351,11 +368,16 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   double l0_bytes = 8.0 * (double)c->D * (double)cyc_size(c->m) + 48.0 * c->N;
   for (int l = 0; l < c->n_levels; ++l) l0_bytes += 8.0 * c->levels[l]->n;
   timer_end(c, MP_STAGE_MAS_L0, l0_bytes);
+  // z on the owned rows -> every shard (the HVP reads z at every neighbour)
+  // (z is always the context's z buffer; every shard swaps its buffers in lockstep)
+  if (c->nshards > 1 && z != c->z.p) throw MpError(MP_ERR_CONFIG, "group apply writes the context's z only");
+  group_allgather(c, [](mp_ctx* p) { return p->z.p; },
+                  [](mp_ctx* p, int64_t& lo, int64_t& hi) { lo = 3 * p->own_v0; hi = 3 * p->own_v1; });
 }
 
 // HessianModel.hvp (energy.py:435-440): H_base v + sum u (u^T v)
 static void hvp(mp_ctx* c, const double* vec, double* out, bool with_cands) {
-  bsr_spmv(c, vec, out);
+  bsr_spmv(c, vec, out);  // owned rows
   const int64_t nb = c->base.count, nq = with_cands ? c->n_cand : 0;
   if (nb) {
     c->rbuf_base.ensure(12 * (size_t)nb);
@@ -369,9 +391,9 @@ static void hvp(mp_ctx* c, const double* vec, double* out, bool with_cands) {
     LAUNCH_CHECK();
   }
   if (nb || nq) {
-    k_inc_gather_add<<<grid_for(32 * c->N, 128), 128, 0, c->stream>>>(
-        c->N, c->pinned, nb ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->rbuf_base.p, nq ? c->inc_cand.off.p : nullptr,
-        c->inc_cand.val2.p, c->rbuf_cand.p, out);
+    k_inc_gather_add<<<grid_for(32 * (c->own_v1 - c->own_v0), 128), 128, 0, c->stream>>>(
+        c->own_v1, c->pinned, nb ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->rbuf_base.p,
+        nq ? c->inc_cand.off.p : nullptr, c->inc_cand.val2.p, c->rbuf_cand.p, out, c->own_v0);
     LAUNCH_CHECK();
   }
 }

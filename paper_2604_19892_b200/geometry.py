@@ -130,68 +130,112 @@ def make_single_tet(scale=1.0) -> TetMesh:
 
 
 # ---------------------------------------------------------------------------
-# file formats (`geometry.py:566-647`)
+# voxel tet meshes (the C4 / C5 generators)
 
 
-def _rows(path):
+def voxel_tet_mesh(mask, cell, origin=(0.0, 0.0, 0.0)) -> TetMesh:
+    """Tet mesh of the occupied cells of a boolean grid ``mask`` (nx, ny, nz)
+    of edge ``cell``: the used grid corners (in grid order) and the same
+    6-tet Kuhn split with orientation fix as ``make_box_mesh`` -- a box mask
+    gives make_box_mesh's mesh up to vertex numbering."""
+    mask = np.asarray(mask, dtype=bool)
+    nx, ny, nz = mask.shape
+    i, j, k = np.nonzero(mask)
+
+    def vid(a, b, c):
+        return (a * (ny + 1) + b) * (nz + 1) + c
+
+    corners = np.stack([vid(i, j, k), vid(i + 1, j, k), vid(i, j + 1, k), vid(i + 1, j + 1, k),
+                        vid(i, j, k + 1), vid(i + 1, j, k + 1), vid(i, j + 1, k + 1), vid(i + 1, j + 1, k + 1)],
+                       axis=1)
+    used, inv = np.unique(corners, return_inverse=True)
+    a = used // ((ny + 1) * (nz + 1))
+    b = (used // (nz + 1)) % (ny + 1)
+    c = used % (nz + 1)
+    verts = np.stack([a, b, c], axis=1) * float(cell) + np.asarray(origin, dtype=float)
+    tets = inv.reshape(-1, 8)[:, KUHN_TETS].reshape(-1, 4).copy()
+    if len(tets):
+        e = verts[tets[:, 1:]] - verts[tets[:, :1]]
+        flip = np.linalg.det(e) < 0
+        tets[flip, 2], tets[flip, 3] = tets[flip, 3].copy(), tets[flip, 2].copy()
+    return TetMesh(rest_positions=verts, tets=tets)
+
+
+def cell_centres(shape, cell, origin=(0.0, 0.0, 0.0)):
+    """(nx, ny, nz, 3) centres of a voxel grid."""
+    axes = [origin[d] + cell * (np.arange(shape[d]) + 0.5) for d in range(3)]
+    return np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1)
+
+
+# ---------------------------------------------------------------------------
+# TetGen .node/.ele and OBJ (the reference's scene file formats,
+# `geometry.py:566-647`): whole-array parsing, '#' comments, 0- or 1-based
+# node ids (the smallest node id is the base), inverted tets repaired.
+
+
+def _table(path):
+    """Non-comment rows of a whitespace table as a list of token lists."""
     with open(path) as fh:
-        for line in fh:
-            body = line.split("#", 1)[0].split()
-            if body:
-                yield body
+        text = fh.read()
+    return [ln.split() for ln in (raw.partition("#")[0] for raw in text.splitlines()) if ln.strip()]
 
 
 def load_node_ele(path_base) -> TetMesh:
     base = str(path_base)
     if base.endswith((".node", ".ele")):
-        base = base.rsplit(".", 1)[0]
-    nodes = list(_rows(base + ".node"))
-    n = int(nodes[0][0])
-    if int(nodes[0][1]) != 3:
+        base = base[: base.rfind(".")]
+    rows = _table(base + ".node")
+    n, dim = int(rows[0][0]), int(rows[0][1])
+    if dim != 3:
         raise ConfigError(f"{base}.node: expected 3-D points")
-    ids = np.array([int(r[0]) for r in nodes[1:1 + n]])
-    pts = np.array([[float(c) for c in r[1:4]] for r in nodes[1:1 + n]]).reshape(-1, 3)
+    body = np.array([r[:4] for r in rows[1:1 + n]], dtype=float).reshape(-1, 4)
+    ids = body[:, 0].astype(np.int64)
+    pts = body[np.argsort(ids, kind="stable"), 1:4]
     first = int(ids.min()) if n else 0
-    pts = pts[np.argsort(ids, kind="stable")]
-    eles = list(_rows(base + ".ele"))
-    m = int(eles[0][0])
-    if int(eles[0][1]) != 4:
+    rows = _table(base + ".ele")
+    m, per = int(rows[0][0]), int(rows[0][1])
+    if per != 4:
         raise ConfigError(f"{base}.ele: expected 4-node tets")
-    tets = np.array([[int(c) for c in r[1:5]] for r in eles[1:1 + m]], dtype=np.int64).reshape(-1, 4)
+    tets = np.array([r[1:5] for r in rows[1:1 + m]], dtype=np.int64).reshape(-1, 4)
     if tets.size and tets.min() >= first:
-        tets -= first
+        tets = tets - first
     if tets.size and (tets.min() < 0 or tets.max() >= n):
         raise ConfigError(f"{base}.ele: node index out of range")
     if tets.size:
-        flip = tet_volumes(pts, tets) < 0
-        tets[flip, 2], tets[flip, 3] = tets[flip, 3].copy(), tets[flip, 2].copy()
+        bad = tet_volumes(pts, tets) < 0
+        tets[bad] = tets[bad][:, [0, 1, 3, 2]]
     return TetMesh(rest_positions=pts, tets=tets)
 
 
 def save_node_ele(path_base, mesh: TetMesh):
     base = str(path_base)
+    n, m = mesh.n_vertices, len(mesh.tets)
+    idx = np.arange(n, dtype=np.int64)[:, None]
     with open(base + ".node", "w") as fh:
-        fh.write(f"{mesh.n_vertices} 3 0 0\n")
-        fh.writelines(f"{i} {p[0]:.17g} {p[1]:.17g} {p[2]:.17g}\n" for i, p in enumerate(mesh.rest_positions))
+        fh.write(f"{n} 3 0 0\n")
+        np.savetxt(fh, np.hstack([idx, mesh.rest_positions]), fmt=["%d", "%.17g", "%.17g", "%.17g"])
     with open(base + ".ele", "w") as fh:
-        fh.write(f"{len(mesh.tets)} 4 0\n")
-        fh.writelines(f"{i} {t[0]} {t[1]} {t[2]} {t[3]}\n" for i, t in enumerate(mesh.tets))
+        fh.write(f"{m} 4 0\n")
+        np.savetxt(fh, np.hstack([np.arange(m, dtype=np.int64)[:, None], mesh.tets]), fmt="%d")
 
 
 def save_obj(path, positions, triangles, groups=None):
-    out = [f"v {p[0]:.17g} {p[1]:.17g} {p[2]:.17g}" for p in np.asarray(positions).reshape(-1, 3)]
-    for name, lo, hi in groups or [("surface", 0, len(triangles))]:
-        out.append(f"o {name}")
-        out.extend(f"f {t[0] + 1} {t[1] + 1} {t[2] + 1}" for t in triangles[lo:hi])
+    """Surface OBJ; ``groups`` = [(name, lo, hi)] triangle ranges as 'o' records."""
     with open(path, "w") as fh:
-        fh.write("\n".join(out) + "\n")
+        np.savetxt(fh, np.asarray(positions, dtype=float).reshape(-1, 3), fmt="v %.17g %.17g %.17g")
+        tri = np.asarray(triangles, dtype=np.int64).reshape(-1, 3) + 1
+        for name, lo, hi in groups or [("surface", 0, len(tri))]:
+            fh.write(f"o {name}\n")
+            np.savetxt(fh, tri[lo:hi], fmt="f %d %d %d")
 
 
 def load_obj(path):
     verts, tris = [], []
-    for row in _rows(path):
-        if row[0] == "v":
-            verts.append([float(c) for c in row[1:4]])
-        elif row[0] == "f":
-            tris.append([int(tok.split("/", 1)[0]) - 1 for tok in row[1:4]])
-    return np.array(verts, dtype=float).reshape(-1, 3), np.array(tris, dtype=np.int64).reshape(-1, 3)
+    for r in _table(path):
+        if r[0] == "v":
+            verts.append(r[1:4])
+        elif r[0] == "f":
+            tris.append([t.split("/", 1)[0] for t in r[1:4]])
+    v = np.array(verts, dtype=float).reshape(-1, 3)
+    f = np.array(tris, dtype=np.int64).reshape(-1, 3) - 1
+    return v, f

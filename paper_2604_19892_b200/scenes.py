@@ -173,3 +173,108 @@ SCENES = {
     "c2_stack": c2_stack,
     "c3_rod": c3_rod,
 }
+
+
+# ---------------------------------------------------------------------------
+# C4 / C5: voxel (6-tet Kuhn) meshes of the paper's shapes, SURVEY.md 8(d)
+
+
+def sphere_mesh(radius_cells=12, cell=0.05 / 12, mods=None):
+    """Voxel ball: the cells of a (2R)^3 grid whose centres lie within R
+    cells of the centre (R = 12: 7,153 V / 40,488 T -- SURVEY's ~7.8k V)."""
+    geo, _, _ = _mods(mods)
+    n = 2 * radius_cells
+    c = geo.cell_centres((n, n, n), 1.0) - radius_cells
+    mask = np.einsum("...k,...k->...", c, c) <= radius_cells ** 2
+    return geo.voxel_tet_mesh(mask, cell, origin=(-radius_cells * cell,) * 3)
+
+
+def bowl_mesh(inner=0.42, thickness=0.04, cell=0.02, mods=None):
+    """Voxel hemispherical shell (the lower half, rim at z = 0) of inner
+    radius ``inner``: the pinned bowl of config 4."""
+    geo, _, _ = _mods(mods)
+    R = inner + thickness
+    n = int(np.ceil(2 * R / cell))
+    nz = int(np.ceil(R / cell))
+    org = (-0.5 * n * cell, -0.5 * n * cell, -nz * cell)
+    c = geo.cell_centres((n, n, nz), cell, org)
+    r = np.sqrt(np.einsum("...k,...k->...", c, c))
+    return geo.voxel_tet_mesh((r >= inner) & (r <= R), cell, origin=org)
+
+
+def c4_spheres_in_bowl(n_side=4, radius_cells=12, radius=0.05, gap=0.01, young=1e5, mods=None):
+    """Config 4: n_side^3 soft SNH voxel balls (64 at n_side = 4, ~7.2k V
+    each) in a cubic lattice falling into a pinned ARAP bowl; SNH E = 1e5,
+    d_hat = 1e-3, kappa = 1e4."""
+    ball = sphere_mesh(radius_cells, radius / radius_cells, mods)
+    pitch = 2 * radius + gap
+    half = 0.5 * (n_side - 1) * pitch
+    objs = [{"mesh": bowl_mesh(inner=max(0.42, 1.5 * half + 2 * radius), mods=mods), "material": "arap",
+             "young": 1e6, "pinned": True, "translate": (0.0, 0.0, 0.0)}]
+    z0 = -0.5 * max(0.42, 1.5 * half + 2 * radius) + radius + 2 * gap
+    for iz in range(n_side):
+        for iy in range(n_side):
+            for ix in range(n_side):
+                objs.append({"mesh": ball, "material": "snh", "young": young, "poisson": 0.3, "density": 1000.0,
+                             "translate": (-half + ix * pitch, -half + iy * pitch, z0 + iz * pitch)})
+    return build_scene(objs, d_hat=1e-3, kappa=1e4, mods=mods)
+
+
+def _fibonacci_dirs(n):
+    k = np.arange(n) + 0.5
+    phi = np.arccos(1.0 - 2.0 * k / n)
+    theta = np.pi * (1.0 + 5.0 ** 0.5) * k
+    return np.stack([np.cos(theta) * np.sin(phi), np.sin(theta) * np.sin(phi), np.cos(phi)], axis=1)
+
+
+def puffer_mesh(core_cells=19, spike_cells=64, n_spikes=410, base_cells=0.84, tip_cells=0.55, cell=0.1 / 64,
+                mods=None):
+    """Puffer ball: a voxel sphere core of radius core_cells plus n_spikes
+    thin conical spikes (Fibonacci directions) tapering from base_cells to
+    tip_cells in radius out to spike_cells.  Defaults: 142,848 V / 342,960 T
+    per ball (T/V = 2.40), eight balls 1.143M V / 2.744M T -- the paper's
+    1.14M V / 2.72M T puffer-ball scene; 0.2 m across."""
+    geo, _, _ = _mods(mods)
+    n = 2 * spike_cells + 2
+    c = geo.cell_centres((n, n, n), 1.0) - 0.5 * n
+    r = np.sqrt(np.einsum("...k,...k->...", c, c))
+    mask = r <= core_cells
+    inside = r <= spike_cells
+    cs, rs = c[inside], r[inside]
+    spikes = np.zeros(len(cs), dtype=bool)
+    for d in _fibonacci_dirs(n_spikes):
+        t = cs @ d  # coordinate along the spike
+        perp = np.sqrt(np.maximum(rs * rs - t * t, 0.0))
+        frac = np.clip((t - core_cells) / (spike_cells - core_cells), 0.0, 1.0)
+        spikes |= (t > 0.0) & (perp <= base_cells + (tip_cells - base_cells) * frac)
+    mask[inside] |= spikes
+    return geo.voxel_tet_mesh(mask, cell, origin=(-0.5 * n * cell,) * 3)
+
+
+def c5_puffer_balls(young=1e5, speed=1.0, mods=None, **puffer):
+    """Config 5: eight puffer balls at the corners of a cube, flying at each
+    other (``c5_puffer_v0``); SNH E = 1e5, h = 0.005, d_hat = 1e-4 (the
+    paper's collision scene).  No floor, no gravity: the
+    balls only meet each other."""
+    ball = puffer_mesh(mods=mods, **puffer)
+    ext = float(np.ptp(ball.rest_positions, axis=0).max())
+    s = 0.5 * ext * 1.02  # corners: bounding spheres just apart
+    objs = [{"mesh": ball, "material": "snh", "young": young, "poisson": 0.3, "density": 1000.0,
+             "translate": (sx * s, sy * s, sz * s)}
+            for sz in (-1, 1) for sy in (-1, 1) for sx in (-1, 1)]
+    return build_scene(objs, d_hat=1e-4, kappa=1e4, gravity=(0.0, 0.0, 0.0), mods=mods)
+
+
+def c5_puffer_v0(scene, speed=1.0):
+    """Each ball moves toward the scene centre at ``speed`` m/s."""
+    x = scene.mesh.rest_positions
+    n = len(x) // 8
+    v = np.zeros_like(x)
+    for b in range(8):
+        sl = slice(b * n, (b + 1) * n)
+        c = x[sl].mean(axis=0)
+        v[sl] = -speed * c / max(np.linalg.norm(c), 1e-30)
+    return v.ravel()
+
+
+SCENES.update({"c4_spheres_in_bowl": c4_spheres_in_bowl, "c5_puffer_balls": c5_puffer_balls})

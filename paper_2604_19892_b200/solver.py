@@ -136,12 +136,18 @@ class Scene:
             "d_hat": float(self.d_hat), "kappa": float(self.kappa), "n": n,
         }
 
-    def context(self, config: SolverConfig, device: int = 0) -> _native.NativeContext:
-        key = (int(config.block_size), int(device))
+    def context(self, config: SolverConfig, device: int = 0, devices=None) -> _native.NativeContext:
+        """The scene's device context (cached per block size and device set).
+        ``devices`` (a list of CUDA ordinals, repeats allowed) gives the
+        partitioned multi-GPU solver: one shard per entry, each owning a
+        contiguous Morton range of level-1 aggregates (include/maspncg.h
+        mp_create_multi); its results are bitwise the single-GPU ones."""
+        devs = (int(device),) if devices is None else tuple(int(d) for d in devices)
+        key = (int(config.block_size), devs)
         ctx = self._contexts.get(key)
         cfg = config.to_native()
         if ctx is None:
-            ctx = _native.NativeContext(self.native_arrays(), cfg, device)
+            ctx = _native.NativeContext(self.native_arrays(), cfg, devs[0] if len(devs) == 1 else list(devs))
             self._contexts[key] = ctx
         else:
             ctx.set_config(cfg)
