@@ -239,7 +239,8 @@ int mp_stage_timing(mp_ctx* ctx, int enable);
  * same results. */
 enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3, MP_OPT_APPLY_STAGES = 4,
        MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6, MP_OPT_KEEP_COARSE = 7,
-       MP_OPT_APPEND_LIMIT = 8 /* test knob: process-wide one-pass list limit (default and max 2^30; <= 0 resets) */ };
+       MP_OPT_APPEND_LIMIT = 8 /* test knob: process-wide one-pass list limit (default and max 2^30; <= 0 resets) */,
+       MP_OPT_GRAD_FUSED = 9 /* gradient: 1 (default) one fused per-vertex pass, 0 per-tet scratch + gather; same bits */ };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 
@@ -251,6 +252,18 @@ const char* mp_create_error(void);
  * of the symmetric n x n row-major A; *not_spd = 1 (and inv undefined) where
  * cho_factor would raise non-spd-subdomain.  Test / parity entry point. */
 int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t* not_spd);
+
+/* The penetration checker's triangle-triangle part (cli.py:393-401 with
+ * geometry.tri_tri_intersect, geometry.py:686-732) on `device`: the number
+ * of intersecting non-adjacent triangle pairs of the surface (x: (N,3),
+ * tris: (F,3)) and the smallest triangle index involved (-1 if none).
+ * Uniform-grid candidates, O(F) instead of the reference's O(F^2). */
+int mp_check_intersections(int device, int64_t n_verts, const double* x, int64_t n_tris, const int64_t* tris,
+                           int64_t* n_hits, int64_t* first_tri);
+
+/* Change the barrier parameters of a context (Scene.d_hat / kappa); the
+ * checker uses a surface-only context with d_hat = its search radius. */
+int mp_set_contact(mp_ctx* ctx, double d_hat, double kappa);
 
 /* Host-only: the owned ranges shard `rank` of `nshards` gets in a group
  * (mp_create_multi): out[0..1] vertices [v0, v1) (renumbered, subdomain

@@ -54,7 +54,7 @@ class IterRecordC(C.Structure):
 EXPORTS = (
     "mp_create", "mp_create_multi", "mp_shards", "mp_destroy", "mp_set_config", "mp_status_code", "mp_last_error", "mp_stream", "mp_partition",
     "mp_step", "mp_advance", "mp_broad_phase", "mp_constraint_set", "mp_gradient", "mp_energy", "mp_snapshot",
-    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_coarse_matrix", "mp_spd_inverse", "mp_shard_range", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
+    "mp_hvp", "mp_precond_apply", "mp_update_at", "mp_ccd", "mp_coarse_matrix", "mp_spd_inverse", "mp_shard_range", "mp_check_intersections", "mp_set_contact", "mp_launch_count", "mp_stage_timing", "mp_stage_stats", "mp_set_option",
 )
 
 STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd", "mas_apply_l0",
@@ -92,6 +92,8 @@ def load_library():
     lib.mp_launch_count.restype = C.c_int64
     lib.mp_partition.argtypes = [vp, _i64p, _i64p]
     lib.mp_partition_host.argtypes = [_f64p, C.c_int64, C.c_int32, _i64p]
+    lib.mp_check_intersections.argtypes = [C.c_int, C.c_int64, _f64p, C.c_int64, _i64p, _i64p, _i64p]
+    lib.mp_set_contact.argtypes = [vp, C.c_double, C.c_double]
     lib.mp_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p]
     lib.mp_spd_inverse.argtypes = [C.c_int, C.c_int64, _f64p, _f64p, C.POINTER(C.c_int32)]
     rec = C.POINTER(IterRecordC)
@@ -144,6 +146,18 @@ def partition_host(rest, block_size):
     out = np.zeros(len(rest), dtype=np.int64)
     raise_status(lib.mp_partition_host(_ptr(rest), len(rest), int(block_size), _ptr(out, C.c_int64)), "")
     return out
+
+
+def check_intersections(positions, triangles, device=0):
+    """(number of intersecting non-adjacent triangle pairs, first triangle
+    index or -1) of a surface, on the device (mp_check_intersections)."""
+    lib = load_library()
+    x = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(triangles, dtype=np.int64).reshape(-1, 3)
+    n, first = C.c_int64(), C.c_int64()
+    raise_status(lib.mp_check_intersections(int(device), len(x), _ptr(x), len(t), _ptr(t, C.c_int64), C.byref(n),
+                                            C.byref(first)), "mp_check_intersections")
+    return int(n.value), int(first.value)
 
 
 def shard_range(n_verts, block_size, levels, coarse_block, rank, nshards):
@@ -367,6 +381,9 @@ class NativeContext:
         self._check(self.lib.mp_ccd(self.h, _ptr(self._vec(x)), _ptr(self._vec(p)), _ptr(alpha_d), _ptr(x_new),
                                     C.byref(ma), C.byref(cert), C.byref(npairs), int(bool(exact_set))))
         return alpha_d, x_new, ma.value, bool(cert.value), npairs.value
+
+    def set_contact(self, d_hat, kappa):
+        self._check(self.lib.mp_set_contact(self.h, float(d_hat), float(kappa)))
 
     def coarse_matrix(self, level):
         """Assembled Galerkin matrix of coarse level `level` (1-based) of the

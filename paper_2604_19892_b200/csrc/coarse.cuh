@@ -261,10 +261,9 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
           if (q < J1 - J0) Bsm[q * 32 * CS_LD + (w & 31) * CS_LD + (w >> 5)] = pre[1 + q][s4];
       }
       __syncthreads();
-      // (3) W_I = A_IK A_KK^-1 = -A_IK Pm
-      cs_compute_W(Csm, Pm, Wsm);
-      __syncthreads();
-      // (4) the chunk's tiles: rows tr*4 + r, column tc of tile J0 + q
+      // (3) the chunk's tiles into registers (rows tr*4 + r, column tc of
+      // tile J0 + q) -- issued before W so their latency hides under it --
+      // then W_I = A_IK A_KK^-1 = -A_IK Pm
       const int tr = tid >> 5, tc = tid & 31;
       const int nq = J1 - J0;
       double acc[4][CS_CH];
@@ -273,6 +272,9 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
 #pragma unroll
         for (int r = 0; r < 4; ++r)
           acc[r][q] = (q < nq && J0 + q != K) ? __ldcg(A.tiles + cs_tile(I, J0 + q) + (tr * 4 + r) * 32 + tc) : 0.0;
+      cs_compute_W(Csm, Pm, Wsm);
+      __syncthreads();
+      // (4) the rank-32 update of the chunk's tiles
 #pragma unroll 4
       for (int d = 0; d < 32; ++d) {
         double wv[4];

@@ -160,6 +160,7 @@ struct mp_ctx {
   int apply_mode = 2;        // level-0 apply: 2 direct loads, 1 TMA-staged, 0 cp.async-staged
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
+  bool fused_grad = true;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
   bool keep_coarse = false;  // keep each coarse level's assembled matrix (mp_coarse_matrix)
   int bp_fused = 1;          // 1: one-pass unordered pair lists, 2: contact work fused into the queries, 0: ordered lists
   StageTimer timers[MP_STAGE_COUNT];

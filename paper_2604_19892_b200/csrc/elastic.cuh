@@ -149,6 +149,61 @@ __global__ void k_grad_gather(int64_t N, const double* __restrict__ x, const dou
   g[3 * v + 2] = mv * (x[3 * v + 2] - xt[3 * v + 2]) + e2 + c2;
 }
 
+// The gradient in one pass (energy.py:357-370), no per-corner scratch: one
+// warp per vertex, lane l computes the elastic force of its incidences
+// l, l+32, ... (tet F, Piola stress, the force on this corner -- the same
+// expression as k_tet_grad, so the same bits) and the warp sums them with
+// the fixed tree of warp_gather3; then inertia and the contact rows.  The
+// tet data are read once from HBM (a tet's 4 corner warps hit L2), x and g
+// once: the 81 N + 113 T + 17 C algorithmic bytes.  Tets [0, T_snh) are
+// SNH, [T_snh, T_el) ARAP (create_ctx sorts them so).
+__global__ void __launch_bounds__(256) k_grad_fused(int64_t v0, int64_t v1, const double* __restrict__ x,
+                                                   const double* __restrict__ xt, const double* __restrict__ mass,
+                                                   const unsigned char* __restrict__ pinned,
+                                                   const int* __restrict__ vt_off, const int* __restrict__ vt_val,
+                                                   const int4* __restrict__ tets, const TetParam* __restrict__ tetp,
+                                                   int64_t T_snh, double h2, const int* __restrict__ c_off,
+                                                   const int* __restrict__ c_val, const double* __restrict__ cbuf,
+                                                   double* __restrict__ g) {
+  const int64_t v = v0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (v >= v1) return;  // warp-uniform
+  if (pinned[v]) {
+    if (lane < 3) g[3 * v + lane] = 0.0;
+    return;
+  }
+  double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+  const int b = vt_off[v], e = vt_off[v + 1];
+  for (int k = b + lane; k < e; k += 32) {
+    const int inc = vt_val[k];
+    const int64_t t = inc >> 2;
+    const int a = inc & 3;
+    const TetParam tp = tetp[t];
+    double X[4][3], bc[4][3];
+    load_tet(x, tets[t], X);
+    M3 F;
+    tet_F(X, tp, F, bc);
+    const M3 P = piola(F, t < T_snh ? 2 : 1, tp.mu, tp.lam);
+    const double s = h2 * tp.vol;
+    e0 += s * (P(0, 0) * bc[a][0] + P(0, 1) * bc[a][1] + P(0, 2) * bc[a][2]);
+    e1 += s * (P(1, 0) * bc[a][0] + P(1, 1) * bc[a][1] + P(1, 2) * bc[a][2]);
+    e2 += s * (P(2, 0) * bc[a][0] + P(2, 1) * bc[a][1] + P(2, 2) * bc[a][2]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e0 += __shfl_down_sync(0xffffffffu, e0, o);
+    e1 += __shfl_down_sync(0xffffffffu, e1, o);
+    e2 += __shfl_down_sync(0xffffffffu, e2, o);
+  }
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  if (c_off) warp_gather3(c_off[v], c_off[v + 1], c_val, cbuf, c0, c1, c2);
+  if (lane) return;
+  const double mv = mass[v];
+  g[3 * v] = mv * (x[3 * v] - xt[3 * v]) + e0 + c0;
+  g[3 * v + 1] = mv * (x[3 * v + 1] - xt[3 * v + 1]) + e1 + c1;
+  g[3 * v + 2] = mv * (x[3 * v + 2] - xt[3 * v + 2]) + e2 + c2;
+}
+
 // energy pieces: 0.5 (x-x~)^T M (x-x~)  and  sum vol*psi  (energy.py:346-354)
 __global__ void k_inertia_energy(int64_t N, const double* __restrict__ x, const double* __restrict__ xt,
                                  const double* __restrict__ mass, double* part) {
@@ -423,6 +478,16 @@ __global__ void k_bsr_spmv(int64_t N, const int* __restrict__ rowptr, const int*
 // forces, then one fixed-order gather per vertex -- bitwise reproducible
 static void gradient_gather(mp_ctx* c, const double* x, const double* xt, double h, double* g, const int* c_off,
                             const int* c_val, const double* cbuf) {
+  if (c->fused_grad) {
+    timer_begin(c, MP_STAGE_TET_GRAD);
+    k_grad_fused<<<grid_for(32 * (c->own_v1 - c->own_v0), 256), 256, 0, c->stream>>>(
+        c->own_v0, c->own_v1, x, xt, c->mass, c->pinned, c->vt_off, c->vt_val, c->tets, c->tetp, c->T_snh, h * h,
+        c_off, c_val, cbuf, g);
+    LAUNCH_CHECK();
+    // algorithmic bytes: 81 B per vertex, 113 B per tet
+    timer_end(c, MP_STAGE_TET_GRAD, 81.0 * c->N + 113.0 * c->T);
+    return;
+  }
   if (c->T_snh) {
     timer_begin(c, MP_STAGE_TET_GRAD);
     k_tet_grad<2><<<grid_for(c->T_snh, 128), 128, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, x, h * h, c->fbuf);

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "stages.cuh"
+#include "check.cuh"
 
 thread_local int64_t* g_launch_counter = nullptr;
 
@@ -352,10 +353,12 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
       }
     }
     c->hs_off.upload(hoff.data(), c->nnzb + 1, st);
-    c->hs_val.upload(hval.data(), std::max<size_t>(1, hval.size()), st);
+    if (hval.empty()) hval.push_back(0);
+    c->hs_val.upload(hval.data(), hval.size(), st);
     c->slot_row.upload(srow.data(), c->nnzb, st);
     c->vt_off.upload(voff.data(), N + 1, st);
-    c->vt_val.upload(vval.data(), std::max<size_t>(1, vval.size()), st);
+    if (vval.empty()) vval.push_back(0);
+    c->vt_val.upload(vval.data(), vval.size(), st);
     c->fbuf.ensure(12 * (size_t)std::max<int64_t>(1, T_el));
     c->hbuf.ensure(90 * (size_t)std::max<int64_t>(1, T_el));
     c->bsr.ensure(9 * (size_t)c->nnzb);
@@ -724,6 +727,7 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_APPLY_STAGES) c->apply_stages = value == 3 ? 3 : 2;
     else if (option == MP_OPT_BP_FUSED) c->bp_fused = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (option == MP_OPT_KEEP_COARSE) c->keep_coarse = value != 0;
+    else if (option == MP_OPT_GRAD_FUSED) c->fused_grad = value != 0;
     else if (option == MP_OPT_APPEND_LIMIT) {
       const int lim = (int)std::max<int64_t>(64, std::min<int64_t>(HQ_APPEND_LIMIT, value <= 0 ? HQ_APPEND_LIMIT : value));
       CUDA_CHECK(cudaMemcpyToSymbol(g_append_limit, &lim, sizeof(int)));
@@ -893,6 +897,45 @@ int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t*
     *not_spd = flag;
     for (int i = 0; i < L.n; ++i)
       for (int j = 0; j < L.n; ++j) inv[(int64_t)i * n + j] = packed[cyc_index(L.n, i, j)];
+  });
+}
+
+int mp_check_intersections(int device, int64_t n_verts, const double* x, int64_t n_tris, const int64_t* tris,
+                           int64_t* n_hits, int64_t* first_tri) {
+  static thread_local mp_ctx* tmp = nullptr;  // scratch context: a stream and the sort helpers
+  if (n_verts < 1 || n_tris < 0 || n_tris >= (1ll << 31)) return MP_ERR_CONFIG;
+  if (!tmp) tmp = new mp_ctx();
+  return guarded(tmp, [&] {
+    mp_ctx* c = tmp;
+    c->device = device;
+    CUDA_CHECK(cudaSetDevice(device));
+    if (!c->stream) CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *n_hits = 0;
+    *first_tri = -1;
+    if (n_tris < 2) return;
+    std::vector<int> t32(3 * n_tris);
+    for (int64_t i = 0; i < 3 * n_tris; ++i) {
+      if (tris[i] < 0 || tris[i] >= n_verts) throw MpError(MP_ERR_CONFIG, "triangle index out of range");
+      t32[i] = (int)tris[i];
+    }
+    DBuf<double> xd;
+    DBuf<int> td;
+    xd.upload(x, 3 * n_verts, c->stream);
+    td.upload(t32.data(), t32.size(), c->stream);
+    int first = INT32_MAX;
+    *n_hits = (int64_t)tri_intersections(c, xd, td, n_tris, &first);
+    *first_tri = first == INT32_MAX ? -1 : first;
+  });
+}
+
+int mp_set_contact(mp_ctx* c, double d_hat, double kappa) {
+  return guarded(c, [&] {
+    if (!(d_hat > 0) || !(kappa > 0)) throw MpError(MP_ERR_CONFIG, "d_hat and kappa must be positive");
+    each_shard(c, [&](mp_ctx* sc) {
+      sc->d_hat = d_hat;
+      sc->kappa = kappa;
+      sc->have_snapshot = sc->have_mas = false;
+    });
   });
 }
 

@@ -36,7 +36,7 @@ def build_scene(objs, d_hat, kappa, gravity=(0.0, 0.0, -9.81), mods=None):
     """Concatenate object meshes into one Scene.
 
     objs: dicts with mesh, translate, material ('arap'|'snh'), young, poisson,
-    density, pinned (whole object)."""
+    density, pinned (whole object) or pin_mask (per vertex)."""
     geo, en, sol = _mods(mods)
     verts, tets, pin, kinds, mus, lams, rhos = [], [], [], [], [], [], []
     off = 0
@@ -44,7 +44,8 @@ def build_scene(objs, d_hat, kappa, gravity=(0.0, 0.0, -9.81), mods=None):
         m = ob["mesh"]
         verts.append(m.rest_positions + np.asarray(ob.get("translate", (0.0, 0.0, 0.0))))
         tets.append(m.tets + off)
-        pin.append(np.full(len(m.rest_positions), bool(ob.get("pinned", False))))
+        pin.append(np.asarray(ob["pin_mask"], bool) if "pin_mask" in ob
+                   else np.full(len(m.rest_positions), bool(ob.get("pinned", False))))
         T = len(m.tets)
         mu, lam = en.lame_parameters(ob.get("young", 1e5), ob.get("poisson", 0.3))
         kinds.append(np.full(T, 1 if ob.get("material", "arap") == "arap" else 2, dtype=np.int8))

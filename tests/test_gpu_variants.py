@@ -81,3 +81,20 @@ def test_append_overflow_rerun_same_bits(name):
             assert ref[2] == low[2] and ref[3] == low[3]
     finally:
         ctx.set_option(8, 0)
+
+
+@pytest.mark.parametrize("name", ["stacked_k256", "locking", "cube3_capped"])
+def test_gradient_fused_same_bits(name):
+    """MP_OPT_GRAD_FUSED (9): the one-pass per-vertex gradient (default)
+    computes each corner force with the per-tet kernel's expression and sums
+    them in the gather's order: the same bits."""
+    g = load_golden(name)
+    scene = scene_from_golden(g)
+    ctx = scene.context(golden_config(g))
+    for t in golden_taps(g, "gradient"):
+        out = []
+        for mode in (1, 0):
+            ctx.set_option(9, mode)
+            out.append(ctx.gradient(t["x"], t["x_tilde"], float(t["h"])))
+        ctx.set_option(9, 1)
+        assert np.array_equal(out[0], out[1])
