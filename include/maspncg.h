@@ -240,7 +240,8 @@ int mp_stage_timing(mp_ctx* ctx, int enable);
 enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3, MP_OPT_APPLY_STAGES = 4,
        MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6, MP_OPT_KEEP_COARSE = 7,
        MP_OPT_APPEND_LIMIT = 8 /* test knob: process-wide one-pass list limit (default and max 2^30; <= 0 resets) */,
-       MP_OPT_GRAD_FUSED = 9 /* gradient: 1 (default) one fused per-vertex pass, 0 per-tet scratch + gather; same bits */ };
+       MP_OPT_GRAD_FUSED = 9 /* gradient: 1 one fused per-vertex pass, 0 (default, faster) per-tet scratch + gather; same bits */,
+       MP_OPT_APPLY_OVERLAP = 10 /* MAS apply: 1 (default) level 0 beside the coarse chain + prolongation pass, 0 fused; same bits */ };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 

@@ -279,3 +279,79 @@ def broad_phase(x, tris, edges, surf_verts, motion_bound, d_hat):
                               cell))
     ee = np.unique(np.concatenate(out), axis=0) if out else np.zeros((0, 2), np.int64)
     return pt.reshape(-1, 2), ee.reshape(-1, 2)
+
+
+# ---------------------------------------------------------------------------
+# triangle-triangle intersection (`geometry.py:654-732`): the reference's
+# decision rules, one pair at a time (test-size inputs only)
+
+
+def _seg_seg_2d(p0, p1, q0, q1):
+    d1, d2, r = p1 - p0, q1 - q0, q0 - p0
+    den = d1[0] * d2[1] - d1[1] * d2[0]
+    if den == 0.0:
+        if r[0] * d1[1] - r[1] * d1[0] != 0.0:
+            return False
+        tt = d1 @ d1
+        if tt == 0.0:
+            return False
+        t0 = (r @ d1) / tt
+        t1 = t0 + (d2 @ d1) / tt
+        return max(min(t0, t1), 0.0) <= min(max(t0, t1), 1.0)
+    s = (r[0] * d2[1] - r[1] * d2[0]) / den
+    t = (r[0] * d1[1] - r[1] * d1[0]) / den
+    return 0.0 <= s <= 1.0 and 0.0 <= t <= 1.0
+
+
+def _in_tri_2d(p, a, b, c):
+    s = [(b[0] - a[0]) * (p[1] - a[1]) - (b[1] - a[1]) * (p[0] - a[0]),
+         (c[0] - b[0]) * (p[1] - b[1]) - (c[1] - b[1]) * (p[0] - b[0]),
+         (a[0] - c[0]) * (p[1] - c[1]) - (a[1] - c[1]) * (p[0] - c[0])]
+    return not (min(s) < 0 and max(s) > 0)
+
+
+def tri_tri_intersect(t1, t2):
+    """Touching counts; the coplanar case in 2-D on the dominant axes."""
+    t1, t2 = np.asarray(t1, float), np.asarray(t2, float)
+    n1 = np.cross(t1[1] - t1[0], t1[2] - t1[0])
+    n2 = np.cross(t2[1] - t2[0], t2[2] - t2[0])
+    d2 = t2 @ n1 - t1[0] @ n1
+    if np.all(d2 > 0) or np.all(d2 < 0):
+        return False
+    d1 = t1 @ n2 - t2[0] @ n2
+    if np.all(d1 > 0) or np.all(d1 < 0):
+        return False
+    if np.all(d2 == 0.0) or np.all(d1 == 0.0):
+        keep = [i for i in range(3) if i != int(np.argmax(np.abs(n1)))]
+        a, b = t1[:, keep], t2[:, keep]
+        if any(_seg_seg_2d(a[i], a[(i + 1) % 3], b[j], b[(j + 1) % 3]) for i in range(3) for j in range(3)):
+            return True
+        return _in_tri_2d(a[0], *b) or _in_tri_2d(b[0], *a)
+    ax = int(np.argmax(np.abs(np.cross(n1, n2))))
+
+    def span(tri, dist):
+        pts = [tri[i, ax] for i in range(3) if dist[i] == 0]
+        pts += [tri[i, ax] + dist[i] / (dist[i] - dist[j]) * (tri[j, ax] - tri[i, ax])
+                for i in range(3) if dist[i] > 0 for j in range(3) if dist[j] < 0]
+        return min(pts), max(pts)
+
+    lo1, hi1 = span(t1, d1)
+    lo2, hi2 = span(t2, d2)
+    return max(lo1, lo2) <= min(hi1, hi2)
+
+
+def count_tri_intersections(x, tris):
+    """Non-adjacent intersecting triangle pairs (`cli.py:393-401`), boxes
+    first (O(F^2) box test, vectorised), exact test on overlapping boxes."""
+    x = np.asarray(x, float).reshape(-1, 3)
+    tris = np.asarray(tris, np.int64).reshape(-1, 3)
+    p = x[tris]
+    lo, hi = p.min(axis=1), p.max(axis=1)
+    n = 0
+    for i in range(len(tris)):
+        ov = np.all((lo[i] <= hi[i + 1:]) & (lo[i + 1:] <= hi[i]), axis=1)
+        for j in np.nonzero(ov)[0] + i + 1:
+            if set(tris[i].tolist()) & set(tris[j].tolist()):
+                continue
+            n += bool(tri_tri_intersect(p[i], p[j]))
+    return n

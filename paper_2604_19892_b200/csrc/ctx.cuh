@@ -160,7 +160,10 @@ struct mp_ctx {
   int apply_mode = 2;        // level-0 apply: 2 direct loads, 1 TMA-staged, 0 cp.async-staged
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
-  bool fused_grad = true;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
+  bool fused_grad = true;
+  bool overlap_apply = true;  // MAS apply: level 0 on the side stream beside the coarse chain (MP_OPT_APPLY_OVERLAP)
+  cudaStream_t side = nullptr;  // side stream (level-0 apply) and its events
+  cudaEvent_t ev_g = nullptr, ev_l0 = nullptr;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
   bool keep_coarse = false;  // keep each coarse level's assembled matrix (mp_coarse_matrix)
   int bp_fused = 1;          // 1: one-pass unordered pair lists, 2: contact work fused into the queries, 0: ordered lists
   StageTimer timers[MP_STAGE_COUNT];
@@ -207,7 +210,7 @@ struct mp_ctx {
   DBuf<int> sverts;         // (V) new ids
 
   // ---- per-step vectors (3N) ----
-  DBuf<double> x, xt, vel, g, z, p, Hp, p_prev, Hp_prev, z_prev, hv, x_start, x_best, tmp, tmp2;
+  DBuf<double> x, xt, vel, g, g_prev, z, p, Hp, p_prev, Hp_prev, z_prev, hv, x_start, x_best, tmp, tmp2;
 
   // ---- contact sets ----
   PairTable cur, base, scratch;
@@ -251,6 +254,7 @@ struct mp_ctx {
   // ---- MAS ----
   DBuf<double> Bblk;        // D * cyc(m) packed inverses
   DBuf<double> Mblk;        // D * cyc(m) packed subdomain blocks (direct refactor path)
+  DBuf<double> jac_inv;     // N * 9 inverse diagonal blocks (Jacobi baseline)
   std::vector<CoarseLevel*> levels;
   int n_levels = 0;
   cudaEvent_t ev_bsr = nullptr;     // H_base ready (coarse streams wait on it)
@@ -302,7 +306,7 @@ static void timer_fold(StageTimer& t) {
   t.pending = false;
 }
 
-static void timer_begin(mp_ctx* c, int id) {
+static void timer_begin(mp_ctx* c, int id, cudaStream_t s = nullptr) {
   if (!c->timing) return;
   StageTimer& t = c->timers[id];
   timer_fold(t);
@@ -310,13 +314,13 @@ static void timer_begin(mp_ctx* c, int id) {
     CUDA_CHECK(cudaEventCreate(&t.a));
     CUDA_CHECK(cudaEventCreate(&t.b));
   }
-  CUDA_CHECK(cudaEventRecord(t.a, c->stream));
+  CUDA_CHECK(cudaEventRecord(t.a, s ? s : c->stream));
 }
 
-static void timer_end(mp_ctx* c, int id, double bytes) {
+static void timer_end(mp_ctx* c, int id, double bytes, cudaStream_t s = nullptr) {
   if (!c->timing) return;
   StageTimer& t = c->timers[id];
-  CUDA_CHECK(cudaEventRecord(t.b, c->stream));
+  CUDA_CHECK(cudaEventRecord(t.b, s ? s : c->stream));
   t.pending = true;
   t.bytes += bytes;
 }

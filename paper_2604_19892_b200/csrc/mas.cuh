@@ -1030,6 +1030,25 @@ k_mas_apply_l0_direct(int64_t D, int64_t N, int bs, int m, const double* __restr
   }
 }
 
+// z += C_l^T y_l over the levels (the prolongation of the level-0 kernel,
+// same order), pinned rows 0; rows of [v0, v1)
+__global__ void k_prolong(int64_t v0, int64_t v1, int64_t N, int bs, const unsigned char* __restrict__ pinned,
+                          LevelViews LV, double* __restrict__ z) {
+  const int64_t dof = 3 * v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (dof >= 3 * v1) return;
+  const int64_t v = dof / 3;
+  const int c = (int)(dof - 3 * v);
+  const int64_t d = v / bs;
+  double acc = z[dof];
+  for (int l = 0; l < LV.L; ++l) {
+    const LevelView& L = LV.lv[l];
+    const int64_t a = d / L.ratio;
+    const int64_t na = (N - a * L.span) < L.span ? (N - a * L.span) : L.span;
+    acc += L.y[3 * a + c] * (1.0 / (double)na);
+  }
+  z[dof] = pinned[v] ? 0.0 : acc;
+}
+
 // ---------------------------------------------------------------------------
 // Sparse-Input Woodbury build, one CTA per touched subdomain.
 // smem: B (m x m full), U (m x K), W (m x K), cap (K x K)

@@ -32,6 +32,9 @@ mp_ctx::~mp_ctx() {
     if (t.b) cudaEventDestroy(t.b);
   }
   if (ev_bsr) cudaEventDestroy(ev_bsr);
+  if (ev_g) cudaEventDestroy(ev_g);
+  if (ev_l0) cudaEventDestroy(ev_l0);
+  if (side) cudaStreamDestroy(side);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -92,10 +95,10 @@ static void validate_config(const mp_solver_config& c) {
   if (!(c.eps > 0)) throw MpError(MP_ERR_CONFIG, "eps must be positive");
   if (!(c.delta > 0 && c.delta < 1)) throw MpError(MP_ERR_CONFIG, "delta must lie in (0, 1)");
   if (c.iter_max < 1) throw MpError(MP_ERR_CONFIG, "iter_max must be >= 1");
-  if (c.preconditioner != MP_PRECOND_MAS)
-    throw MpError(MP_ERR_CONFIG, "the B200 backend implements the MAS preconditioner only");
-  if (c.direction_rule != MP_DIR_SUBSPACE2D)
-    throw MpError(MP_ERR_CONFIG, "the B200 backend implements the Subspace2D direction rule only");
+  if (c.preconditioner != MP_PRECOND_MAS && c.preconditioner != MP_PRECOND_JACOBI)
+    throw MpError(MP_ERR_CONFIG, "unknown preconditioner");
+  if (c.direction_rule < MP_DIR_SUBSPACE2D || c.direction_rule > MP_DIR_CD)
+    throw MpError(MP_ERR_CONFIG, "unknown direction rule");
   if (c.update_strategy < 0 || c.update_strategy > 2) throw MpError(MP_ERR_CONFIG, "unknown update strategy");
   if (c.block_size < 1 || c.block_size > 32) throw MpError(MP_ERR_CONFIG, "block_size must lie in [1, 32]");
   if (c.K < 0) throw MpError(MP_ERR_CONFIG, "K must be >= 0");
@@ -213,6 +216,9 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bsr, cudaEventDisableTiming));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_g, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_l0, cudaEventDisableTiming));
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
   CUDA_CHECK(cudaMallocHost(&c->h_cnt, 16 * sizeof(int)));
@@ -382,7 +388,7 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
   const size_t n3 = 3 * (size_t)N;
-  for (DBuf<double>* b : {&c->x, &c->xt, &c->vel, &c->g, &c->z, &c->p, &c->Hp, &c->p_prev, &c->Hp_prev, &c->z_prev,
+  for (DBuf<double>* b : {&c->x, &c->xt, &c->vel, &c->g, &c->g_prev, &c->z, &c->p, &c->Hp, &c->p_prev, &c->Hp_prev, &c->z_prev,
                           &c->hv, &c->x_start, &c->x_best, &c->tmp, &c->tmp2})
     b->ensure(n3);
   c->counters.zero(16, c->stream);
@@ -460,6 +466,8 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
   bool restart = true;
   bool have_prev = false;   // p_prev / Hp_prev / z_prev valid
   double best = INFINITY;
+  const bool subspace = cfg.direction_rule == MP_DIR_SUBSPACE2D;
+  double prev_zg = 0.0, prev_gp = 0.0;  // g_prev.z_prev, g_prev.p_prev (baseline beta rules)
   R.recs.clear();
   R.converged = false;
   for (int64_t k = 0; k < cfg.iter_max; ++k) {
@@ -503,6 +511,8 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
       i_pg = add(c->p_prev, c->g);
       i_gzp = add(c->g, c->z_prev);
     }
+    int i_gpz = -1;
+    if (have_prev && !subspace) i_gpz = add(c->g_prev, c->z);
     multidot(c, n3, S);
     double dots[MAX_DOTS];
     std::memcpy(dots, c->h_scal, sizeof(double) * S.n);
@@ -515,14 +525,44 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     }
     double mu = 0.0, nu = 0.0;
     double pinf = 0.0;
+    double gp_now = 0.0;
     if (z_norm == 0.0) {
       CUDA_CHECK(cudaMemsetAsync(c->p.p, 0, n3 * 8, st));
       CUDA_CHECK(cudaMemsetAsync(c->Hp.p, 0, n3 * 8, st));
+    } else if (!subspace) {
+      // baseline_direction (solver.py:171-200, 393-400): p = -z + beta p_prev
+      double beta = 0.0;
+      if (!restart && have_prev) {
+        const double gz = zg, gzp = dots[i_gzp], pg = dots[i_pg], gpz = dots[i_gpz];
+        switch (cfg.direction_rule) {
+          case MP_DIR_FR: beta = gz / prev_zg; break;
+          case MP_DIR_PR: beta = (gz - gzp) / prev_zg; break;
+          case MP_DIR_DK: {
+            const double py = pg - prev_gp;  // p_prev.(g - g_prev)
+            if (py != 0.0) beta = (gz - gpz) / py - (gz - gzp - gpz + prev_zg) * pg / (py * py);
+            break;
+          }
+          default: beta = prev_gp != 0.0 ? -gz / prev_gp : 0.0; break;  // CD
+        }
+        beta = std::max(beta, 0.0);
+      }
+      form_direction(c, -1.0, beta, beta != 0.0 ? c->p_prev.p : nullptr, beta != 0.0 ? c->Hp_prev.p : nullptr);
+      gp_now = c->h_scal[0];
+      pinf = c->h_scal[1];
+      if (!restart && have_prev && gp_now >= 0.0) {  // not a descent direction: steepest
+        beta = 0.0;
+        form_direction(c, -1.0, 0.0, nullptr, nullptr);
+        gp_now = c->h_scal[0];
+        pinf = c->h_scal[1];
+      }
+      mu = 1.0;
+      nu = beta;
     } else if (restart || !have_prev) {
       if (zv <= 0.0) throw MpError(MP_ERR_MODEL_NOT_SPD, "z.Hz <= 0 at restart");
       mu = zg / zv;
       nu = 0.0;
       form_direction(c, -mu, 0.0, nullptr, nullptr);
+      gp_now = c->h_scal[0];
       pinf = c->h_scal[1];
     } else {
       // solve_2d_subspace (solver.py:147-161)
@@ -551,13 +591,39 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     double min_alpha = 1.0;
     bool certified = true;
     const double e_iter = c->record_energy ? energy(c, c->x, c->xt, h) : NAN;
-    if (pinf > 0.0) {
+    if (pinf > 0.0 && subspace) {
       timer_begin(c, MP_STAGE_CCD);
       CcdResult cr = ccd_clamp(c, c->x, c->p, pinf, cfg.ccd_per_subdomain != 0, c->tmp, c->ccd_exact_set);
       timer_end(c, MP_STAGE_CCD, 0.0);
       min_alpha = cr.min_alpha;
       certified = cr.certified;
       std::swap(c->x.p, c->tmp.p);
+    } else if (pinf > 0.0) {
+      // baselines: global pair step, then backtracking on the incremental
+      // potential with a fresh constraint set per trial (solver.py:283-293, 406-412)
+      timer_begin(c, MP_STAGE_CCD);
+      CcdResult cr = ccd_clamp(c, c->x, c->p, pinf, false, c->tmp, c->ccd_exact_set);
+      timer_end(c, MP_STAGE_CCD, 0.0);
+      min_alpha = cr.min_alpha;
+      const double e0 = energy(c, c->x, c->xt, h);  // cur still holds the set at x
+      double alpha = std::min(1.0, min_alpha);
+      for (int it = 0; it < 40; ++it) {
+        k_ccd_update<<<grid_for(n3, 256), 256, 0, st>>>(c->N, c->bs, c->x, c->p, nullptr, alpha, c->tmp);
+        LAUNCH_CHECK();
+        bool lower = false;
+        try {
+          constraint_set(c, c->tmp);
+          lower = energy(c, c->tmp, c->xt, h) < e0;
+        } catch (const MpError& e) {
+          if (e.status != MP_ERR_PENETRATION && e.status != MP_ERR_DEGENERATE) throw;
+        }
+        if (lower) break;
+        alpha *= 0.5;
+      }
+      k_ccd_update<<<grid_for(n3, 256), 256, 0, st>>>(c->N, c->bs, c->x, c->p, nullptr, alpha, c->tmp);
+      LAUNCH_CHECK();
+      std::swap(c->x.p, c->tmp.p);
+      mu = alpha;
     }
     sync_stream(c);
     auto t3 = Clock::now();
@@ -599,6 +665,9 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     std::swap(c->z_prev.p, c->z.p);
     std::swap(c->p_prev.p, c->p.p);
     std::swap(c->Hp_prev.p, c->Hp.p);
+    if (!subspace) std::swap(c->g_prev.p, c->g.p);  // history g_prev (solver.py:449)
+    prev_zg = zg;
+    prev_gp = gp_now;
     have_prev = true;
   }
   if (!R.converged) {
@@ -728,6 +797,7 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_BP_FUSED) c->bp_fused = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     else if (option == MP_OPT_KEEP_COARSE) c->keep_coarse = value != 0;
     else if (option == MP_OPT_GRAD_FUSED) c->fused_grad = value != 0;
+    else if (option == MP_OPT_APPLY_OVERLAP) c->overlap_apply = value != 0;
     else if (option == MP_OPT_APPEND_LIMIT) {
       const int lim = (int)std::max<int64_t>(64, std::min<int64_t>(HQ_APPEND_LIMIT, value <= 0 ? HQ_APPEND_LIMIT : value));
       CUDA_CHECK(cudaMemcpyToSymbol(g_append_limit, &lim, sizeof(int)));

@@ -211,6 +211,89 @@ static void mas_build(mp_ctx* c) {
   c->have_mas = true;
 }
 
+// ---------------------------------------------------------------------------
+// 3x3 block Jacobi baseline (solver.py:207-246): per vertex, the diagonal
+// block of H_base (BSR diagonal slot + the vertex's own contact terms
+// k g_a g_a^T) plus, for the non-rebuild branch, the candidates' u_a u_a^T
+// (_blocks_with_updates); Cholesky-checked ("non-spd-block") and inverted.
+
+__device__ __forceinline__ void add_outer3(double B[9], const double* a, const double* b, double s) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) B[3 * r + q] += s * a[r] * b[q];
+}
+
+__global__ void k_jacobi_blocks(int64_t v0, int64_t v1, const int* __restrict__ diag_slot,
+                                const double* __restrict__ bsr, const int* __restrict__ b_off,
+                                const int* __restrict__ b_val, const double* __restrict__ b_grad,
+                                const double* __restrict__ b_k, const int* __restrict__ q_off,
+                                const int* __restrict__ q_val, const double* __restrict__ q_u,
+                                double* __restrict__ inv, int* __restrict__ status) {
+  const int64_t v = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= v1) return;
+  double B[9];
+  const double* d = bsr + 9 * (int64_t)diag_slot[v];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) B[q] = d[q];
+  if (b_off)
+    for (int e = b_off[v]; e < b_off[v + 1]; ++e) {
+      const int inc = b_val[e];
+      const double* g = b_grad + 12 * (int64_t)(inc >> 2) + 3 * (inc & 3);
+      add_outer3(B, g, g, b_k[inc >> 2]);
+    }
+  if (q_off)
+    for (int e = q_off[v]; e < q_off[v + 1]; ++e) {
+      const int inc = q_val[e];
+      const double* u = q_u + 12 * (int64_t)(inc >> 2) + 3 * (inc & 3);
+      if (u[0] != 0.0 || u[1] != 0.0 || u[2] != 0.0) add_outer3(B, u, u, 1.0);
+    }
+  // Cholesky pivots (np.linalg.cholesky's failure), then the inverse
+  const double l00 = B[0];
+  const double l10 = B[3], l20 = B[6];
+  const double p1 = B[4] - l10 * l10 / l00;
+  const double p2 = B[8] - l20 * l20 / l00 - (B[7] - l20 * l10 / l00) * (B[7] - l20 * l10 / l00) / p1;
+  if (!(l00 > 0.0) || !(p1 > 0.0) || !(p2 > 0.0)) {
+    atomicExch(status, 1);
+    return;
+  }
+  const double c00 = B[4] * B[8] - B[5] * B[7], c01 = B[2] * B[7] - B[1] * B[8], c02 = B[1] * B[5] - B[2] * B[4];
+  const double det = B[0] * c00 + B[3] * c01 + B[6] * c02;
+  const double id = 1.0 / det;
+  double* o = inv + 9 * v;
+  o[0] = c00 * id; o[1] = c01 * id; o[2] = c02 * id;
+  o[3] = (B[5] * B[6] - B[3] * B[8]) * id; o[4] = (B[0] * B[8] - B[2] * B[6]) * id; o[5] = (B[2] * B[3] - B[0] * B[5]) * id;
+  o[6] = (B[3] * B[7] - B[4] * B[6]) * id; o[7] = (B[1] * B[6] - B[0] * B[7]) * id; o[8] = (B[0] * B[4] - B[1] * B[3]) * id;
+}
+
+__global__ void k_jacobi_apply(int64_t v0, int64_t v1, const double* __restrict__ inv, const double* __restrict__ g,
+                               double* __restrict__ z) {
+  const int64_t v = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= v1) return;
+  const double* B = inv + 9 * v;
+  const double g0 = g[3 * v], g1 = g[3 * v + 1], g2 = g[3 * v + 2];
+  z[3 * v] = B[0] * g0 + B[1] * g1 + B[2] * g2;
+  z[3 * v + 1] = B[3] * g0 + B[4] * g1 + B[5] * g2;
+  z[3 * v + 2] = B[6] * g0 + B[7] * g1 + B[8] * g2;
+}
+
+// JacobiPreconditioner(blocks) (solver.py:213-231); with_cands adds the
+// update candidates (solver.py:234-241)
+static void jacobi_build(mp_ctx* c, bool with_cands) {
+  c->jac_inv.ensure(9 * (size_t)c->N);
+  CUDA_CHECK(cudaMemsetAsync(c->counters.p + 11, 0, sizeof(int), c->stream));
+  const int64_t nv = c->own_v1 - c->own_v0;
+  const bool nb = c->base.count > 0, nq = with_cands && c->n_cand > 0;
+  if (nv > 0)
+    k_jacobi_blocks<<<grid_for(nv, 128), 128, 0, c->stream>>>(
+        c->own_v0, c->own_v1, c->diag_slot, c->bsr, nb ? c->inc_base.off.p : nullptr, c->inc_base.val2.p,
+        c->base.grad, c->base.k, nq ? c->inc_cand.off.p : nullptr, c->inc_cand.val2.p, c->cand_u, c->jac_inv,
+        c->counters.p + 11);
+  LAUNCH_CHECK();
+  if (group_or(c, read_status(c, c->counters.p + 11))) throw MpError(MP_ERR_NON_SPD_BLOCK, "Jacobi block not SPD");
+  c->have_mas = true;  // "a preconditioner is built"
+}
+
 // rebuild branch of advance_step (solver.py:323-335): base := cur at x,
 // H_base = assemble_base_hessian, MAS hierarchy
 static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
@@ -237,7 +320,8 @@ static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
   c->n_touched = 0;
   if (build_mas) {
     timer_begin(c, MP_STAGE_MAS_BUILD);
-    mas_build(c);
+    if (c->cfg.preconditioner == MP_PRECOND_JACOBI) jacobi_build(c, false);
+    else mas_build(c);
     timer_end(c, MP_STAGE_MAS_BUILD, 0.0);
   }
 }
@@ -248,6 +332,10 @@ static void update_build(mp_ctx* c) {
   classify_all(c, c->cfg.eps_rot);
   c->have_updates = false;
   c->n_touched = 0;
+  if (c->cfg.preconditioner == MP_PRECOND_JACOBI) {  // solver.py:344-346
+    if (c->cfg.update_strategy != MP_UPDATE_FREEZE && c->have_mas) jacobi_build(c, true);
+    return;
+  }
   if (c->cfg.update_strategy == MP_UPDATE_FREEZE || c->n_cand == 0 || !c->have_mas) return;
   const int64_t nc = c->n_cand;
   c->ent_count.ensure(nc + 1);
@@ -317,8 +405,39 @@ static void update_build(mp_ctx* c) {
 
 // mas.apply_preconditioner + z[pinned] = 0
 static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updates) {
+  if (c->cfg.preconditioner == MP_PRECOND_JACOBI) {  // jac.apply (solver.py:228-229)
+    const int64_t nv = c->own_v1 - c->own_v0;
+    if (nv > 0) k_jacobi_apply<<<grid_for(nv, 256), 256, 0, c->stream>>>(c->own_v0, c->own_v1, c->jac_inv, g, z);
+    LAUNCH_CHECK();
+    if (c->nshards > 1 && z != c->z.p) throw MpError(MP_ERR_CONFIG, "group apply writes the context's z only");
+    group_allgather(c, [](mp_ctx* p) { return p->z.p; },
+                    [](mp_ctx* p, int64_t& lo, int64_t& hi) { lo = 3 * p->own_v0; hi = 3 * p->own_v1; });
+    return;
+  }
   LevelViews LV{};
   LV.L = c->n_levels;
+  // overlap (MP_OPT_APPLY_OVERLAP, default): the level-0 block products
+  // (no prolongation) on the side stream, beside the restriction and coarse
+  // matvecs on the main stream; k_prolong adds the coarse correction
+  const bool overlap = c->overlap_apply && c->n_levels > 0;
+  if (overlap) {
+    const bool ov0 = with_updates && c->have_updates;
+    const int64_t Down0 = c->own_d1 - c->own_d0;
+    LevelViews L0{};
+    L0.L = 0;
+    L0.d0 = c->own_d0;
+    CUDA_CHECK(cudaEventRecord(c->ev_g, c->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(c->side, c->ev_g, 0));
+    double b0 = 8.0 * (double)c->D * (double)cyc_size(c->m) + 48.0 * c->N;
+    for (int l = 0; l < c->n_levels; ++l) b0 += 8.0 * c->levels[l]->n;
+    timer_begin(c, MP_STAGE_MAS_L0, c->side);
+    if (Down0 > 0)
+      k_mas_apply_l0_direct<<<(unsigned)Down0, APPLY_THREADS, 0, c->side>>>(
+          Down0, c->N, c->bs, c->m, c->Bblk, ov0 ? c->overlay_of.p : nullptr, c->overlay, g, c->pinned, L0, z);
+    LAUNCH_CHECK();
+    timer_end(c, MP_STAGE_MAS_L0, b0, c->side);
+    CUDA_CHECK(cudaEventRecord(c->ev_l0, c->side));
+  }
   for (int l = 0; l < c->n_levels; ++l) {
     CoarseLevel& L = *c->levels[l];
     if (l == 0) {
@@ -348,26 +467,41 @@ static void precond_apply(mp_ctx* c, const double* g, double* z, bool with_updat
   const int64_t Down = c->own_d1 - c->own_d0;  // this shard's subdomains
   LV.d0 = c->own_d0;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(Down, (int64_t)c->apply_ctas_per_sm * 148));
-  timer_begin(c, MP_STAGE_MAS_L0);
   const int* ovp = ov ? c->overlay_of.p : nullptr;
-#define L0_ARGS Down, c->N, c->bs, c->m, c->Bblk, ovp, c->overlay, g, c->pinned, LV, z
-  if (Down <= 0) {
-  } else if (c->apply_mode == 2) {
-    k_mas_apply_l0_direct<<<(unsigned)Down, APPLY_THREADS, 0, c->stream>>>(L0_ARGS);
-  } else if (c->apply_mode == 1) {
-    if (stages == 3) k_mas_apply_l0<true, 3><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
-    else k_mas_apply_l0<true, 2><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
-  } else {
-    if (stages == 3) k_mas_apply_l0<false, 3><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
-    else k_mas_apply_l0<false, 2><<<grid, APPLY_THREADS, smem, c->stream>>>(L0_ARGS);
-  }
-#undef L0_ARGS
-  LAUNCH_CHECK();
-  // algorithmic bytes of this kernel: every packed block once, g and z,
-  // the coarse corrections it reads (3 A_l doubles per level)
+  // algorithmic bytes of the level-0 kernel: every packed block once, g and
+  // z, the coarse corrections it reads (3 A_l doubles per level)
   double l0_bytes = 8.0 * (double)c->D * (double)cyc_size(c->m) + 48.0 * c->N;
   for (int l = 0; l < c->n_levels; ++l) l0_bytes += 8.0 * c->levels[l]->n;
-  timer_end(c, MP_STAGE_MAS_L0, l0_bytes);
+  auto launch_l0 = [&](cudaStream_t s, const LevelViews& V) {
+    timer_begin(c, MP_STAGE_MAS_L0, s);
+#define L0_ARGS Down, c->N, c->bs, c->m, c->Bblk, ovp, c->overlay, g, c->pinned, V, z
+    if (Down <= 0) {
+    } else if (c->apply_mode == 2) {
+      k_mas_apply_l0_direct<<<(unsigned)Down, APPLY_THREADS, 0, s>>>(L0_ARGS);
+    } else if (c->apply_mode == 1) {
+      if (stages == 3) k_mas_apply_l0<true, 3><<<grid, APPLY_THREADS, smem, s>>>(L0_ARGS);
+      else k_mas_apply_l0<true, 2><<<grid, APPLY_THREADS, smem, s>>>(L0_ARGS);
+    } else {
+      if (stages == 3) k_mas_apply_l0<false, 3><<<grid, APPLY_THREADS, smem, s>>>(L0_ARGS);
+      else k_mas_apply_l0<false, 2><<<grid, APPLY_THREADS, smem, s>>>(L0_ARGS);
+    }
+#undef L0_ARGS
+    LAUNCH_CHECK();
+    timer_end(c, MP_STAGE_MAS_L0, l0_bytes, s);
+  };
+  if (!overlap) {
+    launch_l0(c->stream, LV);
+  } else {
+    // the coarse chain is already queued on the main stream; the level-0
+    // block products ran beside it on the side stream; add the coarse
+    // prolongation once both are done (same sums in the same order as the
+    // fused kernel: acc + C_1^T y_1 + C_2^T y_2)
+    CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_l0, 0));
+    const int64_t nd = 3 * (c->own_v1 - c->own_v0);
+    if (nd > 0)
+      k_prolong<<<grid_for(nd, 256), 256, 0, c->stream>>>(c->own_v0, c->own_v1, c->N, c->bs, c->pinned, LV, z);
+    LAUNCH_CHECK();
+  }
   // z on the owned rows -> every shard (the HVP reads z at every neighbour)
   // (z is always the context's z buffer; every shard swaps its buffers in lockstep)
   if (c->nshards > 1 && z != c->z.p) throw MpError(MP_ERR_CONFIG, "group apply writes the context's z only");

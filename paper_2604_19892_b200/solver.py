@@ -215,3 +215,10 @@ def step(scene: Scene, x, v, h, config: SolverConfig):
     x_out, v_out, recs, conv, flags = ctx.step(x, v, h)
     state = prepare_step(x, v, scene.mass, h, scene.f_ext, scene.dirichlet)
     return replace(state, x=x_out, v=v_out), _trace(recs, conv, flags)
+
+
+def total_energy(scene: Scene, state: SimState, x, config: SolverConfig = None):
+    """Incremental potential at x with a fresh constraint set
+    (`solver.py:262-265`), on the device."""
+    ctx = scene.context(config or SolverConfig())
+    return ctx.energy(x, state.x_tilde, state.h)

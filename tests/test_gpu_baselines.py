@@ -1,0 +1,34 @@
+"""Device baselines against the reference's own
+trajectories (tests/golden/make_baseline_golden.py): the 3x3 block Jacobi
+preconditioner (solver.py:207-246) and the FR / PR / DK / CD direction
+rules with the backtracking line search (solver.py:171-200, 283-293,
+393-412).  Per-frame PNCG iteration counts within +-5% (at least +-1), the
+same convergence flags, and the final positions within 1e-6 relative."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2604_19892_b200 import scenes, solver
+
+pytestmark = pytest.mark.gpu
+G = np.load(Path(__file__).resolve().parent / "golden" / "baselines.npz")
+
+
+@pytest.mark.parametrize("i", range(int(G["n"])))
+def test_baseline_matches_reference(i):
+    name, pre, rule = [str(s) for s in G[f"v{i}_meta"]]
+    scene = scenes.drop() if name == "drop" else scenes.stacked_boxes()
+    v = np.zeros(3 * scene.mesh.n_vertices) if name == "drop" else scenes.stacked_boxes_v0(scene)
+    x = scene.mesh.rest_positions.ravel().copy()
+    cfg = solver.SolverConfig(preconditioner=pre, direction_rule=rule, iter_max=300)
+    ref_iters, ref_conv = G[f"v{i}_iters"], G[f"v{i}_converged"]
+    for f in range(len(ref_iters)):
+        st, tr = solver.step(scene, x, v, 0.01, cfg)
+        x, v = st.x, st.v
+        tol = max(1, int(np.ceil(0.05 * ref_iters[f])))
+        assert abs(tr.iterations - int(ref_iters[f])) <= tol, (f, tr.iterations, ref_iters[f])
+        assert tr.converged == bool(ref_conv[f])
+    ref_x = G[f"v{i}_x"]
+    assert np.linalg.norm(x - ref_x) <= 1e-6 * np.linalg.norm(ref_x)

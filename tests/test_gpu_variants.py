@@ -85,7 +85,7 @@ def test_append_overflow_rerun_same_bits(name):
 
 @pytest.mark.parametrize("name", ["stacked_k256", "locking", "cube3_capped"])
 def test_gradient_fused_same_bits(name):
-    """MP_OPT_GRAD_FUSED (9): the one-pass per-vertex gradient (default)
+    """MP_OPT_GRAD_FUSED (9): the one-pass per-vertex gradient
     computes each corner force with the per-tet kernel's expression and sums
     them in the gather's order: the same bits."""
     g = load_golden(name)
@@ -96,5 +96,25 @@ def test_gradient_fused_same_bits(name):
         for mode in (1, 0):
             ctx.set_option(9, mode)
             out.append(ctx.gradient(t["x"], t["x_tilde"], float(t["h"])))
-        ctx.set_option(9, 1)
+        ctx.set_option(9, 0)
         assert np.array_equal(out[0], out[1])
+
+
+def test_apply_overlap_same_bits():
+    """MP_OPT_APPLY_OVERLAP (10): level 0 on a side stream beside the coarse
+    chain, then the prolongation pass -- the same sums as the fused kernel,
+    with and without a Woodbury overlay."""
+    g = load_golden("stacked_k256")
+    scene = scene_from_golden(g)
+    ctx = scene.context(golden_config(g))
+    for t in golden_taps(g, "precond"):
+        ctx.snapshot(t["x_base"], float(t["h"]), build_mas=True)
+        wb = bool(t["has_wb"])
+        if wb:
+            ctx.update_at(t["x_cur"])
+        zs = []
+        for mode in (1, 0):
+            ctx.set_option(10, mode)
+            zs.append(ctx.precond_apply(t["g"], with_updates=wb))
+        ctx.set_option(10, 1)
+        assert np.array_equal(zs[0], zs[1])

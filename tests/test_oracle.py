@@ -277,3 +277,15 @@ def test_from_scene_matches_golden_arrays():
     for k in ("rest", "tets", "Bm", "vol", "mass", "f_ext", "tris", "edges", "surf_verts"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
+
+
+def test_oracle_tri_tri_cases():
+    """The checker oracle's tri-tri test (geometry.py:686-732 rules)."""
+    from oracle.geometry import tri_tri_intersect
+
+    a = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float)
+    assert tri_tri_intersect(a, [[0.2, 0.2, -0.5], [0.3, 0.2, 0.5], [0.2, 0.3, 0.5]])  # crossing
+    assert not tri_tri_intersect(a, [[0.2, 0.2, 0.1], [0.3, 0.2, 0.5], [0.2, 0.3, 0.5]])  # above
+    assert tri_tri_intersect(a, [[1, 0, 0], [2, 0, 1], [2, 0, -1]])  # touching at a vertex counts
+    assert tri_tri_intersect(a, [[0.1, 0.1, 0], [0.5, 0.1, 0], [0.1, 0.5, 0]])  # coplanar, inside
+    assert not tri_tri_intersect(a, [[2, 2, 0], [3, 2, 0], [2, 3, 0]])  # coplanar, apart

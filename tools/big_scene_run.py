@@ -33,7 +33,11 @@ else:
     v0 = scenes.c5_puffer_v0(scene, speed=2.0)
     h, cfg = 0.005, solver.SolverConfig(iter_max=iter_max, coarse_block=32)
 build_s = time.time() - t0
+print(json.dumps({"scene": which, "n_verts": int(scene.mesh.n_vertices), "n_tets": int(len(scene.elastic.vol)),
+                  "build_s": round(build_s, 1)}), flush=True)
+t0 = time.time()
 ctx = scene.context(cfg, devices=devices) if devices else scene.context(cfg)
+print(json.dumps({"context_s": round(time.time() - t0, 1)}), flush=True)
 x0 = scene.mesh.rest_positions.ravel().copy()
 ctx.set_state(x0, v0)
 stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", 0))
