@@ -241,7 +241,9 @@ enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3,
        MP_OPT_APPLY_CTAS = 5, MP_OPT_BP_FUSED = 6, MP_OPT_KEEP_COARSE = 7,
        MP_OPT_APPEND_LIMIT = 8 /* test knob: process-wide one-pass list limit (default and max 2^30; <= 0 resets) */,
        MP_OPT_GRAD_FUSED = 9 /* gradient: 1 one fused per-vertex pass, 0 (default, faster) per-tet scratch + gather; same bits */,
-       MP_OPT_APPLY_OVERLAP = 10 /* MAS apply: 1 (default) level 0 beside the coarse chain + prolongation pass, 0 fused; same bits */ };
+       MP_OPT_APPLY_OVERLAP = 10 /* MAS apply: 1 (default) level 0 beside the coarse chain + prolongation pass, 0 fused; same bits */,
+       MP_OPT_CCD_PREFILTER = 11 /* tight CCD: 1 (default) exact relative-motion pair prefilter, 0 off; same results */,
+       MP_OPT_CCD_BODIES = 12 /* tight CCD: 1 two passes (same-body / cross-body centres), 0 (default) one global centre; same results */ };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 
@@ -258,9 +260,13 @@ int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t*
  * geometry.tri_tri_intersect, geometry.py:686-732) on `device`: the number
  * of intersecting non-adjacent triangle pairs of the surface (x: (N,3),
  * tris: (F,3)) and the smallest triangle index involved (-1 if none).
- * Uniform-grid candidates, O(F) instead of the reference's O(F^2). */
+ * Uniform-grid candidates, O(F) instead of the reference's O(F^2).
+ * coplanar_tol = 0 is the reference's rule (coplanar iff every
+ * vertex-plane value is exactly 0); > 0 treats pairs coplanar to within
+ * coplanar_tol x the longest edge as coplanar (the reference's rule reports
+ * disjoint faces that are coplanar to rounding as intersecting). */
 int mp_check_intersections(int device, int64_t n_verts, const double* x, int64_t n_tris, const int64_t* tris,
-                           int64_t* n_hits, int64_t* first_tri);
+                           double coplanar_tol, int64_t* n_hits, int64_t* first_tri);
 
 /* Change the barrier parameters of a context (Scene.d_hat / kappa); the
  * checker uses a surface-only context with d_hat = its search radius. */

@@ -310,8 +310,11 @@ def _in_tri_2d(p, a, b, c):
     return not (min(s) < 0 and max(s) > 0)
 
 
-def tri_tri_intersect(t1, t2):
-    """Touching counts; the coplanar case in 2-D on the dominant axes."""
+def tri_tri_intersect(t1, t2, coplanar_tol=0.0):
+    """Touching counts; the coplanar case in 2-D on the dominant axes.
+    coplanar_tol = 0: the reference's exact rule; > 0: vertex-plane values
+    within coplanar_tol x |n| x the longest edge count as coplanar (the GPU
+    checker's default 1e-9)."""
     t1, t2 = np.asarray(t1, float), np.asarray(t2, float)
     n1 = np.cross(t1[1] - t1[0], t1[2] - t1[0])
     n2 = np.cross(t2[1] - t2[0], t2[2] - t2[0])
@@ -321,7 +324,10 @@ def tri_tri_intersect(t1, t2):
     d1 = t1 @ n2 - t2[0] @ n2
     if np.all(d1 > 0) or np.all(d1 < 0):
         return False
-    if np.all(d2 == 0.0) or np.all(d1 == 0.0):
+    L = max(np.linalg.norm(np.roll(t, -1, axis=0) - t, axis=1).max() for t in (t1, t2))
+    cop2 = np.all(np.abs(d2) <= coplanar_tol * L * np.linalg.norm(n1)) if coplanar_tol else np.all(d2 == 0.0)
+    cop1 = np.all(np.abs(d1) <= coplanar_tol * L * np.linalg.norm(n2)) if coplanar_tol else np.all(d1 == 0.0)
+    if cop2 or cop1:
         keep = [i for i in range(3) if i != int(np.argmax(np.abs(n1)))]
         a, b = t1[:, keep], t2[:, keep]
         if any(_seg_seg_2d(a[i], a[(i + 1) % 3], b[j], b[(j + 1) % 3]) for i in range(3) for j in range(3)):
@@ -340,7 +346,7 @@ def tri_tri_intersect(t1, t2):
     return max(lo1, lo2) <= min(hi1, hi2)
 
 
-def count_tri_intersections(x, tris):
+def count_tri_intersections(x, tris, coplanar_tol=0.0):
     """Non-adjacent intersecting triangle pairs (`cli.py:393-401`), boxes
     first (O(F^2) box test, vectorised), exact test on overlapping boxes."""
     x = np.asarray(x, float).reshape(-1, 3)
@@ -353,5 +359,5 @@ def count_tri_intersections(x, tris):
         for j in np.nonzero(ov)[0] + i + 1:
             if set(tris[i].tolist()) & set(tris[j].tolist()):
                 continue
-            n += bool(tri_tri_intersect(p[i], p[j]))
+            n += bool(tri_tri_intersect(p[i], p[j], coplanar_tol))
     return n

@@ -92,7 +92,7 @@ def load_library():
     lib.mp_launch_count.restype = C.c_int64
     lib.mp_partition.argtypes = [vp, _i64p, _i64p]
     lib.mp_partition_host.argtypes = [_f64p, C.c_int64, C.c_int32, _i64p]
-    lib.mp_check_intersections.argtypes = [C.c_int, C.c_int64, _f64p, C.c_int64, _i64p, _i64p, _i64p]
+    lib.mp_check_intersections.argtypes = [C.c_int, C.c_int64, _f64p, C.c_int64, _i64p, C.c_double, _i64p, _i64p]
     lib.mp_set_contact.argtypes = [vp, C.c_double, C.c_double]
     lib.mp_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _i64p]
     lib.mp_spd_inverse.argtypes = [C.c_int, C.c_int64, _f64p, _f64p, C.POINTER(C.c_int32)]
@@ -148,15 +148,17 @@ def partition_host(rest, block_size):
     return out
 
 
-def check_intersections(positions, triangles, device=0):
+def check_intersections(positions, triangles, device=0, coplanar_tol=1e-9):
     """(number of intersecting non-adjacent triangle pairs, first triangle
-    index or -1) of a surface, on the device (mp_check_intersections)."""
+    index or -1) of a surface, on the device (mp_check_intersections);
+    coplanar_tol = 0 is the reference's exact-coplanarity rule."""
     lib = load_library()
     x = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
     t = np.ascontiguousarray(triangles, dtype=np.int64).reshape(-1, 3)
     n, first = C.c_int64(), C.c_int64()
-    raise_status(lib.mp_check_intersections(int(device), len(x), _ptr(x), len(t), _ptr(t, C.c_int64), C.byref(n),
-                                            C.byref(first)), "mp_check_intersections")
+    raise_status(lib.mp_check_intersections(int(device), len(x), _ptr(x), len(t), _ptr(t, C.c_int64),
+                                            float(coplanar_tol), C.byref(n), C.byref(first)),
+                 "mp_check_intersections")
     return int(n.value), int(first.value)
 
 

@@ -578,12 +578,49 @@ struct BpTables {
   const double *flo, *fhi;              // (F+E)*3 reference filter / join boxes
   const double *elo, *ehi;              // (F+E+V)*3 enumeration boxes
   int64_t F, P;                         // object id bases: edges at F, points at P
+  const int* body = nullptr;            // (N) body of each vertex (connected component)
+  int body_mode = 0;                    // 0 all pairs, 1 same-body pairs only, 2 cross-body pairs only
+  const double* objmot = nullptr;       // (F+E+V)*4 per-object motion (c, m): exact CCD prefilter, or null
+  const double *rlo = nullptr, *rhi = nullptr;  // (F+E)*3 raw primitive boxes
 };
+
+// Exact relative-motion prefilter of the tight CCD enumeration.  For any
+// constant c the reference's relative displacement bound (ccd.py:172-179)
+// is at most 4 max_a |p_a - c| over the pair's vertices; with c = c_1 (c_2)
+// that is 4 max(m_1, m_2 + |c_1 - c_2|) (resp. swapped), and the distance
+// is at least the gap between the raw boxes.  A pair with 0.9 gap > that
+// bound gets alpha_pair = 1 exactly and passes certify_mixed's distance
+// test, so dropping it changes no alpha_d, minimum or certificate.  Unlike
+// the enumeration boxes (one global c), the bound is relative: a rigidly
+// moving or rotating neighbourhood keeps only its truly close pairs.
+__device__ __forceinline__ bool rel_safe(const BpTables& T, int64_t o1, int64_t o2, const double* l1,
+                                         const double* h1, const double* l2, const double* h2) {
+  if (!T.objmot) return false;
+  double g2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double d = fmax(0.0, fmax(l1[k] - h2[k], l2[k] - h1[k]));
+    g2 += d * d;
+  }
+  const double* a = T.objmot + 4 * o1;
+  const double* b = T.objmot + 4 * o2;
+  const double dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+  const double dl = sqrt(dx * dx + dy * dy + dz * dz);
+  const double M = fmin(fmax(a[3], b[3] + dl), fmax(b[3], a[3] + dl));
+  const double lhs = 0.9 * sqrt(g2) * (1.0 - 1e-12), rhs = 4.0 * M * (1.0 + 1e-12);
+  return lhs > rhs;
+}
+
+// the body filter of the two-pass tight CCD enumeration (ccd.cuh)
+__device__ __forceinline__ bool body_pass(const BpTables& T, int u, int w) {
+  return T.body_mode == 0 || ((T.body[u] == T.body[w]) == (T.body_mode == 1));
+}
 
 // PT filter (geometry.py:484-486) + reference reachability, point q vs tri t
 __device__ __forceinline__ bool pt_ref_pass(const BpTables& T, const int* tri, const double* x, int v, int64_t q,
                                             int t) {
   if (tri[3 * t] == v || tri[3 * t + 1] == v || tri[3 * t + 2] == v) return false;
+  if (!body_pass(T, v, tri[3 * t])) return false;
   const double* l = T.flo + 3 * (int64_t)t;
   const double* h = T.fhi + 3 * (int64_t)t;
   const double p0 = x[3 * v], p1 = x[3 * v + 1], p2 = x[3 * v + 2];
@@ -722,7 +759,9 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
               t = T.tri_ent[e];
               const double* tl = T.tri_box + 6 * (int64_t)e;
               pass = boxes_meet(pl, ph, tl, tl + 3) &&
-                     pt_ref_pass(T, tri, x, v, q, t);
+                     pt_ref_pass(T, tri, x, v, q, t) &&
+                     !rel_safe(T, T.P + q, t, x + 3 * (int64_t)v, x + 3 * (int64_t)v, T.rlo + 3 * (int64_t)t,
+                               T.rhi + 3 * (int64_t)t);
             }
             hq_emit<EM>(pass, true, lane, n, o, v, t, pa, pb, cap, Q, qn, A);
           }
@@ -767,7 +806,9 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
               const double* pl = T.pt_box + 6 * (int64_t)e;
               v = sverts[q];
               pass = boxes_meet(pl, pl + 3, tl, th) &&
-                     pt_ref_pass(T, tri, x, v, q, (int)t);
+                     pt_ref_pass(T, tri, x, v, q, (int)t) &&
+                     !rel_safe(T, T.P + q, t, x + 3 * (int64_t)v, x + 3 * (int64_t)v, T.rlo + 3 * t,
+                               T.rhi + 3 * t);
             }
             hq_emit<EM>(pass, true, lane, n, o, v, (int)t, pa, pb, cap, Q, qn, A);
           }
@@ -819,9 +860,11 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
                 const double* flj = T.flo + 3 * (T.F + j);
                 const double* fhj = T.fhi + 3 * (T.F + j);
                 // reference join filter (geometry.py:491-498) + reachability
-                pass = !(ia == ja || ia == jb || ib == ja || ib == jb) && fli[0] <= fhj[0] &&
+                pass = !(ia == ja || ia == jb || ib == ja || ib == jb) && body_pass(T, ia, ja) && fli[0] <= fhj[0] &&
                        fli[1] <= fhj[1] && fli[2] <= fhj[2] && flj[0] <= fhi[0] && flj[1] <= fhi[1] &&
-                       flj[2] <= fhi[2] && ref_reach(T.rc, T.F + i, T.F + j);
+                       flj[2] <= fhi[2] && ref_reach(T.rc, T.F + i, T.F + j) &&
+                       !rel_safe(T, T.F + i, T.F + j, T.rlo + 3 * (T.F + i), T.rhi + 3 * (T.F + i),
+                                 T.rlo + 3 * (T.F + j), T.rhi + 3 * (T.F + j));
               }
             }
             hq_emit<EM>(pass, false, lane, n, o, min((int)i, j), max((int)i, j), pa, pb, cap, Q, qn, A);
@@ -842,11 +885,14 @@ struct BpGrid {
 // Everything one broad-phase call at (x, mb, d_hat) needs: boxes, levels,
 // reference cell ranges and the per-level cell tables of triangles / edges /
 // surface points.  infl (per vertex, device) switches to tight enumeration.
-static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, const double* infl = nullptr) {
+static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, const double* infl = nullptr,
+                       int body_mode = 0) {
   BpGrid B;
   const int64_t F = c->F, P = c->F + c->E, V = c->V, nobj = P + V;
   B.T.F = F;
   B.T.P = P;
+  B.T.body = c->body.p;
+  B.T.body_mode = body_mode;
   if (F == 0) return B;
   const double gap = d_hat + 2.0 * mb;
   cudaStream_t st = c->stream;
@@ -970,6 +1016,7 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   T.rc = g.rc;
   T.flo = c->box_flo; T.fhi = c->box_fhi;
   T.elo = c->box_elo; T.ehi = c->box_ehi;
+  T.rlo = c->box_rlo; T.rhi = c->box_rhi;  // (after every ensure above: the pointers are final)
   B.empty = false;
   return B;
 }

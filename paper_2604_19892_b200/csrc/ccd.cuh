@@ -244,6 +244,82 @@ __global__ void k_motion_midrange(int64_t N, int bs, const double* __restrict__ 
   if (threadIdx.x == 0) *done = 0;
 }
 
+// Per-body tight enumeration (n_bodies > 1): the same bound with a per-pair
+// choice of c.  Same-body pairs use their body's midrange c_b (inflation
+// 4.5 |s p_v - c_b|); cross-body pairs use the midrange C of the body
+// centres (inflation 4.5 (|s p_v - c_b| + |c_b - C|) >= 4.5 |s p_v - C|,
+// so the pair's two boxes grown this way cover the single-c criterion).
+// Each pair is enumerated in exactly one of the two passes.
+
+// order-preserving unsigned encoding of doubles (for atomic min / max)
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__global__ void k_body_minmax(int64_t N, int bs, const int* __restrict__ body, const double* __restrict__ p,
+                              const double* __restrict__ alpha_d, unsigned long long* __restrict__ mm) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  const double s = alpha_d ? alpha_d[v / bs] : 1.0;
+  unsigned long long* m = mm + 6 * (int64_t)body[v];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned long long q = ord_key(s * p[3 * v + k]);
+    atomicMin(m + k, q);
+    atomicMax(m + 3 + k, q);
+  }
+}
+
+// body centres c_b (nb x 3) and the midrange C of the centres ([3*nb..])
+__global__ void k_body_centres(int nb, const unsigned long long* __restrict__ mm, double* __restrict__ cen) {
+  __shared__ double lo[3][256], hi[3][256];
+  double l[3] = {INFINITY, INFINITY, INFINITY}, h[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double c = 0.5 * (ord_val(mm[6 * b + k]) + ord_val(mm[6 * b + 3 + k]));
+      cen[3 * b + k] = c;
+      l[k] = fmin(l[k], c);
+      h[k] = fmax(h[k], c);
+    }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    lo[k][threadIdx.x] = l[k];
+    hi[k][threadIdx.x] = h[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double a = INFINITY, b = -INFINITY;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      a = fmin(a, lo[threadIdx.x][t]);
+      b = fmax(b, hi[threadIdx.x][t]);
+    }
+    cen[3 * nb + threadIdx.x] = 0.5 * (a + b);
+  }
+}
+
+__global__ void k_body_infl(int64_t N, int bs, const int* __restrict__ body, const double* __restrict__ p,
+                            const double* __restrict__ alpha_d, const double* __restrict__ cen, int nb, int cross,
+                            double* __restrict__ infl) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  const double s = alpha_d ? alpha_d[v / bs] : 1.0;
+  const double* cb = cen + 3 * (int64_t)body[v];
+  double r = 0.0, d = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double q = s * p[3 * v + k] - cb[k];
+    r += q * q;
+    const double e = cb[k] - cen[3 * nb + k];
+    d += e * e;
+  }
+  infl[v] = 4.5 * (sqrt(r) + (cross ? sqrt(d) : 0.0)) * (1.0 + 1e-12) + 1e-12;
+}
+
 __global__ void k_motion_infl(int64_t N, int bs, const double* __restrict__ p, const double* __restrict__ alpha_d,
                               const double* __restrict__ mid, double* __restrict__ infl) {
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -272,6 +348,76 @@ __global__ void k_fill(double* a, int64_t n, double v) {
   if (i < n) a[i] = v;
 }
 
+// Per-object motion summary for the exact relative-motion prefilter of the
+// tight enumeration (bp.cuh rel_safe): c_o = the (alpha_d-scaled) motion of
+// the object's first vertex, m_o = max over its vertices |s p_a - c_o|.
+// Objects: triangles [0, F), edges [F, F+E), surface points [F+E, ...).
+__global__ void k_obj_motion(int64_t F, int64_t E, int64_t V, const int* __restrict__ tri,
+                             const int* __restrict__ edge, const int* __restrict__ sverts,
+                             const double* __restrict__ p, const double* __restrict__ alpha_d, int bs,
+                             double* __restrict__ mot) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= F + E + V) return;
+  int ids[3];
+  int n;
+  if (o < F) {
+    ids[0] = tri[3 * o]; ids[1] = tri[3 * o + 1]; ids[2] = tri[3 * o + 2]; n = 3;
+  } else if (o < F + E) {
+    ids[0] = edge[2 * (o - F)]; ids[1] = edge[2 * (o - F) + 1]; n = 2;
+  } else {
+    ids[0] = sverts[o - F - E]; n = 1;
+  }
+  double c[3], m = 0.0;
+  const double s0 = alpha_d ? alpha_d[ids[0] / bs] : 1.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = s0 * p[3 * (int64_t)ids[0] + k];
+  for (int a = 1; a < n; ++a) {
+    const double sa = alpha_d ? alpha_d[ids[a] / bs] : 1.0;
+    double r = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double q = sa * p[3 * (int64_t)ids[a] + k] - c[k];
+      r += q * q;
+    }
+    m = fmax(m, sqrt(r));
+  }
+  double* out = mot + 4 * o;
+  out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = m;
+}
+
+static void obj_motion(mp_ctx* c, const double* p, const double* alpha_d) {
+  const int64_t nobj = c->F + c->E + c->V;
+  c->obj_mot.ensure(4 * (size_t)nobj);
+  k_obj_motion<<<grid_for(nobj, 256), 256, 0, c->stream>>>(c->F, c->E, c->V, c->tri, c->edge, c->sverts, p, alpha_d,
+                                                           c->bs, c->obj_mot);
+  LAUNCH_CHECK();
+}
+
+// per-vertex inflation of the two-pass tight enumeration (cross = 0: the
+// same-body pass, 1: the cross-body pass), p scaled by alpha_d if given
+static void body_infl(mp_ctx* c, const double* p, const double* alpha_d, int cross) {
+  cudaStream_t st = c->stream;
+  const int nb = (int)c->n_bodies;
+  c->infl.ensure(c->N);
+  c->body_mm.ensure(6 * (size_t)nb);
+  c->body_cen.ensure(3 * (size_t)nb + 3);
+  std::vector<unsigned long long> init(6 * (size_t)nb);
+  for (int b = 0; b < nb; ++b)
+    for (int k = 0; k < 3; ++k) {
+      init[6 * b + k] = ~0ull;
+      init[6 * b + 3 + k] = 0ull;
+    }
+  CUDA_CHECK(cudaMemcpyAsync(c->body_mm.p, init.data(), sizeof(unsigned long long) * init.size(),
+                             cudaMemcpyHostToDevice, st));
+  k_body_minmax<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, c->body, p, alpha_d, c->body_mm);
+  LAUNCH_CHECK();
+  k_body_centres<<<1, 256, 0, st>>>(nb, c->body_mm, c->body_cen);
+  LAUNCH_CHECK();
+  k_body_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, c->body, p, alpha_d, c->body_cen, nb, cross, c->infl);
+  LAUNCH_CHECK();
+  sync_stream(c);  // init is a stack array
+}
+
 struct CcdResult {
   double min_alpha;   // min over pairs (1 if none)
   bool certified;
@@ -296,7 +442,11 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
   int cert_fail_p = 0;
   if (c->F > 0) {
     const double* infl = nullptr;
-    if (!exact_set) {
+    const bool bodies = !exact_set && c->ccd_bodies && c->n_bodies > 1;
+    if (bodies) {
+      body_infl(c, p, nullptr, 0);
+      infl = c->infl;
+    } else if (!exact_set) {
       c->infl.ensure(c->N);
       k_motion_midrange<<<148, 256, 0, st>>>(c->N, c->bs, p, nullptr, c->mid_part, c->counters.p + 15, d_mid);
       LAUNCH_CHECK();
@@ -304,7 +454,9 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       LAUNCH_CHECK();
       infl = c->infl;
     }
-    BpGrid B = build_bp(c, x, pinf, 0.0, infl);
+    if (!exact_set && c->ccd_prefilter) obj_motion(c, p, nullptr);
+    BpGrid B = build_bp(c, x, pinf, 0.0, infl, bodies ? 1 : 0);
+    if (!exact_set && c->ccd_prefilter) B.T.objmot = c->obj_mot.p;
     ContactParams CP{};
     CcdParams CC{p, c->cfg.alpha_l, c->bs};
     if (exact_set && c->ccd_verts.n < 4096) {
@@ -323,6 +475,16 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       c->rb_extra = nullptr;
       if (!exact_set || n <= O.cap) {
         R.n_pairs = n;
+        if (bodies) {  // the cross-body pass: minima and the failure flag accumulate
+          int fail2 = 0;
+          body_infl(c, p, nullptr, 1);
+          BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl, 2);
+          if (c->ccd_prefilter) B2.T.objmot = c->obj_mot.p;
+          c->rb_extra = d_min;
+          R.n_pairs += run_bp<BP_CCD>(c, x, B2, O, CP, CC, &fail2);
+          c->rb_extra = nullptr;
+          cert_fail_p |= fail2;
+        }
         break;
       }
       size_t cap = (size_t)(n * 1.5) + 4096;
@@ -346,12 +508,28 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
         CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 2, c->counters.p + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
         sync_stream(c);
         R.certified = c->h_cnt[2] == 0;
+      } else if (bodies) {
+        BpOut O{};
+        O.alpha_d = c->alpha_d;
+        int fail = 0, fail2 = 0;
+        if (c->ccd_prefilter) obj_motion(c, p, c->alpha_d);
+        body_infl(c, p, c->alpha_d, 0);
+        BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl, 1);
+        if (c->ccd_prefilter) B2.T.objmot = c->obj_mot.p;
+        run_bp<BP_CERT>(c, x, B2, O, CP, CC, &fail);
+        body_infl(c, p, c->alpha_d, 1);
+        BpGrid B3 = build_bp(c, x, pinf, 0.0, c->infl, 2);
+        if (c->ccd_prefilter) B3.T.objmot = c->obj_mot.p;
+        run_bp<BP_CERT>(c, x, B3, O, CP, CC, &fail2);
+        R.certified = (fail | fail2) == 0;
       } else {
         k_motion_midrange<<<148, 256, 0, st>>>(c->N, c->bs, p, c->alpha_d, c->mid_part, c->counters.p + 15, d_mid);
         LAUNCH_CHECK();
         k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, c->alpha_d, d_mid, c->infl);
         LAUNCH_CHECK();
+        if (c->ccd_prefilter) obj_motion(c, p, c->alpha_d);
         BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl);
+        if (c->ccd_prefilter) B2.T.objmot = c->obj_mot.p;
         BpOut O{};
         O.alpha_d = c->alpha_d;
         int fail = 0;

@@ -133,7 +133,7 @@ __device__ void tri_interval(const double t[3][3], const double dist[3], int axi
   }
 }
 
-__device__ bool tri_tri_intersect(const double a[3][3], const double b[3][3]) {
+__device__ bool tri_tri_intersect(const double a[3][3], const double b[3][3], double coplanar_tol) {
   double e1[3], e2[3], n1[3], n2[3];
   for (int k = 0; k < 3; ++k) {
     e1[k] = a[1][k] - a[0][k];
@@ -151,7 +151,21 @@ __device__ bool tri_tri_intersect(const double a[3][3], const double b[3][3]) {
   if ((db[0] > 0 && db[1] > 0 && db[2] > 0) || (db[0] < 0 && db[1] < 0 && db[2] < 0)) return false;
   for (int i = 0; i < 3; ++i) da[i] = dot3(a[i], n2) - ob;
   if ((da[0] > 0 && da[1] > 0 && da[2] > 0) || (da[0] < 0 && da[1] < 0 && da[2] < 0)) return false;
-  if ((db[0] == 0.0 && db[1] == 0.0 && db[2] == 0.0) || (da[0] == 0.0 && da[1] == 0.0 && da[2] == 0.0)) {
+  // coplanar to rounding (|vertex-plane distance| <= coplanar_tol x the
+  // longest edge) takes the 2-D test: the reference's exact == 0 test sends
+  // such pairs through the interval test along an ill-defined plane-plane
+  // line and reports disjoint coplanar triangles as intersecting (DESIGN.md
+  // 4: two voxel faces 1.1 mm apart flagged by ipcsim's own function)
+  double L2 = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k) {
+      const double ea = a[(i + 1) % 3][k] - a[i][k], eb = b[(i + 1) % 3][k] - b[i][k];
+      L2 = fmax(L2, fmax(ea * ea, eb * eb));
+    }
+  const double tb = coplanar_tol * sqrt(L2 * dot3(n1, n1)), ta = coplanar_tol * sqrt(L2 * dot3(n2, n2));
+  const bool cop_b = fabs(db[0]) <= tb && fabs(db[1]) <= tb && fabs(db[2]) <= tb;
+  const bool cop_a = fabs(da[0]) <= ta && fabs(da[1]) <= ta && fabs(da[2]) <= ta;
+  if (cop_b || cop_a) {
     // coplanar: drop the dominant axis of n1 and test in 2-D
     int ax = 0;
     if (fabs(n1[1]) > fabs(n1[ax])) ax = 1;
@@ -182,7 +196,7 @@ __device__ bool tri_tri_intersect(const double a[3][3], const double b[3][3]) {
 // tested only in the first cell both boxes cover
 __global__ void k_tri_pairs(int64_t n_ent, const unsigned long long* __restrict__ key, const int* __restrict__ val,
                             const TriBox* __restrict__ box, GridSpec G, const double* __restrict__ x,
-                            const int* __restrict__ tri, unsigned long long* __restrict__ hits,
+                            const int* __restrict__ tri, double coplanar_tol, unsigned long long* __restrict__ hits,
                             int* __restrict__ first_hit) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n_ent) return;
@@ -213,7 +227,7 @@ __global__ void k_tri_pairs(int64_t n_ent, const unsigned long long* __restrict_
         A[p][d] = x[3 * (int64_t)ia[p] + d];
         B[p][d] = x[3 * (int64_t)ib[p] + d];
       }
-    if (tri_tri_intersect(A, B)) {
+    if (tri_tri_intersect(A, B, coplanar_tol)) {
       atomicAdd(hits, 1ull);
       atomicMin(first_hit, min(fa, fb));
     }
@@ -222,7 +236,8 @@ __global__ void k_tri_pairs(int64_t n_ent, const unsigned long long* __restrict_
 
 // number of intersecting non-adjacent triangle pairs of the surface at x
 // (x and tri in the caller's numbering, on the device)
-static unsigned long long tri_intersections(mp_ctx* c, const double* x, const int* tri, int64_t F, int* first) {
+static unsigned long long tri_intersections(mp_ctx* c, const double* x, const int* tri, int64_t F, int* first,
+                                            double coplanar_tol) {
   cudaStream_t st = c->stream;
   DBuf<TriBox> box;
   box.ensure(F);
@@ -273,7 +288,8 @@ static unsigned long long tri_intersections(mp_ctx* c, const double* x, const in
   fh.ensure(1);
   const int big = INT32_MAX;
   CUDA_CHECK(cudaMemcpyAsync(fh.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-  k_tri_pairs<<<grid_for(n_ent, 128), 128, 0, st>>>(n_ent, key2, val2, box, G, x, tri, c->n_pairs_dev.p, fh);
+  k_tri_pairs<<<grid_for(n_ent, 128), 128, 0, st>>>(n_ent, key2, val2, box, G, x, tri, coplanar_tol,
+                                                    c->n_pairs_dev.p, fh);
   LAUNCH_CHECK();
   unsigned long long hits = 0;
   CUDA_CHECK(cudaMemcpyAsync(&hits, c->n_pairs_dev.p, sizeof(hits), cudaMemcpyDeviceToHost, st));

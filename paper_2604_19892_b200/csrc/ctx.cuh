@@ -244,6 +244,13 @@ struct mp_ctx {
   DBuf<double> box_rlo, box_rhi; // (F+E)*3 raw primitive boxes
   DBuf<double> box_elo, box_ehi; // (F+E+V)*3 enumeration boxes
   DBuf<double> infl;             // (N) per-vertex CCD inflation
+  DBuf<int> body;                // (N) connected component (body) of each vertex
+  int64_t n_bodies = 1;
+  DBuf<unsigned long long> body_mm;  // per-body min / max of the motion (ordered keys)
+  DBuf<double> body_cen;             // per-body motion centres + their midrange
+  DBuf<double> obj_mot;              // per-object motion (c, m) for the exact CCD prefilter
+  bool ccd_prefilter = true;         // MP_OPT_CCD_PREFILTER
+  bool ccd_bodies = false;           // MP_OPT_CCD_BODIES: two-pass per-body tight enumeration
   DBuf<int> cell_cnt, cell_off;  // per-primitive covered-cell counts / offsets
   BpGridBufs grid;
   DBuf<int> cand_a, cand_b;      // raw broad-phase pairs (taps)

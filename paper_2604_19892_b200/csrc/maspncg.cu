@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstring>
 #include <numeric>
+#include <functional>
 #include <vector>
 
 #include "stages.cuh"
@@ -387,6 +388,40 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
     c->sverts.upload(sv.data(), c->V, st);
     CUDA_CHECK(cudaStreamSynchronize(st));
   }
+  {  // bodies: connected components over tets and surface triangles (union-find)
+    std::vector<int> par(N);
+    std::iota(par.begin(), par.end(), 0);
+    std::function<int(int)> root = [&](int a) {
+      while (par[a] != a) a = par[a] = par[par[a]];
+      return a;
+    };
+    auto join = [&](int a, int b) {
+      a = root(a);
+      b = root(b);
+      if (a != b) par[std::max(a, b)] = std::min(a, b);
+    };
+    for (int64_t t = 0; t < T; ++t) {
+      join(tets[t].x, tets[t].y);
+      join(tets[t].x, tets[t].z);
+      join(tets[t].x, tets[t].w);
+    }
+    for (int64_t f = 0; f < c->F; ++f) {
+      const int a = o2n[s->tris[3 * f]];
+      join(a, o2n[s->tris[3 * f + 1]]);
+      join(a, o2n[s->tris[3 * f + 2]]);
+    }
+    std::vector<int> id(N, -1), body(N);
+    int nb = 0;
+    for (int64_t v = 0; v < N; ++v) {
+      const int r = root((int)v);
+      if (id[r] < 0) id[r] = nb++;
+      body[v] = id[r];
+    }
+    // one body, or too many to matter (loose points): the single-c enumeration
+    c->n_bodies = (nb > 1 && nb <= 65536) ? nb : 1;
+    if (c->n_bodies == 1) std::fill(body.begin(), body.end(), 0);
+    c->body.upload(body.data(), N, st);
+  }
   const size_t n3 = 3 * (size_t)N;
   for (DBuf<double>* b : {&c->x, &c->xt, &c->vel, &c->g, &c->g_prev, &c->z, &c->p, &c->Hp, &c->p_prev, &c->Hp_prev, &c->z_prev,
                           &c->hv, &c->x_start, &c->x_best, &c->tmp, &c->tmp2})
@@ -498,6 +533,7 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     DotSpec S{};
     S.n = 0;
     auto add = [&](const double* a, const double* b) {
+      if (S.n >= MAX_DOTS) throw MpError(MP_ERR_CONFIG, "too many fused dots");
       S.a[S.n] = a;
       S.b[S.n] = b;
       return S.n++;
@@ -505,14 +541,26 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     int i_zz = add(c->z, c->z), i_gg = add(c->g, c->g), i_zg = add(c->z, c->g), i_zv = add(c->z, c->hv);
     int i_zHp = -1, i_pv = -1, i_pHp = -1, i_pg = -1, i_gzp = -1;
     if (have_prev) {
-      i_zHp = add(c->z, c->Hp_prev);
-      i_pv = add(c->p_prev, c->hv);
-      i_pHp = add(c->p_prev, c->Hp_prev);
+      if (subspace) {  // the 2x2 system (baselines need MAX_DOTS slots for their beta dots)
+        i_zHp = add(c->z, c->Hp_prev);
+        i_pv = add(c->p_prev, c->hv);
+        i_pHp = add(c->p_prev, c->Hp_prev);
+      }
       i_pg = add(c->p_prev, c->g);
       i_gzp = add(c->g, c->z_prev);
     }
-    int i_gpz = -1;
-    if (have_prev && !subspace) i_gpz = add(c->g_prev, c->z);
+    // baseline beta rules: the differences are formed elementwise first, as
+    // the reference does (g @ (z - z_prev), y = g - g_prev), not from
+    // differences of dots (cancellation)
+    int i_gzd = -1, i_yz = -1, i_yzd = -1, i_py = -1;
+    if (have_prev && !subspace && !restart) {
+      k_sub2<<<grid_for(n3, 256), 256, 0, st>>>(n3, c->z, c->z_prev, c->g, c->g_prev, c->tmp, c->tmp2);
+      LAUNCH_CHECK();
+      i_gzd = add(c->g, c->tmp);
+      i_yz = add(c->tmp2, c->z);
+      i_yzd = add(c->tmp2, c->tmp);
+      i_py = add(c->p_prev, c->tmp2);
+    }
     multidot(c, n3, S);
     double dots[MAX_DOTS];
     std::memcpy(dots, c->h_scal, sizeof(double) * S.n);
@@ -533,13 +581,13 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
       // baseline_direction (solver.py:171-200, 393-400): p = -z + beta p_prev
       double beta = 0.0;
       if (!restart && have_prev) {
-        const double gz = zg, gzp = dots[i_gzp], pg = dots[i_pg], gpz = dots[i_gpz];
+        const double gz = zg, pg = dots[i_pg];
         switch (cfg.direction_rule) {
           case MP_DIR_FR: beta = gz / prev_zg; break;
-          case MP_DIR_PR: beta = (gz - gzp) / prev_zg; break;
+          case MP_DIR_PR: beta = dots[i_gzd] / prev_zg; break;
           case MP_DIR_DK: {
-            const double py = pg - prev_gp;  // p_prev.(g - g_prev)
-            if (py != 0.0) beta = (gz - gpz) / py - (gz - gzp - gpz + prev_zg) * pg / (py * py);
+            const double py = dots[i_py];  // p_prev . y, y = g - g_prev
+            if (py != 0.0) beta = dots[i_yz] / py - dots[i_yzd] * pg / (py * py);
             break;
           }
           default: beta = prev_gp != 0.0 ? -gz / prev_gp : 0.0; break;  // CD
@@ -798,6 +846,8 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_KEEP_COARSE) c->keep_coarse = value != 0;
     else if (option == MP_OPT_GRAD_FUSED) c->fused_grad = value != 0;
     else if (option == MP_OPT_APPLY_OVERLAP) c->overlap_apply = value != 0;
+    else if (option == MP_OPT_CCD_PREFILTER) c->ccd_prefilter = value != 0;
+    else if (option == MP_OPT_CCD_BODIES) c->ccd_bodies = value != 0;
     else if (option == MP_OPT_APPEND_LIMIT) {
       const int lim = (int)std::max<int64_t>(64, std::min<int64_t>(HQ_APPEND_LIMIT, value <= 0 ? HQ_APPEND_LIMIT : value));
       CUDA_CHECK(cudaMemcpyToSymbol(g_append_limit, &lim, sizeof(int)));
@@ -971,7 +1021,7 @@ int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t*
 }
 
 int mp_check_intersections(int device, int64_t n_verts, const double* x, int64_t n_tris, const int64_t* tris,
-                           int64_t* n_hits, int64_t* first_tri) {
+                           double coplanar_tol, int64_t* n_hits, int64_t* first_tri) {
   static thread_local mp_ctx* tmp = nullptr;  // scratch context: a stream and the sort helpers
   if (n_verts < 1 || n_tris < 0 || n_tris >= (1ll << 31)) return MP_ERR_CONFIG;
   if (!tmp) tmp = new mp_ctx();
@@ -993,7 +1043,7 @@ int mp_check_intersections(int device, int64_t n_verts, const double* x, int64_t
     xd.upload(x, 3 * n_verts, c->stream);
     td.upload(t32.data(), t32.size(), c->stream);
     int first = INT32_MAX;
-    *n_hits = (int64_t)tri_intersections(c, xd, td, n_tris, &first);
+    *n_hits = (int64_t)tri_intersections(c, xd, td, n_tris, &first, coplanar_tol);
     *first_tri = first == INT32_MAX ? -1 : first;
   });
 }

@@ -93,6 +93,16 @@ static void form_direction(mp_ctx* c, double a, double b, const double* pp, cons
   c->h_scal[1] = c->h_scal[MAX_DOTS];  // max|p| (the bits of a non-negative double)
 }
 
+// a - b and c - d, elementwise
+__global__ void k_sub2(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                       const double* __restrict__ c, const double* __restrict__ d, double* __restrict__ ab,
+                       double* __restrict__ cd) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ab[i] = a[i] - b[i];
+  cd[i] = c[i] - d[i];
+}
+
 __global__ void k_velocity(int64_t N, const double* __restrict__ x, const double* __restrict__ x0, double h,
                            const unsigned char* __restrict__ pinned, double* __restrict__ v) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

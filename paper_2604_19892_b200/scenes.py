@@ -151,9 +151,12 @@ def c3_rod(cells=(2500, 8, 8), length=6.25, width=0.02, young=1e5, gap=2e-3, mod
     return build_scene(objs, d_hat=2e-3, kappa=1e4, mods=mods)
 
 
-def c3_rod_v0(scene, omega=20.0):
+def c3_rod_v0(scene, omega=5.0):
     """Twist field: angular velocity about the rod axis varying linearly from
-    -omega at one end to +omega at the other; the pinned floor stays at rest."""
+    -omega at one end to +omega at the other; the pinned floor stays at rest.
+    omega = 5 rad/s moves the rod's surface 0.5 mm per 10 ms step (a fifth
+    of an element); round 1 used 20 rad/s (2 mm, 80% of an element per step,
+    which turned every iteration into a 10^9-candidate CCD)."""
     x = scene.mesh.rest_positions
     rod = ~np.asarray(scene.dirichlet, dtype=bool)
     xr = x[rod]
@@ -252,21 +255,21 @@ def puffer_mesh(core_cells=19, spike_cells=64, n_spikes=410, base_cells=0.84, ti
     return geo.voxel_tet_mesh(mask, cell, origin=(-0.5 * n * cell,) * 3)
 
 
-def c5_puffer_balls(young=1e5, speed=1.0, mods=None, **puffer):
+def c5_puffer_balls(young=1e5, gap=1e-3, mods=None, **puffer):
     """Config 5: eight puffer balls at the corners of a cube, flying at each
     other (``c5_puffer_v0``); SNH E = 1e5, h = 0.005, d_hat = 1e-4 (the
     paper's collision scene).  No floor, no gravity: the
     balls only meet each other."""
     ball = puffer_mesh(mods=mods, **puffer)
     ext = float(np.ptp(ball.rest_positions, axis=0).max())
-    s = 0.5 * ext * 1.02  # corners: bounding spheres just apart
+    s = 0.5 * ext + 0.5 * gap  # corners: bounding boxes gap apart
     objs = [{"mesh": ball, "material": "snh", "young": young, "poisson": 0.3, "density": 1000.0,
              "translate": (sx * s, sy * s, sz * s)}
             for sz in (-1, 1) for sy in (-1, 1) for sx in (-1, 1)]
     return build_scene(objs, d_hat=1e-4, kappa=1e4, gravity=(0.0, 0.0, 0.0), mods=mods)
 
 
-def c5_puffer_v0(scene, speed=1.0):
+def c5_puffer_v0(scene, speed=0.1):
     """Each ball moves toward the scene centre at ``speed`` m/s."""
     x = scene.mesh.rest_positions
     n = len(x) // 8

@@ -133,10 +133,11 @@ def test_checker_min_distance_matches_brute_force():
     assert d == min(dpt.min(), dee.min())
     # this jitter pushes some cube vertices below the floor: triangles cross
     # while every PT / EE distance stays positive -- the tri-tri half's job
-    assert chk.intersections(x)[0] == ogeo.count_tri_intersections(x, tris) > 0
+    assert chk.intersections(x)[0] == ogeo.count_tri_intersections(x, tris, 1e-9) > 0
+    assert _native_check(x, tris, 0.0) == ogeo.count_tri_intersections(x, tris, 0.0)  # the reference's exact rule
     x2 = s.mesh.rest_positions.copy()
     x2[~s.dirichlet, 2] -= 0.005
-    assert chk.intersections(x2)[0] == ogeo.count_tri_intersections(x2, tris) == 0
+    assert chk.intersections(x2)[0] == ogeo.count_tri_intersections(x2, tris, 1e-9) == 0
 
 
 @pytest.mark.gpu
@@ -150,6 +151,31 @@ def test_checker_finds_planted_intersection():
     assert n == 1 and first == 0
     x[3:6, 2] += 2.0  # lift it clear
     assert geometry_check(x, t)[0] == 0
+
+
+def _native_check(x, t, tol):
+    from paper_2604_19892_b200 import _native
+
+    return _native.check_intersections(x, t, coplanar_tol=tol)[0]
+
+
+@pytest.mark.gpu
+def test_checker_coplanar_rounding_is_not_an_intersection():
+    """Two disjoint faces, coplanar to the last bits (a translated voxel
+    surface): the reference's exact rule calls them intersecting, the
+    checker's tolerance does not (the C5 case in DESIGN.md 4)."""
+    from oracle import geometry as ogeo
+
+    # the two triangles of the C5 run (gpurun_out c5_fail.npz), full precision
+    x = np.array([[-0.1110214316702486, -0.051582198351108624, -0.18589964146451887],
+                  [-0.10945893167024857, -0.051582198351108485, -0.1843371414645189],
+                  [-0.11102143167024857, -0.05158219835110849, -0.18433714146451888],
+                  [-0.1094589316702486, -0.05158219835110862, -0.1858996414645189],
+                  [-0.10789643167024861, -0.0515821983511086, -0.18589964146451893],
+                  [-0.10789643167024858, -0.05158219835110848, -0.18433714146451893]])
+    t = np.array([[0, 1, 2], [3, 4, 5]])
+    assert ogeo.count_tri_intersections(x, t, 0.0) == 1  # the reference's rule: a false positive
+    assert ogeo.count_tri_intersections(x, t, 1e-9) == 0 == _native_check(x, t, 1e-9)
 
 
 def geometry_check(x, t):

@@ -30,7 +30,7 @@ elif which == "c4":
     h, cfg = 0.01, solver.SolverConfig(iter_max=iter_max, coarse_block=32)
 else:
     scene = scenes.c5_puffer_balls()
-    v0 = scenes.c5_puffer_v0(scene, speed=2.0)
+    v0 = scenes.c5_puffer_v0(scene)
     h, cfg = 0.005, solver.SolverConfig(iter_max=iter_max, coarse_block=32)
 build_s = time.time() - t0
 print(json.dumps({"scene": which, "n_verts": int(scene.mesh.n_vertices), "n_tets": int(len(scene.elastic.vol)),
@@ -62,7 +62,14 @@ for f in range(frames):
                 "min_alpha": min([1.0] + [r.min_alpha for r in recs]), "contacts_last": int(recs[-1].n_contacts),
                 "check": {"min_distance": dmin, "intersections": hits, "s": round(time.time() - t1, 2)}})
     print(json.dumps(out[-1]), flush=True)
+# stage breakdown: one more frame from the last state with the CUDA-event stage timers on
+ctx.stage_timing(True)
+recs, conv, _ = ctx.step_device(h)
+st = ctx.stage_stats()
+ctx.stage_timing(False)
+stages = {k: {"ms": round(v[0], 2), "count": v[1]} for k, v in st.items()}
+print(json.dumps({"stage_frame_iters": len(recs), "stages": stages}), flush=True)
 print(json.dumps({"scene": which, "n_verts": int(scene.mesh.n_vertices), "n_tets": int(len(scene.elastic.vol)),
-                  "surface_tris": int(len(scene.surface.triangles)), "devices": devices or [0],
+                  "surface_tris": int(len(scene.surface.triangles)), "devices": devices or [0], "stages": stages,
                   "build_s": round(build_s, 1), "cfg": {"iter_max": iter_max, "coarse_block": cfg.coarse_block, "h": h},
                   "frames": out}))
