@@ -401,8 +401,97 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline()
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "unavailable": repr(e)[:200]}
+    if args.configs and ws == 1:
+        line["other_configs"] = {}
+        for name in [c for c in args.configs.split(",") if c]:
+            try:
+                line["other_configs"][name] = measure_config(name, flush, local)
+            except Exception as e:  # reported, never silently replaced
+                line["other_configs"][name] = {"unavailable": repr(e)[:300]}
     print(json.dumps(line), flush=True)
     grp.close()
+
+
+# BASELINE.json configs 3-5 on one B200: bounded device-resident samples
+# (not the headline; SURVEY 8.0 sizes).  Each: the scene built on the host,
+# one untimed frame (buffers grow), then timed frames with CUDA events on
+# the solver stream, L2 flushed before each; PNCG iterations/s and the
+# frames' capped sec/frame; then the GPU penetration checker on the final
+# positions (cli.SurfaceChecker: min PT/EE distance + tri-tri count).
+OTHER = {
+    "c3": {"desc": "c3_rod: SNH rod 8x8x2500 cells (202,589 V / 960,006 T with the floor), twist 5 rad/s at the ends, "
+                   "h=0.01, SolverConfig defaults (levels 2, coarse_block 4)", "frames": 2, "iter_max": 60, "h": 0.01},
+    "c4": {"desc": "c4_spheres_in_bowl: 64 SNH voxel balls (8,625 V each) over a pinned ARAP bowl (562,859 V / "
+                   "2,804,112 T), h=0.01, coarse_block 32", "frames": 2, "iter_max": 60, "h": 0.01, "cb": 32},
+    "c5": {"desc": "c5_puffer_balls: 8 SNH puffer balls (core + 410 spikes; 1,142,784 V / 2,743,680 T) closing at "
+                   "0.1 m/s each, d_hat=1e-4, h=0.005, coarse_block 32", "frames": 2, "iter_max": 30, "h": 0.005,
+           "cb": 32},
+}
+
+
+def measure_config(name, flush, local):
+    import torch
+
+    from paper_2604_19892_b200 import cli, scenes, solver
+
+    spec = OTHER[name]
+    t0 = time.perf_counter()
+    if name == "c3":
+        scene = scenes.c3_rod()
+        v0 = scenes.c3_rod_v0(scene)
+    elif name == "c4":
+        scene = scenes.c4_spheres_in_bowl()
+        v0 = np.zeros(3 * scene.mesh.n_vertices)
+    else:
+        scene = scenes.c5_puffer_balls()
+        v0 = scenes.c5_puffer_v0(scene)
+    build_s = time.perf_counter() - t0
+    cfg = solver.SolverConfig(iter_max=spec["iter_max"], coarse_block=spec.get("cb", 4))
+    ctx = scene.context(cfg, device=local)
+    x0 = scene.mesh.rest_positions.ravel().copy()
+    ctx.set_state(x0, v0)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    ctx.step_device(spec["h"])  # untimed: buffers grow
+    ctx.set_state(x0, v0)
+    frames, tot_ms, tot_it = [], 0.0, 0
+    for _ in range(spec["frames"]):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        recs, conv, _ = ctx.step_device(spec["h"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        tot_ms += ms
+        tot_it += len(recs)
+        frames.append({"iters": len(recs), "ms": round(ms, 1), "restarts": int(sum(r.restart for r in recs)),
+                       "converged": bool(conv), "min_alpha": min([1.0] + [r.min_alpha for r in recs]),
+                       "contacts_last": int(recs[-1].n_contacts) if recs else 0})
+    x, _ = ctx.get_state()
+    # rooflines at this scale: one more frame with the stage timers on
+    ctx.stage_timing(True)
+    ctx.step_device(spec["h"])
+    st = ctx.stage_stats()
+    ctx.stage_timing(False)
+    peaks, _ = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    roof = {}
+    for key, label in (("mas_apply_l0", "k_mas_apply_l0_direct"), ("mas_apply", "MAS apply stage"),
+                       ("tet_grad", "k_tet_grad<SNH>"), ("gradient", "gradient stage"), ("hvp", "HVP stage")):
+        ms, cnt, b = st[key]
+        if cnt and ms > 0:
+            ach = (b / cnt) / (ms / cnt * 1e-3) / 1e9
+            roof[key] = {"kernel": label, "achieved_gbs": round(ach, 1), "frac": round(ach / hbm, 4),
+                         "us_per_launch": round(1e3 * ms / cnt, 2), "bytes_per_launch": round(b / cnt)}
+    stage_ms = {k: round(v[0], 2) for k, v in st.items()}
+    chk = cli.SurfaceChecker(scene.mesh.rest_positions, scene.surface.triangles, local)
+    check = {"min_distance": chk.min_distance(x), "tri_tri_intersections": chk.intersections(x)[0]}
+    return {"workload": spec["desc"], "n_verts": int(scene.mesh.n_vertices), "n_tets": int(len(scene.elastic.vol)),
+            "iter_max": spec["iter_max"], "value": tot_it / (tot_ms * 1e-3), "unit": "iters/s",
+            "sec_per_frame_capped": tot_ms * 1e-3 / spec["frames"], "frames": frames, "build_s": round(build_s, 1),
+            "penetration_check": check, "roofline": roof, "stages_ms_one_frame": stage_ms,
+            "note": "frames capped at iter_max (bounded sample), from rest"}
 
 
 def main():
@@ -413,6 +502,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--iter-max", type=int, default=0, help=f"PNCG iterations cap per frame (default {ITER_MAX})")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--configs", default="c3,c4,c5",
+                    help="extra BASELINE configs measured after the headline at N=1 (comma list; '' for none)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

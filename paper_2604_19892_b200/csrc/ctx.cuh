@@ -160,7 +160,7 @@ struct mp_ctx {
   int apply_mode = 2;        // level-0 apply: 2 direct loads, 1 TMA-staged, 0 cp.async-staged
   int apply_stages = 2;      // level-0 apply pipeline depth (2 or 3)
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
-  bool fused_grad = true;
+  bool fused_grad = false;  // gradient: one fused per-vertex pass (k_grad_fused; measured slower at C2, 98 vs 74 us) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
   bool overlap_apply = true;  // MAS apply: level 0 on the side stream beside the coarse chain (MP_OPT_APPLY_OVERLAP)
   cudaStream_t side = nullptr;  // side stream (level-0 apply) and its events
   cudaEvent_t ev_g = nullptr, ev_l0 = nullptr;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)

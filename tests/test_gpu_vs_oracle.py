@@ -114,14 +114,14 @@ def test_penetration_raises_reference_code():
     _ = solver
 
 
-def test_unsupported_rules_are_config_errors():
+def test_invalid_configs_are_config_errors():
     from paper_2604_19892_b200 import solver
     from paper_2604_19892_b200.errors import ConfigError
 
     g = load_golden("drop")
     scene = scene_from_golden(g)
     x, v = g["rest"].ravel(), np.zeros(g["rest"].size)
-    for bad in ({"preconditioner": "Jacobi"}, {"direction_rule": "FR"}, {"delta": 1.5}, {"iter_max": 0}):
+    for bad in ({"preconditioner": "ILU"}, {"direction_rule": "BFGS"}, {"delta": 1.5}, {"iter_max": 0}):
         cfg = solver.SolverConfig(**bad)
         with pytest.raises(ConfigError) as e:
             solver.step(scene, x, v, 0.01, cfg)
