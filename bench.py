@@ -420,11 +420,11 @@ def run_ours(args):
 # positions (cli.SurfaceChecker: min PT/EE distance + tri-tri count).
 OTHER = {
     "c3": {"desc": "c3_rod: SNH rod 8x8x2500 cells (202,589 V / 960,006 T with the floor), twist 5 rad/s at the ends, "
-                   "h=0.01, SolverConfig defaults (levels 2, coarse_block 4)", "frames": 2, "iter_max": 60, "h": 0.01},
+                   "h=0.01, SolverConfig defaults (levels 2, coarse_block 4)", "frames": 1, "iter_max": 40, "h": 0.01},
     "c4": {"desc": "c4_spheres_in_bowl: 64 SNH voxel balls (8,625 V each) over a pinned ARAP bowl (562,859 V / "
-                   "2,804,112 T), h=0.01, coarse_block 32", "frames": 2, "iter_max": 60, "h": 0.01, "cb": 32},
+                   "2,804,112 T), h=0.01, coarse_block 32", "frames": 1, "iter_max": 40, "h": 0.01, "cb": 32},
     "c5": {"desc": "c5_puffer_balls: 8 SNH puffer balls (core + 410 spikes; 1,142,784 V / 2,743,680 T) closing at "
-                   "0.1 m/s each, d_hat=1e-4, h=0.005, coarse_block 32", "frames": 2, "iter_max": 30, "h": 0.005,
+                   "0.1 m/s each, d_hat=1e-4, h=0.005, coarse_block 32", "frames": 1, "iter_max": 20, "h": 0.005,
            "cb": 32},
 }
 

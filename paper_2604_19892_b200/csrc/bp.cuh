@@ -746,11 +746,24 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_query_span(T.G, l, pl, ph, c0, c1);
-    for (int a = c0[0]; a <= c1[0]; ++a)
-      for (int b = c0[1]; b <= c1[1]; ++b)
-        for (int c = c0[2]; c <= c1[2]; ++c) {
-          const int cell = hg_cell(T.G, l, a, b, c);
-          const int e0 = T.tri_start[cell], e1 = T.tri_start[cell + 1];
+    // the span's cells in (a, b, c) order; every 32 cells each lane loads
+    // one cell's entry range (one memory round trip per 32 cells instead of
+    // one per cell) and the warp walks them in order
+    const int nb_ = c1[1] - c0[1] + 1, nc_ = c1[2] - c0[2] + 1;
+    const int ncell_ = (c1[0] - c0[0] + 1) * nb_ * nc_;
+    int my0 = 0, my1 = 0;
+    for (int ci_ = 0; ci_ < ncell_; ++ci_) {
+          if ((ci_ & 31) == 0) {
+            my0 = my1 = 0;
+            const int idx = ci_ + lane;
+            if (idx < ncell_) {
+              const int r = idx % (nb_ * nc_);
+              const int cell = hg_cell(T.G, l, c0[0] + idx / (nb_ * nc_), c0[1] + r / nc_, c0[2] + r % nc_);
+              my0 = T.tri_start[cell];
+              my1 = T.tri_start[cell + 1];
+            }
+          }
+          const int e0 = __shfl_sync(WARP_FULL, my0, ci_ & 31), e1 = __shfl_sync(WARP_FULL, my1, ci_ & 31);
           for (int base = e0; base < e1; base += 32) {
             const int e = base + lane;
             bool pass = false;
@@ -792,11 +805,24 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_query_span(T.G, l, tl, th, c0, c1);
-    for (int a = c0[0]; a <= c1[0]; ++a)
-      for (int b = c0[1]; b <= c1[1]; ++b)
-        for (int c = c0[2]; c <= c1[2]; ++c) {
-          const int cell = hg_cell(T.G, l, a, b, c);
-          const int e0 = T.pt_start[cell], e1 = T.pt_start[cell + 1];
+    // the span's cells in (a, b, c) order; every 32 cells each lane loads
+    // one cell's entry range (one memory round trip per 32 cells instead of
+    // one per cell) and the warp walks them in order
+    const int nb_ = c1[1] - c0[1] + 1, nc_ = c1[2] - c0[2] + 1;
+    const int ncell_ = (c1[0] - c0[0] + 1) * nb_ * nc_;
+    int my0 = 0, my1 = 0;
+    for (int ci_ = 0; ci_ < ncell_; ++ci_) {
+          if ((ci_ & 31) == 0) {
+            my0 = my1 = 0;
+            const int idx = ci_ + lane;
+            if (idx < ncell_) {
+              const int r = idx % (nb_ * nc_);
+              const int cell = hg_cell(T.G, l, c0[0] + idx / (nb_ * nc_), c0[1] + r / nc_, c0[2] + r % nc_);
+              my0 = T.pt_start[cell];
+              my1 = T.pt_start[cell + 1];
+            }
+          }
+          const int e0 = __shfl_sync(WARP_FULL, my0, ci_ & 31), e1 = __shfl_sync(WARP_FULL, my1, ci_ & 31);
           for (int base = e0; base < e1; base += 32) {
             const int e = base + lane;
             bool pass = false;
@@ -842,11 +868,24 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_query_span(T.G, l, il, ih, c0, c1);
-    for (int a = c0[0]; a <= c1[0]; ++a)
-      for (int b = c0[1]; b <= c1[1]; ++b)
-        for (int c = c0[2]; c <= c1[2]; ++c) {
-          const int cell = hg_cell(T.G, l, a, b, c);
-          const int e0 = T.edge_start[cell], e1 = T.edge_start[cell + 1];
+    // the span's cells in (a, b, c) order; every 32 cells each lane loads
+    // one cell's entry range (one memory round trip per 32 cells instead of
+    // one per cell) and the warp walks them in order
+    const int nb_ = c1[1] - c0[1] + 1, nc_ = c1[2] - c0[2] + 1;
+    const int ncell_ = (c1[0] - c0[0] + 1) * nb_ * nc_;
+    int my0 = 0, my1 = 0;
+    for (int ci_ = 0; ci_ < ncell_; ++ci_) {
+          if ((ci_ & 31) == 0) {
+            my0 = my1 = 0;
+            const int idx = ci_ + lane;
+            if (idx < ncell_) {
+              const int r = idx % (nb_ * nc_);
+              const int cell = hg_cell(T.G, l, c0[0] + idx / (nb_ * nc_), c0[1] + r / nc_, c0[2] + r % nc_);
+              my0 = T.edge_start[cell];
+              my1 = T.edge_start[cell + 1];
+            }
+          }
+          const int e0 = __shfl_sync(WARP_FULL, my0, ci_ & 31), e1 = __shfl_sync(WARP_FULL, my1, ci_ & 31);
           for (int base = e0; base < e1; base += 32) {
             const int e = base + lane;
             bool pass = false;

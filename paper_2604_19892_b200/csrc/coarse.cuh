@@ -35,7 +35,8 @@ struct CoarseSweepArgs {
   int n;                     // matrix order
   int nT;                    // tiles per side (n padded to 32 nT)
   int n_units;               // work units per phase
-  const int2* units;         // (row tile I, chunk c) per unit
+  const int2* units;         // (row tile I, first column tile J0) per unit
+  int ch;                    // column tiles per unit (<= CS_CH; chosen so the units fill the SMs)
   const double* dense;       // n x n assembled M (row-major, both halves valid)
   double* tiles;             // lower tiles, tile-major
   double* colbuf;            // 2 x nT x 1024: panel column A_{I,K} (row-major (i, k))
@@ -135,9 +136,9 @@ __device__ __forceinline__ void cs_compute_W(const double* Csm, const double* Pm
 // A unit's panel tiles into registers: pre[0] = A_IK, pre[1 + q] = A_{J0+q, K};
 // element w = tid + 256 s of each tile.  Unrolled, predicated: every load is
 // in flight at once.
-__device__ __forceinline__ void cs_load_unit(const double* __restrict__ cur, int2 uc, int K,
+__device__ __forceinline__ void cs_load_unit(const double* __restrict__ cur, int2 uc, int K, int ch,
                                              double (&pre)[1 + CS_CH][4]) {
-  const int I = uc.x, J0 = CS_CH * uc.y, nq = min(CS_CH, I + 1 - J0);
+  const int I = uc.x, J0 = uc.y, nq = min(ch, I + 1 - J0);
   const bool live = I != K;
 #pragma unroll
   for (int s4 = 0; s4 < 4; ++s4) {
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
     double pre[1 + CS_CH][4];
     const unsigned long long t0 = A.prof ? cs_now() : 0ull;
     int u = self;
-    if (self >= 0 && u < A.n_units) cs_load_unit(cur, A.units[u], K, pre);
+    if (self >= 0 && u < A.n_units) cs_load_unit(cur, A.units[u], K, A.ch, pre);
     // (1) Pm = -A_KK^-1: swept by every CTA at K = 0, then published one phase ahead
     if (K == 0) {
       const bool ok0 = cs_pivot_sweep(cur, Pm, Wsm);
@@ -243,14 +244,15 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_coarse_sweep(CoarseSweepArgs 
     }
     for (; self >= 0 && u < A.n_units; u += G1) {
       const int2 uc = A.units[u];
-      const int I = uc.x, c = uc.y;
-      const int J0 = CS_CH * c, J1 = min(CS_CH * c + CS_CH, I + 1);
+      const int I = uc.x, J0 = uc.y;
+      const int c = J0;  // 0 for the row's first unit
+      const int J1 = min(J0 + A.ch, I + 1);
       if (I == K) {  // the pivot row: only A_KK <- -P^-1
         if (c == 0)
           for (int w = tid; w < 1024; w += CS_THREADS) A.tiles[cs_tile(K, K) + w] = Pm[(w >> 5) * CS_LD + (w & 31)];
         continue;
       }
-      if (u != self) cs_load_unit(cur, uc, K, pre);
+      if (u != self) cs_load_unit(cur, uc, K, A.ch, pre);
       // (2) own column tile A_IK (row-major) and the chunk's A_JK (transposed, k-major)
 #pragma unroll
       for (int s4 = 0; s4 < 4; ++s4) {

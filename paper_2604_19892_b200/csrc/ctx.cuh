@@ -112,6 +112,7 @@ struct CoarseLevel {
   // the coarse inverse (coarse.cuh): work units, lower tiles, panel columns, grid barrier
   DBuf<int2> cs_units;
   int n_units = 0;
+  int cs_ch = 8;  // column tiles per unit
   DBuf<double> cs_tiles, cs_col, cs_pm, cs_diag;
   DBuf<unsigned> cs_bar;
   int chunks = 1;

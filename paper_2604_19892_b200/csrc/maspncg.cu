@@ -171,11 +171,23 @@ static void setup_levels(mp_ctx* c) {
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_w, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_u, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&L->ev_asm, cudaEventDisableTiming));
-    {  // coarse-inverse work units: (row tile I, chunk of <= CS_CH column tiles J <= I)
+    {  // coarse-inverse work units: (row tile I, first column tile J0), ch tiles J0.. <= I each;
+       // ch: the narrowest that still fits one unit per SM (+ the lookahead CTA)
       const int nT = (L->n + CS_TB - 1) / CS_TB;
+      int sms = 148;
+      CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      L->cs_ch = CS_CH;
+      for (int ch = 1; ch <= CS_CH; ++ch) {
+        int64_t nu = 0;
+        for (int I = 0; I < nT; ++I) nu += (I + ch) / ch;
+        if (nu + 1 <= sms) {
+          L->cs_ch = ch;
+          break;
+        }
+      }
       std::vector<int2> units;
       for (int I = 0; I < nT; ++I)
-        for (int cch = 0; CS_CH * cch <= I; ++cch) units.push_back(make_int2(I, cch));
+        for (int j0 = 0; j0 <= I; j0 += L->cs_ch) units.push_back(make_int2(I, j0));
       L->n_units = (int)units.size();
       L->cs_units.upload(units.data(), units.size(), c->stream);
       CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -1001,8 +1013,17 @@ int mp_spd_inverse(int device, int64_t n, const double* A, double* inv, int32_t*
     L.st = c->stream;
     const int nT = (L.n + CS_TB - 1) / CS_TB;
     std::vector<int2> units;
+    L.cs_ch = CS_CH;
+    for (int ch = 1; ch <= CS_CH; ++ch) {
+      int64_t nu = 0;
+      for (int I = 0; I < nT; ++I) nu += (I + ch) / ch;
+      if (nu + 1 <= 148) {
+        L.cs_ch = ch;
+        break;
+      }
+    }
     for (int I = 0; I < nT; ++I)
-      for (int cch = 0; CS_CH * cch <= I; ++cch) units.push_back(make_int2(I, cch));
+      for (int j0 = 0; j0 <= I; j0 += L.cs_ch) units.push_back(make_int2(I, j0));
     L.n_units = (int)units.size();
     L.cs_units.upload(units.data(), units.size(), c->stream);
     L.dense.upload(A, (size_t)n * n, c->stream);

@@ -119,7 +119,7 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   }
   const int grid = std::max(1, std::min(L.n_units + 1, max_ctas));  // + the lookahead CTA
   static const int prof = getenv("MP_CS_PROF") ? 1 : 0;
-  CoarseSweepArgs A{n, nT, L.n_units, L.cs_units.p, L.dense.p, L.cs_tiles.p, L.cs_col.p, L.inv.p, status,
+  CoarseSweepArgs A{n, nT, L.n_units, L.cs_units.p, L.cs_ch, L.dense.p, L.cs_tiles.p, L.cs_col.p, L.inv.p, status,
                     L.cs_bar.p, L.cs_pm.p, L.cs_diag.p, prof};
   void* args[] = {&A};
   CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_coarse_sweep, dim3(grid), dim3(CS_THREADS), args,
