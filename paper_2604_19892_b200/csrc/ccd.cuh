@@ -393,6 +393,215 @@ static void obj_motion(mp_ctx* c, const double* p, const double* alpha_d) {
   LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// Local-centre tight enumeration.  One global c makes every vertex's box
+// grow with |p_v - C|: bodies moving apart or together, or a large step on
+// one part of the scene, inflate everything.  Per subdomain d (32 vertices,
+// spatially compact) take c_d = the midrange of its (scaled) motion and
+//   delta_d = max |c_d - c_d'| over subdomains d' whose boxes lie within
+//             rho of d's box, rho = 2 max_v 4.5 |p_v - C| + 2 max edge,
+// and inflate vertex v by 4.5 (|p_v - c_d(v)| + delta_d(v)).  Exactness: a
+// pair the global criterion cannot rule out has all its vertices' subdomain
+// boxes within rho of each other; choosing c = c_d(w*) for the pair vertex
+// w* with the largest |p_w - c_d(w)| bounds the pair's max |p - c| by that
+// vertex's inflation / 4.5, so a pair whose boxes grown this way do not
+// overlap has 0.9 gap > 4.05 max|p - c| >= speed (the same argument as the
+// global scheme, ccd.py:172-179).  Pairs beyond rho are safe globally.
+
+__global__ void k_sub_motion(int64_t N, int64_t D, int bs, const double* __restrict__ x, const double* __restrict__ p,
+                             const double* __restrict__ alpha_d, double* __restrict__ cen, double* __restrict__ box) {
+  const int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (d >= D) return;  // warp-uniform
+  const int64_t v = d * bs + lane;
+  const bool live = lane < bs && v < N;
+  const double s = alpha_d ? alpha_d[d] : 1.0;
+  double pl[3], ph[3], xl[3], xh[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double q = live ? s * p[3 * v + k] : 0.0, xx = live ? x[3 * v + k] : 0.0;
+    pl[k] = live ? q : INFINITY;
+    ph[k] = live ? q : -INFINITY;
+    xl[k] = live ? xx : INFINITY;
+    xh[k] = live ? xx : -INFINITY;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    pl[k] = -warp_max(-pl[k]);
+    ph[k] = warp_max(ph[k]);
+    xl[k] = -warp_max(-xl[k]);
+    xh[k] = warp_max(xh[k]);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      cen[3 * d + k] = 0.5 * (pl[k] + ph[k]);
+      box[6 * d + k] = xl[k];
+      box[6 * d + 3 + k] = xh[k];
+    }
+}
+
+// max surface edge length and max global inflation (order-free maxima)
+__global__ void k_reach_parts(int64_t E, const int* __restrict__ edge, const double* __restrict__ x, int64_t N,
+                              const double* __restrict__ infl, double* __restrict__ out) {
+  double me = 0.0, mi = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E || i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < E) {
+      const int a = edge[2 * i], b = edge[2 * i + 1];
+      double r = 0.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double t = x[3 * a + k] - x[3 * b + k];
+        r += t * t;
+      }
+      me = fmax(me, sqrt(r));
+    }
+    if (i < N) mi = fmax(mi, infl[i]);
+  }
+  me = warp_max(me);
+  mi = warp_max(mi);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(out, me);
+    atomic_max_nonneg(out + 1, mi);
+  }
+}
+
+__global__ void k_sub_keys(int64_t D, const double* __restrict__ box, const double* __restrict__ org, double inv_h,
+                           int n1, int n2, unsigned long long* __restrict__ key, int* __restrict__ id) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  int c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = (int)floor((0.5 * (box[6 * d + k] + box[6 * d + 3 + k]) - org[k]) * inv_h);
+  key[d] = ((unsigned long long)c[0] * n1 + c[1]) * n2 + c[2];
+  id[d] = (int)d;
+}
+
+__device__ __forceinline__ int64_t lower_key(const unsigned long long* __restrict__ key, int64_t n,
+                                             unsigned long long k) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key[mid] < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// delta_d over the 27 neighbour cells (cell = rho + the largest box extent)
+__global__ void k_sub_delta(int64_t D, const double* __restrict__ box, const double* __restrict__ cen,
+                            const double* __restrict__ org, double inv_h, int n0, int n1, int n2, double rho,
+                            const unsigned long long* __restrict__ key, const int* __restrict__ id,
+                            double* __restrict__ delta) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  int c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = (int)floor((0.5 * (box[6 * d + k] + box[6 * d + 3 + k]) - org[k]) * inv_h);
+  const double* bd = box + 6 * d;
+  double dl = 0.0;
+  for (int a = max(0, c[0] - 1); a <= min(n0 - 1, c[0] + 1); ++a)
+    for (int b = max(0, c[1] - 1); b <= min(n1 - 1, c[1] + 1); ++b)
+      for (int e = max(0, c[2] - 1); e <= min(n2 - 1, c[2] + 1); ++e) {
+        const unsigned long long k = ((unsigned long long)a * n1 + b) * n2 + e;
+        for (int64_t q = lower_key(key, D, k); q < D && key[q] == k; ++q) {
+          const int64_t o = id[q];
+          const double* bo = box + 6 * o;
+          double g2 = 0.0;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const double gap = fmax(0.0, fmax(bd[t] - bo[3 + t], bo[t] - bd[3 + t]));
+            g2 += gap * gap;
+          }
+          if (g2 > rho * rho) continue;
+          const double dx = cen[3 * d] - cen[3 * o], dy = cen[3 * d + 1] - cen[3 * o + 1],
+                       dz = cen[3 * d + 2] - cen[3 * o + 2];
+          dl = fmax(dl, sqrt(dx * dx + dy * dy + dz * dz));
+        }
+      }
+  delta[d] = dl;
+}
+
+__global__ void k_local_infl(int64_t N, int bs, const double* __restrict__ p, const double* __restrict__ alpha_d,
+                             const double* __restrict__ cen, const double* __restrict__ delta,
+                             double* __restrict__ infl) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  const int64_t d = v / bs;
+  const double s = alpha_d ? alpha_d[d] : 1.0;
+  double r = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double q = s * p[3 * v + k] - cen[3 * d + k];
+    r += q * q;
+  }
+  infl[v] = 4.5 * (sqrt(r) + delta[d]) * (1.0 + 1e-12) + 1e-12;
+}
+
+// c->infl holds the global-centre inflation on entry; replaced by the local
+// one when that is smaller everywhere it matters (its maximum is smaller)
+static void local_infl(mp_ctx* c, const double* x, const double* p, const double* alpha_d) {
+  cudaStream_t st = c->stream;
+  const int64_t D = c->D, N = c->N;
+  c->sub_cen.ensure(3 * (size_t)D);
+  c->sub_box.ensure(6 * (size_t)D);
+  c->sub_delta.ensure(D);
+  c->infl2.ensure(N);
+  k_sub_motion<<<grid_for(32 * D, 256), 256, 0, st>>>(N, D, c->bs, x, p, alpha_d, c->sub_cen, c->sub_box);
+  LAUNCH_CHECK();
+  double* parts = c->dscal.p + 48;  // [48] max edge, [49] max global inflation
+  CUDA_CHECK(cudaMemsetAsync(parts, 0, 2 * sizeof(double), st));
+  k_reach_parts<<<296, 256, 0, st>>>(c->E, c->edge, x, N, c->infl, parts);
+  LAUNCH_CHECK();
+  std::vector<double> boxes(6 * D);
+  double h2[2];
+  CUDA_CHECK(cudaMemcpyAsync(h2, parts, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaMemcpyAsync(boxes.data(), c->sub_box.p, sizeof(double) * 6 * D, cudaMemcpyDeviceToHost, st));
+  sync_stream(c);
+  const double rho = (2.0 * h2[1] + 2.0 * h2[0]) * (1.0 + 1e-9);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0;
+  for (int64_t d = 0; d < D; ++d)
+    for (int k = 0; k < 3; ++k) {
+      const double m = 0.5 * (boxes[6 * d + k] + boxes[6 * d + 3 + k]);
+      lo[k] = std::min(lo[k], m);
+      hi[k] = std::max(hi[k], m);
+      ext = std::max(ext, boxes[6 * d + 3 + k] - boxes[6 * d + k]);
+    }
+  // centres of two subdomains whose boxes are within rho are within rho + ext per axis
+  double h = std::max(rho + ext, 1e-12);
+  int n[3];
+  for (;;) {
+    double cells = 1.0;
+    for (int k = 0; k < 3; ++k) {
+      n[k] = (int)std::floor((hi[k] - lo[k]) / h) + 1;
+      cells *= n[k];
+    }
+    if (cells < 4e18) break;
+    h *= 2.0;
+  }
+  c->dscal_h.assign(lo, lo + 3);
+  CUDA_CHECK(cudaMemcpyAsync(c->dscal.p + 50, lo, 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  c->sub_key.ensure(D); c->sub_key2.ensure(D); c->sub_id.ensure(D); c->sub_id2.ensure(D);
+  k_sub_keys<<<grid_for(D, 256), 256, 0, st>>>(D, c->sub_box, c->dscal.p + 50, 1.0 / h, n[1], n[2], c->sub_key,
+                                                c->sub_id);
+  LAUNCH_CHECK();
+  const unsigned long long ncell = (unsigned long long)n[0] * n[1] * n[2];
+  sort_pairs_u64(c, c->sub_key, c->sub_key2, c->sub_id, c->sub_id2, D, bits_for(ncell));
+  k_sub_delta<<<grid_for(D, 128), 128, 0, st>>>(D, c->sub_box, c->sub_cen, c->dscal.p + 50, 1.0 / h, n[0], n[1], n[2],
+                                                rho, c->sub_key2, c->sub_id2, c->sub_delta);
+  LAUNCH_CHECK();
+  k_local_infl<<<grid_for(N, 256), 256, 0, st>>>(N, c->bs, p, alpha_d, c->sub_cen, c->sub_delta, c->infl2);
+  LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemsetAsync(parts, 0, 2 * sizeof(double), st));
+  k_reach_parts<<<296, 256, 0, st>>>(0, c->edge, x, N, c->infl2, parts);
+  LAUNCH_CHECK();
+  double m2[2];
+  CUDA_CHECK(cudaMemcpyAsync(m2, parts, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  sync_stream(c);
+  if (m2[1] < h2[1]) std::swap(c->infl.p, c->infl2.p);  // the local inflation wins
+}
+
 // per-vertex inflation of the two-pass tight enumeration (cross = 0: the
 // same-body pass, 1: the cross-body pass), p scaled by alpha_d if given
 static void body_infl(mp_ctx* c, const double* p, const double* alpha_d, int cross) {
@@ -452,6 +661,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       LAUNCH_CHECK();
       k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, nullptr, d_mid, c->infl);
       LAUNCH_CHECK();
+      if (c->ccd_local) local_infl(c, x, p, nullptr);
       infl = c->infl;
     }
     if (!exact_set && c->ccd_prefilter) obj_motion(c, p, nullptr);
@@ -527,6 +737,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
         LAUNCH_CHECK();
         k_motion_infl<<<grid_for(c->N, 256), 256, 0, st>>>(c->N, c->bs, p, c->alpha_d, d_mid, c->infl);
         LAUNCH_CHECK();
+        if (c->ccd_local) local_infl(c, x, p, c->alpha_d);
         if (c->ccd_prefilter) obj_motion(c, p, c->alpha_d);
         BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl);
         if (c->ccd_prefilter) B2.T.objmot = c->obj_mot.p;

@@ -252,6 +252,11 @@ struct mp_ctx {
   DBuf<double> obj_mot;              // per-object motion (c, m) for the exact CCD prefilter
   bool ccd_prefilter = true;         // MP_OPT_CCD_PREFILTER
   bool ccd_bodies = false;           // MP_OPT_CCD_BODIES: two-pass per-body tight enumeration
+  bool ccd_local = true;             // MP_OPT_CCD_LOCAL: per-subdomain motion centres (ccd.cuh local_infl)
+  DBuf<double> sub_cen, sub_box, sub_delta, infl2;
+  DBuf<unsigned long long> sub_key, sub_key2;
+  DBuf<int> sub_id, sub_id2;
+  std::vector<double> dscal_h;
   DBuf<int> cell_cnt, cell_off;  // per-primitive covered-cell counts / offsets
   BpGridBufs grid;
   DBuf<int> cand_a, cand_b;      // raw broad-phase pairs (taps)

@@ -168,47 +168,83 @@ __device__ __forceinline__ double fast_rcp(double a) {
   return fma(r, e, r);
 }
 
-// Sweep every pivot of the m x m (m <= 96) symmetric matrix staged in smem
-// S (row-major); on return S holds -S^-1.  rowk: 2 x 96 smem scratch.
-// Returns false (uniformly) when a pivot is not positive.
-//
-// Per step the common path is 12 LDS, 6 DMUL and 36 DFMA per thread; only
-// the 16 threads holding row k and the 16 holding column k take a
-// (warp-divergent, compile-time indexed) fix-up branch, and the owners of
-// row k+1 publish it for the next step right after their update.
+// Sweep every pivot of the m x m (m <= 96) symmetric matrix held in
+// registers (sweep_regs); on return it holds -M^-1.  Returns false
+// (uniformly) when a pivot is not positive.  Per step the common path is 12
+// shared loads and 36 DFMA per thread; the 16 threads holding row k and the
+// 16 holding column k take a compile-time-indexed fix-up, and the owners of
+// row k+1 publish it (raw and scaled by its reciprocal) right after their
+// update.
 
+// The pivot-row buffer of one step: raw row k [0, 96), the row scaled by
+// 1 / A_kk [96, 192), 1 / A_kk at [192], A_kk at [193] (double-buffered).
+#define SW_ROW 196
+
+// Owners of row k1 (one half-warp: tr fixed, tc = 0..15) publish it raw and
+// scaled for the next step; the pivot A_{k1,k1} comes from the half-warp's
+// lane tc = k1 % 16 (register R[A][A]), its reciprocal is computed once here
+// instead of in all 256 threads.
 template <int A>
-__device__ __forceinline__ void publish_row(const double (&R)[SWEEP_T][SWEEP_T], double* rk, int tc, int m) {
+__device__ __forceinline__ void publish_row_scaled(const double (&R)[SWEEP_T][SWEEP_T], double* rk, int tc, int m,
+                                                   int k1) {
+  const unsigned hm = 0xFFFFu << (threadIdx.x & 16);
+  const double piv = __shfl_sync(hm, R[A][A], (threadIdx.x & 16) + (k1 & 15));
+  const double inv = fast_rcp(piv);
 #pragma unroll
   for (int b = 0; b < SWEEP_T; ++b)
-    if (tc + 16 * b < m) rk[tc + 16 * b] = R[A][b];
-}
-
-__device__ __forceinline__ void publish(const double (&R)[SWEEP_T][SWEEP_T], int a, double* rk, int tc, int m) {
-  switch (a) {
-    case 0: publish_row<0>(R, rk, tc, m); break;
-    case 1: publish_row<1>(R, rk, tc, m); break;
-    case 2: publish_row<2>(R, rk, tc, m); break;
-    case 3: publish_row<3>(R, rk, tc, m); break;
-    case 4: publish_row<4>(R, rk, tc, m); break;
-    default: publish_row<5>(R, rk, tc, m); break;
+    if (tc + 16 * b < m) {
+      rk[tc + 16 * b] = R[A][b];
+      rk[96 + tc + 16 * b] = R[A][b] * inv;
+    }
+  if (tc == 0) {
+    rk[192] = inv;
+    rk[193] = piv;
   }
 }
 
-template <int A>
-__device__ __forceinline__ void fix_row(double (&R)[SWEEP_T][SWEEP_T], const double (&cj)[SWEEP_T], double inv) {
+// The 16 pivots of register panel KA (k = 16 KA + kr): the fix-ups index
+// R[KA][.] / R[.][KA] at compile time.  Per step: one barrier, 12 shared
+// loads (the scaled column values, the raw row values), 36 FMA.
+template <int KA>
+__device__ __forceinline__ bool sweep_panel(int m, double* rowk, double (&R)[SWEEP_T][SWEEP_T], int tr, int tc) {
+  for (int kr = 0; kr < 16; ++kr) {
+    const int k = 16 * KA + kr;
+    if (k >= m) return true;  // uniform
+    const double* r = rowk + (k & 1) * SW_ROW;
+    __syncthreads();
+    if (!(r[193] > 0.0)) return false;  // uniform across the CTA
+    const double inv = r[192];
+    double ci[SWEEP_T], cj[SWEEP_T];
 #pragma unroll
-  for (int b = 0; b < SWEEP_T; ++b) R[A][b] = cj[b] * inv;
-}
-
-template <int B>
-__device__ __forceinline__ void fix_col(double (&R)[SWEEP_T][SWEEP_T], const double (&ci)[SWEEP_T]) {
+    for (int a = 0; a < SWEEP_T; ++a) {
+      ci[a] = r[96 + tr + 16 * a];  // A_ik / A_kk (= A_ki / A_kk)
+      cj[a] = r[tc + 16 * a];       // A_kj
+    }
 #pragma unroll
-  for (int a = 0; a < SWEEP_T; ++a) R[a][B] = ci[a];
+    for (int a = 0; a < SWEEP_T; ++a)
+#pragma unroll
+      for (int b = 0; b < SWEEP_T; ++b) R[a][b] = fma(-ci[a], cj[b], R[a][b]);
+    if (tr == kr)  // row k: A_kj <- A_kj / A_kk
+#pragma unroll
+      for (int b = 0; b < SWEEP_T; ++b) R[KA][b] = r[96 + tc + 16 * b];
+    if (tc == kr) {  // column k: A_ik <- A_ik / A_kk, and A_kk <- -1 / A_kk
+#pragma unroll
+      for (int a = 0; a < SWEEP_T; ++a) R[a][KA] = ci[a];
+      if (tr == kr) R[KA][KA] = -inv;
+    }
+    const int k1 = k + 1;
+    if (k1 < m && tr == (k1 & 15)) {
+      double* rn = rowk + (k1 & 1) * SW_ROW;
+      if (kr < 15) publish_row_scaled<KA>(R, rn, tc, m, k1);
+      else if (KA + 1 < SWEEP_T) publish_row_scaled<(KA + 1 < SWEEP_T ? KA + 1 : KA)>(R, rn, tc, m, k1);
+    }
+  }
+  return true;
 }
 
 // The matrix lives in R (thread (tr, tc) holds rows tr + 16a, columns
 // tc + 16b); LOAD(i, j) supplies the input, all 36 loads issued at once.
+// rowk: 2 x SW_ROW doubles of shared memory.
 template <class LOAD>
 __device__ bool sweep_regs(LOAD load, int m, double* rowk, double (&R)[SWEEP_T][SWEEP_T]) {
   const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
@@ -219,166 +255,12 @@ __device__ bool sweep_regs(LOAD load, int m, double* rowk, double (&R)[SWEEP_T][
       int i = tr + 16 * a, j = tc + 16 * b;
       R[a][b] = (i < m && j < m) ? load(i, j) : 0.0;
     }
-  if (tr == 0) publish(R, 0, rowk, tc, m);  // row 0 for step 0
-  for (int k = 0; k < m; ++k) {
-    double* rk = rowk + (k & 1) * 96;
-    __syncthreads();
-    const double piv = rk[k];
-    if (!(piv > 0.0)) return false;  // uniform across the CTA
-    const double inv = fast_rcp(piv);
-    double ci[SWEEP_T], cj[SWEEP_T];
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a) {
-      ci[a] = rk[min(tr + 16 * a, 95)] * inv;
-      cj[a] = rk[min(tc + 16 * a, 95)];
-    }
-    // rank-one update of every element (row / column k fixed below)
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a)
-#pragma unroll
-      for (int b = 0; b < SWEEP_T; ++b) R[a][b] = fma(-ci[a], cj[b], R[a][b]);
-    const int kr = k & 15, ka = k >> 4;
-    if (tr == kr) {  // this thread holds part of row k: A_kj <- A_kj / piv
-      switch (ka) {
-        case 0: fix_row<0>(R, cj, inv); break;
-        case 1: fix_row<1>(R, cj, inv); break;
-        case 2: fix_row<2>(R, cj, inv); break;
-        case 3: fix_row<3>(R, cj, inv); break;
-        case 4: fix_row<4>(R, cj, inv); break;
-        default: fix_row<5>(R, cj, inv); break;
-      }
-    }
-    if (tc == kr) {  // column k: A_ik <- A_ik / piv, and A_kk <- -1 / piv
-      switch (ka) {
-        case 0: fix_col<0>(R, ci); if (tr == kr) R[0][0] = -inv; break;
-        case 1: fix_col<1>(R, ci); if (tr == kr) R[1][1] = -inv; break;
-        case 2: fix_col<2>(R, ci); if (tr == kr) R[2][2] = -inv; break;
-        case 3: fix_col<3>(R, ci); if (tr == kr) R[3][3] = -inv; break;
-        case 4: fix_col<4>(R, ci); if (tr == kr) R[4][4] = -inv; break;
-        default: fix_col<5>(R, ci); if (tr == kr) R[5][5] = -inv; break;
-      }
-    }
-    // publish row k+1 (already updated) into the other buffer
-    const int k1 = k + 1;
-    if (k1 < m && tr == (k1 & 15)) publish(R, k1 >> 4, rowk + (k1 & 1) * 96, tc, m);
-  }
-  return true;
-}
-
-// Blocked sweep (6 panels of 16 pivots) for the coarse-level pivot blocks,
-// where one CTA runs alone on the critical path.  Panel K = tile row/column
-// K of the register layout.  Per panel: the 16 x 16 pivot block P is staged
-// in smem and swept by warp 0 alone (warp-level broadcasts, no CTA barrier
-// inside the 16 pivot steps); W = A_:K P^-1 (column panel and P^-1 staged
-// in smem, rows padded to SWEEP_LD doubles against bank conflicts); the
-// rank-16 update A_ij -= W_i. A_jK. for i, j outside K (400 FMA per thread,
-// no barrier); block row / column K <- W^T / W.  Same sweep operator
-// (A <- -A^-1 after every panel).  Rows >= m are identity padding.
-#define SWEEP_LD 17
-#define SWEEP_SMEM (40 + 256 + 2 * 96 * SWEEP_LD)
-template <class LOAD>
-__device__ bool sweep_blocked(LOAD load, int m, double* sm, double (&R)[SWEEP_T][SWEEP_T]) {
-  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
-  double* pk = sm;                    // 2 x 16 pivot-row broadcast, [32] = SPD flag
-  double* pm = sm + 40;               // 16 x 16 (-P^-1)
-  double* acol = pm + 256;            // 96 x 16: A(i, 16K + d), row stride SWEEP_LD
-  double* wsm = acol + 96 * SWEEP_LD; // 96 x 16: W(i, c), row stride SWEEP_LD
-#pragma unroll
-  for (int a = 0; a < SWEEP_T; ++a)
-#pragma unroll
-    for (int b = 0; b < SWEEP_T; ++b) {
-      int i = tr + 16 * a, j = tc + 16 * b;
-      R[a][b] = (i < m && j < m) ? load(i, j) : (i == j ? 1.0 : 0.0);
-    }
-  const int np = (m + 15) >> 4;
-#pragma unroll
-  for (int K = 0; K < SWEEP_T; ++K) {
-    if (K >= np) break;
-    // (1) pivot block P = R[K][K], swept by warp 0 (lane l: row l/2,
-    //     columns 8 (l%2) .. +8)
-    pm[tr * 16 + tc] = R[K][K];
-    __syncthreads();
-    if (tid < 32) {
-      const int lane = tid, r = lane >> 1, c0 = (lane & 1) * 8;
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = pm[r * 16 + c0 + q];
-      bool ok = true;
-      for (int k = 0; k < 16; ++k) {
-        double* row = pk + (k & 1) * 16;
-        if (r == k) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) row[c0 + q] = v[q];
-        }
-        __syncwarp();
-        const double piv = row[k];
-        if (!(piv > 0.0)) {
-          ok = false;
-          break;  // uniform across the warp
-        }
-        const double inv = fast_rcp(piv);
-        const double ci = row[r] * inv;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int c = c0 + q;
-          const double cj = row[c];
-          double t = fma(-ci, cj, v[q]);
-          if (r == k) t = cj * inv;
-          if (c == k) t = (r == k) ? -inv : ci;
-          v[q] = t;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) pm[r * 16 + c0 + q] = v[q];
-      if (lane == 0) pk[32] = ok ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    if (pk[32] == 0.0) return false;  // uniform across the CTA
-    R[K][K] = pm[tr * 16 + tc];
-    // (2) stage the column panel A(i, K.) for i outside K; -P^-1 is in pm
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a)
-      if (a != K) acol[(tr + 16 * a) * SWEEP_LD + tc] = R[a][K];
-    __syncthreads();
-    // (3) W(i, c) = A_iK P^-1 = -sum_d A(i, Kd) pm(d, c), c = tc
-    double w[SWEEP_T];
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a) {
-      w[a] = 0.0;
-      if (a == K) continue;
-      const double* ar = acol + (tr + 16 * a) * SWEEP_LD;
-#pragma unroll
-      for (int d = 0; d < 16; ++d) w[a] = fma(-ar[d], pm[d * 16 + tc], w[a]);
-      wsm[(tr + 16 * a) * SWEEP_LD + tc] = w[a];
-    }
-    __syncthreads();
-    // (4) A_ij -= W(i, .) . A(j, K.) for i, j outside K
-#pragma unroll
-    for (int d = 0; d < 16; ++d) {
-      double wi[SWEEP_T], aj[SWEEP_T];
-#pragma unroll
-      for (int a = 0; a < SWEEP_T; ++a) {
-        wi[a] = (a == K) ? 0.0 : wsm[(tr + 16 * a) * SWEEP_LD + d];
-        aj[a] = (a == K) ? 0.0 : acol[(tc + 16 * a) * SWEEP_LD + d];
-      }
-#pragma unroll
-      for (int a = 0; a < SWEEP_T; ++a) {
-        if (a == K) continue;
-#pragma unroll
-        for (int b = 0; b < SWEEP_T; ++b)
-          if (b != K) R[a][b] = fma(-wi[a], aj[b], R[a][b]);
-      }
-    }
-    // (5) block column K <- W, block row K <- W^T
-#pragma unroll
-    for (int a = 0; a < SWEEP_T; ++a)
-      if (a != K) R[a][K] = w[a];
-#pragma unroll
-    for (int b = 0; b < SWEEP_T; ++b)
-      if (b != K) R[K][b] = wsm[(tc + 16 * b) * SWEEP_LD + tr];
-    __syncthreads();  // acol / wsm / pm are rewritten by the next panel
-  }
-  return true;
+  for (int e = tid; e < 2 * SW_ROW; e += blockDim.x) rowk[e] = 0.0;
+  __syncthreads();
+  if (tr == 0) publish_row_scaled<0>(R, rowk, tc, m, 0);  // row 0 for step 0
+  return sweep_panel<0>(m, rowk, R, tr, tc) && sweep_panel<1>(m, rowk, R, tr, tc) &&
+         sweep_panel<2>(m, rowk, R, tr, tc) && sweep_panel<3>(m, rowk, R, tr, tc) &&
+         sweep_panel<4>(m, rowk, R, tr, tc) && sweep_panel<5>(m, rowk, R, tr, tc);
 }
 
 // element (i, j) of a symmetric m x m matrix is the stored representative
@@ -408,7 +290,7 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const unsigned char* __restrict
             double* __restrict__ Mblk,
             double* __restrict__ Bblk, int* __restrict__ status, int64_t d0) {
   extern __shared__ double msm[];  // m x m: M_d
-  __shared__ double rowk[2 * 96];
+  __shared__ double rowk[2 * SW_ROW];
   const int64_t d = d0 + blockIdx.x;  // d0: a shard's first owned subdomain
   const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
   const int nd3 = 3 * (int)((N - d * bs) < bs ? (N - d * bs) : bs);
@@ -436,45 +318,6 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const unsigned char* __restrict
       const int i = tr + 16 * a, j = tc + 16 * b;
       if (i < m && j < m && cyc_rep(m, i, j)) bout[cyc_index(m, i, j)] = -R[a][b];
     }
-}
-
-// Pivot block of the blocked dense sweep: out (kb x kb) = -P^-1 for the
-// diagonal block P = A[k0:k0+kb, k0:k0+kb] of the n x n matrix A (lda = n).
-__global__ void __launch_bounds__(256, 1)
-k_block_sweep(int kb, const double* __restrict__ A, int lda, int k0, double* __restrict__ out,
-              int* __restrict__ status) {
-  __shared__ double swsm[SWEEP_SMEM];
-  const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
-  double R[SWEEP_T][SWEEP_T];
-  // the pivot block is symmetric (to rounding of the lookahead GEMM): read
-  // it row-major so a warp's 16-column lanes load contiguous doubles
-  auto load = [&](int i, int j) -> double { return __ldg(A + (int64_t)(k0 + i) * lda + k0 + j); };
-  if (!sweep_blocked(load, kb, swsm, R)) {
-    if (threadIdx.x == 0) atomicExch(status, 1);
-    return;
-  }
-#pragma unroll
-  for (int a = 0; a < SWEEP_T; ++a)
-#pragma unroll
-    for (int b = 0; b < SWEEP_T; ++b) {
-      const int i = tr + 16 * a, j = tc + 16 * b;
-      if (i < kb && j < kb) out[i * kb + j] = R[a][b];
-    }
-}
-
-// after the rank-kb update: block column/row K <- W (= A_iK P^-1), A_KK <- -P^-1
-__global__ void k_block_fix(int n, int kb, int k0, const double* __restrict__ W, const double* __restrict__ Pm,
-                            double* __restrict__ A) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= (int64_t)n * kb) return;
-  int i = (int)(e % n), c = (int)(e / n);  // W is n x kb column-major
-  double w = W[e];
-  if (i >= k0 && i < k0 + kb) {
-    A[(int64_t)(k0 + c) * n + i] = Pm[(i - k0) * kb + c];
-  } else {
-    A[(int64_t)(k0 + c) * n + i] = w;  // A[i, k0+c]
-    A[(int64_t)i * n + k0 + c] = w;    // A[k0+c, i]
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -643,18 +486,6 @@ __global__ void k_sym_lower(int n, double* M, const unsigned long long* __restri
   M[(int64_t)i * n + j] = s;
   M[(int64_t)j * n + i] = s;
 }
-
-// pack sym(-A) (A = -M^-1 after the blocked sweep) in the cyclic layout
-__global__ void k_pack_neg_sym(int n, const double* __restrict__ A, double* __restrict__ out) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= cyc_size(n)) return;
-  int s = (int)(e / n);
-  int i = (int)(e - (int64_t)s * n);
-  int j = i + s;
-  if (j >= n) j -= n;
-  out[e] = -0.5 * (A[(int64_t)j * n + i] + A[(int64_t)i * n + j]);
-}
-
 
 // ---------------------------------------------------------------------------
 // apply

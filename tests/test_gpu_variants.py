@@ -123,8 +123,9 @@ def test_apply_overlap_same_bits():
 
 @pytest.mark.parametrize("name", ["stacked_k256", "locking"])
 def test_ccd_prefilter_and_bodies_same_results(name):
-    """MP_OPT_CCD_PREFILTER (11, exact relative-motion pair prefilter) and
-    MP_OPT_CCD_BODIES (12, two-pass per-body enumeration): the same alpha_d,
+    """MP_OPT_CCD_PREFILTER (11, exact relative-motion pair prefilter),
+    MP_OPT_CCD_BODIES (12, two-pass per-body enumeration) and
+    MP_OPT_CCD_LOCAL (13, per-subdomain motion centres): the same alpha_d,
     minimum, certificate and x_new as the plain tight enumeration."""
     g = load_golden(name)
     scene = scene_from_golden(g)
@@ -136,9 +137,10 @@ def test_ccd_prefilter_and_bodies_same_results(name):
     try:
         for x, p in cases:
             out = []
-            for pre, bod in ((0, 0), (1, 0), (0, 1), (1, 1)):
+            for pre, bod, loc in ((0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0), (0, 0, 1), (1, 0, 1)):
                 ctx.set_option(11, pre)
                 ctx.set_option(12, bod)
+                ctx.set_option(13, loc)
                 out.append(ctx.ccd(x, p, exact_set=False))
             for o in out[1:]:
                 assert np.array_equal(out[0][0], o[0]) and np.array_equal(out[0][1], o[1])
@@ -146,3 +148,4 @@ def test_ccd_prefilter_and_bodies_same_results(name):
     finally:
         ctx.set_option(11, 1)
         ctx.set_option(12, 0)
+        ctx.set_option(13, 1)
