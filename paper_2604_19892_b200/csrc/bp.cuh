@@ -11,6 +11,7 @@
 // our own grid (below) over boxes that provably contain every such pair.
 #pragma once
 
+#include <chrono>
 #include <cub/cub.cuh>
 
 #include "ctx.cuh"
@@ -144,7 +145,13 @@ static int bits_for(unsigned long long v) {
 
 // Boxes of triangles and edges: raw (rlo, rhi); reference filter (flo, fhi:
 // triangle [lo - gap, hi + gap], edge [lo, hi + gap]); enumeration (elo,
-// ehi).  The largest raw-box diagonal (the reference's grid cell candidate,
+// ehi).  A tight inflation (per vertex, ccd.cuh) is capped at gap: every
+// enumerated pair must also pass the reference filter (axis separation <=
+// gap), and two boxes grown by min(i_a, gap), min(i_b, gap) still meet
+// whenever the separation is <= min(i_a + i_b, gap) -- so the enumeration is
+// never looser than the reference's own filter, whatever the motion field
+// (the cap carries a 1e-9 relative margin over the rounded filter).  The
+// largest raw-box diagonal (the reference's grid cell candidate,
 // geometry.py:462-465, same IEEE expression) is max-reduced into *diag_max.
 __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, const int* __restrict__ edge,
                              const double* __restrict__ x, double gap, const double* __restrict__ infl,
@@ -157,7 +164,7 @@ __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, 
     double l[3], h[3], inf = 0.0;
     if (i < F) {
       int a = tri[3 * i], b = tri[3 * i + 1], c = tri[3 * i + 2];
-      if (infl) inf = fmax(fmax(infl[a], infl[b]), infl[c]);
+      if (infl) inf = fmin(fmax(fmax(infl[a], infl[b]), infl[c]), gap * (1.0 + 1e-9));
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double xa = x[3 * a + k], xb = x[3 * b + k], xc = x[3 * c + k];
@@ -167,7 +174,7 @@ __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, 
     } else {
       int64_t e = i - F;
       int a = edge[2 * e], b = edge[2 * e + 1];
-      if (infl) inf = fmax(infl[a], infl[b]);
+      if (infl) inf = fmin(fmax(infl[a], infl[b]), gap * (1.0 + 1e-9));
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double xa = x[3 * a + k], xb = x[3 * b + k];
@@ -196,12 +203,12 @@ __global__ void k_prim_boxes(int64_t F, int64_t E, const int* __restrict__ tri, 
 }
 
 // enumeration boxes of the surface points (object ids F+E+q)
-__global__ void k_point_boxes(int64_t V, const int* __restrict__ sverts, const double* __restrict__ x,
+__global__ void k_point_boxes(int64_t V, const int* __restrict__ sverts, const double* __restrict__ x, double gap,
                               const double* __restrict__ infl, double* __restrict__ elo, double* __restrict__ ehi) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= V) return;
   int v = sverts[q];
-  double e = infl ? infl[v] : 0.0;
+  double e = infl ? fmin(infl[v], gap * (1.0 + 1e-9)) : 0.0;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     elo[3 * q + k] = x[3 * v + k] - e;
@@ -210,34 +217,39 @@ __global__ void k_point_boxes(int64_t V, const int* __restrict__ sverts, const d
 }
 
 // stats for the grid: [0..2] min lo, [3..5] max hi, [6] sum of max extents
+// of the enumeration boxes, [7] the same of the raw boxes
+#define BOX_STATS 8
 __global__ void k_box_stats(int64_t P, const double* __restrict__ lo, const double* __restrict__ hi,
+                            const double* __restrict__ rlo, const double* __restrict__ rhi,
                             double* __restrict__ part) {
-  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0;
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0, rext = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    double e = 0.0;
+    double e = 0.0, r = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       double l = lo[3 * i + k], h = hi[3 * i + k];
       mn[k] = fmin(mn[k], l);
       mx[k] = fmax(mx[k], h);
       e = fmax(e, h - l);
+      r = fmax(r, rhi[3 * i + k] - rlo[3 * i + k]);
     }
     ext += e;
+    rext += r;
   }
-  __shared__ double sh[7][8];
-  double vals[7] = {-mn[0], -mn[1], -mn[2], mx[0], mx[1], mx[2], ext};
+  __shared__ double sh[BOX_STATS][8];
+  double vals[BOX_STATS] = {-mn[0], -mn[1], -mn[2], mx[0], mx[1], mx[2], ext, rext};
 #pragma unroll
-  for (int q = 0; q < 7; ++q) {
+  for (int q = 0; q < BOX_STATS; ++q) {
     double v = vals[q];
     v = (q < 6) ? warp_max(v) : warp_sum(v);
     if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x >> 5] = v;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int q = 0; q < 7; ++q) {
+    for (int q = 0; q < BOX_STATS; ++q) {
       double v = sh[q][0];
       for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = (q < 6) ? fmax(v, sh[q][w]) : v + sh[q][w];
-      part[7 * blockIdx.x + q] = v;
+      part[BOX_STATS * blockIdx.x + q] = v;
     }
   }
 }
@@ -919,13 +931,20 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
 struct BpGrid {
   BpTables T{};
   bool empty = true;
+  bool has_grid = false;  // false: boxes / filters only (the BVH enumeration, bvh.cuh)
+  double filter_gap = 0.0;  // the reference filter gap with a rounding margin (bvh.cuh node tests)
 };
+
+enum { BP_GRID_NONE = 0, BP_GRID_ALWAYS = 1, BP_GRID_AUTO = 2 };
+// measured at C5 (bvh.cuh): the grid wins below ~1.5x (10 vs 28 ms per CCD
+// call), the BVH above (49 vs 615 ms at 4.4x, 0.6 vs 15.5 s at 18x)
+#define BP_AUTO_RATIO 1.6
 
 // Everything one broad-phase call at (x, mb, d_hat) needs: boxes, levels,
 // reference cell ranges and the per-level cell tables of triangles / edges /
 // surface points.  infl (per vertex, device) switches to tight enumeration.
 static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, const double* infl = nullptr,
-                       int body_mode = 0) {
+                       int body_mode = 0, int grid_mode = BP_GRID_ALWAYS) {
   BpGrid B;
   const int64_t F = c->F, P = c->F + c->E, V = c->V, nobj = P + V;
   B.T.F = F;
@@ -943,34 +962,57 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
                                                   c->box_flo, c->box_fhi, c->box_elo, c->box_ehi, c->dscal.p + 40);
   LAUNCH_CHECK();
   if (V) {
-    k_point_boxes<<<grid_for(V, 256), 256, 0, st>>>(V, c->sverts, x, infl, c->box_elo.p + 3 * P,
+    k_point_boxes<<<grid_for(V, 256), 256, 0, st>>>(V, c->sverts, x, gap, infl, c->box_elo.p + 3 * P,
                                                      c->box_ehi.p + 3 * P);
     LAUNCH_CHECK();
   }
   const int nb = 64;
-  c->red_part.ensure(7 * nb + 1);
-  k_box_stats<<<nb, 256, 0, st>>>(P, c->box_elo, c->box_ehi, c->red_part);
+  c->red_part.ensure(BOX_STATS * nb + 1);
+  k_box_stats<<<nb, 256, 0, st>>>(P, c->box_elo, c->box_ehi, c->box_rlo, c->box_rhi, c->red_part);
   LAUNCH_CHECK();
-  CUDA_CHECK(cudaMemcpyAsync(c->red_part.p + 7 * nb, c->dscal.p + 40, sizeof(double), cudaMemcpyDeviceToDevice, st));
-  std::vector<double> part(7 * nb + 1);
-  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * (7 * nb + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_CHECK(cudaMemcpyAsync(c->red_part.p + BOX_STATS * nb, c->dscal.p + 40, sizeof(double), cudaMemcpyDeviceToDevice,
+                             st));
+  std::vector<double> part(BOX_STATS * nb + 1);
+  CUDA_CHECK(cudaMemcpyAsync(part.data(), c->red_part.p, sizeof(double) * (BOX_STATS * nb + 1), cudaMemcpyDeviceToHost,
+                             st));
   sync_stream(c);
-  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0;
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, ext = 0.0, rext = 0.0;
   for (int b = 0; b < nb; ++b) {
     for (int k = 0; k < 3; ++k) {
-      mn[k] = fmin(mn[k], -part[7 * b + k]);
-      mx[k] = fmax(mx[k], part[7 * b + 3 + k]);
+      mn[k] = fmin(mn[k], -part[BOX_STATS * b + k]);
+      mx[k] = fmax(mx[k], part[BOX_STATS * b + 3 + k]);
     }
-    ext += part[7 * b + 6];
+    ext += part[BOX_STATS * b + 6];
+    rext += part[BOX_STATS * b + 7];
   }
   auto& g = c->grid;
   // the reference's cell and pad (geometry.py:465-466) -> per-object ranges
-  const double ref_cell = fmax(part[7 * nb], d_hat + mb);
+  const double ref_cell = fmax(part[BOX_STATS * nb], d_hat + mb);
   const double ref_pad = 0.5 * d_hat + mb;
   g.rc.ensure(6 * nobj);
   k_ref_cells<<<grid_for(nobj, 256), 256, 0, st>>>(P, V, c->sverts, x, c->box_rlo, c->box_rhi, ref_pad, ref_cell,
                                                    g.rc);
   LAUNCH_CHECK();
+  {
+    // the filter tests of the BVH nodes: gap plus a relative and an absolute
+    // (a few ulps of the largest coordinate) rounding margin
+    double amax = 0.0;
+    for (int k = 0; k < 3; ++k) amax = fmax(amax, fmax(fabs(mn[k]), fabs(mx[k])));
+    B.filter_gap = gap * (1.0 + 1e-9) + 1e-15 * (std::isfinite(amax) ? amax : 0.0);
+  }
+  // the grid's box tests grow with the cube of the enumeration-to-raw extent
+  // ratio; past BP_AUTO_RATIO the BVH (bvh.cuh) enumerates instead
+  const bool want_grid = grid_mode == BP_GRID_ALWAYS || (grid_mode == BP_GRID_AUTO && !(ext > BP_AUTO_RATIO * rext));
+  if (!want_grid) {
+    BpTables& T = B.T;
+    T.rc = g.rc;
+    T.flo = c->box_flo; T.fhi = c->box_fhi;
+    T.elo = c->box_elo; T.ehi = c->box_ehi;
+    T.rlo = c->box_rlo; T.rhi = c->box_rhi;
+    B.empty = false;
+    return B;
+  }
+  B.has_grid = true;
   // level 0: about the mean primitive extent, at most ~4M cells
   double span = fmax(fmax(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
   if (!(span > 0.0) || !std::isfinite(span)) span = 1.0;
@@ -1156,6 +1198,51 @@ static void fused_pairs(mp_ctx* c, const double* x, const BpGrid& B, const PairA
   }
 }
 
+// MP_BP_TRACE=1: per-kernel host timings of the one-pass enumeration and a
+// per-level summary of the grid (objects per class, largest cell) on stderr
+struct BpTrace {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit BpTrace(cudaStream_t s) : on(getenv("MP_BP_TRACE") != nullptr), st(s) {
+    if (on) { CUDA_CHECK(cudaStreamSynchronize(st)); t0 = std::chrono::steady_clock::now(); }
+  }
+  void lap(const char* what) {
+    if (!on) return;
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "  bp %-8s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
+static void bp_trace_levels(mp_ctx* c, const BpGrid& B) {
+  const HGrid& G = B.T.G;
+  const int64_t nobj = B.T.P + c->V;
+  std::vector<int> lev(nobj);
+  CUDA_CHECK(cudaMemcpy(lev.data(), B.T.level, sizeof(int) * nobj, cudaMemcpyDeviceToHost));
+  const int64_t ncell = G.off[G.nlev];
+  std::vector<int> st[3];
+  const int* starts[3] = {B.T.tri_start, B.T.edge_start, B.T.pt_start};
+  for (int q = 0; q < 3; ++q) {
+    st[q].resize(ncell + 1);
+    CUDA_CHECK(cudaMemcpy(st[q].data(), starts[q], sizeof(int) * (ncell + 1), cudaMemcpyDeviceToHost));
+  }
+  fprintf(stderr, "  bp grid h0=%.4g nlev=%d\n", G.h0, G.nlev);
+  for (int l = 0; l < G.nlev; ++l) {
+    int64_t cnt[3] = {0, 0, 0};
+    for (int64_t i = 0; i < nobj; ++i)
+      if (lev[i] == l) ++cnt[i < B.T.F ? 0 : (i < B.T.P ? 1 : 2)];
+    int mx[3] = {0, 0, 0};
+    for (int64_t cc = G.off[l]; cc < G.off[l + 1]; ++cc)
+      for (int q = 0; q < 3; ++q) mx[q] = std::max(mx[q], st[q][cc + 1] - st[q][cc]);
+    if (cnt[0] + cnt[1] + cnt[2])
+      fprintf(stderr, "  bp L%-2d cells %dx%dx%d  tri %lld (max/cell %d)  edge %lld (%d)  pt %lld (%d)\n", l,
+              G.n[l][0], G.n[l][1], G.n[l][2], (long long)cnt[0], mx[0], (long long)cnt[1], mx[1],
+              (long long)cnt[2], mx[2]);
+  }
+}
+
 template <int MODE>
 static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
                       int* flag, int which = 3, int64_t* n_pt_out = nullptr) {
@@ -1195,14 +1282,18 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
       CUDA_CHECK(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), c->stream));  // [10]: append overflow flag
       const int64_t cap_pt = (int64_t)std::min(g.pa.n, g.pb.n), cap_ee = (int64_t)std::min(g.ea.n, g.eb.n);
       if (!B.empty) {
+        if (getenv("MP_BP_TRACE")) bp_trace_levels(c, B);
+        BpTrace tr(c->stream);
         PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr, g.pa, g.pb, cnt, cap_pt};
         if (V) {
           k_hq_points<HQ_APPEND><<<grid_for(32 * V, 128), 128, 0, c->stream>>>(B.T, V, c->sverts, c->tri, x, nullptr,
                                                                                nullptr, nullptr, nullptr, 0, A);
           LAUNCH_CHECK();
+          tr.lap("points");
           k_hq_tris<HQ_APPEND><<<grid_for(32 * F, 128), 128, 0, c->stream>>>(B.T, F, c->sverts, c->tri, x, nullptr,
                                                                              nullptr, nullptr, nullptr, 0, A);
           LAUNCH_CHECK();
+          tr.lap("tris");
         }
         if (E > 1) {
           PairArgs Ae = A;
@@ -1210,9 +1301,11 @@ static int64_t run_bp(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Cont
           k_hq_edges<HQ_APPEND><<<grid_for(32 * E, 128), 128, 0, c->stream>>>(B.T, E, c->edge, nullptr, nullptr,
                                                                               nullptr, nullptr, 0, Ae);
           LAUNCH_CHECK();
+          tr.lap("edges");
         }
         k_pairs_app<MODE><<<8 * 148, 256, 0, c->stream>>>(cnt, cap_pt, cap_ee, g.pa, g.pb, g.ea, g.eb, A);
         LAUNCH_CHECK();
+        tr.lap("pairs");
       }
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));

@@ -1,0 +1,576 @@
+// bvh.cuh -- motion-aware bounding-volume hierarchy for the tight CCD and
+// certificate enumeration (the reference pair set of ccd.py:221-241 under the
+// exact filters of bp.cuh).
+//
+// The hierarchical grid (bp.cuh) sizes its cells on the enumeration boxes.
+// When a direction p is large over much of the scene (a restart direction
+// before alpha_d clamps it), every box grows to ~2 |p|_inf, the grid
+// collapses to a few cells holding 10^4-10^5 objects each, and the box tests
+// explode quadratically (seconds per call at C5), although the exact
+// relative-motion prefilter (bp.cuh rel_safe) keeps only ~10^7 pairs: most
+// of a ball moves with its neighbourhood.  Here the pruning itself is
+// relative.  Each node of a fixed-topology 8-ary tree over the objects
+// (ordered by their smallest Morton-renumbered vertex id, so siblings are
+// spatial neighbours) carries, rounded outward to float:
+//   - the union of its objects' raw boxes and enumeration boxes,
+//   - the box of their motion centres c_o and the largest motion radius m_o
+//     (k_obj_motion),
+// and a query object q skips a child whose enumeration box misses q's, whose
+// raw box is beyond the reference filter gap, or for which
+//   0.9 dist(raw_q, raw_node) > 4 max(m_q, m_node + max_{c in cbox} |c_q - c|),
+// the node-wide form of rel_safe (M <= max(m_q, m_o + |c_q - c_o|)).  Every
+// skip is implied for each object below, so the objects reached and tested
+// with the unchanged per-pair predicate are a superset of the passing ones:
+// the emitted pair set is the grid's, bit for bit.
+#pragma once
+
+#include "bp.cuh"
+
+#define BVH_W 8
+#define BVH_MAX_LEVELS 12
+// depth-first, children pushed after their parent is popped: at most
+// 1 + 7 (levels - 1) entries are live
+#define BVH_STACK (1 + (BVH_W - 1) * (BVH_MAX_LEVELS - 1))
+
+struct BvhNode {
+  float rlo[3], rhi[3];  // raw boxes (union)
+  float elo[3], ehi[3];  // enumeration boxes (union)
+  float clo[3], chi[3];  // motion centres (box)
+  float m;               // largest motion radius
+  int pad;
+};
+
+struct BvhTree {
+  const BvhNode* node;        // all levels, leaves (level 0) first
+  const int* order;           // sorted position -> object index within the class
+  int64_t n;                  // objects
+  int nlev;                   // levels; level nlev-1 is the root
+  int64_t off[BVH_MAX_LEVELS + 1];
+  int64_t cnt[BVH_MAX_LEVELS];
+};
+
+__device__ __forceinline__ float f_dn(double v) { return __double2float_rd(v); }
+__device__ __forceinline__ float f_up(double v) { return __double2float_ru(v); }
+
+// leaf level: thread per object, groups of 8 lanes reduce one leaf.  base =
+// object id offset of the class in the per-object arrays (tris 0, edges F).
+__global__ void k_bvh_leaves(int64_t n, int64_t base, const int* __restrict__ order, const double* __restrict__ rlo,
+                             const double* __restrict__ rhi, const double* __restrict__ elo,
+                             const double* __restrict__ ehi, const double* __restrict__ mot,
+                             BvhNode* __restrict__ leaf) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = s < n;
+  float v[19];
+  if (live) {
+    const int64_t o = base + order[s];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v[k] = f_dn(rlo[3 * o + k]);
+      v[3 + k] = f_up(rhi[3 * o + k]);
+      v[6 + k] = f_dn(elo[3 * o + k]);
+      v[9 + k] = f_up(ehi[3 * o + k]);
+      const double cc = mot ? mot[4 * o + k] : 0.0;
+      v[12 + k] = f_dn(cc);
+      v[15 + k] = f_up(cc);
+    }
+    v[18] = mot ? f_up(mot[4 * o + 3]) : 0.0f;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v[k] = v[6 + k] = v[12 + k] = INFINITY;
+      v[3 + k] = v[9 + k] = v[15 + k] = -INFINITY;
+    }
+    v[18] = 0.0f;
+  }
+#pragma unroll
+  for (int o = 1; o < BVH_W; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 19; ++q) {
+      const float w = __shfl_xor_sync(0xffffffffu, v[q], o);
+      const bool is_lo = (q < 3) || (q >= 6 && q < 9) || (q >= 12 && q < 15);
+      v[q] = is_lo ? fminf(v[q], w) : fmaxf(v[q], w);
+    }
+  }
+  if (live && (s & (BVH_W - 1)) == 0) {
+    BvhNode& d = leaf[s / BVH_W];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      d.rlo[k] = v[k]; d.rhi[k] = v[3 + k];
+      d.elo[k] = v[6 + k]; d.ehi[k] = v[9 + k];
+      d.clo[k] = v[12 + k]; d.chi[k] = v[15 + k];
+    }
+    d.m = v[18];
+  }
+}
+
+// one level up: thread per child, groups of 8 lanes reduce one parent
+__global__ void k_bvh_up(int64_t nchild, const BvhNode* __restrict__ child, BvhNode* __restrict__ parent) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = s < nchild;
+  float v[19];
+  if (live) {
+    const BvhNode& c = child[s];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v[k] = c.rlo[k]; v[3 + k] = c.rhi[k];
+      v[6 + k] = c.elo[k]; v[9 + k] = c.ehi[k];
+      v[12 + k] = c.clo[k]; v[15 + k] = c.chi[k];
+    }
+    v[18] = c.m;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v[k] = v[6 + k] = v[12 + k] = INFINITY;
+      v[3 + k] = v[9 + k] = v[15 + k] = -INFINITY;
+    }
+    v[18] = 0.0f;
+  }
+#pragma unroll
+  for (int o = 1; o < BVH_W; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 19; ++q) {
+      const float w = __shfl_xor_sync(0xffffffffu, v[q], o);
+      const bool is_lo = (q < 3) || (q >= 6 && q < 9) || (q >= 12 && q < 15);
+      v[q] = is_lo ? fminf(v[q], w) : fmaxf(v[q], w);
+    }
+  }
+  if (live && (s & (BVH_W - 1)) == 0) {
+    BvhNode& d = parent[s / BVH_W];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      d.rlo[k] = v[k]; d.rhi[k] = v[3 + k];
+      d.elo[k] = v[6 + k]; d.ehi[k] = v[9 + k];
+      d.clo[k] = v[12 + k]; d.chi[k] = v[15 + k];
+    }
+    d.m = v[18];
+  }
+}
+
+// the query side of a node test
+struct BvhQuery {
+  double elo[3], ehi[3];  // enumeration box
+  double rlo[3], rhi[3];  // raw box
+  double c[3], m;         // motion centre / radius (rel != 0)
+  double gap;             // reference filter gap (with margin)
+  bool rel;
+};
+
+// May any object below `nd` pass the per-pair predicate against q?
+__device__ __forceinline__ bool bvh_visit(const BvhQuery& q, const BvhNode& nd) {
+  double d2 = 0.0, c2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    // enumeration boxes meet (boxes_meet on every object below)
+    if (q.elo[k] > (double)nd.ehi[k] || (double)nd.elo[k] > q.ehi[k]) return false;
+    // reference filter: per-axis separation of the raw boxes <= gap
+    const double sep = fmax(0.0, fmax(q.rlo[k] - (double)nd.rhi[k], (double)nd.rlo[k] - q.rhi[k]));
+    if (sep > q.gap) return false;
+    d2 += sep * sep;
+    const double dc = fmax(fabs(q.c[k] - (double)nd.clo[k]), fabs(q.c[k] - (double)nd.chi[k]));
+    c2 += dc * dc;
+  }
+  if (!q.rel) return true;
+  const double U = fmax(q.m, (double)nd.m + sqrt(c2));
+  return !(0.9 * sqrt(d2) * (1.0 - 1e-9) > 4.0 * U * (1.0 + 1e-9));
+}
+
+// Pair emission from divergent traversals: each thread buffers its pairs
+// (BVH_BUF) and flushes a full buffer alone (one atomic per BVH_BUF pairs);
+// after the traversal loop the converged warp flushes the remainders with
+// one atomic per warp.  (One atomic per pair on the shared list counter
+// serialises at ~1 ns each: 9 of the 10 ms of a C5 points pass.)
+#define BVH_BUF 16
+#define BVH_BUDGET 64          // node expansions per thread per round
+#define BVH_TASKS0 (1 << 20)   // initial task-list capacity per list
+// MP_BP_TRACE: [0] inner-node expansions, [1] leaf expansions, [2] objects tested, [3] queries
+__device__ unsigned long long g_bvh_stats[4];
+struct BvhOut {
+  int2 buf[BVH_BUF];
+  int n = 0;
+};
+
+__device__ __forceinline__ bool bvh_reserve(int k, int& base, const PairArgs& A) {
+  const int lim = g_append_limit;
+  base = atomicAdd(A.app_cnt, k);
+  if (base < 0 || base > lim - k) {
+    atomicExch(A.app_cnt + (A.app_ee ? 1 : 2), 1);
+    return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void bvh_write(int base, int k, const int2* buf, const PairArgs& A) {
+  for (int r = 0; r < k; ++r)
+    if ((int64_t)base + r < A.app_cap) {
+      A.app_a[base + r] = buf[r].x;
+      A.app_b[base + r] = buf[r].y;
+    }
+}
+
+__device__ __forceinline__ void bvh_emit(BvhOut& o, int a, int b, const PairArgs& A) {
+  o.buf[o.n++] = make_int2(a, b);
+  if (o.n == BVH_BUF) {
+    int base;
+    if (bvh_reserve(BVH_BUF, base, A)) bvh_write(base, BVH_BUF, o.buf, A);
+    o.n = 0;
+  }
+}
+
+// all 32 lanes, converged
+__device__ __forceinline__ void bvh_flush_warp(BvhOut& o, const PairArgs& A) {
+  const int lane = threadIdx.x & 31;
+  int incl = o.n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  int base = 0;
+  bool ok = true;
+  if (lane == 31) ok = bvh_reserve(total, base, A);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  ok = __shfl_sync(0xffffffffu, ok, 31);
+  if (ok) bvh_write(base + incl - o.n, o.n, o.buf, A);
+}
+
+// Load balance: a thread stops after `budget` node expansions and hands its
+// remaining stack to the next round as (query, entry) tasks, so a few
+// queries meeting thousands of nodes (a fast vertex among slow neighbours)
+// are spread over many threads instead of one thread finishing last.
+struct BvhTasks {
+  const int2* in;    // this round's (query, stack entry) tasks, or null: one root task per query
+  const int* n_in;
+  int2* out;         // entries handed to the next round
+  int* n_out;        // [0] count, [1] overflow flag
+  int64_t cap;
+  int budget;
+};
+
+__device__ __forceinline__ void bvh_dump(const BvhTasks& K, int query, const int* stack, int sp) {
+  const int base = atomicAdd(K.n_out, sp);
+  if (base < 0 || (int64_t)base + sp > K.cap) {
+    atomicExch(K.n_out + 1, 1);
+    return;
+  }
+  for (int r = 0; r < sp; ++r) K.out[base + r] = make_int2(query, stack[r]);
+}
+
+// Points query the triangle tree (PT pairs (v, t)); the leaf predicate is
+// k_hq_points' (boxes_meet, pt_ref_pass, rel_safe).
+__global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int64_t V, const int* __restrict__ sverts,
+                                                    const int* __restrict__ tri, const double* __restrict__ x,
+                                                    double gap, PairArgs A, BvhTasks K, bool stats) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = K.in ? (int64_t)*K.n_in : V;
+  if (blockIdx.x * (int64_t)blockDim.x >= nt || TT.n == 0) return;  // block-uniform
+  BvhOut out;
+  const bool live = t0 < nt;
+  const int2 task = K.in ? K.in[live ? t0 : nt - 1] : make_int2((int)(live ? t0 : V - 1), ((TT.nlev - 1) << 26) | 0);
+  const int64_t q = task.x;
+  const int v = sverts[q];
+  const int64_t oq = T.P + q;
+  BvhQuery Q;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    Q.elo[k] = T.elo[3 * oq + k];
+    Q.ehi[k] = T.ehi[3 * oq + k];
+    Q.rlo[k] = Q.rhi[k] = x[3 * (int64_t)v + k];
+    Q.c[k] = T.objmot ? T.objmot[4 * oq + k] : 0.0;
+  }
+  Q.m = T.objmot ? T.objmot[4 * oq + 3] : 0.0;
+  Q.rel = T.objmot != nullptr;
+  Q.gap = gap;
+  int stack[BVH_STACK];
+  int sp = 0;
+  if (live) stack[sp++] = task.y;
+  unsigned n_in = 0, n_leaf = 0;
+  while (sp > 0) {
+    if ((int)(n_in + n_leaf) >= K.budget) {
+      bvh_dump(K, (int)q, stack, sp);
+      break;
+    }
+    const int e = stack[--sp];
+    const int L = e >> 26;
+    const int64_t k = e & ((1 << 26) - 1);
+    if (L == 0) {
+      ++n_leaf;
+      const int64_t s1 = min((int64_t)(k + 1) * BVH_W, TT.n);
+      for (int64_t s = k * BVH_W; s < s1; ++s) {
+        const int t = TT.order[s];
+        const double* tl = T.elo + 3 * (int64_t)t;
+        const double* th = T.ehi + 3 * (int64_t)t;
+        if (boxes_meet(Q.elo, Q.ehi, tl, th) && pt_ref_pass(T, tri, x, v, q, t) &&
+            !rel_safe(T, oq, t, Q.rlo, Q.rhi, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t))
+          bvh_emit(out, v, t, A);
+      }
+    } else {
+      ++n_in;
+      const int64_t c0 = k * BVH_W, c1 = min(c0 + BVH_W, TT.cnt[L - 1]);
+      const BvhNode* base = TT.node + TT.off[L - 1];
+      for (int64_t j = c1 - 1; j >= c0; --j)
+        if (bvh_visit(Q, base[j])) stack[sp++] = ((L - 1) << 26) | (int)j;
+    }
+  }
+  if (stats) {
+    atomicAdd(&g_bvh_stats[0], (unsigned long long)n_in);
+    atomicAdd(&g_bvh_stats[1], (unsigned long long)n_leaf);
+    atomicAdd(&g_bvh_stats[3], 1ull);
+  }
+  __syncwarp();
+  bvh_flush_warp(out, A);
+}
+
+// Edges query the edge tree at sorted positions above their own (each
+// unordered pair once); the leaf predicate is k_hq_edges'.
+__global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64_t E, const int* __restrict__ edge,
+                                                   double gap, PairArgs A, BvhTasks K, bool stats) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = K.in ? (int64_t)*K.n_in : E;
+  if (blockIdx.x * (int64_t)blockDim.x >= nt) return;  // block-uniform
+  BvhOut out;
+  const bool live = t0 < nt;
+  const int2 task = K.in ? K.in[live ? t0 : nt - 1] : make_int2((int)(live ? t0 : E - 1), ((TE.nlev - 1) << 26) | 0);
+  const int64_t si = task.x;
+  const int i = TE.order[si];
+  const int64_t oi = T.F + i;
+  BvhQuery Q;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    Q.elo[k] = T.elo[3 * oi + k];
+    Q.ehi[k] = T.ehi[3 * oi + k];
+    Q.rlo[k] = T.rlo[3 * oi + k];
+    Q.rhi[k] = T.rhi[3 * oi + k];
+    Q.c[k] = T.objmot ? T.objmot[4 * oi + k] : 0.0;
+  }
+  Q.m = T.objmot ? T.objmot[4 * oi + 3] : 0.0;
+  Q.rel = T.objmot != nullptr;
+  Q.gap = gap;
+  const double* fli = T.flo + 3 * oi;
+  const double* fhi = T.fhi + 3 * oi;
+  const int ia = edge[2 * i], ib = edge[2 * i + 1];
+  int stack[BVH_STACK];
+  int sp = 0;
+  if (live) stack[sp++] = task.y;
+  unsigned n_in = 0, n_leaf = 0;
+  while (sp > 0) {
+    if ((int)(n_in + n_leaf) >= K.budget) {
+      bvh_dump(K, (int)si, stack, sp);
+      break;
+    }
+    const int e = stack[--sp];
+    const int L = e >> 26;
+    const int64_t k = e & ((1 << 26) - 1);
+    if (L == 0) {
+      ++n_leaf;
+      const int64_t s1 = min((int64_t)(k + 1) * BVH_W, TE.n);
+      for (int64_t s = max(k * BVH_W, si + 1); s < s1; ++s) {
+        const int j = TE.order[s];
+        const int64_t oj = T.F + j;
+        if (!boxes_meet(Q.elo, Q.ehi, T.elo + 3 * oj, T.ehi + 3 * oj)) continue;
+        const int ja = edge[2 * j], jb = edge[2 * j + 1];
+        const double* flj = T.flo + 3 * oj;
+        const double* fhj = T.fhi + 3 * oj;
+        const bool pass = !(ia == ja || ia == jb || ib == ja || ib == jb) && body_pass(T, ia, ja) &&
+                          fli[0] <= fhj[0] && fli[1] <= fhj[1] && fli[2] <= fhj[2] && flj[0] <= fhi[0] &&
+                          flj[1] <= fhi[1] && flj[2] <= fhi[2] && ref_reach(T.rc, oi, oj) &&
+                          !rel_safe(T, oi, oj, Q.rlo, Q.rhi, T.rlo + 3 * oj, T.rhi + 3 * oj);
+        if (pass) bvh_emit(out, min(i, j), max(i, j), A);
+      }
+    } else {
+      ++n_in;
+      const int64_t c0 = k * BVH_W, c1 = min(c0 + BVH_W, TE.cnt[L - 1]);
+      // a child whose last sorted position is <= si holds no partner
+      int64_t per = BVH_W;  // objects per level-(L-1) node: 8^L
+      for (int l = 1; l < L; ++l) per *= BVH_W;
+      const BvhNode* base = TE.node + TE.off[L - 1];
+      for (int64_t j = c1 - 1; j >= c0; --j) {
+        if ((j + 1) * per - 1 <= si) break;
+        if (bvh_visit(Q, base[j])) stack[sp++] = ((L - 1) << 26) | (int)j;
+      }
+    }
+  }
+  if (stats) {
+    atomicAdd(&g_bvh_stats[0], (unsigned long long)n_in);
+    atomicAdd(&g_bvh_stats[1], (unsigned long long)n_leaf);
+    atomicAdd(&g_bvh_stats[3], 1ull);
+  }
+  __syncwarp();
+  bvh_flush_warp(out, A);
+}
+
+// the class trees: order fixed at first use (by smallest vertex id -- the
+// vertex ids are Morton-renumbered), boxes refit every call
+__global__ void k_min_vertex_key(int64_t n, int per, const int* __restrict__ ids, int* __restrict__ key,
+                                 int* __restrict__ val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int k = ids[per * i];
+  for (int a = 1; a < per; ++a) k = min(k, ids[per * i + a]);
+  key[i] = k;
+  val[i] = (int)i;
+}
+
+static void bvh_shape(BvhTree& T, int64_t n) {
+  T.n = n;
+  int64_t m = (n + BVH_W - 1) / BVH_W, off = 0;
+  T.nlev = 0;
+  for (;;) {
+    if (T.nlev >= BVH_MAX_LEVELS) throw MpError(MP_ERR_CAPACITY, "bvh depth");
+    T.off[T.nlev] = off;
+    T.cnt[T.nlev] = m;
+    off += m;
+    ++T.nlev;
+    if (m <= 1) break;
+    m = (m + BVH_W - 1) / BVH_W;
+  }
+  T.off[T.nlev] = off;
+}
+
+static void bvh_trace_stats(bool on, const char* what, const BvhTree& T) {
+  if (!on) return;
+  unsigned long long h[4];
+  CUDA_CHECK(cudaMemcpyFromSymbol(h, g_bvh_stats, sizeof(h)));
+  fprintf(stderr, "  bvh %s: levels %d, per query %.1f inner / %.1f leaf expansions (%llu queries)\n", what, T.nlev,
+          (double)h[0] / fmax(1.0, (double)h[3]), (double)h[1] / fmax(1.0, (double)h[3]), h[3]);
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  CUDA_CHECK(cudaMemcpyToSymbol(g_bvh_stats, z, sizeof(z)));
+}
+
+// Tight CCD / certificate enumeration through the class trees: the same
+// reference pair list as run_bp's one-pass append (bp.cuh), then the mode's
+// pair kernel.  Returns the pair count, or -1 when the 2^30 list limit was
+// hit (the caller reruns on the grid, whose list-free mode counts in 64 bits).
+template <int MODE>
+static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
+                       int* flag) {
+  const int64_t V = c->V, F = c->F, E = c->E;
+  cudaStream_t st = c->stream;
+  auto& g = c->grid;
+  BvhTree TT{}, TE{};
+  bvh_shape(TT, F);
+  bvh_shape(TE, E);
+  if (!c->bvh_ready) {  // fixed object order, by smallest (Morton-renumbered) vertex id
+    c->bvh_tri_order.ensure(F + 1);
+    c->bvh_edge_order.ensure(E + 1);
+    const int64_t nmax = std::max(F, E) + 1;
+    c->bvh_key.ensure(2 * nmax);
+    c->bvh_val.ensure(nmax);
+    const int bits = bits_for((unsigned long long)std::max<int64_t>(1, c->N));
+    if (F) {
+      k_min_vertex_key<<<grid_for(F, 256), 256, 0, st>>>(F, 3, c->tri, c->bvh_key, c->bvh_val);
+      LAUNCH_CHECK();
+      sort_pairs_i32(c, c->bvh_key, c->bvh_key.p + nmax, c->bvh_val, c->bvh_tri_order, F, bits);
+    }
+    if (E) {
+      k_min_vertex_key<<<grid_for(E, 256), 256, 0, st>>>(E, 2, c->edge, c->bvh_key, c->bvh_val);
+      LAUNCH_CHECK();
+      sort_pairs_i32(c, c->bvh_key, c->bvh_key.p + nmax, c->bvh_val, c->bvh_edge_order, E, bits);
+    }
+    c->bvh_ready = true;
+  }
+  c->bvh_tri_nodes.ensure(5 * (size_t)(TT.off[TT.nlev] + 1));
+  c->bvh_edge_nodes.ensure(5 * (size_t)(TE.off[TE.nlev] + 1));
+  BvhNode* nt = reinterpret_cast<BvhNode*>(c->bvh_tri_nodes.p);
+  BvhNode* ne = reinterpret_cast<BvhNode*>(c->bvh_edge_nodes.p);
+  TT.node = nt; TT.order = c->bvh_tri_order;
+  TE.node = ne; TE.order = c->bvh_edge_order;
+  const BpTables& T = B.T;
+  auto refit = [&](BvhTree& R, BvhNode* nodes, int64_t base) {
+    if (R.n == 0) return;
+    k_bvh_leaves<<<grid_for(R.n, 256), 256, 0, st>>>(R.n, base, R.order, T.rlo, T.rhi, T.elo, T.ehi, T.objmot,
+                                                      nodes);
+    LAUNCH_CHECK();
+    for (int l = 1; l < R.nlev; ++l) {
+      k_bvh_up<<<grid_for(R.cnt[l - 1], 256), 256, 0, st>>>(R.cnt[l - 1], nodes + R.off[l - 1], nodes + R.off[l]);
+      LAUNCH_CHECK();
+    }
+  };
+  BpTrace tr(st);
+  refit(TT, nt, 0);
+  refit(TE, ne, F);
+  tr.lap("refit");
+  // task lists: [class][ping-pong]; counters: per class and buffer (count, overflow)
+  if (c->bvh_tasks.n < 4 * (size_t)BVH_TASKS0) c->bvh_tasks.ensure(4 * (size_t)BVH_TASKS0);
+  c->bvh_task_cnt.ensure(8);
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), st));
+    O.counter = c->counters.p;
+    if (g.pa.n < 1024) { g.pa.ensure(1 << 16); g.pb.ensure(1 << 16); }
+    if (g.ea.n < 1024) { g.ea.ensure(1 << 16); g.eb.ensure(1 << 16); }
+    int* cnt = c->counters.p + 8;  // [8] PT, [9] EE appended, [10] overflow flag
+    CUDA_CHECK(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), st));
+    const int64_t cap_pt = (int64_t)std::min(g.pa.n, g.pb.n), cap_ee = (int64_t)std::min(g.ea.n, g.eb.n);
+    const int64_t tcap = (int64_t)(c->bvh_tasks.n / 4);
+    int2* tbuf[2][2];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) tbuf[a][b] = reinterpret_cast<int2*>(c->bvh_tasks.p) + (2 * a + b) * tcap;
+    int* tcnt = c->bvh_task_cnt.p;  // [2 * (2 * class + buffer)] count, [+1] overflow
+    bool task_overflow = false;
+    if (!B.empty) {
+      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr, g.pa, g.pb, cnt, cap_pt};
+      PairArgs Ae = A;
+      Ae.app_a = g.ea; Ae.app_b = g.eb; Ae.app_cnt = cnt + 1; Ae.app_cap = cap_ee; Ae.app_ee = 1;
+      const bool do_pt = V && F, do_ee = E > 1;
+      int64_t n_task[2] = {do_pt ? V : 0, do_ee ? E : 0};
+      for (int round = 0; n_task[0] || n_task[1]; ++round) {
+        const int cur = round & 1, nxt = cur ^ 1;
+        CUDA_CHECK(cudaMemsetAsync(tcnt + 4 * 0 + 2 * nxt, 0, 2 * sizeof(int), st));
+        CUDA_CHECK(cudaMemsetAsync(tcnt + 4 * 1 + 2 * nxt, 0, 2 * sizeof(int), st));
+        if (n_task[0]) {
+          BvhTasks K{round ? tbuf[0][cur] : nullptr, tcnt + 2 * cur, tbuf[0][nxt], tcnt + 2 * nxt, tcap, BVH_BUDGET};
+          k_bvh_points<<<grid_for(n_task[0], 128), 128, 0, st>>>(T, TT, V, c->sverts, c->tri, x, B.filter_gap, A, K,
+                                                                   tr.on);
+          LAUNCH_CHECK();
+          tr.lap("points");
+          bvh_trace_stats(tr.on, "points", TT);
+        }
+        if (n_task[1]) {
+          BvhTasks K{round ? tbuf[1][cur] : nullptr, tcnt + 4 + 2 * cur, tbuf[1][nxt], tcnt + 4 + 2 * nxt, tcap,
+                     BVH_BUDGET};
+          k_bvh_edges<<<grid_for(n_task[1], 128), 128, 0, st>>>(T, TE, E, c->edge, B.filter_gap, Ae, K, tr.on);
+          LAUNCH_CHECK();
+          tr.lap("edges");
+          bvh_trace_stats(tr.on, "edges", TE);
+        }
+        int h[8];
+        CUDA_CHECK(cudaMemcpyAsync(h, tcnt, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        sync_stream(c);
+        if (h[2 * nxt + 1] || h[4 + 2 * nxt + 1]) {
+          task_overflow = true;
+          break;
+        }
+        n_task[0] = h[2 * nxt];
+        n_task[1] = h[4 + 2 * nxt];
+        if (tr.on && (n_task[0] || n_task[1]))
+          fprintf(stderr, "  bvh round %d hands on %lld + %lld tasks\n", round + 1, (long long)n_task[0],
+                  (long long)n_task[1]);
+      }
+      if (!task_overflow) {
+        k_pairs_app<MODE><<<8 * 148, 256, 0, st>>>(cnt, cap_pt, cap_ee, g.pa, g.pb, g.ea, g.eb, A);
+        LAUNCH_CHECK();
+        tr.lap("pairs");
+      }
+    }
+    if (task_overflow) {  // grow the task lists and start over (the pair list is rebuilt from scratch)
+      c->bvh_tasks.ensure(8 * (size_t)tcap);
+      continue;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (c->rb_extra)  // the caller's scalar rides on this readback (h_scal[0])
+      CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync_stream(c);
+    if (c->h_cnt[7]) return -1;
+    const int64_t n_pt = c->h_cnt[5], n_ee = c->h_cnt[6];
+    if (n_pt > cap_pt || n_ee > cap_ee) {  // grow and rerun (minima / flags are idempotent)
+      if (n_pt > cap_pt) { g.pa.ensure((size_t)(n_pt * 1.25) + 1024); g.pb.ensure((size_t)(n_pt * 1.25) + 1024); }
+      if (n_ee > cap_ee) { g.ea.ensure((size_t)(n_ee * 1.25) + 1024); g.eb.ensure((size_t)(n_ee * 1.25) + 1024); }
+      continue;
+    }
+    if (flag) *flag = c->h_cnt[1];
+    return n_pt + n_ee;
+  }
+  throw MpError(MP_ERR_CAPACITY, "bvh pair list capacity retry failed");
+}

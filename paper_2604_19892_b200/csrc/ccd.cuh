@@ -12,6 +12,7 @@
 #pragma once
 
 #include "contact.cuh"
+#include "bvh.cuh"
 #include "exact.cuh"
 
 #define CCD_S 0.1
@@ -642,6 +643,17 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
                            double* x_out, bool exact_set = false) {
   CcdResult R{1.0, true, 0};
   cudaStream_t st = c->stream;
+  // MP_CCD_TRACE=1: per-call host timings of the CCD phases on stderr
+  static const bool trace = getenv("MP_CCD_TRACE") != nullptr;
+  auto tr0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what, int64_t n) {
+    if (!trace) return;
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "ccd %-10s %9.3f ms  n=%lld\n", what, std::chrono::duration<double, std::milli>(t - tr0).count(),
+            (long long)n);
+    tr0 = t;
+  };
   k_fill<<<grid_for(c->D, 256), 256, 0, st>>>(c->alpha_d, c->D, 1.0);
   LAUNCH_CHECK();
   double* d_min = c->dscal.p + 41;
@@ -665,8 +677,27 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       infl = c->infl;
     }
     if (!exact_set && c->ccd_prefilter) obj_motion(c, p, nullptr);
-    BpGrid B = build_bp(c, x, pinf, 0.0, infl, bodies ? 1 : 0);
+    lap("infl", 0);
+    // the motion-aware BVH (bvh.cuh) for the tight single-centre passes; the
+    // grid for the exact set, the per-body passes and the >2^30 fallback
+    const int gmode = (exact_set || bodies || c->ccd_bvh == 0) ? BP_GRID_ALWAYS
+                      : (c->ccd_bvh == 1 ? BP_GRID_NONE : BP_GRID_AUTO);
+    BpGrid B = build_bp(c, x, pinf, 0.0, infl, bodies ? 1 : 0, gmode);
+    lap("grid", 0);
     if (!exact_set && c->ccd_prefilter) B.T.objmot = c->obj_mot.p;
+    // one enumeration + pair pass of MODE over the boxes of G (grid rebuilt
+    // for the list-free rerun when the BVH's one-pass list would pass 2^30)
+    auto enumerate = [&](auto mode_tag, BpGrid& G, BpOut O, const double* inf, int* fl) -> int64_t {
+      constexpr int M = decltype(mode_tag)::value;
+      if (!G.has_grid) {
+        const int64_t n = run_bvh<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
+        if (n >= 0) return n;
+        const double* mot = G.T.objmot;
+        G = build_bp(c, x, pinf, 0.0, inf, 0, BP_GRID_ALWAYS);
+        G.T.objmot = mot;
+      }
+      return run_bp<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
+    };
     ContactParams CP{};
     CcdParams CC{p, c->cfg.alpha_l, c->bs};
     if (exact_set && c->ccd_verts.n < 4096) {
@@ -681,7 +712,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       O.alpha_d = c->alpha_d;
       O.min_alpha = d_min;
       c->rb_extra = d_min;  // read back with run_bp's counters: no extra sync
-      int64_t n = run_bp<BP_CCD>(c, x, B, O, CP, CC, &cert_fail_p);
+      int64_t n = enumerate(std::integral_constant<int, BP_CCD>{}, B, O, infl, &cert_fail_p);
       c->rb_extra = nullptr;
       if (!exact_set || n <= O.cap) {
         R.n_pairs = n;
@@ -706,6 +737,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       if (attempt == 3) throw MpError(MP_ERR_CAPACITY, "ccd pair capacity retry failed");
     }
     R.min_alpha = c->h_scal[0];
+    lap("pairs", R.n_pairs);
     if (per_subdomain && R.n_pairs > 0) {
       if (R.min_alpha == 1.0) {
         // every alpha_d is 1: p_mix == p, the certificate was evaluated inline
@@ -739,13 +771,15 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
         LAUNCH_CHECK();
         if (c->ccd_local) local_infl(c, x, p, c->alpha_d);
         if (c->ccd_prefilter) obj_motion(c, p, c->alpha_d);
-        BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl);
+        BpGrid B2 = build_bp(c, x, pinf, 0.0, c->infl, 0, gmode);
         if (c->ccd_prefilter) B2.T.objmot = c->obj_mot.p;
         BpOut O{};
         O.alpha_d = c->alpha_d;
         int fail = 0;
-        run_bp<BP_CERT>(c, x, B2, O, CP, CC, &fail);
+        lap("cert-grid", 0);
+        const int64_t nc = enumerate(std::integral_constant<int, BP_CERT>{}, B2, O, c->infl, &fail);
         R.certified = fail == 0;
+        lap("cert", nc);
       }
     }
   }

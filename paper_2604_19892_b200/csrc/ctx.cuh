@@ -252,7 +252,13 @@ struct mp_ctx {
   DBuf<double> obj_mot;              // per-object motion (c, m) for the exact CCD prefilter
   bool ccd_prefilter = true;         // MP_OPT_CCD_PREFILTER
   bool ccd_bodies = false;           // MP_OPT_CCD_BODIES: two-pass per-body tight enumeration
-  bool ccd_local = true;             // MP_OPT_CCD_LOCAL: per-subdomain motion centres (ccd.cuh local_infl)
+  int ccd_bvh = 2;                   // MP_OPT_CCD_BVH: tight CCD enumeration 0 grid, 1 BVH (bvh.cuh), 2 per call
+  bool bvh_ready = false;            // class orders built (fixed topology)
+  DBuf<int> bvh_tri_order, bvh_edge_order, bvh_key, bvh_val;
+  DBuf<float4> bvh_tri_nodes, bvh_edge_nodes;  // BvhNode = 5 float4
+  DBuf<int2> bvh_tasks;              // 4 task lists (class x ping-pong) of the load-balanced traversal
+  DBuf<int> bvh_task_cnt;
+  bool ccd_local = false;            // MP_OPT_CCD_LOCAL: per-subdomain motion centres (ccd.cuh local_infl)
   DBuf<double> sub_cen, sub_box, sub_delta, infl2;
   DBuf<unsigned long long> sub_key, sub_key2;
   DBuf<int> sub_id, sub_id2;

@@ -108,6 +108,30 @@ def test_c2_ccd_clamped(c2):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("scale", [1.0, 40.0, 400.0])
+def test_c2_ccd_bvh_vs_grid(c2, scale):
+    """MP_OPT_CCD_BVH (14): the motion-aware BVH enumeration emits the grid's
+    pair set (same count) and so the same alpha_d, minimum, certificate and
+    x_new -- at bench scale, up to a 400x restart step (boxes ~ the scene)."""
+    g, _, ctx = c2
+    rng = np.random.default_rng(7)
+    p0 = scale * g["p"]
+    cases = [p0, p0 + 0.3 * np.abs(p0).max() * rng.standard_normal(p0.shape)]
+    try:
+        for p in cases:
+            out = []
+            for bvh in (0, 1):
+                ctx.set_option(14, bvh)
+                out.append(ctx.ccd(g["x0"], p, exact_set=False))
+            a, b = out
+            assert a[4] == b[4]  # reference pairs after the exact filters
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            assert a[2] == b[2] and a[3] == b[3]
+    finally:
+        ctx.set_option(14, 2)
+
+
+@pytest.mark.gpu
 def test_c2_update_branch(c2):
     """The non-rebuild branch at x1 against the x0 snapshot: classify_all,
     select_top_k (K=8), build_update (Sparse-Input Woodbury), then z and HVP

@@ -125,8 +125,10 @@ def test_apply_overlap_same_bits():
 def test_ccd_prefilter_and_bodies_same_results(name):
     """MP_OPT_CCD_PREFILTER (11, exact relative-motion pair prefilter),
     MP_OPT_CCD_BODIES (12, two-pass per-body enumeration) and
-    MP_OPT_CCD_LOCAL (13, per-subdomain motion centres): the same alpha_d,
-    minimum, certificate and x_new as the plain tight enumeration."""
+    MP_OPT_CCD_LOCAL (13, per-subdomain motion centres) and MP_OPT_CCD_BVH
+    (14, motion-aware BVH instead of the grid): the same alpha_d, minimum,
+    certificate and x_new as the plain tight enumeration, and the BVH the
+    grid's pair count."""
     g = load_golden(name)
     scene = scene_from_golden(g)
     ctx = scene.context(golden_config(g))
@@ -136,16 +138,22 @@ def test_ccd_prefilter_and_bodies_same_results(name):
         cases.append((x, 4.0 * p + 0.5 * np.abs(p).max() * rng.standard_normal(p.shape)))
     try:
         for x, p in cases:
-            out = []
-            for pre, bod, loc in ((0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0), (0, 0, 1), (1, 0, 1)):
+            out = {}
+            for pre, bod, loc, bvh in ((0, 0, 0, 0), (1, 0, 0, 0), (0, 1, 0, 0), (1, 1, 0, 0), (0, 0, 1, 0),
+                                       (1, 0, 1, 0), (0, 0, 0, 1), (1, 0, 0, 1), (1, 0, 1, 1)):
                 ctx.set_option(11, pre)
                 ctx.set_option(12, bod)
                 ctx.set_option(13, loc)
-                out.append(ctx.ccd(x, p, exact_set=False))
-            for o in out[1:]:
-                assert np.array_equal(out[0][0], o[0]) and np.array_equal(out[0][1], o[1])
-                assert out[0][2] == o[2] and out[0][3] == o[3]
+                ctx.set_option(14, bvh)
+                out[(pre, bod, loc, bvh)] = ctx.ccd(x, p, exact_set=False)
+            ref = out[(0, 0, 0, 0)]
+            for o in out.values():
+                assert np.array_equal(ref[0], o[0]) and np.array_equal(ref[1], o[1])
+                assert ref[2] == o[2] and ref[3] == o[3]
+            assert out[(0, 0, 0, 1)][4] == out[(0, 0, 0, 0)][4]
+            assert out[(1, 0, 0, 1)][4] == out[(1, 0, 0, 0)][4]
     finally:
         ctx.set_option(11, 1)
         ctx.set_option(12, 0)
-        ctx.set_option(13, 1)
+        ctx.set_option(13, 0)
+        ctx.set_option(14, 2)

@@ -1,5 +1,6 @@
 """C5 frame 1 from rest with stage timers: where do the seconds go?"""
 import json
+import os
 import sys
 
 import numpy as np
@@ -11,6 +12,8 @@ scene = scenes.c5_puffer_balls()
 v0 = scenes.c5_puffer_v0(scene)
 x0 = scene.mesh.rest_positions.ravel().copy()
 ctx = scene.context(solver.SolverConfig(iter_max=int(sys.argv[1]) if len(sys.argv) > 1 else 20, coarse_block=32))
+if os.environ.get("MP_CCD_BVH"):  # 0 grid, 1 BVH, 2 per call (default)
+    ctx.set_option(14, int(os.environ["MP_CCD_BVH"]))
 for rep in range(2):
     ctx.set_state(x0, v0)
     ctx.stage_timing(True)
