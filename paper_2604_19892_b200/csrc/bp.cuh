@@ -933,12 +933,39 @@ struct BpGrid {
   bool empty = true;
   bool has_grid = false;  // false: boxes / filters only (the BVH enumeration, bvh.cuh)
   double filter_gap = 0.0;  // the reference filter gap with a rounding margin (bvh.cuh node tests)
+  double crowd = 0.0;       // BP_GRID_AUTO: the crowding probe when it ran (> BP_CROWD_LIMIT: a timed choice)
 };
 
 enum { BP_GRID_NONE = 0, BP_GRID_ALWAYS = 1, BP_GRID_AUTO = 2 };
-// measured at C5 (bvh.cuh): the grid wins below ~1.5x (10 vs 28 ms per CCD
-// call), the BVH above (49 vs 615 ms at 4.4x, 0.6 vs 15.5 s at 18x)
+// BP_GRID_AUTO: when the enumeration boxes average more than BP_AUTO_RATIO
+// times the raw ones, the grid is built and its crowding measured -- sum
+// over cells of (objects in the cell)^2, per object, ~ the box tests per
+// query.  Up to BP_CROWD_LIMIT the grid enumerates.  Past it the cheaper
+// method depends on the motion: where the relative-motion prefilter rejects
+// most box-overlapping pairs (bodies moving coherently: C5 restart
+// directions, crowd 250-60000) the BVH prunes whole subtrees (0.05-0.13 s
+// vs the grid's 0.6-15.5 s); where most of them pass (the C3 twist, up to
+// 2^31 pairs) the grid's warp-wide cell scans are 1.5-3x faster.  So
+// crowded calls are timed: each method's cost per unit of crowding is kept
+// as a running mean and the cheaper one runs, the other re-tried every
+// BP_REPROBE crowded calls -- the grid only below BP_GRID_TRY, where a wrong
+// guess costs at most ~0.2 s.  (Both emit the same pair set: timing only.)
 #define BP_AUTO_RATIO 1.6
+#define BP_CROWD_LIMIT 100.0
+#define BP_REPROBE 32
+#define BP_GRID_TRY 1000.0
+
+__global__ void k_cell_crowd(int64_t ncell, const int* __restrict__ a, const int* __restrict__ b,
+                             const int* __restrict__ c, unsigned long long* __restrict__ out) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncell; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long n = (unsigned long long)(a[i] + b[i] + c[i]);
+    s += n * n;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
 
 // Everything one broad-phase call at (x, mb, d_hat) needs: boxes, levels,
 // reference cell ranges and the per-level cell tables of triangles / edges /
@@ -1000,18 +1027,20 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
     for (int k = 0; k < 3; ++k) amax = fmax(amax, fmax(fabs(mn[k]), fabs(mx[k])));
     B.filter_gap = gap * (1.0 + 1e-9) + 1e-15 * (std::isfinite(amax) ? amax : 0.0);
   }
-  // the grid's box tests grow with the cube of the enumeration-to-raw extent
-  // ratio; past BP_AUTO_RATIO the BVH (bvh.cuh) enumerates instead
-  const bool want_grid = grid_mode == BP_GRID_ALWAYS || (grid_mode == BP_GRID_AUTO && !(ext > BP_AUTO_RATIO * rext));
-  if (!want_grid) {
+  auto boxes_only = [&]() {  // the BVH's inputs: boxes, filters, reference cell ranges
     BpTables& T = B.T;
     T.rc = g.rc;
     T.flo = c->box_flo; T.fhi = c->box_fhi;
     T.elo = c->box_elo; T.ehi = c->box_ehi;
     T.rlo = c->box_rlo; T.rhi = c->box_rhi;
     B.empty = false;
+    B.has_grid = false;
+  };
+  if (grid_mode == BP_GRID_NONE) {
+    boxes_only();
     return B;
   }
+  const bool probe = grid_mode == BP_GRID_AUTO && ext > BP_AUTO_RATIO * rext;
   B.has_grid = true;
   // level 0: about the mean primitive extent, at most ~4M cells
   double span = fmax(fmax(mx[0] - mn[0], mx[1] - mn[1]), mx[2] - mn[2]);
@@ -1076,6 +1105,34 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
   k_entry_hist<<<grid_for(total_cap, 256), 256, 0, st>>>(total_dev, nobj, F, P, G, c->cell_off, g.level, c->box_elo,
                                                          c->box_ehi, g.ecell, g.tri_cnt, g.edge_cnt, g.pt_cnt);
   LAUNCH_CHECK();
+  if (probe) {
+    c->crowd_dev.ensure(1);
+    CUDA_CHECK(cudaMemsetAsync(c->crowd_dev.p, 0, sizeof(unsigned long long), st));
+    k_cell_crowd<<<4 * 148, 256, 0, st>>>((int64_t)ncell, g.tri_cnt, g.edge_cnt, g.pt_cnt, c->crowd_dev);
+    LAUNCH_CHECK();
+    unsigned long long sq = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&sq, c->crowd_dev.p, sizeof(sq), cudaMemcpyDeviceToHost, st));
+    sync_stream(c);
+    const double crowd = (double)sq / (double)std::max<int64_t>(1, nobj);
+    if (getenv("MP_BP_TRACE"))
+      fprintf(stderr, "  bp crowd %.1f (enumeration / raw extent %.2f)\n", crowd, ext / fmax(rext, 1e-300));
+    if (crowd > BP_CROWD_LIMIT) {
+      B.crowd = crowd;
+      const double* cost = c->enum_cost;  // [0] grid, [1] BVH: ms per unit of crowding, < 0 unknown
+      // the grid's cost grows with the crowding, the BVH's much less: the
+      // grid is only tried (unknown cost, or a re-probe) below BP_GRID_TRY
+      const bool may_try_grid = crowd < BP_GRID_TRY;
+      bool bvh;
+      if (cost[1] < 0.0) bvh = true;
+      else if (cost[0] < 0.0) bvh = !may_try_grid;
+      else bvh = cost[1] <= cost[0];
+      if (++c->n_crowded % BP_REPROBE == 0 && (!bvh || may_try_grid)) bvh = !bvh;
+      if (bvh) {
+        boxes_only();
+        return B;
+      }
+    }
+  }
   exclusive_scan(c, g.tri_cnt, g.tri_start, ncell + 1);
   exclusive_scan(c, g.edge_cnt, g.edge_start, ncell + 1);
   exclusive_scan(c, g.pt_cnt, g.pt_start, ncell + 1);

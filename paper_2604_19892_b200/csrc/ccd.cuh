@@ -687,16 +687,29 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
     if (!exact_set && c->ccd_prefilter) B.T.objmot = c->obj_mot.p;
     // one enumeration + pair pass of MODE over the boxes of G (grid rebuilt
     // for the list-free rerun when the BVH's one-pass list would pass 2^30)
+    // (crowded calls are timed: bp.cuh BP_GRID_AUTO keeps each method's cost)
     auto enumerate = [&](auto mode_tag, BpGrid& G, BpOut O, const double* inf, int* fl) -> int64_t {
       constexpr int M = decltype(mode_tag)::value;
+      const auto t0 = std::chrono::steady_clock::now();
+      const int method = G.has_grid ? 0 : 1;
+      int64_t n = -1;
       if (!G.has_grid) {
-        const int64_t n = run_bvh<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
-        if (n >= 0) return n;
-        const double* mot = G.T.objmot;
-        G = build_bp(c, x, pinf, 0.0, inf, 0, BP_GRID_ALWAYS);
-        G.T.objmot = mot;
+        n = run_bvh<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
+        if (n < 0) {
+          const double* mot = G.T.objmot;
+          G = build_bp(c, x, pinf, 0.0, inf, 0, BP_GRID_ALWAYS);
+          G.T.objmot = mot;
+        }
       }
-      return run_bp<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
+      if (n < 0) n = run_bp<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
+      if (G.crowd > 0.0) {  // run_bvh / run_bp end on a host sync: the interval is the enumeration's
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const double cost = ms / G.crowd;
+        double& e = c->enum_cost[method];
+        e = e < 0.0 ? cost : 0.5 * (e + cost);
+        if (trace) fprintf(stderr, "ccd crowded  %s %.3f ms (crowd %.1f)\n", method ? "bvh" : "grid", ms, G.crowd);
+      }
+      return n;
     };
     ContactParams CP{};
     CcdParams CC{p, c->cfg.alpha_l, c->bs};

@@ -258,6 +258,9 @@ struct mp_ctx {
   DBuf<float4> bvh_tri_nodes, bvh_edge_nodes;  // BvhNode = 5 float4
   DBuf<int2> bvh_tasks;              // 4 task lists (class x ping-pong) of the load-balanced traversal
   DBuf<int> bvh_task_cnt;
+  DBuf<unsigned long long> crowd_dev;  // grid crowding probe (bp.cuh BP_GRID_AUTO)
+  double enum_cost[2] = {-1.0, -1.0};  // crowded CCD enumerations: ms per unit of crowding, grid / BVH
+  int64_t n_crowded = 0;
   bool ccd_local = false;            // MP_OPT_CCD_LOCAL: per-subdomain motion centres (ccd.cuh local_infl)
   DBuf<double> sub_cen, sub_box, sub_delta, infl2;
   DBuf<unsigned long long> sub_key, sub_key2;
