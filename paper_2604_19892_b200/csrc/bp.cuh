@@ -735,6 +735,43 @@ __device__ __forceinline__ void hq_finish(bool is_pt, int lane, int n, int* cnt,
   }
 }
 
+// A warp walks the entries of up to 32 consecutive cells FLATTENED: lane t
+// of round r takes entry r*32 + t of the batch's concatenated ranges (an
+// exclusive warp scan of the cell sizes, then a 5-step shuffle search for
+// the lane's cell), so a batch of small cells costs one memory round trip
+// per 32 entries instead of one per cell.  The order -- cells ascending,
+// entries ascending -- is the per-cell walk's, so ordered lists keep their
+// order.
+struct CellBatch {
+  int my0;    // this lane's cell: first entry
+  int excl;   // entries of the batch's cells before this lane's
+  int total;  // entries in the batch
+};
+
+__device__ __forceinline__ CellBatch cell_batch(int my0, int my1) {
+  const int lane = threadIdx.x & 31;
+  const int cnt = my1 - my0;
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(WARP_FULL, incl, d);
+    if (lane >= d) incl += y;
+  }
+  return CellBatch{my0, incl - cnt, __shfl_sync(WARP_FULL, incl, 31)};
+}
+
+// the entry at flattened position f (all 32 lanes call; f < total for a
+// valid result)
+__device__ __forceinline__ int batch_entry(const CellBatch& b, int f) {
+  int c = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int v = __shfl_sync(WARP_FULL, b.excl, c + step);
+    if (v <= f) c += step;
+  }
+  return __shfl_sync(WARP_FULL, b.my0, c) + (f - __shfl_sync(WARP_FULL, b.excl, c));
+}
+
 // points query the triangles of every level >= their own
 template <int EM>
 __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const int* __restrict__ sverts,
@@ -758,16 +795,14 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_query_span(T.G, l, pl, ph, c0, c1);
-    // the span's cells in (a, b, c) order; every 32 cells each lane loads
-    // one cell's entry range (one memory round trip per 32 cells instead of
-    // one per cell) and the warp walks them in order
+    // the span's cells in (a, b, c) order, 32 at a time: each lane loads one
+    // cell's entry range, the warp walks the batch's entries flattened
     const int nb_ = c1[1] - c0[1] + 1, nc_ = c1[2] - c0[2] + 1;
     const int ncell_ = (c1[0] - c0[0] + 1) * nb_ * nc_;
-    int my0 = 0, my1 = 0;
-    for (int ci_ = 0; ci_ < ncell_; ++ci_) {
-          if ((ci_ & 31) == 0) {
-            my0 = my1 = 0;
-            const int idx = ci_ + lane;
+    for (int cb_ = 0; cb_ < ncell_; cb_ += 32) {
+          int my0 = 0, my1 = 0;
+          {
+            const int idx = cb_ + lane;
             if (idx < ncell_) {
               const int r = idx % (nb_ * nc_);
               const int cell = hg_cell(T.G, l, c0[0] + idx / (nb_ * nc_), c0[1] + r / nc_, c0[2] + r % nc_);
@@ -775,12 +810,13 @@ __global__ void __launch_bounds__(128) k_hq_points(BpTables T, int64_t V, const 
               my1 = T.tri_start[cell + 1];
             }
           }
-          const int e0 = __shfl_sync(WARP_FULL, my0, ci_ & 31), e1 = __shfl_sync(WARP_FULL, my1, ci_ & 31);
-          for (int base = e0; base < e1; base += 32) {
-            const int e = base + lane;
+          const CellBatch cbt = cell_batch(my0, my1);
+          for (int base = 0; base < cbt.total; base += 32) {
+            const int f = base + lane;
+            const int e = batch_entry(cbt, f < cbt.total ? f : cbt.total - 1);
             bool pass = false;
             int t = 0;
-            if (e < e1) {
+            if (f < cbt.total) {
               t = T.tri_ent[e];
               const double* tl = T.tri_box + 6 * (int64_t)e;
               pass = boxes_meet(pl, ph, tl, tl + 3) &&
@@ -817,16 +853,14 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_query_span(T.G, l, tl, th, c0, c1);
-    // the span's cells in (a, b, c) order; every 32 cells each lane loads
-    // one cell's entry range (one memory round trip per 32 cells instead of
-    // one per cell) and the warp walks them in order
+    // the span's cells in (a, b, c) order, 32 at a time: each lane loads one
+    // cell's entry range, the warp walks the batch's entries flattened
     const int nb_ = c1[1] - c0[1] + 1, nc_ = c1[2] - c0[2] + 1;
     const int ncell_ = (c1[0] - c0[0] + 1) * nb_ * nc_;
-    int my0 = 0, my1 = 0;
-    for (int ci_ = 0; ci_ < ncell_; ++ci_) {
-          if ((ci_ & 31) == 0) {
-            my0 = my1 = 0;
-            const int idx = ci_ + lane;
+    for (int cb_ = 0; cb_ < ncell_; cb_ += 32) {
+          int my0 = 0, my1 = 0;
+          {
+            const int idx = cb_ + lane;
             if (idx < ncell_) {
               const int r = idx % (nb_ * nc_);
               const int cell = hg_cell(T.G, l, c0[0] + idx / (nb_ * nc_), c0[1] + r / nc_, c0[2] + r % nc_);
@@ -834,12 +868,13 @@ __global__ void __launch_bounds__(128) k_hq_tris(BpTables T, int64_t F, const in
               my1 = T.pt_start[cell + 1];
             }
           }
-          const int e0 = __shfl_sync(WARP_FULL, my0, ci_ & 31), e1 = __shfl_sync(WARP_FULL, my1, ci_ & 31);
-          for (int base = e0; base < e1; base += 32) {
-            const int e = base + lane;
+          const CellBatch cbt = cell_batch(my0, my1);
+          for (int base = 0; base < cbt.total; base += 32) {
+            const int f = base + lane;
+            const int e = batch_entry(cbt, f < cbt.total ? f : cbt.total - 1);
             bool pass = false;
             int v = 0;
-            if (e < e1) {
+            if (f < cbt.total) {
               const int q = T.pt_ent[e];
               const double* pl = T.pt_box + 6 * (int64_t)e;
               v = sverts[q];
@@ -880,16 +915,14 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
     if (!((mask >> l) & 1u)) continue;
     int c0[3], c1[3];
     hg_query_span(T.G, l, il, ih, c0, c1);
-    // the span's cells in (a, b, c) order; every 32 cells each lane loads
-    // one cell's entry range (one memory round trip per 32 cells instead of
-    // one per cell) and the warp walks them in order
+    // the span's cells in (a, b, c) order, 32 at a time: each lane loads one
+    // cell's entry range, the warp walks the batch's entries flattened
     const int nb_ = c1[1] - c0[1] + 1, nc_ = c1[2] - c0[2] + 1;
     const int ncell_ = (c1[0] - c0[0] + 1) * nb_ * nc_;
-    int my0 = 0, my1 = 0;
-    for (int ci_ = 0; ci_ < ncell_; ++ci_) {
-          if ((ci_ & 31) == 0) {
-            my0 = my1 = 0;
-            const int idx = ci_ + lane;
+    for (int cb_ = 0; cb_ < ncell_; cb_ += 32) {
+          int my0 = 0, my1 = 0;
+          {
+            const int idx = cb_ + lane;
             if (idx < ncell_) {
               const int r = idx % (nb_ * nc_);
               const int cell = hg_cell(T.G, l, c0[0] + idx / (nb_ * nc_), c0[1] + r / nc_, c0[2] + r % nc_);
@@ -897,12 +930,13 @@ __global__ void __launch_bounds__(128) k_hq_edges(BpTables T, int64_t E, const i
               my1 = T.edge_start[cell + 1];
             }
           }
-          const int e0 = __shfl_sync(WARP_FULL, my0, ci_ & 31), e1 = __shfl_sync(WARP_FULL, my1, ci_ & 31);
-          for (int base = e0; base < e1; base += 32) {
-            const int e = base + lane;
+          const CellBatch cbt = cell_batch(my0, my1);
+          for (int base = 0; base < cbt.total; base += 32) {
+            const int f = base + lane;
+            const int e = batch_entry(cbt, f < cbt.total ? f : cbt.total - 1);
             bool pass = false;
             int j = 0;
-            if (e < e1) {
+            if (f < cbt.total) {
               j = T.edge_ent[e];
               const double* jl = T.edge_box + 6 * (int64_t)e;
               pass = !(l == lv && j <= (int)i) && boxes_meet(il, ih, jl, jl + 3);
@@ -934,9 +968,20 @@ struct BpGrid {
   bool has_grid = false;  // false: boxes / filters only (the BVH enumeration, bvh.cuh)
   double filter_gap = 0.0;  // the reference filter gap with a rounding margin (bvh.cuh node tests)
   double crowd = 0.0;       // BP_GRID_AUTO: the crowding probe when it ran (> BP_CROWD_LIMIT: a timed choice)
+  int crowd_bucket = 0;     // ilogb(crowd)
 };
 
 enum { BP_GRID_NONE = 0, BP_GRID_ALWAYS = 1, BP_GRID_AUTO = 2 };
+// Crowded calls: the measured times of each method per log2 bucket of the
+// crowding (ctx enum_ms).  The grid's time grows ~linearly with the
+// crowding (extrapolated from the nearest lower bucket it ran in), the
+// BVH's much less (nearest bucket it ran in).  Unknown BVH -> BVH (bounded);
+// unknown grid -> tried only below BP_GRID_TRY; else the faster estimate,
+// with the other re-tried every BP_REPROBE crowded calls when it is not
+// predicted to be more than 4x slower.
+#define BP_BUCKETS 32
+static bool choose_bvh(mp_ctx* c, int k, double crowd);
+
 // BP_GRID_AUTO: when the enumeration boxes average more than BP_AUTO_RATIO
 // times the raw ones, the grid is built and its crowding measured -- sum
 // over cells of (objects in the cell)^2, per object, ~ the box tests per
@@ -946,14 +991,35 @@ enum { BP_GRID_NONE = 0, BP_GRID_ALWAYS = 1, BP_GRID_AUTO = 2 };
 // directions, crowd 250-60000) the BVH prunes whole subtrees (0.05-0.13 s
 // vs the grid's 0.6-15.5 s); where most of them pass (the C3 twist, up to
 // 2^31 pairs) the grid's warp-wide cell scans are 1.5-3x faster.  So
-// crowded calls are timed: each method's cost per unit of crowding is kept
-// as a running mean and the cheaper one runs, the other re-tried every
-// BP_REPROBE crowded calls -- the grid only below BP_GRID_TRY, where a wrong
-// guess costs at most ~0.2 s.  (Both emit the same pair set: timing only.)
+// crowded calls are timed and chosen by choose_bvh below (the grid is only
+// tried blind below BP_GRID_TRY, where a wrong guess costs at most ~0.2 s).
+// Both emit the same pair set: the choice changes timing only.
 #define BP_AUTO_RATIO 1.6
 #define BP_CROWD_LIMIT 100.0
 #define BP_REPROBE 32
 #define BP_GRID_TRY 1000.0
+
+static bool choose_bvh(mp_ctx* c, int k, double crowd) {
+  const double* g = c->enum_ms.ms[0];
+  const double* b = c->enum_ms.ms[1];
+  double tg = -1.0, tb = -1.0;
+  for (int j = k; j >= 0 && tg < 0.0; --j)
+    if (g[j] >= 0.0) tg = g[j] * ldexp(1.0, k - j);
+  for (int d = 0; d < BP_BUCKETS && tb < 0.0; ++d) {
+    if (k - d >= 0 && b[k - d] >= 0.0) tb = b[k - d];
+    else if (k + d < BP_BUCKETS && b[k + d] >= 0.0) tb = b[k + d];
+  }
+  const bool may_try_grid = crowd < BP_GRID_TRY;
+  bool bvh;
+  if (tb < 0.0) bvh = true;
+  else if (tg < 0.0) bvh = !may_try_grid;
+  else bvh = tb <= tg;
+  if (++c->n_crowded % BP_REPROBE == 0) {
+    if (bvh && (may_try_grid || (tg >= 0.0 && tg < 4.0 * tb))) bvh = false;
+    else if (!bvh) bvh = true;
+  }
+  return bvh;
+}
 
 __global__ void k_cell_crowd(int64_t ncell, const int* __restrict__ a, const int* __restrict__ b,
                              const int* __restrict__ c, unsigned long long* __restrict__ out) {
@@ -1118,15 +1184,8 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
       fprintf(stderr, "  bp crowd %.1f (enumeration / raw extent %.2f)\n", crowd, ext / fmax(rext, 1e-300));
     if (crowd > BP_CROWD_LIMIT) {
       B.crowd = crowd;
-      const double* cost = c->enum_cost;  // [0] grid, [1] BVH: ms per unit of crowding, < 0 unknown
-      // the grid's cost grows with the crowding, the BVH's much less: the
-      // grid is only tried (unknown cost, or a re-probe) below BP_GRID_TRY
-      const bool may_try_grid = crowd < BP_GRID_TRY;
-      bool bvh;
-      if (cost[1] < 0.0) bvh = true;
-      else if (cost[0] < 0.0) bvh = !may_try_grid;
-      else bvh = cost[1] <= cost[0];
-      if (++c->n_crowded % BP_REPROBE == 0 && (!bvh || may_try_grid)) bvh = !bvh;
+      B.crowd_bucket = std::min(BP_BUCKETS - 1, std::max(0, ilogb(crowd)));
+      const bool bvh = choose_bvh(c, B.crowd_bucket, crowd);
       if (bvh) {
         boxes_only();
         return B;

@@ -704,9 +704,8 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       if (n < 0) n = run_bp<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
       if (G.crowd > 0.0) {  // run_bvh / run_bp end on a host sync: the interval is the enumeration's
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        const double cost = ms / G.crowd;
-        double& e = c->enum_cost[method];
-        e = e < 0.0 ? cost : 0.5 * (e + cost);
+        double& e = c->enum_ms.ms[method][G.crowd_bucket];
+        e = e < 0.0 ? ms : 0.5 * (e + ms);
         if (trace) fprintf(stderr, "ccd crowded  %s %.3f ms (crowd %.1f)\n", method ? "bvh" : "grid", ms, G.crowd);
       }
       return n;

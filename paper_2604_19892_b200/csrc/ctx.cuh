@@ -259,7 +259,13 @@ struct mp_ctx {
   DBuf<int2> bvh_tasks;              // 4 task lists (class x ping-pong) of the load-balanced traversal
   DBuf<int> bvh_task_cnt;
   DBuf<unsigned long long> crowd_dev;  // grid crowding probe (bp.cuh BP_GRID_AUTO)
-  double enum_cost[2] = {-1.0, -1.0};  // crowded CCD enumerations: ms per unit of crowding, grid / BVH
+  struct EnumTimes {                 // crowded CCD enumerations: ms per log2 crowding bucket, grid / BVH (< 0 unknown)
+    double ms[2][32];
+    EnumTimes() {
+      for (auto& r : ms)
+        for (double& v : r) v = -1.0;
+    }
+  } enum_ms;
   int64_t n_crowded = 0;
   bool ccd_local = false;            // MP_OPT_CCD_LOCAL: per-subdomain motion centres (ccd.cuh local_infl)
   DBuf<double> sub_cen, sub_box, sub_delta, infl2;

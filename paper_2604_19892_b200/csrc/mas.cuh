@@ -329,16 +329,31 @@ k_mas_sweep(int64_t D, int64_t N, int bs, int m, const unsigned char* __restrict
 __global__ void k_coarse_gather(int nblk, const int* __restrict__ cb_key, const int* __restrict__ cb_off,
                                 const int* __restrict__ cb_slot, const double* __restrict__ bsr, int nA, int64_t N,
                                 int span, int n, double* __restrict__ M) {
+  // one warp per nonzero coarse block; lane l sums slots l, l + 32, ... in
+  // that order (fixed), four slots' loads in flight at a time (a diagonal
+  // block gathers ~|A| x 14 slots: dependent slot -> block loads otherwise
+  // serialise on latency)
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= nblk) return;
   double acc[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-  for (int k = cb_off[w] + lane; k < cb_off[w + 1]; k += 32) {
-    const double* b = bsr + 9 * (int64_t)cb_slot[k];
+  const int k1 = cb_off[w + 1];
+  for (int k = cb_off[w] + lane; k < k1; k += 4 * 32) {
+    int sl[4];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += b[q];
+    for (int u = 0; u < 4; ++u) sl[u] = (k + 32 * u < k1) ? cb_slot[k + 32 * u] : -1;
+    double b[4][9];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 9; ++q) b[u][q] = sl[u] >= 0 ? bsr[9 * (int64_t)sl[u] + q] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (sl[u] >= 0)
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += b[u][q];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -399,39 +414,70 @@ __device__ __forceinline__ void fx_add(unsigned long long* p, double y) {
   atomicAdd(p + 1, hi + (old + lo < old ? 1ull : 0ull));
 }
 
+// the two words fx_add adds (false: rounds to zero, nothing to add)
+__device__ __forceinline__ bool fx_split(double y, unsigned long long& lo, unsigned long long& hi) {
+  const double yi = rint(y);
+  if (yi == 0.0) return false;
+  __int128 v;
+  const int e = ilogb(yi);
+  if (e < 62) {
+    v = (__int128)(long long)yi;
+  } else {
+    const long long m = (long long)scalbn(yi, 52 - e);
+    v = (__int128)m * ((__int128)1 << (e - 52));
+  }
+  lo = (unsigned long long)v;
+  hi = (unsigned long long)(v >> 64);
+  return true;
+}
+
 __device__ __forceinline__ double fx_get(const unsigned long long* p) {
   return (double)(long long)p[1] * 18446744073709551616.0 + (double)p[0];
 }
 
 // fixed-point unit from T = sum_i k_i |grad_i|^2 >= |any coarse contact entry|:
 // out[0] = 1 / unit, out[1] = unit = 2^(ilogb(T) + 1 - 120).  One block, fixed order.
-__global__ void k_fx_scale(int64_t nc, const double* __restrict__ k, const double* __restrict__ nrm,
-                           double* __restrict__ out) {
+#define FX_PARTS 64
+__global__ void k_fx_scale_part(int64_t nc, const double* __restrict__ k, const double* __restrict__ nrm,
+                                double* __restrict__ part) {
+  // block b sums the fixed chunk [b c, (b + 1) c): strided lanes, fixed tree
   __shared__ double sh[256];
+  const int64_t c = (nc + FX_PARTS - 1) / FX_PARTS;
+  const int64_t i0 = blockIdx.x * c, i1 = min(nc, i0 + c);
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < nc; i += 256) s += fabs(k[i]) * nrm[i] * nrm[i];
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += 256) s += fabs(k[i]) * nrm[i] * nrm[i];
   sh[threadIdx.x] = s;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    const double T = sh[0];
-    const int e = (T > 0.0 && isfinite(T)) ? ilogb(T) + 1 - 120 : 0;
-    out[0] = ldexp(1.0, -e);
-    out[1] = ldexp(1.0, e);
-  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_fx_scale(const double* __restrict__ part, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double T = 0.0;
+  for (int b = 0; b < FX_PARTS; ++b) T += part[b];
+  const int e = (T > 0.0 && isfinite(T)) ? ilogb(T) + 1 - 120 : 0;
+  out[0] = ldexp(1.0, -e);
+  out[1] = ldexp(1.0, e);
 }
 
 // contacts -> the coarse level's 128-bit accumulators: k w_A w_B^T over the
 // contact's distinct aggregates, w_A = sum_{a in A} grad_a / |A| (the same
-// sum as k grad_a grad_b^T / (|A||B|) over vertex pairs)
+// sum as k grad_a grad_b^T / (|A||B|) over vertex pairs).  One thread per
+// (contact, aggregate pair): a contact's <= 16 blocks go to 16 threads, and
+// each thread issues its 9 low-word atomics before it uses any returned
+// word (a thread per contact made 144 dependent atomic round trips: ~200 us
+// at C2 for 13k contacts).
 __global__ void k_contact_coarse(int64_t nc, const int4* __restrict__ verts, const double* __restrict__ grad,
                                  const double* __restrict__ k, int64_t N, int span, int n,
                                  const double* __restrict__ fx, unsigned long long* __restrict__ acc) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = t >> 4;
   if (i >= nc) return;
+  const int pa = (int)(t & 15) >> 2, pb = (int)(t & 3);
   int4 v = verts[i];
   const int id[4] = {v.x, v.y, v.z, v.w};
   const double* gr = grad + 12 * i;
@@ -449,42 +495,85 @@ __global__ void k_contact_coarse(int64_t nc, const int4* __restrict__ verts, con
     }
     w[q][0] += gr[3 * a]; w[q][1] += gr[3 * a + 1]; w[q][2] += gr[3 * a + 2];
   }
-  for (int q = 0; q < na; ++q) {
-    const int64_t sz = (N - (int64_t)agg[q] * span) < span ? (N - (int64_t)agg[q] * span) : span;
-    const double inv = 1.0 / (double)sz;
-    w[q][0] *= inv; w[q][1] *= inv; w[q][2] *= inv;
+  if (pa >= na || pb >= na) return;
+  double wa[3], wb[3];
+  {
+    const int64_t sa = (N - (int64_t)agg[pa] * span) < span ? (N - (int64_t)agg[pa] * span) : span;
+    const int64_t sb = (N - (int64_t)agg[pb] * span) < span ? (N - (int64_t)agg[pb] * span) : span;
+    const double ia = 1.0 / (double)sa, ib = 1.0 / (double)sb;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      wa[r] = w[pa][r] * ia;
+      wb[r] = w[pb][r] * ib;
+    }
   }
   const double s = k[i] * fx[0];
-  for (int qa = 0; qa < na; ++qa)
-    for (int qb = 0; qb < na; ++qb)
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) {
-          const double val = s * w[qa][r] * w[qb][c];
-          if (val != 0.0) fx_add(acc + 2 * ((int64_t)(3 * agg[qa] + r) * n + 3 * agg[qb] + c), val);
-        }
+  unsigned long long lo[9], hi[9];
+  bool live[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    const double val = s * wa[e / 3] * wb[e % 3];
+    live[e] = fx_split(val, lo[e], hi[e]);
+  }
+  unsigned long long old[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    unsigned long long* p = acc + 2 * ((int64_t)(3 * agg[pa] + e / 3) * n + 3 * agg[pb] + e % 3);
+    old[e] = live[e] ? atomicAdd(p, lo[e]) : 0ull;
+  }
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    if (!live[e]) continue;
+    unsigned long long* p = acc + 2 * ((int64_t)(3 * agg[pa] + e / 3) * n + 3 * agg[pb] + e % 3);
+    atomicAdd(p + 1, hi[e] + (old[e] + lo[e] < old[e] ? 1ull : 0ull));
+  }
 }
 
 // 0.5 (M + M^T) on the lower triangle (the only half potrf reads)
 // (plus the contact accumulators when acc != nullptr)
-__global__ void k_sym_lower(int n, double* M, const unsigned long long* __restrict__ acc,
-                            const double* __restrict__ fx) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= (int64_t)n * n) return;
-  int i = (int)(e / n), j = (int)(e % n);
-  if (j > i) return;
-  const int64_t ij = (int64_t)i * n + j, ji = (int64_t)j * n + i;
-  double a = M[ij], b = M[ji];
-  if (acc) {
-    a += fx_get(acc + 2 * ij) * fx[1];
-    b += fx_get(acc + 2 * ji) * fx[1];
+// 32 x 32 tile pairs (I, J), I >= J, through shared memory so both the
+// (i, j) and the transposed (j, i) accesses are coalesced
+__global__ void __launch_bounds__(256) k_sym_lower(int n, double* M, const unsigned long long* __restrict__ acc,
+                                                   const double* __restrict__ fx) {
+  const int nt = (n + 31) / 32;
+  // blockIdx.x -> (I, J) with J <= I, row-major over the lower triangle
+  const int64_t b = blockIdx.x;
+  int I = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= b) ++I;
+  while ((int64_t)I * (I + 1) / 2 > b) --I;
+  const int J = (int)(b - (int64_t)I * (I + 1) / 2);
+  if (I >= nt) return;
+  __shared__ double ta[32][33], tb[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const double unit = acc ? fx[1] : 0.0;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = 32 * I + r, j = 32 * J + tx;
+    if (i < n && j < n) {
+      double a = M[(int64_t)i * n + j];
+      if (acc) a += fx_get(acc + 2 * ((int64_t)i * n + j)) * unit;
+      ta[r][tx] = a;
+    }
+    const int i2 = 32 * J + r, j2 = 32 * I + tx;
+    if (i2 < n && j2 < n) {
+      double a = M[(int64_t)i2 * n + j2];
+      if (acc) a += fx_get(acc + 2 * ((int64_t)i2 * n + j2)) * unit;
+      tb[r][tx] = a;
+    }
   }
-  if (j == i) {
-    M[ij] = a;
-    return;
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = 32 * I + r, j = 32 * J + tx;
+    if (i < n && j < n) {
+      // (i, j) with its transpose (j, i) = tb[tx][r]
+      const double a = ta[r][tx], bt = tb[tx][r];
+      M[(int64_t)i * n + j] = (i == j) ? a : 0.5 * (a + bt);
+    }
+    const int i2 = 32 * J + r, j2 = 32 * I + tx;
+    if (I != J && i2 < n && j2 < n) {
+      const double a = tb[r][tx], bt = ta[tx][r];
+      M[(int64_t)i2 * n + j2] = 0.5 * (bt + a);
+    }
   }
-  double s = 0.5 * (a + b);
-  M[(int64_t)i * n + j] = s;
-  M[(int64_t)j * n + i] = s;
 }
 
 // ---------------------------------------------------------------------------

@@ -117,7 +117,9 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_sweep, CS_THREADS, coarse_sweep_smem()));
     max_ctas = std::max(1, sms * std::max(1, per));
   }
-  const int grid = std::max(1, std::min(L.n_units + 1, max_ctas));  // + the lookahead CTA
+  static const int cap = getenv("MP_CS_GRID") ? atoi(getenv("MP_CS_GRID")) : 0;  // experiment knob
+  int grid = std::max(1, std::min(L.n_units + 1, max_ctas));  // + the lookahead CTA
+  if (cap > 1) grid = std::min(grid, cap);
   static const int prof = getenv("MP_CS_PROF") ? 1 : 0;
   CoarseSweepArgs A{n, nT, L.n_units, L.cs_units.p, L.cs_ch, L.dense.p, L.cs_tiles.p, L.cs_col.p, L.inv.p, status,
                     L.cs_bar.p, L.cs_pm.p, L.cs_diag.p, prof};
@@ -128,17 +130,57 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
 }
 
 // build_hierarchy (mas.py:138-179) from the BSR + base contacts
+static unsigned sym_tiles(int n) {
+  const int64_t nt = (n + 31) / 32;
+  return (unsigned)(nt * (nt + 1) / 2);
+}
+
+// MP_MAS_TRACE=1: a CUDA-event timeline of every 50th MAS build on stderr
+// (assembly and sweep end of each coarse level, level-0 sweep end, readback)
+struct MasTrace {
+  bool on = false;
+  cudaEvent_t e[16];
+  int ne = 0;
+  const char* name[16];
+  cudaStream_t st0 = nullptr;
+  explicit MasTrace(cudaStream_t s) : st0(s) {
+    static const bool want = getenv("MP_MAS_TRACE") != nullptr;
+    static int64_t calls = 0;
+    on = want && (calls++ % 50 == 0);
+    if (on) mark("start", s);
+  }
+  void mark(const char* what, cudaStream_t s) {
+    if (!on || ne >= 16) return;
+    CUDA_CHECK(cudaEventCreate(&e[ne]));
+    CUDA_CHECK(cudaEventRecord(e[ne], s));
+    name[ne++] = what;
+  }
+  ~MasTrace() {
+    if (!on) return;
+    cudaEventSynchronize(e[ne - 1]);
+    fprintf(stderr, "mas_build:");
+    for (int i = 1; i < ne; ++i) {
+      float ms = 0.f;
+      cudaEventSynchronize(e[i]);
+      cudaEventElapsedTime(&ms, e[0], e[i]);
+      fprintf(stderr, "  %s %.1f", name[i], 1e3 * ms);
+    }
+    fprintf(stderr, " us\n");
+    for (int i = 0; i < ne; ++i) cudaEventDestroy(e[i]);
+  }
+};
+
 static void mas_build(mp_ctx* c) {
   const int m = c->m;
   const int64_t D = c->D;
+  MasTrace mt(c->stream);
+  if (mt.on) fprintf(stderr, "mas_build: %lld contacts, coarse n %d\n", (long long)c->base.count,
+                     c->n_levels ? c->levels[0]->n : 0);
+  static const char* asm_name[4] = {"asm1", "asm2", "asm3", "asm4"};
+  static const char* inv_name[4] = {"inv1", "inv2", "inv3", "inv4"};
   // coarse levels: own streams, concurrent with the level-0 blocks below
   CUDA_CHECK(cudaMemsetAsync(c->counters.p + 3, 0, 8 * sizeof(int), c->stream));
   const int64_t nc = c->base.count;
-  if (nc && c->n_levels) {
-    c->fx_scale.ensure(2);
-    k_fx_scale<<<1, 256, 0, c->stream>>>(nc, c->base.k, c->base.nrm, c->fx_scale);
-    LAUNCH_CHECK();
-  }
   CUDA_CHECK(cudaEventRecord(c->ev_bsr, c->stream));
   // assembly: the first coarse level from the BSR (static gather map) plus
   // the contact terms (fixed point); every further level from the previous
@@ -151,21 +193,29 @@ static void mas_build(mp_ctx* c) {
       if (nc) {
         // contact terms on the level's second stream, beside the BSR gather
         CUDA_CHECK(cudaStreamWaitEvent(L.st2, c->ev_bsr, 0));
+        // the fixed-point unit (off the level-0 sweep's stream)
+        c->fx_scale.ensure(2 + FX_PARTS);
+        k_fx_scale_part<<<FX_PARTS, 256, 0, L.st2>>>(nc, c->base.k, c->base.nrm, c->fx_scale.p + 2);
+        LAUNCH_CHECK();
+        k_fx_scale<<<1, 32, 0, L.st2>>>(c->fx_scale.p + 2, c->fx_scale);
+        LAUNCH_CHECK();
+        mt.mark("fx_scale", L.st2);
         L.fx_acc.zero(2 * (size_t)L.n * L.n, L.st2);
-        k_contact_coarse<<<grid_for(nc, 128), 128, 0, L.st2>>>(nc, c->base.verts, c->base.grad, c->base.k, c->N,
-                                                               L.span, L.n, c->fx_scale, L.fx_acc);
+        k_contact_coarse<<<grid_for(16 * nc, 128), 128, 0, L.st2>>>(nc, c->base.verts, c->base.grad, c->base.k, c->N,
+                                                                    L.span, L.n, c->fx_scale, L.fx_acc);
         LAUNCH_CHECK();
         CUDA_CHECK(cudaEventRecord(L.ev_w, L.st2));
+        mt.mark("contact1", L.st2);
       }
       L.dense.zero((size_t)L.n * L.n, st);
       if (L.nblk) {
         k_coarse_gather<<<grid_for(32 * (int64_t)L.nblk, 128), 128, 0, st>>>(L.nblk, L.cb_key, L.cb_off, L.cb_slot,
                                                                              c->bsr, L.A, c->N, L.span, L.n, L.dense);
         LAUNCH_CHECK();
+        mt.mark("gather1", st);
       }
       if (nc) CUDA_CHECK(cudaStreamWaitEvent(st, L.ev_w, 0));
-      k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense, nc ? L.fx_acc.p : nullptr,
-                                                                     c->fx_scale.p);
+      k_sym_lower<<<sym_tiles(L.n), 256, 0, st>>>(L.n, L.dense, nc ? L.fx_acc.p : nullptr, c->fx_scale.p);
     } else {
       CoarseLevel& F = *c->levels[l - 1];
       CUDA_CHECK(cudaStreamWaitEvent(st, F.ev_asm, 0));
@@ -173,10 +223,11 @@ static void mas_build(mp_ctx* c) {
       k_coarse_up<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.A, c->cfg.coarse_block, F.A, F.dense, F.n,
                                                                      c->N, L.span, F.span, L.dense);
       LAUNCH_CHECK();
-      k_sym_lower<<<grid_for((int64_t)L.n * L.n, 256), 256, 0, st>>>(L.n, L.dense, nullptr, nullptr);
+      k_sym_lower<<<sym_tiles(L.n), 256, 0, st>>>(L.n, L.dense, nullptr, nullptr);
     }
     LAUNCH_CHECK();
     CUDA_CHECK(cudaEventRecord(L.ev_asm, st));
+    mt.mark(asm_name[std::min(l, 3)], st);
   }
   for (int l = 0; l < c->n_levels; ++l) {
     CoarseLevel& L = *c->levels[l];
@@ -189,19 +240,26 @@ static void mas_build(mp_ctx* c) {
     }
     dense_spd_inverse(c, L, c->counters.p + 4 + std::min(l, 3));
     CUDA_CHECK(cudaEventRecord(L.done, L.st));
+    mt.mark(inv_name[std::min(l, 3)], L.st);
   }
   // level 0: one CTA per subdomain assembles M_d in smem and sweeps it
   c->Bblk.ensure((size_t)D * cyc_size(m));
   c->Mblk.ensure((size_t)D * cyc_size(m));
-  // (a shard sweeps its owned subdomains only)
+  // (a shard sweeps its owned subdomains only).  The level-0 sweep starts
+  // after the coarse assembly: its 2 CTAs per SM otherwise hold every SM for
+  // ~100 us and the assembly chain (the critical path into the coarse
+  // inverse) waits behind them (MP_MAS_TRACE: assembly 290 us -> see DESIGN)
+  if (c->n_levels) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[c->n_levels - 1]->ev_asm, 0));
   if (c->own_d1 > c->own_d0) {
     k_mas_sweep<<<(unsigned)(c->own_d1 - c->own_d0), 256, sizeof(double) * m * m, c->stream>>>(
         D, c->N, c->bs, m, c->pinned, nc ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->base.verts,
         c->base.grad, c->base.k, c->rowptr, c->slot_row, c->cols, c->bsr, c->Mblk, c->Bblk, c->counters.p + 3,
         c->own_d0);
     LAUNCH_CHECK();
+    mt.mark("sweep0", c->stream);
   }
   for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
+  mt.mark("joined", c->stream);
   // one readback of every level's non-SPD flag (counters 3..7)
   CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 8, c->counters.p + 3, 5 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync_stream(c);
