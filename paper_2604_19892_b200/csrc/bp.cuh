@@ -973,12 +973,9 @@ struct BpGrid {
 
 enum { BP_GRID_NONE = 0, BP_GRID_ALWAYS = 1, BP_GRID_AUTO = 2 };
 // Crowded calls: the measured times of each method per log2 bucket of the
-// crowding (ctx enum_ms).  The grid's time grows ~linearly with the
-// crowding (extrapolated from the nearest lower bucket it ran in), the
-// BVH's much less (nearest bucket it ran in).  Unknown BVH -> BVH (bounded);
+// crowding (ctx enum_ms) give the estimates; unknown BVH -> BVH (bounded),
 // unknown grid -> tried only below BP_GRID_TRY; else the faster estimate,
-// with the other re-tried every BP_REPROBE crowded calls when it is not
-// predicted to be more than 4x slower.
+// the other re-measured every BP_REPROBE crowded calls when it is within 2x.
 #define BP_BUCKETS 32
 static bool choose_bvh(mp_ctx* c, int k, double crowd);
 
@@ -1000,23 +997,25 @@ static bool choose_bvh(mp_ctx* c, int k, double crowd);
 #define BP_GRID_TRY 1000.0
 
 static bool choose_bvh(mp_ctx* c, int k, double crowd) {
-  const double* g = c->enum_ms.ms[0];
-  const double* b = c->enum_ms.ms[1];
-  double tg = -1.0, tb = -1.0;
-  for (int j = k; j >= 0 && tg < 0.0; --j)
-    if (g[j] >= 0.0) tg = g[j] * ldexp(1.0, k - j);
-  for (int d = 0; d < BP_BUCKETS && tb < 0.0; ++d) {
-    if (k - d >= 0 && b[k - d] >= 0.0) tb = b[k - d];
-    else if (k + d < BP_BUCKETS && b[k + d] >= 0.0) tb = b[k + d];
-  }
-  const bool may_try_grid = crowd < BP_GRID_TRY;
+  // estimate of method m at bucket k: its time there, else extrapolated x2
+  // per bucket from the nearest lower bucket it ran in, else the nearest
+  // higher one as is; < 0 when it never ran
+  auto estimate = [&](int m) {
+    const double* t = c->enum_ms.ms[m];
+    for (int j = k; j >= 0; --j)
+      if (t[j] >= 0.0) return t[j] * ldexp(1.0, k - j);
+    for (int j = k + 1; j < BP_BUCKETS; ++j)
+      if (t[j] >= 0.0) return t[j];
+    return -1.0;
+  };
+  const double tg = estimate(0), tb = estimate(1);
   bool bvh;
-  if (tb < 0.0) bvh = true;
-  else if (tg < 0.0) bvh = !may_try_grid;
+  if (tb < 0.0) bvh = true;                            // the BVH's worst cases are bounded
+  else if (tg < 0.0) bvh = !(crowd < BP_GRID_TRY);     // the grid's are not
   else bvh = tb <= tg;
-  if (++c->n_crowded % BP_REPROBE == 0) {
-    if (bvh && (may_try_grid || (tg >= 0.0 && tg < 4.0 * tb))) bvh = false;
-    else if (!bvh) bvh = true;
+  if (++c->n_crowded % BP_REPROBE == 0 && tg >= 0.0 && tb >= 0.0) {
+    const double chosen = bvh ? tb : tg, other = bvh ? tg : tb;
+    if (other <= 2.0 * chosen) bvh = !bvh;  // re-measure a close alternative
   }
   return bvh;
 }
