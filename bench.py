@@ -81,6 +81,17 @@ def _peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+def _fp64_peak():
+    """FP64 FMA peak measured on this GPU by tools/micro/fp64_peak (built by
+    __graft_entry__.build()); else 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz."""
+    exe = ROOT / "tools" / "micro" / "fp64_peak"
+    try:
+        out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout
+        return float(json.loads(out.strip().splitlines()[-1])["fp64_fma_tflops"]), "measured"
+    except Exception:
+        return 37.2, "nominal (148 SMs x 64 DFMA/clk x 2 flops x 1.965 GHz)"
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle sampling during the timed region."""
 
@@ -356,6 +367,18 @@ def run_ours(args):
                 "frac": round(ach / hbm, 4), "traffic": traffic, "bytes_per_launch": round(b / cnt),
                 "us_per_launch": round(1e3 * ms / cnt, 2), "launches": cnt, "peak_kind": peak_kind}
 
+    fp64_peak, fp64_kind = _fp64_peak()
+
+    def roof_fp64(name, kernel):
+        ms, cnt, f = stats[name]
+        if cnt == 0 or ms <= 0:
+            return None
+        ach = (f / cnt) / (ms / cnt * 1e-3) / 1e12
+        return {"bound": "fp64", "kernel": kernel, "achieved": round(ach, 2), "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": round(ach / fp64_peak, 4), "flops_per_launch": round(f / cnt),
+                "us_per_launch": round(1e3 * ms / cnt, 2), "launches": cnt, "peak_kind": fp64_kind,
+                "note": "timed in place, concurrent with the other levels' kernels of the same build"}
+
     host = {"loop_ms": round(stats["loop"][0], 2), "blocked_in_syncs_ms": round(stats["host_wait"][0], 2),
             "syncs": stats["host_wait"][1],
             "note": "host wall time of the advance loops and the part spent blocked on the stream"}
@@ -388,6 +411,10 @@ def run_ours(args):
         "roofline_gradient_stage": roof("gradient",
                                         "gradient stage: k_contact_grad_rows + k_tet_grad x2 + k_grad_gather"),
         "roofline_hvp": roof("hvp", "HVP: k_bsr_spmv + k_rank1_rows + k_inc_gather_add"),
+        "roofline_mas_sweep0": roof_fp64("mas_sweep0", "k_mas_sweep: level-0 block assembly + symmetric sweep "
+                                                       "(m^3 FMA per subdomain)"),
+        "roofline_coarse_inv": roof_fp64("coarse_inv", "k_coarse_sweep: first coarse level's inverse "
+                                                       "((32 nT)^3 FMA, persistent, one grid barrier per panel)"),
         "stages": stage_share,
         "stages_note": ("stage times, rooflines and host stats come from a replay of the same frames with "
                         "CUDA-event stage timers on (bitwise-identical trajectory: %s; %.1f ms vs %.1f ms "

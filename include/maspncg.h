@@ -221,7 +221,9 @@ enum {
   MP_STAGE_TET_GRAD = 9,       /* the SNH per-tet gradient kernel alone        */
   MP_STAGE_HOST_WAIT = 10,     /* host wall time blocked on the stream (syncs) */
   MP_STAGE_LOOP = 11,          /* host wall time of advance_step loops         */
-  MP_STAGE_COUNT = 12
+  MP_STAGE_MAS_SWEEP0 = 12,    /* the level-0 block sweep kernel alone (work = FP64 flops, not bytes) */
+  MP_STAGE_COARSE_INV = 13,    /* the first coarse level's inverse kernel alone (work = FP64 flops)   */
+  MP_STAGE_COUNT = 14
 };
 int mp_stage_timing(mp_ctx* ctx, int enable);
 

@@ -58,7 +58,7 @@ EXPORTS = (
 )
 
 STAGES = ("gradient", "mas_apply", "hvp", "constraint_set", "hessian", "mas_build", "update", "ccd", "mas_apply_l0",
-          "tet_grad", "host_wait", "loop")
+          "tet_grad", "host_wait", "loop", "mas_sweep0", "coarse_inv")
 
 _lib = None
 

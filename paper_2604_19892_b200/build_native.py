@@ -56,3 +56,19 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)
+
+
+FP64_PEAK = PKG.parent / "tools" / "micro" / "fp64_peak"
+
+
+def build_fp64_peak() -> Path:
+    """The FP64 FMA peak probe bench.py runs for the FP64 rooflines
+    (tools/micro/fp64_peak.cu; a diagnostic binary, not part of the library)."""
+    src = FP64_PEAK.with_suffix(".cu")
+    if FP64_PEAK.exists() and FP64_PEAK.stat().st_mtime >= src.stat().st_mtime:
+        return FP64_PEAK
+    cmd = [str(CUDA_HOME / "bin" / "nvcc"), *ARCH, "-O3", "-o", str(FP64_PEAK), str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed for fp64_peak:\n" + res.stderr[-2000:])
+    return FP64_PEAK

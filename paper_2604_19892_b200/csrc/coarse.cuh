@@ -95,7 +95,11 @@ __device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double*
   for (int k = 0; k < 32; ++k) {
     const double* r = rk + (k & 1) * 32;
     __syncthreads();
-    const double piv = r[k];
+    // the step's shared loads all issue before the pivot test
+    const double piv = r[k], rik = r[i];
+    double rkj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rkj[q] = r[j0 + q];
     if (!(piv > 0.0)) return false;  // uniform across the CTA
     double inv;  // 1/piv to ~1 ulp: MUFU seed + two Newton steps (the IEEE
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(piv));  // division sits on the serial path)
@@ -103,11 +107,11 @@ __device__ bool cs_pivot_sweep(const double* __restrict__ P, double* Pm, double*
     inv = fma(inv, e, inv);
     e = fma(-piv, inv, 1.0);
     inv = fma(inv, e, inv);
-    const double cik = r[i] * inv;   // A_ik / A_kk (= A_ki / A_kk)
+    const double cik = rik * inv;   // A_ik / A_kk (= A_ki / A_kk)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int j = j0 + q;
-      const double ckj = r[j];
+      const double ckj = rkj[q];
       v[q] = (i == k) ? ((j == k) ? -inv : ckj * inv) : ((j == k) ? cik : fma(-cik, ckj, v[q]));
     }
     if (i == k + 1 && k + 1 < 32)

@@ -212,21 +212,24 @@ __device__ __forceinline__ bool sweep_panel(int m, double* rowk, double (&R)[SWE
     if (k >= m) return true;  // uniform
     const double* r = rowk + (k & 1) * SW_ROW;
     __syncthreads();
-    if (!(r[193] > 0.0)) return false;  // uniform across the CTA
-    const double inv = r[192];
-    double ci[SWEEP_T], cj[SWEEP_T];
+    // every shared load of the step issued before the pivot test (which
+    // would otherwise serialise a second shared-memory round trip behind it)
+    const double piv = r[193], inv = r[192];
+    double ci[SWEEP_T], cj[SWEEP_T], rs[SWEEP_T];
 #pragma unroll
     for (int a = 0; a < SWEEP_T; ++a) {
       ci[a] = r[96 + tr + 16 * a];  // A_ik / A_kk (= A_ki / A_kk)
       cj[a] = r[tc + 16 * a];       // A_kj
+      rs[a] = r[96 + tc + 16 * a];  // A_kj / A_kk (row k's fix-up)
     }
+    if (!(piv > 0.0)) return false;  // uniform across the CTA
 #pragma unroll
     for (int a = 0; a < SWEEP_T; ++a)
 #pragma unroll
       for (int b = 0; b < SWEEP_T; ++b) R[a][b] = fma(-ci[a], cj[b], R[a][b]);
     if (tr == kr)  // row k: A_kj <- A_kj / A_kk
 #pragma unroll
-      for (int b = 0; b < SWEEP_T; ++b) R[KA][b] = r[96 + tc + 16 * b];
+      for (int b = 0; b < SWEEP_T; ++b) R[KA][b] = rs[b];
     if (tc == kr) {  // column k: A_ik <- A_ik / A_kk, and A_kk <- -1 / A_kk
 #pragma unroll
       for (int a = 0; a < SWEEP_T; ++a) R[a][KA] = ci[a];

@@ -238,7 +238,10 @@ static void mas_build(mp_ctx* c) {
       CUDA_CHECK(cudaMemcpyAsync(L.keep.p, L.dense.p, sizeof(double) * (size_t)L.n * L.n, cudaMemcpyDeviceToDevice,
                                  L.st));
     }
+    if (l == 0) timer_begin(c, MP_STAGE_COARSE_INV, L.st);
     dense_spd_inverse(c, L, c->counters.p + 4 + std::min(l, 3));
+    // work: the padded order's (32 nT)^3 FMAs of the panel sweep (2 flops each)
+    if (l == 0) timer_end(c, MP_STAGE_COARSE_INV, 2.0 * std::pow(32.0 * ((L.n + 31) / 32), 3.0), L.st);
     CUDA_CHECK(cudaEventRecord(L.done, L.st));
     mt.mark(inv_name[std::min(l, 3)], L.st);
   }
@@ -251,11 +254,14 @@ static void mas_build(mp_ctx* c) {
   // inverse) waits behind them (MP_MAS_TRACE: assembly 290 us -> see DESIGN)
   if (c->n_levels) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[c->n_levels - 1]->ev_asm, 0));
   if (c->own_d1 > c->own_d0) {
+    timer_begin(c, MP_STAGE_MAS_SWEEP0);
     k_mas_sweep<<<(unsigned)(c->own_d1 - c->own_d0), 256, sizeof(double) * m * m, c->stream>>>(
         D, c->N, c->bs, m, c->pinned, nc ? c->inc_base.off.p : nullptr, c->inc_base.val2.p, c->base.verts,
         c->base.grad, c->base.k, c->rowptr, c->slot_row, c->cols, c->bsr, c->Mblk, c->Bblk, c->counters.p + 3,
         c->own_d0);
     LAUNCH_CHECK();
+    // work: the sweep operator's m^3 FMAs per subdomain (2 flops each)
+    timer_end(c, MP_STAGE_MAS_SWEEP0, 2.0 * (double)m * m * m * (double)(c->own_d1 - c->own_d0));
     mt.mark("sweep0", c->stream);
   }
   for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
