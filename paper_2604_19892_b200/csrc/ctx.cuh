@@ -163,7 +163,9 @@ struct mp_ctx {
   int apply_ctas_per_sm = 3; // level-0 apply persistent CTAs per SM
   bool fused_grad = false;  // gradient: one fused per-vertex pass (k_grad_fused; measured slower at C2, 98 vs 74 us) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
   bool overlap_apply = true;  // MAS apply: level 0 on the side stream beside the coarse chain (MP_OPT_APPLY_OVERLAP)
-  cudaStream_t side = nullptr;  // side stream (level-0 apply) and its events
+  cudaStream_t side = nullptr;  // side stream (level-0 apply, elastic H_base ahead) and its events
+  cudaEvent_t ev_it = nullptr, ev_bsr_ahead = nullptr;  // bsr_ahead (elastic.cuh)
+  bool bsr_ahead_pending = false;
   cudaEvent_t ev_g = nullptr, ev_l0 = nullptr;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
   bool keep_coarse = false;  // keep each coarse level's assembled matrix (mp_coarse_matrix)
   int bp_fused = 1;          // 1: one-pass unordered pair lists, 2: contact work fused into the queries, 0: ordered lists

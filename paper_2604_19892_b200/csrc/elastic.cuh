@@ -506,20 +506,32 @@ static void gradient_gather(mp_ctx* c, const double* x, const double* xt, double
   LAUNCH_CHECK();
 }
 
-static void assemble_elastic_bsr(mp_ctx* c, const double* x, double h) {
+static void assemble_elastic_bsr(mp_ctx* c, const double* x, double h, cudaStream_t s = nullptr) {
+  if (!s) s = c->stream;
   if (c->T_snh) {
-    k_tet_hessian<2><<<grid_for(c->T_snh, 64), 64, 0, c->stream>>>(0, c->T_snh, c->tets, c->tetp, c->pinned, x,
-                                                                   h * h, c->hbuf);
+    k_tet_hessian<2><<<grid_for(c->T_snh, 64), 64, 0, s>>>(0, c->T_snh, c->tets, c->tetp, c->pinned, x, h * h,
+                                                           c->hbuf);
     LAUNCH_CHECK();
   }
   if (c->T_arap) {
-    k_tet_hessian<1><<<grid_for(c->T_arap, 64), 64, 0, c->stream>>>(c->T_snh, c->T_arap, c->tets, c->tetp,
-                                                                    c->pinned, x, h * h, c->hbuf);
+    k_tet_hessian<1><<<grid_for(c->T_arap, 64), 64, 0, s>>>(c->T_snh, c->T_arap, c->tets, c->tetp, c->pinned, x,
+                                                            h * h, c->hbuf);
     LAUNCH_CHECK();
   }
-  k_hess_gather<<<grid_for(c->nnzb, 128), 128, 0, c->stream>>>(c->nnzb, c->slot_row, c->cols, c->hs_off, c->hs_val,
-                                                               c->hbuf, c->mass, c->pinned, c->bsr);
+  k_hess_gather<<<grid_for(c->nnzb, 128), 128, 0, s>>>(c->nnzb, c->slot_row, c->cols, c->hs_off, c->hs_val, c->hbuf,
+                                                       c->mass, c->pinned, c->bsr);
   LAUNCH_CHECK();
+}
+
+// The elastic part of H_base depends on x alone: when an iteration is known
+// to rebuild, it is assembled on the side stream while the constraint set
+// (sync-bound at small scale) runs on the main one; snapshot joins it.
+static void bsr_ahead(mp_ctx* c, const double* x, double h) {
+  CUDA_CHECK(cudaEventRecord(c->ev_it, c->stream));  // after every reader of the previous BSR
+  CUDA_CHECK(cudaStreamWaitEvent(c->side, c->ev_it, 0));
+  assemble_elastic_bsr(c, x, h, c->side);
+  CUDA_CHECK(cudaEventRecord(c->ev_bsr_ahead, c->side));
+  c->bsr_ahead_pending = true;
 }
 
 static void bsr_spmv(mp_ctx* c, const double* xin, double* y) {

@@ -35,6 +35,8 @@ mp_ctx::~mp_ctx() {
   if (ev_bsr) cudaEventDestroy(ev_bsr);
   if (ev_g) cudaEventDestroy(ev_g);
   if (ev_l0) cudaEventDestroy(ev_l0);
+  if (ev_it) cudaEventDestroy(ev_it);
+  if (ev_bsr_ahead) cudaEventDestroy(ev_bsr_ahead);
   if (side) cudaStreamDestroy(side);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -228,6 +230,8 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_g, cudaEventDisableTiming));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_l0, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_it, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bsr_ahead, cudaEventDisableTiming));
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
   CUDA_CHECK(cudaMallocHost(&c->h_cnt, 16 * sizeof(int)));
@@ -513,9 +517,11 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
   double prev_zg = 0.0, prev_gp = 0.0;  // g_prev.z_prev, g_prev.p_prev (baseline beta rules)
   R.recs.clear();
   R.converged = false;
+  c->bsr_ahead_pending = false;
   for (int64_t k = 0; k < cfg.iter_max; ++k) {
     auto t0 = Clock::now();
     const bool rebuild = restart || full_every;
+    if (rebuild) bsr_ahead(c, c->x, h);
     timer_begin(c, MP_STAGE_CONSTRAINT_SET);
     constraint_set(c, c->x);
     timer_end(c, MP_STAGE_CONSTRAINT_SET, 0.0);
@@ -754,6 +760,7 @@ static int guarded(mp_ctx* c, Fn&& fn) {
   g_launch_counter = c ? &c->launches : nullptr;
   try {
     if (c) CUDA_CHECK(cudaSetDevice(c->device));
+    if (c) c->bsr_ahead_pending = false;  // an H_base assembled ahead belongs to one loop iteration only
     fn();
     return MP_OK;
   } catch (const MpError& e) {

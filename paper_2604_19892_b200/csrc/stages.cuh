@@ -375,7 +375,12 @@ static void snapshot(mp_ctx* c, const double* x, double h, bool build_mas) {
   } else {
     build_inc(c, c->inc_base, c->base.verts, c->base.count);
   }
-  assemble_elastic_bsr(c, x, h);
+  if (c->bsr_ahead_pending) {  // assembled ahead on the side stream (bsr_ahead) from the same x
+    CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_bsr_ahead, 0));
+    c->bsr_ahead_pending = false;
+  } else {
+    assemble_elastic_bsr(c, x, h);
+  }
   timer_end(c, MP_STAGE_HESSIAN, hessian_bytes(c));
   c->have_snapshot = true;
   c->have_mas = false;
