@@ -187,6 +187,8 @@ __device__ unsigned long long g_bvh_stats[4];
 struct BvhOut {
   int2 buf[BVH_BUF];
   int n = 0;
+  double amin = 1.0;              // list-free mode: this thread's smallest alpha_pair
+  unsigned long long npairs = 0;  // list-free mode: pairs worked
 };
 
 __device__ __forceinline__ bool bvh_reserve(int k, int& base, const PairArgs& A) {
@@ -216,6 +218,44 @@ __device__ __forceinline__ void bvh_emit(BvhOut& o, int a, int b, const PairArgs
   }
 }
 
+// One passing pair: appended to the list (FM < 0), or worked at once by this
+// thread (FM = BP_CCD / BP_CERT, the list-free mode for calls past the 2^30
+// list limit): pair_work's per-pair steps without its warp collectives --
+// the alpha_d minima are order-free atomics, the global minimum and the pair
+// count are reduced per thread and flushed once per warp at the end.
+template <int FM>
+__device__ __forceinline__ void bvh_take(BvhOut& o, bool is_pt, int a, int b, const PairArgs& A) {
+  if (FM < 0) {
+    bvh_emit(o, a, b, A);
+    return;
+  }
+  ++o.npairs;
+  int vid[4];
+  if (is_pt) {
+    vid[0] = a; vid[1] = A.tri[3 * b]; vid[2] = A.tri[3 * b + 1]; vid[3] = A.tri[3 * b + 2];
+  } else {
+    vid[0] = A.edge[2 * a]; vid[1] = A.edge[2 * a + 1]; vid[2] = A.edge[2 * b]; vid[3] = A.edge[2 * b + 1];
+  }
+  if (FM == BP_CCD) {
+    bool cert_p = true;
+    const double al = ccd_pair_alpha(A.x, A.CC.p, vid, is_pt, A.CC.alpha_l, &cert_p);
+    if (al < 1.0)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double* ad = &A.O.alpha_d[vid[r] / A.CC.bs];
+        if (al < *(volatile double*)ad) atomic_min_nonneg(ad, al);
+      }
+    o.amin = fmin(o.amin, al);
+    if (!cert_p) A.O.counter[1] = 1;
+  } else if (FM == BP_CERT) {
+    if (!ccd_certify_pair(A.x, A.CC.p, A.O.alpha_d, A.CC.bs, vid, is_pt)) A.O.counter[1] = 1;
+  }
+}
+
+// all 32 lanes, converged: the list-free mode's warp minimum and pair count
+template <int FM>
+__device__ __forceinline__ void bvh_finish_warp(BvhOut& o, const PairArgs& A);
+
 // all 32 lanes, converged
 __device__ __forceinline__ void bvh_flush_warp(BvhOut& o, const PairArgs& A) {
   const int lane = threadIdx.x & 31;
@@ -242,32 +282,62 @@ __device__ __forceinline__ void bvh_flush_warp(BvhOut& o, const PairArgs& A) {
 struct BvhTasks {
   const int2* in;    // this round's (query, stack entry) tasks, or null: one root task per query
   const int* n_in;
+  int64_t in_cap;    // capacity of `in` (its count may exceed it after an overflow)
   int2* out;         // entries handed to the next round
   int* n_out;        // [0] count, [1] overflow flag
   int64_t cap;
   int budget;
+  bool abandon;      // on a full list: stop (the host grows the lists and reruns) or finish the traversal here
 };
 
-__device__ __forceinline__ void bvh_dump(const BvhTasks& K, int query, const int* stack, int sp) {
+// Hands the stack on; false when the task list is full: the thread then
+// abandons (the host grows the lists to the requested total and reruns the
+// enumeration from scratch -- minima and flags are idempotent) or, with a
+// fixed capacity, finishes its traversal itself.  The slots a failed
+// reservation still got below the capacity are marked (query -1) and
+// skipped by the next round.
+__device__ __forceinline__ bool bvh_dump(const BvhTasks& K, int query, const int* stack, int sp) {
   const int base = atomicAdd(K.n_out, sp);
   if (base < 0 || (int64_t)base + sp > K.cap) {
     atomicExch(K.n_out + 1, 1);
-    return;
+    for (int r = 0; r < sp; ++r)
+      if (base >= 0 && (int64_t)base + r < K.cap) K.out[base + r] = make_int2(-1, 0);
+    return false;
   }
   for (int r = 0; r < sp; ++r) K.out[base + r] = make_int2(query, stack[r]);
+  return true;
+}
+
+template <int FM>
+__device__ __forceinline__ void bvh_finish_warp(BvhOut& o, const PairArgs& A) {
+  if (FM < 0) {
+    bvh_flush_warp(o, A);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned long long n = o.npairs;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) n += __shfl_down_sync(0xffffffffu, n, d);
+  if (lane == 0 && n) atomicAdd(A.n_pairs, n);
+  if (FM == BP_CCD) {
+    const double wm = warp_min_all(o.amin);
+    if (lane == 0 && wm < *(volatile double*)A.O.min_alpha) atomic_min_nonneg(A.O.min_alpha, wm);
+  }
 }
 
 // Points query the triangle tree (PT pairs (v, t)); the leaf predicate is
 // k_hq_points' (boxes_meet, pt_ref_pass, rel_safe).
+template <int FM>
 __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int64_t V, const int* __restrict__ sverts,
                                                     const int* __restrict__ tri, const double* __restrict__ x,
                                                     double gap, PairArgs A, BvhTasks K, bool stats) {
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nt = K.in ? (int64_t)*K.n_in : V;
+  const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : V;
   if (blockIdx.x * (int64_t)blockDim.x >= nt || TT.n == 0) return;  // block-uniform
   BvhOut out;
-  const bool live = t0 < nt;
-  const int2 task = K.in ? K.in[live ? t0 : nt - 1] : make_int2((int)(live ? t0 : V - 1), ((TT.nlev - 1) << 26) | 0);
+  int2 task = K.in ? K.in[t0 < nt ? t0 : nt - 1] : make_int2((int)(t0 < nt ? t0 : V - 1), ((TT.nlev - 1) << 26) | 0);
+  const bool live = t0 < nt && task.x >= 0;
+  if (task.x < 0) task.x = 0;
   const int64_t q = task.x;
   const int v = sverts[q];
   const int64_t oq = T.P + q;
@@ -286,10 +356,11 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
   int sp = 0;
   if (live) stack[sp++] = task.y;
   unsigned n_in = 0, n_leaf = 0;
+  int budget = K.budget;
   while (sp > 0) {
-    if ((int)(n_in + n_leaf) >= K.budget) {
-      bvh_dump(K, (int)q, stack, sp);
-      break;
+    if ((int)(n_in + n_leaf) >= budget) {
+      if (bvh_dump(K, (int)q, stack, sp) || K.abandon) break;
+      budget = INT_MAX;  // the list is full and fixed (test knob): finish here
     }
     const int e = stack[--sp];
     const int L = e >> 26;
@@ -303,7 +374,7 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
         const double* th = T.ehi + 3 * (int64_t)t;
         if (boxes_meet(Q.elo, Q.ehi, tl, th) && pt_ref_pass(T, tri, x, v, q, t) &&
             !rel_safe(T, oq, t, Q.rlo, Q.rhi, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t))
-          bvh_emit(out, v, t, A);
+          bvh_take<FM>(out, true, v, t, A);
       }
     } else {
       ++n_in;
@@ -319,19 +390,21 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
     atomicAdd(&g_bvh_stats[3], 1ull);
   }
   __syncwarp();
-  bvh_flush_warp(out, A);
+  bvh_finish_warp<FM>(out, A);
 }
 
 // Edges query the edge tree at sorted positions above their own (each
 // unordered pair once); the leaf predicate is k_hq_edges'.
+template <int FM>
 __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64_t E, const int* __restrict__ edge,
                                                    double gap, PairArgs A, BvhTasks K, bool stats) {
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nt = K.in ? (int64_t)*K.n_in : E;
+  const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : E;
   if (blockIdx.x * (int64_t)blockDim.x >= nt) return;  // block-uniform
   BvhOut out;
-  const bool live = t0 < nt;
-  const int2 task = K.in ? K.in[live ? t0 : nt - 1] : make_int2((int)(live ? t0 : E - 1), ((TE.nlev - 1) << 26) | 0);
+  int2 task = K.in ? K.in[t0 < nt ? t0 : nt - 1] : make_int2((int)(t0 < nt ? t0 : E - 1), ((TE.nlev - 1) << 26) | 0);
+  const bool live = t0 < nt && task.x >= 0;
+  if (task.x < 0) task.x = 0;
   const int64_t si = task.x;
   const int i = TE.order[si];
   const int64_t oi = T.F + i;
@@ -354,10 +427,11 @@ __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64
   int sp = 0;
   if (live) stack[sp++] = task.y;
   unsigned n_in = 0, n_leaf = 0;
+  int budget = K.budget;
   while (sp > 0) {
-    if ((int)(n_in + n_leaf) >= K.budget) {
-      bvh_dump(K, (int)si, stack, sp);
-      break;
+    if ((int)(n_in + n_leaf) >= budget) {
+      if (bvh_dump(K, (int)si, stack, sp) || K.abandon) break;
+      budget = INT_MAX;  // the list is full and fixed (test knob): finish here
     }
     const int e = stack[--sp];
     const int L = e >> 26;
@@ -376,7 +450,7 @@ __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64
                           fli[0] <= fhj[0] && fli[1] <= fhj[1] && fli[2] <= fhj[2] && flj[0] <= fhi[0] &&
                           flj[1] <= fhi[1] && flj[2] <= fhi[2] && ref_reach(T.rc, oi, oj) &&
                           !rel_safe(T, oi, oj, Q.rlo, Q.rhi, T.rlo + 3 * oj, T.rhi + 3 * oj);
-        if (pass) bvh_emit(out, min(i, j), max(i, j), A);
+        if (pass) bvh_take<FM>(out, false, min(i, j), max(i, j), A);
       }
     } else {
       ++n_in;
@@ -397,7 +471,7 @@ __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64
     atomicAdd(&g_bvh_stats[3], 1ull);
   }
   __syncwarp();
-  bvh_flush_warp(out, A);
+  bvh_finish_warp<FM>(out, A);
 }
 
 // the class trees: order fixed at first use (by smallest vertex id -- the
@@ -440,8 +514,8 @@ static void bvh_trace_stats(bool on, const char* what, const BvhTree& T) {
 
 // Tight CCD / certificate enumeration through the class trees: the same
 // reference pair list as run_bp's one-pass append (bp.cuh), then the mode's
-// pair kernel.  Returns the pair count, or -1 when the 2^30 list limit was
-// hit (the caller reruns on the grid, whose list-free mode counts in 64 bits).
+// pair kernel; past the 2^30 list limit the traversal reruns list-free, the
+// pairs worked where they are found (64-bit count).  Returns the pair count.
 template <int MODE>
 static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, ContactParams CP, CcdParams CC,
                        int* flag) {
@@ -492,24 +566,30 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
   refit(TE, ne, F);
   tr.lap("refit");
   // task lists: [class][ping-pong]; counters: per class and buffer (count, overflow)
-  if (c->bvh_tasks.n < 4 * (size_t)BVH_TASKS0) c->bvh_tasks.ensure(4 * (size_t)BVH_TASKS0);
+  const size_t want = 4 * (size_t)(c->bvh_task_cap > 0 ? c->bvh_task_cap : BVH_TASKS0);
+  if (c->bvh_tasks.n < want) c->bvh_tasks.ensure(want);
   c->bvh_task_cnt.ensure(8);
-  for (int attempt = 0; attempt < 6; ++attempt) {
+  bool list_free = false;  // set when the one-pass list would pass 2^30 pairs
+  for (int attempt = 0; attempt < 10; ++attempt) {
     CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), st));
+    c->n_pairs_dev.ensure(1);
+    if (list_free) CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), st));
     O.counter = c->counters.p;
     if (g.pa.n < 1024) { g.pa.ensure(1 << 16); g.pb.ensure(1 << 16); }
     if (g.ea.n < 1024) { g.ea.ensure(1 << 16); g.eb.ensure(1 << 16); }
     int* cnt = c->counters.p + 8;  // [8] PT, [9] EE appended, [10] overflow flag
     CUDA_CHECK(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), st));
     const int64_t cap_pt = (int64_t)std::min(g.pa.n, g.pb.n), cap_ee = (int64_t)std::min(g.ea.n, g.eb.n);
-    const int64_t tcap = (int64_t)(c->bvh_tasks.n / 4);
+    const int64_t tcap = c->bvh_task_cap > 0 ? c->bvh_task_cap : (int64_t)(c->bvh_tasks.n / 4);
     int2* tbuf[2][2];
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b) tbuf[a][b] = reinterpret_cast<int2*>(c->bvh_tasks.p) + (2 * a + b) * tcap;
     int* tcnt = c->bvh_task_cnt.p;  // [2 * (2 * class + buffer)] count, [+1] overflow
     bool task_overflow = false;
+    const bool growable = c->bvh_task_cap <= 0;
+    int64_t need = 0;
     if (!B.empty) {
-      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, nullptr, g.pa, g.pb, cnt, cap_pt};
+      PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, c->n_pairs_dev.p, g.pa, g.pb, cnt, cap_pt};
       PairArgs Ae = A;
       Ae.app_a = g.ea; Ae.app_b = g.eb; Ae.app_cnt = cnt + 1; Ae.app_cap = cap_ee; Ae.app_ee = 1;
       const bool do_pt = V && F, do_ee = E > 1;
@@ -519,17 +599,26 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
         CUDA_CHECK(cudaMemsetAsync(tcnt + 4 * 0 + 2 * nxt, 0, 2 * sizeof(int), st));
         CUDA_CHECK(cudaMemsetAsync(tcnt + 4 * 1 + 2 * nxt, 0, 2 * sizeof(int), st));
         if (n_task[0]) {
-          BvhTasks K{round ? tbuf[0][cur] : nullptr, tcnt + 2 * cur, tbuf[0][nxt], tcnt + 2 * nxt, tcap, BVH_BUDGET};
-          k_bvh_points<<<grid_for(n_task[0], 128), 128, 0, st>>>(T, TT, V, c->sverts, c->tri, x, B.filter_gap, A, K,
-                                                                   tr.on);
+          BvhTasks K{round ? tbuf[0][cur] : nullptr, tcnt + 2 * cur, tcap, tbuf[0][nxt], tcnt + 2 * nxt, tcap,
+                     BVH_BUDGET, growable};
+          if (list_free)
+            k_bvh_points<MODE><<<grid_for(n_task[0], 128), 128, 0, st>>>(T, TT, V, c->sverts, c->tri, x,
+                                                                         B.filter_gap, A, K, tr.on);
+          else
+            k_bvh_points<-1><<<grid_for(n_task[0], 128), 128, 0, st>>>(T, TT, V, c->sverts, c->tri, x, B.filter_gap,
+                                                                       A, K, tr.on);
           LAUNCH_CHECK();
           tr.lap("points");
           bvh_trace_stats(tr.on, "points", TT);
         }
         if (n_task[1]) {
-          BvhTasks K{round ? tbuf[1][cur] : nullptr, tcnt + 4 + 2 * cur, tbuf[1][nxt], tcnt + 4 + 2 * nxt, tcap,
-                     BVH_BUDGET};
-          k_bvh_edges<<<grid_for(n_task[1], 128), 128, 0, st>>>(T, TE, E, c->edge, B.filter_gap, Ae, K, tr.on);
+          BvhTasks K{round ? tbuf[1][cur] : nullptr, tcnt + 4 + 2 * cur, tcap, tbuf[1][nxt], tcnt + 4 + 2 * nxt,
+                     tcap, BVH_BUDGET, growable};
+          if (list_free)
+            k_bvh_edges<MODE><<<grid_for(n_task[1], 128), 128, 0, st>>>(T, TE, E, c->edge, B.filter_gap, Ae, K,
+                                                                        tr.on);
+          else
+            k_bvh_edges<-1><<<grid_for(n_task[1], 128), 128, 0, st>>>(T, TE, E, c->edge, B.filter_gap, Ae, K, tr.on);
           LAUNCH_CHECK();
           tr.lap("edges");
           bvh_trace_stats(tr.on, "edges", TE);
@@ -539,30 +628,41 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
         sync_stream(c);
         if (h[2 * nxt + 1] || h[4 + 2 * nxt + 1]) {
           task_overflow = true;
-          break;
+          need = std::max<int64_t>(need, std::max<int64_t>(h[2 * nxt], h[4 + 2 * nxt]));
+          if (growable) break;  // threads abandoned work: rerun with lists of the requested size
         }
-        n_task[0] = h[2 * nxt];
-        n_task[1] = h[4 + 2 * nxt];
+        n_task[0] = std::min<int64_t>(h[2 * nxt], tcap);
+        n_task[1] = std::min<int64_t>(h[4 + 2 * nxt], tcap);
         if (tr.on && (n_task[0] || n_task[1]))
           fprintf(stderr, "  bvh round %d hands on %lld + %lld tasks\n", round + 1, (long long)n_task[0],
                   (long long)n_task[1]);
       }
-      if (!task_overflow) {
+      if (task_overflow && growable) {  // lists of the requested size (all four), then from scratch
+        c->bvh_tasks.ensure(4 * (size_t)(need + need / 4 + 1024));
+        continue;
+      }
+      if (!list_free) {
         k_pairs_app<MODE><<<8 * 148, 256, 0, st>>>(cnt, cap_pt, cap_ee, g.pa, g.pb, g.ea, g.eb, A);
         LAUNCH_CHECK();
         tr.lap("pairs");
       }
     }
-    if (task_overflow) {  // grow the task lists and start over (the pair list is rebuilt from scratch)
-      c->bvh_tasks.ensure(8 * (size_t)tcap);
-      continue;
-    }
     CUDA_CHECK(cudaMemcpyAsync(c->h_cnt, c->counters.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 5, cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     if (c->rb_extra)  // the caller's scalar rides on this readback (h_scal[0])
       CUDA_CHECK(cudaMemcpyAsync(c->h_scal, c->rb_extra, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (list_free)
+      CUDA_CHECK(cudaMemcpyAsync(c->h_npairs, c->n_pairs_dev.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 st));
     sync_stream(c);
-    if (c->h_cnt[7]) return -1;
+    if (list_free) {
+      if (flag) *flag = c->h_cnt[1];
+      return (int64_t)*c->h_npairs;
+    }
+    if (c->h_cnt[7]) {  // >= 2^30 pairs: rerun list-free (minima / flags are idempotent)
+      list_free = true;
+      continue;
+    }
     const int64_t n_pt = c->h_cnt[5], n_ee = c->h_cnt[6];
     if (n_pt > cap_pt || n_ee > cap_ee) {  // grow and rerun (minima / flags are idempotent)
       if (n_pt > cap_pt) { g.pa.ensure((size_t)(n_pt * 1.25) + 1024); g.pb.ensure((size_t)(n_pt * 1.25) + 1024); }

@@ -260,6 +260,7 @@ struct mp_ctx {
   DBuf<float4> bvh_tri_nodes, bvh_edge_nodes;  // BvhNode = 5 float4
   DBuf<int2> bvh_tasks;              // 4 task lists (class x ping-pong) of the load-balanced traversal
   DBuf<int> bvh_task_cnt;
+  int64_t bvh_task_cap = 0;          // MP_OPT_BVH_TASKS test knob: fixed task-list capacity (0: grown as needed)
   DBuf<unsigned long long> crowd_dev;  // grid crowding probe (bp.cuh BP_GRID_AUTO)
   struct EnumTimes {                 // crowded CCD enumerations: ms per log2 crowding bucket, grid / BVH (< 0 unknown)
     double ms[2][32];

@@ -132,6 +132,48 @@ def test_c2_ccd_bvh_vs_grid(c2, scale):
 
 
 @pytest.mark.gpu
+def test_c2_ccd_bvh_task_overflow(c2):
+    """MP_OPT_BVH_TASKS (15): with hand-on task lists far too small, threads
+    finish their own traversals -- the same pair count and results."""
+    g, _, ctx = c2
+    p = 400.0 * g["p"]
+    try:
+        ctx.set_option(14, 0)
+        ref = ctx.ccd(g["x0"], p, exact_set=False)
+        ctx.set_option(14, 1)
+        for cap in (64, 4096):
+            ctx.set_option(15, cap)
+            out = ctx.ccd(g["x0"], p, exact_set=False)
+            assert out[4] == ref[4]
+            assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
+            assert out[2] == ref[2] and out[3] == ref[3]
+    finally:
+        ctx.set_option(15, 0)
+        ctx.set_option(14, 2)
+
+
+@pytest.mark.gpu
+def test_c2_ccd_bvh_list_free(c2):
+    """Past the one-pass list limit (lowered by MP_OPT_APPEND_LIMIT, 8) the
+    BVH reruns list-free, working each pair where it is found: the same
+    64-bit pair count, alpha_d, minimum, certificate and x_new."""
+    g, _, ctx = c2
+    p = 40.0 * g["p"]
+    try:
+        ctx.set_option(14, 0)
+        ref = ctx.ccd(g["x0"], p, exact_set=False)
+        ctx.set_option(14, 1)
+        ctx.set_option(8, 4096)
+        out = ctx.ccd(g["x0"], p, exact_set=False)
+        assert ref[4] > 4096 and out[4] == ref[4]
+        assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
+        assert out[2] == ref[2] and out[3] == ref[3]
+    finally:
+        ctx.set_option(8, 0)
+        ctx.set_option(14, 2)
+
+
+@pytest.mark.gpu
 def test_c2_update_branch(c2):
     """The non-rebuild branch at x1 against the x0 snapshot: classify_all,
     select_top_k (K=8), build_update (Sparse-Input Woodbury), then z and HVP
