@@ -182,6 +182,7 @@ __device__ __forceinline__ bool bvh_visit(const BvhQuery& q, const BvhNode& nd) 
 #define BVH_BUF 16
 #define BVH_BUDGET 64          // node expansions per thread per round
 #define BVH_TASKS0 (1 << 20)   // initial task-list capacity per list
+#define BVH_TASKS_MAX (1ll << 27)  // largest task list grown on demand (1 GiB each, 4 lists)
 // MP_BP_TRACE: [0] inner-node expansions, [1] leaf expansions, [2] objects tested, [3] queries
 __device__ unsigned long long g_bvh_stats[4];
 struct BvhOut {
@@ -281,13 +282,14 @@ __device__ __forceinline__ void bvh_flush_warp(BvhOut& o, const PairArgs& A) {
 // are spread over many threads instead of one thread finishing last.
 struct BvhTasks {
   const int2* in;    // this round's (query, stack entry) tasks, or null: one root task per query
-  const int* n_in;
+  const unsigned long long* n_in;
   int64_t in_cap;    // capacity of `in` (its count may exceed it after an overflow)
   int2* out;         // entries handed to the next round
-  int* n_out;        // [0] count, [1] overflow flag
+  unsigned long long* n_out;  // [0] count (64-bit: requests can pass 2^31), [1] overflow flag
   int64_t cap;
   int budget;
   bool abandon;      // on a full list: stop (the host grows the lists and reruns) or finish the traversal here
+  int64_t q_base;    // root round: queries [q_base, n) (the kernel's V / E argument is the chunk's end)
 };
 
 // Hands the stack on; false when the task list is full: the thread then
@@ -297,11 +299,11 @@ struct BvhTasks {
 // reservation still got below the capacity are marked (query -1) and
 // skipped by the next round.
 __device__ __forceinline__ bool bvh_dump(const BvhTasks& K, int query, const int* stack, int sp) {
-  const int base = atomicAdd(K.n_out, sp);
-  if (base < 0 || (int64_t)base + sp > K.cap) {
-    atomicExch(K.n_out + 1, 1);
+  const unsigned long long base = atomicAdd(K.n_out, (unsigned long long)sp);
+  if (base + sp > (unsigned long long)K.cap) {
+    atomicExch(K.n_out + 1, 1ull);
     for (int r = 0; r < sp; ++r)
-      if (base >= 0 && (int64_t)base + r < K.cap) K.out[base + r] = make_int2(-1, 0);
+      if (base + r < (unsigned long long)K.cap) K.out[base + r] = make_int2(-1, 0);
     return false;
   }
   for (int r = 0; r < sp; ++r) K.out[base + r] = make_int2(query, stack[r]);
@@ -332,10 +334,11 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
                                                     const int* __restrict__ tri, const double* __restrict__ x,
                                                     double gap, PairArgs A, BvhTasks K, bool stats) {
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : V;
+  const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : V - K.q_base;
   if (blockIdx.x * (int64_t)blockDim.x >= nt || TT.n == 0) return;  // block-uniform
   BvhOut out;
-  int2 task = K.in ? K.in[t0 < nt ? t0 : nt - 1] : make_int2((int)(t0 < nt ? t0 : V - 1), ((TT.nlev - 1) << 26) | 0);
+  int2 task = K.in ? K.in[t0 < nt ? t0 : nt - 1]
+                   : make_int2((int)(K.q_base + (t0 < nt ? t0 : nt - 1)), ((TT.nlev - 1) << 26) | 0);
   const bool live = t0 < nt && task.x >= 0;
   if (task.x < 0) task.x = 0;
   const int64_t q = task.x;
@@ -399,10 +402,11 @@ template <int FM>
 __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64_t E, const int* __restrict__ edge,
                                                    double gap, PairArgs A, BvhTasks K, bool stats) {
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : E;
+  const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : E - K.q_base;
   if (blockIdx.x * (int64_t)blockDim.x >= nt) return;  // block-uniform
   BvhOut out;
-  int2 task = K.in ? K.in[t0 < nt ? t0 : nt - 1] : make_int2((int)(t0 < nt ? t0 : E - 1), ((TE.nlev - 1) << 26) | 0);
+  int2 task = K.in ? K.in[t0 < nt ? t0 : nt - 1]
+                   : make_int2((int)(K.q_base + (t0 < nt ? t0 : nt - 1)), ((TE.nlev - 1) << 26) | 0);
   const bool live = t0 < nt && task.x >= 0;
   if (task.x < 0) task.x = 0;
   const int64_t si = task.x;
@@ -569,77 +573,118 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
   const size_t want = 4 * (size_t)(c->bvh_task_cap > 0 ? c->bvh_task_cap : BVH_TASKS0);
   if (c->bvh_tasks.n < want) c->bvh_tasks.ensure(want);
   c->bvh_task_cnt.ensure(8);
+  const bool fixed_cap = c->bvh_task_cap > 0;
+  if (c->bvh_task_max <= 0) c->bvh_task_max = BVH_TASKS_MAX;  // test knob: overflowing threads finish their traversals
   bool list_free = false;  // set when the one-pass list would pass 2^30 pairs
-  for (int attempt = 0; attempt < 10; ++attempt) {
+  for (int attempt = 0; attempt < 6; ++attempt) {
     CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), st));
     c->n_pairs_dev.ensure(1);
-    if (list_free) CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), st));
+    CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), st));
     O.counter = c->counters.p;
     if (g.pa.n < 1024) { g.pa.ensure(1 << 16); g.pb.ensure(1 << 16); }
     if (g.ea.n < 1024) { g.ea.ensure(1 << 16); g.eb.ensure(1 << 16); }
     int* cnt = c->counters.p + 8;  // [8] PT, [9] EE appended, [10] overflow flag
     CUDA_CHECK(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), st));
     const int64_t cap_pt = (int64_t)std::min(g.pa.n, g.pb.n), cap_ee = (int64_t)std::min(g.ea.n, g.eb.n);
-    const int64_t tcap = c->bvh_task_cap > 0 ? c->bvh_task_cap : (int64_t)(c->bvh_tasks.n / 4);
-    int2* tbuf[2][2];
-    for (int a = 0; a < 2; ++a)
-      for (int b = 0; b < 2; ++b) tbuf[a][b] = reinterpret_cast<int2*>(c->bvh_tasks.p) + (2 * a + b) * tcap;
-    int* tcnt = c->bvh_task_cnt.p;  // [2 * (2 * class + buffer)] count, [+1] overflow
-    bool task_overflow = false;
-    const bool growable = c->bvh_task_cap <= 0;
-    int64_t need = 0;
+    unsigned long long* tcnt = c->bvh_task_cnt.p;  // [2 * (2 * class + buffer)] count, [+1] overflow
     if (!B.empty) {
       PairArgs A{c->tri, c->tri_sorted, c->edge, x, O, CP, CC, c->n_pairs_dev.p, g.pa, g.pb, cnt, cap_pt};
       PairArgs Ae = A;
       Ae.app_a = g.ea; Ae.app_b = g.eb; Ae.app_cnt = cnt + 1; Ae.app_cap = cap_ee; Ae.app_ee = 1;
-      const bool do_pt = V && F, do_ee = E > 1;
-      int64_t n_task[2] = {do_pt ? V : 0, do_ee ? E : 0};
-      for (int round = 0; n_task[0] || n_task[1]; ++round) {
-        const int cur = round & 1, nxt = cur ^ 1;
-        CUDA_CHECK(cudaMemsetAsync(tcnt + 4 * 0 + 2 * nxt, 0, 2 * sizeof(int), st));
-        CUDA_CHECK(cudaMemsetAsync(tcnt + 4 * 1 + 2 * nxt, 0, 2 * sizeof(int), st));
-        if (n_task[0]) {
-          BvhTasks K{round ? tbuf[0][cur] : nullptr, tcnt + 2 * cur, tcap, tbuf[0][nxt], tcnt + 2 * nxt, tcap,
-                     BVH_BUDGET, growable};
-          if (list_free)
-            k_bvh_points<MODE><<<grid_for(n_task[0], 128), 128, 0, st>>>(T, TT, V, c->sverts, c->tri, x,
-                                                                         B.filter_gap, A, K, tr.on);
-          else
-            k_bvh_points<-1><<<grid_for(n_task[0], 128), 128, 0, st>>>(T, TT, V, c->sverts, c->tri, x, B.filter_gap,
-                                                                       A, K, tr.on);
-          LAUNCH_CHECK();
-          tr.lap("points");
-          bvh_trace_stats(tr.on, "points", TT);
+      // The rounds of one class over the queries [q0, q1); false when a round
+      // overflowed the task lists (*need = the entries it requested): the
+      // threads abandoned work and the caller rolls the chunk back.
+      // (finish_here: a single query still overflowing at the largest lists
+      // finishes its traversal in its own threads -- guaranteed progress)
+      auto traverse = [&](int cls, int64_t q0, int64_t q1, int64_t* need, bool finish_here) -> bool {
+        const bool keep = fixed_cap || finish_here;
+        const int64_t tcap = fixed_cap ? c->bvh_task_cap
+                                       : std::min<int64_t>((int64_t)(c->bvh_tasks.n / 4), c->bvh_task_max);
+        int2* tb[2];
+        for (int b = 0; b < 2; ++b) tb[b] = reinterpret_cast<int2*>(c->bvh_tasks.p) + (2 * cls + b) * tcap;
+        unsigned long long* tc = tcnt + 4 * cls;
+        int64_t n_task = q1 - q0;
+        for (int round = 0; n_task; ++round) {
+          const int cur = round & 1, nxt = cur ^ 1;
+          CUDA_CHECK(cudaMemsetAsync(tc + 2 * nxt, 0, 2 * sizeof(unsigned long long), st));
+          BvhTasks K{round ? tb[cur] : nullptr, tc + 2 * cur, tcap, tb[nxt], tc + 2 * nxt, tcap, BVH_BUDGET, !keep,
+                     q0};
+          if (cls == 0) {
+            if (list_free)
+              k_bvh_points<MODE><<<grid_for(n_task, 128), 128, 0, st>>>(T, TT, q1, c->sverts, c->tri, x,
+                                                                        B.filter_gap, A, K, tr.on);
+            else
+              k_bvh_points<-1><<<grid_for(n_task, 128), 128, 0, st>>>(T, TT, q1, c->sverts, c->tri, x,
+                                                                      B.filter_gap, A, K, tr.on);
+            LAUNCH_CHECK();
+            tr.lap("points");
+            bvh_trace_stats(tr.on, "points", TT);
+          } else {
+            if (list_free)
+              k_bvh_edges<MODE><<<grid_for(n_task, 128), 128, 0, st>>>(T, TE, q1, c->edge, B.filter_gap, Ae, K,
+                                                                       tr.on);
+            else
+              k_bvh_edges<-1><<<grid_for(n_task, 128), 128, 0, st>>>(T, TE, q1, c->edge, B.filter_gap, Ae, K,
+                                                                     tr.on);
+            LAUNCH_CHECK();
+            tr.lap("edges");
+            bvh_trace_stats(tr.on, "edges", TE);
+          }
+          unsigned long long hh[2];
+          CUDA_CHECK(cudaMemcpyAsync(hh, tc + 2 * nxt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+          sync_stream(c);
+          const int64_t req = (int64_t)std::min<unsigned long long>(hh[0], 1ull << 62);
+          if (hh[1] && !keep) {
+            *need = req;
+            return false;
+          }
+          n_task = std::min<int64_t>(req, tcap);
+          if (tr.on && n_task)
+            fprintf(stderr, "  bvh %s round %d hands on %lld tasks\n", cls ? "edges" : "points", round + 1,
+                    (long long)n_task);
         }
-        if (n_task[1]) {
-          BvhTasks K{round ? tbuf[1][cur] : nullptr, tcnt + 4 + 2 * cur, tcap, tbuf[1][nxt], tcnt + 4 + 2 * nxt,
-                     tcap, BVH_BUDGET, growable};
-          if (list_free)
-            k_bvh_edges<MODE><<<grid_for(n_task[1], 128), 128, 0, st>>>(T, TE, E, c->edge, B.filter_gap, Ae, K,
-                                                                        tr.on);
-          else
-            k_bvh_edges<-1><<<grid_for(n_task[1], 128), 128, 0, st>>>(T, TE, E, c->edge, B.filter_gap, Ae, K, tr.on);
-          LAUNCH_CHECK();
-          tr.lap("edges");
-          bvh_trace_stats(tr.on, "edges", TE);
+        return true;
+      };
+      // each class in query chunks: a chunk whose rounds overflow is rolled
+      // back (its appended pairs / list-free count dropped; minima and flags
+      // are idempotent) and rerun with lists of the requested size, or --
+      // past BVH_TASKS_MAX -- split in four
+      for (int cls = 0; cls < 2; ++cls) {
+        const int64_t nq = cls == 0 ? ((V && F) ? V : 0) : (E > 1 ? E : 0);
+        int64_t q0 = 0, chunk = nq;
+        while (q0 < nq) {
+          const int64_t q1 = std::min(nq, q0 + chunk);
+          int app0 = 0;
+          unsigned long long np0 = 0;
+          if (q0 > 0) {  // the chunk's starting counts (zero for a class's first chunk)
+            CUDA_CHECK(cudaMemcpyAsync(&app0, cnt + cls, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaMemcpyAsync(&np0, c->n_pairs_dev.p, sizeof(np0), cudaMemcpyDeviceToHost, st));
+            sync_stream(c);
+          } else if (cls == 1) {
+            CUDA_CHECK(cudaMemcpyAsync(&np0, c->n_pairs_dev.p, sizeof(np0), cudaMemcpyDeviceToHost, st));
+            sync_stream(c);
+          }
+          int64_t need = 0;
+          const bool at_max = (int64_t)(c->bvh_tasks.n / 4) >= c->bvh_task_max;
+          if (traverse(cls, q0, q1, &need, at_max && q1 - q0 == 1)) {
+            q0 = q1;
+            continue;
+          }
+          CUDA_CHECK(cudaMemcpyAsync(cnt + cls, &app0, sizeof(int), cudaMemcpyHostToDevice, st));
+          CUDA_CHECK(cudaMemcpyAsync(c->n_pairs_dev.p, &np0, sizeof(np0), cudaMemcpyHostToDevice, st));
+          sync_stream(c);
+          const int64_t want_n = need + need / 4 + 1024;
+          if (want_n <= c->bvh_task_max && (int64_t)(c->bvh_tasks.n / 4) < want_n) {
+            c->bvh_tasks.ensure(4 * (size_t)want_n);
+          } else {
+            if ((int64_t)(c->bvh_tasks.n / 4) < c->bvh_task_max) c->bvh_tasks.ensure(4 * (size_t)c->bvh_task_max);
+            chunk = std::max<int64_t>(1, (q1 - q0) / 4);
+          }
+          if (tr.on)
+            fprintf(stderr, "  bvh %s chunk [%lld, %lld) overflowed (%lld tasks): retry with %lld per list, chunk %lld\n",
+                    cls ? "edges" : "points", (long long)q0, (long long)q1, (long long)need,
+                    (long long)(c->bvh_tasks.n / 4), (long long)chunk);
         }
-        int h[8];
-        CUDA_CHECK(cudaMemcpyAsync(h, tcnt, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
-        sync_stream(c);
-        if (h[2 * nxt + 1] || h[4 + 2 * nxt + 1]) {
-          task_overflow = true;
-          need = std::max<int64_t>(need, std::max<int64_t>(h[2 * nxt], h[4 + 2 * nxt]));
-          if (growable) break;  // threads abandoned work: rerun with lists of the requested size
-        }
-        n_task[0] = std::min<int64_t>(h[2 * nxt], tcap);
-        n_task[1] = std::min<int64_t>(h[4 + 2 * nxt], tcap);
-        if (tr.on && (n_task[0] || n_task[1]))
-          fprintf(stderr, "  bvh round %d hands on %lld + %lld tasks\n", round + 1, (long long)n_task[0],
-                  (long long)n_task[1]);
-      }
-      if (task_overflow && growable) {  // lists of the requested size (all four), then from scratch
-        c->bvh_tasks.ensure(4 * (size_t)(need + need / 4 + 1024));
-        continue;
       }
       if (!list_free) {
         k_pairs_app<MODE><<<8 * 148, 256, 0, st>>>(cnt, cap_pt, cap_ee, g.pa, g.pb, g.ea, g.eb, A);

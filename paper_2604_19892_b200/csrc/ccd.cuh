@@ -685,23 +685,16 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
     BpGrid B = build_bp(c, x, pinf, 0.0, infl, bodies ? 1 : 0, gmode);
     lap("grid", 0);
     if (!exact_set && c->ccd_prefilter) B.T.objmot = c->obj_mot.p;
-    // one enumeration + pair pass of MODE over the boxes of G (grid rebuilt
-    // for the list-free rerun when the BVH's one-pass list would pass 2^30)
-    // (crowded calls are timed: bp.cuh BP_GRID_AUTO keeps each method's cost)
-    auto enumerate = [&](auto mode_tag, BpGrid& G, BpOut O, const double* inf, int* fl) -> int64_t {
+    // one enumeration + pair pass of MODE over the boxes of G: the BVH when
+    // build_bp left no grid, else the grid (crowded calls are timed:
+    // bp.cuh BP_GRID_AUTO keeps each method's cost)
+    auto enumerate = [&](auto mode_tag, BpGrid& G, BpOut O, int* fl) -> int64_t {
       constexpr int M = decltype(mode_tag)::value;
       const auto t0 = std::chrono::steady_clock::now();
       const int method = G.has_grid ? 0 : 1;
-      int64_t n = -1;
-      if (!G.has_grid) {
-        n = run_bvh<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
-        if (n < 0) {
-          const double* mot = G.T.objmot;
-          G = build_bp(c, x, pinf, 0.0, inf, 0, BP_GRID_ALWAYS);
-          G.T.objmot = mot;
-        }
-      }
-      if (n < 0) n = run_bp<M>(c, x, G, O, ContactParams{}, CcdParams{p, c->cfg.alpha_l, c->bs}, fl);
+      const CcdParams cc{p, c->cfg.alpha_l, c->bs};
+      const int64_t n = G.has_grid ? run_bp<M>(c, x, G, O, ContactParams{}, cc, fl)
+                                   : run_bvh<M>(c, x, G, O, ContactParams{}, cc, fl);
       if (G.crowd > 0.0) {  // run_bvh / run_bp end on a host sync: the interval is the enumeration's
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         double& e = c->enum_ms.ms[method][G.crowd_bucket];
@@ -724,7 +717,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
       O.alpha_d = c->alpha_d;
       O.min_alpha = d_min;
       c->rb_extra = d_min;  // read back with run_bp's counters: no extra sync
-      int64_t n = enumerate(std::integral_constant<int, BP_CCD>{}, B, O, infl, &cert_fail_p);
+      int64_t n = enumerate(std::integral_constant<int, BP_CCD>{}, B, O, &cert_fail_p);
       c->rb_extra = nullptr;
       if (!exact_set || n <= O.cap) {
         R.n_pairs = n;
@@ -789,7 +782,7 @@ static CcdResult ccd_clamp(mp_ctx* c, const double* x, const double* p, double p
         O.alpha_d = c->alpha_d;
         int fail = 0;
         lap("cert-grid", 0);
-        const int64_t nc = enumerate(std::integral_constant<int, BP_CERT>{}, B2, O, c->infl, &fail);
+        const int64_t nc = enumerate(std::integral_constant<int, BP_CERT>{}, B2, O, &fail);
         R.certified = fail == 0;
         lap("cert", nc);
       }

@@ -259,8 +259,9 @@ struct mp_ctx {
   DBuf<int> bvh_tri_order, bvh_edge_order, bvh_key, bvh_val;
   DBuf<float4> bvh_tri_nodes, bvh_edge_nodes;  // BvhNode = 5 float4
   DBuf<int2> bvh_tasks;              // 4 task lists (class x ping-pong) of the load-balanced traversal
-  DBuf<int> bvh_task_cnt;
+  DBuf<unsigned long long> bvh_task_cnt;
   int64_t bvh_task_cap = 0;          // MP_OPT_BVH_TASKS test knob: fixed task-list capacity (0: grown as needed)
+  int64_t bvh_task_max = 0;          // largest grown task list (0: BVH_TASKS_MAX; MP_OPT_BVH_TASKS < 0 lowers it)
   DBuf<unsigned long long> crowd_dev;  // grid crowding probe (bp.cuh BP_GRID_AUTO)
   struct EnumTimes {                 // crowded CCD enumerations: ms per log2 crowding bucket, grid / BVH (< 0 unknown)
     double ms[2][32];

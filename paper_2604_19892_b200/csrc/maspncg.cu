@@ -865,7 +865,10 @@ int mp_set_option(mp_ctx* c, int option, int64_t value) {
     else if (option == MP_OPT_CCD_BODIES) c->ccd_bodies = value != 0;
     else if (option == MP_OPT_CCD_LOCAL) c->ccd_local = value != 0;
     else if (option == MP_OPT_CCD_BVH) c->ccd_bvh = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
-    else if (option == MP_OPT_BVH_TASKS) c->bvh_task_cap = std::max<int64_t>(0, value);
+    else if (option == MP_OPT_BVH_TASKS) {
+      c->bvh_task_cap = std::max<int64_t>(0, value);
+      c->bvh_task_max = value < 0 ? -value : 0;
+    }
     else if (option == MP_OPT_APPEND_LIMIT) {
       const int lim = (int)std::max<int64_t>(64, std::min<int64_t>(HQ_APPEND_LIMIT, value <= 0 ? HQ_APPEND_LIMIT : value));
       CUDA_CHECK(cudaMemcpyToSymbol(g_append_limit, &lim, sizeof(int)));

@@ -134,14 +134,16 @@ def test_c2_ccd_bvh_vs_grid(c2, scale):
 @pytest.mark.gpu
 def test_c2_ccd_bvh_task_overflow(c2):
     """MP_OPT_BVH_TASKS (15): with hand-on task lists far too small, threads
-    finish their own traversals -- the same pair count and results."""
+    finish their own traversals (fixed lists) or the queries are split into
+    chunks rolled back and rerun (capped growth) -- the same pair count and
+    results."""
     g, _, ctx = c2
     p = 400.0 * g["p"]
     try:
         ctx.set_option(14, 0)
         ref = ctx.ccd(g["x0"], p, exact_set=False)
         ctx.set_option(14, 1)
-        for cap in (64, 4096):
+        for cap in (16384, -16384):  # fixed lists; grown lists capped low (query chunks)
             ctx.set_option(15, cap)
             out = ctx.ccd(g["x0"], p, exact_set=False)
             assert out[4] == ref[4]
