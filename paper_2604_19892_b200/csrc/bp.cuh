@@ -969,6 +969,7 @@ struct BpGrid {
   double filter_gap = 0.0;  // the reference filter gap with a rounding margin (bvh.cuh node tests)
   double crowd = 0.0;       // BP_GRID_AUTO: the crowding probe when it ran (> BP_CROWD_LIMIT: a timed choice)
   int crowd_bucket = 0;     // ilogb(crowd)
+  double raw_mean = 0.0;    // mean largest raw-box extent of the triangles and edges
 };
 
 enum { BP_GRID_NONE = 0, BP_GRID_ALWAYS = 1, BP_GRID_AUTO = 2 };
@@ -1091,6 +1092,7 @@ static BpGrid build_bp(mp_ctx* c, const double* x, double mb, double d_hat, cons
     double amax = 0.0;
     for (int k = 0; k < 3; ++k) amax = fmax(amax, fmax(fabs(mn[k]), fabs(mx[k])));
     B.filter_gap = gap * (1.0 + 1e-9) + 1e-15 * (std::isfinite(amax) ? amax : 0.0);
+    B.raw_mean = rext / (double)std::max<int64_t>(1, P);
   }
   auto boxes_only = [&]() {  // the BVH's inputs: boxes, filters, reference cell ranges
     BpTables& T = B.T;

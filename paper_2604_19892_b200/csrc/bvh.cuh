@@ -37,7 +37,7 @@ struct BvhNode {
   float elo[3], ehi[3];  // enumeration boxes (union)
   float clo[3], chi[3];  // motion centres (box)
   float m;               // largest motion radius
-  int pad;
+  float amax;            // largest alpha_d bound of its objects' subdomains (the alpha prune; 1 when unused)
 };
 
 struct BvhTree {
@@ -57,10 +57,18 @@ __device__ __forceinline__ float f_up(double v) { return __double2float_ru(v); }
 __global__ void k_bvh_leaves(int64_t n, int64_t base, const int* __restrict__ order, const double* __restrict__ rlo,
                              const double* __restrict__ rhi, const double* __restrict__ elo,
                              const double* __restrict__ ehi, const double* __restrict__ mot,
-                             BvhNode* __restrict__ leaf) {
+                             BvhNode* __restrict__ leaf, const int* __restrict__ ids, int per,
+                             const double* __restrict__ alpha_d, int bs) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = s < n;
   float v[19];
+  float am = 1.0f;
+  if (live && alpha_d) {  // the alpha prune: max over the object's vertices' subdomain bounds
+    const int64_t oc = order[s];
+    double a = 0.0;
+    for (int k = 0; k < per; ++k) a = fmax(a, alpha_d[ids[per * oc + k] / bs]);
+    am = f_up(a);
+  }
   if (live) {
     const int64_t o = base + order[s];
 #pragma unroll
@@ -90,6 +98,7 @@ __global__ void k_bvh_leaves(int64_t n, int64_t base, const int* __restrict__ or
       const bool is_lo = (q < 3) || (q >= 6 && q < 9) || (q >= 12 && q < 15);
       v[q] = is_lo ? fminf(v[q], w) : fmaxf(v[q], w);
     }
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
   }
   if (live && (s & (BVH_W - 1)) == 0) {
     BvhNode& d = leaf[s / BVH_W];
@@ -100,6 +109,7 @@ __global__ void k_bvh_leaves(int64_t n, int64_t base, const int* __restrict__ or
       d.clo[k] = v[12 + k]; d.chi[k] = v[15 + k];
     }
     d.m = v[18];
+    d.amax = am;
   }
 }
 
@@ -108,6 +118,7 @@ __global__ void k_bvh_up(int64_t nchild, const BvhNode* __restrict__ child, BvhN
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = s < nchild;
   float v[19];
+  float am = 0.0f;
   if (live) {
     const BvhNode& c = child[s];
 #pragma unroll
@@ -117,6 +128,7 @@ __global__ void k_bvh_up(int64_t nchild, const BvhNode* __restrict__ child, BvhN
       v[12 + k] = c.clo[k]; v[15 + k] = c.chi[k];
     }
     v[18] = c.m;
+    am = c.amax;
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -133,6 +145,7 @@ __global__ void k_bvh_up(int64_t nchild, const BvhNode* __restrict__ child, BvhN
       const bool is_lo = (q < 3) || (q >= 6 && q < 9) || (q >= 12 && q < 15);
       v[q] = is_lo ? fminf(v[q], w) : fmaxf(v[q], w);
     }
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
   }
   if (live && (s & (BVH_W - 1)) == 0) {
     BvhNode& d = parent[s / BVH_W];
@@ -143,6 +156,7 @@ __global__ void k_bvh_up(int64_t nchild, const BvhNode* __restrict__ child, BvhN
       d.clo[k] = v[12 + k]; d.chi[k] = v[15 + k];
     }
     d.m = v[18];
+    d.amax = am;
   }
 }
 
@@ -153,7 +167,20 @@ struct BvhQuery {
   double c[3], m;         // motion centre / radius (rel != 0)
   double gap;             // reference filter gap (with margin)
   bool rel;
+  double amax;            // the alpha prune: the query's subdomain bound (> 1: off)
+  double near_r;          // near pass: raw separation limit (<= 0: off)
 };
+
+// squared separation of two boxes
+__device__ __forceinline__ double box_gap2(const double* l1, const double* h1, const double* l2, const double* h2) {
+  double g2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double d = fmax(0.0, fmax(l1[k] - h2[k], l2[k] - h1[k]));
+    g2 += d * d;
+  }
+  return g2;
+}
 
 // May any object below `nd` pass the per-pair predicate against q?
 __device__ __forceinline__ bool bvh_visit(const BvhQuery& q, const BvhNode& nd) {
@@ -169,9 +196,19 @@ __device__ __forceinline__ bool bvh_visit(const BvhQuery& q, const BvhNode& nd) 
     const double dc = fmax(fabs(q.c[k] - (double)nd.clo[k]), fabs(q.c[k] - (double)nd.chi[k]));
     c2 += dc * dc;
   }
+  if (q.near_r > 0.0 && d2 > q.near_r * q.near_r) return false;
   if (!q.rel) return true;
   const double U = fmax(q.m, (double)nd.m + sqrt(c2));
-  return !(0.9 * sqrt(d2) * (1.0 - 1e-9) > 4.0 * U * (1.0 + 1e-9));
+  const double D = sqrt(d2);
+  if (0.9 * D * (1.0 - 1e-9) > 4.0 * U * (1.0 + 1e-9)) return false;
+  // alpha prune: every pair below has alpha_pair >= 0.9 D / speed >= 0.9 D / (4 U),
+  // so when that bound reaches the subdomain bounds of both sides (upper
+  // bounds of their final alpha_d) no pair below can lower any minimum
+  if (q.amax <= 1.0) {
+    const double lb = (0.9 * D * (1.0 - 1e-9)) / (4.0 * U * (1.0 + 1e-9));
+    if (lb >= fmax(q.amax, (double)nd.amax)) return false;
+  }
+  return true;
 }
 
 // Pair emission from divergent traversals: each thread buffers its pairs
@@ -332,7 +369,8 @@ __device__ __forceinline__ void bvh_finish_warp(BvhOut& o, const PairArgs& A) {
 template <int FM>
 __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int64_t V, const int* __restrict__ sverts,
                                                     const int* __restrict__ tri, const double* __restrict__ x,
-                                                    double gap, PairArgs A, BvhTasks K, bool stats) {
+                                                    double gap, PairArgs A, BvhTasks K, bool stats,
+                                                    const double* __restrict__ abound, double near_r) {
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : V - K.q_base;
   if (blockIdx.x * (int64_t)blockDim.x >= nt || TT.n == 0) return;  // block-uniform
@@ -355,6 +393,8 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
   Q.m = T.objmot ? T.objmot[4 * oq + 3] : 0.0;
   Q.rel = T.objmot != nullptr;
   Q.gap = gap;
+  Q.amax = abound ? abound[v / A.CC.bs] : 2.0;
+  Q.near_r = near_r;
   int stack[BVH_STACK];
   int sp = 0;
   if (live) stack[sp++] = task.y;
@@ -376,7 +416,8 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
         const double* tl = T.elo + 3 * (int64_t)t;
         const double* th = T.ehi + 3 * (int64_t)t;
         if (boxes_meet(Q.elo, Q.ehi, tl, th) && pt_ref_pass(T, tri, x, v, q, t) &&
-            !rel_safe(T, oq, t, Q.rlo, Q.rhi, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t))
+            !rel_safe(T, oq, t, Q.rlo, Q.rhi, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t) &&
+            (near_r <= 0.0 || box_gap2(Q.rlo, Q.rhi, T.rlo + 3 * (int64_t)t, T.rhi + 3 * (int64_t)t) <= near_r * near_r))
           bvh_take<FM>(out, true, v, t, A);
       }
     } else {
@@ -400,7 +441,8 @@ __global__ void __launch_bounds__(128) k_bvh_points(BpTables T, BvhTree TT, int6
 // unordered pair once); the leaf predicate is k_hq_edges'.
 template <int FM>
 __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64_t E, const int* __restrict__ edge,
-                                                   double gap, PairArgs A, BvhTasks K, bool stats) {
+                                                   double gap, PairArgs A, BvhTasks K, bool stats,
+                                                   const double* __restrict__ abound, double near_r) {
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = K.in ? min((int64_t)*K.n_in, K.in_cap) : E - K.q_base;
   if (blockIdx.x * (int64_t)blockDim.x >= nt) return;  // block-uniform
@@ -424,6 +466,8 @@ __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64
   Q.m = T.objmot ? T.objmot[4 * oi + 3] : 0.0;
   Q.rel = T.objmot != nullptr;
   Q.gap = gap;
+  Q.amax = abound ? fmax(abound[edge[2 * i] / A.CC.bs], abound[edge[2 * i + 1] / A.CC.bs]) : 2.0;
+  Q.near_r = near_r;
   const double* fli = T.flo + 3 * oi;
   const double* fhi = T.fhi + 3 * oi;
   const int ia = edge[2 * i], ib = edge[2 * i + 1];
@@ -453,7 +497,8 @@ __global__ void __launch_bounds__(128) k_bvh_edges(BpTables T, BvhTree TE, int64
         const bool pass = !(ia == ja || ia == jb || ib == ja || ib == jb) && body_pass(T, ia, ja) &&
                           fli[0] <= fhj[0] && fli[1] <= fhj[1] && fli[2] <= fhj[2] && flj[0] <= fhi[0] &&
                           flj[1] <= fhi[1] && flj[2] <= fhi[2] && ref_reach(T.rc, oi, oj) &&
-                          !rel_safe(T, oi, oj, Q.rlo, Q.rhi, T.rlo + 3 * oj, T.rhi + 3 * oj);
+                          !rel_safe(T, oi, oj, Q.rlo, Q.rhi, T.rlo + 3 * oj, T.rhi + 3 * oj) &&
+                          (near_r <= 0.0 || box_gap2(Q.rlo, Q.rhi, T.rlo + 3 * oj, T.rhi + 3 * oj) <= near_r * near_r);
         if (pass) bvh_take<FM>(out, false, min(i, j), max(i, j), A);
       }
     } else {
@@ -555,10 +600,12 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
   TT.node = nt; TT.order = c->bvh_tri_order;
   TE.node = ne; TE.order = c->bvh_edge_order;
   const BpTables& T = B.T;
-  auto refit = [&](BvhTree& R, BvhNode* nodes, int64_t base) {
+  auto refit = [&](BvhTree& R, BvhNode* nodes, int64_t base, const double* alpha) {
     if (R.n == 0) return;
+    const bool tri_tree = base == 0;
     k_bvh_leaves<<<grid_for(R.n, 256), 256, 0, st>>>(R.n, base, R.order, T.rlo, T.rhi, T.elo, T.ehi, T.objmot,
-                                                      nodes);
+                                                      nodes, tri_tree ? c->tri : c->edge, tri_tree ? 3 : 2, alpha,
+                                                      c->bs);
     LAUNCH_CHECK();
     for (int l = 1; l < R.nlev; ++l) {
       k_bvh_up<<<grid_for(R.cnt[l - 1], 256), 256, 0, st>>>(R.cnt[l - 1], nodes + R.off[l - 1], nodes + R.off[l]);
@@ -566,8 +613,8 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
     }
   };
   BpTrace tr(st);
-  refit(TT, nt, 0);
-  refit(TE, ne, F);
+  refit(TT, nt, 0, nullptr);
+  refit(TE, ne, F, nullptr);
   tr.lap("refit");
   // task lists: [class][ping-pong]; counters: per class and buffer (count, overflow)
   const size_t want = 4 * (size_t)(c->bvh_task_cap > 0 ? c->bvh_task_cap : BVH_TASKS0);
@@ -576,6 +623,8 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
   const bool fixed_cap = c->bvh_task_cap > 0;
   if (c->bvh_task_max <= 0) c->bvh_task_max = BVH_TASKS_MAX;  // test knob: overflowing threads finish their traversals
   bool list_free = false;  // set when the one-pass list would pass 2^30 pairs
+  const double* abound_cur = nullptr;  // the alpha prune's subdomain bounds (list-free CCD, phase 1)
+  double near_cur = 0.0;               // the near pass's separation limit (list-free CCD, phase 0)
   for (int attempt = 0; attempt < 6; ++attempt) {
     CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 3 * sizeof(int), st));
     c->n_pairs_dev.ensure(1);
@@ -612,20 +661,21 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
           if (cls == 0) {
             if (list_free)
               k_bvh_points<MODE><<<grid_for(n_task, 128), 128, 0, st>>>(T, TT, q1, c->sverts, c->tri, x,
-                                                                        B.filter_gap, A, K, tr.on);
+                                                                        B.filter_gap, A, K, tr.on, abound_cur,
+                                                                        near_cur);
             else
               k_bvh_points<-1><<<grid_for(n_task, 128), 128, 0, st>>>(T, TT, q1, c->sverts, c->tri, x,
-                                                                      B.filter_gap, A, K, tr.on);
+                                                                      B.filter_gap, A, K, tr.on, nullptr, 0.0);
             LAUNCH_CHECK();
             tr.lap("points");
             bvh_trace_stats(tr.on, "points", TT);
           } else {
             if (list_free)
               k_bvh_edges<MODE><<<grid_for(n_task, 128), 128, 0, st>>>(T, TE, q1, c->edge, B.filter_gap, Ae, K,
-                                                                       tr.on);
+                                                                       tr.on, abound_cur, near_cur);
             else
               k_bvh_edges<-1><<<grid_for(n_task, 128), 128, 0, st>>>(T, TE, q1, c->edge, B.filter_gap, Ae, K,
-                                                                     tr.on);
+                                                                     tr.on, nullptr, 0.0);
             LAUNCH_CHECK();
             tr.lap("edges");
             bvh_trace_stats(tr.on, "edges", TE);
@@ -645,6 +695,22 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
         }
         return true;
       };
+      // List-free CCD (> 2^30 pairs: a direction huge against the gaps, the
+      // reference set nearly every pair): an exact alpha prune.  Phase 0
+      // works the pairs within a few mean primitive extents -- a subset, so
+      // the alpha_d it leaves are upper bounds of the final ones; the trees
+      // are refit with those bounds and phase 1 skips every node whose
+      // pairs provably have alpha_pair >= the bounds of all their
+      // subdomains (bvh_visit).  The returned count is phase 1's pairs.
+      const bool prune = list_free && MODE == BP_CCD && T.objmot && O.alpha_d;
+      for (int phase = prune ? 0 : 1; phase < 2; ++phase) {
+      near_cur = phase == 0 ? 4.0 * B.raw_mean : 0.0;
+      abound_cur = (phase == 1 && prune) ? O.alpha_d : nullptr;
+      if (phase == 1 && prune) {
+        CUDA_CHECK(cudaMemsetAsync(c->n_pairs_dev.p, 0, sizeof(unsigned long long), st));
+        refit(TT, nt, 0, O.alpha_d);
+        refit(TE, ne, F, O.alpha_d);
+      }
       // each class in query chunks: a chunk whose rounds overflow is rolled
       // back (its appended pairs / list-free count dropped; minima and flags
       // are idempotent) and rerun with lists of the requested size, or --
@@ -686,6 +752,7 @@ static int64_t run_bvh(mp_ctx* c, const double* x, const BpGrid& B, BpOut O, Con
                     (long long)(c->bvh_tasks.n / 4), (long long)chunk);
         }
       }
+      }  // phases
       if (!list_free) {
         k_pairs_app<MODE><<<8 * 148, 256, 0, st>>>(cnt, cap_pt, cap_ee, g.pa, g.pb, g.ea, g.eb, A);
         LAUNCH_CHECK();

@@ -157,8 +157,10 @@ def test_c2_ccd_bvh_task_overflow(c2):
 @pytest.mark.gpu
 def test_c2_ccd_bvh_list_free(c2):
     """Past the one-pass list limit (lowered by MP_OPT_APPEND_LIMIT, 8) the
-    BVH reruns list-free, working each pair where it is found: the same
-    64-bit pair count, alpha_d, minimum, certificate and x_new."""
+    BVH reruns list-free, working each pair where it is found, with the
+    exact alpha prune (a near pass bounds alpha_d, then subtrees whose pairs
+    cannot lower any bound are skipped): the same alpha_d, minimum,
+    certificate and x_new; the count is the pairs worked (<= the set)."""
     g, _, ctx = c2
     p = 40.0 * g["p"]
     try:
@@ -167,7 +169,7 @@ def test_c2_ccd_bvh_list_free(c2):
         ctx.set_option(14, 1)
         ctx.set_option(8, 4096)
         out = ctx.ccd(g["x0"], p, exact_set=False)
-        assert ref[4] > 4096 and out[4] == ref[4]
+        assert ref[4] > 4096 and 0 < out[4] <= ref[4]
         assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
         assert out[2] == ref[2] and out[3] == ref[3]
     finally:
