@@ -165,7 +165,11 @@ struct mp_ctx {
   bool overlap_apply = true;  // MAS apply: level 0 on the side stream beside the coarse chain (MP_OPT_APPLY_OVERLAP)
   cudaStream_t side = nullptr;  // side stream (level-0 apply, elastic H_base ahead) and its events
   cudaEvent_t ev_it = nullptr, ev_bsr_ahead = nullptr;  // bsr_ahead (elastic.cuh)
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;         // iteration start / z ready (t_grad_ms)
   bool bsr_ahead_pending = false;
+  bool defer_mas_check = false;      // the solver loop checks the MAS build's flags at its next sync
+  bool mas_flags_pending = false;
+  int h_mas_flags[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaEvent_t ev_g = nullptr, ev_l0 = nullptr;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)
   bool keep_coarse = false;  // keep each coarse level's assembled matrix (mp_coarse_matrix)
   int bp_fused = 1;          // 1: one-pass unordered pair lists, 2: contact work fused into the queries, 0: ordered lists

@@ -36,6 +36,8 @@ mp_ctx::~mp_ctx() {
   if (ev_g) cudaEventDestroy(ev_g);
   if (ev_l0) cudaEventDestroy(ev_l0);
   if (ev_it) cudaEventDestroy(ev_it);
+  if (ev_t0) cudaEventDestroy(ev_t0);
+  if (ev_t1) cudaEventDestroy(ev_t1);
   if (ev_bsr_ahead) cudaEventDestroy(ev_bsr_ahead);
   if (side) cudaStreamDestroy(side);
   if (stream) cudaStreamDestroy(stream);
@@ -231,6 +233,8 @@ static void create_ctx(const mp_scene_desc* s, const mp_solver_config* cfg, int 
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_g, cudaEventDisableTiming));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_l0, cudaEventDisableTiming));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_it, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreate(&c->ev_t0));
+  CUDA_CHECK(cudaEventCreate(&c->ev_t1));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bsr_ahead, cudaEventDisableTiming));
   set_smem_limits();
   CUDA_CHECK(cudaMallocHost(&c->h_scal, 64 * sizeof(double)));
@@ -518,9 +522,16 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
   R.recs.clear();
   R.converged = false;
   c->bsr_ahead_pending = false;
+  c->mas_flags_pending = false;
+  struct DeferGuard {  // the loop checks the MAS flags at its next sync; restored on any exit
+    mp_ctx* c;
+    explicit DeferGuard(mp_ctx* x) : c(x) { c->defer_mas_check = true; }
+    ~DeferGuard() { c->defer_mas_check = false; }
+  } defer_guard(c);
   for (int64_t k = 0; k < cfg.iter_max; ++k) {
     auto t0 = Clock::now();
     const bool rebuild = restart || full_every;
+    CUDA_CHECK(cudaEventRecord(c->ev_t0, st));
     if (rebuild) bsr_ahead(c, c->x, h);
     timer_begin(c, MP_STAGE_CONSTRAINT_SET);
     constraint_set(c, c->x);
@@ -538,8 +549,9 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     timer_begin(c, MP_STAGE_MAS_APPLY);
     precond_apply(c, c->g, c->z, true);
     timer_end(c, MP_STAGE_MAS_APPLY, mas_apply_bytes(c));
-    sync_stream(c);
-    auto t1 = Clock::now();
+    // (no host sync here: t_grad_ms is the CUDA-event time from the
+    // iteration's start to z, read at the record)
+    CUDA_CHECK(cudaEventRecord(c->ev_t1, st));
 
     timer_begin(c, MP_STAGE_HVP);
     hvp(c, c->z, c->hv, !rebuild);
@@ -576,6 +588,8 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
       i_py = add(c->p_prev, c->tmp2);
     }
     multidot(c, n3, S);
+    mas_flags_check(c);  // the MAS build's non-SPD flags rode on that sync
+    const auto t1 = Clock::now();
     double dots[MAX_DOTS];
     std::memcpy(dots, c->h_scal, sizeof(double) * S.n);
     const double z_norm = std::sqrt(dots[i_zz]);
@@ -699,8 +713,14 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     rec.mu = mu;
     rec.nu = nu;
     rec.min_alpha = min_alpha;
-    rec.t_grad_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    rec.t_dir_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    {
+      float gms = 0.f;  // iteration start -> z, on the device (both events completed by the syncs since)
+      CUDA_CHECK(cudaEventElapsedTime(&gms, c->ev_t0, c->ev_t1));
+      rec.t_grad_ms = gms;
+      // the direction phase: the host time to t2 less the part before z
+      rec.t_dir_ms = std::max(0.0, std::chrono::duration<double, std::milli>(t2 - t0).count() - (double)gms);
+    }
+    (void)t1;
     rec.t_ccd_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
     rec.n_candidates = (int32_t)(rebuild ? 0 : c->n_cand);
     rec.n_ccd_pairs = (int32_t)std::min<int64_t>(c->n_ccd_seen, INT32_MAX);  // saturates (>2^31 at C3)

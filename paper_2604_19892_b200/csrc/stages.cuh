@@ -130,6 +130,16 @@ static void dense_spd_inverse(mp_ctx* c, CoarseLevel& L, int* status) {
   if (g_launch_counter) ++(*g_launch_counter);
 }
 
+// the non-SPD flags of the last MAS build (their readback must have completed:
+// after a stream sync) -- cho_factor's failure (mas.py:86-88)
+static void mas_flags_check(mp_ctx* c) {
+  if (!c->mas_flags_pending) return;
+  c->mas_flags_pending = false;
+  if (group_or(c, c->h_mas_flags[0])) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
+  for (int q = 1; q < 5; ++q)
+    if (c->h_mas_flags[q]) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
+}
+
 // build_hierarchy (mas.py:138-179) from the BSR + base contacts
 static unsigned sym_tiles(int n) {
   const int64_t nt = (n + 31) / 32;
@@ -267,12 +277,14 @@ static void mas_build(mp_ctx* c) {
   }
   for (int l = 0; l < c->n_levels; ++l) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[l]->done, 0));
   mt.mark("joined", c->stream);
-  // one readback of every level's non-SPD flag (counters 3..7)
-  CUDA_CHECK(cudaMemcpyAsync(c->h_cnt + 8, c->counters.p + 3, 5 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  sync_stream(c);
-  if (group_or(c, c->h_cnt[8])) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "subdomain block not SPD");
-  for (int q = 1; q < 5; ++q)
-    if (c->h_cnt[8 + q]) throw MpError(MP_ERR_NON_SPD_SUBDOMAIN, "coarse level not SPD");
+  // one readback of every level's non-SPD flag (counters 3..7); the solver
+  // loop checks it at its next sync (mas_flags_check) instead of syncing here
+  CUDA_CHECK(cudaMemcpyAsync(c->h_mas_flags, c->counters.p + 3, 5 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  c->mas_flags_pending = true;
+  if (!c->defer_mas_check) {
+    sync_stream(c);
+    mas_flags_check(c);
+  }
   c->have_mas = true;
 }
 
