@@ -247,10 +247,11 @@ enum { MP_OPT_CCD_EXACT_SET = 1, MP_OPT_RECORD_ENERGY = 2, MP_OPT_APPLY_TMA = 3,
        MP_OPT_CCD_PREFILTER = 11 /* tight CCD: 1 (default) exact relative-motion pair prefilter, 0 off; same results */,
        MP_OPT_CCD_BODIES = 12 /* tight CCD: 1 two passes (same-body / cross-body centres), 0 (default) one global centre; same results */,
        MP_OPT_CCD_LOCAL = 13 /* tight CCD: 1 per-subdomain motion centres when they inflate less, 0 (default) global; same results */,
-       MP_OPT_CCD_BVH = 14 /* tight CCD / certificate enumeration: 0 hierarchical grid, 1 motion-aware BVH, 2 (default) the BVH when
-                              the enumeration boxes average > 1.6x the raw ones; same results */,
-       MP_OPT_BVH_TASKS = 15 /* test knob: fixed capacity of the BVH's hand-on task lists (0, default: grown as needed);
-                                a full list makes threads finish their own traversal; same results */ };
+       MP_OPT_CCD_BVH = 14 /* tight CCD / certificate enumeration: 0 hierarchical grid, 1 motion-aware BVH, 2 (default) per
+                              call: the grid unless it is crowded, then the method measured faster; same results */,
+       MP_OPT_BVH_TASKS = 15 /* test knob for the BVH's hand-on task lists: > 0 a fixed capacity (a full list makes
+                                threads finish their own traversals); < 0 grown as needed up to -value, then the
+                                queries split in chunks; 0 (default) grown up to 2^27; same results */ };
 int mp_set_option(mp_ctx* ctx, int option, int64_t value);
 int mp_stage_stats(mp_ctx* ctx, int stage, double* total_ms, int64_t* count, double* bytes);
 
