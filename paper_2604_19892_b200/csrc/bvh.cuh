@@ -22,6 +22,11 @@
 // skip is implied for each object below, so the objects reached and tested
 // with the unchanged per-pair predicate are a superset of the passing ones:
 // the emitted pair set is the grid's, bit for bit.
+//
+// Scale: threads hand long traversals on as tasks (rounds, lists grown to
+// the requested size, query chunks past the memory budget); past the 2^30
+// one-pass list the pairs are worked where they are found (list-free), and
+// the CCD then adds an exact alpha prune (run_bvh).
 #pragma once
 
 #include "bp.cuh"
