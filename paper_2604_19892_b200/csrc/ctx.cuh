@@ -16,6 +16,7 @@
 #include <condition_variable>
 #include <atomic>
 #include <chrono>
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -168,6 +169,7 @@ struct mp_ctx {
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;         // iteration start / z ready (t_grad_ms)
   bool bsr_ahead_pending = false;
   bool defer_mas_check = false;      // the solver loop checks the MAS build's flags at its next sync
+  std::function<void()> mas_overlap; // launched by mas_build beside the coarse assembly (the loop's gradient)
   bool mas_flags_pending = false;
   int h_mas_flags[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaEvent_t ev_g = nullptr, ev_l0 = nullptr;   // gradient: one fused pass (k_grad_fused) or per-tet scratch + gather (MP_OPT_GRAD_FUSED)

@@ -526,7 +526,10 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
   struct DeferGuard {  // the loop checks the MAS flags at its next sync; restored on any exit
     mp_ctx* c;
     explicit DeferGuard(mp_ctx* x) : c(x) { c->defer_mas_check = true; }
-    ~DeferGuard() { c->defer_mas_check = false; }
+    ~DeferGuard() {
+      c->defer_mas_check = false;
+      c->mas_overlap = nullptr;  // (it captures this loop's locals)
+    }
   } defer_guard(c);
   for (int64_t k = 0; k < cfg.iter_max; ++k) {
     auto t0 = Clock::now();
@@ -536,16 +539,23 @@ static void advance_loop_body(mp_ctx* c, double h, LoopResult& R) {
     timer_begin(c, MP_STAGE_CONSTRAINT_SET);
     constraint_set(c, c->x);
     timer_end(c, MP_STAGE_CONSTRAINT_SET, 0.0);
+    bool grad_done = false;
+    auto grad = [&]() {
+      timer_begin(c, MP_STAGE_GRADIENT);
+      gradient(c, c->x, c->xt, h, c->g);
+      timer_end(c, MP_STAGE_GRADIENT, gradient_bytes(c));
+      grad_done = true;
+    };
     if (rebuild) {
+      c->mas_overlap = grad;  // launched inside mas_build, beside the coarse assembly
       snapshot(c, c->x, h, true);
+      c->mas_overlap = nullptr;
     } else {
       timer_begin(c, MP_STAGE_UPDATE);
       update_build(c);
       timer_end(c, MP_STAGE_UPDATE, 0.0);
     }
-    timer_begin(c, MP_STAGE_GRADIENT);
-    gradient(c, c->x, c->xt, h, c->g);
-    timer_end(c, MP_STAGE_GRADIENT, gradient_bytes(c));
+    if (!grad_done) grad();
     timer_begin(c, MP_STAGE_MAS_APPLY);
     precond_apply(c, c->g, c->z, true);
     timer_end(c, MP_STAGE_MAS_APPLY, mas_apply_bytes(c));
@@ -781,6 +791,7 @@ static int guarded(mp_ctx* c, Fn&& fn) {
   try {
     if (c) CUDA_CHECK(cudaSetDevice(c->device));
     if (c) c->bsr_ahead_pending = false;  // an H_base assembled ahead belongs to one loop iteration only
+    if (c) c->mas_overlap = nullptr;
     fn();
     return MP_OK;
   } catch (const MpError& e) {

@@ -263,6 +263,13 @@ static void mas_build(mp_ctx* c) {
   // after the coarse assembly: its 2 CTAs per SM otherwise hold every SM for
   // ~100 us and the assembly chain (the critical path into the coarse
   // inverse) waits behind them (MP_MAS_TRACE: assembly 290 us -> see DESIGN)
+  // the solver loop's gradient (independent of the MAS) runs here, on the
+  // main stream, while the coarse assembly runs on the level streams
+  if (c->mas_overlap) {
+    auto fn = std::move(c->mas_overlap);
+    c->mas_overlap = nullptr;
+    fn();
+  }
   if (c->n_levels) CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->levels[c->n_levels - 1]->ev_asm, 0));
   if (c->own_d1 > c->own_d0) {
     timer_begin(c, MP_STAGE_MAS_SWEEP0);
